@@ -1,0 +1,148 @@
+/*
+ * octfuse_b200 -- C ABI of the B200 (sm_100a) octree range-fusion hot path.
+ *
+ * This is the drop-in boundary for the reference's native kernel module
+ * (/root/reference/pkg/src/octfuse/_kernels.pyx, selected through
+ * _backend.get(), _backend.py:24-26).  Each entry point below names the
+ * reference routine it replaces.  Conventions:
+ *
+ *  - Node pools keep the reference layout (octree.py:49-71): node 0 = root,
+ *    children = 8 contiguous slots at child[n] (-1 for a leaf), blocks start
+ *    at slots b with b % 8 == 1, state = {slots used, free-list head, live
+ *    nodes}.  Pool arrays (value, snap, child, joined, weight, grids,
+ *    pyramids, jlog) are DEVICE pointers; `state`, `out3`, `offs`, `cam`,
+ *    `origin` and the per-view pointer tables are HOST pointers (the
+ *    tables hold device pointers).
+ *  - dtype selects the value pool type: OCTF_F64 (parity mode, bit-exact
+ *    with the reference) or OCTF_F32 (throughput mode).
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls that
+ *    return host values synchronise that stream.
+ *  - Return value: OCTF_OK or an error code mirroring the reference's
+ *    exceptions (_kernels.pyx:26-27 ValueError, :84-87 MemoryError,
+ *    :454-455 RuntimeError); octf_last_error() has the message.
+ *  - There is no CPU fallback: without a CUDA device every call fails with
+ *    OCTF_ECUDA.
+ */
+#ifndef OCTFUSE_B200_H
+#define OCTFUSE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OCTF_OK 0
+#define OCTF_EDEPTH 1 /* ValueError("tree depth out of range")          */
+#define OCTF_ENOMEM 2 /* MemoryError                                     */
+#define OCTF_EPOOL 3  /* RuntimeError("node pool capacity exhausted")    */
+#define OCTF_EARG 4   /* ValueError (bad argument)                       */
+#define OCTF_ECUDA 5  /* RuntimeError (CUDA failure / no device)         */
+
+#define OCTF_F64 0
+#define OCTF_F32 1
+
+#define OCTF_MAX_DEPTH 19
+
+typedef struct octf_ctx octf_ctx;
+
+/* message of the last failed call on this thread */
+const char *octf_last_error(void);
+/* ABI version (major * 100 + minor) */
+int octf_version(void);
+/* host-only consistency checks of the index helpers (no GPU needed):
+ * returns 0 when every check passes */
+int octf_selftest(void);
+
+/* Solver context: device structures derived from one pool (level lists,
+ * leaf blocks, stencil neighbour tables, gathered per-leaf view samples,
+ * free-list mirror).  The reference keeps none (it re-descends from the
+ * root on every lookup, _kernels.pyx:193-202).  Call octf_ctx_invalidate
+ * after modifying a pool or view tree outside this library. */
+int octf_ctx_create(octf_ctx **out);
+int octf_ctx_destroy(octf_ctx *ctx);
+int octf_ctx_invalidate(octf_ctx *ctx);
+/* out[0..7] = leaf blocks, leaves, live blocks, free blocks, mask-format
+ * samples (0/1), sample stride, views, valid */
+int octf_ctx_info(octf_ctx *ctx, int64_t *out);
+
+/* _kernels.pyx:384-461 iterate_pass -- one Jacobi descent pass with the
+ * in-pass split cascade, join cascade and sweep.  snapshot=1 reproduces the
+ * reference's own first step (copy uval into usnap, :390-393); snapshot=0
+ * lets a caller that ping-pongs two buffers skip that copy (usnap must then
+ * hold the pass-start values; uval's old contents are not read).
+ * out3 = {splits, joins, join-log rows}.  jlog: jcap rows of 12 doubles. */
+int octf_iterate_pass(octf_ctx *ctx, int dtype, void *usnap, void *uval,
+                      int32_t *uchild, uint8_t *ujoined, int64_t *ustate,
+                      int64_t cap, int nviews, const float *const *vvals,
+                      const float *const *vws, const int32_t *const *vchilds,
+                      int d_max, double lam, double eps, double gamma,
+                      double xi, double tau_s, double tau_j, int clamp,
+                      int reverse, int snapshot, double *jlog, int64_t jcap,
+                      int64_t *out3, void *stream);
+
+/* _kernels.pyx:80-113 propagate -- inner value = (sequential sum of the 8
+ * children)/8, bottom-up.  ctx may be NULL (a temporary one is built). */
+int octf_propagate(octf_ctx *ctx, int dtype, void *value,
+                   const int32_t *child, const int64_t *state, int64_t cap,
+                   int d_max, void *stream);
+
+/* _kernels.pyx:536-578 tree_energy -- leaf-summed energy.  The per-leaf
+ * terms equal the reference's bit for bit in OCTF_F64; the sum is a
+ * deterministic tree reduction.  terms (optional, device, cap doubles)
+ * receives every leaf's term at its slot. */
+int octf_tree_energy(octf_ctx *ctx, int dtype, const void *uval,
+                     const int32_t *uchild, const int64_t *ustate, int64_t cap,
+                     int nviews, const float *const *vvals,
+                     const float *const *vws, const int32_t *const *vchilds,
+                     int d_max, double lam, double eps, double gamma,
+                     double *out, double *terms, void *stream);
+
+/* _kernels.pyx:116-158 densify -- leaves to a dense (2^d)^3 f64 grid */
+int octf_densify(int dtype, const void *value, const int32_t *child,
+                 int d_max, double *out, void *stream);
+
+/* _kernels.pyx:21-77 build_tree -- spread-rule build from flattened
+ * pyramids (offs: host level offsets; NULL = sum_{l<L} 8^l).  Produces the
+ * reference's exact pool layout (depth-first, child 7 expanded first). */
+int octf_build_tree(const double *meanf, const double *minf,
+                    const double *maxf, const int64_t *offs, int has_w,
+                    const uint8_t *wminf, const uint8_t *wmaxf,
+                    const double *wmeanf, double tau, void *value, int dtype,
+                    float *weight, int32_t *child, int64_t *state, int64_t cap,
+                    int d_max, void *stream);
+
+/* octree.py:193-225 reduce_pyramid/flatten_pyramid on device (numpy's
+ * summation order).  f: dense (2^d)^3 grid, f_dtype OCTF_F32/OCTF_F64;
+ * w (optional) u8 weights.  Outputs are flattened, root first, sized
+ * sum_{l<=d} 8^l.  wm_tmp..pl_tmp: scratch of the same size when w given. */
+int octf_pyramids(const void *f, int f_dtype, const uint8_t *w, int d_max,
+                  double *minf, double *maxf, double *meanf, uint8_t *wminf,
+                  uint8_t *wmaxf, double *wmeanf, double *wf_tmp,
+                  double *pl_tmp, void *stream);
+
+/* octree.py:243-306 build_octree -- pyramids + build (+ propagate_means
+ * when unweighted) in one call; scratch is allocated internally. */
+int octf_build_octree(const void *f, int f_dtype, const uint8_t *w, int d_max,
+                      double tau, void *value, int dtype, float *weight,
+                      int32_t *child, int64_t *state, int64_t cap,
+                      void *stream);
+
+/* tsdf.py:87-120 build_view_tsdf -- per-voxel projective TSDF in f64 with
+ * numpy's operand order.  cam = {fx, fy, cx, cy, R (3x3 camera-to-world,
+ * row-major), t (camera centre)}; origin = volume minimum corner.  When
+ * wf_sum/w_sum are given the view is also accumulated into them
+ * (cli.py:148-149). */
+int octf_view_tsdf(const float *depth, int width, int height,
+                   const double *cam, const double *origin, double voxel,
+                   int n, double delta, double eta, float *f, uint8_t *w,
+                   double *wf_sum, double *w_sum, void *stream);
+
+/* fusion.py:149-155 initial_field */
+int octf_initial_field(const double *wf_sum, const double *w_sum, double gamma,
+                       int64_t n, double *u, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

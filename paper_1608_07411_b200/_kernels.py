@@ -1,0 +1,120 @@
+"""The kernel module behind ``_backend.get()`` -- the reference's plugin
+boundary (reference ``_backend.py:24-26``, ``_kernels.pyx``) on the GPU.
+
+Same function names, argument order, return values and exception types as
+the reference's compiled module, with pools as CUDA tensors (torch is only
+the allocator here) instead of numpy arrays; ``state`` stays a host int64[3]
+array exactly like the reference.  Every call goes through the C ABI of
+``liboctfuse_b200.so``; there is no CPU path.
+
+The reference's kernels are stateless, so by default each call here starts
+from a fresh view of the pool (the solver context is rebuilt).  ``fusion.fuse``
+passes a persistent ``ctx`` so structure is only rebuilt when a pass changes
+it.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._device import ptr, stream_handle
+from ._lib import OCTF_F32, OCTF_F64, call, ptr_table
+
+_shared_ctx = None
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.float64:
+        return OCTF_F64
+    if t.dtype == torch.float32:
+        return OCTF_F32
+    raise TypeError(f"unsupported pool dtype {t.dtype}")
+
+
+def _fresh_ctx():
+    global _shared_ctx
+    if _shared_ctx is None:
+        _shared_ctx = _lib.Ctx()
+    _shared_ctx.invalidate()
+    return _shared_ctx
+
+
+def _state_ptr(state: np.ndarray) -> int:
+    if not (isinstance(state, np.ndarray) and state.dtype == np.int64
+            and state.flags.c_contiguous and state.shape[0] >= 3):
+        raise TypeError("state must be a contiguous host int64[3] array")
+    return state.ctypes.data
+
+
+def _views(vvals, vws, vchilds):
+    if not (len(vvals) == len(vws) == len(vchilds)):
+        raise ValueError("view pool lists differ in length")
+    for v in vvals:
+        if v.dtype != torch.float32:
+            raise TypeError("view values must be float32 pools")
+    return (ptr_table([ptr(v) for v in vvals]), ptr_table([ptr(v) for v in vws]),
+            ptr_table([ptr(v) for v in vchilds]))
+
+
+def build_tree(meanf, minf, maxf, offs, has_w, wminf, wmaxf, wmeanf, tau,
+               value, weight, child, state, d_max):
+    """_kernels.pyx:21-77 (pyramids and pools on device, offs/state host)."""
+    if d_max > 60:
+        raise ValueError("tree depth out of range")
+    offs = np.ascontiguousarray(np.asarray(offs, dtype=np.int64))
+    call("octf_build_tree", ptr(meanf), ptr(minf), ptr(maxf), offs.ctypes.data,
+         int(bool(has_w)), ptr(wminf) if has_w else None,
+         ptr(wmaxf) if has_w else None, ptr(wmeanf) if has_w else None,
+         float(tau), ptr(value), _dtype_code(value),
+         ptr(weight) if has_w else None, ptr(child), _state_ptr(state),
+         value.shape[0], int(d_max), stream_handle())
+
+
+def propagate(value, child, *, state=None, d_max=_lib.MAX_DEPTH, ctx=None):
+    """_kernels.pyx:80-113."""
+    c = ctx if ctx is not None else _fresh_ctx()
+    call("octf_propagate", c.h, _dtype_code(value), ptr(value), ptr(child),
+         _state_ptr(state) if state is not None else None, child.shape[0],
+         int(d_max), stream_handle())
+
+
+def densify(value, child, d_max, out):
+    """_kernels.pyx:116-158 (out: device (2^d)^3 float64)."""
+    if d_max > 60:
+        raise ValueError("tree depth out of range")
+    call("octf_densify", _dtype_code(value), ptr(value), ptr(child),
+         int(d_max), ptr(out), stream_handle())
+
+
+def iterate_pass(uval, usnap, uchild, ujoined, ustate, vvals, vws, vchilds,
+                 d_max, lam, eps, gamma, xi, tau_s, tau_j, clamp, reverse,
+                 jlog, *, ctx=None, snapshot=True):
+    """_kernels.pyx:384-461; returns (splits, joins, jrows)."""
+    if d_max > 60:
+        raise ValueError("tree depth out of range")
+    c = ctx if ctx is not None else _fresh_ctx()
+    tv, tw, tc = _views(vvals, vws, vchilds)
+    out3 = np.zeros(3, dtype=np.int64)
+    jcap = 0 if jlog is None else int(jlog.shape[0])
+    call("octf_iterate_pass", c.h, _dtype_code(uval), ptr(usnap), ptr(uval),
+         ptr(uchild), ptr(ujoined), _state_ptr(ustate), uval.shape[0],
+         len(vvals), tv, tw, tc, int(d_max), float(lam), float(eps),
+         float(gamma), float(xi), float(tau_s), float(tau_j), int(bool(clamp)),
+         int(bool(reverse)), int(bool(snapshot)),
+         ptr(jlog) if jcap else None, jcap, out3.ctypes.data, stream_handle())
+    return int(out3[0]), int(out3[1]), int(out3[2])
+
+
+def tree_energy(uval, uchild, vvals, vws, vchilds, d_max, lam, eps, gamma, *,
+                state=None, ctx=None, terms=None):
+    """_kernels.pyx:536-578; returns the energy as a Python float."""
+    c = ctx if ctx is not None else _fresh_ctx()
+    tv, tw, tc = _views(vvals, vws, vchilds)
+    out = np.zeros(1, dtype=np.float64)
+    call("octf_tree_energy", c.h, _dtype_code(uval), ptr(uval), ptr(uchild),
+         _state_ptr(state) if state is not None else None, uchild.shape[0],
+         len(vvals), tv, tw, tc, int(d_max), float(lam), float(eps),
+         float(gamma), out.ctypes.data, ptr(terms), stream_handle())
+    return float(out[0])

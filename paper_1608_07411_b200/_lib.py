@@ -1,0 +1,124 @@
+"""ctypes binding of the C ABI in include/octfuse_b200.h.
+
+The shared library is built in-tree (``liboctfuse_b200.so`` next to this
+file, see ``csrc/Makefile``).  There is no fallback: if the library or a CUDA
+device is missing, every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liboctfuse_b200.so")
+
+OCTF_F64 = 0
+OCTF_F32 = 1
+MAX_DEPTH = 19
+
+_ERRORS = {1: ValueError, 2: MemoryError, 3: RuntimeError, 4: ValueError,
+           5: RuntimeError}
+
+P = ctypes.c_void_p
+I32 = ctypes.c_int
+I64 = ctypes.c_int64
+DBL = ctypes.c_double
+
+_SIGS = {
+    "octf_last_error": ([], ctypes.c_char_p),
+    "octf_version": ([], I32),
+    "octf_selftest": ([], I32),
+    "octf_ctx_create": ([P], I32),
+    "octf_ctx_destroy": ([P], I32),
+    "octf_ctx_invalidate": ([P], I32),
+    "octf_ctx_info": ([P, P], I32),
+    "octf_iterate_pass": ([P, I32, P, P, P, P, P, I64, I32, P, P, P, I32, DBL,
+                           DBL, DBL, DBL, DBL, DBL, I32, I32, I32, P, I64, P,
+                           P], I32),
+    "octf_propagate": ([P, I32, P, P, P, I64, I32, P], I32),
+    "octf_tree_energy": ([P, I32, P, P, P, I64, I32, P, P, P, I32, DBL, DBL,
+                          DBL, P, P, P], I32),
+    "octf_densify": ([I32, P, P, I32, P, P], I32),
+    "octf_build_tree": ([P, P, P, P, I32, P, P, P, DBL, P, I32, P, P, P, I64,
+                         I32, P], I32),
+    "octf_pyramids": ([P, I32, P, I32, P, P, P, P, P, P, P, P, P], I32),
+    "octf_build_octree": ([P, I32, P, I32, DBL, P, I32, P, P, P, I64, P], I32),
+    "octf_view_tsdf": ([P, I32, I32, P, P, DBL, I32, DBL, DBL, P, P, P, P, P],
+                       I32),
+    "octf_initial_field": ([P, P, DBL, I64, P, P], I32),
+}
+
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile the CUDA library for sm_100a (nvcc cross-compiles, no GPU
+    needed)."""
+    if force or not os.path.exists(LIB_PATH):
+        subprocess.check_call(["make", "-s", "-j8", "-C",
+                               os.path.join(_HERE, "csrc")])
+    return LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with "
+                "`make -C paper_1608_07411_b200/csrc` (there is no CPU "
+                "fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (args, res) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc:
+        msg = lib().octf_last_error().decode(errors="replace")
+        raise _ERRORS.get(rc, RuntimeError)(msg)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(lib(), name)(*args))
+
+
+def ptr_table(ptrs):
+    return (ctypes.c_void_p * max(len(ptrs), 1))(*ptrs)
+
+
+class Ctx:
+    """Owning handle of an ``octf_ctx`` (solver acceleration structures)."""
+
+    def __init__(self):
+        h = ctypes.c_void_p()
+        call("octf_ctx_create", ctypes.byref(h))
+        self.h = h
+
+    def invalidate(self):
+        call("octf_ctx_invalidate", self.h)
+
+    def info(self) -> dict:
+        import numpy as np
+        out = np.zeros(8, dtype=np.int64)
+        call("octf_ctx_info", self.h, out.ctypes.data)
+        keys = ("leaf_blocks", "leaves", "blocks", "free_blocks", "mask_samples",
+                "sample_stride", "views", "valid")
+        return dict(zip(keys, (int(v) for v in out)))
+
+    def close(self):
+        if self.h:
+            lib().octf_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

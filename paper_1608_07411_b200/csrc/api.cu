@@ -1,0 +1,354 @@
+// extern "C" boundary (include/octfuse_b200.h): argument checks, error
+// mapping and precision dispatch.  No compute happens here.
+#include <cstring>
+#include <string>
+
+#include "../../include/octfuse_b200.h"
+#include "octf_build.h"
+#include "octf_ctx.h"
+
+struct octf_ctx {
+  octf::Ctx c;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return OCTF_OK;
+  } catch (const octf::Error& e) {
+    return fail(e.code, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(OCTF_ENOMEM, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(OCTF_ECUDA, e.what());
+  }
+}
+
+inline cudaStream_t S(void* s) { return (cudaStream_t)s; }
+
+void need_device() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    throw octf::Error(octf::kECuda, "no CUDA device available");
+  }
+}
+
+void check_dtype(int dtype) {
+  if (dtype != OCTF_F64 && dtype != OCTF_F32)
+    throw octf::Error(octf::kEArg, "dtype must be OCTF_F64 or OCTF_F32");
+}
+
+octf::PassParams make_params(int d_max, double lam, double eps, double gamma,
+                             double xi, double tau_s, double tau_j, int clamp,
+                             int reverse) {
+  octf::PassParams p;
+  p.d_max = d_max;
+  p.lam = lam;
+  p.eps2 = eps * eps;  // _kernels.pyx:405
+  p.gamma = gamma;
+  p.xi = xi;
+  p.tau_s = tau_s;
+  p.tau_j = tau_j;
+  p.clamp = clamp;
+  p.reverse = reverse;
+  return p;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* octf_last_error(void) { return g_err.c_str(); }
+
+int octf_version(void) { return 100; }
+
+int octf_selftest(void) {
+  using namespace octf;
+  // Morton order == x-major child index at every level
+  for (int x = 0; x < 4; ++x)
+    for (int y = 0; y < 4; ++y)
+      for (int z = 0; z < 4; ++z) {
+        uint64_t k = morton3(x, y, z);
+        uint64_t ref = ((uint64_t)octant(x >> 1, y >> 1, z >> 1) << 3) |
+                       (uint64_t)octant(x, y, z);
+        if (k != ref) return 1;
+      }
+  // neighbour directions round-trip
+  for (int d = 0; d < 12; ++d) {
+    int ox, oy, oz;
+    dir_offset(d, ox, oy, oz);
+    if (nbr_dir(ox, oy, oz) != d) return 2;
+  }
+  int used = 0;
+  for (int ox = -1; ox <= 1; ++ox)
+    for (int oy = -1; oy <= 1; ++oy)
+      for (int oz = -1; oz <= 1; ++oz) used += nbr_dir(ox, oy, oz) >= 0;
+  if (used != 12) return 3;
+  // every stencil point of the reference's delta_u (_kernels.pyx:205-242)
+  // maps to its own block or one of the 12 tabled neighbours
+  const int pts[13][3] = {{0, 0, 0},  {1, 0, 0},  {0, 1, 0},  {0, 0, 1},
+                          {-1, 0, 0}, {-1, 1, 0}, {-1, 0, 1}, {0, -1, 0},
+                          {1, -1, 0}, {0, -1, 1}, {0, 0, -1}, {1, 0, -1},
+                          {0, 1, -1}};
+  for (int c = 0; c < 8; ++c)
+    for (auto& p : pts) {
+      int tx = ((c >> 2) & 1) + p[0], ty = ((c >> 1) & 1) + p[1],
+          tz = (c & 1) + p[2];
+      int ox = tx >> 1, oy = ty >> 1, oz = tz >> 1;
+      if ((ox | oy | oz) != 0 && nbr_dir(ox, oy, oz) < 0) return 4;
+    }
+  // pack/unpack
+  int L, x, y, z;
+  unpack_cell(pack_cell(19, 524287, 3, 524000), L, x, y, z);
+  if (L != 19 || x != 524287 || y != 3 || z != 524000) return 5;
+  // pre/post-order keys: parent before child, child before parent
+  if (!(preorder_key(1, 1, 0, 0, 3, false) < preorder_key(2, 2, 0, 0, 3, false)))
+    return 6;
+  if (!(postorder_key(2, 3, 1, 1, 3, false) < postorder_key(1, 1, 0, 0, 3, false)))
+    return 7;
+  if (!(postorder_key(1, 0, 1, 1, 3, false) < postorder_key(2, 2, 0, 0, 3, false)))
+    return 8;
+  return 0;
+}
+
+int octf_ctx_create(octf_ctx** out) {
+  return guard([&] {
+    if (!out) throw octf::Error(octf::kEArg, "null output pointer");
+    need_device();
+    *out = new octf_ctx();
+  });
+}
+
+int octf_ctx_destroy(octf_ctx* ctx) {
+  delete ctx;
+  return OCTF_OK;
+}
+
+int octf_ctx_invalidate(octf_ctx* ctx) {
+  if (ctx) {
+    ctx->c.valid = false;
+    ctx->c.vkey.clear();
+    ctx->c.nviews = 0;
+  }
+  return OCTF_OK;
+}
+
+int octf_ctx_info(octf_ctx* ctx, int64_t* out) {
+  return guard([&] {
+    if (!ctx || !out) throw octf::Error(octf::kEArg, "null argument");
+    const octf::Ctx& c = ctx->c;
+    out[0] = c.nlb;
+    out[1] = c.nleaves;
+    out[2] = c.nblocks;
+    out[3] = c.nfree;
+    out[4] = c.binw;
+    out[5] = c.sstride;
+    out[6] = c.nviews;
+    out[7] = c.valid;
+  });
+}
+
+int octf_iterate_pass(octf_ctx* ctx, int dtype, void* usnap, void* uval,
+                      int32_t* uchild, uint8_t* ujoined, int64_t* ustate,
+                      int64_t cap, int nviews, const float* const* vvals,
+                      const float* const* vws, const int32_t* const* vchilds,
+                      int d_max, double lam, double eps, double gamma,
+                      double xi, double tau_s, double tau_j, int clamp,
+                      int reverse, int snapshot, double* jlog, int64_t jcap,
+                      int64_t* out3, void* stream) {
+  return guard([&] {
+    if (!ctx || !usnap || !uval || !uchild || !ujoined || !ustate || !out3)
+      throw octf::Error(octf::kEArg, "null argument");
+    check_dtype(dtype);
+    if (d_max > 60 || d_max > OCTF_MAX_DEPTH || d_max < 0)
+      throw octf::Error(octf::kEDepth, "tree depth out of range");
+    if (nviews < 1) throw octf::Error(octf::kEArg, "at least one view is required");
+    octf::ctx_set_views(ctx->c, nviews, vvals, vws, vchilds, S(stream));
+    octf::IterArgs a;
+    a.usnap = usnap;
+    a.uval = uval;
+    a.child = uchild;
+    a.joined = ujoined;
+    a.state = ustate;
+    a.cap = cap;
+    a.prm = make_params(d_max, lam, eps, gamma, xi, tau_s, tau_j, clamp,
+                        reverse);
+    a.jlog = jlog;
+    a.jcap = jlog ? jcap : 0;
+    a.snapshot = snapshot;
+    if (dtype == OCTF_F64)
+      octf::iterate_pass_f64(ctx->c, a, S(stream));
+    else
+      octf::iterate_pass_f32(ctx->c, a, S(stream));
+    out3[0] = a.out3[0];
+    out3[1] = a.out3[1];
+    out3[2] = a.out3[2];
+  });
+}
+
+int octf_propagate(octf_ctx* ctx, int dtype, void* value, const int32_t* child,
+                   const int64_t* state, int64_t cap, int d_max, void* stream) {
+  return guard([&] {
+    check_dtype(dtype);
+    if (!value || !child) throw octf::Error(octf::kEArg, "null argument");
+    if (d_max < 0 || d_max > OCTF_MAX_DEPTH)
+      throw octf::Error(octf::kEDepth, "tree depth out of range");
+    need_device();
+    octf_ctx tmp;
+    octf::Ctx& c = ctx ? ctx->c : tmp.c;
+    int64_t st3[3] = {cap, -1, cap};
+    const int64_t* stp = state ? state : st3;
+    if (!c.valid || c.child_key != child || c.cap != cap || c.d_max != d_max)
+      octf::ctx_prepare(c, child, cap, stp, d_max, S(stream));
+    if (dtype == OCTF_F64)
+      octf::propagate_ctx_f64(c, (double*)value, child, S(stream));
+    else
+      octf::propagate_ctx_f32(c, (float*)value, child, S(stream));
+    if (!ctx) OCTF_CUDA(cudaStreamSynchronize(S(stream)));
+  });
+}
+
+int octf_tree_energy(octf_ctx* ctx, int dtype, const void* uval,
+                     const int32_t* uchild, const int64_t* ustate, int64_t cap,
+                     int nviews, const float* const* vvals,
+                     const float* const* vws, const int32_t* const* vchilds,
+                     int d_max, double lam, double eps, double gamma,
+                     double* out, double* terms, void* stream) {
+  return guard([&] {
+    check_dtype(dtype);
+    if (!uval || !uchild || !out) throw octf::Error(octf::kEArg, "null argument");
+    if (d_max < 0 || d_max > OCTF_MAX_DEPTH)
+      throw octf::Error(octf::kEDepth, "tree depth out of range");
+    need_device();
+    octf_ctx tmp;
+    octf::Ctx& c = ctx ? ctx->c : tmp.c;
+    int64_t st3[3] = {cap, -1, cap};
+    const int64_t* stp = ustate ? ustate : st3;
+    octf::ctx_set_views(c, nviews, vvals, vws, vchilds, S(stream));
+    if (!c.valid || c.child_key != uchild || c.cap != cap || c.d_max != d_max)
+      octf::ctx_prepare(c, uchild, cap, stp, d_max, S(stream));
+    const octf::PassParams p =
+        make_params(d_max, lam, eps, gamma, 0.0, 0.0, 1.0, 1, 0);
+    *out = dtype == OCTF_F64
+               ? octf::energy_f64(c, (const double*)uval, uchild, p, terms,
+                                  S(stream))
+               : octf::energy_f32(c, (const float*)uval, uchild, p, terms,
+                                  S(stream));
+  });
+}
+
+int octf_densify(int dtype, const void* value, const int32_t* child, int d_max,
+                 double* out, void* stream) {
+  return guard([&] {
+    check_dtype(dtype);
+    need_device();
+    octf::densify(dtype, value, child, d_max, out, S(stream));
+    OCTF_CUDA(cudaStreamSynchronize(S(stream)));
+  });
+}
+
+int octf_build_tree(const double* meanf, const double* minf,
+                    const double* maxf, const int64_t* offs, int has_w,
+                    const uint8_t* wminf, const uint8_t* wmaxf,
+                    const double* wmeanf, double tau, void* value, int dtype,
+                    float* weight, int32_t* child, int64_t* state, int64_t cap,
+                    int d_max, void* stream) {
+  return guard([&] {
+    check_dtype(dtype);
+    if (d_max > 60) throw octf::Error(octf::kEDepth, "tree depth out of range");
+    if (!meanf || !minf || !maxf || !value || !child || !state)
+      throw octf::Error(octf::kEArg, "null argument");
+    if (has_w && (!wminf || !wmaxf || !wmeanf || !weight))
+      throw octf::Error(octf::kEArg, "weighted build needs weight pyramids");
+    need_device();
+    octf::BuildIn in{meanf, minf, maxf, offs, has_w, wminf, wmaxf, wmeanf,
+                     tau, d_max, cap};
+    octf::build_tree(in, value, dtype, weight, child, state, false, S(stream));
+  });
+}
+
+int octf_pyramids(const void* f, int f_dtype, const uint8_t* w, int d_max,
+                  double* minf, double* maxf, double* meanf, uint8_t* wminf,
+                  uint8_t* wmaxf, double* wmeanf, double* wf_tmp,
+                  double* pl_tmp, void* stream) {
+  return guard([&] {
+    check_dtype(f_dtype);
+    if (w && (!wminf || !wmaxf || !wmeanf || !wf_tmp || !pl_tmp))
+      throw octf::Error(octf::kEArg, "weighted pyramids need all outputs");
+    need_device();
+    octf::pyramids(f, f_dtype, w, d_max, minf, maxf, meanf, wminf, wmaxf,
+                   wmeanf, wf_tmp, pl_tmp, S(stream));
+  });
+}
+
+int octf_build_octree(const void* f, int f_dtype, const uint8_t* w, int d_max,
+                      double tau, void* value, int dtype, float* weight,
+                      int32_t* child, int64_t* state, int64_t cap,
+                      void* stream) {
+  return guard([&] {
+    check_dtype(f_dtype);
+    check_dtype(dtype);
+    if (d_max < 0 || d_max > OCTF_MAX_DEPTH)
+      throw octf::Error(octf::kEDepth, "tree depth out of range");
+    if (w && !weight) throw octf::Error(octf::kEArg, "weighted build needs weight");
+    need_device();
+    int64_t total = 0;
+    for (int l = 0; l <= d_max; ++l) total += (int64_t)1 << (3 * l);
+    octf::DevBuf<double> mn, mx, mean, wm, wf, pl;
+    octf::DevBuf<uint8_t> wmn, wmx;
+    mn.ensure(total);
+    mx.ensure(total);
+    mean.ensure(total);
+    if (w) {
+      wm.ensure(total);
+      wf.ensure(total);
+      pl.ensure(total);
+      wmn.ensure(total);
+      wmx.ensure(total);
+    }
+    octf::pyramids(f, f_dtype, w, d_max, mn.p, mx.p, mean.p, wmn.p, wmx.p,
+                   wm.p, wf.p, pl.p, S(stream));
+    octf::BuildIn in{mean.p, mn.p, mx.p, nullptr, w != nullptr, wmn.p, wmx.p,
+                     wm.p, tau, d_max, cap};
+    // weighted trees keep their pyramid values (octree.py:302-305)
+    octf::build_tree(in, value, dtype, w ? weight : nullptr, child, state,
+                     w == nullptr, S(stream));
+  });
+}
+
+int octf_view_tsdf(const float* depth, int width, int height,
+                   const double* cam, const double* origin, double voxel,
+                   int n, double delta, double eta, float* f, uint8_t* w,
+                   double* wf_sum, double* w_sum, void* stream) {
+  return guard([&] {
+    if (!depth || !cam || !origin || !f || !w)
+      throw octf::Error(octf::kEArg, "null argument");
+    if ((wf_sum == nullptr) != (w_sum == nullptr))
+      throw octf::Error(octf::kEArg, "wf_sum and w_sum go together");
+    need_device();
+    octf::view_tsdf(depth, width, height, cam, origin, voxel, n, delta, eta, f,
+                    w, wf_sum, w_sum, S(stream));
+  });
+}
+
+int octf_initial_field(const double* wf_sum, const double* w_sum, double gamma,
+                       int64_t n, double* u, void* stream) {
+  return guard([&] {
+    need_device();
+    octf::initial_field(wf_sum, w_sum, gamma, n, u, S(stream));
+  });
+}
+
+}  // extern "C"

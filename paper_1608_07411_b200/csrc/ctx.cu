@@ -1,0 +1,398 @@
+// Solver-context structure rebuild: level lists, leaf-block list, neighbour
+// tables, per-leaf sample gather and the free-list mirror.
+//
+// The reference recomputes neighbours by descending from the root on every
+// access (_kernels.pyx:193-202, 16 descents per node per pass).  Here the
+// descents happen once per structure: each leaf block (8 sibling leaves, the
+// reference's contiguous child block) gets a 12-entry table of the blocks or
+// coarser leaves that hold its 13-point stencil, and each leaf gets its N
+// per-view samples (the reference's per-view cursors, _kernels.pyx:265-273)
+// gathered into a coalesced [view][leaf] store.
+#include <cub/cub.cuh>
+
+#include "octf_ctx.h"
+
+namespace octf {
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw Error(kECuda, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+Ctx::Ctx() {
+  OCTF_CUDA(cudaMallocHost((void**)&h_counters, 64 * sizeof(int32_t)));
+  OCTF_CUDA(cudaMallocHost((void**)&h_scalar, 8 * sizeof(double)));
+}
+Ctx::~Ctx() {
+  if (h_counters) cudaFreeHost(h_counters);
+  if (h_scalar) cudaFreeHost(h_scalar);
+}
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline unsigned grid_for(int64_t n, int per_thread = 1) {
+  int64_t t = (n + per_thread - 1) / per_thread;
+  int64_t g = (t + kThreads - 1) / kThreads;
+  return (unsigned)(g < 1 ? 1 : g);
+}
+
+__device__ __forceinline__ void slot_cell(int32_t b, int c, uint64_t pc,
+                                          int& x, int& y, int& z) {
+  if (b == 0) {
+    x = y = z = 0;
+    return;
+  }
+  int L, px, py, pz;
+  unpack_cell(pc, L, px, py, pz);
+  x = 2 * px + ((c >> 2) & 1);
+  y = 2 * py + ((c >> 1) & 1);
+  z = 2 * pz + (c & 1);
+}
+
+// one level of the top-down walk: every inner slot of a level-L block emits
+// its child block into the level-(L+1) list
+__global__ void k_expand(const int32_t* __restrict__ child,
+                         const int32_t* __restrict__ blocks, int64_t nblk,
+                         int L, int64_t used, int8_t* blevel, uint64_t* bcoord,
+                         int32_t* next, int32_t* counter, int32_t* bad) {
+  int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t i = gid >> 3;
+  int c = (int)(gid & 7);
+  if (i >= nblk) return;
+  int32_t b = blocks[i];
+  if (b == 0 && c != 0) return;
+  int32_t s = b + c;
+  int32_t nb = child[s];
+  if (nb < 0) return;
+  if (nb + 8 > used || (nb & 7) != 1) {
+    atomicExch(bad, 1);
+    return;
+  }
+  int x, y, z;
+  slot_cell(b, c, bcoord[block_id(b)], x, y, z);
+  int k = block_id(nb);
+  blevel[k] = (int8_t)(L + 1);
+  bcoord[k] = pack_cell(L, x, y, z);
+  int pos = atomicAdd(counter, 1);
+  next[pos] = nb;
+}
+
+__global__ void k_leaf_flags(const int32_t* __restrict__ child,
+                             const int32_t* __restrict__ blocks, int64_t nblk,
+                             uint8_t* flags, int32_t* nleaves) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nblk) return;
+  int32_t b = blocks[i];
+  int n = 0;
+  if (b == 0) {
+    n = child[0] < 0;
+  } else {
+    for (int c = 0; c < 8; ++c) n += child[b + c] < 0;
+  }
+  flags[i] = n > 0;
+  if (n) atomicAdd(nleaves, n);
+}
+
+// per leaf block: packed (level, parent cell) and the 12 neighbour refs.
+// ref >= 0: base slot of the same-level block holding that neighbour octet;
+// ref <= -2: node -(ref+2), a coarser leaf covering it; kNone: outside.
+__global__ void k_leaf_tables(const int32_t* __restrict__ child,
+                              const int32_t* __restrict__ lblocks, int64_t nlb,
+                              const int8_t* __restrict__ blevel,
+                              const uint64_t* __restrict__ bcoord,
+                              uint64_t* lkey, int32_t* nbr) {
+  int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t i = gid / 12;
+  int d = (int)(gid % 12);
+  if (i >= nlb) return;
+  int32_t b = lblocks[i];
+  int k = block_id(b);
+  int L = b == 0 ? 0 : blevel[k];
+  int pL, px, py, pz;
+  unpack_cell(bcoord[k], pL, px, py, pz);
+  if (b == 0) px = py = pz = 0;
+  if (d == 0) lkey[i] = pack_cell(L, px, py, pz);
+  int32_t ref = kNone;
+  if (b != 0) {
+    int ox, oy, oz;
+    dir_offset(d, ox, oy, oz);
+    int qx = px + ox, qy = py + oy, qz = pz + oz;
+    int m = 1 << (L - 1);
+    if (qx >= 0 && qy >= 0 && qz >= 0 && qx < m && qy < m && qz < m) {
+      int lq;
+      int32_t q = descend(child, L - 1, qx, qy, qz, &lq);
+      int32_t qb = child[q];
+      ref = (lq == L - 1 && qb >= 0) ? qb : -q - 2;
+    }
+  }
+  nbr[i * 12 + d] = ref;
+}
+
+// per (leaf, view): the view node answering at the leaf's level
+// (_kernels.pyx:265-273 cursors == root descent in the view tree)
+__global__ void k_gather(const int32_t* __restrict__ ucs,
+                         const int32_t* __restrict__ lblocks, int64_t nlb,
+                         const uint64_t* __restrict__ lkey, ViewSet vs,
+                         float* F, float* W, int64_t stride, int32_t* nonbin) {
+  int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t i = gid >> 3;
+  int c = (int)(gid & 7);
+  if (i >= nlb) return;
+  int32_t b = lblocks[i];
+  int64_t sidx = i * 8 + c;
+  bool active = !(b == 0 && c != 0) && ucs[b + c] < 0;
+  int L, px, py, pz;
+  unpack_cell(lkey[i], L, px, py, pz);
+  int x = b == 0 ? 0 : 2 * px + ((c >> 2) & 1);
+  int y = b == 0 ? 0 : 2 * py + ((c >> 1) & 1);
+  int z = b == 0 ? 0 : 2 * pz + (c & 1);
+  int flag = 0;
+  for (int v = 0; v < vs.n; ++v) {
+    float f = 0.f, w = 0.f;
+    if (active) {
+      int32_t n = descend(vs.child[v], L, x, y, z);
+      f = vs.val[v][n];
+      w = vs.w[v][n];
+      flag |= (w != 0.f && w != 1.f);
+    }
+    F[v * stride + sidx] = f;
+    W[v * stride + sidx] = w;
+  }
+  if (flag) atomicExch(nonbin, 1);
+}
+
+__global__ void k_masks(const float* __restrict__ W, int64_t stride, int nv,
+                        int64_t n, uint32_t* M) {
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  uint32_t m = 0;
+  for (int v = 0; v < nv; ++v) m |= (W[v * stride + s] != 0.f ? 1u : 0u) << v;
+  M[s] = m;
+}
+
+__global__ void k_walk_free(const int32_t* __restrict__ child, int64_t head,
+                            int64_t nmax, int32_t* chain, int32_t* count) {
+  // single thread: follow the free list links (child[b] of a free block)
+  int64_t n = 0;
+  int64_t b = head;
+  while (b >= 0 && n < nmax) {
+    chain[n++] = (int32_t)b;
+    b = child[b];
+  }
+  *count = (int32_t)n;
+}
+
+__global__ void k_reverse(const int32_t* in, int64_t n, int32_t* out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[n - 1 - i] = in[i];
+}
+
+}  // namespace
+
+void sort_u64_i32(Ctx& c, uint64_t* keys, int32_t* vals, int64_t n,
+                  cudaStream_t st) {
+  if (n <= 1) return;
+  DevBuf<uint64_t> k2;
+  DevBuf<int32_t> v2;
+  k2.ensure(n);
+  v2.ensure(n);
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys, k2.p, vals, v2.p,
+                                  (int)n, 0, 64, st);
+  c.cub_tmp.ensure(bytes);
+  OCTF_CUDA(cub::DeviceRadixSort::SortPairs(c.cub_tmp.p, bytes, keys, k2.p,
+                                            vals, v2.p, (int)n, 0, 64, st));
+  OCTF_CUDA(cudaMemcpyAsync(keys, k2.p, n * sizeof(uint64_t),
+                            cudaMemcpyDeviceToDevice, st));
+  OCTF_CUDA(cudaMemcpyAsync(vals, v2.p, n * sizeof(int32_t),
+                            cudaMemcpyDeviceToDevice, st));
+  OCTF_CUDA(cudaStreamSynchronize(st));
+}
+
+void sort_i32(Ctx& c, int32_t* keys, int64_t n, cudaStream_t st) {
+  if (n <= 1) return;
+  DevBuf<int32_t> k2;
+  k2.ensure(n);
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, bytes, keys, k2.p, (int)n, 0, 32,
+                                 st);
+  c.cub_tmp.ensure(bytes);
+  OCTF_CUDA(cub::DeviceRadixSort::SortKeys(c.cub_tmp.p, bytes, keys, k2.p,
+                                           (int)n, 0, 32, st));
+  OCTF_CUDA(cudaMemcpyAsync(keys, k2.p, n * sizeof(int32_t),
+                            cudaMemcpyDeviceToDevice, st));
+  OCTF_CUDA(cudaStreamSynchronize(st));
+}
+
+void ctx_free_stack(Ctx& c, const int32_t* child, const int64_t* state,
+                    cudaStream_t st) {
+  int64_t used = state[0];
+  int64_t nmax = (used + 7) / 8 + 1;
+  c.free_stack.ensure(nmax);
+  c.nfree = 0;
+  if (state[1] < 0) return;
+  DevBuf<int32_t> chain;
+  chain.ensure(nmax);
+  c.counters.ensure(64);
+  k_walk_free<<<1, 1, 0, st>>>(child, state[1], nmax, chain.p, c.counters.p);
+  OCTF_CUDA(cudaGetLastError());
+  OCTF_CUDA(cudaMemcpyAsync(c.h_counters, c.counters.p, sizeof(int32_t),
+                            cudaMemcpyDeviceToHost, st));
+  OCTF_CUDA(cudaStreamSynchronize(st));
+  int64_t n = c.h_counters[0];
+  // stack order: bottom = last link, top = head
+  if (n) k_reverse<<<grid_for(n), kThreads, 0, st>>>(chain.p, n, c.free_stack.p);
+  OCTF_CUDA(cudaGetLastError());
+  OCTF_CUDA(cudaStreamSynchronize(st));
+  c.nfree = n;
+}
+
+void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
+                 const int64_t* state, int d_max, cudaStream_t st) {
+  if (d_max < 0 || d_max > kMaxDepth)
+    throw Error(kEDepth, "tree depth out of range");
+  int64_t used = state[0];
+  if (used < 1 || used > cap)
+    throw Error(kEArg, "pool state is inconsistent with its capacity");
+  int64_t nbid = block_id(used) + 1;
+  c.blevel.ensure(nbid);
+  c.bcoord.ensure(nbid);
+  c.lvl_blocks.ensure(nbid + 1);
+  c.counters.ensure(64);
+  OCTF_CUDA(cudaMemsetAsync(c.blevel.p, 0xff, nbid, st));
+  int8_t zero = 0;
+  uint64_t zc = 0;
+  int32_t root = 0;
+  OCTF_CUDA(cudaMemcpyAsync(c.blevel.p, &zero, 1, cudaMemcpyHostToDevice, st));
+  OCTF_CUDA(cudaMemcpyAsync(c.bcoord.p, &zc, 8, cudaMemcpyHostToDevice, st));
+  OCTF_CUDA(cudaMemcpyAsync(c.lvl_blocks.p, &root, 4, cudaMemcpyHostToDevice,
+                            st));
+  c.lvl_off.assign(d_max + 2, 0);
+  c.lvl_cnt.assign(d_max + 2, 0);
+  c.lvl_cnt[0] = 1;
+  int64_t total = 1;
+  for (int L = 0; L < d_max; ++L) {
+    int64_t n = c.lvl_cnt[L];
+    c.lvl_off[L + 1] = total;
+    if (n == 0) break;
+    OCTF_CUDA(cudaMemsetAsync(c.counters.p, 0, 2 * sizeof(int32_t), st));
+    k_expand<<<grid_for(n * 8), kThreads, 0, st>>>(
+        child, c.lvl_blocks.p + c.lvl_off[L], n, L, used, c.blevel.p,
+        c.bcoord.p, c.lvl_blocks.p + total, c.counters.p, c.counters.p + 1);
+    OCTF_CUDA(cudaGetLastError());
+    OCTF_CUDA(cudaMemcpyAsync(c.h_counters, c.counters.p, 2 * sizeof(int32_t),
+                              cudaMemcpyDeviceToHost, st));
+    OCTF_CUDA(cudaStreamSynchronize(st));
+    if (c.h_counters[1]) throw Error(kEArg, "corrupt child links in pool");
+    int64_t m = c.h_counters[0];
+    if (total + m > nbid) throw Error(kEArg, "corrupt child links in pool");
+    sort_i32(c, c.lvl_blocks.p + total, m, st);
+    c.lvl_cnt[L + 1] = m;
+    total += m;
+  }
+  c.nblocks = total;
+  // a finest-level node must be a leaf
+  // (checked implicitly: blocks at level d_max are never expanded)
+
+  // leaf blocks, ascending base slot
+  DevBuf<uint8_t> flags;
+  flags.ensure(total);
+  c.lblocks.ensure(total);
+  OCTF_CUDA(cudaMemsetAsync(c.counters.p, 0, 2 * sizeof(int32_t), st));
+  k_leaf_flags<<<grid_for(total), kThreads, 0, st>>>(
+      child, c.lvl_blocks.p, total, flags.p, c.counters.p + 1);
+  OCTF_CUDA(cudaGetLastError());
+  size_t bytes = 0;
+  cub::DeviceSelect::Flagged(nullptr, bytes, c.lvl_blocks.p, flags.p,
+                             c.lblocks.p, c.counters.p, (int)total, st);
+  c.cub_tmp.ensure(bytes);
+  OCTF_CUDA(cub::DeviceSelect::Flagged(c.cub_tmp.p, bytes, c.lvl_blocks.p,
+                                       flags.p, c.lblocks.p, c.counters.p,
+                                       (int)total, st));
+  OCTF_CUDA(cudaMemcpyAsync(c.h_counters, c.counters.p, 2 * sizeof(int32_t),
+                            cudaMemcpyDeviceToHost, st));
+  OCTF_CUDA(cudaStreamSynchronize(st));
+  c.nlb = c.h_counters[0];
+  c.nleaves = c.h_counters[1];
+  sort_i32(c, c.lblocks.p, c.nlb, st);
+  c.lkey.ensure(c.nlb);
+  c.nbr.ensure(c.nlb * 12);
+  k_leaf_tables<<<grid_for(c.nlb * 12), kThreads, 0, st>>>(
+      child, c.lblocks.p, c.nlb, c.blevel.p, c.bcoord.p, c.lkey.p, c.nbr.p);
+  OCTF_CUDA(cudaGetLastError());
+
+  c.smark.ensure(cap);
+  OCTF_CUDA(cudaMemsetAsync(c.smark.p, 0, cap, st));
+  ctx_free_stack(c, child, state, st);
+  c.child_key = child;
+  c.cap = cap;
+  c.d_max = d_max;
+  c.hstate[0] = state[0];
+  c.hstate[1] = state[1];
+  c.hstate[2] = state[2];
+  c.valid = true;
+  if (c.nviews > 0) ctx_gather(c, st);
+  OCTF_CUDA(cudaStreamSynchronize(st));
+}
+
+void ctx_set_views(Ctx& c, int nviews, const float* const* vval,
+                   const float* const* vw, const int32_t* const* vchild,
+                   cudaStream_t st) {
+  std::vector<const void*> key;
+  for (int v = 0; v < nviews; ++v) {
+    key.push_back(vval[v]);
+    key.push_back(vw[v]);
+    key.push_back(vchild[v]);
+  }
+  if (key == c.vkey && nviews == c.nviews) return;
+  c.vkey = key;
+  c.nviews = nviews;
+  c.dv_val.ensure(nviews);
+  c.dv_w.ensure(nviews);
+  c.dv_child.ensure(nviews);
+  OCTF_CUDA(cudaMemcpyAsync(c.dv_val.p, vval, nviews * sizeof(void*),
+                            cudaMemcpyHostToDevice, st));
+  OCTF_CUDA(cudaMemcpyAsync(c.dv_w.p, vw, nviews * sizeof(void*),
+                            cudaMemcpyHostToDevice, st));
+  OCTF_CUDA(cudaMemcpyAsync(c.dv_child.p, vchild, nviews * sizeof(void*),
+                            cudaMemcpyHostToDevice, st));
+  OCTF_CUDA(cudaStreamSynchronize(st));
+  if (c.valid) ctx_gather(c, st);
+}
+
+ViewSet ctx_views(const Ctx& c) {
+  ViewSet v;
+  v.val = c.dv_val.p;
+  v.w = c.dv_w.p;
+  v.child = c.dv_child.p;
+  v.n = c.nviews;
+  return v;
+}
+
+void ctx_gather(Ctx& c, cudaStream_t st) {
+  int64_t n = c.nlb * 8;
+  c.sstride = n;
+  int nv = c.nviews;
+  c.F.ensure((size_t)nv * n);
+  c.W.ensure((size_t)nv * n);
+  OCTF_CUDA(cudaMemsetAsync(c.counters.p, 0, sizeof(int32_t), st));
+  k_gather<<<grid_for(n), kThreads, 0, st>>>(c.child_key, c.lblocks.p, c.nlb,
+                                              c.lkey.p, ctx_views(c), c.F.p,
+                                              c.W.p, n, c.counters.p);
+  OCTF_CUDA(cudaGetLastError());
+  OCTF_CUDA(cudaMemcpyAsync(c.h_counters, c.counters.p, sizeof(int32_t),
+                            cudaMemcpyDeviceToHost, st));
+  OCTF_CUDA(cudaStreamSynchronize(st));
+  c.binw = (c.h_counters[0] == 0) && nv <= 32;
+  if (c.binw) {
+    c.M.ensure(n);
+    k_masks<<<grid_for(n), kThreads, 0, st>>>(c.W.p, n, nv, n, c.M.p);
+    OCTF_CUDA(cudaGetLastError());
+  }
+}
+
+}  // namespace octf

@@ -1,0 +1,142 @@
+// Shared device helpers for the octree fusion kernels (sm_100a).
+//
+// Node pools keep the reference layout (reference octree.py:49-71,
+// _kernels.pyx:21-77): node 0 is the root, the children of a node are eight
+// contiguous slots starting at child[n] (or child[n] == -1 for a leaf), and
+// every allocated block of eight starts at a slot b with b % 8 == 1.  Block
+// ids are k = (b + 7) >> 3, so the root's pseudo-block (b = 0) is k = 0 and
+// the first real block (b = 1) is k = 1.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace octf {
+
+constexpr int kMaxDepth = 19;   // 3*19 coordinate bits + 5 level bits fit u64
+constexpr int32_t kNone = -1;   // neighbour table: outside the domain
+
+__host__ __device__ __forceinline__ int octant(int x, int y, int z) {
+  return ((x & 1) << 2) | ((y & 1) << 1) | (z & 1);
+}
+
+__host__ __device__ __forceinline__ int block_id(int64_t b) {
+  return (int)((b + 7) >> 3);
+}
+
+// level (5 bits) | x | y | z (19 bits each): one u64 per block or cell
+__host__ __device__ __forceinline__ uint64_t pack_cell(int L, uint32_t x,
+                                                       uint32_t y, uint32_t z) {
+  return ((uint64_t)L << 57) | ((uint64_t)x << 38) | ((uint64_t)y << 19) |
+         (uint64_t)z;
+}
+__host__ __device__ __forceinline__ void unpack_cell(uint64_t p, int& L, int& x,
+                                                     int& y, int& z) {
+  L = (int)(p >> 57);
+  x = (int)((p >> 38) & 0x7ffff);
+  y = (int)((p >> 19) & 0x7ffff);
+  z = (int)(p & 0x7ffff);
+}
+
+// spread the low 21 bits of v to every third bit
+__host__ __device__ __forceinline__ uint64_t spread3(uint64_t v) {
+  v &= 0x1fffff;
+  v = (v | (v << 32)) & 0x1f00000000ffffULL;
+  v = (v | (v << 16)) & 0x1f0000ff0000ffULL;
+  v = (v | (v << 8)) & 0x100f00f00f00f00fULL;
+  v = (v | (v << 4)) & 0x10c30c30c30c30c3ULL;
+  v = (v | (v << 2)) & 0x1249249249249249ULL;
+  return v;
+}
+// x-major Morton key: the child index c = x<<2|y<<1|z at every level, so
+// ascending keys are the reference's canonical leaf order (octree.py:168-181)
+__host__ __device__ __forceinline__ uint64_t morton3(uint32_t x, uint32_t y,
+                                                     uint32_t z) {
+  return (spread3(x) << 2) | (spread3(y) << 1) | spread3(z);
+}
+
+// depth-first pre-order position (parents before children, children in
+// visit order) of a cell: (first finest key << 5) | level
+__host__ __device__ __forceinline__ uint64_t preorder_key(int L, int x, int y,
+                                                          int z, int d_max,
+                                                          bool reverse) {
+  if (reverse) {
+    int m = (1 << L) - 1;
+    x = m - x;
+    y = m - y;
+    z = m - z;
+  }
+  uint64_t first = morton3(x, y, z) << (3 * (d_max - L));
+  return (first << 5) | (uint64_t)L;
+}
+// post-order position (children before parents): (last finest key << 5) |
+// (31 - level)
+__host__ __device__ __forceinline__ uint64_t postorder_key(int L, int x, int y,
+                                                           int z, int d_max,
+                                                           bool reverse) {
+  if (reverse) {
+    int m = (1 << L) - 1;
+    x = m - x;
+    y = m - y;
+    z = m - z;
+  }
+  uint64_t last = ((morton3(x, y, z) + 1) << (3 * (d_max - L))) - 1;
+  return (last << 5) | (uint64_t)(31 - L);
+}
+
+// deepest node at level <= L on the root path of cell (x,y,z)@L
+// (reference octree.py:148-166, _kernels.pyx:193-202)
+__device__ __forceinline__ int32_t descend(const int32_t* __restrict__ child,
+                                           int L, int x, int y, int z,
+                                           int* lvl_out = nullptr) {
+  int32_t n = 0;
+  int l = 0;
+  for (; l < L; ++l) {
+    int32_t b = __ldg(child + n);
+    if (b < 0) break;
+    int s = L - l - 1;
+    n = b + octant(x >> s, y >> s, z >> s);
+  }
+  if (lvl_out) *lvl_out = l;
+  return n;
+}
+
+// neighbour-table direction of a parent-level block offset (ox,oy,oz):
+// faces -x +x -y +y -z +z, then the six edge offsets the 13-point stencil
+// reaches: (-x+y) (-x+z) (+x-y) (-y+z) (+x-z) (+y-z); -1 = never used
+__host__ __device__ __forceinline__ int nbr_dir(int ox, int oy, int oz) {
+  const int nz = (ox != 0) + (oy != 0) + (oz != 0);
+  if (nz == 1) return ox ? (ox < 0 ? 0 : 1) : oy ? (oy < 0 ? 2 : 3)
+                                                 : (oz < 0 ? 4 : 5);
+  if (nz != 2) return -1;
+  if (oz == 0) return ox == -oy ? (ox < 0 ? 6 : 8) : -1;   // (-x+y) (+x-y)
+  if (oy == 0) return ox == -oz ? (ox < 0 ? 7 : 10) : -1;  // (-x+z) (+x-z)
+  return oy == -oz ? (oy < 0 ? 9 : 11) : -1;               // (-y+z) (+y-z)
+}
+
+// (ox,oy,oz) of each of the 12 table directions
+__host__ __device__ __forceinline__ void dir_offset(int d, int& ox, int& oy,
+                                                    int& oz) {
+  constexpr int kOff[12][3] = {{-1, 0, 0}, {1, 0, 0},  {0, -1, 0}, {0, 1, 0},
+                               {0, 0, -1}, {0, 0, 1},  {-1, 1, 0}, {-1, 0, 1},
+                               {1, -1, 0}, {0, -1, 1}, {1, 0, -1}, {0, 1, -1}};
+  ox = kOff[d][0];
+  oy = kOff[d][1];
+  oz = kOff[d][2];
+}
+
+struct PassParams {
+  int d_max;
+  double lam, eps2, gamma, xi, tau_s, tau_j;
+  int clamp;
+  int reverse;
+};
+
+// per-view tree pools as device arrays of device pointers
+struct ViewSet {
+  const float* const* val;
+  const float* const* w;
+  const int32_t* const* child;
+  int n;
+};
+
+}  // namespace octf

@@ -1,0 +1,162 @@
+// Host-side solver context: device acceleration structures derived from a
+// reference-layout node pool, kept across passes so a pass only streams the
+// leaves.  Everything here is an implementation detail behind the C ABI in
+// include/octfuse_b200.h.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "octf_common.cuh"
+
+namespace octf {
+
+// error kinds mirror the reference's three exceptions (_kernels.pyx:26-27,
+// :84-87, :454-455) plus argument and CUDA failures
+enum Err : int {
+  kOk = 0,
+  kEDepth = 1,  // ValueError("tree depth out of range")
+  kENoMem = 2,  // MemoryError
+  kEPool = 3,   // RuntimeError("node pool capacity exhausted")
+  kEArg = 4,    // ValueError (bad argument)
+  kECuda = 5,   // RuntimeError (CUDA failure)
+};
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void check_cuda(cudaError_t e, const char* what);
+#define OCTF_CUDA(call) ::octf::check_cuda((call), #call)
+
+// owning device buffer (grow-only)
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  T* ensure(size_t count) {
+    if (count <= n && p) return p;
+    release();
+    size_t c = count ? count : 1;
+    cudaError_t e = cudaMalloc((void**)&p, c * sizeof(T));
+    if (e != cudaSuccess) {
+      p = nullptr;
+      cudaGetLastError();
+      throw Error(kENoMem, "device allocation of " +
+                               std::to_string(c * sizeof(T)) + " bytes failed");
+    }
+    n = c;
+    return p;
+  }
+};
+
+struct Ctx {
+  // ---- identity of the pool / views the cached structures describe
+  const int32_t* child_key = nullptr;
+  int64_t cap = 0;
+  int d_max = -1;
+  bool valid = false;
+  int64_t hstate[3] = {1, -1, 1};  // last known pool state
+  std::vector<const void*> vkey;
+  int nviews = 0;
+
+  // ---- structure (rebuilt by prepare())
+  DevBuf<int8_t> blevel;      // per block id: level of its nodes (-1 free)
+  DevBuf<uint64_t> bcoord;    // per block id: packed parent cell
+  std::vector<int64_t> lvl_off, lvl_cnt;  // per level ranges in lvl_blocks
+  DevBuf<int32_t> lvl_blocks;             // live block bases, level-major
+  int64_t nblocks = 0;
+  DevBuf<int32_t> lblocks;    // blocks holding >= 1 leaf, ascending base
+  DevBuf<uint64_t> lkey;      // per leaf block: packed (level, parent cell)
+  DevBuf<int32_t> nbr;        // per leaf block: 12 neighbour refs
+  int64_t nlb = 0;
+  int64_t nleaves = 0;
+
+  // ---- per-leaf samples, index i*8+c over the leaf-block list
+  DevBuf<float> F;            // [view][sample]
+  DevBuf<float> W;            // [view][sample] (general weights)
+  DevBuf<uint32_t> M;         // [sample] bit v = weight of view v is 1
+  bool binw = false;          // samples use the mask format
+  int64_t sstride = 0;
+
+  // ---- views (device arrays of device pointers)
+  DevBuf<const float*> dv_val, dv_w;
+  DevBuf<const int32_t*> dv_child;
+
+  // ---- free list mirror: stack of free block bases, top = free-list head
+  DevBuf<int32_t> free_stack;
+  int64_t nfree = 0;
+
+  // ---- pass scratch
+  DevBuf<uint8_t> smark;      // per slot: leaf split this pass
+  DevBuf<int32_t> counters;   // device counters
+  DevBuf<int32_t> split_list;
+  DevBuf<uint8_t> cub_tmp;
+  DevBuf<double> partials;
+  DevBuf<double> dscalar;
+
+  // host pinned staging for small readbacks
+  int32_t* h_counters = nullptr;
+  double* h_scalar = nullptr;
+
+  Ctx();
+  ~Ctx();
+};
+
+// structure rebuild from the pool (BFS over levels, leaf-block list,
+// neighbour tables); views gather when given.  Syncs the stream.
+void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
+                 const int64_t* state, int d_max, cudaStream_t st);
+void ctx_set_views(Ctx& c, int nviews, const float* const* vval,
+                   const float* const* vw, const int32_t* const* vchild,
+                   cudaStream_t st);
+void ctx_gather(Ctx& c, cudaStream_t st);
+void ctx_free_stack(Ctx& c, const int32_t* child, const int64_t* state,
+                    cudaStream_t st);
+ViewSet ctx_views(const Ctx& c);
+
+// cub wrappers (ctx.cu)
+void sort_u64_i32(Ctx& c, uint64_t* keys, int32_t* vals, int64_t n,
+                  cudaStream_t st);
+void sort_i32(Ctx& c, int32_t* keys, int64_t n, cudaStream_t st);
+
+struct IterArgs {
+  const void* usnap;  // pass-start values (+ new children's snapshots)
+  void* uval;         // post-pass values
+  int32_t* child;
+  uint8_t* joined;
+  int64_t* state;     // host int64[3]
+  int64_t cap;
+  PassParams prm;
+  double* jlog;       // device rows of 12 doubles (may be null)
+  int64_t jcap;
+  int snapshot;       // 1: copy uval -> usnap first (_kernels.pyx:390-393)
+  int64_t out3[3];    // splits, joins, log rows
+};
+
+// per precision entry points (solver_f64.cu / solver_f32.cu)
+void iterate_pass_f64(Ctx& c, IterArgs& a, cudaStream_t st);
+void iterate_pass_f32(Ctx& c, IterArgs& a, cudaStream_t st);
+void propagate_ctx_f64(Ctx& c, double* value, const int32_t* child,
+                       cudaStream_t st);
+void propagate_ctx_f32(Ctx& c, float* value, const int32_t* child,
+                       cudaStream_t st);
+double energy_f64(Ctx& c, const double* u, const int32_t* child,
+                  const PassParams& p, double* terms, cudaStream_t st);
+double energy_f32(Ctx& c, const float* u, const int32_t* child,
+                  const PassParams& p, double* terms, cudaStream_t st);
+
+}  // namespace octf

@@ -1,0 +1,16 @@
+// Throughput mode: T = float (fp32 u, SFU rsqrt); see octf_arith.cuh.
+#include "solver_impl.cuh"
+
+namespace octf {
+void iterate_pass_f32(Ctx& c, IterArgs& a, cudaStream_t st) {
+  iterate_pass_impl<float>(c, a, st);
+}
+void propagate_ctx_f32(Ctx& c, float* value, const int32_t* child,
+                       cudaStream_t st) {
+  propagate_impl<float>(c, value, child, st);
+}
+double energy_f32(Ctx& c, const float* u, const int32_t* child,
+                  const PassParams& p, double* terms, cudaStream_t st) {
+  return energy_impl<float>(c, u, child, p, terms, st);
+}
+}  // namespace octf

@@ -1,0 +1,16 @@
+// Parity mode: T = double, compiled with -fmad=false (see octf_arith.cuh).
+#include "solver_impl.cuh"
+
+namespace octf {
+void iterate_pass_f64(Ctx& c, IterArgs& a, cudaStream_t st) {
+  iterate_pass_impl<double>(c, a, st);
+}
+void propagate_ctx_f64(Ctx& c, double* value, const int32_t* child,
+                       cudaStream_t st) {
+  propagate_impl<double>(c, value, child, st);
+}
+double energy_f64(Ctx& c, const double* u, const int32_t* child,
+                  const PassParams& p, double* terms, cudaStream_t st) {
+  return energy_impl<double>(c, u, child, p, terms, st);
+}
+}  // namespace octf

@@ -1,0 +1,874 @@
+// The restructuring descent pass, propagate and energy on device.
+//
+// Included once per precision: solver_f64.cu (T = double, -fmad=false, the
+// bit-exact parity mode) and solver_f32.cu (T = float, throughput mode).
+// Everything lives in an anonymous namespace so the two instantiations never
+// meet at link time.
+//
+// Semantics follow the reference's recursive visit (_kernels.pyx:256-381),
+// restated data-parallel:
+//  1. every pre-pass leaf is updated from the immutable snapshot S
+//     (k_leaf_pass: 13-point stencil through the block neighbour tables,
+//     view samples from the gathered store);
+//  2. leaves with |dn| < tau_s split; the cascade below them is evaluated
+//     level by level on virtual children that carry the parent's snapshot,
+//     which is exactly what the reference's lookups see (a new child's
+//     snapshot equals the leaf that contained it), then blocks are
+//     allocated in the reference's depth-first order (free list first);
+//  3. joins are tested bottom-up level by level on post-update child values;
+//  4. joined subtrees are freed in the reference's post-order, which fixes
+//     the free-list order; then propagate and energy.
+// The pool (value/snap/child/joined/state) therefore ends every pass
+// identical to the reference's on live nodes.
+#pragma once
+#include <cub/cub.cuh>
+
+#include "octf_arith.cuh"
+#include "octf_ctx.h"
+
+namespace octf {
+namespace {
+
+constexpr int kT = 256;
+
+inline unsigned blocks_for(int64_t n) {
+  int64_t g = (n + kT - 1) / kT;
+  return (unsigned)(g < 1 ? 1 : g);
+}
+
+template <typename T>
+struct LeafParams {
+  int d_max;
+  T lam, eps2, gamma, xi;
+  double tau_s, tau_j;
+  int clamp;
+};
+
+template <typename T>
+LeafParams<T> leaf_params(const PassParams& p) {
+  LeafParams<T> q;
+  q.d_max = p.d_max;
+  q.lam = (T)p.lam;
+  q.eps2 = (T)p.eps2;
+  q.gamma = (T)p.gamma;
+  q.xi = (T)p.xi;
+  q.tau_s = p.tau_s;
+  q.tau_j = p.tau_j;
+  q.clamp = p.clamp;
+  return q;
+}
+
+// exact powers of two built from the exponent field
+template <typename T>
+__device__ __forceinline__ T pow2(int e);
+template <>
+__device__ __forceinline__ float pow2<float>(int e) {
+  return __int_as_float((e + 127) << 23);
+}
+template <>
+__device__ __forceinline__ double pow2<double>(int e) {
+  return __longlong_as_double((long long)(e + 1023) << 52);
+}
+// 1/h = 2^-(d_max - L) (h = finest-cell units, reference fusion.py:14-15)
+template <typename T>
+__device__ __forceinline__ T inv_spacing(int d_max, int L) {
+  return pow2<T>(L - d_max);
+}
+
+template <typename T>
+__device__ __forceinline__ T clamp1(T v) {
+  return v > (T)1 ? (T)1 : (v < (T)-1 ? (T)-1 : v);
+}
+
+// ---------------------------------------------------------------------------
+// 1. fast leaf update over leaf blocks.  8 lanes = the 8 sibling slots of a
+// block; the 13-point stencil resolves through the block's neighbour table.
+template <typename T, bool FROZEN, bool BINW>
+__global__ void __launch_bounds__(kT)
+    k_leaf_pass(const int32_t* __restrict__ lblocks, int64_t nlb,
+                const uint64_t* __restrict__ lkey,
+                const int32_t* __restrict__ nbr,
+                const int32_t* __restrict__ child, const T* __restrict__ snap,
+                T* __restrict__ uval, const float* __restrict__ F,
+                const float* __restrict__ W, const uint32_t* __restrict__ M,
+                int64_t stride, int nv, LeafParams<T> p, uint8_t* smark,
+                int32_t* split_list, int32_t* counters) {
+  using A = Arith<T>;
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = gid >> 3;
+  const int c = (int)(gid & 7);
+  bool active = i < nlb;
+  const int32_t b = active ? __ldg(lblocks + i) : 0;
+  const int32_t s = b + c;
+  if (active && b == 0 && c != 0) active = false;
+  if (active && __ldg(child + s) >= 0) active = false;
+  bool ok_join = false, positive = false;
+  if (active) {
+    int L, px, py, pz;
+    unpack_cell(__ldg(lkey + i), L, px, py, pz);
+    const int cx = (c >> 2) & 1, cy = (c >> 1) & 1, cz = c & 1;
+    const int x = 2 * px + cx, y = 2 * py + cy, z = 2 * pz + cz;
+    const int m = 1 << L;
+    const T ih = inv_spacing<T>(p.d_max, L);
+    const int32_t* nb = nbr + i * 12;
+    auto S = [&](int dx, int dy, int dz) -> T {
+      const int tx = cx + dx, ty = cy + dy, tz = cz + dz;
+      const int ox = tx >> 1, oy = ty >> 1, oz = tz >> 1;
+      const int cc = ((tx & 1) << 2) | ((ty & 1) << 1) | (tz & 1);
+      if ((ox | oy | oz) == 0) return snap[b + cc];
+      const int32_t r = __ldg(nb + nbr_dir(ox, oy, oz));
+      return r >= 0 ? snap[r + cc] : snap[-r - 2];
+    };
+    const T S0 = snap[s];
+    // flux at the cell (_kernels.pyx:205-220 with the cell itself)
+    T gx = 0, gy = 0, gz = 0;
+    if (x + 1 < m) gx = (S(1, 0, 0) - S0) * ih;
+    if (y + 1 < m) gy = (S(0, 1, 0) - S0) * ih;
+    if (z + 1 < m) gz = (S(0, 0, 1) - S0) * ih;
+    T p0, p1, p2;
+    A::flux(gx, gy, gz, p.eps2, p0, p1, p2);
+    // backward fluxes, one component each (_kernels.pyx:234-242)
+    T bx = 0, by = 0, bz = 0;
+    if (x > 0) {
+      const T cm = S(-1, 0, 0);
+      const T hx = (S0 - cm) * ih;
+      const T hy = (y + 1 < m) ? (S(-1, 1, 0) - cm) * ih : (T)0;
+      const T hz = (z + 1 < m) ? (S(-1, 0, 1) - cm) * ih : (T)0;
+      bx = A::flux1(hx, hx, hy, hz, p.eps2);
+    }
+    if (y > 0) {
+      const T cm = S(0, -1, 0);
+      const T hx = (x + 1 < m) ? (S(1, -1, 0) - cm) * ih : (T)0;
+      const T hy = (S0 - cm) * ih;
+      const T hz = (z + 1 < m) ? (S(0, -1, 1) - cm) * ih : (T)0;
+      by = A::flux1(hy, hx, hy, hz, p.eps2);
+    }
+    if (z > 0) {
+      const T cm = S(0, 0, -1);
+      const T hx = (x + 1 < m) ? (S(1, 0, -1) - cm) * ih : (T)0;
+      const T hy = (y + 1 < m) ? (S(0, 1, -1) - cm) * ih : (T)0;
+      const T hz = (S0 - cm) * ih;
+      bz = A::flux1(hz, hx, hy, hz, p.eps2);
+    }
+    const T div = ((p0 - bx) + (p1 - by) + (p2 - bz)) * ih;
+    // data term in view order, zero weights skipped (_kernels.pyx:244-252)
+    T num = 0, den = p.gamma;
+    const int64_t sidx = i * 8 + c;
+    if (BINW) {
+      const uint32_t mk = __ldg(M + sidx);
+      for (int v = 0; v < nv; ++v) {
+        const T d = S0 - (T)__ldg(F + v * stride + sidx);
+        if ((mk >> v) & 1u) {
+          num += A::data_grad((T)1, d, p.eps2);
+          den += (T)1;
+        }
+      }
+    } else {
+      for (int v = 0; v < nv; ++v) {
+        const float w = __ldg(W + v * stride + sidx);
+        const T d = S0 - (T)__ldg(F + v * stride + sidx);
+        if (w != 0.f) {
+          num += A::data_grad((T)w, d, p.eps2);
+          den += (T)w;
+        }
+      }
+    }
+    const T du = p.lam * div - A::div(num, den);
+    T dn = S0 + p.xi * du;
+    if (!FROZEN && L < p.d_max && fabs((double)dn) < p.tau_s) {
+      smark[s] = 1;
+      split_list[atomicAdd(counters, 1)] = s;
+    } else {
+      if (p.clamp) dn = clamp1(dn);
+      uval[s] = dn;
+      ok_join = (double)dn > p.tau_j || (double)dn < -p.tau_j;
+      positive = dn > (T)0;
+    }
+  }
+  if (!FROZEN) {
+    // bottom join candidates: blocks of 8 unsplit leaves past tau_j with one
+    // sign; without one no join can happen anywhere this pass
+    unsigned all = ok_join, pos = ok_join && positive,
+             neg = ok_join && !positive;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      all &= __shfl_xor_sync(0xffffffffu, all, o);
+      pos |= __shfl_xor_sync(0xffffffffu, pos, o);
+      neg |= __shfl_xor_sync(0xffffffffu, neg, o);
+    }
+    if (c == 0 && i < nlb && b != 0 && all && !(pos && neg))
+      atomicAdd(counters + 1, 1);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// generic update of one cell at level L from the snapshot by root descents:
+// the reference's delta_u (_kernels.pyx:223-253) verbatim in structure.
+// Used for split cascades (virtual children) and join candidates.
+template <typename T>
+__device__ __forceinline__ T look(const int32_t* child, const T* snap, int L,
+                                  int x, int y, int z) {
+  return snap[descend(child, L, x, y, z)];
+}
+
+template <typename T>
+__device__ void flux_at(const int32_t* child, const T* snap, int L, int x,
+                        int y, int z, T ih, T eps2, T out[3]) {
+  const int m = 1 << L;
+  const T c = look(child, snap, L, x, y, z);
+  T gx = 0, gy = 0, gz = 0;
+  if (x + 1 < m) gx = (look(child, snap, L, x + 1, y, z) - c) * ih;
+  if (y + 1 < m) gy = (look(child, snap, L, x, y + 1, z) - c) * ih;
+  if (z + 1 < m) gz = (look(child, snap, L, x, y, z + 1) - c) * ih;
+  Arith<T>::flux(gx, gy, gz, eps2, out[0], out[1], out[2]);
+}
+
+template <typename T>
+__device__ T slow_dn(const int32_t* child, const T* snap, ViewSet vs,
+                     const LeafParams<T>& p, int L, int x, int y, int z,
+                     T S0) {
+  using A = Arith<T>;
+  const T ih = inv_spacing<T>(p.d_max, L);
+  T q[3], r[3];
+  T bx = 0, by = 0, bz = 0;
+  flux_at(child, snap, L, x, y, z, ih, p.eps2, q);
+  if (x > 0) {
+    flux_at(child, snap, L, x - 1, y, z, ih, p.eps2, r);
+    bx = r[0];
+  }
+  if (y > 0) {
+    flux_at(child, snap, L, x, y - 1, z, ih, p.eps2, r);
+    by = r[1];
+  }
+  if (z > 0) {
+    flux_at(child, snap, L, x, y, z - 1, ih, p.eps2, r);
+    bz = r[2];
+  }
+  const T div = ((q[0] - bx) + (q[1] - by) + (q[2] - bz)) * ih;
+  T num = 0, den = p.gamma;
+  for (int v = 0; v < vs.n; ++v) {
+    const int32_t n = descend(vs.child[v], L, x, y, z);
+    const float w = vs.w[v][n];
+    if (w != 0.f) {
+      const T d = S0 - (T)vs.val[v][n];
+      num += A::data_grad((T)w, d, p.eps2);
+      den += (T)w;
+    }
+  }
+  const T du = p.lam * div - A::div(num, den);
+  return S0 + p.xi * du;
+}
+
+// ---------------------------------------------------------------------------
+// 2. split cascade on events.  Event = one split, i.e. one block of eight
+// children to allocate.  Root events are pre-pass leaves; child events are
+// virtual children that split again.
+template <typename T>
+struct Events {
+  int32_t* slot;     // root events: the pre-pass leaf slot; else -1
+  int32_t* parent;   // parent event or -1
+  int8_t* pc;        // child position inside the parent event's block
+  uint64_t* cell;    // packed (level, x, y, z) of the splitting node
+  T* S;              // snapshot value every node of this cascade carries
+  T* cval;           // [8] final values of non-splitting children
+  int32_t* cmask;    // bit c: child c splits further
+  uint64_t* key;     // depth-first pre-order key
+  int32_t* idx;      // 0..E-1 (sorted alongside key)
+  int32_t* rank;     // event -> allocation rank
+  int32_t* blk;      // event -> allocated block base
+};
+
+__device__ __forceinline__ void slot_cell_of(int32_t s, const int8_t* blevel,
+                                             const uint64_t* bcoord, int& L,
+                                             int& x, int& y, int& z) {
+  if (s == 0) {
+    L = x = y = z = 0;
+    return;
+  }
+  const int32_t b = ((s - 1) & ~7) + 1;
+  const int c = (s - 1) & 7;
+  const int k = block_id(b);
+  int pl, px, py, pz;
+  unpack_cell(bcoord[k], pl, px, py, pz);
+  L = blevel[k];
+  x = 2 * px + ((c >> 2) & 1);
+  y = 2 * py + ((c >> 1) & 1);
+  z = 2 * pz + (c & 1);
+}
+
+template <typename T>
+__global__ void k_events_init(const int32_t* split_list, int64_t n,
+                              const int8_t* blevel, const uint64_t* bcoord,
+                              const T* snap, Events<T> ev) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const int32_t s = split_list[e];
+  int L, x, y, z;
+  slot_cell_of(s, blevel, bcoord, L, x, y, z);
+  ev.slot[e] = s;
+  ev.parent[e] = -1;
+  ev.pc[e] = 0;
+  ev.cell[e] = pack_cell(L, x, y, z);
+  ev.S[e] = snap[s];
+  ev.cmask[e] = 0;
+}
+
+template <typename T>
+__global__ void k_cascade(int64_t e0, int64_t e1, Events<T> ev,
+                          const int32_t* __restrict__ child,
+                          const T* __restrict__ snap, ViewSet vs,
+                          LeafParams<T> p, int32_t* counters, int64_t ev_cap) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t e = e0 + (gid >> 3);
+  const int c = (int)(gid & 7);
+  if (e >= e1) return;
+  int L, x, y, z;
+  unpack_cell(ev.cell[e], L, x, y, z);
+  const int L1 = L + 1;
+  const int x1 = 2 * x + ((c >> 2) & 1), y1 = 2 * y + ((c >> 1) & 1),
+            z1 = 2 * z + (c & 1);
+  const T S0 = ev.S[e];
+  T dn = slow_dn<T>(child, snap, vs, p, L1, x1, y1, z1, S0);
+  if (L1 < p.d_max && fabs((double)dn) < p.tau_s) {
+    atomicOr(ev.cmask + e, 1 << c);
+    const int32_t ne = atomicAdd(counters + 2, 1);
+    if (ne >= ev_cap) {
+      atomicExch(counters + 3, 1);
+      return;
+    }
+    ev.slot[ne] = -1;
+    ev.parent[ne] = (int32_t)e;
+    ev.pc[ne] = (int8_t)c;
+    ev.cell[ne] = pack_cell(L1, x1, y1, z1);
+    ev.S[ne] = S0;
+    ev.cmask[ne] = 0;
+  } else {
+    if (p.clamp) dn = clamp1(dn);
+    ev.cval[e * 8 + c] = dn;
+  }
+}
+
+template <typename T>
+__global__ void k_event_keys(Events<T> ev, int64_t n, int d_max, int reverse) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  int L, x, y, z;
+  unpack_cell(ev.cell[e], L, x, y, z);
+  ev.key[e] = preorder_key(L, x, y, z, d_max, reverse != 0);
+  ev.idx[e] = (int32_t)e;
+}
+
+// rank -> block: free-list entries from the head down, then the bump pointer
+template <typename T>
+__global__ void k_event_alloc(Events<T> ev, int64_t n,
+                              const int32_t* free_stack, int64_t nfree,
+                              int64_t used) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int32_t e = ev.idx[r];
+  ev.rank[e] = (int32_t)r;
+  ev.blk[e] = r < nfree ? free_stack[nfree - 1 - r]
+                        : (int32_t)(used + 8 * (r - nfree));
+}
+
+template <typename T>
+__global__ void k_event_materialize(Events<T> ev, int64_t n, int32_t* child,
+                                    T* usnap, T* uval, uint8_t* joined) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t e = gid >> 3;
+  const int c = (int)(gid & 7);
+  if (e >= n) return;
+  const int32_t be = ev.blk[e];
+  const T S0 = ev.S[e];
+  const bool splits = (ev.cmask[e] >> c) & 1;
+  const int32_t s = be + c;
+  usnap[s] = S0;
+  uval[s] = splits ? S0 : ev.cval[e * 8 + c];
+  joined[s] = 0;
+  if (!splits) child[s] = -1;
+  if (c == 0) {
+    const int32_t par = ev.parent[e];
+    const int32_t ps = par < 0 ? ev.slot[e] : ev.blk[par] + ev.pc[e];
+    child[ps] = be;
+    if (par < 0) uval[ps] = S0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 3. joins, one level at a time from d_max-1 up to the root
+template <typename T>
+struct JoinRecs {
+  int32_t* slot;
+  int32_t* blk;
+  uint64_t* cell;
+  double* vals;   // [8] children's post-update values (log row)
+  uint64_t* key;
+  int32_t* idx;
+};
+
+template <typename T>
+__global__ void k_join_level(const int32_t* __restrict__ blocks, int64_t nblk,
+                             const int8_t* blevel, const uint64_t* bcoord,
+                             int32_t* child, uint8_t* joined,
+                             const uint8_t* smark, const T* snap, T* uval,
+                             ViewSet vs, LeafParams<T> p, JoinRecs<T> rec,
+                             int32_t* counters) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = gid >> 3;
+  const int c = (int)(gid & 7);
+  if (i >= nblk) return;
+  const int32_t b = blocks[i];
+  if (b == 0 && c != 0) return;
+  const int32_t s = b + c;
+  const int32_t cb = child[s];
+  if (cb < 0 || smark[s]) return;  // leaf, or a leaf that split this pass
+  bool pos = false, neg = false;
+  double acc = 0.0;
+  for (int q = 0; q < 8; ++q) {
+    const int32_t cs = cb + q;
+    if (child[cs] >= 0 && !joined[cs]) return;
+    const double v = (double)uval[cs];
+    if (!(v > p.tau_j || v < -p.tau_j)) return;
+    if (v > 0.0)
+      pos = true;
+    else
+      neg = true;
+    acc += v;
+  }
+  if (pos && neg) return;
+  int L, x, y, z;
+  slot_cell_of(s, blevel, bcoord, L, x, y, z);
+  const T dn = slow_dn<T>(child, snap, vs, p, L, x, y, z, snap[s]);
+  if (!(fabs((double)dn) > p.tau_j)) return;
+  joined[s] = 1;
+  uval[s] = (T)(acc / 8.0);
+  const int32_t r = atomicAdd(counters + 4, 1);
+  rec.slot[r] = s;
+  rec.blk[r] = cb;
+  rec.cell[r] = pack_cell(L, x, y, z);
+  for (int q = 0; q < 8; ++q) rec.vals[r * 8 + q] = (double)uval[cb + q];
+}
+
+template <typename T>
+__global__ void k_join_keys(JoinRecs<T> rec, int64_t n, int d_max,
+                            int reverse) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  int L, x, y, z;
+  unpack_cell(rec.cell[r], L, x, y, z);
+  rec.key[r] = postorder_key(L, x, y, z, d_max, reverse != 0);
+  rec.idx[r] = (int32_t)r;
+}
+
+// 4. sweep (_kernels.pyx:357-381): every joined node's child block is freed
+// (all inner nodes under a topmost joined node are joined themselves)
+template <typename T>
+__global__ void k_sweep_clear(JoinRecs<T> rec, int64_t n, int32_t* child,
+                              uint8_t* joined) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int32_t s = rec.slot[r], b = rec.blk[r];
+  child[s] = -1;
+  joined[s] = 0;
+  for (int q = 0; q < 8; ++q) {
+    joined[b + q] = 0;
+    if (q) child[b + q] = -1;
+  }
+}
+
+// push in post-order: child[b_i] links to the previous head
+template <typename T>
+__global__ void k_sweep_link(JoinRecs<T> rec, int64_t n, int64_t old_head,
+                             int32_t* child, int32_t* free_stack,
+                             int64_t nfree) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int32_t b = rec.blk[rec.idx[r]];
+  const int32_t prev = r == 0 ? (int32_t)old_head : rec.blk[rec.idx[r - 1]];
+  child[b] = prev;
+  free_stack[nfree + r] = b;
+}
+
+template <typename T>
+__global__ void k_join_log(JoinRecs<T> rec, int64_t n, double* jlog) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int32_t j = rec.idx[r];
+  int L, x, y, z;
+  unpack_cell(rec.cell[j], L, x, y, z);
+  double* row = jlog + r * 12;
+  row[0] = L;
+  row[1] = x;
+  row[2] = y;
+  row[3] = z;
+  for (int q = 0; q < 8; ++q) row[4 + q] = rec.vals[j * 8 + q];
+}
+
+__global__ void k_unmark(const int32_t* list, int64_t n, uint8_t* smark) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) smark[list[i]] = 0;
+}
+
+// ---------------------------------------------------------------------------
+// propagate (_kernels.pyx:80-113): inner = sequential f64 sum of children / 8
+template <typename T>
+__global__ void k_propagate_level(const int32_t* __restrict__ blocks,
+                                  int64_t nblk, const int32_t* __restrict__ child,
+                                  T* value) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = gid >> 3;
+  const int c = (int)(gid & 7);
+  if (i >= nblk) return;
+  const int32_t b = blocks[i];
+  if (b == 0 && c != 0) return;
+  const int32_t s = b + c;
+  const int32_t cb = child[s];
+  if (cb < 0) return;
+  double acc = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) acc += (double)value[cb + q];
+  value[s] = (T)(acc / 8.0);
+}
+
+// ---------------------------------------------------------------------------
+// energy (_kernels.pyx:494-533) per leaf, deterministic block sums
+template <typename T, bool BINW>
+__global__ void __launch_bounds__(kT)
+    k_energy(const int32_t* __restrict__ lblocks, int64_t nlb,
+             const uint64_t* __restrict__ lkey, const int32_t* __restrict__ nbr,
+             const int32_t* __restrict__ child, const T* __restrict__ u,
+             const float* __restrict__ F, const float* __restrict__ W,
+             const uint32_t* __restrict__ M, int64_t stride, int nv,
+             LeafParams<T> p, double* partials, double* terms) {
+  using A = Arith<T>;
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = gid >> 3;
+  const int c = (int)(gid & 7);
+  bool active = i < nlb;
+  const int32_t b = active ? lblocks[i] : 0;
+  const int32_t s = b + c;
+  if (active && b == 0 && c != 0) active = false;
+  if (active && child[s] >= 0) active = false;
+  double term = 0.0;
+  if (active) {
+    int L, px, py, pz;
+    unpack_cell(lkey[i], L, px, py, pz);
+    const int cx = (c >> 2) & 1, cy = (c >> 1) & 1, cz = c & 1;
+    const int x = 2 * px + cx, y = 2 * py + cy, z = 2 * pz + cz;
+    const int m = 1 << L;
+    const T ih = inv_spacing<T>(p.d_max, L);
+    const T h = pow2<T>(p.d_max - L);
+    const int32_t* nb = nbr + i * 12;
+    auto U = [&](int dx, int dy, int dz) -> T {
+      const int tx = cx + dx, ty = cy + dy, tz = cz + dz;
+      const int ox = tx >> 1, oy = ty >> 1, oz = tz >> 1;
+      const int cc = ((tx & 1) << 2) | ((ty & 1) << 1) | (tz & 1);
+      if ((ox | oy | oz) == 0) return u[b + cc];
+      const int32_t r = nb[nbr_dir(ox, oy, oz)];
+      return r >= 0 ? u[r + cc] : u[-r - 2];
+    };
+    const T u0 = u[s];
+    const T gx = x + 1 < m ? (U(1, 0, 0) - u0) * ih : (T)0;
+    const T gy = y + 1 < m ? (U(0, 1, 0) - u0) * ih : (T)0;
+    const T gz = z + 1 < m ? (U(0, 0, 1) - u0) * ih : (T)0;
+    const T smooth = p.lam * A::smooth_val(gx, gy, gz, p.eps2);
+    T num = 0, den = p.gamma;
+    const int64_t sidx = i * 8 + c;
+    const uint32_t mk = BINW ? M[sidx] : 0u;
+    for (int v = 0; v < nv; ++v) {
+      const float w = BINW ? (float)((mk >> v) & 1u) : W[v * stride + sidx];
+      if (w != 0.f) {
+        const T d = u0 - (T)F[v * stride + sidx];
+        num += A::data_val((T)w, d, p.eps2);
+        den += (T)w;
+      }
+    }
+    const T t = (A::div(num, den) + smooth) * (h * h * h);
+    term = (double)t;
+    if (terms) terms[s] = term;
+  }
+  typedef cub::BlockReduce<double, kT> BR;
+  __shared__ typename BR::TempStorage tmp;
+  const double tot = BR(tmp).Sum(term);
+  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+}
+
+__global__ void k_sum_partials(const double* partials, int64_t n,
+                               double* out) {
+  double acc = 0.0;
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) acc += partials[j];
+  typedef cub::BlockReduce<double, kT> BR;
+  __shared__ typename BR::TempStorage tmp;
+  const double tot = BR(tmp).Sum(acc);
+  if (threadIdx.x == 0) *out = tot;
+}
+
+// ---------------------------------------------------------------------------
+// host orchestration
+template <typename T>
+void ensure_prepared(Ctx& c, const int32_t* child, int64_t cap, int d_max,
+                     const int64_t* state, cudaStream_t st) {
+  if (!c.valid || c.child_key != child || c.cap != cap || c.d_max != d_max)
+    ctx_prepare(c, child, cap, state, d_max, st);
+}
+
+template <typename T>
+void launch_leaf_pass(Ctx& c, const IterArgs& a, const LeafParams<T>& lp,
+                      bool frozen, cudaStream_t st) {
+  const int64_t n = c.nlb * 8;
+  const unsigned g = blocks_for(n);
+  const T* snap = (const T*)a.usnap;
+  T* uval = (T*)a.uval;
+#define OCTF_LEAF(FZ, BW)                                                   \
+  k_leaf_pass<T, FZ, BW><<<g, kT, 0, st>>>(                                 \
+      c.lblocks.p, c.nlb, c.lkey.p, c.nbr.p, a.child, snap, uval, c.F.p,    \
+      c.W.p, c.M.p, c.sstride, c.nviews, lp, c.smark.p, c.split_list.p,     \
+      c.counters.p)
+  if (frozen) {
+    if (c.binw)
+      OCTF_LEAF(true, true);
+    else
+      OCTF_LEAF(true, false);
+  } else {
+    if (c.binw)
+      OCTF_LEAF(false, true);
+    else
+      OCTF_LEAF(false, false);
+  }
+#undef OCTF_LEAF
+  OCTF_CUDA(cudaGetLastError());
+}
+
+template <typename T>
+struct EventBufs {
+  DevBuf<int32_t> slot, parent, cmask, idx, rank, blk;
+  DevBuf<int8_t> pc;
+  DevBuf<uint64_t> cell, key;
+  DevBuf<T> S, cval;
+  Events<T> view(int64_t cap) {
+    Events<T> e;
+    e.slot = slot.ensure(cap);
+    e.parent = parent.ensure(cap);
+    e.pc = pc.ensure(cap);
+    e.cell = cell.ensure(cap);
+    e.S = S.ensure(cap);
+    e.cval = cval.ensure(cap * 8);
+    e.cmask = cmask.ensure(cap);
+    e.key = key.ensure(cap);
+    e.idx = idx.ensure(cap);
+    e.rank = rank.ensure(cap);
+    e.blk = blk.ensure(cap);
+    return e;
+  }
+};
+
+template <typename T>
+struct JoinBufs {
+  DevBuf<int32_t> slot, blk, idx;
+  DevBuf<uint64_t> cell, key;
+  DevBuf<double> vals;
+  JoinRecs<T> view(int64_t cap) {
+    JoinRecs<T> r;
+    r.slot = slot.ensure(cap);
+    r.blk = blk.ensure(cap);
+    r.cell = cell.ensure(cap);
+    r.vals = vals.ensure(cap * 8);
+    r.key = key.ensure(cap);
+    r.idx = idx.ensure(cap);
+    return r;
+  }
+};
+
+template <typename T>
+void read_counters(Ctx& c, int n, cudaStream_t st) {
+  OCTF_CUDA(cudaMemcpyAsync(c.h_counters, c.counters.p, n * sizeof(int32_t),
+                            cudaMemcpyDeviceToHost, st));
+  OCTF_CUDA(cudaStreamSynchronize(st));
+}
+
+template <typename T>
+void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
+  const PassParams& prm = a.prm;
+  if (prm.d_max < 0 || prm.d_max > kMaxDepth)
+    throw Error(kEDepth, "tree depth out of range");
+  ensure_prepared<T>(c, a.child, a.cap, prm.d_max, a.state, st);
+  if (c.nviews <= 0) throw Error(kEArg, "at least one view is required");
+  const int64_t used = a.state[0];
+  if (a.snapshot)
+    OCTF_CUDA(cudaMemcpyAsync((void*)a.usnap, a.uval, used * sizeof(T),
+                              cudaMemcpyDeviceToDevice, st));
+  const LeafParams<T> lp = leaf_params<T>(prm);
+  const bool frozen = prm.tau_s <= 0.0 && prm.clamp && prm.tau_j >= 1.0;
+  c.counters.ensure(64);
+  c.split_list.ensure(c.nlb * 8 + 1);
+  OCTF_CUDA(cudaMemsetAsync(c.counters.p, 0, 8 * sizeof(int32_t), st));
+  launch_leaf_pass<T>(c, a, lp, frozen, st);
+  read_counters<T>(c, 2, st);
+  const int64_t nsplit = c.h_counters[0];
+  const int64_t ncand = c.h_counters[1];
+  const T* snap = (const T*)a.usnap;
+  T* usnap = (T*)a.usnap;
+  T* uval = (T*)a.uval;
+  const ViewSet vs = ctx_views(c);
+  int64_t splits = 0, joins = 0, jrows = 0;
+  bool changed = false;
+
+  // ---- split cascade + allocation in depth-first order
+  if (nsplit > 0) {
+    static thread_local EventBufs<T> eb;
+    const int64_t ev_cap = nsplit + (a.cap - used) / 8 + c.nfree + 8;
+    Events<T> ev = eb.view(ev_cap);
+    k_events_init<T><<<blocks_for(nsplit), kT, 0, st>>>(
+        c.split_list.p, nsplit, c.blevel.p, c.bcoord.p, snap, ev);
+    OCTF_CUDA(cudaGetLastError());
+    int64_t e0 = 0, e1 = nsplit;
+    int32_t ecount = (int32_t)nsplit;
+    OCTF_CUDA(cudaMemcpyAsync(c.counters.p + 2, &ecount, sizeof(int32_t),
+                              cudaMemcpyHostToDevice, st));
+    while (e1 > e0) {
+      k_cascade<T><<<blocks_for((e1 - e0) * 8), kT, 0, st>>>(
+          e0, e1, ev, a.child, snap, vs, lp, c.counters.p, ev_cap);
+      OCTF_CUDA(cudaGetLastError());
+      read_counters<T>(c, 4, st);
+      if (c.h_counters[3]) throw Error(kEPool, "node pool capacity exhausted");
+      e0 = e1;
+      e1 = c.h_counters[2];
+    }
+    const int64_t E = e1;
+    const int64_t fresh = E > c.nfree ? E - c.nfree : 0;
+    if (used + 8 * fresh > a.cap)
+      throw Error(kEPool, "node pool capacity exhausted");
+    k_event_keys<T><<<blocks_for(E), kT, 0, st>>>(ev, E, prm.d_max,
+                                                   prm.reverse);
+    OCTF_CUDA(cudaGetLastError());
+    sort_u64_i32(c, ev.key, ev.idx, E, st);
+    k_event_alloc<T><<<blocks_for(E), kT, 0, st>>>(ev, E, c.free_stack.p,
+                                                    c.nfree, used);
+    OCTF_CUDA(cudaGetLastError());
+    k_event_materialize<T><<<blocks_for(E * 8), kT, 0, st>>>(
+        ev, E, a.child, usnap, uval, a.joined);
+    OCTF_CUDA(cudaGetLastError());
+    // new free-list head
+    int64_t head = -1;
+    if (E < c.nfree) {
+      int32_t h;
+      OCTF_CUDA(cudaMemcpyAsync(&h, c.free_stack.p + (c.nfree - 1 - E),
+                                sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      OCTF_CUDA(cudaStreamSynchronize(st));
+      head = h;
+      c.nfree -= E;
+    } else {
+      c.nfree = 0;
+    }
+    a.state[0] = used + 8 * fresh;
+    a.state[1] = head;
+    a.state[2] += 8 * E;
+    splits = E;
+    changed = true;
+  }
+
+  // ---- join cascade, bottom-up
+  if (ncand > 0) {
+    static thread_local JoinBufs<T> jb;
+    const int64_t jcap_rec = c.nblocks * 8 + 8;
+    JoinRecs<T> rec = jb.view(jcap_rec);
+    for (int L = prm.d_max - 1; L >= 0; --L) {
+      const int64_t n = c.lvl_cnt[L];
+      if (n == 0) continue;
+      k_join_level<T><<<blocks_for(n * 8), kT, 0, st>>>(
+          c.lvl_blocks.p + c.lvl_off[L], n, c.blevel.p, c.bcoord.p, a.child,
+          a.joined, c.smark.p, snap, uval, vs, lp, rec, c.counters.p);
+      OCTF_CUDA(cudaGetLastError());
+    }
+    read_counters<T>(c, 5, st);
+    const int64_t J = c.h_counters[4];
+    if (J > 0) {
+      // sweep order: forward post-order (sweep ignores `reverse`)
+      k_join_keys<T><<<blocks_for(J), kT, 0, st>>>(rec, J, prm.d_max, 0);
+      OCTF_CUDA(cudaGetLastError());
+      sort_u64_i32(c, rec.key, rec.idx, J, st);
+      k_sweep_clear<T><<<blocks_for(J), kT, 0, st>>>(rec, J, a.child,
+                                                      a.joined);
+      OCTF_CUDA(cudaGetLastError());
+      c.free_stack.ensure(c.nfree + J + 1);
+      k_sweep_link<T><<<blocks_for(J), kT, 0, st>>>(
+          rec, J, a.state[1], a.child, c.free_stack.p, c.nfree);
+      OCTF_CUDA(cudaGetLastError());
+      int32_t last;
+      OCTF_CUDA(cudaMemcpyAsync(&last, c.free_stack.p + c.nfree + J - 1,
+                                sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      if (a.jlog && a.jcap > 0) {
+        if (prm.reverse) {
+          k_join_keys<T><<<blocks_for(J), kT, 0, st>>>(rec, J, prm.d_max, 1);
+          OCTF_CUDA(cudaGetLastError());
+          sort_u64_i32(c, rec.key, rec.idx, J, st);
+        }
+        jrows = J < a.jcap ? J : a.jcap;
+        k_join_log<T><<<blocks_for(jrows), kT, 0, st>>>(rec, jrows, a.jlog);
+        OCTF_CUDA(cudaGetLastError());
+      }
+      OCTF_CUDA(cudaStreamSynchronize(st));
+      c.nfree += J;
+      a.state[1] = last;
+      a.state[2] -= 8 * J;
+      joins = J;
+      changed = true;
+    }
+  }
+  if (nsplit > 0) {
+    k_unmark<<<blocks_for(nsplit), kT, 0, st>>>(c.split_list.p, nsplit,
+                                                c.smark.p);
+    OCTF_CUDA(cudaGetLastError());
+  }
+  c.hstate[0] = a.state[0];
+  c.hstate[1] = a.state[1];
+  c.hstate[2] = a.state[2];
+  if (changed) c.valid = false;
+  OCTF_CUDA(cudaStreamSynchronize(st));
+  a.out3[0] = splits;
+  a.out3[1] = joins;
+  a.out3[2] = jrows;
+}
+
+template <typename T>
+void propagate_impl(Ctx& c, T* value, const int32_t* child, cudaStream_t st) {
+  ensure_prepared<T>(c, child, c.cap, c.d_max, c.hstate, st);
+  for (int L = c.d_max - 1; L >= 0; --L) {
+    const int64_t n = c.lvl_cnt[L];
+    if (n == 0) continue;
+    k_propagate_level<T><<<blocks_for(n * 8), kT, 0, st>>>(
+        c.lvl_blocks.p + c.lvl_off[L], n, child, value);
+    OCTF_CUDA(cudaGetLastError());
+  }
+}
+
+template <typename T>
+double energy_impl(Ctx& c, const T* u, const int32_t* child,
+                   const PassParams& prm, double* terms, cudaStream_t st) {
+  ensure_prepared<T>(c, child, c.cap, prm.d_max, c.hstate, st);
+  const LeafParams<T> lp = leaf_params<T>(prm);
+  const int64_t n = c.nlb * 8;
+  const unsigned g = blocks_for(n);
+  c.partials.ensure(g);
+  c.dscalar.ensure(1);
+  if (c.binw)
+    k_energy<T, true><<<g, kT, 0, st>>>(c.lblocks.p, c.nlb, c.lkey.p, c.nbr.p,
+                                        child, u, c.F.p, c.W.p, c.M.p,
+                                        c.sstride, c.nviews, lp, c.partials.p,
+                                        terms);
+  else
+    k_energy<T, false><<<g, kT, 0, st>>>(c.lblocks.p, c.nlb, c.lkey.p,
+                                         c.nbr.p, child, u, c.F.p, c.W.p,
+                                         c.M.p, c.sstride, c.nviews, lp,
+                                         c.partials.p, terms);
+  OCTF_CUDA(cudaGetLastError());
+  k_sum_partials<<<1, kT, 0, st>>>(c.partials.p, g, c.dscalar.p);
+  OCTF_CUDA(cudaGetLastError());
+  OCTF_CUDA(cudaMemcpyAsync(c.h_scalar, c.dscalar.p, sizeof(double),
+                            cudaMemcpyDeviceToHost, st));
+  OCTF_CUDA(cudaStreamSynchronize(st));
+  return c.h_scalar[0];
+}
+
+}  // namespace
+}  // namespace octf

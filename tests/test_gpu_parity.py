@@ -1,0 +1,384 @@
+"""GPU parity: the CUDA path through the C ABI against the CPU oracle and the
+reference-generated golden fixtures.  fp64 mode must be bit-exact; fp32
+mode must keep the structure and stay within 1e-4 (north_star tolerance)."""
+import io
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as orc
+from tests.conftest import has_gpu
+from tests.goldens import (cameras_from, cfg1_inputs, load, load_json, sha,
+                           small_views)
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")]
+
+FP32_TOL = 1e-4
+
+
+def dev(pool, cap=None, dtype=None):
+    from paper_1608_07411_b200.octree import OctreeField
+    return OctreeField.from_host(pool.value, pool.child, pool.state, pool.d_max,
+                                 weight=pool.weight, cap=cap, dtype=dtype)
+
+
+def leaf_table(child, value):
+    """(level, x, y, z) -> value over the leaves of a host pool."""
+    from paper_1608_07411_b200.octree import _leaves
+    return {(l, x, y, z): float(value[n]) for n, l, x, y, z in _leaves(child)}
+
+
+# ----------------------------------------------------------------- build --
+class TestBuild:
+    z = load("octree_kat")
+
+    @pytest.mark.parametrize("name", ["blocky", "smooth"])
+    @pytest.mark.parametrize("tau", [-1.0, 0.0, 0.05, 0.25, 1.0])
+    def test_plain_build_bitexact(self, name, tau):
+        from paper_1608_07411_b200 import octree
+        key = f"{name}_{tau:g}"
+        t = octree.build_octree(self.z[name], tau=tau)
+        h = t.to_host()
+        assert np.array_equal(h.value, self.z[key + "_value"])
+        assert np.array_equal(h.child, self.z[key + "_child"])
+        assert np.array_equal(h.state, self.z[key + "_state"])
+        assert np.array_equal(octree.densify(t), self.z[key + "_dense"])
+
+    def test_weighted_build_bitexact(self):
+        from paper_1608_07411_b200 import octree
+        t = octree.build_octree(self.z["wf"], self.z["ww"], tau=0.3,
+                                dtype=np.float32)
+        h = t.to_host()
+        assert np.array_equal(h.value, self.z["w_value"])
+        assert np.array_equal(h.weight, self.z["w_weight"])
+        assert np.array_equal(h.child, self.z["w_child"])
+        assert np.array_equal(h.state, self.z["w_state"])
+
+    def test_mean_pyramid_matches_numpy(self):
+        from paper_1608_07411_b200 import octree
+        rng = np.random.default_rng(5)
+        g = rng.standard_normal((32, 32, 32)) * np.exp(rng.uniform(-20, 20, (32,) * 3))
+        got = octree.mean_pyramid(g)
+        want = orc.reduce_pyramid(g, "mean")
+        for a, b in zip(got, want):
+            assert np.array_equal(a, b)
+
+    def test_propagate_matches_oracle(self):
+        from paper_1608_07411_b200 import octree
+        t = octree.build_octree(self.z["smooth"], tau=0.05)
+        h = t.to_host()
+        v = h.value.copy()
+        v[h.child >= 0] = 123.0
+        t2 = dev(orc.Pool(v, h.child, h.state, h.d_max))
+        octree.propagate_means(t2)
+        ref = v.copy()
+        orc.propagate(ref, h.child)
+        assert np.array_equal(t2.to_host().value, ref)
+
+    def test_rejects_bad_grids(self):
+        from paper_1608_07411_b200 import octree
+        with pytest.raises(ValueError):
+            octree.build_octree(np.zeros((4, 4)))
+        with pytest.raises(ValueError):
+            octree.build_octree(np.zeros((6, 6, 6)))
+        with pytest.raises(ValueError):
+            octree.build_octree(np.zeros((8, 8, 8)), np.zeros((4, 4, 4)))
+
+
+# ------------------------------------------------------------------ TSDF --
+class TestTsdf:
+    z = load("small")
+
+    def test_tsdf_views_u0_bitexact(self):
+        from paper_1608_07411_b200 import fusion, octree, tsdf, volume
+        z = self.z
+        n = int(z["resolution"])
+        dom = volume.VolumeDomain(tuple(z["origin"]), float(z["voxel_size"]), n)
+        wf = torch.zeros((n, n, n), dtype=torch.float64, device="cuda")
+        ws = torch.zeros_like(wf)
+        for i, (d, c) in enumerate(zip(z["depths"], cameras_from(z))):
+            vt = tsdf.build_view_tsdf(d, c, dom, 0.004, 0.02, accumulate=(wf, ws))
+            assert np.array_equal(vt.f.cpu().numpy(), z["tsdf_f"][i])
+            assert np.array_equal(vt.w.cpu().numpy(), z["tsdf_w"][i])
+            tree = fusion.build_view_tree(vt, 0.1).to_host()
+            ref = small_views(z)[i]
+            assert np.array_equal(tree.value, ref.value)
+            assert np.array_equal(tree.weight, ref.weight)
+            assert np.array_equal(tree.child, ref.child)
+        ub = fusion.initial_field(wf, ws, 1e-4)
+        assert np.array_equal(ub.cpu().numpy(), z["ubar"])
+        u0 = octree.build_octree(ub, tau=0.1).to_host()
+        assert np.array_equal(u0.value, z["u0_value"])
+        assert np.array_equal(u0.child, z["u0_child"])
+
+    def test_cfg1_tsdf_and_trees(self):
+        from paper_1608_07411_b200 import fusion, octree, tsdf, volume
+        depths, cams, origin, vox, n, p = cfg1_inputs()
+        meta = load_json("cfg1")
+        dom = volume.VolumeDomain(origin, vox, n)
+        wf = torch.zeros((n, n, n), dtype=torch.float64, device="cuda")
+        ws = torch.zeros_like(wf)
+        for i, (d, c) in enumerate(zip(depths, cams)):
+            vt = tsdf.build_view_tsdf(d, c, dom, p.delta, p.eta, accumulate=(wf, ws))
+            assert sha(vt.f.cpu().numpy()) == meta["tsdf_f"][i]
+            assert sha(vt.w.cpu().numpy()) == meta["tsdf_w"][i]
+            t = fusion.build_view_tree(vt, p.tau).to_host()
+            assert sha(t.value) == meta["views"][i]["value"]
+            assert sha(t.weight) == meta["views"][i]["weight"]
+            assert sha(t.child) == meta["views"][i]["child"]
+        ub = fusion.initial_field(wf, ws, p.gamma)
+        assert sha(ub.cpu().numpy()) == meta["ubar"]
+        u0 = octree.build_octree(ub, tau=p.tau).to_host()
+        assert sha(u0.value) == meta["u0"]["value"]
+        assert sha(u0.child) == meta["u0"]["child"]
+
+
+# ---------------------------------------------------------------- solver --
+def cfg1_views_u0():
+    z = load("cfg1")
+    depths, cams, origin, vox, n, p = cfg1_inputs()
+    views = []
+    for d, c in zip(depths, cams):
+        f, w = orc.build_view_tsdf(d, c, origin, vox, n, p.delta, p.eta)
+        views.append(orc.build_octree(f, w, tau=p.tau, dtype=np.float32))
+    u0 = orc.Pool(z["u0_value"], z["u0_child"], z["u0_state"], 6)
+    return views, u0, p, z
+
+
+class TestKernelLevelParity:
+    """The reference plugin signature (kernel module) in snapshot mode: every
+    pass's full pools hash-equal to the reference's (cfg1, 50 passes)."""
+
+    def test_cfg1_every_pass_pools(self):
+        from paper_1608_07411_b200 import _backend, _lib
+        kern = _backend.get()
+        views_h, u0h, p, _ = cfg1_views_u0()
+        meta = load_json("cfg1")
+        sp = orc.solver_pool(u0h)
+        u = dev(orc.Pool(sp.value, sp.child, sp.state, 6))
+        snap = dev(orc.Pool(sp.snap, sp.child, sp.state, 6)).value
+        joined = torch.zeros(u.capacity, dtype=torch.uint8, device="cuda")
+        vs = [dev(v) for v in views_h]
+        vv, vw, vc = [v.value for v in vs], [v.weight for v in vs], [v.child for v in vs]
+        ctx = _lib.Ctx()
+        for t, ref in enumerate(meta["passes"]):
+            xi = orc.step_scale(t, p)
+            s, j, r = kern.iterate_pass(u.value, snap, u.child, joined, u.state,
+                                        vv, vw, vc, 6, p.lam, p.eps, p.gamma, xi,
+                                        p.tau_split, p.tau_join, p.clamp, False,
+                                        None, ctx=ctx)
+            kern.propagate(u.value, u.child, state=u.state, d_max=6, ctx=ctx)
+            e = kern.tree_energy(u.value, u.child, vv, vw, vc, 6, p.lam, p.eps,
+                                 p.gamma, state=u.state, ctx=ctx)
+            used = int(u.state[0])
+            assert (s, j) == (ref["splits"], ref["joins"]), t
+            assert [int(q) for q in u.state] == ref["state"], t
+            assert sha(u.child[:used].cpu().numpy()) == ref["child"], t
+            assert sha(u.value[:used].cpu().numpy()) == ref["value"], t
+            assert sha(snap[:used].cpu().numpy()) == ref["snap"], t
+            assert sha(joined[:used].cpu().numpy()) == ref["joined"], t
+            assert e == pytest.approx(ref["energy"], rel=1e-13, abs=0), t
+
+
+class TestFuse:
+    def test_small_scene_fp64_matches_golden(self):
+        from paper_1608_07411_b200 import fusion, octree
+        z = load("small")
+        u0 = dev(orc.Pool(z["u0_value"], z["u0_child"], z["u0_state"], 4))
+        views = [dev(v) for v in small_views(z)]
+        res = fusion.fuse(u0, views, fusion.FusionParams(iterations=6),
+                          log_joins=True)
+        h = res.field.to_host()
+        assert np.array_equal(h.child, z["final_child"])
+        assert np.array_equal(h.state, z["final_state"])
+        assert leaf_table(h.child, h.value) == leaf_table(z["final_child"],
+                                                          z["final_value"])
+        assert np.array_equal(res.join_log, z["join_log"])
+        assert [[s.splits, s.joins, s.node_count] for s in res.stats] == \
+            z["counts"].tolist()
+        np.testing.assert_allclose([s.energy for s in res.stats], z["energies"],
+                                   rtol=1e-13, atol=0)
+
+    def test_cfg1_fp64_fifty_passes(self):
+        from paper_1608_07411_b200 import fusion, octree
+        views_h, u0h, p, z = cfg1_views_u0()
+        meta = load_json("cfg1")
+        params = fusion.FusionParams(delta=p.delta, eta=p.eta, lam=p.lam,
+                                     iterations=p.iterations)
+        res = fusion.fuse(dev(u0h), [dev(v) for v in views_h], params,
+                          log_joins=True)
+        h = res.field.to_host()
+        assert np.array_equal(h.child, z["final_child"])
+        assert np.array_equal(h.state, z["final_state"])
+        assert leaf_table(h.child, h.value) == leaf_table(z["final_child"],
+                                                          z["final_value"])
+        assert np.array_equal(res.join_log, z["join_log"])
+        for s, ref in zip(res.stats, meta["passes"]):
+            assert (s.splits, s.joins, s.node_count) == \
+                (ref["splits"], ref["joins"], ref["node_count"])
+            assert s.energy == pytest.approx(ref["energy"], rel=1e-13, abs=0)
+        buf = io.StringIO()
+        octree.serialize(res.field, buf)
+        assert sha(np.frombuffer(buf.getvalue().encode(), np.uint8)) == \
+            meta["serialize_sha"]
+
+    def test_cfg1_fp32_structure_and_tolerance(self):
+        from paper_1608_07411_b200 import fusion
+        views_h, u0h, p, z = cfg1_views_u0()
+        params = fusion.FusionParams(delta=p.delta, eta=p.eta, lam=p.lam,
+                                     iterations=p.iterations)
+        res = fusion.fuse(dev(u0h), [dev(v) for v in views_h], params,
+                          precision="fp32")
+        h = res.field.to_host()
+        got = leaf_table(h.child, h.value)
+        want = leaf_table(z["final_child"], z["final_value"])
+        assert got.keys() == want.keys()
+        err = max(abs(got[k] - want[k]) for k in want)
+        assert err <= FP32_TOL, err
+
+    def test_traversal_order_does_not_change_result(self):
+        from paper_1608_07411_b200 import fusion, octree
+        views_h, u0h, p, _ = cfg1_views_u0()
+        params = fusion.FusionParams(delta=p.delta, eta=p.eta, lam=p.lam,
+                                     iterations=8)
+        outs = []
+        for rev in (False, True):
+            res = fusion.fuse(dev(u0h), [dev(v) for v in views_h], params,
+                              reverse=rev, log_joins=True)
+            buf = io.StringIO()
+            octree.serialize(res.field, buf)
+            outs.append(buf.getvalue())
+            ref = orc.fuse(u0h, views_h, orc.Params(delta=p.delta, eta=p.eta,
+                                                    lam=p.lam, iterations=8),
+                           reverse=rev, log_joins=True)
+            assert np.array_equal(res.join_log, ref.join_log)
+        assert outs[0] == outs[1]
+
+    @pytest.mark.parametrize("d", [4, 5])
+    def test_cfg2_fixed_structure(self, d):
+        from paper_1608_07411_b200 import fusion, octree, scenes
+        zc = load("cfg2")
+        fs, ws = scenes.make_cfg2_samples(d_max=d)
+        params = fusion.FusionParams(lam=1.0, iterations=12, tau=-1.0,
+                                     tau_split=0.0, tau_join=1.5)
+        views = [octree.build_octree(f, w, tau=-1.0, dtype=np.float32)
+                 for f, w in zip(fs, ws)]
+        wf = sum(w.astype(np.float64) * f.astype(np.float64) for f, w in zip(fs, ws))
+        wsum = sum(w.astype(np.float64) for w in ws)
+        u0 = octree.build_octree(fusion.initial_field(wf, wsum, params.gamma),
+                                 tau=-1.0)
+        assert np.array_equal(u0.to_host().value, zc[f"d{d}_u0_value"])
+        res = fusion.fuse(u0, views, params)
+        got = res.field.to_host().value
+        assert np.array_equal(got, zc[f"d{d}_final_value"])
+        # per-leaf terms are bit-exact; the sum is a tree reduction instead
+        # of the reference's sequential Morton-order sum
+        np.testing.assert_allclose([s.energy for s in res.stats],
+                                   zc[f"d{d}_energies"], rtol=1e-12, atol=0)
+        res32 = fusion.fuse(u0, views, params, precision="fp32")
+        g32 = res32.field.to_host().value
+        assert np.max(np.abs(g32 - zc[f"d{d}_final_value"])) <= FP32_TOL
+
+
+class TestRandomTrees:
+    """Live oracle comparison on seeded random blocky scenes with mixed
+    leaf depths, splits and joins."""
+
+    @pytest.mark.parametrize("seed", range(6))
+    def test_random_scene_passes(self, seed):
+        from paper_1608_07411_b200 import fusion
+        rng = np.random.default_rng(100 + seed)
+        d = 4
+        n = 1 << d
+        views_h = []
+        for _ in range(3):
+            f = (rng.integers(-2, 3, (n, n, n)) * 0.45).astype(np.float32)
+            w = (rng.random((n, n, n)) < 0.8).astype(np.uint8)
+            f[w == 0] = -1.0
+            views_h.append(orc.build_octree(f, w, tau=0.3, dtype=np.float32))
+        ub = np.clip(rng.standard_normal((n, n, n)) * 0.6, -1, 1)
+        u0h = orc.build_octree(ub, tau=0.4)
+        pr = orc.Params(iterations=10, xi0=0.3, tau_split=0.15, tau_join=0.45,
+                        lam=0.4)
+        ref = orc.fuse(u0h, views_h, pr, log_joins=True)
+        params = fusion.FusionParams(iterations=10, xi0=0.3, tau_split=0.15,
+                                     tau_join=0.45, lam=0.4)
+        res = fusion.fuse(dev(u0h), [dev(v) for v in views_h], params,
+                          log_joins=True)
+        h = res.field.to_host()
+        assert np.array_equal(h.child, ref.field.child[:ref.field.used])
+        assert list(h.state) == list(ref.field.state)
+        assert leaf_table(h.child, h.value) == leaf_table(
+            ref.field.child, ref.field.value)
+        assert np.array_equal(res.join_log, ref.join_log)
+        assert [(s.splits, s.joins) for s in res.stats] == \
+            [(s.splits, s.joins) for s in ref.stats]
+
+
+class TestEdgeCases:
+    def test_single_leaf_tree(self):
+        from paper_1608_07411_b200 import fusion, octree
+        f = np.full((8, 8, 8), 0.3, dtype=np.float32)
+        w = np.ones((8, 8, 8), dtype=np.uint8)
+        view = octree.build_octree(f, w, tau=0.1, dtype=np.float32)
+        u0 = octree.build_octree(np.full((8, 8, 8), 0.9), tau=0.1)
+        assert u0.node_count == 1
+        p = fusion.FusionParams(iterations=3)
+        res = fusion.fuse(u0, [view], p, log_joins=True)
+        vh = view.to_host()
+        ref = orc.fuse(orc.Pool(u0.to_host().value, u0.to_host().child,
+                                u0.state.copy(), 3),
+                       [orc.Pool(vh.value, vh.child, vh.state, 3, weight=vh.weight)],
+                       orc.Params(iterations=3), log_joins=True)
+        h = res.field.to_host()
+        assert np.array_equal(h.child, ref.field.child[:ref.field.used])
+        assert leaf_table(h.child, h.value) == leaf_table(ref.field.child,
+                                                          ref.field.value)
+
+    def test_zero_iterations_and_errors(self):
+        from paper_1608_07411_b200 import fusion, octree
+        z = load("small")
+        u0 = dev(orc.Pool(z["u0_value"], z["u0_child"], z["u0_state"], 4))
+        views = [dev(v) for v in small_views(z)]
+        res = fusion.fuse(u0, views, fusion.FusionParams(iterations=0))
+        assert res.stats == []
+        assert np.array_equal(octree.densify(res.field), octree.densify(u0))
+        with pytest.raises(ValueError):
+            fusion.fuse(u0, [], fusion.FusionParams(iterations=1))
+        small = octree.build_octree(np.zeros((8, 8, 8)),
+                                    np.zeros((8, 8, 8), dtype=np.uint8))
+        with pytest.raises(ValueError):
+            fusion.fuse(u0, [small], fusion.FusionParams(iterations=1))
+
+    def test_pool_growth_on_exhaustion(self):
+        # a flat zero field splits all the way down: a kernel-level pass on a
+        # pool with no spare slots raises the reference's RuntimeError, while
+        # fuse() grows its pool and matches the full-capacity oracle
+        from paper_1608_07411_b200 import _backend, fusion, octree
+        kern = _backend.get()
+        n = 8
+        f = np.zeros((n, n, n), dtype=np.float32)
+        w = np.ones((n, n, n), dtype=np.uint8)
+        view = octree.build_octree(f, w, tau=0.1, dtype=np.float32)
+        u = octree.build_octree(np.zeros((n, n, n)), tau=0.1)
+        assert u.capacity == 1
+        snap = u.value.clone()
+        joined = torch.zeros(1, dtype=torch.uint8, device="cuda")
+        with pytest.raises(RuntimeError, match="capacity"):
+            kern.iterate_pass(u.value, snap, u.child, joined, u.state,
+                              [view.value], [view.weight], [view.child], 3,
+                              0.3, 0.25, 1e-4, 0.1, 0.1, 0.5, True, False, None)
+        p = fusion.FusionParams(iterations=2)
+        res = fusion.fuse(u, [view], p)
+        vh = view.to_host()
+        ref = orc.fuse(orc.Pool(np.zeros(1), np.full(1, -1, np.int32),
+                                np.array([1, -1, 1], np.int64), 3),
+                       [orc.Pool(vh.value, vh.child, vh.state, 3, weight=vh.weight)],
+                       orc.Params(iterations=2))
+        assert res.stats[0].splits == ref.stats[0].splits > 0
+        h = res.field.to_host()
+        assert np.array_equal(h.child, ref.field.child[:ref.field.used])
+        assert leaf_table(h.child, h.value) == leaf_table(ref.field.child,
+                                                          ref.field.value)

@@ -66,6 +66,12 @@ int octf_ctx_invalidate(octf_ctx *ctx);
  * samples (0/1), sample stride, views, valid */
 int octf_ctx_info(octf_ctx *ctx, int64_t *out);
 
+/* Live profiling: enable != 0 brackets the leaf-update and energy kernels
+ * with CUDA events on their launch stream.  out[0..4] (optional) receives
+ * {leaf-update ms, leaf-update launches, energy ms, energy launches, kernel
+ * launches} accumulated since the previous call, which resets them. */
+int octf_ctx_profile(octf_ctx *ctx, int enable, double *out);
+
 /* _kernels.pyx:384-461 iterate_pass -- one Jacobi descent pass with the
  * in-pass split cascade, join cascade and sweep.  snapshot=1 reproduces the
  * reference's own first step (copy uval into usnap, :390-393); snapshot=0
@@ -80,6 +86,34 @@ int octf_iterate_pass(octf_ctx *ctx, int dtype, void *usnap, void *uval,
                       double xi, double tau_s, double tau_j, int clamp,
                       int reverse, int snapshot, double *jlog, int64_t jcap,
                       int64_t *out3, void *stream);
+
+/* One pass of the reference's fuse loop (fusion.py:221-228) in one call:
+ * iterate_pass in ping-pong mode (snapshot=0) + propagate of uval.  The
+ * energy of the incoming (snapshot) state -- i.e. the previous pass's
+ * post-propagate energy, _kernels.pyx:536-578 -- is evaluated by the same
+ * leaf kernel from the same stencil values and returned in *energy_pre. */
+int octf_fuse_pass(octf_ctx *ctx, int dtype, void *usnap, void *uval,
+                   int32_t *uchild, uint8_t *ujoined, int64_t *ustate,
+                   int64_t cap, int nviews, const float *const *vvals,
+                   const float *const *vws, const int32_t *const *vchilds,
+                   int d_max, double lam, double eps, double gamma, double xi,
+                   double tau_s, double tau_j, int clamp, int reverse,
+                   double *jlog, int64_t jcap, int64_t *out3,
+                   double *energy_pre, void *stream);
+
+/* npasses passes of a frozen structure (tau_s <= 0, tau_j >= 1 with clamp:
+ * no split or join can happen) without any host round trip.  Buffers
+ * alternate: pass k reads ubuf[k%2] and writes ubuf[(k+1)%2];
+ * energies_pre[k] (host) = energy before pass k.  xis: host step sizes. */
+int octf_fuse_passes_frozen(octf_ctx *ctx, int dtype, void *ubuf0, void *ubuf1,
+                            const int32_t *uchild, const int64_t *ustate,
+                            int64_t cap, int nviews, const float *const *vvals,
+                            const float *const *vws,
+                            const int32_t *const *vchilds, int d_max,
+                            double lam, double eps, double gamma,
+                            double tau_s, double tau_j, int clamp,
+                            const double *xis, int npasses,
+                            double *energies_pre, void *stream);
 
 /* _kernels.pyx:80-113 propagate -- inner value = (sequential sum of the 8
  * children)/8, bottom-up.  ctx may be NULL (a temporary one is built). */

@@ -107,6 +107,40 @@ def iterate_pass(uval, usnap, uchild, ujoined, ustate, vvals, vws, vchilds,
     return int(out3[0]), int(out3[1]), int(out3[2])
 
 
+def fuse_pass(usnap, uval, uchild, ujoined, ustate, vvals, vws, vchilds,
+              d_max, lam, eps, gamma, xi, tau_s, tau_j, clamp, reverse, jlog,
+              *, ctx):
+    """One pass of the fuse loop (iterate + propagate) with the energy of the
+    incoming state; returns (splits, joins, jrows, energy_pre)."""
+    tv, tw, tc = _views(vvals, vws, vchilds)
+    out3 = np.zeros(3, dtype=np.int64)
+    e = np.zeros(1, dtype=np.float64)
+    jcap = 0 if jlog is None else int(jlog.shape[0])
+    call("octf_fuse_pass", ctx.h, _dtype_code(uval), ptr(usnap), ptr(uval),
+         ptr(uchild), ptr(ujoined), _state_ptr(ustate), uval.shape[0],
+         len(vvals), tv, tw, tc, int(d_max), float(lam), float(eps),
+         float(gamma), float(xi), float(tau_s), float(tau_j), int(bool(clamp)),
+         int(bool(reverse)), ptr(jlog) if jcap else None, jcap,
+         out3.ctypes.data, e.ctypes.data, stream_handle())
+    return int(out3[0]), int(out3[1]), int(out3[2]), float(e[0])
+
+
+def fuse_passes_frozen(ubuf0, ubuf1, uchild, ustate, vvals, vws, vchilds,
+                       d_max, lam, eps, gamma, tau_s, tau_j, clamp, xis, *,
+                       ctx):
+    """len(xis) passes of a frozen structure in one call; returns the
+    energies before each pass.  Pass k reads buffer k%2."""
+    tv, tw, tc = _views(vvals, vws, vchilds)
+    xis = np.ascontiguousarray(np.asarray(xis, dtype=np.float64))
+    en = np.zeros(len(xis), dtype=np.float64)
+    call("octf_fuse_passes_frozen", ctx.h, _dtype_code(ubuf0), ptr(ubuf0),
+         ptr(ubuf1), ptr(uchild), _state_ptr(ustate), ubuf0.shape[0],
+         len(vvals), tv, tw, tc, int(d_max), float(lam), float(eps),
+         float(gamma), float(tau_s), float(tau_j), int(bool(clamp)),
+         xis.ctypes.data, len(xis), en.ctypes.data, stream_handle())
+    return en
+
+
 def tree_energy(uval, uchild, vvals, vws, vchilds, d_max, lam, eps, gamma, *,
                 state=None, ctx=None, terms=None):
     """_kernels.pyx:536-578; returns the energy as a Python float."""

@@ -34,9 +34,16 @@ _SIGS = {
     "octf_ctx_destroy": ([P], I32),
     "octf_ctx_invalidate": ([P], I32),
     "octf_ctx_info": ([P, P], I32),
+    "octf_ctx_profile": ([P, I32, P], I32),
     "octf_iterate_pass": ([P, I32, P, P, P, P, P, I64, I32, P, P, P, I32, DBL,
                            DBL, DBL, DBL, DBL, DBL, I32, I32, I32, P, I64, P,
                            P], I32),
+    "octf_fuse_pass": ([P, I32, P, P, P, P, P, I64, I32, P, P, P, I32, DBL,
+                        DBL, DBL, DBL, DBL, DBL, I32, I32, P, I64, P, P, P],
+                       I32),
+    "octf_fuse_passes_frozen": ([P, I32, P, P, P, P, I64, I32, P, P, P, I32,
+                                 DBL, DBL, DBL, DBL, DBL, I32, P, I32, P, P],
+                                I32),
     "octf_propagate": ([P, I32, P, P, P, I64, I32, P], I32),
     "octf_tree_energy": ([P, I32, P, P, P, I64, I32, P, P, P, I32, DBL, DBL,
                           DBL, P, P, P], I32),
@@ -111,6 +118,15 @@ class Ctx:
         keys = ("leaf_blocks", "leaves", "blocks", "free_blocks", "mask_samples",
                 "sample_stride", "views", "valid")
         return dict(zip(keys, (int(v) for v in out)))
+
+    def profile(self, enable: bool = True) -> dict:
+        """Read and reset the live kernel timers; (re)arm them if enable."""
+        import numpy as np
+        out = np.zeros(5, dtype=np.float64)
+        call("octf_ctx_profile", self.h, int(bool(enable)), out.ctypes.data)
+        return {"leaf_ms": float(out[0]), "leaf_launches": int(out[1]),
+                "energy_ms": float(out[2]), "energy_launches": int(out[3]),
+                "launches": int(out[4])}
 
     def close(self):
         if self.h:

@@ -160,6 +160,25 @@ int octf_ctx_info(octf_ctx* ctx, int64_t* out) {
   });
 }
 
+int octf_ctx_profile(octf_ctx* ctx, int enable, double* out) {
+  return guard([&] {
+    if (!ctx) throw octf::Error(octf::kEArg, "null context");
+    octf::Ctx& c = ctx->c;
+    if (enable && !c.tev[0])
+      for (auto& e : c.tev) OCTF_CUDA(cudaEventCreate(&e));
+    if (out) {
+      out[0] = c.t_leaf_ms;
+      out[1] = (double)c.n_leaf;
+      out[2] = c.t_energy_ms;
+      out[3] = (double)c.n_energy;
+      out[4] = (double)c.launches;
+    }
+    c.t_leaf_ms = c.t_energy_ms = 0;
+    c.n_leaf = c.n_energy = c.launches = 0;
+    c.timing = enable != 0;
+  });
+}
+
 int octf_iterate_pass(octf_ctx* ctx, int dtype, void* usnap, void* uval,
                       int32_t* uchild, uint8_t* ujoined, int64_t* ustate,
                       int64_t cap, int nviews, const float* const* vvals,
@@ -195,6 +214,85 @@ int octf_iterate_pass(octf_ctx* ctx, int dtype, void* usnap, void* uval,
     out3[0] = a.out3[0];
     out3[1] = a.out3[1];
     out3[2] = a.out3[2];
+  });
+}
+
+int octf_fuse_pass(octf_ctx* ctx, int dtype, void* usnap, void* uval,
+                   int32_t* uchild, uint8_t* ujoined, int64_t* ustate,
+                   int64_t cap, int nviews, const float* const* vvals,
+                   const float* const* vws, const int32_t* const* vchilds,
+                   int d_max, double lam, double eps, double gamma, double xi,
+                   double tau_s, double tau_j, int clamp, int reverse,
+                   double* jlog, int64_t jcap, int64_t* out3,
+                   double* energy_pre, void* stream) {
+  return guard([&] {
+    if (!ctx || !usnap || !uval || !uchild || !ujoined || !ustate || !out3 ||
+        !energy_pre)
+      throw octf::Error(octf::kEArg, "null argument");
+    check_dtype(dtype);
+    if (d_max < 0 || d_max > OCTF_MAX_DEPTH)
+      throw octf::Error(octf::kEDepth, "tree depth out of range");
+    if (nviews < 1) throw octf::Error(octf::kEArg, "at least one view is required");
+    octf::ctx_set_views(ctx->c, nviews, vvals, vws, vchilds, S(stream));
+    octf::IterArgs a;
+    a.usnap = usnap;
+    a.uval = uval;
+    a.child = uchild;
+    a.joined = ujoined;
+    a.state = ustate;
+    a.cap = cap;
+    a.prm = make_params(d_max, lam, eps, gamma, xi, tau_s, tau_j, clamp,
+                        reverse);
+    a.jlog = jlog;
+    a.jcap = jlog ? jcap : 0;
+    a.snapshot = 0;
+    a.want_energy = 1;
+    if (dtype == OCTF_F64) {
+      octf::iterate_pass_f64(ctx->c, a, S(stream));
+      octf::propagate_ctx_f64(ctx->c, (double*)uval, uchild, S(stream));
+    } else {
+      octf::iterate_pass_f32(ctx->c, a, S(stream));
+      octf::propagate_ctx_f32(ctx->c, (float*)uval, uchild, S(stream));
+    }
+    out3[0] = a.out3[0];
+    out3[1] = a.out3[1];
+    out3[2] = a.out3[2];
+    *energy_pre = a.energy_pre;
+  });
+}
+
+int octf_fuse_passes_frozen(octf_ctx* ctx, int dtype, void* ubuf0, void* ubuf1,
+                            const int32_t* uchild, const int64_t* ustate,
+                            int64_t cap, int nviews, const float* const* vvals,
+                            const float* const* vws,
+                            const int32_t* const* vchilds, int d_max,
+                            double lam, double eps, double gamma,
+                            double tau_s, double tau_j, int clamp,
+                            const double* xis, int npasses,
+                            double* energies_pre, void* stream) {
+  return guard([&] {
+    if (!ctx || !ubuf0 || !ubuf1 || !uchild || !ustate || !xis ||
+        !energies_pre)
+      throw octf::Error(octf::kEArg, "null argument");
+    check_dtype(dtype);
+    if (d_max < 0 || d_max > OCTF_MAX_DEPTH)
+      throw octf::Error(octf::kEDepth, "tree depth out of range");
+    if (nviews < 1) throw octf::Error(octf::kEArg, "at least one view is required");
+    octf::ctx_set_views(ctx->c, nviews, vvals, vws, vchilds, S(stream));
+    octf::FrozenArgs a;
+    a.ubuf[0] = ubuf0;
+    a.ubuf[1] = ubuf1;
+    a.child = uchild;
+    a.state = ustate;
+    a.cap = cap;
+    a.prm = make_params(d_max, lam, eps, gamma, 0.0, tau_s, tau_j, clamp, 0);
+    a.xis = xis;
+    a.npasses = npasses;
+    a.energies_pre = energies_pre;
+    if (dtype == OCTF_F64)
+      octf::frozen_passes_f64(ctx->c, a, S(stream));
+    else
+      octf::frozen_passes_f32(ctx->c, a, S(stream));
   });
 }
 

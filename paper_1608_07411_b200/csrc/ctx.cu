@@ -28,6 +28,9 @@ Ctx::Ctx() {
 Ctx::~Ctx() {
   if (h_counters) cudaFreeHost(h_counters);
   if (h_scalar) cudaFreeHost(h_scalar);
+  for (auto& e : tev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : pev) cudaEventDestroy(e);
 }
 
 namespace {

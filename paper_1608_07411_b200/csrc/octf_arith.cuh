@@ -48,6 +48,15 @@ struct Arith<double> {
                                                       double gz, double eps2) {
     return sqrt(gx * gx + gy * gy + gz * gz + eps2);
   }
+  // both data terms from one root: gradient w*d/s (_kernels.pyx:251) and
+  // value w*s (_kernels.pyx:531), s = sqrt(d^2 + eps^2)
+  __device__ __forceinline__ static void data_both(double w, double d,
+                                                   double eps2, double& g,
+                                                   double& e) {
+    const double s = sqrt(d * d + eps2);
+    g = w * d / s;
+    e = w * s;
+  }
   __device__ __forceinline__ static double div(double a, double b) {
     return a / b;
   }
@@ -78,6 +87,13 @@ struct Arith<float> {
   __device__ __forceinline__ static float smooth_val(float gx, float gy,
                                                      float gz, float eps2) {
     return sqrtf(gx * gx + gy * gy + gz * gz + eps2);
+  }
+  __device__ __forceinline__ static void data_both(float w, float d, float eps2,
+                                                   float& g, float& e) {
+    const float q = d * d + eps2;
+    const float r = rsqrtf(q);
+    g = w * d * r;
+    e = w * q * r;
   }
   __device__ __forceinline__ static float div(float a, float b) {
     return __fdividef(a, b);

@@ -108,6 +108,13 @@ struct Ctx {
   DevBuf<double> partials;
   DevBuf<double> dscalar;
 
+  // live profiling (octf_ctx_profile): CUDA events on the launch stream
+  bool timing = false;
+  cudaEvent_t tev[4] = {nullptr, nullptr, nullptr, nullptr};
+  std::vector<cudaEvent_t> pev;  // per-pass pairs for batched passes
+  double t_leaf_ms = 0, t_energy_ms = 0;
+  int64_t n_leaf = 0, n_energy = 0, launches = 0;
+
   // host pinned staging for small readbacks
   int32_t* h_counters = nullptr;
   double* h_scalar = nullptr;
@@ -144,7 +151,22 @@ struct IterArgs {
   double* jlog;       // device rows of 12 doubles (may be null)
   int64_t jcap;
   int snapshot;       // 1: copy uval -> usnap first (_kernels.pyx:390-393)
+  int want_energy = 0;      // also evaluate the energy of the snapshot state
+  double energy_pre = 0.0;  // ... returned here
   int64_t out3[3];    // splits, joins, log rows
+};
+
+// K passes on a frozen structure (no split or join can occur) with no host
+// round trip: buffers alternate, energies_pre[k] = energy before pass k
+struct FrozenArgs {
+  void* ubuf[2];
+  const int32_t* child;
+  const int64_t* state;
+  int64_t cap;
+  PassParams prm;     // xi is taken from xis[]
+  const double* xis;  // host, npasses
+  int npasses;
+  double* energies_pre;  // host, npasses
 };
 
 // per precision entry points (solver_f64.cu / solver_f32.cu)
@@ -158,5 +180,7 @@ double energy_f64(Ctx& c, const double* u, const int32_t* child,
                   const PassParams& p, double* terms, cudaStream_t st);
 double energy_f32(Ctx& c, const float* u, const int32_t* child,
                   const PassParams& p, double* terms, cudaStream_t st);
+void frozen_passes_f64(Ctx& c, FrozenArgs& a, cudaStream_t st);
+void frozen_passes_f32(Ctx& c, FrozenArgs& a, cudaStream_t st);
 
 }  // namespace octf

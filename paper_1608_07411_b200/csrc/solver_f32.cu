@@ -14,3 +14,9 @@ double energy_f32(Ctx& c, const float* u, const int32_t* child,
   return energy_impl<float>(c, u, child, p, terms, st);
 }
 }  // namespace octf
+
+namespace octf {
+void frozen_passes_f32(Ctx& c, FrozenArgs& a, cudaStream_t st) {
+  frozen_passes_impl<float>(c, a, st);
+}
+}  // namespace octf

@@ -14,3 +14,9 @@ double energy_f64(Ctx& c, const double* u, const int32_t* child,
   return energy_impl<double>(c, u, child, p, terms, st);
 }
 }  // namespace octf
+
+namespace octf {
+void frozen_passes_f64(Ctx& c, FrozenArgs& a, cudaStream_t st) {
+  frozen_passes_impl<double>(c, a, st);
+}
+}  // namespace octf

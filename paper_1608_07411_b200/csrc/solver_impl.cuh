@@ -83,34 +83,66 @@ __device__ __forceinline__ T clamp1(T v) {
 // ---------------------------------------------------------------------------
 // 1. fast leaf update over leaf blocks.  8 lanes = the 8 sibling slots of a
 // block; the 13-point stencil resolves through the block's neighbour table.
-template <typename T, bool FROZEN, bool BINW>
-__global__ void __launch_bounds__(kT)
-    k_leaf_pass(const int32_t* __restrict__ lblocks, int64_t nlb,
-                const uint64_t* __restrict__ lkey,
-                const int32_t* __restrict__ nbr,
-                const int32_t* __restrict__ child, const T* __restrict__ snap,
-                T* __restrict__ uval, const float* __restrict__ F,
-                const float* __restrict__ W, const uint32_t* __restrict__ M,
-                int64_t stride, int nv, LeafParams<T> p, uint8_t* smark,
-                int32_t* split_list, int32_t* counters) {
+// ENERGY also evaluates the reference's per-leaf energy term
+// (_kernels.pyx:517-533) of the snapshot state -- the post-propagate state
+// of the previous pass -- from the same stencil values and the same square
+// roots, so energy costs no extra pass over the samples.
+template <typename T>
+struct LeafArgs {
+  const int32_t* __restrict__ lblocks;
+  int64_t nlb;
+  const uint64_t* __restrict__ lkey;
+  const int32_t* __restrict__ nbr;
+  const int32_t* __restrict__ child;
+  const T* __restrict__ snap;
+  T* __restrict__ uval;
+  const float* __restrict__ F;
+  const float* __restrict__ W;
+  const uint32_t* __restrict__ M;
+  int64_t stride;
+  int nv;
+  LeafParams<T> p;
+  uint8_t* smark;
+  int32_t* split_list;
+  int32_t* counters;
+  double* epart;  // per-CTA energy partial sums
+};
+
+constexpr int kVC = 8;  // views per register chunk (independent loads)
+
+template <typename T, bool FROZEN, bool BINW, bool ENERGY>
+__global__ void __launch_bounds__(kT) k_leaf_pass(LeafArgs<T> a) {
   using A = Arith<T>;
+  const LeafParams<T>& p = a.p;
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t i = gid >> 3;
   const int c = (int)(gid & 7);
-  bool active = i < nlb;
-  const int32_t b = active ? __ldg(lblocks + i) : 0;
+  bool active = i < a.nlb;
+  const int32_t b = active ? __ldg(a.lblocks + i) : 0;
   const int32_t s = b + c;
   if (active && b == 0 && c != 0) active = false;
-  if (active && __ldg(child + s) >= 0) active = false;
+  if (active && __ldg(a.child + s) >= 0) active = false;
   bool ok_join = false, positive = false;
+  double eterm = 0.0;
   if (active) {
+    const int64_t sidx = i * 8 + c;
+    const float* __restrict__ Fp = a.F + sidx;
+    const uint32_t mk = BINW ? __ldg(a.M + sidx) : 0u;
+    // first chunk of samples in flight before the stencil work
+    float f[kVC], w[kVC];
+#pragma unroll
+    for (int j = 0; j < kVC; ++j) {
+      f[j] = j < a.nv ? __ldg(Fp + j * a.stride) : 0.f;
+      if (!BINW) w[j] = j < a.nv ? __ldg(a.W + j * a.stride + sidx) : 0.f;
+    }
     int L, px, py, pz;
-    unpack_cell(__ldg(lkey + i), L, px, py, pz);
+    unpack_cell(__ldg(a.lkey + i), L, px, py, pz);
     const int cx = (c >> 2) & 1, cy = (c >> 1) & 1, cz = c & 1;
     const int x = 2 * px + cx, y = 2 * py + cy, z = 2 * pz + cz;
     const int m = 1 << L;
     const T ih = inv_spacing<T>(p.d_max, L);
-    const int32_t* nb = nbr + i * 12;
+    const int32_t* nb = a.nbr + i * 12;
+    const T* __restrict__ snap = a.snap;
     auto S = [&](int dx, int dy, int dz) -> T {
       const int tx = cx + dx, ty = cy + dy, tz = cz + dz;
       const int ox = tx >> 1, oy = ty >> 1, oz = tz >> 1;
@@ -152,35 +184,49 @@ __global__ void __launch_bounds__(kT)
     }
     const T div = ((p0 - bx) + (p1 - by) + (p2 - bz)) * ih;
     // data term in view order, zero weights skipped (_kernels.pyx:244-252)
-    T num = 0, den = p.gamma;
-    const int64_t sidx = i * 8 + c;
-    if (BINW) {
-      const uint32_t mk = __ldg(M + sidx);
-      for (int v = 0; v < nv; ++v) {
-        const T d = S0 - (T)__ldg(F + v * stride + sidx);
-        if ((mk >> v) & 1u) {
-          num += A::data_grad((T)1, d, p.eps2);
-          den += (T)1;
+    T num = 0, den = p.gamma, enm = 0;
+    for (int v0 = 0; v0 < a.nv; v0 += kVC) {
+      if (v0) {
+#pragma unroll
+        for (int j = 0; j < kVC; ++j) {
+          const int v = v0 + j;
+          f[j] = v < a.nv ? __ldg(Fp + v * a.stride) : 0.f;
+          if (!BINW) w[j] = v < a.nv ? __ldg(a.W + v * a.stride + sidx) : 0.f;
         }
       }
-    } else {
-      for (int v = 0; v < nv; ++v) {
-        const float w = __ldg(W + v * stride + sidx);
-        const T d = S0 - (T)__ldg(F + v * stride + sidx);
-        if (w != 0.f) {
-          num += A::data_grad((T)w, d, p.eps2);
-          den += (T)w;
+#pragma unroll
+      for (int j = 0; j < kVC; ++j) {
+        const int v = v0 + j;
+        const bool on = BINW ? (((mk >> (v & 31)) & 1u) && v < a.nv)
+                             : (w[j] != 0.f);
+        if (on) {
+          const T wv = BINW ? (T)1 : (T)w[j];
+          const T d = S0 - (T)f[j];
+          if (ENERGY) {
+            T g, e;
+            A::data_both(wv, d, p.eps2, g, e);
+            num += g;
+            enm += e;
+          } else {
+            num += A::data_grad(wv, d, p.eps2);
+          }
+          den += wv;
         }
       }
+    }
+    if (ENERGY) {
+      const T h = pow2<T>(p.d_max - L);
+      const T smooth = p.lam * A::smooth_val(gx, gy, gz, p.eps2);
+      eterm = (double)((A::div(enm, den) + smooth) * (h * h * h));
     }
     const T du = p.lam * div - A::div(num, den);
     T dn = S0 + p.xi * du;
     if (!FROZEN && L < p.d_max && fabs((double)dn) < p.tau_s) {
-      smark[s] = 1;
-      split_list[atomicAdd(counters, 1)] = s;
+      a.smark[s] = 1;
+      a.split_list[atomicAdd(a.counters, 1)] = s;
     } else {
       if (p.clamp) dn = clamp1(dn);
-      uval[s] = dn;
+      a.uval[s] = dn;
       ok_join = (double)dn > p.tau_j || (double)dn < -p.tau_j;
       positive = dn > (T)0;
     }
@@ -196,8 +242,14 @@ __global__ void __launch_bounds__(kT)
       pos |= __shfl_xor_sync(0xffffffffu, pos, o);
       neg |= __shfl_xor_sync(0xffffffffu, neg, o);
     }
-    if (c == 0 && i < nlb && b != 0 && all && !(pos && neg))
-      atomicAdd(counters + 1, 1);
+    if (c == 0 && i < a.nlb && b != 0 && all && !(pos && neg))
+      atomicAdd(a.counters + 1, 1);
+  }
+  if (ENERGY) {
+    typedef cub::BlockReduce<double, kT> BR;
+    __shared__ typename BR::TempStorage tmp;
+    const double tot = BR(tmp).Sum(eterm);
+    if (threadIdx.x == 0) a.epart[blockIdx.x] = tot;
   }
 }
 
@@ -612,31 +664,52 @@ void ensure_prepared(Ctx& c, const int32_t* child, int64_t cap, int d_max,
     ctx_prepare(c, child, cap, state, d_max, st);
 }
 
+// grid of the leaf kernel (also the number of energy partials per pass)
+inline unsigned leaf_grid(const Ctx& c) { return blocks_for(c.nlb * 8); }
+
 template <typename T>
-void launch_leaf_pass(Ctx& c, const IterArgs& a, const LeafParams<T>& lp,
-                      bool frozen, cudaStream_t st) {
-  const int64_t n = c.nlb * 8;
-  const unsigned g = blocks_for(n);
-  const T* snap = (const T*)a.usnap;
-  T* uval = (T*)a.uval;
-#define OCTF_LEAF(FZ, BW)                                                   \
-  k_leaf_pass<T, FZ, BW><<<g, kT, 0, st>>>(                                 \
-      c.lblocks.p, c.nlb, c.lkey.p, c.nbr.p, a.child, snap, uval, c.F.p,    \
-      c.W.p, c.M.p, c.sstride, c.nviews, lp, c.smark.p, c.split_list.p,     \
-      c.counters.p)
+void launch_leaf_pass(Ctx& c, const T* snap, T* uval, const int32_t* child,
+                      const LeafParams<T>& lp, bool frozen, double* epart,
+                      cudaStream_t st, bool timed = true) {
+  const unsigned g = leaf_grid(c);
+  LeafArgs<T> a;
+  a.lblocks = c.lblocks.p;
+  a.nlb = c.nlb;
+  a.lkey = c.lkey.p;
+  a.nbr = c.nbr.p;
+  a.child = child;
+  a.snap = snap;
+  a.uval = uval;
+  a.F = c.F.p;
+  a.W = c.W.p;
+  a.M = c.M.p;
+  a.stride = c.sstride;
+  a.nv = c.nviews;
+  a.p = lp;
+  a.smark = c.smark.p;
+  a.split_list = c.split_list.p;
+  a.counters = c.counters.p;
+  a.epart = epart;
+  const bool en = epart != nullptr;
+  if (timed && c.timing) OCTF_CUDA(cudaEventRecord(c.tev[0], st));
+#define OCTF_LEAF(FZ, BW, EN) k_leaf_pass<T, FZ, BW, EN><<<g, kT, 0, st>>>(a)
   if (frozen) {
-    if (c.binw)
-      OCTF_LEAF(true, true);
-    else
-      OCTF_LEAF(true, false);
+    if (c.binw) {
+      if (en) OCTF_LEAF(true, true, true); else OCTF_LEAF(true, true, false);
+    } else {
+      if (en) OCTF_LEAF(true, false, true); else OCTF_LEAF(true, false, false);
+    }
   } else {
-    if (c.binw)
-      OCTF_LEAF(false, true);
-    else
-      OCTF_LEAF(false, false);
+    if (c.binw) {
+      if (en) OCTF_LEAF(false, true, true); else OCTF_LEAF(false, true, false);
+    } else {
+      if (en) OCTF_LEAF(false, false, true); else OCTF_LEAF(false, false, false);
+    }
   }
 #undef OCTF_LEAF
   OCTF_CUDA(cudaGetLastError());
+  ++c.launches;
+  if (timed && c.timing) OCTF_CUDA(cudaEventRecord(c.tev[1], st));
 }
 
 template <typename T>
@@ -702,8 +775,29 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
   c.counters.ensure(64);
   c.split_list.ensure(c.nlb * 8 + 1);
   OCTF_CUDA(cudaMemsetAsync(c.counters.p, 0, 8 * sizeof(int32_t), st));
-  launch_leaf_pass<T>(c, a, lp, frozen, st);
+  double* epart = nullptr;
+  if (a.want_energy) {
+    c.partials.ensure(leaf_grid(c));
+    c.dscalar.ensure(1);
+    epart = c.partials.p;
+  }
+  launch_leaf_pass<T>(c, (const T*)a.usnap, (T*)a.uval, a.child, lp, frozen,
+                      epart, st);
+  if (epart) {
+    k_sum_partials<<<1, kT, 0, st>>>(epart, leaf_grid(c), c.dscalar.p);
+    OCTF_CUDA(cudaGetLastError());
+    ++c.launches;
+    OCTF_CUDA(cudaMemcpyAsync(c.h_scalar, c.dscalar.p, sizeof(double),
+                              cudaMemcpyDeviceToHost, st));
+  }
   read_counters<T>(c, 2, st);
+  a.energy_pre = epart ? c.h_scalar[0] : 0.0;
+  if (c.timing) {
+    float ms = 0.f;
+    OCTF_CUDA(cudaEventElapsedTime(&ms, c.tev[0], c.tev[1]));
+    c.t_leaf_ms += ms;
+    ++c.n_leaf;
+  }
   const int64_t nsplit = c.h_counters[0];
   const int64_t ncand = c.h_counters[1];
   const T* snap = (const T*)a.usnap;
@@ -721,6 +815,7 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
     k_events_init<T><<<blocks_for(nsplit), kT, 0, st>>>(
         c.split_list.p, nsplit, c.blevel.p, c.bcoord.p, snap, ev);
     OCTF_CUDA(cudaGetLastError());
+  ++c.launches;
     int64_t e0 = 0, e1 = nsplit;
     int32_t ecount = (int32_t)nsplit;
     OCTF_CUDA(cudaMemcpyAsync(c.counters.p + 2, &ecount, sizeof(int32_t),
@@ -729,6 +824,7 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
       k_cascade<T><<<blocks_for((e1 - e0) * 8), kT, 0, st>>>(
           e0, e1, ev, a.child, snap, vs, lp, c.counters.p, ev_cap);
       OCTF_CUDA(cudaGetLastError());
+  ++c.launches;
       read_counters<T>(c, 4, st);
       if (c.h_counters[3]) throw Error(kEPool, "node pool capacity exhausted");
       e0 = e1;
@@ -741,13 +837,16 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
     k_event_keys<T><<<blocks_for(E), kT, 0, st>>>(ev, E, prm.d_max,
                                                    prm.reverse);
     OCTF_CUDA(cudaGetLastError());
+  ++c.launches;
     sort_u64_i32(c, ev.key, ev.idx, E, st);
     k_event_alloc<T><<<blocks_for(E), kT, 0, st>>>(ev, E, c.free_stack.p,
                                                     c.nfree, used);
     OCTF_CUDA(cudaGetLastError());
+  ++c.launches;
     k_event_materialize<T><<<blocks_for(E * 8), kT, 0, st>>>(
         ev, E, a.child, usnap, uval, a.joined);
     OCTF_CUDA(cudaGetLastError());
+  ++c.launches;
     // new free-list head
     int64_t head = -1;
     if (E < c.nfree) {
@@ -779,6 +878,7 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
           c.lvl_blocks.p + c.lvl_off[L], n, c.blevel.p, c.bcoord.p, a.child,
           a.joined, c.smark.p, snap, uval, vs, lp, rec, c.counters.p);
       OCTF_CUDA(cudaGetLastError());
+  ++c.launches;
     }
     read_counters<T>(c, 5, st);
     const int64_t J = c.h_counters[4];
@@ -786,14 +886,17 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
       // sweep order: forward post-order (sweep ignores `reverse`)
       k_join_keys<T><<<blocks_for(J), kT, 0, st>>>(rec, J, prm.d_max, 0);
       OCTF_CUDA(cudaGetLastError());
+  ++c.launches;
       sort_u64_i32(c, rec.key, rec.idx, J, st);
       k_sweep_clear<T><<<blocks_for(J), kT, 0, st>>>(rec, J, a.child,
                                                       a.joined);
       OCTF_CUDA(cudaGetLastError());
+  ++c.launches;
       c.free_stack.ensure(c.nfree + J + 1);
       k_sweep_link<T><<<blocks_for(J), kT, 0, st>>>(
           rec, J, a.state[1], a.child, c.free_stack.p, c.nfree);
       OCTF_CUDA(cudaGetLastError());
+  ++c.launches;
       int32_t last;
       OCTF_CUDA(cudaMemcpyAsync(&last, c.free_stack.p + c.nfree + J - 1,
                                 sizeof(int32_t), cudaMemcpyDeviceToHost, st));
@@ -801,11 +904,13 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
         if (prm.reverse) {
           k_join_keys<T><<<blocks_for(J), kT, 0, st>>>(rec, J, prm.d_max, 1);
           OCTF_CUDA(cudaGetLastError());
+  ++c.launches;
           sort_u64_i32(c, rec.key, rec.idx, J, st);
         }
         jrows = J < a.jcap ? J : a.jcap;
         k_join_log<T><<<blocks_for(jrows), kT, 0, st>>>(rec, jrows, a.jlog);
         OCTF_CUDA(cudaGetLastError());
+  ++c.launches;
       }
       OCTF_CUDA(cudaStreamSynchronize(st));
       c.nfree += J;
@@ -819,6 +924,7 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
     k_unmark<<<blocks_for(nsplit), kT, 0, st>>>(c.split_list.p, nsplit,
                                                 c.smark.p);
     OCTF_CUDA(cudaGetLastError());
+  ++c.launches;
   }
   c.hstate[0] = a.state[0];
   c.hstate[1] = a.state[1];
@@ -831,15 +937,22 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
 }
 
 template <typename T>
-void propagate_impl(Ctx& c, T* value, const int32_t* child, cudaStream_t st) {
-  ensure_prepared<T>(c, child, c.cap, c.d_max, c.hstate, st);
+void launch_propagate(Ctx& c, T* value, const int32_t* child,
+                      cudaStream_t st) {
   for (int L = c.d_max - 1; L >= 0; --L) {
     const int64_t n = c.lvl_cnt[L];
     if (n == 0) continue;
     k_propagate_level<T><<<blocks_for(n * 8), kT, 0, st>>>(
         c.lvl_blocks.p + c.lvl_off[L], n, child, value);
     OCTF_CUDA(cudaGetLastError());
+    ++c.launches;
   }
+}
+
+template <typename T>
+void propagate_impl(Ctx& c, T* value, const int32_t* child, cudaStream_t st) {
+  ensure_prepared<T>(c, child, c.cap, c.d_max, c.hstate, st);
+  launch_propagate<T>(c, value, child, st);
 }
 
 template <typename T>
@@ -851,6 +964,7 @@ double energy_impl(Ctx& c, const T* u, const int32_t* child,
   const unsigned g = blocks_for(n);
   c.partials.ensure(g);
   c.dscalar.ensure(1);
+  if (c.timing) OCTF_CUDA(cudaEventRecord(c.tev[2], st));
   if (c.binw)
     k_energy<T, true><<<g, kT, 0, st>>>(c.lblocks.p, c.nlb, c.lkey.p, c.nbr.p,
                                         child, u, c.F.p, c.W.p, c.M.p,
@@ -862,12 +976,89 @@ double energy_impl(Ctx& c, const T* u, const int32_t* child,
                                          c.M.p, c.sstride, c.nviews, lp,
                                          c.partials.p, terms);
   OCTF_CUDA(cudaGetLastError());
+  ++c.launches;
+  if (c.timing) OCTF_CUDA(cudaEventRecord(c.tev[3], st));
   k_sum_partials<<<1, kT, 0, st>>>(c.partials.p, g, c.dscalar.p);
   OCTF_CUDA(cudaGetLastError());
+  ++c.launches;
   OCTF_CUDA(cudaMemcpyAsync(c.h_scalar, c.dscalar.p, sizeof(double),
                             cudaMemcpyDeviceToHost, st));
   OCTF_CUDA(cudaStreamSynchronize(st));
+  if (c.timing) {
+    float ms = 0.f;
+    OCTF_CUDA(cudaEventElapsedTime(&ms, c.tev[2], c.tev[3]));
+    c.t_energy_ms += ms;
+    ++c.n_energy;
+  }
   return c.h_scalar[0];
+}
+
+
+__global__ void k_sum_partials_multi(const double* partials, int64_t n,
+                                     double* out) {
+  // one CTA per pass, same reduction shape as k_sum_partials
+  const double* p = partials + (int64_t)blockIdx.x * n;
+  double acc = 0.0;
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) acc += p[j];
+  typedef cub::BlockReduce<double, kT> BR;
+  __shared__ typename BR::TempStorage tmp;
+  const double tot = BR(tmp).Sum(acc);
+  if (threadIdx.x == 0) out[blockIdx.x] = tot;
+}
+
+// K passes of a frozen structure back to back: per pass one leaf kernel
+// (update + energy of the incoming state) and the propagate levels; the
+// host only waits once, for the K energies.
+template <typename T>
+void frozen_passes_impl(Ctx& c, FrozenArgs& a, cudaStream_t st) {
+  const PassParams& prm = a.prm;
+  if (prm.d_max < 0 || prm.d_max > kMaxDepth)
+    throw Error(kEDepth, "tree depth out of range");
+  if (!(prm.tau_s <= 0.0 && prm.clamp && prm.tau_j >= 1.0))
+    throw Error(kEArg, "batched passes need a frozen structure "
+                       "(tau_split <= 0, tau_join >= 1, clamp)");
+  if (a.npasses < 1) return;
+  ensure_prepared<T>(c, a.child, a.cap, prm.d_max, a.state, st);
+  if (c.nviews <= 0) throw Error(kEArg, "at least one view is required");
+  const unsigned g = leaf_grid(c);
+  c.partials.ensure((size_t)g * a.npasses);
+  c.dscalar.ensure(a.npasses);
+  c.counters.ensure(64);
+  c.split_list.ensure(c.nlb * 8 + 1);
+  if (c.timing && (int)c.pev.size() < 2 * a.npasses) {
+    for (int k = (int)c.pev.size(); k < 2 * a.npasses; ++k) {
+      cudaEvent_t e;
+      OCTF_CUDA(cudaEventCreate(&e));
+      c.pev.push_back(e);
+    }
+  }
+  for (int k = 0; k < a.npasses; ++k) {
+    PassParams pk = prm;
+    pk.xi = a.xis[k];
+    const LeafParams<T> lp = leaf_params<T>(pk);
+    const T* snap = (const T*)a.ubuf[k & 1];
+    T* uval = (T*)a.ubuf[(k + 1) & 1];
+    if (c.timing) OCTF_CUDA(cudaEventRecord(c.pev[2 * k], st));
+    launch_leaf_pass<T>(c, snap, uval, a.child, lp, true,
+                        c.partials.p + (size_t)k * g, st, false);
+    if (c.timing) OCTF_CUDA(cudaEventRecord(c.pev[2 * k + 1], st));
+    launch_propagate<T>(c, uval, a.child, st);
+  }
+  k_sum_partials_multi<<<a.npasses, kT, 0, st>>>(c.partials.p, g, c.dscalar.p);
+  OCTF_CUDA(cudaGetLastError());
+  ++c.launches;
+  OCTF_CUDA(cudaMemcpyAsync(a.energies_pre, c.dscalar.p,
+                            a.npasses * sizeof(double), cudaMemcpyDeviceToHost,
+                            st));
+  OCTF_CUDA(cudaStreamSynchronize(st));
+  if (c.timing) {
+    for (int k = 0; k < a.npasses; ++k) {
+      float ms = 0.f;
+      OCTF_CUDA(cudaEventElapsedTime(&ms, c.pev[2 * k], c.pev[2 * k + 1]));
+      c.t_leaf_ms += ms;
+      ++c.n_leaf;
+    }
+  }
 }
 
 }  // namespace

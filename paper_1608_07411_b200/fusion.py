@@ -38,6 +38,7 @@ __all__ = [
     "view_arrays",
     "initial_field",
     "fuse",
+    "Solver",
     "tree_energy",
     "write_report",
     "read_report",
@@ -183,74 +184,151 @@ def tree_energy(u: OctreeField, views, params: FusionParams, *,
         params.eps, params.gamma, state=u.state, ctx=ctx))
 
 
+class Solver:
+    """The descent schedule as a stepping object (reference fusion.py:218-236).
+
+    One pass = iterate + propagate; the energy of a pass's result is
+    evaluated by the next pass's leaf kernel from the same stencil and sample
+    reads (``octf_fuse_pass``) -- or, after the last pass, by ``finish()``.
+    With a frozen structure (tau_split <= 0, tau_join >= 1, clamp: no split
+    or join can happen) ``run`` issues many passes in one call with no host
+    round trip (``octf_fuse_passes_frozen``).  Used by ``fuse`` and the
+    benchmark.
+    """
+
+    def __init__(self, u0: OctreeField, views, params: FusionParams, *,
+                 log_joins: bool = False, reverse: bool = False,
+                 precision: str = "fp64"):
+        if not views:
+            raise ValueError("at least one view is required")
+        for v in views:
+            if v.d_max != u0.d_max:
+                raise ValueError("view and iterate depths differ")
+        if precision not in ("fp64", "fp32"):
+            raise ValueError("precision must be 'fp64' or 'fp32'")
+        self.params = params
+        self.reverse = reverse
+        self.log_joins = log_joins
+        self.frozen = (params.tau_split <= 0.0 and params.clamp
+                       and params.tau_join >= 1.0)
+        self.dtype = torch.float64 if precision == "fp64" else torch.float32
+        self.kern = _backend.get()
+        self.u = _solver_field(u0, self.dtype)
+        self.vvals, self.vws, self.vchilds = view_arrays(views)
+        self.ctx = _lib.Ctx()
+        self.jbuf = None
+        self.chunks: list[np.ndarray] = []
+        self.stats: list[IterationStats] = []
+        # `cur` holds the latest values; `nxt` receives the next pass
+        self.cur, self.nxt = self.u.value, self.u.snap
+
+    def _itemsize(self) -> int:
+        return 2 * self.u.value.element_size() + self.u.child.element_size()
+
+    def _settle(self, energy_pre: float) -> None:
+        if self.stats and self.stats[-1].energy is None:
+            self.stats[-1].energy = energy_pre
+
+    def step(self, t: int) -> IterationStats:
+        p, u = self.params, self.u
+        xi = step_scale(t, p)
+        t0 = time.perf_counter()
+        while True:
+            if self.log_joins and (self.jbuf is None
+                                   or self.jbuf.shape[0] < u.capacity // 8 + 8):
+                self.jbuf = torch.zeros((u.capacity // 8 + 8, 12),
+                                        dtype=torch.float64, device=device())
+            try:
+                splits, joins, jrows, e_pre = self.kern.fuse_pass(
+                    self.cur, self.nxt, u.child, u.joined, u.state, self.vvals,
+                    self.vws, self.vchilds, u.d_max, p.lam, p.eps, p.gamma, xi,
+                    p.tau_split, p.tau_join, p.clamp, self.reverse, self.jbuf,
+                    ctx=self.ctx)
+                break
+            except RuntimeError as exc:
+                if "capacity" not in str(exc):
+                    raise
+                u.value, u.snap = self.cur, self.nxt
+                _grow(u)
+                self.cur, self.nxt = u.value, u.snap
+                self.ctx.invalidate()
+        self._settle(e_pre)
+        wall_ms = (time.perf_counter() - t0) * 1e3
+        if self.jbuf is not None:
+            if jrows != joins:
+                raise RuntimeError("join log truncated")
+            if jrows:
+                self.chunks.append(to_numpy(self.jbuf[:jrows]).copy())
+        self.cur, self.nxt = self.nxt, self.cur
+        st = IterationStats(t + 1, None, u.node_count,
+                            u.node_count * self._itemsize(), splits, joins,
+                            wall_ms)
+        self.stats.append(st)
+        return st
+
+    def run(self, t0: int, k: int) -> list:
+        """Passes t0 .. t0+k-1; batched on the GPU when the structure is
+        frozen."""
+        if k <= 0:
+            return []
+        if not self.frozen or self.log_joins:
+            return [self.step(t) for t in range(t0, t0 + k)]
+        p, u = self.params, self.u
+        xis = [step_scale(t, p) for t in range(t0, t0 + k)]
+        w0 = time.perf_counter()
+        en = self.kern.fuse_passes_frozen(
+            self.cur, self.nxt, u.child, u.state, self.vvals, self.vws,
+            self.vchilds, u.d_max, p.lam, p.eps, p.gamma, p.tau_split,
+            p.tau_join, p.clamp, xis, ctx=self.ctx)
+        wall = (time.perf_counter() - w0) * 1e3 / k
+        if k % 2:
+            self.cur, self.nxt = self.nxt, self.cur
+        out = []
+        for j, t in enumerate(range(t0, t0 + k)):
+            self._settle(float(en[j]))
+            st = IterationStats(t + 1, None, u.node_count,
+                                u.node_count * self._itemsize(), 0, 0, wall)
+            self.stats.append(st)
+            out.append(st)
+        return out
+
+    def finish(self) -> None:
+        """Evaluate the energy of the latest state (after the last pass)."""
+        if self.stats and self.stats[-1].energy is None:
+            u, p = self.u, self.params
+            self.stats[-1].energy = self.kern.tree_energy(
+                self.cur, u.child, self.vvals, self.vws, self.vchilds, u.d_max,
+                p.lam, p.eps, p.gamma, state=u.state, ctx=self.ctx)
+
+    def result(self) -> FuseResult:
+        self.finish()
+        self.u.value, self.u.snap = self.cur, self.nxt
+        join_log = None
+        if self.log_joins:
+            join_log = (np.vstack(self.chunks) if self.chunks
+                        else np.zeros((0, 12), dtype=np.float64))
+        return FuseResult(field=self.u, stats=list(self.stats),
+                          join_log=join_log)
+
+    def close(self):
+        self.ctx.close()
+
+
 def fuse(u0: OctreeField, views, params: FusionParams, *,
          log_joins: bool = False, reverse: bool = False,
          precision: str = "fp64") -> FuseResult:
     """Run the full descent schedule on an octree iterate (fusion.py:186-241).
 
     ``u0`` is left untouched.  Statistics carry one row per pass; energies
-    are evaluated after the pass's restructuring and re-propagation.
+    are those after the pass's restructuring and re-propagation.
     """
-    if not views:
-        raise ValueError("at least one view is required")
-    for v in views:
-        if v.d_max != u0.d_max:
-            raise ValueError("view and iterate depths differ")
-    if precision not in ("fp64", "fp32"):
-        raise ValueError("precision must be 'fp64' or 'fp32'")
-    dtype = torch.float64 if precision == "fp64" else torch.float32
-    kern = _backend.get()
-    u = _solver_field(u0, dtype)
-    vvals, vws, vchilds = view_arrays(views)
-    ctx = _lib.Ctx()
-    jbuf = None
-    chunks: list[np.ndarray] = []
-    stats: list[IterationStats] = []
-    itemsize = 2 * u.value.element_size() + u.child.element_size()
-    # `cur` holds the latest values; `nxt` receives the next pass
-    cur, nxt = u.value, u.snap
-    for t in range(params.iterations):
-        xi = step_scale(t, params)
-        t0 = time.perf_counter()
-        while True:
-            if log_joins and (jbuf is None or jbuf.shape[0] < u.capacity // 8 + 8):
-                jbuf = torch.zeros((u.capacity // 8 + 8, 12), dtype=torch.float64,
-                                   device=device())
-            try:
-                splits, joins, jrows = kern.iterate_pass(
-                    nxt, cur, u.child, u.joined, u.state, vvals, vws, vchilds,
-                    u.d_max, params.lam, params.eps, params.gamma, xi,
-                    params.tau_split, params.tau_join, params.clamp, reverse,
-                    jbuf, ctx=ctx, snapshot=False)
-                break
-            except RuntimeError as exc:
-                if "capacity" not in str(exc):
-                    raise
-                u.value, u.snap = cur, nxt
-                _grow(u)
-                cur, nxt = u.value, u.snap
-                ctx.invalidate()
-        kern.propagate(nxt, u.child, state=u.state, d_max=u.d_max, ctx=ctx)
-        energy = kern.tree_energy(nxt, u.child, vvals, vws, vchilds, u.d_max,
-                                  params.lam, params.eps, params.gamma,
-                                  state=u.state, ctx=ctx)
-        wall_ms = (time.perf_counter() - t0) * 1e3
-        if jbuf is not None:
-            if jrows != joins:
-                raise RuntimeError("join log truncated")
-            if jrows:
-                chunks.append(to_numpy(jbuf[:jrows]).copy())
-        cur, nxt = nxt, cur
-        stats.append(IterationStats(t + 1, energy, u.node_count,
-                                    u.node_count * itemsize, splits, joins,
-                                    wall_ms))
-    u.value, u.snap = cur, nxt
-    join_log = None
-    if log_joins:
-        join_log = (np.vstack(chunks) if chunks
-                    else np.zeros((0, 12), dtype=np.float64))
-    ctx.close()
-    return FuseResult(field=u, stats=stats, join_log=join_log)
+    solver = Solver(u0, views, params, log_joins=log_joins, reverse=reverse,
+                    precision=precision)
+    solver.run(0, params.iterations)
+    res = solver.result()
+    solver.close()
+    return res
+
 
 
 # -- iteration reports (fusion.py:363-403) ----------------------------------

@@ -190,11 +190,16 @@ class OctreeField:
     @classmethod
     def from_host(cls, value, child, state, d_max, weight=None,
                   cap: int | None = None, dtype=None) -> "OctreeField":
-        value = np.asarray(value)
+        if not isinstance(value, torch.Tensor):
+            value = np.asarray(value)
+        if not isinstance(child, torch.Tensor):
+            child = np.asarray(child, dtype=np.int32)
+        if weight is not None and not isinstance(weight, torch.Tensor):
+            weight = np.asarray(weight, np.float32)
         cap = value.shape[0] if cap is None else cap
         v = to_pool(value, dtype=dtype, cap=cap, fill=0)
-        c = to_pool(np.asarray(child, dtype=np.int32), cap=cap, fill=-1)
-        w = None if weight is None else to_pool(np.asarray(weight, np.float32),
+        c = to_pool(child, dtype=np.int32, cap=cap, fill=-1)
+        w = None if weight is None else to_pool(weight, dtype=np.float32,
                                                 cap=cap, fill=0)
         return cls(v, c, state, d_max, weight=w)
 

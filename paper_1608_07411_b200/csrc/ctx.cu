@@ -162,8 +162,8 @@ __global__ void k_gather(const int32_t* __restrict__ ucs,
       w = vs.w[v][n];
       flag |= (w != 0.f && w != 1.f);
     }
-    F[v * stride + sidx] = f;
-    W[v * stride + sidx] = w;
+    F[sidx * stride + v] = f;
+    W[sidx * stride + v] = w;
   }
   if (flag) atomicExch(nonbin, 1);
 }
@@ -173,7 +173,7 @@ __global__ void k_masks(const float* __restrict__ W, int64_t stride, int nv,
   int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   uint32_t m = 0;
-  for (int v = 0; v < nv; ++v) m |= (W[v * stride + s] != 0.f ? 1u : 0u) << v;
+  for (int v = 0; v < nv; ++v) m |= (W[s * stride + v] != 0.f ? 1u : 0u) << v;
   M[s] = m;
 }
 
@@ -377,15 +377,20 @@ ViewSet ctx_views(const Ctx& c) {
 }
 
 void ctx_gather(Ctx& c, cudaStream_t st) {
+  // one contiguous vector of views per leaf, padded to 16 B: a lane reads
+  // its samples with 128-bit loads, a warp reads 32 vectors back to back
   int64_t n = c.nlb * 8;
-  c.sstride = n;
   int nv = c.nviews;
-  c.F.ensure((size_t)nv * n);
-  c.W.ensure((size_t)nv * n);
+  const int64_t nvp = (nv + 3) & ~3;
+  c.sstride = nvp;
+  c.F.ensure((size_t)nvp * n);
+  c.W.ensure((size_t)nvp * n);
+  OCTF_CUDA(cudaMemsetAsync(c.F.p, 0, (size_t)nvp * n * sizeof(float), st));
+  OCTF_CUDA(cudaMemsetAsync(c.W.p, 0, (size_t)nvp * n * sizeof(float), st));
   OCTF_CUDA(cudaMemsetAsync(c.counters.p, 0, sizeof(int32_t), st));
   k_gather<<<grid_for(n), kThreads, 0, st>>>(c.child_key, c.lblocks.p, c.nlb,
                                               c.lkey.p, ctx_views(c), c.F.p,
-                                              c.W.p, n, c.counters.p);
+                                              c.W.p, nvp, c.counters.p);
   OCTF_CUDA(cudaGetLastError());
   OCTF_CUDA(cudaMemcpyAsync(c.h_counters, c.counters.p, sizeof(int32_t),
                             cudaMemcpyDeviceToHost, st));
@@ -393,7 +398,7 @@ void ctx_gather(Ctx& c, cudaStream_t st) {
   c.binw = (c.h_counters[0] == 0) && nv <= 32;
   if (c.binw) {
     c.M.ensure(n);
-    k_masks<<<grid_for(n), kThreads, 0, st>>>(c.W.p, n, nv, n, c.M.p);
+    k_masks<<<grid_for(n), kThreads, 0, st>>>(c.W.p, nvp, nv, n, c.M.p);
     OCTF_CUDA(cudaGetLastError());
   }
 }

@@ -1,0 +1,259 @@
+// The leaf-update kernel: the hot path of every solver pass.
+//
+// Included by solver_impl.cuh inside namespace octf::{anonymous}.
+//
+// Mapping: one CTA = 256 threads = 32 leaf blocks; the 8 lanes of a group are
+// the 8 sibling slots of one block (the reference's contiguous child block,
+// octree.py:49-71), so
+//  * the block's own values reach every lane with one __shfl_xor per stencil
+//    point: a +-1 step along an axis flips exactly that axis's bit of the
+//    child index, for the own block and the neighbour block alike;
+//  * only lanes whose step leaves the block read memory, through the
+//    block's 12-entry neighbour table (compile-time direction per stencil
+//    point and lane parity);
+//  * each leaf's N samples are one contiguous 16 B-aligned vector read with
+//    128-bit loads (a warp streams 32 consecutive vectors), all issued
+//    before the stencil arithmetic.
+// ENERGY also evaluates the reference's per-leaf energy term
+// (_kernels.pyx:517-533) of the incoming (snapshot) state, which is the
+// previous pass's post-propagate state, from the same values and roots.
+#pragma once
+
+template <typename T>
+struct LeafArgs {
+  const int32_t* __restrict__ lblocks;
+  int64_t nlb;
+  const uint64_t* __restrict__ lkey;
+  const int32_t* __restrict__ nbr;
+  const int32_t* __restrict__ child;
+  const T* __restrict__ snap;
+  T* __restrict__ uval;
+  const float* __restrict__ F;
+  const float* __restrict__ W;
+  const uint32_t* __restrict__ M;
+  int64_t stride;  // floats per leaf sample vector (views padded to 4)
+  int nv;
+  LeafParams<T> p;
+  uint8_t* smark;
+  int32_t* split_list;
+  int32_t* counters;
+  double* epart;  // per-CTA energy partial sums
+};
+
+// table direction of a step that leaves the block along the given axes
+template <int DX, int DY, int DZ>
+__device__ __forceinline__ int step_dir(bool ex, bool ey, bool ez) {
+  constexpr int fx = DX < 0 ? 0 : 1, fy = DY < 0 ? 2 : 3, fz = DZ < 0 ? 4 : 5;
+  // edge directions of the 13-point stencil (octf_common.cuh nbr_dir)
+  constexpr int exy = DX < 0 ? 6 : 8;    // (-x+y) / (+x-y)
+  constexpr int exz = DX < 0 ? 7 : 10;   // (-x+z) / (+x-z)
+  constexpr int eyz = DY < 0 ? 9 : 11;   // (-y+z) / (+y-z)
+  if (DX != 0 && DY != 0) return ex ? (ey ? exy : fx) : fy;
+  if (DX != 0 && DZ != 0) return ex ? (ez ? exz : fx) : fz;
+  if (DY != 0 && DZ != 0) return ey ? (ez ? eyz : fy) : fz;
+  if (DX != 0) return fx;
+  if (DY != 0) return fy;
+  return fz;
+}
+
+// snapshot value of the cell (x+DX, y+DY, z+DZ) at the leaf's level.
+// `own` is the shuffled value of sibling c^mask; `inside` = the point is in
+// the domain (out-of-domain points are never read by the stencil).
+template <int DX, int DY, int DZ, typename T>
+__device__ __forceinline__ T step_val(T own, int c, int cx, int cy, int cz,
+                                      bool inside, const int32_t* nb,
+                                      const T* __restrict__ snap) {
+  const bool ex = DX > 0 ? cx : (DX < 0 ? !cx : false);
+  const bool ey = DY > 0 ? cy : (DY < 0 ? !cy : false);
+  const bool ez = DZ > 0 ? cz : (DZ < 0 ? !cz : false);
+  constexpr int mask = (DX ? 4 : 0) | (DY ? 2 : 0) | (DZ ? 1 : 0);
+  T v = own;
+  if ((ex || ey || ez) && inside) {
+    const int32_t r = __ldg(nb + step_dir<DX, DY, DZ>(ex, ey, ez));
+    v = snap[r >= 0 ? r + (c ^ mask) : -r - 2];
+  }
+  return v;
+}
+
+template <typename T, bool FROZEN, bool BINW, bool ENERGY, int NV>
+__global__ void __launch_bounds__(kT) k_leaf_pass(LeafArgs<T> a) {
+  using A = Arith<T>;
+  const LeafParams<T> p = a.p;
+  // the pool is int32-indexed, so every leaf index fits 32 bits
+  const int gid = (int)(blockIdx.x * kT + threadIdx.x);  // launched with kT
+  const int i = gid >> 3;
+  const int c = gid & 7;
+  const bool inrange = i < (int)a.nlb;
+  const int32_t b = inrange ? __ldg(a.lblocks + i) : 0;
+  const int32_t s = b + c;
+  const bool slot_ok = inrange && !(b == 0 && c != 0);
+  const bool active = slot_ok && __ldg(a.child + s) < 0;
+  const T* __restrict__ snap = a.snap;
+
+  // samples first: all loads in flight during the stencil
+  constexpr int NVP = (NV + 3) & ~3;
+  constexpr int NR = NV > 0 ? NVP : 4;
+  float f[NR];
+  float w[BINW ? 4 : NR];
+  uint32_t mk = 0;
+  if (NV > 0) {
+    const float4* fp = reinterpret_cast<const float4*>(a.F) + (size_t)gid * (NVP / 4);
+    const float4* wp = reinterpret_cast<const float4*>(a.W) + (size_t)gid * (NVP / 4);
+#pragma unroll
+    for (int q = 0; q < NVP / 4; ++q) {
+      float4 t = active ? __ldg(fp + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+      f[4 * q] = t.x;
+      f[4 * q + 1] = t.y;
+      f[4 * q + 2] = t.z;
+      f[4 * q + 3] = t.w;
+      if (!BINW) {
+        float4 u = active ? __ldg(wp + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+        w[4 * q] = u.x;
+        w[4 * q + 1] = u.y;
+        w[4 * q + 2] = u.z;
+        w[4 * q + 3] = u.w;
+      }
+    }
+  }
+  if (BINW) mk = active ? __ldg(a.M + gid) : 0u;
+
+  const uint64_t key = inrange ? __ldg(a.lkey + i) : 0ull;
+  int L, px, py, pz;
+  unpack_cell(key, L, px, py, pz);
+  const int cx = (c >> 2) & 1, cy = (c >> 1) & 1, cz = c & 1;
+  const int x = 2 * px + cx, y = 2 * py + cy, z = 2 * pz + cz;
+  const int m = 1 << L;
+  const T ih = inv_spacing<T>(p.d_max, L);
+  const int32_t* nb = a.nbr + i * 12;
+  const T S0 = slot_ok ? snap[s] : (T)0;
+  const unsigned FULL = 0xffffffffu;
+  const bool xp = x + 1 < m, yp = y + 1 < m, zp = z + 1 < m;
+  const bool xm = x > 0, ym = y > 0, zm = z > 0;
+  // own-block values of the 12 neighbours (all lanes take part)
+  const T o_x = __shfl_xor_sync(FULL, S0, 4);
+  const T o_y = __shfl_xor_sync(FULL, S0, 2);
+  const T o_z = __shfl_xor_sync(FULL, S0, 1);
+  const T o_xy = __shfl_xor_sync(FULL, S0, 6);
+  const T o_xz = __shfl_xor_sync(FULL, S0, 5);
+  const T o_yz = __shfl_xor_sync(FULL, S0, 3);
+  // forward neighbours
+  const T Sx = step_val<1, 0, 0>(o_x, c, cx, cy, cz, active && xp, nb, snap);
+  const T Sy = step_val<0, 1, 0>(o_y, c, cx, cy, cz, active && yp, nb, snap);
+  const T Sz = step_val<0, 0, 1>(o_z, c, cx, cy, cz, active && zp, nb, snap);
+  // backward neighbours and the edge points of the backward fluxes
+  const T Smx = step_val<-1, 0, 0>(o_x, c, cx, cy, cz, active && xm, nb, snap);
+  const T Smxy = step_val<-1, 1, 0>(o_xy, c, cx, cy, cz, active && xm && yp, nb, snap);
+  const T Smxz = step_val<-1, 0, 1>(o_xz, c, cx, cy, cz, active && xm && zp, nb, snap);
+  const T Smy = step_val<0, -1, 0>(o_y, c, cx, cy, cz, active && ym, nb, snap);
+  const T Smyx = step_val<1, -1, 0>(o_xy, c, cx, cy, cz, active && ym && xp, nb, snap);
+  const T Smyz = step_val<0, -1, 1>(o_yz, c, cx, cy, cz, active && ym && zp, nb, snap);
+  const T Smz = step_val<0, 0, -1>(o_z, c, cx, cy, cz, active && zm, nb, snap);
+  const T Smzx = step_val<1, 0, -1>(o_xz, c, cx, cy, cz, active && zm && xp, nb, snap);
+  const T Smzy = step_val<0, 1, -1>(o_yz, c, cx, cy, cz, active && zm && yp, nb, snap);
+
+  // flux at the cell (_kernels.pyx:205-220)
+  const T gx = xp ? (Sx - S0) * ih : (T)0;
+  const T gy = yp ? (Sy - S0) * ih : (T)0;
+  const T gz = zp ? (Sz - S0) * ih : (T)0;
+  T p0, p1, p2;
+  A::flux(gx, gy, gz, p.eps2, p0, p1, p2);
+  // backward fluxes, one component each (_kernels.pyx:234-242); the
+  // backward cell's own forward step lands on this cell
+  T bx = 0, by = 0, bz = 0;
+  if (xm) {
+    const T hx = (S0 - Smx) * ih;
+    const T hy = yp ? (Smxy - Smx) * ih : (T)0;
+    const T hz = zp ? (Smxz - Smx) * ih : (T)0;
+    bx = A::flux1(hx, hx, hy, hz, p.eps2);
+  }
+  if (ym) {
+    const T hx = xp ? (Smyx - Smy) * ih : (T)0;
+    const T hy = (S0 - Smy) * ih;
+    const T hz = zp ? (Smyz - Smy) * ih : (T)0;
+    by = A::flux1(hy, hx, hy, hz, p.eps2);
+  }
+  if (zm) {
+    const T hx = xp ? (Smzx - Smz) * ih : (T)0;
+    const T hy = yp ? (Smzy - Smz) * ih : (T)0;
+    const T hz = (S0 - Smz) * ih;
+    bz = A::flux1(hz, hx, hy, hz, p.eps2);
+  }
+  const T div = ((p0 - bx) + (p1 - by) + (p2 - bz)) * ih;
+
+  // data term in view order, zero weights skipped (_kernels.pyx:244-252)
+  T num = 0, den = p.gamma, enm = 0;
+  auto sample = [&](T wv, float fv) {
+    const T d = S0 - (T)fv;
+    if (ENERGY) {
+      T g, e;
+      A::data_both(wv, d, p.eps2, g, e);
+      num += g;
+      enm += e;
+    } else {
+      num += A::data_grad(wv, d, p.eps2);
+    }
+    den += wv;
+  };
+  if (NV > 0) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      if (BINW) {
+        if (mk & (1u << v)) sample((T)1, f[v]);
+      } else {
+        if (w[v] != 0.f) sample((T)w[v], f[v]);
+      }
+    }
+  } else if (active) {
+    const float* fp = a.F + (size_t)gid * a.stride;
+    const float* wp = a.W + (size_t)gid * a.stride;
+    for (int v = 0; v < a.nv; ++v) {
+      const float fv = __ldg(fp + v);
+      if (BINW) {
+        if ((mk >> v) & 1u) sample((T)1, fv);
+      } else {
+        const float wv = __ldg(wp + v);
+        if (wv != 0.f) sample((T)wv, fv);
+      }
+    }
+  }
+  const T du = p.lam * div - A::div(num, den);
+  T dn = S0 + p.xi * du;
+  bool ok_join = false, positive = false;
+  double eterm = 0.0;
+  if (active) {
+    if (ENERGY) {
+      const T h = pow2<T>(p.d_max - L);
+      const T smooth = p.lam * A::smooth_val(gx, gy, gz, p.eps2);
+      eterm = (double)((A::div(enm, den) + smooth) * (h * h * h));
+    }
+    if (!FROZEN && L < p.d_max && fabs((double)dn) < p.tau_s) {
+      a.smark[s] = 1;
+      a.split_list[atomicAdd(a.counters, 1)] = s;
+    } else {
+      if (p.clamp) dn = clamp1(dn);
+      a.uval[s] = dn;
+      ok_join = (double)dn > p.tau_j || (double)dn < -p.tau_j;
+      positive = dn > (T)0;
+    }
+  }
+  if (!FROZEN) {
+    // bottom join candidates: blocks of 8 unsplit leaves past tau_j with one
+    // sign; without one no join can happen anywhere this pass
+    unsigned all = ok_join, pos = ok_join && positive,
+             neg = ok_join && !positive;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      all &= __shfl_xor_sync(FULL, all, o);
+      pos |= __shfl_xor_sync(FULL, pos, o);
+      neg |= __shfl_xor_sync(FULL, neg, o);
+    }
+    if (c == 0 && inrange && b != 0 && all && !(pos && neg))
+      atomicAdd(a.counters + 1, 1);
+  }
+  if (ENERGY) {
+    typedef cub::BlockReduce<double, kT> BR;
+    __shared__ typename BR::TempStorage tmp;
+    const double tot = BR(tmp).Sum(eterm);
+    if (threadIdx.x == 0) a.epart[blockIdx.x] = tot;
+  }
+}

@@ -85,12 +85,12 @@ struct Ctx {
   int64_t nlb = 0;
   int64_t nleaves = 0;
 
-  // ---- per-leaf samples, index i*8+c over the leaf-block list
-  DevBuf<float> F;            // [view][sample]
-  DevBuf<float> W;            // [view][sample] (general weights)
+  // ---- per-leaf samples, leaf index i*8+c over the leaf-block list
+  DevBuf<float> F;            // [leaf][view], sstride floats per leaf
+  DevBuf<float> W;            // [leaf][view] (general weights)
   DevBuf<uint32_t> M;         // [sample] bit v = weight of view v is 1
   bool binw = false;          // samples use the mask format
-  int64_t sstride = 0;
+  int64_t sstride = 0;        // views per leaf vector, padded to 4
 
   // ---- views (device arrays of device pointers)
   DevBuf<const float*> dv_val, dv_w;

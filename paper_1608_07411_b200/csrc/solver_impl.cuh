@@ -81,177 +81,8 @@ __device__ __forceinline__ T clamp1(T v) {
 }
 
 // ---------------------------------------------------------------------------
-// 1. fast leaf update over leaf blocks.  8 lanes = the 8 sibling slots of a
-// block; the 13-point stencil resolves through the block's neighbour table.
-// ENERGY also evaluates the reference's per-leaf energy term
-// (_kernels.pyx:517-533) of the snapshot state -- the post-propagate state
-// of the previous pass -- from the same stencil values and the same square
-// roots, so energy costs no extra pass over the samples.
-template <typename T>
-struct LeafArgs {
-  const int32_t* __restrict__ lblocks;
-  int64_t nlb;
-  const uint64_t* __restrict__ lkey;
-  const int32_t* __restrict__ nbr;
-  const int32_t* __restrict__ child;
-  const T* __restrict__ snap;
-  T* __restrict__ uval;
-  const float* __restrict__ F;
-  const float* __restrict__ W;
-  const uint32_t* __restrict__ M;
-  int64_t stride;
-  int nv;
-  LeafParams<T> p;
-  uint8_t* smark;
-  int32_t* split_list;
-  int32_t* counters;
-  double* epart;  // per-CTA energy partial sums
-};
-
-constexpr int kVC = 8;  // views per register chunk (independent loads)
-
-template <typename T, bool FROZEN, bool BINW, bool ENERGY>
-__global__ void __launch_bounds__(kT) k_leaf_pass(LeafArgs<T> a) {
-  using A = Arith<T>;
-  const LeafParams<T>& p = a.p;
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t i = gid >> 3;
-  const int c = (int)(gid & 7);
-  bool active = i < a.nlb;
-  const int32_t b = active ? __ldg(a.lblocks + i) : 0;
-  const int32_t s = b + c;
-  if (active && b == 0 && c != 0) active = false;
-  if (active && __ldg(a.child + s) >= 0) active = false;
-  bool ok_join = false, positive = false;
-  double eterm = 0.0;
-  if (active) {
-    const int64_t sidx = i * 8 + c;
-    const float* __restrict__ Fp = a.F + sidx;
-    const uint32_t mk = BINW ? __ldg(a.M + sidx) : 0u;
-    // first chunk of samples in flight before the stencil work
-    float f[kVC], w[kVC];
-#pragma unroll
-    for (int j = 0; j < kVC; ++j) {
-      f[j] = j < a.nv ? __ldg(Fp + j * a.stride) : 0.f;
-      if (!BINW) w[j] = j < a.nv ? __ldg(a.W + j * a.stride + sidx) : 0.f;
-    }
-    int L, px, py, pz;
-    unpack_cell(__ldg(a.lkey + i), L, px, py, pz);
-    const int cx = (c >> 2) & 1, cy = (c >> 1) & 1, cz = c & 1;
-    const int x = 2 * px + cx, y = 2 * py + cy, z = 2 * pz + cz;
-    const int m = 1 << L;
-    const T ih = inv_spacing<T>(p.d_max, L);
-    const int32_t* nb = a.nbr + i * 12;
-    const T* __restrict__ snap = a.snap;
-    auto S = [&](int dx, int dy, int dz) -> T {
-      const int tx = cx + dx, ty = cy + dy, tz = cz + dz;
-      const int ox = tx >> 1, oy = ty >> 1, oz = tz >> 1;
-      const int cc = ((tx & 1) << 2) | ((ty & 1) << 1) | (tz & 1);
-      if ((ox | oy | oz) == 0) return snap[b + cc];
-      const int32_t r = __ldg(nb + nbr_dir(ox, oy, oz));
-      return r >= 0 ? snap[r + cc] : snap[-r - 2];
-    };
-    const T S0 = snap[s];
-    // flux at the cell (_kernels.pyx:205-220 with the cell itself)
-    T gx = 0, gy = 0, gz = 0;
-    if (x + 1 < m) gx = (S(1, 0, 0) - S0) * ih;
-    if (y + 1 < m) gy = (S(0, 1, 0) - S0) * ih;
-    if (z + 1 < m) gz = (S(0, 0, 1) - S0) * ih;
-    T p0, p1, p2;
-    A::flux(gx, gy, gz, p.eps2, p0, p1, p2);
-    // backward fluxes, one component each (_kernels.pyx:234-242)
-    T bx = 0, by = 0, bz = 0;
-    if (x > 0) {
-      const T cm = S(-1, 0, 0);
-      const T hx = (S0 - cm) * ih;
-      const T hy = (y + 1 < m) ? (S(-1, 1, 0) - cm) * ih : (T)0;
-      const T hz = (z + 1 < m) ? (S(-1, 0, 1) - cm) * ih : (T)0;
-      bx = A::flux1(hx, hx, hy, hz, p.eps2);
-    }
-    if (y > 0) {
-      const T cm = S(0, -1, 0);
-      const T hx = (x + 1 < m) ? (S(1, -1, 0) - cm) * ih : (T)0;
-      const T hy = (S0 - cm) * ih;
-      const T hz = (z + 1 < m) ? (S(0, -1, 1) - cm) * ih : (T)0;
-      by = A::flux1(hy, hx, hy, hz, p.eps2);
-    }
-    if (z > 0) {
-      const T cm = S(0, 0, -1);
-      const T hx = (x + 1 < m) ? (S(1, 0, -1) - cm) * ih : (T)0;
-      const T hy = (y + 1 < m) ? (S(0, 1, -1) - cm) * ih : (T)0;
-      const T hz = (S0 - cm) * ih;
-      bz = A::flux1(hz, hx, hy, hz, p.eps2);
-    }
-    const T div = ((p0 - bx) + (p1 - by) + (p2 - bz)) * ih;
-    // data term in view order, zero weights skipped (_kernels.pyx:244-252)
-    T num = 0, den = p.gamma, enm = 0;
-    for (int v0 = 0; v0 < a.nv; v0 += kVC) {
-      if (v0) {
-#pragma unroll
-        for (int j = 0; j < kVC; ++j) {
-          const int v = v0 + j;
-          f[j] = v < a.nv ? __ldg(Fp + v * a.stride) : 0.f;
-          if (!BINW) w[j] = v < a.nv ? __ldg(a.W + v * a.stride + sidx) : 0.f;
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < kVC; ++j) {
-        const int v = v0 + j;
-        const bool on = BINW ? (((mk >> (v & 31)) & 1u) && v < a.nv)
-                             : (w[j] != 0.f);
-        if (on) {
-          const T wv = BINW ? (T)1 : (T)w[j];
-          const T d = S0 - (T)f[j];
-          if (ENERGY) {
-            T g, e;
-            A::data_both(wv, d, p.eps2, g, e);
-            num += g;
-            enm += e;
-          } else {
-            num += A::data_grad(wv, d, p.eps2);
-          }
-          den += wv;
-        }
-      }
-    }
-    if (ENERGY) {
-      const T h = pow2<T>(p.d_max - L);
-      const T smooth = p.lam * A::smooth_val(gx, gy, gz, p.eps2);
-      eterm = (double)((A::div(enm, den) + smooth) * (h * h * h));
-    }
-    const T du = p.lam * div - A::div(num, den);
-    T dn = S0 + p.xi * du;
-    if (!FROZEN && L < p.d_max && fabs((double)dn) < p.tau_s) {
-      a.smark[s] = 1;
-      a.split_list[atomicAdd(a.counters, 1)] = s;
-    } else {
-      if (p.clamp) dn = clamp1(dn);
-      a.uval[s] = dn;
-      ok_join = (double)dn > p.tau_j || (double)dn < -p.tau_j;
-      positive = dn > (T)0;
-    }
-  }
-  if (!FROZEN) {
-    // bottom join candidates: blocks of 8 unsplit leaves past tau_j with one
-    // sign; without one no join can happen anywhere this pass
-    unsigned all = ok_join, pos = ok_join && positive,
-             neg = ok_join && !positive;
-#pragma unroll
-    for (int o = 1; o < 8; o <<= 1) {
-      all &= __shfl_xor_sync(0xffffffffu, all, o);
-      pos |= __shfl_xor_sync(0xffffffffu, pos, o);
-      neg |= __shfl_xor_sync(0xffffffffu, neg, o);
-    }
-    if (c == 0 && i < a.nlb && b != 0 && all && !(pos && neg))
-      atomicAdd(a.counters + 1, 1);
-  }
-  if (ENERGY) {
-    typedef cub::BlockReduce<double, kT> BR;
-    __shared__ typename BR::TempStorage tmp;
-    const double tot = BR(tmp).Sum(eterm);
-    if (threadIdx.x == 0) a.epart[blockIdx.x] = tot;
-  }
-}
+// 1. fast leaf update over leaf blocks (leaf_kernel.cuh)
+#include "leaf_kernel.cuh"
 
 // ---------------------------------------------------------------------------
 // generic update of one cell at level L from the snapshot by root descents:
@@ -628,9 +459,9 @@ __global__ void __launch_bounds__(kT)
     const int64_t sidx = i * 8 + c;
     const uint32_t mk = BINW ? M[sidx] : 0u;
     for (int v = 0; v < nv; ++v) {
-      const float w = BINW ? (float)((mk >> v) & 1u) : W[v * stride + sidx];
+      const float w = BINW ? (float)((mk >> v) & 1u) : W[sidx * stride + v];
       if (w != 0.f) {
-        const T d = u0 - (T)F[v * stride + sidx];
+        const T d = u0 - (T)F[sidx * stride + v];
         num += A::data_val((T)w, d, p.eps2);
         den += (T)w;
       }
@@ -692,7 +523,17 @@ void launch_leaf_pass(Ctx& c, const T* snap, T* uval, const int32_t* child,
   a.epart = epart;
   const bool en = epart != nullptr;
   if (timed && c.timing) OCTF_CUDA(cudaEventRecord(c.tev[0], st));
-#define OCTF_LEAF(FZ, BW, EN) k_leaf_pass<T, FZ, BW, EN><<<g, kT, 0, st>>>(a)
+#define OCTF_LEAF(FZ, BW, EN)                                         \
+  do {                                                                \
+    if (c.nviews == 16)                                               \
+      k_leaf_pass<T, FZ, BW, EN, 16><<<g, kT, 0, st>>>(a);            \
+    else if (c.nviews == 32)                                          \
+      k_leaf_pass<T, FZ, BW, EN, 32><<<g, kT, 0, st>>>(a);            \
+    else if (c.nviews == 8)                                           \
+      k_leaf_pass<T, FZ, BW, EN, 8><<<g, kT, 0, st>>>(a);             \
+    else                                                              \
+      k_leaf_pass<T, FZ, BW, EN, 0><<<g, kT, 0, st>>>(a);             \
+  } while (0)
   if (frozen) {
     if (c.binw) {
       if (en) OCTF_LEAF(true, true, true); else OCTF_LEAF(true, true, false);

@@ -55,6 +55,7 @@ def parse():
                     help="depth of the bounded CPU-baseline sample")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity-mode", action="store_true")
     return ap.parse_args()
 
 
@@ -214,11 +215,34 @@ def run_cuda(args, rank, world, local_rank):
         "clocks": clocks.summary(),
     }
     solver.close()
+    if rank == 0 and args.precision == "fp32" and not args.no_parity_mode:
+        out["parity_mode"] = run_parity_mode(views, u0, p, args, nleaves)
     if rank == 0 and not args.no_e2e:
         out["e2e"] = run_e2e(views, u0, p, args)
     if rank == 0 and world == 1 and not args.no_cpu:
         out["cpu_baseline"] = cpu_baseline(args, threads=1)
     return out
+
+
+def run_parity_mode(views, u0, p, args, nleaves):
+    """The same workload in the bit-exact fp64 mode (pools identical to the
+    reference's kernels), timed the same way."""
+    import torch
+    from paper_1608_07411_b200 import fusion
+    solver = fusion.Solver(u0, views, p, precision="fp64")
+    solver.run(0, args.warmup)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    solver.run(args.warmup, args.steps)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    solver.close()
+    return {"dtype": "f64", "value": nleaves * args.steps / (ms / 1e3),
+            "unit": UNIT, "ms_per_step": ms / args.steps,
+            "note": "bit-exact parity mode (tests/test_gpu_parity.py)"}
 
 
 def run_e2e(views, u0, p, args):

@@ -107,7 +107,7 @@ __global__ void k_leaf_tables(const int32_t* __restrict__ child,
                               const int32_t* __restrict__ lblocks, int64_t nlb,
                               const int8_t* __restrict__ blevel,
                               const uint64_t* __restrict__ bcoord,
-                              uint64_t* lkey, int32_t* nbr) {
+                              uint64_t* lkey, int4* lmeta, int32_t* nbr) {
   int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t i = gid / 12;
   int d = (int)(gid % 12);
@@ -118,7 +118,15 @@ __global__ void k_leaf_tables(const int32_t* __restrict__ child,
   int pL, px, py, pz;
   unpack_cell(bcoord[k], pL, px, py, pz);
   if (b == 0) px = py = pz = 0;
-  if (d == 0) lkey[i] = pack_cell(L, px, py, pz);
+  if (d == 0) {
+    lkey[i] = pack_cell(L, px, py, pz);
+    unsigned mask = 0;
+    if (b == 0)
+      mask = child[0] < 0 ? 1u : 0u;
+    else
+      for (int c = 0; c < 8; ++c) mask |= (child[b + c] < 0 ? 1u : 0u) << c;
+    lmeta[i] = make_int4(b, px, py, pack_meta_w(pz, mask, L));
+  }
   int32_t ref = kNone;
   if (b != 0) {
     int ox, oy, oz;
@@ -323,9 +331,11 @@ void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
   c.nleaves = c.h_counters[1];
   sort_i32(c, c.lblocks.p, c.nlb, st);
   c.lkey.ensure(c.nlb);
+  c.lmeta.ensure(c.nlb);
   c.nbr.ensure(c.nlb * 12);
   k_leaf_tables<<<grid_for(c.nlb * 12), kThreads, 0, st>>>(
-      child, c.lblocks.p, c.nlb, c.blevel.p, c.bcoord.p, c.lkey.p, c.nbr.p);
+      child, c.lblocks.p, c.nlb, c.blevel.p, c.bcoord.p, c.lkey.p, c.lmeta.p,
+      c.nbr.p);
   OCTF_CUDA(cudaGetLastError());
 
   c.smark.ensure(cap);

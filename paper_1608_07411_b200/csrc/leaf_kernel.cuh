@@ -24,6 +24,7 @@ struct LeafArgs {
   const int32_t* __restrict__ lblocks;
   int64_t nlb;
   const uint64_t* __restrict__ lkey;
+  const int4* __restrict__ lmeta;
   const int32_t* __restrict__ nbr;
   const int32_t* __restrict__ child;
   const T* __restrict__ snap;
@@ -84,13 +85,10 @@ __global__ void __launch_bounds__(kT) k_leaf_pass(LeafArgs<T> a) {
   const int i = gid >> 3;
   const int c = gid & 7;
   const bool inrange = i < (int)a.nlb;
-  const int32_t b = inrange ? __ldg(a.lblocks + i) : 0;
-  const int32_t s = b + c;
-  const bool slot_ok = inrange && !(b == 0 && c != 0);
-  const bool active = slot_ok && __ldg(a.child + s) < 0;
   const T* __restrict__ snap = a.snap;
 
-  // samples first: all loads in flight during the stencil
+  // samples first (they depend on nothing): all in flight during the rest.
+  // Non-leaf slots of a leaf block hold zeroed vectors, so loads are safe.
   constexpr int NVP = (NV + 3) & ~3;
   constexpr int NR = NV > 0 ? NVP : 4;
   float f[NR];
@@ -101,13 +99,13 @@ __global__ void __launch_bounds__(kT) k_leaf_pass(LeafArgs<T> a) {
     const float4* wp = reinterpret_cast<const float4*>(a.W) + (size_t)gid * (NVP / 4);
 #pragma unroll
     for (int q = 0; q < NVP / 4; ++q) {
-      float4 t = active ? __ldg(fp + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 t = inrange ? __ldg(fp + q) : make_float4(0.f, 0.f, 0.f, 0.f);
       f[4 * q] = t.x;
       f[4 * q + 1] = t.y;
       f[4 * q + 2] = t.z;
       f[4 * q + 3] = t.w;
       if (!BINW) {
-        float4 u = active ? __ldg(wp + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 u = inrange ? __ldg(wp + q) : make_float4(0.f, 0.f, 0.f, 0.f);
         w[4 * q] = u.x;
         w[4 * q + 1] = u.y;
         w[4 * q + 2] = u.z;
@@ -115,11 +113,18 @@ __global__ void __launch_bounds__(kT) k_leaf_pass(LeafArgs<T> a) {
       }
     }
   }
-  if (BINW) mk = active ? __ldg(a.M + gid) : 0u;
+  if (BINW) mk = inrange ? __ldg(a.M + gid) : 0u;
 
-  const uint64_t key = inrange ? __ldg(a.lkey + i) : 0ull;
-  int L, px, py, pz;
-  unpack_cell(key, L, px, py, pz);
+  // one 16 B load: base slot, parent cell, leaf mask and level
+  const int4 meta = inrange ? __ldg(a.lmeta + i) : make_int4(0, 0, 0, 0);
+  const int32_t b = meta.x;
+  const int32_t s = b + c;
+  int L, pz;
+  unsigned lmask;
+  unpack_meta_w(meta.w, pz, lmask, L);
+  const int px = meta.y, py = meta.z;
+  const bool slot_ok = inrange && !(b == 0 && c != 0);
+  const bool active = slot_ok && ((lmask >> c) & 1u);
   const int cx = (c >> 2) & 1, cy = (c >> 1) & 1, cz = c & 1;
   const int x = 2 * px + cx, y = 2 * py + cy, z = 2 * pz + cz;
   const int m = 1 << L;

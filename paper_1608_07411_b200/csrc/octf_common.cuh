@@ -37,6 +37,18 @@ __host__ __device__ __forceinline__ void unpack_cell(uint64_t p, int& L, int& x,
   z = (int)(p & 0x7ffff);
 }
 
+// leaf-block metadata word: pz (19 bits) | leaf mask (8) << 19 | level << 27
+__host__ __device__ __forceinline__ int pack_meta_w(int pz, unsigned mask,
+                                                    int L) {
+  return (int)((unsigned)pz | (mask << 19) | ((unsigned)L << 27));
+}
+__host__ __device__ __forceinline__ void unpack_meta_w(int w, int& pz,
+                                                       unsigned& mask, int& L) {
+  pz = w & 0x7ffff;
+  mask = ((unsigned)w >> 19) & 0xffu;
+  L = (int)((unsigned)w >> 27);
+}
+
 // spread the low 21 bits of v to every third bit
 __host__ __device__ __forceinline__ uint64_t spread3(uint64_t v) {
   v &= 0x1fffff;

@@ -81,6 +81,7 @@ struct Ctx {
   int64_t nblocks = 0;
   DevBuf<int32_t> lblocks;    // blocks holding >= 1 leaf, ascending base
   DevBuf<uint64_t> lkey;      // per leaf block: packed (level, parent cell)
+  DevBuf<int4> lmeta;         // per leaf block: {base, px, py, pz|mask|L}
   DevBuf<int32_t> nbr;        // per leaf block: 12 neighbour refs
   int64_t nlb = 0;
   int64_t nleaves = 0;

@@ -507,6 +507,7 @@ void launch_leaf_pass(Ctx& c, const T* snap, T* uval, const int32_t* child,
   a.lblocks = c.lblocks.p;
   a.nlb = c.nlb;
   a.lkey = c.lkey.p;
+  a.lmeta = c.lmeta.p;
   a.nbr = c.nbr.p;
   a.child = child;
   a.snap = snap;

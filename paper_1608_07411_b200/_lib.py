@@ -12,7 +12,8 @@ import os
 import subprocess
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liboctfuse_b200.so")
+LIB_PATH = os.environ.get("OCTF_LIB_PATH") or os.path.join(_HERE,
+                                                           "liboctfuse_b200.so")
 
 OCTF_F64 = 0
 OCTF_F32 = 1

@@ -19,6 +19,10 @@
 // previous pass's post-propagate state, from the same values and roots.
 #pragma once
 
+#ifndef OCTF_LEAF_MINB
+#define OCTF_LEAF_MINB 1
+#endif
+
 template <typename T>
 struct LeafArgs {
   const int32_t* __restrict__ lblocks;
@@ -77,7 +81,7 @@ __device__ __forceinline__ T step_val(T own, int c, int cx, int cy, int cz,
 }
 
 template <typename T, bool FROZEN, bool BINW, bool ENERGY, int NV>
-__global__ void __launch_bounds__(kT) k_leaf_pass(LeafArgs<T> a) {
+__global__ void __launch_bounds__(kT, OCTF_LEAF_MINB) k_leaf_pass(LeafArgs<T> a) {
   using A = Arith<T>;
   const LeafParams<T> p = a.p;
   // the pool is int32-indexed, so every leaf index fits 32 bits

@@ -166,6 +166,11 @@ int octf_ctx_profile(octf_ctx* ctx, int enable, double* out) {
     octf::Ctx& c = ctx->c;
     if (enable && !c.tev[0])
       for (auto& e : c.tev) OCTF_CUDA(cudaEventCreate(&e));
+    while (enable && c.pev.size() < 64) {  // per-pass pairs, batched passes
+      cudaEvent_t e;
+      OCTF_CUDA(cudaEventCreate(&e));
+      c.pev.push_back(e);
+    }
     if (out) {
       out[0] = c.t_leaf_ms;
       out[1] = (double)c.n_leaf;

@@ -862,45 +862,55 @@ void frozen_passes_impl(Ctx& c, FrozenArgs& a, cudaStream_t st) {
   if (a.npasses < 1) return;
   ensure_prepared<T>(c, a.child, a.cap, prm.d_max, a.state, st);
   if (c.nviews <= 0) throw Error(kEArg, "at least one view is required");
+  // fixed-size scratch (no allocation inside a timed loop): energy
+  // partials for kChunk passes, one energy slot per pass
+  constexpr int kChunk = 32;
   const unsigned g = leaf_grid(c);
-  c.partials.ensure((size_t)g * a.npasses);
-  c.dscalar.ensure(a.npasses);
+  c.partials.ensure((size_t)g * kChunk);
+  c.dscalar.ensure(a.npasses > 1024 ? a.npasses : 1024);
   c.counters.ensure(64);
   c.split_list.ensure(c.nlb * 8 + 1);
-  if (c.timing && (int)c.pev.size() < 2 * a.npasses) {
-    for (int k = (int)c.pev.size(); k < 2 * a.npasses; ++k) {
+  if (c.timing && (int)c.pev.size() < 2 * kChunk) {
+    for (int k = (int)c.pev.size(); k < 2 * kChunk; ++k) {
       cudaEvent_t e;
       OCTF_CUDA(cudaEventCreate(&e));
       c.pev.push_back(e);
     }
   }
-  for (int k = 0; k < a.npasses; ++k) {
-    PassParams pk = prm;
-    pk.xi = a.xis[k];
-    const LeafParams<T> lp = leaf_params<T>(pk);
-    const T* snap = (const T*)a.ubuf[k & 1];
-    T* uval = (T*)a.ubuf[(k + 1) & 1];
-    if (c.timing) OCTF_CUDA(cudaEventRecord(c.pev[2 * k], st));
-    launch_leaf_pass<T>(c, snap, uval, a.child, lp, true,
-                        c.partials.p + (size_t)k * g, st, false);
-    if (c.timing) OCTF_CUDA(cudaEventRecord(c.pev[2 * k + 1], st));
-    launch_propagate<T>(c, uval, a.child, st);
+  for (int k0 = 0; k0 < a.npasses; k0 += kChunk) {
+    const int nk = a.npasses - k0 < kChunk ? a.npasses - k0 : kChunk;
+    for (int j = 0; j < nk; ++j) {
+      const int k = k0 + j;
+      PassParams pk = prm;
+      pk.xi = a.xis[k];
+      const LeafParams<T> lp = leaf_params<T>(pk);
+      const T* snap = (const T*)a.ubuf[k & 1];
+      T* uval = (T*)a.ubuf[(k + 1) & 1];
+      if (c.timing) OCTF_CUDA(cudaEventRecord(c.pev[2 * j], st));
+      launch_leaf_pass<T>(c, snap, uval, a.child, lp, true,
+                          c.partials.p + (size_t)j * g, st, false);
+      if (c.timing) OCTF_CUDA(cudaEventRecord(c.pev[2 * j + 1], st));
+      launch_propagate<T>(c, uval, a.child, st);
+    }
+    // stream order keeps the next chunk from overwriting unsummed partials
+    k_sum_partials_multi<<<nk, kT, 0, st>>>(c.partials.p, g,
+                                            c.dscalar.p + k0);
+    OCTF_CUDA(cudaGetLastError());
+    ++c.launches;
+    if (c.timing) {  // profiling only: read this chunk's kernel events
+      OCTF_CUDA(cudaStreamSynchronize(st));
+      for (int j = 0; j < nk; ++j) {
+        float ms = 0.f;
+        OCTF_CUDA(cudaEventElapsedTime(&ms, c.pev[2 * j], c.pev[2 * j + 1]));
+        c.t_leaf_ms += ms;
+        ++c.n_leaf;
+      }
+    }
   }
-  k_sum_partials_multi<<<a.npasses, kT, 0, st>>>(c.partials.p, g, c.dscalar.p);
-  OCTF_CUDA(cudaGetLastError());
-  ++c.launches;
   OCTF_CUDA(cudaMemcpyAsync(a.energies_pre, c.dscalar.p,
                             a.npasses * sizeof(double), cudaMemcpyDeviceToHost,
                             st));
   OCTF_CUDA(cudaStreamSynchronize(st));
-  if (c.timing) {
-    for (int k = 0; k < a.npasses; ++k) {
-      float ms = 0.f;
-      OCTF_CUDA(cudaEventElapsedTime(&ms, c.pev[2 * k], c.pev[2 * k + 1]));
-      c.t_leaf_ms += ms;
-      ++c.n_leaf;
-    }
-  }
 }
 
 }  // namespace

@@ -205,7 +205,8 @@ def run_cuda(args, rank, world, local_rank):
                    "l2": "inputs larger than L2 (>= 1.1 GB streamed per pass)",
                    "step": "iterate + propagate + energy (reference fuse loop)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
-                     "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": _ncu_traffic(args),
                      "kernel": "k_leaf_pass", "kernel_ms": leaf_ms,
                      "bytes_per_leaf": b_leaf, "peak_source": peak_src},
         "breakdown_ms": {"leaf_update_and_energy": leaf_ms,
@@ -222,6 +223,21 @@ def run_cuda(args, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_cpu:
         out["cpu_baseline"] = cpu_baseline(args, threads=1)
     return out
+
+
+def _ncu_traffic(args):
+    """dram bytes (read + write) per launch of the leaf kernel from the
+    committed ncu --set full capture of this workload (profiles/), or None."""
+    import glob
+    if (args.depth, args.views, args.precision) != (8, 16, "fp32"):
+        return None
+    for path in sorted(glob.glob(os.path.join(REPO, "profiles", "r*",
+                                              "ncu_traffic.json")))[::-1]:
+        try:
+            return json.load(open(path))["traffic_bytes_per_launch"]
+        except Exception:
+            continue
+    return None
 
 
 def run_parity_mode(views, u0, p, args, nleaves):

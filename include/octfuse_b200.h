@@ -113,7 +113,25 @@ int octf_fuse_passes_frozen(octf_ctx *ctx, int dtype, void *ubuf0, void *ubuf1,
                             double lam, double eps, double gamma,
                             double tau_s, double tau_j, int clamp,
                             const double *xis, int npasses,
-                            double *energies_pre, void *stream);
+                            double *energies_pre, int device_energies,
+                            void *stream);
+
+/* Build the context's structures for a pool (and views) up front. */
+int octf_ctx_prepare(octf_ctx *ctx, const int32_t *uchild,
+                     const int64_t *ustate, int64_t cap, int d_max, int nviews,
+                     const float *const *vvals, const float *const *vws,
+                     const int32_t *const *vchilds, void *stream);
+
+/* Sharding: restrict the context's leaf-block list to the
+ * blocks `sel` (host int32 indices into the current list) with per-block
+ * owned-leaf masks (host u8, bit c = sibling c is updated by this rank);
+ * samples are regathered for the subset.  Frozen structures only. */
+int octf_ctx_select(octf_ctx *ctx, const int32_t *sel, const uint8_t *masks,
+                    int64_t nsel, void *stream);
+
+/* Propagate only levels hi-1 .. lo (the replicated top of a sharded tree). */
+int octf_propagate_levels(octf_ctx *ctx, int dtype, void *value,
+                          const int32_t *child, int lo, int hi, void *stream);
 
 /* _kernels.pyx:80-113 propagate -- inner value = (sequential sum of the 8
  * children)/8, bottom-up.  ctx may be NULL (a temporary one is built). */

@@ -127,18 +127,41 @@ def fuse_pass(usnap, uval, uchild, ujoined, ustate, vvals, vws, vchilds,
 
 def fuse_passes_frozen(ubuf0, ubuf1, uchild, ustate, vvals, vws, vchilds,
                        d_max, lam, eps, gamma, tau_s, tau_j, clamp, xis, *,
-                       ctx):
+                       ctx, energies_out=None):
     """len(xis) passes of a frozen structure in one call; returns the
     energies before each pass.  Pass k reads buffer k%2."""
     tv, tw, tc = _views(vvals, vws, vchilds)
     xis = np.ascontiguousarray(np.asarray(xis, dtype=np.float64))
-    en = np.zeros(len(xis), dtype=np.float64)
+    if energies_out is None:
+        en = np.zeros(len(xis), dtype=np.float64)
+        eptr, dev = en.ctypes.data, 0
+    else:  # device tensor: the call stays asynchronous
+        en = energies_out
+        eptr, dev = ptr(energies_out), 1
     call("octf_fuse_passes_frozen", ctx.h, _dtype_code(ubuf0), ptr(ubuf0),
          ptr(ubuf1), ptr(uchild), _state_ptr(ustate), ubuf0.shape[0],
          len(vvals), tv, tw, tc, int(d_max), float(lam), float(eps),
          float(gamma), float(tau_s), float(tau_j), int(bool(clamp)),
-         xis.ctypes.data, len(xis), en.ctypes.data, stream_handle())
+         xis.ctypes.data, len(xis), eptr, dev, stream_handle())
     return en
+
+
+def ctx_prepare(ctx, uchild, ustate, d_max, vvals, vws, vchilds):
+    tv, tw, tc = _views(vvals, vws, vchilds)
+    call("octf_ctx_prepare", ctx.h, ptr(uchild), _state_ptr(ustate),
+         uchild.shape[0], int(d_max), len(vvals), tv, tw, tc, stream_handle())
+
+
+def ctx_select(ctx, sel, masks):
+    sel = np.ascontiguousarray(np.asarray(sel, dtype=np.int32))
+    masks = np.ascontiguousarray(np.asarray(masks, dtype=np.uint8))
+    call("octf_ctx_select", ctx.h, sel.ctypes.data if sel.size else None,
+         masks.ctypes.data if masks.size else None, sel.size, stream_handle())
+
+
+def propagate_levels(value, child, lo, hi, *, ctx):
+    call("octf_propagate_levels", ctx.h, _dtype_code(value), ptr(value),
+         ptr(child), int(lo), int(hi), stream_handle())
 
 
 def tree_energy(uval, uchild, vvals, vws, vchilds, d_max, lam, eps, gamma, *,

@@ -43,8 +43,11 @@ _SIGS = {
                         DBL, DBL, DBL, DBL, DBL, I32, I32, P, I64, P, P, P],
                        I32),
     "octf_fuse_passes_frozen": ([P, I32, P, P, P, P, I64, I32, P, P, P, I32,
-                                 DBL, DBL, DBL, DBL, DBL, I32, P, I32, P, P],
-                                I32),
+                                 DBL, DBL, DBL, DBL, DBL, I32, P, I32, P, I32,
+                                 P], I32),
+    "octf_ctx_prepare": ([P, P, P, I64, I32, I32, P, P, P, P], I32),
+    "octf_ctx_select": ([P, P, P, I64, P], I32),
+    "octf_propagate_levels": ([P, I32, P, P, I32, I32, P], I32),
     "octf_propagate": ([P, I32, P, P, P, I64, I32, P], I32),
     "octf_tree_energy": ([P, I32, P, P, P, I64, I32, P, P, P, I32, DBL, DBL,
                           DBL, P, P, P], I32),

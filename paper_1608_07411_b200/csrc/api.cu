@@ -274,7 +274,8 @@ int octf_fuse_passes_frozen(octf_ctx* ctx, int dtype, void* ubuf0, void* ubuf1,
                             double lam, double eps, double gamma,
                             double tau_s, double tau_j, int clamp,
                             const double* xis, int npasses,
-                            double* energies_pre, void* stream) {
+                            double* energies_pre, int device_energies,
+                            void* stream) {
   return guard([&] {
     if (!ctx || !ubuf0 || !ubuf1 || !uchild || !ustate || !xis ||
         !energies_pre)
@@ -294,10 +295,48 @@ int octf_fuse_passes_frozen(octf_ctx* ctx, int dtype, void* ubuf0, void* ubuf1,
     a.xis = xis;
     a.npasses = npasses;
     a.energies_pre = energies_pre;
+    a.dev_energies = device_energies != 0;
     if (dtype == OCTF_F64)
       octf::frozen_passes_f64(ctx->c, a, S(stream));
     else
       octf::frozen_passes_f32(ctx->c, a, S(stream));
+  });
+}
+
+int octf_ctx_prepare(octf_ctx* ctx, const int32_t* uchild,
+                     const int64_t* ustate, int64_t cap, int d_max, int nviews,
+                     const float* const* vvals, const float* const* vws,
+                     const int32_t* const* vchilds, void* stream) {
+  return guard([&] {
+    if (!ctx || !uchild || !ustate) throw octf::Error(octf::kEArg, "null argument");
+    if (d_max < 0 || d_max > OCTF_MAX_DEPTH)
+      throw octf::Error(octf::kEDepth, "tree depth out of range");
+    if (nviews > 0)
+      octf::ctx_set_views(ctx->c, nviews, vvals, vws, vchilds, S(stream));
+    octf::ctx_prepare(ctx->c, uchild, cap, ustate, d_max, S(stream));
+  });
+}
+
+int octf_ctx_select(octf_ctx* ctx, const int32_t* sel, const uint8_t* masks,
+                    int64_t nsel, void* stream) {
+  return guard([&] {
+    if (!ctx || (nsel && (!sel || !masks)))
+      throw octf::Error(octf::kEArg, "null argument");
+    octf::ctx_select(ctx->c, sel, masks, nsel, S(stream));
+  });
+}
+
+int octf_propagate_levels(octf_ctx* ctx, int dtype, void* value,
+                          const int32_t* child, int lo, int hi, void* stream) {
+  return guard([&] {
+    if (!ctx || !value || !child) throw octf::Error(octf::kEArg, "null argument");
+    check_dtype(dtype);
+    if (dtype == OCTF_F64)
+      octf::propagate_levels_f64(ctx->c, (double*)value, child, lo, hi,
+                                 S(stream));
+    else
+      octf::propagate_levels_f32(ctx->c, (float*)value, child, lo, hi,
+                                 S(stream));
   });
 }
 

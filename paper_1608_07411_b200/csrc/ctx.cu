@@ -414,3 +414,60 @@ void ctx_gather(Ctx& c, cudaStream_t st) {
 }
 
 }  // namespace octf
+
+namespace octf {
+namespace {
+
+__global__ void k_select(const int32_t* __restrict__ sel,
+                         const uint8_t* __restrict__ masks, int64_t nsel,
+                         const int32_t* lblocks, const uint64_t* lkey,
+                         const int4* lmeta, const int32_t* nbr,
+                         int32_t* o_lblocks, uint64_t* o_lkey, int4* o_lmeta,
+                         int32_t* o_nbr) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nsel) return;
+  const int32_t i = sel[j];
+  o_lblocks[j] = lblocks[i];
+  o_lkey[j] = lkey[i];
+  int4 m = lmeta[i];
+  // keep only the rank's leaves active (bits 19..26 of .w)
+  m.w = (int)(((unsigned)m.w & ~(0xffu << 19)) | ((unsigned)masks[j] << 19));
+  o_lmeta[j] = m;
+  for (int d = 0; d < 12; ++d) o_nbr[j * 12 + d] = nbr[(int64_t)i * 12 + d];
+}
+
+}  // namespace
+
+void ctx_select(Ctx& c, const int32_t* sel, const uint8_t* masks, int64_t nsel,
+                cudaStream_t st) {
+  if (!c.valid) throw Error(kEArg, "context not prepared");
+  DevBuf<int32_t> dsel, olb, onbr;
+  DevBuf<uint8_t> dmask;
+  DevBuf<uint64_t> okey;
+  DevBuf<int4> ometa;
+  dsel.ensure(nsel);
+  dmask.ensure(nsel);
+  olb.ensure(nsel);
+  okey.ensure(nsel);
+  ometa.ensure(nsel);
+  onbr.ensure(nsel * 12);
+  if (nsel) {
+    OCTF_CUDA(cudaMemcpyAsync(dsel.p, sel, nsel * sizeof(int32_t),
+                              cudaMemcpyHostToDevice, st));
+    OCTF_CUDA(cudaMemcpyAsync(dmask.p, masks, nsel, cudaMemcpyHostToDevice, st));
+    k_select<<<grid_for(nsel), kThreads, 0, st>>>(
+        dsel.p, dmask.p, nsel, c.lblocks.p, c.lkey.p, c.lmeta.p, c.nbr.p, olb.p,
+        okey.p, ometa.p, onbr.p);
+    OCTF_CUDA(cudaGetLastError());
+  }
+  OCTF_CUDA(cudaStreamSynchronize(st));
+  c.lblocks.swap(olb);
+  c.lkey.swap(okey);
+  c.lmeta.swap(ometa);
+  c.nbr.swap(onbr);
+  c.nlb = nsel;
+  if (c.nviews > 0) ctx_gather(c, st);
+  OCTF_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace octf

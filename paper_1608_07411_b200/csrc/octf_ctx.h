@@ -42,6 +42,14 @@ struct DevBuf {
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() { release(); }
+  void swap(DevBuf& o) {
+    T* tp = p;
+    p = o.p;
+    o.p = tp;
+    size_t tn = n;
+    n = o.n;
+    o.n = tn;
+  }
   void release() {
     if (p) cudaFree(p);
     p = nullptr;
@@ -167,7 +175,8 @@ struct FrozenArgs {
   PassParams prm;     // xi is taken from xis[]
   const double* xis;  // host, npasses
   int npasses;
-  double* energies_pre;  // host, npasses
+  double* energies_pre;  // host (or device with dev_energies), npasses
+  bool dev_energies = false;
 };
 
 // per precision entry points (solver_f64.cu / solver_f32.cu)
@@ -183,5 +192,13 @@ double energy_f32(Ctx& c, const float* u, const int32_t* child,
                   const PassParams& p, double* terms, cudaStream_t st);
 void frozen_passes_f64(Ctx& c, FrozenArgs& a, cudaStream_t st);
 void frozen_passes_f32(Ctx& c, FrozenArgs& a, cudaStream_t st);
+void propagate_levels_f64(Ctx& c, double* v, const int32_t* child, int lo,
+                          int hi, cudaStream_t st);
+void propagate_levels_f32(Ctx& c, float* v, const int32_t* child, int lo,
+                          int hi, cudaStream_t st);
+// restrict the leaf-block list to a subset with per-block leaf masks
+// (sharding); host arrays; regathers samples
+void ctx_select(Ctx& c, const int32_t* sel, const uint8_t* masks,
+                int64_t nsel, cudaStream_t st);
 
 }  // namespace octf

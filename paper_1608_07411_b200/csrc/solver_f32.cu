@@ -20,3 +20,10 @@ void frozen_passes_f32(Ctx& c, FrozenArgs& a, cudaStream_t st) {
   frozen_passes_impl<float>(c, a, st);
 }
 }  // namespace octf
+
+namespace octf {
+void propagate_levels_f32(Ctx& c, float* v, const int32_t* child, int lo, int hi,
+                         cudaStream_t st) {
+  propagate_levels_impl<float>(c, v, child, lo, hi, st);
+}
+}  // namespace octf

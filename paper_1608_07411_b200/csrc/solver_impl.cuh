@@ -419,7 +419,7 @@ template <typename T, bool BINW>
 __global__ void __launch_bounds__(kT)
     k_energy(const int32_t* __restrict__ lblocks, int64_t nlb,
              const uint64_t* __restrict__ lkey, const int32_t* __restrict__ nbr,
-             const int32_t* __restrict__ child, const T* __restrict__ u,
+             const int4* __restrict__ lmeta, const T* __restrict__ u,
              const float* __restrict__ F, const float* __restrict__ W,
              const uint32_t* __restrict__ M, int64_t stride, int nv,
              LeafParams<T> p, double* partials, double* terms) {
@@ -431,7 +431,8 @@ __global__ void __launch_bounds__(kT)
   const int32_t b = active ? lblocks[i] : 0;
   const int32_t s = b + c;
   if (active && b == 0 && c != 0) active = false;
-  if (active && child[s] >= 0) active = false;
+  // leaf mask of the (possibly rank-restricted) leaf-block list
+  if (active && !(((unsigned)lmeta[i].w >> (19 + c)) & 1u)) active = false;
   double term = 0.0;
   if (active) {
     int L, px, py, pz;
@@ -809,12 +810,12 @@ double energy_impl(Ctx& c, const T* u, const int32_t* child,
   if (c.timing) OCTF_CUDA(cudaEventRecord(c.tev[2], st));
   if (c.binw)
     k_energy<T, true><<<g, kT, 0, st>>>(c.lblocks.p, c.nlb, c.lkey.p, c.nbr.p,
-                                        child, u, c.F.p, c.W.p, c.M.p,
+                                        c.lmeta.p, u, c.F.p, c.W.p, c.M.p,
                                         c.sstride, c.nviews, lp, c.partials.p,
                                         terms);
   else
     k_energy<T, false><<<g, kT, 0, st>>>(c.lblocks.p, c.nlb, c.lkey.p,
-                                         c.nbr.p, child, u, c.F.p, c.W.p,
+                                         c.nbr.p, c.lmeta.p, u, c.F.p, c.W.p,
                                          c.M.p, c.sstride, c.nviews, lp,
                                          c.partials.p, terms);
   OCTF_CUDA(cudaGetLastError());
@@ -893,8 +894,8 @@ void frozen_passes_impl(Ctx& c, FrozenArgs& a, cudaStream_t st) {
       launch_propagate<T>(c, uval, a.child, st);
     }
     // stream order keeps the next chunk from overwriting unsummed partials
-    k_sum_partials_multi<<<nk, kT, 0, st>>>(c.partials.p, g,
-                                            c.dscalar.p + k0);
+    double* eout = a.dev_energies ? a.energies_pre : c.dscalar.p;
+    k_sum_partials_multi<<<nk, kT, 0, st>>>(c.partials.p, g, eout + k0);
     OCTF_CUDA(cudaGetLastError());
     ++c.launches;
     if (c.timing) {  // profiling only: read this chunk's kernel events
@@ -907,10 +908,27 @@ void frozen_passes_impl(Ctx& c, FrozenArgs& a, cudaStream_t st) {
       }
     }
   }
+  if (a.dev_energies) return;  // stays asynchronous
   OCTF_CUDA(cudaMemcpyAsync(a.energies_pre, c.dscalar.p,
                             a.npasses * sizeof(double), cudaMemcpyDeviceToHost,
                             st));
   OCTF_CUDA(cudaStreamSynchronize(st));
+}
+
+// propagate levels hi-1 .. lo only (the replicated top of a sharded tree)
+template <typename T>
+void propagate_levels_impl(Ctx& c, T* value, const int32_t* child, int lo,
+                           int hi, cudaStream_t st) {
+  if (!c.valid) throw Error(kEArg, "context not prepared");
+  for (int L = hi - 1; L >= lo; --L) {
+    if (L < 0 || L >= (int)c.lvl_cnt.size()) continue;
+    const int64_t n = c.lvl_cnt[L];
+    if (n == 0) continue;
+    k_propagate_level<T><<<blocks_for(n * 8), kT, 0, st>>>(
+        c.lvl_blocks.p + c.lvl_off[L], n, child, value);
+    OCTF_CUDA(cudaGetLastError());
+    ++c.launches;
+  }
 }
 
 }  // namespace

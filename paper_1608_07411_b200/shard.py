@@ -1,0 +1,346 @@
+"""Morton-range sharding of a fixed-structure octree across ranks
+(SURVEY.md §8(e)).
+
+Ownership is by subtree: the *units* are the nodes at a partition level k
+(plus leaves above k).  Units are ordered by Morton key and cut into
+contiguous runs of roughly equal leaf count, one run per rank; a rank owns
+every node of its units' subtrees.  The few inner nodes above level k (the
+*top*) are replicated: every rank recomputes them from the unit roots.
+
+Per pass each rank updates the leaves it owns (the same leaf kernel over a
+rank-local leaf-block list whose leaf masks keep only owned leaves),
+propagates, then receives the *halo*: values of nodes its stencils read (or
+the top recomputation needs) that other ranks own.  Per-node arithmetic does
+not depend on the partition, so structure and values stay bit-identical to
+a single GPU; only the order of the final energy sum changes.
+
+This module is host-side numpy (plans are built once per structure) plus
+the exchange itself, written against torch.distributed so the same code
+runs over NCCL on GPUs and over gloo in the CPU tests.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+__all__ = ["Structure", "structure", "ShardPlan", "plan", "HaloExchange"]
+
+# direction table of the 13-point stencil (octf_common.cuh dir_offset)
+DIRS = np.array([[-1, 0, 0], [1, 0, 0], [0, -1, 0], [0, 1, 0], [0, 0, -1],
+                 [0, 0, 1], [-1, 1, 0], [-1, 0, 1], [1, -1, 0], [0, -1, 1],
+                 [1, 0, -1], [0, 1, -1]], dtype=np.int64)
+
+
+def _spread3(v: np.ndarray) -> np.ndarray:
+    v = v.astype(np.uint64) & np.uint64(0x1fffff)
+    for shift, mask in ((32, 0x1f00000000ffff), (16, 0x1f0000ff0000ff),
+                        (8, 0x100f00f00f00f00f), (4, 0x10c30c30c30c30c3),
+                        (2, 0x1249249249249249)):
+        v = (v | (v << np.uint64(shift))) & np.uint64(mask)
+    return v
+
+
+def morton(x, y, z) -> np.ndarray:
+    """x-major Morton key (child index c = x<<2|y<<1|z at every level)."""
+    return (_spread3(x) << np.uint64(2)) | (_spread3(y) << np.uint64(1)) | _spread3(z)
+
+
+@dataclass
+class Structure:
+    """Per-node geometry of a reference-layout pool, and its leaf blocks."""
+    d_max: int
+    level: np.ndarray       # int8 per slot (-1: not a live node)
+    x: np.ndarray
+    y: np.ndarray
+    z: np.ndarray
+    parent: np.ndarray      # int64 per slot (-1 root / free)
+    leaf: np.ndarray        # bool per slot
+    lblocks: np.ndarray     # ascending base slots of blocks with >=1 leaf
+    nbr: np.ndarray         # [nlb, 12] neighbour refs (csrc/ctx.cu encoding)
+
+
+def structure(child: np.ndarray, d_max: int, used: int | None = None) -> Structure:
+    """Level, cell, parent of every live node (top-down BFS) and the leaf
+    blocks with their 12-entry neighbour tables -- the host restatement of
+    ctx_prepare / k_leaf_tables (csrc/ctx.cu)."""
+    child = np.asarray(child)
+    n = child.shape[0] if used is None else used
+    child = child[:n].astype(np.int64)
+    level = np.full(n, -1, dtype=np.int8)
+    x = np.zeros(n, dtype=np.int64)
+    y = np.zeros(n, dtype=np.int64)
+    z = np.zeros(n, dtype=np.int64)
+    parent = np.full(n, -1, dtype=np.int64)
+    level[0] = 0
+    frontier = np.array([0], dtype=np.int64)
+    for L in range(d_max):
+        cb = child[frontier]
+        inner = frontier[cb >= 0]
+        if inner.size == 0:
+            break
+        base = child[inner]
+        kids = (base[:, None] + np.arange(8)[None, :]).ravel()
+        par = np.repeat(inner, 8)
+        c = np.tile(np.arange(8), inner.size)
+        level[kids] = L + 1
+        parent[kids] = par
+        x[kids] = 2 * x[par] + ((c >> 2) & 1)
+        y[kids] = 2 * y[par] + ((c >> 1) & 1)
+        z[kids] = 2 * z[par] + (c & 1)
+        frontier = kids
+    live = level >= 0
+    leaf = live & (child < 0)
+    # leaf blocks: base slots of blocks holding a leaf (root pseudo-block 0)
+    lslots = np.nonzero(leaf)[0]
+    bases = np.where(lslots == 0, 0, ((lslots - 1) & ~7) + 1)
+    lblocks = np.unique(bases)
+    nbr = _tables(child, level, x, y, z, parent, lblocks)
+    return Structure(d_max, level, x, y, z, parent, leaf, lblocks, nbr)
+
+
+def _descend(child, L, qx, qy, qz):
+    node = np.zeros(qx.shape, dtype=np.int64)
+    lvl = np.zeros(qx.shape, dtype=np.int64)
+    for l in range(int(L.max()) if L.size else 0):
+        go = (l < L) & (child[node] >= 0)
+        if not go.any():
+            break
+        s = (L - l - 1).clip(min=0)
+        sel = (((qx >> s) & 1) << 2) | (((qy >> s) & 1) << 1) | ((qz >> s) & 1)
+        node = np.where(go, child[node] + sel, node)
+        lvl = np.where(go, lvl + 1, lvl)
+    return node, lvl
+
+
+def _tables(child, level, x, y, z, parent, lblocks):
+    nlb = lblocks.size
+    nbr = np.full((nlb, 12), -1, dtype=np.int64)
+    real = lblocks != 0
+    b = lblocks[real]
+    L = level[b].astype(np.int64)            # level of the block's nodes
+    par = parent[b]
+    px, py, pz = x[par], y[par], z[par]
+    m = (1 << (L - 1))
+    out = np.full((b.size, 12), -1, dtype=np.int64)
+    for d in range(12):
+        qx, qy, qz = px + DIRS[d, 0], py + DIRS[d, 1], pz + DIRS[d, 2]
+        ok = (qx >= 0) & (qy >= 0) & (qz >= 0) & (qx < m) & (qy < m) & (qz < m)
+        q, lq = _descend(child, np.where(ok, L - 1, 0), np.where(ok, qx, 0),
+                         np.where(ok, qy, 0), np.where(ok, qz, 0))
+        qb = child[q]
+        ref = np.where((lq == L - 1) & (qb >= 0), qb, -q - 2)
+        out[:, d] = np.where(ok, ref, -1)
+    nbr[real] = out
+    return nbr.astype(np.int32)
+
+
+@dataclass
+class ShardPlan:
+    nranks: int
+    k: int                      # partition level
+    owner: np.ndarray           # per slot: owning rank, -1 top / not live
+    leaves_per_rank: np.ndarray
+    sel: list = field(default_factory=list)     # per rank: leaf-block indices
+    masks: list = field(default_factory=list)   # per rank: owned-leaf masks (u8)
+    halo: list = field(default_factory=list)    # per rank: slots to receive
+    send: dict = field(default_factory=dict)    # (src, dst) -> slots
+    top_levels: int = 0                         # propagate levels [0, k)
+
+
+def _unit_of(st: Structure, k: int) -> np.ndarray:
+    """Unit (level-k ancestor, or the node itself if a leaf above k) of every
+    live node; -1 for inner nodes above k (the replicated top)."""
+    n = st.level.shape[0]
+    unit = np.full(n, -1, dtype=np.int64)
+    live = st.level >= 0
+    lvl = st.level.astype(np.int64)
+    atk = live & (lvl == k)
+    unit[atk] = np.nonzero(atk)[0]
+    shallow_leaf = st.leaf & (lvl < k)
+    unit[shallow_leaf] = np.nonzero(shallow_leaf)[0]
+    for L in range(k + 1, st.d_max + 1):          # inherit top-down
+        at = np.nonzero(live & (lvl == L))[0]
+        unit[at] = unit[st.parent[at]]
+    return unit
+
+
+def plan(child, d_max: int, nranks: int, used: int | None = None,
+         k: int | None = None, st: Structure | None = None) -> ShardPlan:
+    st = st if st is not None else structure(child, d_max, used)
+    if k is None:  # enough units to balance: ~64 per rank
+        k = 0
+        while k < d_max and 8 ** k < 64 * nranks:
+            k += 1
+    unit = _unit_of(st, k)
+    n = st.level.shape[0]
+    units = np.unique(unit[unit >= 0])
+    lvl_u = st.level[units].astype(np.int64)
+    shift = (st.d_max - lvl_u).astype(np.uint64) * np.uint64(3)
+    key = morton(st.x[units], st.y[units], st.z[units]) << shift
+    order = np.argsort(key, kind="stable")
+    units = units[order]
+    # leaves per unit
+    leaf_slots = np.nonzero(st.leaf)[0]
+    pos = np.empty(n, dtype=np.int64)
+    pos[units] = np.arange(units.size)
+    counts = np.bincount(pos[unit[leaf_slots]], minlength=units.size)
+    cum = np.cumsum(counts)
+    total = cum[-1] if cum.size else 0
+    cuts = np.searchsorted(cum, (np.arange(1, nranks) * total) / nranks,
+                           side="left")
+    urank = np.zeros(units.size, dtype=np.int64)
+    for r, cidx in enumerate(cuts):
+        urank[cidx + 1:] = r + 1
+    owner = np.full(n, -1, dtype=np.int64)
+    has = unit >= 0
+    owner[has] = urank[pos[unit[has]]]
+    p = ShardPlan(nranks, k, owner, np.bincount(owner[leaf_slots],
+                                                minlength=nranks), top_levels=k)
+    # per-rank leaf blocks and owned masks
+    lb = st.lblocks
+    slots = np.where(lb[:, None] == 0, np.array([0] + [-1] * 7)[None, :],
+                     lb[:, None] + np.arange(8)[None, :])
+    valid = slots >= 0
+    sl = np.where(valid, slots, 0)
+    isleaf = valid & st.leaf[sl]
+    for r in range(nranks):
+        own = isleaf & (owner[sl] == r)
+        m = (own * (1 << np.arange(8))[None, :]).sum(axis=1).astype(np.uint8)
+        idx = np.nonzero(m)[0]
+        p.sel.append(idx.astype(np.int32))
+        p.masks.append(m[idx])
+    # halo: every slot the rank's stencils can read (whole neighbour blocks,
+    # coarse leaves, all siblings of processed blocks) plus the unit roots
+    # the top recomputation needs, minus what it owns
+    top = (owner < 0) & (st.level >= 0)
+    roots = units
+    for r in range(nranks):
+        idx = p.sel[r]
+        need = [slots[idx][valid[idx]]]
+        refs = st.nbr[idx].astype(np.int64).ravel()
+        same = refs[refs >= 0]
+        need.append((same[:, None] + np.arange(8)[None, :]).ravel())
+        need.append(-refs[refs <= -2] - 2)
+        need.append(roots)
+        need = np.unique(np.concatenate(need))
+        need = need[(owner[need] != r) & ~top[need]]
+        p.halo.append(need)
+        for q in range(nranks):
+            if q != r:
+                p.send[(q, r)] = need[owner[need] == q]
+    return p
+
+
+class ShardedSolver:
+    """Frozen-structure descent on one rank's shard.
+
+    Every rank keeps the (cheap) pool replicated and updates only the leaves
+    it owns: the context's leaf-block list is cut to the rank's blocks with
+    owned-leaf masks, so samples are gathered and streamed for owned leaves
+    only.  Per pass: leaf kernel + propagate (``compute``), halo exchange of
+    the post-pass values, recomputation of the replicated top (``finish``).
+    Energies stay per rank on the device until ``energies()`` sums them.
+    """
+
+    def __init__(self, u0, views, params, plan: ShardPlan, rank: int, *,
+                 precision: str = "fp32", exchange=None, group=None):
+        import torch
+        from . import fusion
+        if not (params.tau_split <= 0 and params.clamp and params.tau_join >= 1):
+            raise ValueError("sharded solving needs a frozen structure "
+                             "(tau_split <= 0, tau_join >= 1, clamp)")
+        self.params = params
+        self.plan = plan
+        self.rank = rank
+        self.group = group
+        self.s = fusion.Solver(u0, views, params, precision=precision)
+        s = self.s
+        s.kern.ctx_prepare(s.ctx, s.u.child, s.u.state, s.u.d_max, s.vvals,
+                           s.vws, s.vchilds)
+        s.kern.ctx_select(s.ctx, plan.sel[rank], plan.masks[rank])
+        self.exchange = exchange if exchange is not None else HaloExchange(
+            plan, rank, s.u.value.device, s.u.value.dtype)
+        self.e = torch.zeros(max(params.iterations, 1), dtype=torch.float64,
+                             device=s.u.value.device)
+        self.t = 0
+
+    @property
+    def values(self):
+        """Buffer holding the latest values (after ``finish``)."""
+        return self.s.cur
+
+    def compute(self, t: int) -> None:
+        from .fusion import step_scale
+        s, p, u = self.s, self.params, self.s.u
+        if t >= self.e.shape[0]:
+            import torch
+            self.e = torch.cat([self.e, torch.zeros_like(self.e)])
+        s.kern.fuse_passes_frozen(s.cur, s.nxt, u.child, u.state, s.vvals,
+                                  s.vws, s.vchilds, u.d_max, p.lam, p.eps,
+                                  p.gamma, p.tau_split, p.tau_join, p.clamp,
+                                  [step_scale(t, p)], ctx=s.ctx,
+                                  energies_out=self.e[t:t + 1])
+        self.t = t + 1
+
+    def finish(self) -> None:
+        s, u = self.s, self.s.u
+        s.kern.propagate_levels(s.nxt, u.child, 0, self.plan.top_levels,
+                                ctx=s.ctx)
+        s.cur, s.nxt = s.nxt, s.cur
+
+    def run(self, t0: int, k: int) -> None:
+        for t in range(t0, t0 + k):
+            self.compute(t)
+            self.exchange.exchange(self.s.nxt[:self.s.u.used], self.group)
+            self.finish()
+
+    def energies(self, reduce: bool = True):
+        """Energy before each pass run so far, summed over ranks."""
+        import torch.distributed as dist
+        e = self.e[:self.t].clone()
+        if reduce and dist.is_available() and dist.is_initialized():
+            dist.all_reduce(e, group=self.group)
+        return e
+
+    def close(self):
+        self.s.close()
+
+
+class HaloExchange:
+    """Per-pass exchange of owned values into the other ranks' halos
+    (torch.distributed point-to-point; NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, plan: ShardPlan, rank: int, device, dtype):
+        import torch
+        self.rank = rank
+        self.nranks = plan.nranks
+        self.sends = {}
+        self.recvs = {}
+        for q in range(plan.nranks):
+            if q == rank:
+                continue
+            s = plan.send.get((rank, q))
+            r = plan.send.get((q, rank))
+            if s is not None and s.size:
+                idx = torch.as_tensor(s, dtype=torch.int64, device=device)
+                self.sends[q] = (idx, torch.empty(s.size, dtype=dtype, device=device))
+            if r is not None and r.size:
+                idx = torch.as_tensor(r, dtype=torch.int64, device=device)
+                self.recvs[q] = (idx, torch.empty(r.size, dtype=dtype, device=device))
+
+    def exchange(self, values, group=None):
+        import torch
+        import torch.distributed as dist
+        ops = []
+        for q, (idx, buf) in self.sends.items():
+            torch.index_select(values, 0, idx, out=buf)
+            ops.append(dist.P2POp(dist.isend, buf, q, group))
+        for q, (idx, buf) in self.recvs.items():
+            ops.append(dist.P2POp(dist.irecv, buf, q, group))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        for q, (idx, buf) in self.recvs.items():
+            values.index_copy_(0, idx, buf)

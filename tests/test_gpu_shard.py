@@ -1,0 +1,71 @@
+"""Sharded solving on one GPU: the ranks of a plan run in lock-step in one
+process (each rank's kernels complete before the next starts; no kernel
+waits on another), the halo exchange is a device copy between the ranks'
+buffers.  fp64 results must equal the single-GPU run bit for bit."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as orc
+from tests.conftest import has_gpu
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")]
+
+
+class _NoExchange:
+    def exchange(self, values, group=None):
+        pass
+
+
+def _dev(pool):
+    from paper_1608_07411_b200.octree import OctreeField
+    return OctreeField.from_host(pool.value, pool.child, pool.state, pool.d_max,
+                                 weight=pool.weight)
+
+
+def _scene(full: bool, d=5, seed=3):
+    rng = np.random.default_rng(seed)
+    n = 1 << d
+    views = []
+    for _ in range(4):
+        f = np.clip(rng.standard_normal((n, n, n)) * 0.4, -1, 1).astype(np.float32)
+        w = (rng.random((n, n, n)) < 0.85).astype(np.uint8)
+        f[w == 0] = -1.0
+        views.append(orc.build_octree(f, w, tau=-1.0 if full else 0.5,
+                                      dtype=np.float32))
+    g = rng.integers(0, 3, (n, n, n)).astype(np.float64) * 0.3 - 0.3
+    u0 = orc.build_octree(g, tau=-1.0 if full else 0.2)
+    return u0, views
+
+
+@pytest.mark.parametrize("full,world", [(True, 2), (False, 2), (False, 3)])
+def test_lockstep_shards_match_single_gpu(full, world):
+    from paper_1608_07411_b200 import fusion, shard
+    u0h, views_h = _scene(full)
+    p = fusion.FusionParams(iterations=6, tau=-1.0, tau_split=0.0,
+                            tau_join=1.5, lam=0.4)
+    views = [_dev(v) for v in views_h]
+    ref = fusion.fuse(_dev(u0h), views, p)
+    rh = ref.field.to_host()
+    pl = shard.plan(u0h.child, u0h.d_max, world, used=u0h.used, k=2)
+    ranks = [shard.ShardedSolver(_dev(u0h), views, p, pl, r, precision="fp64",
+                                 exchange=_NoExchange()) for r in range(world)]
+    for t in range(p.iterations):
+        for s in ranks:
+            s.compute(t)
+        for (src, dst), idx in pl.send.items():
+            if idx.size:
+                ii = torch.as_tensor(idx, device="cuda")
+                ranks[dst].s.nxt[ii] = ranks[src].s.nxt[ii]
+        for s in ranks:
+            s.finish()
+    leaves = np.nonzero(rh.child < 0)[0]
+    for r, s in enumerate(ranks):
+        mine = leaves[pl.owner[leaves] == r]
+        got = s.values[:s.s.u.used].cpu().numpy()
+        assert np.array_equal(got[mine], rh.value[mine]), r
+    # energies: per-rank partial sums add up to the single-GPU energies
+    e = sum(s.energies(reduce=False).cpu().numpy() for s in ranks)
+    want = [st.energy for st in ref.stats]
+    np.testing.assert_allclose(e[1:], want[:-1], rtol=1e-12, atol=0)

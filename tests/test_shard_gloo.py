@@ -1,0 +1,165 @@
+"""Multi-rank sharding on CPU: world_size 2 (and 3) over gloo.
+
+Each rank owns a Morton range of subtrees (paper_1608_07411_b200.shard).  To
+test the decomposition without a GPU, every rank runs the CPU oracle's pass
+over its replicated pool, then *forgets* every value it does not own (NaN),
+receives its halo over gloo and recomputes the replicated top.  If the plan
+is right, the next pass's owned leaves read only owned/halo/top values, so
+after K passes the owned leaves equal the single-process result bit for bit
+(and any missing halo entry shows up as a NaN)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import oracle as orc
+from paper_1608_07411_b200 import shard
+
+K_PASSES = 4
+
+
+def scene(seed=7, d=5, nviews=3):
+    rng = np.random.default_rng(seed)
+    n = 1 << d
+    views = []
+    for _ in range(nviews):
+        f = (rng.integers(-2, 3, (n, n, n)) * 0.45).astype(np.float32)
+        w = (rng.random((n, n, n)) < 0.8).astype(np.uint8)
+        f[w == 0] = -1.0
+        views.append(orc.build_octree(f, w, tau=0.3, dtype=np.float32))
+    g = rng.integers(0, 3, (n, n, n)).astype(np.float64) * 0.3 - 0.3
+    u0 = orc.build_octree(g, tau=0.2)        # mixed leaf depths
+    p = orc.Params(iterations=K_PASSES, tau_split=0.0, tau_join=1.5, lam=0.4)
+    return u0, views, p
+
+
+def top_propagate(u, plan_):
+    """Recompute the replicated inner nodes above the partition level
+    (sequential child sums, _kernels.pyx:104-110)."""
+    st = shard.structure(u.child, u.d_max, u.used)
+    for L in range(plan_.k - 1, -1, -1):
+        nodes = np.nonzero((st.level == L) & (u.child[:u.used] >= 0))[0]
+        for n in nodes:
+            b = u.child[n]
+            acc = 0.0
+            for c in range(8):
+                acc += u.value[b + c]
+            u.value[n] = acc / 8.0
+
+
+def run_pass(u, views, p, t):
+    vv = [v.value for v in views]
+    vw = [v.weight for v in views]
+    vc = [v.child for v in views]
+    orc.iterate_pass(u.value, u.snap, u.child, u.joined, u.state, vv, vw, vc,
+                     u.d_max, p.lam, p.eps, p.gamma, orc.step_scale(t, p),
+                     p.tau_split, p.tau_join, p.clamp, False, None)
+    orc.propagate(u.value, u.child)
+
+
+def worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        u0, views, p = scene()
+        u = orc.solver_pool(u0, cap=u0.used)
+        pl = shard.plan(u.child, u.d_max, world, used=u.used, k=2)
+        ex = shard.HaloExchange(pl, rank, torch.device("cpu"), torch.float64)
+        owned = pl.owner[:u.used] == rank
+        top = (pl.owner[:u.used] < 0)
+        vals = torch.from_numpy(u.value)       # shares memory with the pool
+        for t in range(p.iterations):
+            run_pass(u, views, p, t)
+            keep = owned | top
+            u.value[:u.used][~keep] = np.nan
+            ex.exchange(vals[:u.used])
+            top_propagate(u, pl)
+        leaves = np.nonzero(u.child[:u.used] < 0)[0]
+        mine = leaves[owned[leaves]]
+        q.put((rank, mine, u.value[mine].copy(), pl.leaves_per_rank))
+    finally:
+        dist.destroy_process_group()
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_passes_match_single_process(world):
+    u0, views, p = scene()
+    ref = orc.fuse(u0, views, p).field
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=worker, args=(r, world, port, q))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    out = [q.get(timeout=300) for _ in procs]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    covered = []
+    for rank, mine, vals, counts in out:
+        assert np.all(np.isfinite(vals)), f"rank {rank} read a missing halo value"
+        assert np.array_equal(vals, ref.value[mine])
+        covered.append(mine)
+        assert counts.min() > 0
+    allv = np.sort(np.concatenate(covered))
+    leaves = np.nonzero(ref.child[:ref.used] < 0)[0]
+    assert np.array_equal(allv, leaves)      # every leaf owned exactly once
+
+
+def test_plan_is_balanced_and_disjoint():
+    u0, _, _ = scene(d=6)
+    pl = shard.plan(u0.child, u0.d_max, 4, used=u0.used)
+    leaves = np.nonzero(u0.child < 0)[0]
+    own = pl.owner[leaves]
+    assert (own >= 0).all()
+    counts = np.bincount(own, minlength=4)
+    assert counts.max() <= 1.5 * counts.mean()
+    # selected leaf blocks' masks cover each owned leaf once
+    st = shard.structure(u0.child, u0.d_max)
+    total = sum(int(np.unpackbits(m[:, None], axis=1).sum()) for m in pl.masks)
+    assert total == leaves.size
+    # halo never contains own or top nodes
+    for r in range(4):
+        h = pl.halo[r]
+        assert (pl.owner[h] != r).all() and (pl.owner[h] >= 0).all()
+
+
+def test_host_tables_match_reference_descent():
+    """shard.structure's neighbour tables == root descents of the oracle."""
+    u0, _, _ = scene(d=4)
+    st = shard.structure(u0.child, u0.d_max)
+    child = u0.child
+    for i, b in enumerate(st.lblocks):
+        if b == 0:
+            continue
+        L = int(st.level[b])
+        par = st.parent[b]
+        for d in range(12):
+            qx, qy, qz = (st.x[par] + shard.DIRS[d, 0], st.y[par] + shard.DIRS[d, 1],
+                          st.z[par] + shard.DIRS[d, 2])
+            m = 1 << (L - 1)
+            if not (0 <= qx < m and 0 <= qy < m and 0 <= qz < m):
+                assert st.nbr[i, d] == -1
+                continue
+            node, lvl = 0, 0
+            while lvl < L - 1 and child[node] >= 0:
+                s = L - 1 - lvl - 1
+                node = child[node] + ((((qx >> s) & 1) << 2) | (((qy >> s) & 1) << 1)
+                                      | ((qz >> s) & 1))
+                lvl += 1
+            want = child[node] if (lvl == L - 1 and child[node] >= 0) else -node - 2
+            assert st.nbr[i, d] == want

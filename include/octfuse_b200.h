@@ -116,6 +116,21 @@ int octf_fuse_passes_frozen(octf_ctx *ctx, int dtype, void *ubuf0, void *ubuf1,
                             double *energies_pre, int device_energies,
                             void *stream);
 
+/* solver="pd" (north_star; no reference counterpart,
+ * definition in oracle/pd_oracle.c): npasses TV-L1 primal-dual passes on a
+ * frozen tree.  set_a / set_b: host tables of 5 device pools {u, ubar, px,
+ * py, pz}; pass k reads set_a (k even) or set_b (k odd) and writes the
+ * other, then propagates all five.  energies_pre (host): E(u) before each
+ * pass (exact TV + L1 data, same normalisation as the descent's data term).
+ * 4, 8, 16 or 32 views. */
+int octf_pd_passes(octf_ctx *ctx, int dtype, void *const *set_a,
+                   void *const *set_b, const int32_t *uchild,
+                   const int64_t *ustate, int64_t cap, int nviews,
+                   const float *const *vvals, const float *const *vws,
+                   const int32_t *const *vchilds, int d_max, double lam,
+                   double tau, double sigma, double gamma, int clamp,
+                   int npasses, double *energies_pre, void *stream);
+
 /* Build the context's structures for a pool (and views) up front. */
 int octf_ctx_prepare(octf_ctx *ctx, const int32_t *uchild,
                      const int64_t *ustate, int64_t cap, int d_max, int nviews,

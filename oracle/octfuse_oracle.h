@@ -62,6 +62,16 @@ int orc_tree_energy(const double *uval, const int32_t *uchild, int nviews,
                     const int32_t *const *vchild, int d_max, double lam,
                     double eps, double gamma, double *out);
 
+/* pd_oracle.c -- the north_star's TV-L1 primal-dual pass (PARITY UNPINNED:
+ * no reference implementation exists; see the definition in that file). */
+int orc_pd_pass(const double *u, const double *ub, const double *px,
+                const double *py, const double *pz, double *u_o, double *ub_o,
+                double *px_o, double *py_o, double *pz_o,
+                const int32_t *child, int64_t used, int nviews,
+                const float *const *vval, const float *const *vw,
+                const int32_t *const *vchild, int d_max, double lam, double tau,
+                double sigma, double gamma, int clamp, double *energy);
+
 #ifdef __cplusplus
 }
 #endif

@@ -63,6 +63,8 @@ def lib():
                                        P, i64, P]
         L.orc_tree_energy.argtypes = [P, P, i32, P, P, P, i32, dbl, dbl, dbl,
                                       P]
+        L.orc_pd_pass.argtypes = [P] * 10 + [P, i64, i32, P, P, P, i32, dbl,
+                                             dbl, dbl, dbl, i32, P]
         _lib = L
     return _lib
 
@@ -311,6 +313,49 @@ def fuse(u0: Pool, views: list, p, *, log_joins=False, reverse=False,
     if log_joins:
         jl = np.vstack(chunks) if chunks else np.zeros((0, 12))
     return FuseOut(u, stats, jl)
+
+
+# ------------------------------------------------- primal-dual (unpinned) ----
+
+def pd_steps(lam: float):
+    """Default primal/dual step sizes: tau*sigma*||K||^2 < 1 with
+    ||K|| <= lam*sqrt(12) at unit spacing."""
+    t = 0.99 / (lam * np.sqrt(12.0))
+    return t, t
+
+
+def pd_fuse(u0: Pool, views: list, lam: float, gamma: float, iterations: int,
+            tau: float | None = None, sigma: float | None = None,
+            clamp: bool = True):
+    """TV-L1 primal-dual schedule on a frozen tree (pd_oracle.c definition,
+    PARITY UNPINNED).  Returns (u, ubar, px, py, pz pools, energies_pre)."""
+    if tau is None or sigma is None:
+        tau, sigma = pd_steps(lam)
+    used = u0.used
+    u = u0.value[:used].astype(np.float64).copy()
+    ub = u.copy()
+    px = np.zeros(used)
+    py = np.zeros(used)
+    pz = np.zeros(used)
+    child = u0.child[:used]
+    vv = [v.value for v in views]
+    vw = [v.weight for v in views]
+    vc = [v.child for v in views]
+    energies = []
+    e = np.zeros(1)
+    for _ in range(iterations):
+        outs = [a.copy() for a in (u, ub, px, py, pz)]
+        _check(lib().orc_pd_pass(
+            _ptr(u), _ptr(ub), _ptr(px), _ptr(py), _ptr(pz),
+            *[_ptr(o) for o in outs], _ptr(child), used, len(views),
+            _ptr_array(vv), _ptr_array(vw), _ptr_array(vc), u0.d_max,
+            float(lam), float(tau), float(sigma), float(gamma),
+            int(bool(clamp)), _ptr(e)))
+        energies.append(float(e[0]))
+        for o in outs:
+            propagate(o, child)
+        u, ub, px, py, pz = outs
+    return u, ub, px, py, pz, energies
 
 
 # ------------------------------------------------------------ traversal ----

@@ -146,6 +146,21 @@ def fuse_passes_frozen(ubuf0, ubuf1, uchild, ustate, vvals, vws, vchilds,
     return en
 
 
+def pd_passes(set_a, set_b, uchild, ustate, vvals, vws, vchilds, d_max, lam,
+              tau, sigma, gamma, clamp, npasses, *, ctx):
+    """solver='pd': npasses primal-dual passes; set_a/set_b = 5 pools
+    (u, ubar, px, py, pz).  Returns the energies before each pass."""
+    tv, tw, tc = _views(vvals, vws, vchilds)
+    ta = ptr_table([ptr(t) for t in set_a])
+    tb = ptr_table([ptr(t) for t in set_b])
+    en = np.zeros(max(int(npasses), 1), dtype=np.float64)
+    call("octf_pd_passes", ctx.h, _dtype_code(set_a[0]), ta, tb, ptr(uchild),
+         _state_ptr(ustate), uchild.shape[0], len(vvals), tv, tw, tc,
+         int(d_max), float(lam), float(tau), float(sigma), float(gamma),
+         int(bool(clamp)), int(npasses), en.ctypes.data, stream_handle())
+    return en[:npasses]
+
+
 def ctx_prepare(ctx, uchild, ustate, d_max, vvals, vws, vchilds):
     tv, tw, tc = _views(vvals, vws, vchilds)
     call("octf_ctx_prepare", ctx.h, ptr(uchild), _state_ptr(ustate),

@@ -303,6 +303,46 @@ int octf_fuse_passes_frozen(octf_ctx* ctx, int dtype, void* ubuf0, void* ubuf1,
   });
 }
 
+int octf_pd_passes(octf_ctx* ctx, int dtype, void* const* set_a,
+                   void* const* set_b, const int32_t* uchild,
+                   const int64_t* ustate, int64_t cap, int nviews,
+                   const float* const* vvals, const float* const* vws,
+                   const int32_t* const* vchilds, int d_max, double lam,
+                   double tau, double sigma, double gamma, int clamp,
+                   int npasses, double* energies_pre, void* stream) {
+  return guard([&] {
+    if (!ctx || !set_a || !set_b || !uchild || !ustate || !energies_pre)
+      throw octf::Error(octf::kEArg, "null argument");
+    check_dtype(dtype);
+    if (d_max < 0 || d_max > OCTF_MAX_DEPTH)
+      throw octf::Error(octf::kEDepth, "tree depth out of range");
+    if (nviews < 1) throw octf::Error(octf::kEArg, "at least one view is required");
+    if (!(tau > 0 && sigma > 0 && lam > 0 && gamma > 0))
+      throw octf::Error(octf::kEArg, "tau, sigma, lam, gamma must be positive");
+    octf::ctx_set_views(ctx->c, nviews, vvals, vws, vchilds, S(stream));
+    octf::PdHostArgs a;
+    for (int q = 0; q < 5; ++q) {
+      a.in[q] = set_a[q];
+      a.out[q] = set_b[q];
+    }
+    a.child = uchild;
+    a.state = ustate;
+    a.cap = cap;
+    a.d_max = d_max;
+    a.lam = lam;
+    a.tau = tau;
+    a.sigma = sigma;
+    a.gamma = gamma;
+    a.clamp = clamp;
+    a.npasses = npasses;
+    a.energies = energies_pre;
+    if (dtype == OCTF_F64)
+      octf::pd_passes_f64(ctx->c, a, S(stream));
+    else
+      octf::pd_passes_f32(ctx->c, a, S(stream));
+  });
+}
+
 int octf_ctx_prepare(octf_ctx* ctx, const int32_t* uchild,
                      const int64_t* ustate, int64_t cap, int d_max, int nviews,
                      const float* const* vvals, const float* const* vws,

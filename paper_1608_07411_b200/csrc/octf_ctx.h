@@ -190,6 +190,22 @@ double energy_f64(Ctx& c, const double* u, const int32_t* child,
                   const PassParams& p, double* terms, cudaStream_t st);
 double energy_f32(Ctx& c, const float* u, const int32_t* child,
                   const PassParams& p, double* terms, cudaStream_t st);
+// solver="pd": TV-L1 primal-dual passes (frozen tree), 5 arrays per set
+// {u, ubar, px, py, pz}; pass k reads in (k even) / out (k odd)
+struct PdHostArgs {
+  void* in[5];
+  void* out[5];
+  const int32_t* child;
+  const int64_t* state;
+  int64_t cap;
+  int d_max;
+  double lam, tau, sigma, gamma;
+  int clamp;
+  int npasses;
+  double* energies;  // host, npasses: energy of u before each pass
+};
+void pd_passes_f64(Ctx& c, PdHostArgs& a, cudaStream_t st);
+void pd_passes_f32(Ctx& c, PdHostArgs& a, cudaStream_t st);
 void frozen_passes_f64(Ctx& c, FrozenArgs& a, cudaStream_t st);
 void frozen_passes_f32(Ctx& c, FrozenArgs& a, cudaStream_t st);
 void propagate_levels_f64(Ctx& c, double* v, const int32_t* child, int lo,

@@ -27,3 +27,9 @@ void propagate_levels_f32(Ctx& c, float* v, const int32_t* child, int lo, int hi
   propagate_levels_impl<float>(c, v, child, lo, hi, st);
 }
 }  // namespace octf
+
+namespace octf {
+void pd_passes_f32(Ctx& c, PdHostArgs& a, cudaStream_t st) {
+  pd_passes_impl<float>(c, a, st);
+}
+}  // namespace octf

@@ -27,3 +27,9 @@ void propagate_levels_f64(Ctx& c, double* v, const int32_t* child, int lo, int h
   propagate_levels_impl<double>(c, v, child, lo, hi, st);
 }
 }  // namespace octf
+
+namespace octf {
+void pd_passes_f64(Ctx& c, PdHostArgs& a, cudaStream_t st) {
+  pd_passes_impl<double>(c, a, st);
+}
+}  // namespace octf

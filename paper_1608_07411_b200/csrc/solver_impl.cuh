@@ -83,6 +83,7 @@ __device__ __forceinline__ T clamp1(T v) {
 // ---------------------------------------------------------------------------
 // 1. fast leaf update over leaf blocks (leaf_kernel.cuh)
 #include "leaf_kernel.cuh"
+#include "pd_kernel.cuh"
 
 // ---------------------------------------------------------------------------
 // generic update of one cell at level L from the snapshot by root descents:
@@ -912,6 +913,77 @@ void frozen_passes_impl(Ctx& c, FrozenArgs& a, cudaStream_t st) {
   OCTF_CUDA(cudaMemcpyAsync(a.energies_pre, c.dscalar.p,
                             a.npasses * sizeof(double), cudaMemcpyDeviceToHost,
                             st));
+  OCTF_CUDA(cudaStreamSynchronize(st));
+}
+
+// npasses of the TV-L1 primal-dual scheme on a frozen tree; set A = a.in,
+// set B = a.out; pass k reads the set k%2 and writes the other
+template <typename T>
+void pd_passes_impl(Ctx& c, PdHostArgs& a, cudaStream_t st) {
+  if (a.d_max < 0 || a.d_max > kMaxDepth)
+    throw Error(kEDepth, "tree depth out of range");
+  if (a.npasses < 1) return;
+  ensure_prepared<T>(c, a.child, a.cap, a.d_max, a.state, st);
+  const int nv = c.nviews;
+  if (!(nv == 4 || nv == 8 || nv == 16 || nv == 32) || c.sstride != nv)
+    throw Error(kEArg, "solver='pd' supports 4, 8, 16 or 32 views");
+  constexpr int kChunk = 32;
+  const unsigned g = leaf_grid(c);
+  c.partials.ensure((size_t)g * kChunk);
+  c.dscalar.ensure(a.npasses > 1024 ? a.npasses : 1024);
+  for (int k0 = 0; k0 < a.npasses; k0 += kChunk) {
+    const int nk = a.npasses - k0 < kChunk ? a.npasses - k0 : kChunk;
+    for (int j = 0; j < nk; ++j) {
+      const int k = k0 + j;
+      void* const* in = (k & 1) ? a.out : a.in;
+      void* const* out = (k & 1) ? a.in : a.out;
+      PdArgs<T> p;
+      p.lblocks = c.lblocks.p;
+      p.nlb = c.nlb;
+      p.lmeta = c.lmeta.p;
+      p.nbr = c.nbr.p;
+      p.u = (const T*)in[0];
+      p.ub = (const T*)in[1];
+      p.px = (const T*)in[2];
+      p.py = (const T*)in[3];
+      p.pz = (const T*)in[4];
+      p.u_o = (T*)out[0];
+      p.ub_o = (T*)out[1];
+      p.px_o = (T*)out[2];
+      p.py_o = (T*)out[3];
+      p.pz_o = (T*)out[4];
+      p.F = c.F.p;
+      p.W = c.W.p;
+      p.M = c.M.p;
+      p.stride = c.sstride;
+      p.nv = nv;
+      p.d_max = a.d_max;
+      p.lam = (T)a.lam;
+      p.tl = (T)(a.tau * a.lam);
+      p.sl = (T)(a.sigma * a.lam);
+      p.tau = (T)a.tau;
+      p.gamma = (T)a.gamma;
+      p.clamp = a.clamp;
+      p.epart = c.partials.p + (size_t)j * g;
+#define OCTF_PD(BW, N) k_pd_pass<T, BW, N><<<g, kT, 0, st>>>(p)
+      if (c.binw) {
+        if (nv == 4) OCTF_PD(true, 4); else if (nv == 8) OCTF_PD(true, 8);
+        else if (nv == 16) OCTF_PD(true, 16); else OCTF_PD(true, 32);
+      } else {
+        if (nv == 4) OCTF_PD(false, 4); else if (nv == 8) OCTF_PD(false, 8);
+        else if (nv == 16) OCTF_PD(false, 16); else OCTF_PD(false, 32);
+      }
+#undef OCTF_PD
+      OCTF_CUDA(cudaGetLastError());
+      ++c.launches;
+      for (int q = 0; q < 5; ++q) launch_propagate<T>(c, (T*)out[q], a.child, st);
+    }
+    k_sum_partials_multi<<<nk, kT, 0, st>>>(c.partials.p, g, c.dscalar.p + k0);
+    OCTF_CUDA(cudaGetLastError());
+    ++c.launches;
+  }
+  OCTF_CUDA(cudaMemcpyAsync(a.energies, c.dscalar.p, a.npasses * sizeof(double),
+                            cudaMemcpyDeviceToHost, st));
   OCTF_CUDA(cudaStreamSynchronize(st));
 }
 

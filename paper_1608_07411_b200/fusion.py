@@ -314,14 +314,111 @@ class Solver:
         self.ctx.close()
 
 
+def pd_steps(lam: float):
+    """Default primal/dual steps for solver='pd': tau*sigma*||K||^2 < 1 with
+    ||K|| <= lam*sqrt(12) at unit (finest-cell) spacing."""
+    t = 0.99 / (lam * np.sqrt(12.0))
+    return t, t
+
+
+class PDSolver:
+    """The north_star's TV-L1 primal-dual iteration (solver='pd') on a frozen
+    tree: dual ascent with projection, divergence, generalised-median prox
+    (the reference has none -- its definition and
+    CPU oracle are oracle/pd_oracle.c).  State: u, ubar, p = (px, py, pz)
+    per node, double-buffered; p starts at 0 and ubar at u0."""
+
+    def __init__(self, u0: OctreeField, views, params: FusionParams, *,
+                 precision: str = "fp32", tau: float | None = None,
+                 sigma: float | None = None):
+        if not views:
+            raise ValueError("at least one view is required")
+        for v in views:
+            if v.d_max != u0.d_max:
+                raise ValueError("view and iterate depths differ")
+        dtype = torch.float64 if precision == "fp64" else torch.float32
+        self.params = params
+        t, s = pd_steps(params.lam)
+        self.tau = t if tau is None else tau
+        self.sigma = s if sigma is None else sigma
+        self.kern = _backend.get()
+        self.u = _solver_field(u0, dtype)
+        used, cap = self.u.used, self.u.capacity
+        self.vvals, self.vws, self.vchilds = view_arrays(views)
+        self.ctx = _lib.Ctx()
+        def z():
+            return pool_empty(cap, dtype, fill=0)
+        ub = z()
+        ub[:used].copy_(self.u.value[:used])
+        self.a = [self.u.value, ub, z(), z(), z()]
+        self.b = [self.u.snap, z(), z(), z(), z()]
+        self.stats: list[IterationStats] = []
+
+    def run(self, t0: int, k: int) -> list:
+        p, u = self.params, self.u
+        w0 = time.perf_counter()
+        en = self.kern.pd_passes(self.a, self.b, u.child, u.state, self.vvals,
+                                 self.vws, self.vchilds, u.d_max, p.lam,
+                                 self.tau, self.sigma, p.gamma, p.clamp, k,
+                                 ctx=self.ctx)
+        wall = (time.perf_counter() - w0) * 1e3 / max(k, 1)
+        if k % 2:
+            self.a, self.b = self.b, self.a
+        out = []
+        for j, t in enumerate(range(t0, t0 + k)):
+            if self.stats and self.stats[-1].energy is None:
+                self.stats[-1].energy = float(en[j])
+            st = IterationStats(t + 1, None, u.node_count,
+                                u.node_count * 10 * u.value.element_size(), 0, 0,
+                                wall)
+            self.stats.append(st)
+            out.append(st)
+        return out
+
+    def finish(self) -> None:
+        """Energy of the latest u: one more evaluation pass on a scratch
+        copy (the state is not advanced)."""
+        if self.stats and self.stats[-1].energy is None:
+            p, u = self.params, self.u
+            scratch = [t.clone() for t in self.b]
+            en = self.kern.pd_passes(self.a, scratch, u.child, u.state,
+                                     self.vvals, self.vws, self.vchilds,
+                                     u.d_max, p.lam, self.tau, self.sigma,
+                                     p.gamma, p.clamp, 1, ctx=self.ctx)
+            self.stats[-1].energy = float(en[0])
+
+    def result(self) -> FuseResult:
+        self.finish()
+        self.u.value, self.u.snap = self.a[0], self.b[0]
+        return FuseResult(field=self.u, stats=list(self.stats))
+
+    @property
+    def state(self):
+        """(u, ubar, px, py, pz) after the last pass."""
+        return tuple(self.a)
+
+    def close(self):
+        self.ctx.close()
+
+
 def fuse(u0: OctreeField, views, params: FusionParams, *,
          log_joins: bool = False, reverse: bool = False,
-         precision: str = "fp64") -> FuseResult:
+         precision: str = "fp64", solver: str = "descent") -> FuseResult:
     """Run the full descent schedule on an octree iterate (fusion.py:186-241).
 
     ``u0`` is left untouched.  Statistics carry one row per pass; energies
     are those after the pass's restructuring and re-propagation.
+    ``solver="pd"`` runs the north_star's TV-L1 primal-dual iteration
+    instead (frozen structure; no reference counterpart, see PDSolver).
     """
+    if solver == "pd":
+        pds = PDSolver(u0, views, params, precision=precision)
+        pds.run(0, params.iterations)
+        res = pds.result()
+        pds.close()
+        return res
+    if solver != "descent":
+        raise ValueError("solver must be 'descent' or 'pd'")
     solver = Solver(u0, views, params, log_joins=log_joins, reverse=reverse,
                     precision=precision)
     solver.run(0, params.iterations)

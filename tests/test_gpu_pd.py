@@ -1,0 +1,76 @@
+"""solver='pd' (the north_star's TV-L1 primal-dual iteration) against its CPU
+restatement oracle/pd_oracle.c.  PARITY UNPINNED: the reference has no
+primal-dual solver, so the oracle is the written definition, not reference
+code.  fp64: every leaf value and dual bit-exact; fp32 within 1e-4."""
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+from tests.conftest import has_gpu
+from tests.goldens import load, small_views
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")]
+
+
+def _dev(pool):
+    from paper_1608_07411_b200.octree import OctreeField
+    return OctreeField.from_host(pool.value, pool.child, pool.state, pool.d_max,
+                                 weight=pool.weight)
+
+
+def _views_u0(kind):
+    if kind == "small":            # 3 views: pad to 4 with an unobserved view
+        z = load("small")
+        views = small_views(z)
+        blank = orc.Pool(np.zeros(1, np.float32), np.full(1, -1, np.int32),
+                         np.array([1, -1, 1], np.int64), views[0].d_max,
+                         weight=np.zeros(1, np.float32))
+        return views + [blank], orc.Pool(z["u0_value"], z["u0_child"],
+                                         z["u0_state"], 4), 0.3
+    rng = np.random.default_rng(11)
+    d = 5
+    n = 1 << d
+    views = []
+    for _ in range(8 if kind == "mixed" else 16):
+        f = np.clip(rng.standard_normal((n, n, n)) * 0.5, -1, 1).astype(np.float32)
+        w = (rng.random((n, n, n)) < 0.9).astype(np.uint8)
+        f[w == 0] = -1.0
+        views.append(orc.build_octree(f, w, tau=0.6 if kind == "mixed" else -1.0,
+                                      dtype=np.float32))
+    g = rng.integers(0, 3, (n, n, n)).astype(np.float64) * 0.4 - 0.4
+    return views, orc.build_octree(g, tau=0.2 if kind == "mixed" else -1.0), 0.5
+
+
+@pytest.mark.parametrize("kind", ["small", "mixed", "full"])
+def test_pd_fp64_matches_cpu_restatement(kind):
+    from paper_1608_07411_b200 import fusion
+    views_h, u0h, lam = _views_u0(kind)
+    iters = 8
+    u, ub, px, py, pz, en = orc.pd_fuse(u0h, views_h, lam, 1e-4, iters)
+    p = fusion.FusionParams(lam=lam, iterations=iters)
+    s = fusion.PDSolver(_dev(u0h), [_dev(v) for v in views_h], p,
+                        precision="fp64")
+    s.run(0, iters)
+    used = u0h.used
+    leaves = np.nonzero(u0h.child[:used] < 0)[0]
+    got = [t[:used].cpu().numpy() for t in s.state]
+    for g, w in zip(got, (u, ub, px, py, pz)):
+        assert np.array_equal(g[leaves], w[leaves])
+        assert np.array_equal(g, w)            # inner nodes: propagate
+    e = [st.energy for st in s.stats[:-1]]
+    np.testing.assert_allclose(e, en[1:], rtol=1e-12, atol=0)
+
+
+def test_pd_fp32_tolerance_and_descent():
+    from paper_1608_07411_b200 import fusion
+    views_h, u0h, lam = _views_u0("full")
+    iters = 30
+    u, *_ , en = orc.pd_fuse(u0h, views_h, lam, 1e-4, iters)
+    p = fusion.FusionParams(lam=lam, iterations=iters)
+    res = fusion.fuse(_dev(u0h), [_dev(v) for v in views_h], p, solver="pd",
+                      precision="fp32")
+    got = res.field.to_host().value
+    assert np.max(np.abs(got - u)) <= 1e-4
+    # the primal-dual scheme lowers the TV-L1 energy from its start
+    assert en[-1] < en[0]

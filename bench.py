@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity-mode", action="store_true")
+    ap.add_argument("--no-pd", action="store_true")
     return ap.parse_args()
 
 
@@ -235,6 +236,8 @@ def run_cuda(args, rank, world, local_rank):
     solver.close()
     if rank == 0 and args.precision == "fp32" and not args.no_parity_mode:
         out["parity_mode"] = run_parity_mode(views, u0, p, args, nleaves)
+    if rank == 0 and not args.no_pd:
+        out["pd_mode"] = run_pd_mode(views, u0, p, args, nleaves, peak)
     if rank == 0 and not args.no_e2e:
         out["e2e"] = run_e2e(views, u0, p, args)
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -276,6 +279,40 @@ def run_parity_mode(views, u0, p, args, nleaves):
     return {"dtype": "f64", "value": nleaves * args.steps / (ms / 1e3),
             "unit": UNIT, "ms_per_step": ms / args.steps,
             "note": "bit-exact parity mode (tests/test_gpu_parity.py)"}
+
+
+def run_pd_mode(views, u0, p, args, nleaves, peak):
+    """The north_star's TV-L1 primal-dual iteration (solver='pd') on the same
+    workload: one step = one primal-dual pass (dual + primal + prox +
+    propagate of u, ubar, p) with its energy.  Parity is against its own CPU
+    restatement (oracle/pd_oracle.c; the reference has no such solver)."""
+    import torch
+    from paper_1608_07411_b200 import fusion
+    s = fusion.PDSolver(u0, views, p, precision=args.precision)
+    s.run(0, args.warmup)
+    s.ctx.profile(True)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    s.run(args.warmup, args.steps)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    prof = s.ctx.profile(False)
+    s.close()
+    kms = prof["leaf_ms"] / max(prof["leaf_launches"], 1)
+    vsz = 4 if args.precision == "fp32" else 8
+    b_leaf = 10 * vsz + 4 * args.views + (args.views + 7) // 8
+    ach = nleaves * b_leaf / (kms / 1e3) / 1e9
+    return {"solver": "pd", "value": nleaves * args.steps / (ms / 1e3),
+            "unit": UNIT, "ms_per_step": ms / args.steps,
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": peak,
+                         "unit": "GB/s", "frac": ach / peak,
+                         "kernel": "k_pd_pass", "kernel_ms": kms,
+                         "bytes_per_leaf": b_leaf},
+            "note": "north_star TV-L1 primal-dual; parity vs its CPU "
+                    "restatement (tests/test_gpu_pd.py), unpinned vs reference"}
 
 
 def run_e2e(views, u0, p, args):

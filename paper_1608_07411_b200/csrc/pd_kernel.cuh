@@ -221,6 +221,11 @@ __global__ void __launch_bounds__(kT) k_pd_pass(PdArgs<T> a) {
   }
   const T den = W + a.gamma;
   bitonic<NV, !BINW>(f, w, ix);
+  if (BINW) {  // unit weights were not carried through the sort
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+      w[v] = f[v] != __int_as_float(0x7f800000) ? 1.f : 0.f;
+  }
   // generalised weighted median (oracle/pd_oracle.c wmedian_prox)
   const T cc = a.tau / den;
   T S = 0, res = v0;

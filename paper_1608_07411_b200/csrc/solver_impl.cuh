@@ -965,6 +965,8 @@ void pd_passes_impl(Ctx& c, PdHostArgs& a, cudaStream_t st) {
       p.gamma = (T)a.gamma;
       p.clamp = a.clamp;
       p.epart = c.partials.p + (size_t)j * g;
+      if (c.timing && (int)c.pev.size() >= 2 * kChunk)
+        OCTF_CUDA(cudaEventRecord(c.pev[2 * j], st));
 #define OCTF_PD(BW, N) k_pd_pass<T, BW, N><<<g, kT, 0, st>>>(p)
       if (c.binw) {
         if (nv == 4) OCTF_PD(true, 4); else if (nv == 8) OCTF_PD(true, 8);
@@ -976,11 +978,22 @@ void pd_passes_impl(Ctx& c, PdHostArgs& a, cudaStream_t st) {
 #undef OCTF_PD
       OCTF_CUDA(cudaGetLastError());
       ++c.launches;
+      if (c.timing && (int)c.pev.size() >= 2 * kChunk)
+        OCTF_CUDA(cudaEventRecord(c.pev[2 * j + 1], st));
       for (int q = 0; q < 5; ++q) launch_propagate<T>(c, (T*)out[q], a.child, st);
     }
     k_sum_partials_multi<<<nk, kT, 0, st>>>(c.partials.p, g, c.dscalar.p + k0);
     OCTF_CUDA(cudaGetLastError());
     ++c.launches;
+    if (c.timing && (int)c.pev.size() >= 2 * kChunk) {
+      OCTF_CUDA(cudaStreamSynchronize(st));
+      for (int j = 0; j < nk; ++j) {
+        float ms = 0.f;
+        OCTF_CUDA(cudaEventElapsedTime(&ms, c.pev[2 * j], c.pev[2 * j + 1]));
+        c.t_leaf_ms += ms;
+        ++c.n_leaf;
+      }
+    }
   }
   OCTF_CUDA(cudaMemcpyAsync(a.energies, c.dscalar.p, a.npasses * sizeof(double),
                             cudaMemcpyDeviceToHost, st));

@@ -170,8 +170,8 @@ __global__ void k_gather(const int32_t* __restrict__ ucs,
       w = vs.w[v][n];
       flag |= (w != 0.f && w != 1.f);
     }
-    F[sidx * stride + v] = f;
-    W[sidx * stride + v] = w;
+    F[samp_idx(sidx, v, stride)] = f;
+    W[samp_idx(sidx, v, stride)] = w;
   }
   if (flag) atomicExch(nonbin, 1);
 }
@@ -181,7 +181,8 @@ __global__ void k_masks(const float* __restrict__ W, int64_t stride, int nv,
   int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   uint32_t m = 0;
-  for (int v = 0; v < nv; ++v) m |= (W[s * stride + v] != 0.f ? 1u : 0u) << v;
+  for (int v = 0; v < nv; ++v)
+    m |= (W[samp_idx(s, v, stride)] != 0.f ? 1u : 0u) << v;
   M[s] = m;
 }
 
@@ -387,16 +388,17 @@ ViewSet ctx_views(const Ctx& c) {
 }
 
 void ctx_gather(Ctx& c, cudaStream_t st) {
-  // one contiguous vector of views per leaf, padded to 16 B: a lane reads
-  // its samples with 128-bit loads, a warp reads 32 vectors back to back
+  // tiles of 256 leaves, view-major inside a tile (octf_common.cuh
+  // samp_idx); views padded to 4 and leaves to whole tiles
   int64_t n = c.nlb * 8;
+  const int64_t npad = (n + kTileLeaves - 1) / kTileLeaves * kTileLeaves;
   int nv = c.nviews;
   const int64_t nvp = (nv + 3) & ~3;
   c.sstride = nvp;
-  c.F.ensure((size_t)nvp * n);
-  c.W.ensure((size_t)nvp * n);
-  OCTF_CUDA(cudaMemsetAsync(c.F.p, 0, (size_t)nvp * n * sizeof(float), st));
-  OCTF_CUDA(cudaMemsetAsync(c.W.p, 0, (size_t)nvp * n * sizeof(float), st));
+  c.F.ensure((size_t)nvp * npad);
+  c.W.ensure((size_t)nvp * npad);
+  OCTF_CUDA(cudaMemsetAsync(c.F.p, 0, (size_t)nvp * npad * sizeof(float), st));
+  OCTF_CUDA(cudaMemsetAsync(c.W.p, 0, (size_t)nvp * npad * sizeof(float), st));
   OCTF_CUDA(cudaMemsetAsync(c.counters.p, 0, sizeof(int32_t), st));
   k_gather<<<grid_for(n), kThreads, 0, st>>>(c.child_key, c.lblocks.p, c.nlb,
                                               c.lkey.p, ctx_views(c), c.F.p,
@@ -407,8 +409,8 @@ void ctx_gather(Ctx& c, cudaStream_t st) {
   OCTF_CUDA(cudaStreamSynchronize(st));
   c.binw = (c.h_counters[0] == 0) && nv <= 32;
   if (c.binw) {
-    c.M.ensure(n);
-    k_masks<<<grid_for(n), kThreads, 0, st>>>(c.W.p, nvp, nv, n, c.M.p);
+    c.M.ensure(npad);
+    k_masks<<<grid_for(npad), kThreads, 0, st>>>(c.W.p, nvp, nv, npad, c.M.p);
     OCTF_CUDA(cudaGetLastError());
   }
 }

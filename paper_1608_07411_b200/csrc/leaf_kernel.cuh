@@ -11,9 +11,12 @@
 //  * only lanes whose step leaves the block read memory, through the
 //    block's 12-entry neighbour table (compile-time direction per stencil
 //    point and lane parity);
-//  * each leaf's N samples are one contiguous 16 B-aligned vector read with
-//    128-bit loads (a warp streams 32 consecutive vectors), all issued
-//    before the stencil arithmetic.
+//  * the CTA's 256 leaves are one sample tile ([view][256], contiguous in
+//    HBM, octf_common.cuh samp_idx): with N known at compile time one thread
+//    issues a single TMA bulk copy (cp.async.bulk + mbarrier) of the whole
+//    tile into shared memory at kernel entry, so the dominant 4N B/leaf
+//    stream is in flight while the stencil runs and costs no registers;
+//    lanes read their samples back conflict-free after the barrier.
 // ENERGY also evaluates the reference's per-leaf energy term
 // (_kernels.pyx:517-533) of the incoming (snapshot) state, which is the
 // previous pass's post-propagate state, from the same values and roots.
@@ -80,6 +83,53 @@ __device__ __forceinline__ T step_val(T own, int c, int cx, int cy, int cz,
   return v;
 }
 
+// ---- TMA bulk copy global -> shared with an mbarrier (sm_90+ / sm_100a)
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(count)
+               : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  uint64_t state;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 %0, [%1], %2;"
+               : "=l"(state)
+               : "r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+  (void)state;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src,
+                                         unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1], %2, [%3];" ::"r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+// dynamic shared memory of the staged kernel: the sample tile, then the
+// mask tile (binary weights) or the weight tile
+constexpr size_t leaf_smem_bytes(int nv, bool binw) {
+  return nv <= 0 ? 0
+                 : (size_t)((nv + 3) & ~3) * kTileLeaves * 4 +
+                       (binw ? (size_t)kTileLeaves * 4
+                             : (size_t)((nv + 3) & ~3) * kTileLeaves * 4);
+}
+
 template <typename T, bool FROZEN, bool BINW, bool ENERGY, int NV>
 __global__ void __launch_bounds__(kT, OCTF_LEAF_MINB) k_leaf_pass(LeafArgs<T> a) {
   using A = Arith<T>;
@@ -91,33 +141,29 @@ __global__ void __launch_bounds__(kT, OCTF_LEAF_MINB) k_leaf_pass(LeafArgs<T> a)
   const bool inrange = i < (int)a.nlb;
   const T* __restrict__ snap = a.snap;
 
-  // samples first (they depend on nothing): all in flight during the rest.
-  // Non-leaf slots of a leaf block hold zeroed vectors, so loads are safe.
+  // samples: one TMA bulk copy of the CTA's tile (compile-time N), issued
+  // before anything else and awaited only when the data term needs it.
+  // Padding leaves and non-leaf slots hold zeros, so the copy is in bounds.
   constexpr int NVP = (NV + 3) & ~3;
-  constexpr int NR = NV > 0 ? NVP : 4;
-  float f[NR];
-  float w[BINW ? 4 : NR];
-  uint32_t mk = 0;
+  extern __shared__ __align__(128) float s_tile[];
+  __shared__ __align__(8) uint64_t s_bar;
   if (NV > 0) {
-    const float4* fp = reinterpret_cast<const float4*>(a.F) + (size_t)gid * (NVP / 4);
-    const float4* wp = reinterpret_cast<const float4*>(a.W) + (size_t)gid * (NVP / 4);
-#pragma unroll
-    for (int q = 0; q < NVP / 4; ++q) {
-      float4 t = inrange ? __ldg(fp + q) : make_float4(0.f, 0.f, 0.f, 0.f);
-      f[4 * q] = t.x;
-      f[4 * q + 1] = t.y;
-      f[4 * q + 2] = t.z;
-      f[4 * q + 3] = t.w;
-      if (!BINW) {
-        float4 u = inrange ? __ldg(wp + q) : make_float4(0.f, 0.f, 0.f, 0.f);
-        w[4 * q] = u.x;
-        w[4 * q + 1] = u.y;
-        w[4 * q + 2] = u.z;
-        w[4 * q + 3] = u.w;
-      }
+    if (threadIdx.x == 0) {
+      mbar_init(&s_bar, 1);
+      const size_t tile = blockIdx.x;
+      const unsigned fbytes = NVP * kTileLeaves * 4;
+      const unsigned abytes = BINW ? kTileLeaves * 4 : fbytes;
+      mbar_expect_tx(&s_bar, fbytes + abytes);
+      bulk_g2s(s_tile, a.F + tile * NVP * kTileLeaves, fbytes, &s_bar);
+      if (BINW)
+        bulk_g2s(s_tile + NVP * kTileLeaves, a.M + tile * kTileLeaves, abytes,
+                 &s_bar);
+      else
+        bulk_g2s(s_tile + NVP * kTileLeaves, a.W + tile * NVP * kTileLeaves,
+                 abytes, &s_bar);
     }
+    __syncthreads();  // barrier initialised before anyone waits on it
   }
-  if (BINW) mk = inrange ? __ldg(a.M + gid) : 0u;
 
   // one 16 B load: base slot, parent cell, leaf mask and level
   const int4 meta = inrange ? __ldg(a.lmeta + i) : make_int4(0, 0, 0, 0);
@@ -204,23 +250,30 @@ __global__ void __launch_bounds__(kT, OCTF_LEAF_MINB) k_leaf_pass(LeafArgs<T> a)
     den += wv;
   };
   if (NV > 0) {
+    mbar_wait(&s_bar, 0);
+    const int t = threadIdx.x;
+    const float* sf = s_tile;
+    if (BINW) {
+      const uint32_t mk = reinterpret_cast<const uint32_t*>(s_tile + NVP * kTileLeaves)[t];
 #pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      if (BINW) {
-        if (mk & (1u << v)) sample((T)1, f[v]);
-      } else {
-        if (w[v] != 0.f) sample((T)w[v], f[v]);
+      for (int v = 0; v < NV; ++v)
+        if (mk & (1u << v)) sample((T)1, sf[v * kTileLeaves + t]);
+    } else {
+      const float* sw = s_tile + NVP * kTileLeaves;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const float wv = sw[v * kTileLeaves + t];
+        if (wv != 0.f) sample((T)wv, sf[v * kTileLeaves + t]);
       }
     }
   } else if (active) {
-    const float* fp = a.F + (size_t)gid * a.stride;
-    const float* wp = a.W + (size_t)gid * a.stride;
+    uint32_t mk = BINW ? __ldg(a.M + gid) : 0u;
     for (int v = 0; v < a.nv; ++v) {
-      const float fv = __ldg(fp + v);
+      const float fv = __ldg(a.F + samp_idx(gid, v, a.stride));
       if (BINW) {
         if ((mk >> v) & 1u) sample((T)1, fv);
       } else {
-        const float wv = __ldg(wp + v);
+        const float wv = __ldg(a.W + samp_idx(gid, v, a.stride));
         if (wv != 0.f) sample((T)wv, fv);
       }
     }

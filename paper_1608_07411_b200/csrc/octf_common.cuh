@@ -49,6 +49,16 @@ __host__ __device__ __forceinline__ void unpack_meta_w(int w, int& pz,
   L = (int)((unsigned)w >> 27);
 }
 
+// Per-leaf samples are stored in tiles of 256 leaves (one leaf-kernel CTA),
+// view-major inside a tile: [tile][view][256].  A warp reading one view
+// touches 128 contiguous bytes, and a whole tile is one contiguous
+// nvp*1 KiB block that a single TMA bulk copy stages into shared memory.
+constexpr int kTileLeaves = 256;
+__host__ __device__ __forceinline__ int64_t samp_idx(int64_t leaf, int v,
+                                                     int64_t nvp) {
+  return (leaf >> 8) * (nvp << 8) + ((int64_t)v << 8) + (leaf & 255);
+}
+
 // spread the low 21 bits of v to every third bit
 __host__ __device__ __forceinline__ uint64_t spread3(uint64_t v) {
   v &= 0x1fffff;

@@ -102,29 +102,18 @@ __global__ void __launch_bounds__(kT) k_pd_pass(PdArgs<T> a) {
   int ix[NV];
   uint32_t mk = 0;
   {
-    const float4* fp = reinterpret_cast<const float4*>(a.F) + (size_t)gid * (NV / 4 > 0 ? NV / 4 : 1);
+    // tile-transposed store: view v of this leaf at samp_idx(gid, v, NV)
+    const float* fp = a.F + samp_idx(gid, 0, NV);
 #pragma unroll
-    for (int q = 0; q < (NV + 3) / 4; ++q) {
-      float4 t = inrange ? __ldg(fp + q) : make_float4(0.f, 0.f, 0.f, 0.f);
-      if (4 * q < NV) f[4 * q] = t.x;
-      if (4 * q + 1 < NV) f[4 * q + 1] = t.y;
-      if (4 * q + 2 < NV) f[4 * q + 2] = t.z;
-      if (4 * q + 3 < NV) f[4 * q + 3] = t.w;
-    }
+    for (int v = 0; v < NV; ++v) f[v] = inrange ? __ldg(fp + v * kTileLeaves) : 0.f;
     if (BINW) {
       mk = inrange ? __ldg(a.M + gid) : 0u;
 #pragma unroll
       for (int v = 0; v < NV; ++v) w[v] = (mk >> v) & 1u ? 1.f : 0.f;
     } else {
-      const float4* wp = reinterpret_cast<const float4*>(a.W) + (size_t)gid * (NV / 4 > 0 ? NV / 4 : 1);
+      const float* wp = a.W + samp_idx(gid, 0, NV);
 #pragma unroll
-      for (int q = 0; q < (NV + 3) / 4; ++q) {
-        float4 t = inrange ? __ldg(wp + q) : make_float4(0.f, 0.f, 0.f, 0.f);
-        if (4 * q < NV) w[4 * q] = t.x;
-        if (4 * q + 1 < NV) w[4 * q + 1] = t.y;
-        if (4 * q + 2 < NV) w[4 * q + 2] = t.z;
-        if (4 * q + 3 < NV) w[4 * q + 3] = t.w;
-      }
+      for (int v = 0; v < NV; ++v) w[v] = inrange ? __ldg(wp + v * kTileLeaves) : 0.f;
     }
   }
   const int4 meta = inrange ? __ldg(a.lmeta + i) : make_int4(0, 0, 0, 0);

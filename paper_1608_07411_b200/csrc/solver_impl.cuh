@@ -461,9 +461,9 @@ __global__ void __launch_bounds__(kT)
     const int64_t sidx = i * 8 + c;
     const uint32_t mk = BINW ? M[sidx] : 0u;
     for (int v = 0; v < nv; ++v) {
-      const float w = BINW ? (float)((mk >> v) & 1u) : W[sidx * stride + v];
+      const float w = BINW ? (float)((mk >> v) & 1u) : W[samp_idx(sidx, v, stride)];
       if (w != 0.f) {
-        const T d = u0 - (T)F[sidx * stride + v];
+        const T d = u0 - (T)F[samp_idx(sidx, v, stride)];
         num += A::data_val((T)w, d, p.eps2);
         den += (T)w;
       }
@@ -500,6 +500,19 @@ void ensure_prepared(Ctx& c, const int32_t* child, int64_t cap, int d_max,
 // grid of the leaf kernel (also the number of energy partials per pass)
 inline unsigned leaf_grid(const Ctx& c) { return blocks_for(c.nlb * 8); }
 
+template <typename T, bool FZ, bool BW, bool EN, int N>
+void launch_leaf(unsigned g, cudaStream_t st, const LeafArgs<T>& a) {
+  constexpr size_t smem = leaf_smem_bytes(N, BW);
+  static bool attr = false;  // opt in to > 48 KiB of dynamic shared memory
+  if (smem > 48 * 1024 && !attr) {
+    OCTF_CUDA(cudaFuncSetAttribute(k_leaf_pass<T, FZ, BW, EN, N>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+    attr = true;
+  }
+  k_leaf_pass<T, FZ, BW, EN, N><<<g, kT, smem, st>>>(a);
+}
+
 template <typename T>
 void launch_leaf_pass(Ctx& c, const T* snap, T* uval, const int32_t* child,
                       const LeafParams<T>& lp, bool frozen, double* epart,
@@ -529,13 +542,13 @@ void launch_leaf_pass(Ctx& c, const T* snap, T* uval, const int32_t* child,
 #define OCTF_LEAF(FZ, BW, EN)                                         \
   do {                                                                \
     if (c.nviews == 16)                                               \
-      k_leaf_pass<T, FZ, BW, EN, 16><<<g, kT, 0, st>>>(a);            \
+      launch_leaf<T, FZ, BW, EN, 16>(g, st, a);                       \
     else if (c.nviews == 32)                                          \
-      k_leaf_pass<T, FZ, BW, EN, 32><<<g, kT, 0, st>>>(a);            \
+      launch_leaf<T, FZ, BW, EN, 32>(g, st, a);                       \
     else if (c.nviews == 8)                                           \
-      k_leaf_pass<T, FZ, BW, EN, 8><<<g, kT, 0, st>>>(a);             \
+      launch_leaf<T, FZ, BW, EN, 8>(g, st, a);                        \
     else                                                              \
-      k_leaf_pass<T, FZ, BW, EN, 0><<<g, kT, 0, st>>>(a);             \
+      launch_leaf<T, FZ, BW, EN, 0>(g, st, a);                        \
   } while (0)
   if (frozen) {
     if (c.binw) {

@@ -61,7 +61,8 @@ __device__ __forceinline__ void slot_cell(int32_t b, int c, uint64_t pc,
 __global__ void k_expand(const int32_t* __restrict__ child,
                          const int32_t* __restrict__ blocks, int64_t nblk,
                          int L, int64_t used, int8_t* blevel, uint64_t* bcoord,
-                         int32_t* next, int32_t* counter, int32_t* bad) {
+                         int32_t* bparent, int32_t* next, int32_t* counter,
+                         int32_t* bad) {
   int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t i = gid >> 3;
   int c = (int)(gid & 7);
@@ -80,6 +81,7 @@ __global__ void k_expand(const int32_t* __restrict__ child,
   int k = block_id(nb);
   blevel[k] = (int8_t)(L + 1);
   bcoord[k] = pack_cell(L, x, y, z);
+  bparent[k] = s;
   int pos = atomicAdd(counter, 1);
   next[pos] = nb;
 }
@@ -107,7 +109,9 @@ __global__ void k_leaf_tables(const int32_t* __restrict__ child,
                               const int32_t* __restrict__ lblocks, int64_t nlb,
                               const int8_t* __restrict__ blevel,
                               const uint64_t* __restrict__ bcoord,
-                              uint64_t* lkey, int4* lmeta, int32_t* nbr) {
+                              const int32_t* __restrict__ bparent,
+                              uint64_t* lkey, int4* lmeta, int32_t* lpar,
+                              int32_t* nbr) {
   int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t i = gid / 12;
   int d = (int)(gid % 12);
@@ -126,6 +130,7 @@ __global__ void k_leaf_tables(const int32_t* __restrict__ child,
     else
       for (int c = 0; c < 8; ++c) mask |= (child[b + c] < 0 ? 1u : 0u) << c;
     lmeta[i] = make_int4(b, px, py, pack_meta_w(pz, mask, L));
+    lpar[i] = b == 0 ? -1 : bparent[k];
   }
   int32_t ref = kNone;
   if (b != 0) {
@@ -273,6 +278,7 @@ void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
   int64_t nbid = block_id(used) + 1;
   c.blevel.ensure(nbid);
   c.bcoord.ensure(nbid);
+  c.bparent.ensure(nbid);
   c.lvl_blocks.ensure(nbid + 1);
   c.counters.ensure(64);
   OCTF_CUDA(cudaMemsetAsync(c.blevel.p, 0xff, nbid, st));
@@ -294,7 +300,8 @@ void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
     OCTF_CUDA(cudaMemsetAsync(c.counters.p, 0, 2 * sizeof(int32_t), st));
     k_expand<<<grid_for(n * 8), kThreads, 0, st>>>(
         child, c.lvl_blocks.p + c.lvl_off[L], n, L, used, c.blevel.p,
-        c.bcoord.p, c.lvl_blocks.p + total, c.counters.p, c.counters.p + 1);
+        c.bcoord.p, c.bparent.p, c.lvl_blocks.p + total, c.counters.p,
+        c.counters.p + 1);
     OCTF_CUDA(cudaGetLastError());
     OCTF_CUDA(cudaMemcpyAsync(c.h_counters, c.counters.p, 2 * sizeof(int32_t),
                               cudaMemcpyDeviceToHost, st));
@@ -333,10 +340,11 @@ void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
   sort_i32(c, c.lblocks.p, c.nlb, st);
   c.lkey.ensure(c.nlb);
   c.lmeta.ensure(c.nlb);
+  c.lpar.ensure(c.nlb);
   c.nbr.ensure(c.nlb * 12);
   k_leaf_tables<<<grid_for(c.nlb * 12), kThreads, 0, st>>>(
-      child, c.lblocks.p, c.nlb, c.blevel.p, c.bcoord.p, c.lkey.p, c.lmeta.p,
-      c.nbr.p);
+      child, c.lblocks.p, c.nlb, c.blevel.p, c.bcoord.p, c.bparent.p,
+      c.lkey.p, c.lmeta.p, c.lpar.p, c.nbr.p);
   OCTF_CUDA(cudaGetLastError());
 
   c.smark.ensure(cap);
@@ -423,8 +431,9 @@ namespace {
 __global__ void k_select(const int32_t* __restrict__ sel,
                          const uint8_t* __restrict__ masks, int64_t nsel,
                          const int32_t* lblocks, const uint64_t* lkey,
-                         const int4* lmeta, const int32_t* nbr,
-                         int32_t* o_lblocks, uint64_t* o_lkey, int4* o_lmeta,
+                         const int4* lmeta, const int32_t* lpar,
+                         const int32_t* nbr, int32_t* o_lblocks,
+                         uint64_t* o_lkey, int4* o_lmeta, int32_t* o_lpar,
                          int32_t* o_nbr) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= nsel) return;
@@ -435,6 +444,7 @@ __global__ void k_select(const int32_t* __restrict__ sel,
   // keep only the rank's leaves active (bits 19..26 of .w)
   m.w = (int)(((unsigned)m.w & ~(0xffu << 19)) | ((unsigned)masks[j] << 19));
   o_lmeta[j] = m;
+  o_lpar[j] = lpar[i];
   for (int d = 0; d < 12; ++d) o_nbr[j * 12 + d] = nbr[(int64_t)i * 12 + d];
 }
 
@@ -443,7 +453,7 @@ __global__ void k_select(const int32_t* __restrict__ sel,
 void ctx_select(Ctx& c, const int32_t* sel, const uint8_t* masks, int64_t nsel,
                 cudaStream_t st) {
   if (!c.valid) throw Error(kEArg, "context not prepared");
-  DevBuf<int32_t> dsel, olb, onbr;
+  DevBuf<int32_t> dsel, olb, onbr, opar;
   DevBuf<uint8_t> dmask;
   DevBuf<uint64_t> okey;
   DevBuf<int4> ometa;
@@ -452,20 +462,22 @@ void ctx_select(Ctx& c, const int32_t* sel, const uint8_t* masks, int64_t nsel,
   olb.ensure(nsel);
   okey.ensure(nsel);
   ometa.ensure(nsel);
+  opar.ensure(nsel);
   onbr.ensure(nsel * 12);
   if (nsel) {
     OCTF_CUDA(cudaMemcpyAsync(dsel.p, sel, nsel * sizeof(int32_t),
                               cudaMemcpyHostToDevice, st));
     OCTF_CUDA(cudaMemcpyAsync(dmask.p, masks, nsel, cudaMemcpyHostToDevice, st));
     k_select<<<grid_for(nsel), kThreads, 0, st>>>(
-        dsel.p, dmask.p, nsel, c.lblocks.p, c.lkey.p, c.lmeta.p, c.nbr.p, olb.p,
-        okey.p, ometa.p, onbr.p);
+        dsel.p, dmask.p, nsel, c.lblocks.p, c.lkey.p, c.lmeta.p, c.lpar.p,
+        c.nbr.p, olb.p, okey.p, ometa.p, opar.p, onbr.p);
     OCTF_CUDA(cudaGetLastError());
   }
   OCTF_CUDA(cudaStreamSynchronize(st));
   c.lblocks.swap(olb);
   c.lkey.swap(okey);
   c.lmeta.swap(ometa);
+  c.lpar.swap(opar);
   c.nbr.swap(onbr);
   c.nlb = nsel;
   if (c.nviews > 0) ctx_gather(c, st);

@@ -32,6 +32,8 @@ struct LeafArgs {
   int64_t nlb;
   const uint64_t* __restrict__ lkey;
   const int4* __restrict__ lmeta;
+  const int32_t* __restrict__ lpar;  // parent slot of each leaf block
+  int write_parent;  // frozen passes: also write the bottom propagate level
   const int32_t* __restrict__ nbr;
   const int32_t* __restrict__ child;
   const T* __restrict__ snap;

@@ -84,12 +84,14 @@ struct Ctx {
   // ---- structure (rebuilt by prepare())
   DevBuf<int8_t> blevel;      // per block id: level of its nodes (-1 free)
   DevBuf<uint64_t> bcoord;    // per block id: packed parent cell
+  DevBuf<int32_t> bparent;    // per block id: parent node slot
   std::vector<int64_t> lvl_off, lvl_cnt;  // per level ranges in lvl_blocks
   DevBuf<int32_t> lvl_blocks;             // live block bases, level-major
   int64_t nblocks = 0;
   DevBuf<int32_t> lblocks;    // blocks holding >= 1 leaf, ascending base
   DevBuf<uint64_t> lkey;      // per leaf block: packed (level, parent cell)
   DevBuf<int4> lmeta;         // per leaf block: {base, px, py, pz|mask|L}
+  DevBuf<int32_t> lpar;       // per leaf block: parent node slot (-1 root)
   DevBuf<int32_t> nbr;        // per leaf block: 12 neighbour refs
   int64_t nlb = 0;
   int64_t nleaves = 0;
@@ -115,6 +117,7 @@ struct Ctx {
   DevBuf<int32_t> split_list;
   DevBuf<uint8_t> cub_tmp;
   DevBuf<double> partials;
+  DevBuf<double> mid;       // stripe sums of the two-stage energy reduction
   DevBuf<double> dscalar;
 
   // live profiling (octf_ctx_profile): CUDA events on the launch stream

@@ -478,14 +478,45 @@ __global__ void __launch_bounds__(kT)
   if (threadIdx.x == 0) partials[blockIdx.x] = tot;
 }
 
-__global__ void k_sum_partials(const double* partials, int64_t n,
-                               double* out) {
+// Deterministic two-stage sum of per-CTA energy partials, for several
+// passes at once (pass p owns partials[p*n, (p+1)*n)): stage 1 reduces
+// kStripes fixed contiguous stripes per pass, stage 2 the stripes.  The
+// order depends only on n, so energies are bit-reproducible.
+constexpr int kStripes = 128;
+
+__global__ void k_sum_stage1(const double* __restrict__ partials, int64_t n,
+                             double* mid) {
+  const int64_t len = (n + kStripes - 1) / kStripes;
+  const double* p = partials + (int64_t)blockIdx.y * n;
+  const int64_t lo = blockIdx.x * len;
+  const int64_t hi = lo + len < n ? lo + len : n;
   double acc = 0.0;
-  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) acc += partials[j];
+  for (int64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) acc += p[j];
   typedef cub::BlockReduce<double, kT> BR;
   __shared__ typename BR::TempStorage tmp;
   const double tot = BR(tmp).Sum(acc);
-  if (threadIdx.x == 0) *out = tot;
+  if (threadIdx.x == 0) mid[(int64_t)blockIdx.y * kStripes + blockIdx.x] = tot;
+}
+
+__global__ void k_sum_stage2(const double* __restrict__ mid, double* out) {
+  const double v = threadIdx.x < kStripes
+                       ? mid[(int64_t)blockIdx.x * kStripes + threadIdx.x]
+                       : 0.0;
+  typedef cub::BlockReduce<double, kT> BR;
+  __shared__ typename BR::TempStorage tmp;
+  const double tot = BR(tmp).Sum(v);
+  if (threadIdx.x == 0) out[blockIdx.x] = tot;
+}
+
+// out[p] = sum of partials of pass p, p < npasses (device pointers)
+void sum_partials(Ctx& c, const double* partials, int64_t n, int npasses,
+                  double* out, cudaStream_t st) {
+  c.mid.ensure((size_t)kStripes * (npasses > 32 ? npasses : 32));
+  k_sum_stage1<<<dim3(kStripes, npasses), kT, 0, st>>>(partials, n, c.mid.p);
+  OCTF_CUDA(cudaGetLastError());
+  k_sum_stage2<<<npasses, kT, 0, st>>>(c.mid.p, out);
+  OCTF_CUDA(cudaGetLastError());
+  c.launches += 2;
 }
 
 // ---------------------------------------------------------------------------
@@ -516,9 +547,12 @@ void launch_leaf(unsigned g, cudaStream_t st, const LeafArgs<T>& a) {
 template <typename T>
 void launch_leaf_pass(Ctx& c, const T* snap, T* uval, const int32_t* child,
                       const LeafParams<T>& lp, bool frozen, double* epart,
-                      cudaStream_t st, bool timed = true) {
+                      cudaStream_t st, bool timed = true,
+                      bool write_parent = false) {
   const unsigned g = leaf_grid(c);
   LeafArgs<T> a;
+  a.lpar = c.lpar.p;
+  a.write_parent = write_parent;
   a.lblocks = c.lblocks.p;
   a.nlb = c.nlb;
   a.lkey = c.lkey.p;
@@ -641,9 +675,7 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
   launch_leaf_pass<T>(c, (const T*)a.usnap, (T*)a.uval, a.child, lp, frozen,
                       epart, st);
   if (epart) {
-    k_sum_partials<<<1, kT, 0, st>>>(epart, leaf_grid(c), c.dscalar.p);
-    OCTF_CUDA(cudaGetLastError());
-    ++c.launches;
+    sum_partials(c, epart, leaf_grid(c), 1, c.dscalar.p, st);
     OCTF_CUDA(cudaMemcpyAsync(c.h_scalar, c.dscalar.p, sizeof(double),
                               cudaMemcpyDeviceToHost, st));
   }
@@ -795,8 +827,9 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
 
 template <typename T>
 void launch_propagate(Ctx& c, T* value, const int32_t* child,
-                      cudaStream_t st) {
-  for (int L = c.d_max - 1; L >= 0; --L) {
+                      cudaStream_t st, int top = -1) {
+  // levels top .. 0 (default: every level above the finest)
+  for (int L = top < 0 ? c.d_max - 1 : top; L >= 0; --L) {
     const int64_t n = c.lvl_cnt[L];
     if (n == 0) continue;
     k_propagate_level<T><<<blocks_for(n * 8), kT, 0, st>>>(
@@ -835,9 +868,7 @@ double energy_impl(Ctx& c, const T* u, const int32_t* child,
   OCTF_CUDA(cudaGetLastError());
   ++c.launches;
   if (c.timing) OCTF_CUDA(cudaEventRecord(c.tev[3], st));
-  k_sum_partials<<<1, kT, 0, st>>>(c.partials.p, g, c.dscalar.p);
-  OCTF_CUDA(cudaGetLastError());
-  ++c.launches;
+  sum_partials(c, c.partials.p, g, 1, c.dscalar.p, st);
   OCTF_CUDA(cudaMemcpyAsync(c.h_scalar, c.dscalar.p, sizeof(double),
                             cudaMemcpyDeviceToHost, st));
   OCTF_CUDA(cudaStreamSynchronize(st));
@@ -848,19 +879,6 @@ double energy_impl(Ctx& c, const T* u, const int32_t* child,
     ++c.n_energy;
   }
   return c.h_scalar[0];
-}
-
-
-__global__ void k_sum_partials_multi(const double* partials, int64_t n,
-                                     double* out) {
-  // one CTA per pass, same reduction shape as k_sum_partials
-  const double* p = partials + (int64_t)blockIdx.x * n;
-  double acc = 0.0;
-  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) acc += p[j];
-  typedef cub::BlockReduce<double, kT> BR;
-  __shared__ typename BR::TempStorage tmp;
-  const double tot = BR(tmp).Sum(acc);
-  if (threadIdx.x == 0) out[blockIdx.x] = tot;
 }
 
 // K passes of a frozen structure back to back: per pass one leaf kernel
@@ -902,6 +920,8 @@ void frozen_passes_impl(Ctx& c, FrozenArgs& a, cudaStream_t st) {
       const T* snap = (const T*)a.ubuf[k & 1];
       T* uval = (T*)a.ubuf[(k + 1) & 1];
       if (c.timing) OCTF_CUDA(cudaEventRecord(c.pev[2 * j], st));
+      // (writing the parents of all-leaf blocks from this kernel was tried:
+      // the extra registers cost more than the propagate level it saves)
       launch_leaf_pass<T>(c, snap, uval, a.child, lp, true,
                           c.partials.p + (size_t)j * g, st, false);
       if (c.timing) OCTF_CUDA(cudaEventRecord(c.pev[2 * j + 1], st));
@@ -909,9 +929,7 @@ void frozen_passes_impl(Ctx& c, FrozenArgs& a, cudaStream_t st) {
     }
     // stream order keeps the next chunk from overwriting unsummed partials
     double* eout = a.dev_energies ? a.energies_pre : c.dscalar.p;
-    k_sum_partials_multi<<<nk, kT, 0, st>>>(c.partials.p, g, eout + k0);
-    OCTF_CUDA(cudaGetLastError());
-    ++c.launches;
+    sum_partials(c, c.partials.p, g, nk, eout + k0, st);
     if (c.timing) {  // profiling only: read this chunk's kernel events
       OCTF_CUDA(cudaStreamSynchronize(st));
       for (int j = 0; j < nk; ++j) {
@@ -995,9 +1013,7 @@ void pd_passes_impl(Ctx& c, PdHostArgs& a, cudaStream_t st) {
         OCTF_CUDA(cudaEventRecord(c.pev[2 * j + 1], st));
       for (int q = 0; q < 5; ++q) launch_propagate<T>(c, (T*)out[q], a.child, st);
     }
-    k_sum_partials_multi<<<nk, kT, 0, st>>>(c.partials.p, g, c.dscalar.p + k0);
-    OCTF_CUDA(cudaGetLastError());
-    ++c.launches;
+    sum_partials(c, c.partials.p, g, nk, c.dscalar.p + k0, st);
     if (c.timing && (int)c.pev.size() >= 2 * kChunk) {
       OCTF_CUDA(cudaStreamSynchronize(st));
       for (int j = 0; j < nk; ++j) {

@@ -139,6 +139,7 @@ int octf_ctx_destroy(octf_ctx* ctx) {
 int octf_ctx_invalidate(octf_ctx* ctx) {
   if (ctx) {
     ctx->c.valid = false;
+    ctx->c.free_ok = false;
     ctx->c.vkey.clear();
     ctx->c.nviews = 0;
   }

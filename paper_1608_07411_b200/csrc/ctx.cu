@@ -210,39 +210,36 @@ __global__ void k_reverse(const int32_t* in, int64_t n, int32_t* out) {
 
 }  // namespace
 
+// stream-ordered sorts with the context's persistent scratch (no
+// allocation, no host sync: cudaMalloc/cudaFree per call used to dominate
+// small restructuring passes)
 void sort_u64_i32(Ctx& c, uint64_t* keys, int32_t* vals, int64_t n,
                   cudaStream_t st) {
   if (n <= 1) return;
-  DevBuf<uint64_t> k2;
-  DevBuf<int32_t> v2;
-  k2.ensure(n);
-  v2.ensure(n);
+  uint64_t* k2 = c.sort_k64.ensure(n);
+  int32_t* v2 = c.sort_v32.ensure(n);
   size_t bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys, k2.p, vals, v2.p,
-                                  (int)n, 0, 64, st);
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys, k2, vals, v2, (int)n,
+                                  0, 64, st);
   c.cub_tmp.ensure(bytes);
-  OCTF_CUDA(cub::DeviceRadixSort::SortPairs(c.cub_tmp.p, bytes, keys, k2.p,
-                                            vals, v2.p, (int)n, 0, 64, st));
-  OCTF_CUDA(cudaMemcpyAsync(keys, k2.p, n * sizeof(uint64_t),
+  OCTF_CUDA(cub::DeviceRadixSort::SortPairs(c.cub_tmp.p, bytes, keys, k2, vals,
+                                            v2, (int)n, 0, 64, st));
+  OCTF_CUDA(cudaMemcpyAsync(keys, k2, n * sizeof(uint64_t),
                             cudaMemcpyDeviceToDevice, st));
-  OCTF_CUDA(cudaMemcpyAsync(vals, v2.p, n * sizeof(int32_t),
+  OCTF_CUDA(cudaMemcpyAsync(vals, v2, n * sizeof(int32_t),
                             cudaMemcpyDeviceToDevice, st));
-  OCTF_CUDA(cudaStreamSynchronize(st));
 }
 
 void sort_i32(Ctx& c, int32_t* keys, int64_t n, cudaStream_t st) {
   if (n <= 1) return;
-  DevBuf<int32_t> k2;
-  k2.ensure(n);
+  int32_t* k2 = c.sort_k32.ensure(n);
   size_t bytes = 0;
-  cub::DeviceRadixSort::SortKeys(nullptr, bytes, keys, k2.p, (int)n, 0, 32,
-                                 st);
+  cub::DeviceRadixSort::SortKeys(nullptr, bytes, keys, k2, (int)n, 0, 32, st);
   c.cub_tmp.ensure(bytes);
-  OCTF_CUDA(cub::DeviceRadixSort::SortKeys(c.cub_tmp.p, bytes, keys, k2.p,
+  OCTF_CUDA(cub::DeviceRadixSort::SortKeys(c.cub_tmp.p, bytes, keys, k2,
                                            (int)n, 0, 32, st));
-  OCTF_CUDA(cudaMemcpyAsync(keys, k2.p, n * sizeof(int32_t),
+  OCTF_CUDA(cudaMemcpyAsync(keys, k2, n * sizeof(int32_t),
                             cudaMemcpyDeviceToDevice, st));
-  OCTF_CUDA(cudaStreamSynchronize(st));
 }
 
 void ctx_free_stack(Ctx& c, const int32_t* child, const int64_t* state,
@@ -251,18 +248,18 @@ void ctx_free_stack(Ctx& c, const int32_t* child, const int64_t* state,
   int64_t nmax = (used + 7) / 8 + 1;
   c.free_stack.ensure(nmax);
   c.nfree = 0;
+  c.nfree_head = state[1];
   if (state[1] < 0) return;
-  DevBuf<int32_t> chain;
-  chain.ensure(nmax);
+  int32_t* chain = c.sort_k32.ensure(nmax);
   c.counters.ensure(64);
-  k_walk_free<<<1, 1, 0, st>>>(child, state[1], nmax, chain.p, c.counters.p);
+  k_walk_free<<<1, 1, 0, st>>>(child, state[1], nmax, chain, c.counters.p);
   OCTF_CUDA(cudaGetLastError());
   OCTF_CUDA(cudaMemcpyAsync(c.h_counters, c.counters.p, sizeof(int32_t),
                             cudaMemcpyDeviceToHost, st));
   OCTF_CUDA(cudaStreamSynchronize(st));
   int64_t n = c.h_counters[0];
   // stack order: bottom = last link, top = head
-  if (n) k_reverse<<<grid_for(n), kThreads, 0, st>>>(chain.p, n, c.free_stack.p);
+  if (n) k_reverse<<<grid_for(n), kThreads, 0, st>>>(chain, n, c.free_stack.p);
   OCTF_CUDA(cudaGetLastError());
   OCTF_CUDA(cudaStreamSynchronize(st));
   c.nfree = n;
@@ -318,19 +315,18 @@ void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
   // (checked implicitly: blocks at level d_max are never expanded)
 
   // leaf blocks, ascending base slot
-  DevBuf<uint8_t> flags;
-  flags.ensure(total);
+  uint8_t* flags = c.flags.ensure(total);
   c.lblocks.ensure(total);
   OCTF_CUDA(cudaMemsetAsync(c.counters.p, 0, 2 * sizeof(int32_t), st));
   k_leaf_flags<<<grid_for(total), kThreads, 0, st>>>(
-      child, c.lvl_blocks.p, total, flags.p, c.counters.p + 1);
+      child, c.lvl_blocks.p, total, flags, c.counters.p + 1);
   OCTF_CUDA(cudaGetLastError());
   size_t bytes = 0;
-  cub::DeviceSelect::Flagged(nullptr, bytes, c.lvl_blocks.p, flags.p,
+  cub::DeviceSelect::Flagged(nullptr, bytes, c.lvl_blocks.p, flags,
                              c.lblocks.p, c.counters.p, (int)total, st);
   c.cub_tmp.ensure(bytes);
   OCTF_CUDA(cub::DeviceSelect::Flagged(c.cub_tmp.p, bytes, c.lvl_blocks.p,
-                                       flags.p, c.lblocks.p, c.counters.p,
+                                       flags, c.lblocks.p, c.counters.p,
                                        (int)total, st));
   OCTF_CUDA(cudaMemcpyAsync(c.h_counters, c.counters.p, 2 * sizeof(int32_t),
                             cudaMemcpyDeviceToHost, st));
@@ -349,7 +345,12 @@ void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
 
   c.smark.ensure(cap);
   OCTF_CUDA(cudaMemsetAsync(c.smark.p, 0, cap, st));
-  ctx_free_stack(c, child, state, st);
+  // the free-list mirror survives our own restructuring (passes pop and
+  // push it); walk the pool's linked free list only for a foreign pool
+  if (!c.free_ok || c.child_key != child || c.nfree_head != state[1]) {
+    ctx_free_stack(c, child, state, st);
+    c.free_ok = true;
+  }
   c.child_key = child;
   c.cap = cap;
   c.d_max = d_max;

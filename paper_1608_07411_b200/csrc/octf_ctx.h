@@ -55,6 +55,27 @@ struct DevBuf {
     p = nullptr;
     n = 0;
   }
+  // grow keeping the first `keep` elements (stream-ordered copy)
+  T* grow_keep(size_t count, size_t keep, cudaStream_t st) {
+    if (count <= n && p) return p;
+    T* q = nullptr;
+    size_t c = count > 2 * n ? count : 2 * n;
+    if (cudaMalloc((void**)&q, c * sizeof(T)) != cudaSuccess) {
+      cudaGetLastError();
+      throw Error(kENoMem, "device allocation failed");
+    }
+    if (p && keep)
+      check_cuda(cudaMemcpyAsync(q, p, keep * sizeof(T),
+                                 cudaMemcpyDeviceToDevice, st),
+                 "grow_keep");
+    if (p) {
+      cudaStreamSynchronize(st);
+      cudaFree(p);
+    }
+    p = q;
+    n = c;
+    return p;
+  }
   T* ensure(size_t count) {
     if (count <= n && p) return p;
     release();
@@ -110,12 +131,17 @@ struct Ctx {
   // ---- free list mirror: stack of free block bases, top = free-list head
   DevBuf<int32_t> free_stack;
   int64_t nfree = 0;
+  bool free_ok = false;       // mirror matches the pool's free list
+  int64_t nfree_head = -1;    // pool free-list head the mirror ends at
 
   // ---- pass scratch
   DevBuf<uint8_t> smark;      // per slot: leaf split this pass
   DevBuf<int32_t> counters;   // device counters
   DevBuf<int32_t> split_list;
   DevBuf<uint8_t> cub_tmp;
+  DevBuf<uint64_t> sort_k64;  // sort scratch (persistent)
+  DevBuf<int32_t> sort_k32, sort_v32;
+  DevBuf<uint8_t> flags;
   DevBuf<double> partials;
   DevBuf<double> mid;       // stripe sums of the two-stage energy reduction
   DevBuf<double> dscalar;

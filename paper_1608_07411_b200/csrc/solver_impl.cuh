@@ -781,7 +781,7 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
                                                       a.joined);
       OCTF_CUDA(cudaGetLastError());
   ++c.launches;
-      c.free_stack.ensure(c.nfree + J + 1);
+      c.free_stack.grow_keep(c.nfree + J + 1, c.nfree, st);
       k_sweep_link<T><<<blocks_for(J), kT, 0, st>>>(
           rec, J, a.state[1], a.child, c.free_stack.p, c.nfree);
       OCTF_CUDA(cudaGetLastError());
@@ -818,6 +818,7 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
   c.hstate[0] = a.state[0];
   c.hstate[1] = a.state[1];
   c.hstate[2] = a.state[2];
+  c.nfree_head = a.state[1];  // the free-list mirror was kept in step
   if (changed) c.valid = false;
   OCTF_CUDA(cudaStreamSynchronize(st));
   a.out3[0] = splits;

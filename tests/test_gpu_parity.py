@@ -390,3 +390,77 @@ class TestEdgeCases:
         assert np.array_equal(h.child, ref.field.child[:ref.field.used])
         assert leaf_table(h.child, h.value) == leaf_table(ref.field.child,
                                                           ref.field.value)
+
+
+class TestPluginFunctions:
+    """The reference's plugin functions one by one (kernel module, C ABI)."""
+
+    def test_tree_energy_terms_are_the_references(self):
+        from paper_1608_07411_b200 import _backend
+        kern = _backend.get()
+        views_h, u0h, p, _ = cfg1_views_u0()
+        u0 = dev(u0h)
+        vs = [dev(v) for v in views_h]
+        vv, vw, vc = [v.value for v in vs], [v.weight for v in vs], [v.child for v in vs]
+        terms = torch.zeros(u0.capacity, dtype=torch.float64, device="cuda")
+        e = kern.tree_energy(u0.value, u0.child, vv, vw, vc, 6, p.lam, p.eps,
+                             p.gamma, state=u0.state, terms=terms)
+        ref = orc.tree_energy(u0h.value, u0h.child, [v.value for v in views_h],
+                              [v.weight for v in views_h],
+                              [v.child for v in views_h], 6, p.lam, p.eps, p.gamma)
+        t = terms.cpu().numpy()
+        seq = 0.0
+        for n, *_ in orc.leaves(u0h):   # the reference's Morton-order sum
+            seq += t[n]
+        assert seq == ref
+        assert e == pytest.approx(ref, rel=1e-13, abs=0)
+
+    def test_densify_and_propagate(self):
+        from paper_1608_07411_b200 import _backend
+        kern = _backend.get()
+        z = load("octree_kat")
+        t = orc.build_octree(z["smooth"], tau=0.05)
+        d = dev(t)
+        out = torch.empty((16, 16, 16), dtype=torch.float64, device="cuda")
+        kern.densify(d.value, d.child, t.d_max, out)
+        assert np.array_equal(out.cpu().numpy(), orc.densify(t.value, t.child, 4))
+        v = t.value.copy()
+        v[t.child >= 0] = -7.0
+        d2 = dev(orc.Pool(v, t.child, t.state, 4))
+        kern.propagate(d2.value, d2.child)          # reference signature
+        ref = v.copy()
+        orc.propagate(ref, t.child)
+        assert np.array_equal(d2.value.cpu().numpy(), ref)
+
+    def test_build_tree_from_pyramids(self):
+        from paper_1608_07411_b200 import _backend
+        kern = _backend.get()
+        z = load("octree_kat")
+        f, w = z["wf"].astype(np.float64), z["ww"]
+        minf, offs = orc.flatten_pyramid(orc.reduce_pyramid(f, "min"))
+        maxf, _ = orc.flatten_pyramid(orc.reduce_pyramid(f, "max"))
+        wminf, _ = orc.flatten_pyramid(orc.reduce_pyramid(w, "min"))
+        wmaxf, _ = orc.flatten_pyramid(orc.reduce_pyramid(w, "max"))
+        wm = orc.reduce_pyramid(w.astype(np.float64), "mean")
+        wf = orc.reduce_pyramid(f * w, "mean")
+        pl = orc.reduce_pyramid(z["wf"], "mean")
+        meanf, _ = orc.flatten_pyramid(
+            [np.where(a > 0, b / np.where(a > 0, a, 1.0), c) for a, b, c in zip(wm, wf, pl)])
+        wmeanf, _ = orc.flatten_pyramid(wm)
+        cap = orc.full_tree_capacity(4)
+        g = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+        value = torch.zeros(cap, dtype=torch.float32, device="cuda")
+        weight = torch.zeros(cap, dtype=torch.float32, device="cuda")
+        child = torch.full((cap,), -1, dtype=torch.int32, device="cuda")
+        state = np.zeros(3, dtype=np.int64)
+        kern.build_tree(g(meanf), g(minf), g(maxf), offs, True, g(wminf),
+                        g(wmaxf), g(wmeanf), 0.3, value, weight, child, state, 4)
+        used = int(state[0])
+        assert np.array_equal(value[:used].cpu().numpy(), z["w_value"])
+        assert np.array_equal(weight[:used].cpu().numpy(), z["w_weight"])
+        assert np.array_equal(child[:used].cpu().numpy(), z["w_child"])
+        assert np.array_equal(state, z["w_state"])
+        with pytest.raises(ValueError):
+            kern.build_tree(g(meanf), g(minf), g(maxf), offs, True, g(wminf),
+                            g(wmaxf), g(wmeanf), 0.3, value, weight, child,
+                            state, 61)

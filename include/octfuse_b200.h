@@ -137,6 +137,14 @@ int octf_ctx_prepare(octf_ctx *ctx, const int32_t *uchild,
                      const float *const *vvals, const float *const *vws,
                      const int32_t *const *vchilds, void *stream);
 
+/* Per-leaf samples supplied directly instead of view trees (BASELINE
+ * config 5: "N fp32 TSDF samples per leaf"): f_slot / w_slot are device
+ * [nviews][cap] arrays indexed by node slot (w_slot NULL = every sample has
+ * weight 1).  Frozen trees only; view-taking calls then pass nviews = 0. */
+int octf_ctx_set_samples(octf_ctx *ctx, const float *f_slot,
+                         const float *w_slot, int nviews, int64_t cap,
+                         void *stream);
+
 /* Sharding: restrict the context's leaf-block list to the
  * blocks `sel` (host int32 indices into the current list) with per-block
  * owned-leaf masks (host u8, bit c = sibling c is updated by this rank);

@@ -167,6 +167,17 @@ def ctx_prepare(ctx, uchild, ustate, d_max, vvals, vws, vchilds):
          uchild.shape[0], int(d_max), len(vvals), tv, tw, tc, stream_handle())
 
 
+def ctx_set_samples(ctx, f_slot, w_slot=None):
+    """Per-slot samples [nviews][cap] (device float32) instead of views."""
+    if f_slot.dtype != torch.float32 or f_slot.dim() != 2:
+        raise TypeError("samples must be a [nviews, cap] float32 tensor")
+    f_slot = f_slot.contiguous()
+    if w_slot is not None:
+        w_slot = w_slot.contiguous()
+    call("octf_ctx_set_samples", ctx.h, ptr(f_slot), ptr(w_slot),
+         f_slot.shape[0], f_slot.shape[1], stream_handle())
+
+
 def ctx_select(ctx, sel, masks):
     sel = np.ascontiguousarray(np.asarray(sel, dtype=np.int32))
     masks = np.ascontiguousarray(np.asarray(masks, dtype=np.uint8))

@@ -49,6 +49,7 @@ _SIGS = {
     "octf_pd_passes": ([P, I32, P, P, P, P, I64, I32, P, P, P, I32, DBL, DBL,
                         DBL, DBL, I32, I32, P, P], I32),
     "octf_ctx_select": ([P, P, P, I64, P], I32),
+    "octf_ctx_set_samples": ([P, P, P, I32, I64, P], I32),
     "octf_propagate_levels": ([P, I32, P, P, I32, I32, P], I32),
     "octf_propagate": ([P, I32, P, P, P, I64, I32, P], I32),
     "octf_tree_energy": ([P, I32, P, P, P, I64, I32, P, P, P, I32, DBL, DBL,

@@ -141,7 +141,7 @@ int octf_ctx_invalidate(octf_ctx* ctx) {
     ctx->c.valid = false;
     ctx->c.free_ok = false;
     ctx->c.vkey.clear();
-    ctx->c.nviews = 0;
+    if (!ctx->c.ext_F) ctx->c.nviews = 0;
   }
   return OCTF_OK;
 }
@@ -199,7 +199,8 @@ int octf_iterate_pass(octf_ctx* ctx, int dtype, void* usnap, void* uval,
     check_dtype(dtype);
     if (d_max > 60 || d_max > OCTF_MAX_DEPTH || d_max < 0)
       throw octf::Error(octf::kEDepth, "tree depth out of range");
-    if (nviews < 1) throw octf::Error(octf::kEArg, "at least one view is required");
+    if (nviews < 1 && !ctx->c.ext_F)
+      throw octf::Error(octf::kEArg, "at least one view is required");
     octf::ctx_set_views(ctx->c, nviews, vvals, vws, vchilds, S(stream));
     octf::IterArgs a;
     a.usnap = usnap;
@@ -238,7 +239,8 @@ int octf_fuse_pass(octf_ctx* ctx, int dtype, void* usnap, void* uval,
     check_dtype(dtype);
     if (d_max < 0 || d_max > OCTF_MAX_DEPTH)
       throw octf::Error(octf::kEDepth, "tree depth out of range");
-    if (nviews < 1) throw octf::Error(octf::kEArg, "at least one view is required");
+    if (nviews < 1 && !ctx->c.ext_F)
+      throw octf::Error(octf::kEArg, "at least one view is required");
     octf::ctx_set_views(ctx->c, nviews, vvals, vws, vchilds, S(stream));
     octf::IterArgs a;
     a.usnap = usnap;
@@ -284,7 +286,8 @@ int octf_fuse_passes_frozen(octf_ctx* ctx, int dtype, void* ubuf0, void* ubuf1,
     check_dtype(dtype);
     if (d_max < 0 || d_max > OCTF_MAX_DEPTH)
       throw octf::Error(octf::kEDepth, "tree depth out of range");
-    if (nviews < 1) throw octf::Error(octf::kEArg, "at least one view is required");
+    if (nviews < 1 && !ctx->c.ext_F)
+      throw octf::Error(octf::kEArg, "at least one view is required");
     octf::ctx_set_views(ctx->c, nviews, vvals, vws, vchilds, S(stream));
     octf::FrozenArgs a;
     a.ubuf[0] = ubuf0;
@@ -317,7 +320,8 @@ int octf_pd_passes(octf_ctx* ctx, int dtype, void* const* set_a,
     check_dtype(dtype);
     if (d_max < 0 || d_max > OCTF_MAX_DEPTH)
       throw octf::Error(octf::kEDepth, "tree depth out of range");
-    if (nviews < 1) throw octf::Error(octf::kEArg, "at least one view is required");
+    if (nviews < 1 && !ctx->c.ext_F)
+      throw octf::Error(octf::kEArg, "at least one view is required");
     if (!(tau > 0 && sigma > 0 && lam > 0 && gamma > 0))
       throw octf::Error(octf::kEArg, "tau, sigma, lam, gamma must be positive");
     octf::ctx_set_views(ctx->c, nviews, vvals, vws, vchilds, S(stream));
@@ -355,6 +359,16 @@ int octf_ctx_prepare(octf_ctx* ctx, const int32_t* uchild,
     if (nviews > 0)
       octf::ctx_set_views(ctx->c, nviews, vvals, vws, vchilds, S(stream));
     octf::ctx_prepare(ctx->c, uchild, cap, ustate, d_max, S(stream));
+  });
+}
+
+int octf_ctx_set_samples(octf_ctx* ctx, const float* f_slot,
+                         const float* w_slot, int nviews, int64_t cap,
+                         void* stream) {
+  return guard([&] {
+    if (!ctx || !f_slot) throw octf::Error(octf::kEArg, "null argument");
+    if (nviews < 1) throw octf::Error(octf::kEArg, "at least one view is required");
+    octf::ctx_set_samples(ctx->c, f_slot, w_slot, nviews, cap, S(stream));
   });
 }
 

@@ -181,6 +181,34 @@ __global__ void k_gather(const int32_t* __restrict__ ucs,
   if (flag) atomicExch(nonbin, 1);
 }
 
+// per (leaf, view) from caller-supplied per-slot arrays [view][cap]
+// (W null: every sample has weight 1)
+__global__ void k_gather_slots(const int32_t* __restrict__ ucs,
+                               const int32_t* __restrict__ lblocks, int64_t nlb,
+                               const float* __restrict__ Fs,
+                               const float* __restrict__ Ws, int64_t cap,
+                               int nv, float* F, float* W, int64_t stride,
+                               int32_t* nonbin) {
+  int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t i = gid >> 3;
+  int c = (int)(gid & 7);
+  if (i >= nlb) return;
+  int32_t b = lblocks[i];
+  bool active = !(b == 0 && c != 0) && ucs[b + c] < 0;
+  int flag = 0;
+  for (int v = 0; v < nv; ++v) {
+    float f = 0.f, w = 0.f;
+    if (active) {
+      f = Fs[(int64_t)v * cap + b + c];
+      w = Ws ? Ws[(int64_t)v * cap + b + c] : 1.f;
+      flag |= (w != 0.f && w != 1.f);
+    }
+    F[samp_idx(gid, v, stride)] = f;
+    W[samp_idx(gid, v, stride)] = w;
+  }
+  if (flag) atomicExch(nonbin, 1);
+}
+
 __global__ void k_masks(const float* __restrict__ W, int64_t stride, int nv,
                         int64_t n, uint32_t* M) {
   int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -365,6 +393,9 @@ void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
 void ctx_set_views(Ctx& c, int nviews, const float* const* vval,
                    const float* const* vw, const int32_t* const* vchild,
                    cudaStream_t st) {
+  if (nviews == 0 && c.ext_F) return;  // samples supplied per slot
+  c.ext_F = nullptr;
+  c.ext_W = nullptr;
   std::vector<const void*> key;
   for (int v = 0; v < nviews; ++v) {
     key.push_back(vval[v]);
@@ -385,6 +416,18 @@ void ctx_set_views(Ctx& c, int nviews, const float* const* vval,
                             cudaMemcpyHostToDevice, st));
   OCTF_CUDA(cudaStreamSynchronize(st));
   if (c.valid) ctx_gather(c, st);
+}
+
+void ctx_set_samples(Ctx& c, const float* F, const float* W, int nviews,
+                     int64_t cap, cudaStream_t st) {
+  if (!F || nviews < 1) throw Error(kEArg, "samples and a view count needed");
+  c.ext_F = F;
+  c.ext_W = W;
+  c.ext_cap = cap;
+  c.nviews = nviews;
+  c.vkey.clear();
+  if (c.valid) ctx_gather(c, st);
+  OCTF_CUDA(cudaStreamSynchronize(st));
 }
 
 ViewSet ctx_views(const Ctx& c) {
@@ -409,9 +452,14 @@ void ctx_gather(Ctx& c, cudaStream_t st) {
   OCTF_CUDA(cudaMemsetAsync(c.F.p, 0, (size_t)nvp * npad * sizeof(float), st));
   OCTF_CUDA(cudaMemsetAsync(c.W.p, 0, (size_t)nvp * npad * sizeof(float), st));
   OCTF_CUDA(cudaMemsetAsync(c.counters.p, 0, sizeof(int32_t), st));
-  k_gather<<<grid_for(n), kThreads, 0, st>>>(c.child_key, c.lblocks.p, c.nlb,
-                                              c.lkey.p, ctx_views(c), c.F.p,
-                                              c.W.p, nvp, c.counters.p);
+  if (c.ext_F)  // per-slot sample arrays supplied by the caller
+    k_gather_slots<<<grid_for(n), kThreads, 0, st>>>(
+        c.child_key, c.lblocks.p, c.nlb, c.ext_F, c.ext_W, c.ext_cap, nv, c.F.p,
+        c.W.p, nvp, c.counters.p);
+  else
+    k_gather<<<grid_for(n), kThreads, 0, st>>>(c.child_key, c.lblocks.p,
+                                                c.nlb, c.lkey.p, ctx_views(c),
+                                                c.F.p, c.W.p, nvp, c.counters.p);
   OCTF_CUDA(cudaGetLastError());
   OCTF_CUDA(cudaMemcpyAsync(c.h_counters, c.counters.p, sizeof(int32_t),
                             cudaMemcpyDeviceToHost, st));

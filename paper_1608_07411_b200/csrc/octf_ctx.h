@@ -124,6 +124,11 @@ struct Ctx {
   bool binw = false;          // samples use the mask format
   int64_t sstride = 0;        // views per leaf vector, padded to 4
 
+  // ---- or samples supplied per slot by the caller (frozen trees only)
+  const float* ext_F = nullptr;  // [view][ext_cap]
+  const float* ext_W = nullptr;  // [view][ext_cap] or null (all weight 1)
+  int64_t ext_cap = 0;
+
   // ---- views (device arrays of device pointers)
   DevBuf<const float*> dv_val, dv_w;
   DevBuf<const int32_t*> dv_child;
@@ -169,6 +174,8 @@ void ctx_set_views(Ctx& c, int nviews, const float* const* vval,
                    const float* const* vw, const int32_t* const* vchild,
                    cudaStream_t st);
 void ctx_gather(Ctx& c, cudaStream_t st);
+void ctx_set_samples(Ctx& c, const float* F, const float* W, int nviews,
+                     int64_t cap, cudaStream_t st);
 void ctx_free_stack(Ctx& c, const int32_t* child, const int64_t* state,
                     cudaStream_t st);
 ViewSet ctx_views(const Ctx& c);

@@ -663,6 +663,9 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
                               cudaMemcpyDeviceToDevice, st));
   const LeafParams<T> lp = leaf_params<T>(prm);
   const bool frozen = prm.tau_s <= 0.0 && prm.clamp && prm.tau_j >= 1.0;
+  if (!frozen && c.ext_F)
+    throw Error(kEArg, "per-slot samples need a frozen structure "
+                       "(tau_split <= 0, tau_join >= 1, clamp)");
   c.counters.ensure(64);
   c.split_list.ensure(c.nlb * 8 + 1);
   OCTF_CUDA(cudaMemsetAsync(c.counters.p, 0, 8 * sizeof(int32_t), st));

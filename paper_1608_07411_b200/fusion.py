@@ -198,10 +198,10 @@ class Solver:
 
     def __init__(self, u0: OctreeField, views, params: FusionParams, *,
                  log_joins: bool = False, reverse: bool = False,
-                 precision: str = "fp64"):
-        if not views:
+                 precision: str = "fp64", samples=None):
+        if not views and samples is None:
             raise ValueError("at least one view is required")
-        for v in views:
+        for v in views or ():
             if v.d_max != u0.d_max:
                 raise ValueError("view and iterate depths differ")
         if precision not in ("fp64", "fp32"):
@@ -214,8 +214,16 @@ class Solver:
         self.dtype = torch.float64 if precision == "fp64" else torch.float32
         self.kern = _backend.get()
         self.u = _solver_field(u0, self.dtype)
-        self.vvals, self.vws, self.vchilds = view_arrays(views)
+        self.vvals, self.vws, self.vchilds = view_arrays(views or [])
         self.ctx = _lib.Ctx()
+        self.samples = samples
+        if samples is not None:
+            # per-slot samples (BASELINE config 5): frozen trees only
+            if not self.frozen:
+                raise ValueError("per-leaf samples need a frozen structure")
+            self.kern.ctx_prepare(self.ctx, self.u.child, self.u.state,
+                                  self.u.d_max, [], [], [])
+            self.kern.ctx_set_samples(self.ctx, *samples)
         self.jbuf = None
         self.chunks: list[np.ndarray] = []
         self.stats: list[IterationStats] = []
@@ -330,10 +338,10 @@ class PDSolver:
 
     def __init__(self, u0: OctreeField, views, params: FusionParams, *,
                  precision: str = "fp32", tau: float | None = None,
-                 sigma: float | None = None):
-        if not views:
+                 sigma: float | None = None, samples=None):
+        if not views and samples is None:
             raise ValueError("at least one view is required")
-        for v in views:
+        for v in views or ():
             if v.d_max != u0.d_max:
                 raise ValueError("view and iterate depths differ")
         dtype = torch.float64 if precision == "fp64" else torch.float32
@@ -344,8 +352,13 @@ class PDSolver:
         self.kern = _backend.get()
         self.u = _solver_field(u0, dtype)
         used, cap = self.u.used, self.u.capacity
-        self.vvals, self.vws, self.vchilds = view_arrays(views)
+        self.vvals, self.vws, self.vchilds = view_arrays(views or [])
         self.ctx = _lib.Ctx()
+        self.samples = samples
+        if samples is not None:
+            self.kern.ctx_prepare(self.ctx, self.u.child, self.u.state,
+                                  self.u.d_max, [], [], [])
+            self.kern.ctx_set_samples(self.ctx, *samples)
         def z():
             return pool_empty(cap, dtype, fill=0)
         ub = z()
@@ -403,7 +416,8 @@ class PDSolver:
 
 def fuse(u0: OctreeField, views, params: FusionParams, *,
          log_joins: bool = False, reverse: bool = False,
-         precision: str = "fp64", solver: str = "descent") -> FuseResult:
+         precision: str = "fp64", solver: str = "descent",
+         samples=None) -> FuseResult:
     """Run the full descent schedule on an octree iterate (fusion.py:186-241).
 
     ``u0`` is left untouched.  Statistics carry one row per pass; energies
@@ -412,7 +426,8 @@ def fuse(u0: OctreeField, views, params: FusionParams, *,
     instead (frozen structure; no reference counterpart, see PDSolver).
     """
     if solver == "pd":
-        pds = PDSolver(u0, views, params, precision=precision)
+        pds = PDSolver(u0, views, params, precision=precision,
+                       samples=samples)
         pds.run(0, params.iterations)
         res = pds.result()
         pds.close()
@@ -420,7 +435,7 @@ def fuse(u0: OctreeField, views, params: FusionParams, *,
     if solver != "descent":
         raise ValueError("solver must be 'descent' or 'pd'")
     solver = Solver(u0, views, params, log_joins=log_joins, reverse=reverse,
-                    precision=precision)
+                    precision=precision, samples=samples)
     solver.run(0, params.iterations)
     res = solver.result()
     solver.close()

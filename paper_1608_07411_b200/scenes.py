@@ -152,3 +152,117 @@ def make_cfg2_samples(d_max: int = 8, n_samples: int = 16, seed: int = 0,
         fs.append(f)
         ws.append(w)
     return fs, ws
+
+
+def cfg5_tree(n_target: int = 100_000_000, d_max: int = 12, seed: int = 0,
+              n_spheres: int = 32, device="cpu", radius_scale: float | None = None):
+    """BASELINE config 4 ("solver microbenchmark") structure: a random adaptive
+    octree refined around a random implicit surface (union of ``n_spheres``
+    spheres, assumed), built directly as a reference-layout pool.
+
+    A cell at level L < d_max splits iff |sd(centre)| < a_L * h_L * sqrt(3)/2
+    (h_L = cell edge), with a_L = 1 above level d_max-2 (every cell the
+    surface may cross) and thinner bands a = 0.55 / 0.24 at the last two
+    levels, which puts roughly 60/30/10 % of the leaves at depths 12/11/10
+    (the real histogram is returned).  ``radius_scale`` (default: calibrated
+    from a depth-9 pilot) sets the surface area and so the leaf count.
+    Slots are assigned breadth-first (children of the k-th inner node of the
+    whole tree at 1 + 8k) -- a valid pool layout in which every level is in
+    Morton order.  Returns (child int32 tensor, d_max, level histogram dict).
+    """
+    import torch
+    g = torch.Generator().manual_seed(seed)
+    centres = (torch.rand((n_spheres, 3), generator=g, dtype=torch.float64)
+               * 0.6 + 0.2).to(device)
+    radii0 = (torch.rand(n_spheres, generator=g, dtype=torch.float64)
+              * 0.1 + 0.05).to(device)
+
+    def build(scale, depth):
+        radii = radii0 * scale
+        levels = []   # per level: split flags (bool tensor)
+        x = torch.zeros(1, dtype=torch.int64, device=device)
+        y = torch.zeros_like(x)
+        z = torch.zeros_like(x)
+        hist = {}
+        for L in range(depth + 1):
+            n = x.numel()
+            if L == depth:
+                levels.append(torch.zeros(n, dtype=torch.bool, device=device))
+                hist[L] = n
+                break
+            h = 1.0 / (1 << L)
+            a = 1.0 if L < depth - 2 else (0.55 if L == depth - 2 else 0.24)
+            split = torch.empty(n, dtype=torch.bool, device=device)
+            for lo in range(0, n, 1 << 20):   # bound the [cells, spheres] temp
+                hi = min(n, lo + (1 << 20))
+                p = torch.stack([(x[lo:hi].double() + 0.5) * h,
+                                 (y[lo:hi].double() + 0.5) * h,
+                                 (z[lo:hi].double() + 0.5) * h], dim=1)
+                dist = ((p[:, None, :] - centres[None, :, :]) ** 2).sum(-1).sqrt()
+                sd = (dist - radii[None, :]).min(dim=1).values
+                split[lo:hi] = sd.abs() < a * h * 0.8660254037844386
+            levels.append(split)
+            hist[L] = int((~split).sum())
+            px, py, pz = x[split], y[split], z[split]
+            c = torch.arange(8, device=device)
+            x = (2 * px[:, None] + ((c >> 2) & 1)).reshape(-1)
+            y = (2 * py[:, None] + ((c >> 1) & 1)).reshape(-1)
+            z = (2 * pz[:, None] + (c & 1)).reshape(-1)
+        return levels, hist
+
+    if radius_scale is None:
+        # pilot at depth d_max-3 (leaf count ~ area * 4^depth), then one
+        # correction at full depth (count ~ radius^2)
+        _, hp = build(1.0, d_max - 3)
+        radius_scale = (n_target / (sum(hp.values()) * 64.0)) ** 0.5
+        _, h1 = build(radius_scale, d_max)
+        radius_scale *= (n_target / sum(h1.values())) ** 0.5
+    levels, hist = build(radius_scale, d_max)
+    # breadth-first slots: level-L nodes sit at 1 + 8*R_{L-1} + j
+    used = 1 + 8 * sum(int(s.sum()) for s in levels)
+    child = torch.full((used,), -1, dtype=torch.int32, device=device)
+    start, inner_before = 0, 0
+    for L, split in enumerate(levels):
+        n = split.numel()
+        slots = torch.arange(start, start + n, device=device)
+        k = torch.cumsum(split.to(torch.int64), 0) - 1 + inner_before
+        child[slots[split]] = (1 + 8 * k[split]).to(torch.int32)
+        inner_before += int(split.sum())
+        # the next level's nodes are the children of this level's inner
+        # nodes: their blocks start at 1 + 8 * (inner nodes before level L)
+        start = 1 + 8 * (inner_before - int(split.sum()))
+    return child, d_max, {"leaves_per_level": hist,
+                          "leaves": sum(hist.values()), "nodes": used,
+                          "radius_scale": radius_scale}
+
+
+def cfg5_inputs(n_target: int = 100_000_000, nviews: int = 32, seed: int = 0,
+                device="cuda", d_max: int = 12, radius_scale=None):
+    """Config 4's solver microbenchmark inputs on ``device``: the tree of
+    ``cfg5_tree``, N = ``nviews`` per-leaf fp32 samples U(-1, 1), all valid,
+    as a per-slot [nviews, nodes] array (the solver's ``samples=``), and
+    u0 = the initial field (sum f / (N + gamma), reference fusion.py:149-155)
+    with inner nodes propagated.  Returns (u0 OctreeField, (F_slot, None),
+    info)."""
+    import torch
+    from .octree import OctreeField, propagate_means
+    from ._device import pool_empty
+    child, d, info = cfg5_tree(n_target, d_max, seed, device=device,
+                               radius_scale=radius_scale)
+    used = child.numel()
+    g = torch.Generator(device=device).manual_seed(seed + 1)
+    F = torch.empty((nviews, used), dtype=torch.float32, device=device)
+    F.uniform_(-1.0, 1.0, generator=g)
+    fsum = torch.zeros(used, dtype=torch.float64, device=device)
+    for v in range(nviews):          # view order, f64 (cli.py:148-149)
+        fsum += F[v].double()
+    u = fsum / (nviews + 1e-4)
+    value = pool_empty(used, torch.float64)
+    value.copy_(u)
+    ch = pool_empty(used, torch.int32)
+    ch.copy_(child)
+    state = np.array([used, -1, used], dtype=np.int64)
+    u0 = OctreeField(value, ch, state, d)
+    propagate_means(u0)
+    return u0, (F, None), info
+

@@ -469,6 +469,10 @@ void ctx_gather(Ctx& c, cudaStream_t st) {
     c.M.ensure(npad);
     k_masks<<<grid_for(npad), kThreads, 0, st>>>(c.W.p, nvp, nv, npad, c.M.p);
     OCTF_CUDA(cudaGetLastError());
+    OCTF_CUDA(cudaStreamSynchronize(st));
+    c.W.release();  // the mask format replaces the weight vectors
+  } else {
+    c.M.release();
   }
 }
 

@@ -97,25 +97,26 @@ __global__ void __launch_bounds__(kT) k_pd_pass(PdArgs<T> a) {
   const int i = gid >> 3;
   const int c = gid & 7;
   const bool inrange = i < (int)a.nlb;
-  // samples (view order) -- first, they depend on nothing
-  float f[NV], w[NV];
-  int ix[NV];
-  uint32_t mk = 0;
-  {
-    // tile-transposed store: view v of this leaf at samp_idx(gid, v, NV)
-    const float* fp = a.F + samp_idx(gid, 0, NV);
-#pragma unroll
-    for (int v = 0; v < NV; ++v) f[v] = inrange ? __ldg(fp + v * kTileLeaves) : 0.f;
-    if (BINW) {
-      mk = inrange ? __ldg(a.M + gid) : 0u;
-#pragma unroll
-      for (int v = 0; v < NV; ++v) w[v] = (mk >> v) & 1u ? 1.f : 0.f;
-    } else {
-      const float* wp = a.W + samp_idx(gid, 0, NV);
-#pragma unroll
-      for (int v = 0; v < NV; ++v) w[v] = inrange ? __ldg(wp + v * kTileLeaves) : 0.f;
-    }
+  // samples: the CTA's tile staged by one TMA bulk copy (as k_leaf_pass),
+  // read into registers only after the stencil, so the stencil values and
+  // the sort network never hold registers at the same time
+  extern __shared__ __align__(128) float s_tile[];
+  __shared__ __align__(8) uint64_t s_bar;
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar, 1);
+    const size_t tile = blockIdx.x;
+    const unsigned fbytes = NV * kTileLeaves * 4;
+    const unsigned abytes = BINW ? kTileLeaves * 4 : fbytes;
+    mbar_expect_tx(&s_bar, fbytes + abytes);
+    bulk_g2s(s_tile, a.F + tile * NV * kTileLeaves, fbytes, &s_bar);
+    if (BINW)
+      bulk_g2s(s_tile + NV * kTileLeaves, a.M + tile * kTileLeaves, abytes,
+               &s_bar);
+    else
+      bulk_g2s(s_tile + NV * kTileLeaves, a.W + tile * NV * kTileLeaves,
+               abytes, &s_bar);
   }
+  __syncthreads();
   const int4 meta = inrange ? __ldg(a.lmeta + i) : make_int4(0, 0, 0, 0);
   const int32_t b = meta.x;
   const int32_t s = b + c;
@@ -193,29 +194,36 @@ __global__ void __launch_bounds__(kT) k_pd_pass(PdArgs<T> a) {
   const T div = ((D0 - bx) + (D1 - by) + (D2 - bz)) * ih;
   const T v0 = U0 + a.tl * div;
 
+  // samples from the staged tile, view order
+  mbar_wait(&s_bar, 0);
+  const int t = threadIdx.x;
+  float f[NV];
+  float w[NV];  // (unused with binary weights: the sort carries f only)
+  int ix[NV];
+  const uint32_t mk =
+      BINW ? reinterpret_cast<const uint32_t*>(s_tile + NV * kTileLeaves)[t] : 0u;
   // data: weight sum and energy numerator in view order
   T W = 0, num = 0;
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
-    const bool on = v < a.nv && w[v] != 0.f;
+    f[v] = s_tile[v * kTileLeaves + t];
+    const float wv = BINW ? ((mk >> v) & 1u ? 1.f : 0.f)
+                          : s_tile[(NV + v) * kTileLeaves + t];
+    const bool on = v < a.nv && wv != 0.f;
     if (on) {
-      W += (T)w[v];
-      num += (T)w[v] * fabs(U0 - (T)f[v]);
+      W += (T)wv;
+      num += (T)wv * fabs(U0 - (T)f[v]);
     }
-    if (!on) {  // absent samples sort to the end and carry no weight
-      f[v] = __int_as_float(0x7f800000);
-      w[v] = 0.f;
+    if (!on) f[v] = __int_as_float(0x7f800000);  // absent: sorts last
+    if (!BINW) {
+      w[v] = on ? wv : 0.f;
+      ix[v] = v;
     }
-    ix[v] = v;
   }
   const T den = W + a.gamma;
   bitonic<NV, !BINW>(f, w, ix);
-  if (BINW) {  // unit weights were not carried through the sort
-#pragma unroll
-    for (int v = 0; v < NV; ++v)
-      w[v] = f[v] != __int_as_float(0x7f800000) ? 1.f : 0.f;
-  }
-  // generalised weighted median (oracle/pd_oracle.c wmedian_prox)
+  // generalised weighted median (oracle/pd_oracle.c wmedian_prox); with
+  // unit weights the running weight after k sorted samples is simply k
   const T cc = a.tau / den;
   T S = 0, res = v0;
   bool done = false;
@@ -230,7 +238,8 @@ __global__ void __launch_bounds__(kT) k_pd_pass(PdArgs<T> a) {
       res = cand;
       done = true;
     }
-    if (k < NV) S += (T)w[k];
+    if (k < NV) S += BINW ? (f[k] != __int_as_float(0x7f800000) ? (T)1 : (T)0)
+                          : (T)w[k];
   }
   if (a.clamp) res = clamp1(res);
   double eterm = 0.0;

@@ -954,6 +954,22 @@ void frozen_passes_impl(Ctx& c, FrozenArgs& a, cudaStream_t st) {
 // npasses of the TV-L1 primal-dual scheme on a frozen tree; set A = a.in,
 // set B = a.out; pass k reads the set k%2 and writes the other
 template <typename T>
+void pd_passes_impl(Ctx& c, PdHostArgs& a, cudaStream_t st);
+
+template <typename T, bool BW, int N>
+void launch_pd(unsigned g, cudaStream_t st, const PdArgs<T>& p) {
+  constexpr size_t smem = leaf_smem_bytes(N, BW);
+  static bool attr = false;  // opt in to > 48 KiB of dynamic shared memory
+  if (smem > 48 * 1024 && !attr) {
+    OCTF_CUDA(cudaFuncSetAttribute(k_pd_pass<T, BW, N>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+    attr = true;
+  }
+  k_pd_pass<T, BW, N><<<g, kT, smem, st>>>(p);
+}
+
+template <typename T>
 void pd_passes_impl(Ctx& c, PdHostArgs& a, cudaStream_t st) {
   if (a.d_max < 0 || a.d_max > kMaxDepth)
     throw Error(kEDepth, "tree depth out of range");
@@ -1002,7 +1018,7 @@ void pd_passes_impl(Ctx& c, PdHostArgs& a, cudaStream_t st) {
       p.epart = c.partials.p + (size_t)j * g;
       if (c.timing && (int)c.pev.size() >= 2 * kChunk)
         OCTF_CUDA(cudaEventRecord(c.pev[2 * j], st));
-#define OCTF_PD(BW, N) k_pd_pass<T, BW, N><<<g, kT, 0, st>>>(p)
+#define OCTF_PD(BW, N) launch_pd<T, BW, N>(g, st, p)
       if (c.binw) {
         if (nv == 4) OCTF_PD(true, 4); else if (nv == 8) OCTF_PD(true, 8);
         else if (nv == 16) OCTF_PD(true, 16); else OCTF_PD(true, 32);

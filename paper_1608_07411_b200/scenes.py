@@ -215,8 +215,9 @@ def cfg5_tree(n_target: int = 100_000_000, d_max: int = 12, seed: int = 0,
         # correction at full depth (count ~ radius^2)
         _, hp = build(1.0, d_max - 3)
         radius_scale = (n_target / (sum(hp.values()) * 64.0)) ** 0.5
-        _, h1 = build(radius_scale, d_max)
-        radius_scale *= (n_target / sum(h1.values())) ** 0.5
+        for _ in range(2):
+            _, h1 = build(radius_scale, d_max)
+            radius_scale *= (n_target / sum(h1.values())) ** 0.5
     levels, hist = build(radius_scale, d_max)
     # breadth-first slots: level-L nodes sit at 1 + 8*R_{L-1} + j
     used = 1 + 8 * sum(int(s.sum()) for s in levels)

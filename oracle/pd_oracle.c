@@ -16,7 +16,8 @@
  *            level L (p' of a backward neighbour evaluated at level L)
  *            u' = prox_{tau D}(v) = argmin_x (x-v)^2/2 + c sum_i w_i|x-f_i|,
  *            c = tau/(W+gamma): generalised weighted median, samples sorted
- *            by (f, view index)
+ *            by (f, view index); a -0 sample is taken as +0 (so the sorted
+ *            values do not depend on how a sort orders equal keys)
  *   extrapolation  ubar' = 2u' - u;  u' clamped to [-1,1] when clamp.
  * Inner nodes of u, ubar, p are child means (propagate) after every pass.
  * Built with -ffp-contract=off; the GPU's f64 mode keeps this exact order.
@@ -139,7 +140,7 @@ int orc_pd_pass(const double *u, const double *ub, const double *px,
             int64_t vn = node_at(vchild[v], L, x, y, z);
             double w = (double)vw[v][vn];
             if (w != 0.0) {
-                fs[ns] = (double)vval[v][vn];
+                fs[ns] = (double)vval[v][vn] + 0.0; /* -0 -> +0 */
                 ws[ns] = w;
                 ix[ns] = v;
                 ns++;

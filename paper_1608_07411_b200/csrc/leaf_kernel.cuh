@@ -85,6 +85,48 @@ __device__ __forceinline__ T step_val(T own, int c, int cx, int cy, int cz,
   return v;
 }
 
+// slot read for the cell (x+DX, y+DY, z+DZ) at the leaf's level, or -1 when
+// the cell is the sibling c^mask of the own block (value by shuffle) or the
+// point is not read; lets several fields share one neighbour-table lookup
+template <int DX, int DY, int DZ>
+__device__ __forceinline__ int step_idx(int c, int cx, int cy, int cz,
+                                        bool inside, const int32_t* nb) {
+  const bool ex = DX > 0 ? cx : (DX < 0 ? !cx : false);
+  const bool ey = DY > 0 ? cy : (DY < 0 ? !cy : false);
+  const bool ez = DZ > 0 ? cz : (DZ < 0 ? !cz : false);
+  constexpr int mask = (DX ? 4 : 0) | (DY ? 2 : 0) | (DZ ? 1 : 0);
+  int idx = -1;
+  if ((ex || ey || ez) && inside) {
+    const int32_t r = __ldg(nb + step_dir<DX, DY, DZ>(ex, ey, ez));
+    idx = r >= 0 ? r + (c ^ mask) : -r - 2;
+  }
+  return idx;
+}
+
+// as step_idx, from the block's 12 table entries already in registers
+template <int DX, int DY, int DZ>
+__device__ __forceinline__ int step_idx_r(int c, int cx, int cy, int cz,
+                                          bool inside, const int32_t (&N)[12]) {
+  const bool ex = DX > 0 ? cx : (DX < 0 ? !cx : false);
+  const bool ey = DY > 0 ? cy : (DY < 0 ? !cy : false);
+  const bool ez = DZ > 0 ? cz : (DZ < 0 ? !cz : false);
+  constexpr int mask = (DX ? 4 : 0) | (DY ? 2 : 0) | (DZ ? 1 : 0);
+  constexpr int fx = DX < 0 ? 0 : 1, fy = DY < 0 ? 2 : 3, fz = DZ < 0 ? 4 : 5;
+  constexpr int exy = DX < 0 ? 6 : 8, exz = DX < 0 ? 7 : 10, eyz = DY < 0 ? 9 : 11;
+  int32_t r;
+  if (DX != 0 && DY != 0) r = ex ? (ey ? N[exy] : N[fx]) : N[fy];
+  else if (DX != 0 && DZ != 0) r = ex ? (ez ? N[exz] : N[fx]) : N[fz];
+  else if (DY != 0 && DZ != 0) r = ey ? (ez ? N[eyz] : N[fy]) : N[fz];
+  else r = DX != 0 ? N[fx] : (DY != 0 ? N[fy] : N[fz]);
+  const int idx = r >= 0 ? r + (c ^ mask) : -r - 2;
+  return ((ex || ey || ez) && inside) ? idx : -1;
+}
+
+template <typename T>
+__device__ __forceinline__ T pick(T own, int idx, const T* __restrict__ arr) {
+  return idx >= 0 ? arr[idx] : own;
+}
+
 // ---- TMA bulk copy global -> shared with an mbarrier (sm_90+ / sm_100a)
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);

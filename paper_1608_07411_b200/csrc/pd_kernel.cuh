@@ -60,34 +60,58 @@ __device__ __forceinline__ void dual3(T p0, T p1, T p2, T gx, T gy, T gz, T sl,
   o2 = az / s;
 }
 
-// compare-swap on (key, weight, view index) with index tie-break
+// ascending compare-exchange: keys only (binary weights: equal keys are
+// interchangeable, so min/max suffices) or (key, weight, view index) with the
+// index tie-break of oracle/pd_oracle.c
 template <bool WEIGHTED>
-__device__ __forceinline__ void cas(float& fa, float& wa, int& ia, float& fb,
-                                    float& wb, int& ib, bool up) {
-  const bool gt = WEIGHTED ? (fa > fb || (fa == fb && ia > ib)) : (fa > fb);
-  if (gt == up) {
-    float t = fa; fa = fb; fb = t;
-    if (WEIGHTED) {
+__device__ __forceinline__ void cx(float& fa, float& wa, int& ia, float& fb,
+                                   float& wb, int& ib) {
+  if (WEIGHTED) {
+    const bool gt = fa > fb || (fa == fb && ia > ib);
+    if (gt) {
+      float t = fa; fa = fb; fb = t;
       t = wa; wa = wb; wb = t;
       int u = ia; ia = ib; ib = u;
     }
+  } else {
+    const float lo = fminf(fa, fb);
+    fb = fmaxf(fa, fb);
+    fa = lo;
   }
 }
 
-// in-register bitonic sort of N (power of two) entries, ascending
-template <int N, bool WEIGHTED>
-__device__ __forceinline__ void bitonic(float* f, float* w, int* ix) {
+// Batcher odd-even merge sort of N (power of two) entries in registers,
+// ascending: 191 comparators at N = 32 (bitonic: 240).  Written as template
+// recursion so every register index is a compile-time constant.
+template <int LO, int N, int R, bool WEIGHTED>
+struct OeMerge {
+  static __device__ __forceinline__ void run(float* f, float* w, int* ix) {
+    if constexpr (2 * R < N) {
+      OeMerge<LO, N, 2 * R, WEIGHTED>::run(f, w, ix);
+      OeMerge<LO + R, N, 2 * R, WEIGHTED>::run(f, w, ix);
 #pragma unroll
-  for (int k = 2; k <= N; k <<= 1) {
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        const int l = i ^ j;
-        if (l > i) cas<WEIGHTED>(f[i], w[i], ix[i], f[l], w[l], ix[l], (i & k) == 0);
-      }
+      for (int i = LO + R; i + R < LO + N; i += 2 * R)
+        cx<WEIGHTED>(f[i], w[i], ix[i], f[i + R], w[i + R], ix[i + R]);
+    } else {
+      cx<WEIGHTED>(f[LO], w[LO], ix[LO], f[LO + R], w[LO + R], ix[LO + R]);
     }
   }
+};
+
+template <int LO, int N, bool WEIGHTED>
+struct OeSort {
+  static __device__ __forceinline__ void run(float* f, float* w, int* ix) {
+    if constexpr (N > 1) {
+      OeSort<LO, N / 2, WEIGHTED>::run(f, w, ix);
+      OeSort<LO + N / 2, N / 2, WEIGHTED>::run(f, w, ix);
+      OeMerge<LO, N, 1, WEIGHTED>::run(f, w, ix);
+    }
+  }
+};
+
+template <int N, bool WEIGHTED>
+__device__ __forceinline__ void oddeven_sort(float* f, float* w, int* ix) {
+  OeSort<0, N, WEIGHTED>::run(f, w, ix);
 }
 
 template <typename T, bool BINW, int NV>
@@ -140,34 +164,50 @@ __global__ void __launch_bounds__(kT) k_pd_pass(PdArgs<T> a) {
   const T P0 = slot_ok ? a.px[s] : (T)0;
   const T P1 = slot_ok ? a.py[s] : (T)0;
   const T P2 = slot_ok ? a.pz[s] : (T)0;
-#define NB(ARR, V0, DX, DY, DZ, MASK, PRED)                                   \
-  step_val<DX, DY, DZ>(__shfl_xor_sync(FULL, V0, MASK), c, cx, cy, cz,       \
-                       active && (PRED), nb, ARR)
+  // one neighbour-table lookup per stencil direction, shared by the fields
+  int32_t N[12];
+  {
+    const int4* nb4 = reinterpret_cast<const int4*>(nb);
+    const int4 n0 = active ? __ldg(nb4) : make_int4(-1, -1, -1, -1);
+    const int4 n1 = active ? __ldg(nb4 + 1) : make_int4(-1, -1, -1, -1);
+    const int4 n2 = active ? __ldg(nb4 + 2) : make_int4(-1, -1, -1, -1);
+    N[0] = n0.x; N[1] = n0.y; N[2] = n0.z; N[3] = n0.w;
+    N[4] = n1.x; N[5] = n1.y; N[6] = n1.z; N[7] = n1.w;
+    N[8] = n2.x; N[9] = n2.y; N[10] = n2.z; N[11] = n2.w;
+  }
+#define IX(DX, DY, DZ, PRED) step_idx_r<DX, DY, DZ>(c, cx, cy, cz, active && (PRED), N)
+  const int ixp = IX(1, 0, 0, xp), iyp = IX(0, 1, 0, yp), izp = IX(0, 0, 1, zp);
+  const int ixm = IX(-1, 0, 0, xm), iym = IX(0, -1, 0, ym), izm = IX(0, 0, -1, zm);
+  const int ixmyp = IX(-1, 1, 0, xm && yp), ixmzp = IX(-1, 0, 1, xm && zp);
+  const int iymxp = IX(1, -1, 0, ym && xp), iymzp = IX(0, -1, 1, ym && zp);
+  const int izmxp = IX(1, 0, -1, zm && xp), izmyp = IX(0, 1, -1, zm && yp);
+#undef IX
+#define SH(V, MASK) __shfl_xor_sync(FULL, V, MASK)
   // ubar at the 13-point stencil
-  const T Bx = NB(a.ub, B0, 1, 0, 0, 4, xp);
-  const T By = NB(a.ub, B0, 0, 1, 0, 2, yp);
-  const T Bz = NB(a.ub, B0, 0, 0, 1, 1, zp);
-  const T Bmx = NB(a.ub, B0, -1, 0, 0, 4, xm);
-  const T Bmxy = NB(a.ub, B0, -1, 1, 0, 6, xm && yp);
-  const T Bmxz = NB(a.ub, B0, -1, 0, 1, 5, xm && zp);
-  const T Bmy = NB(a.ub, B0, 0, -1, 0, 2, ym);
-  const T Bmyx = NB(a.ub, B0, 1, -1, 0, 6, ym && xp);
-  const T Bmyz = NB(a.ub, B0, 0, -1, 1, 3, ym && zp);
-  const T Bmz = NB(a.ub, B0, 0, 0, -1, 1, zm);
-  const T Bmzx = NB(a.ub, B0, 1, 0, -1, 5, zm && xp);
-  const T Bmzy = NB(a.ub, B0, 0, 1, -1, 3, zm && yp);
+  const T Bx = pick(SH(B0, 4), ixp, a.ub);
+  const T By = pick(SH(B0, 2), iyp, a.ub);
+  const T Bz = pick(SH(B0, 1), izp, a.ub);
+  const T Bmx = pick(SH(B0, 4), ixm, a.ub);
+  const T Bmxy = pick(SH(B0, 6), ixmyp, a.ub);
+  const T Bmxz = pick(SH(B0, 5), ixmzp, a.ub);
+  const T Bmy = pick(SH(B0, 2), iym, a.ub);
+  const T Bmyx = pick(SH(B0, 6), iymxp, a.ub);
+  const T Bmyz = pick(SH(B0, 3), iymzp, a.ub);
+  const T Bmz = pick(SH(B0, 1), izm, a.ub);
+  const T Bmzx = pick(SH(B0, 5), izmxp, a.ub);
+  const T Bmzy = pick(SH(B0, 3), izmyp, a.ub);
   // p at the three backward neighbours (all components, for the norms)
-  const T Qx0 = NB(a.px, P0, -1, 0, 0, 4, xm), Qx1 = NB(a.py, P1, -1, 0, 0, 4, xm),
-          Qx2 = NB(a.pz, P2, -1, 0, 0, 4, xm);
-  const T Qy0 = NB(a.px, P0, 0, -1, 0, 2, ym), Qy1 = NB(a.py, P1, 0, -1, 0, 2, ym),
-          Qy2 = NB(a.pz, P2, 0, -1, 0, 2, ym);
-  const T Qz0 = NB(a.px, P0, 0, 0, -1, 1, zm), Qz1 = NB(a.py, P1, 0, 0, -1, 1, zm),
-          Qz2 = NB(a.pz, P2, 0, 0, -1, 1, zm);
+  const T Qx0 = pick(SH(P0, 4), ixm, a.px), Qx1 = pick(SH(P1, 4), ixm, a.py),
+          Qx2 = pick(SH(P2, 4), ixm, a.pz);
+  const T Qy0 = pick(SH(P0, 2), iym, a.px), Qy1 = pick(SH(P1, 2), iym, a.py),
+          Qy2 = pick(SH(P2, 2), iym, a.pz);
+  const T Qz0 = pick(SH(P0, 1), izm, a.px), Qz1 = pick(SH(P1, 1), izm, a.py),
+          Qz2 = pick(SH(P2, 1), izm, a.pz);
   // u at the forward neighbours (energy of the incoming state)
-  const T Ux = NB(a.u, U0, 1, 0, 0, 4, xp);
-  const T Uy = NB(a.u, U0, 0, 1, 0, 2, yp);
-  const T Uz = NB(a.u, U0, 0, 0, 1, 1, zp);
-#undef NB
+  const T Ux = pick(SH(U0, 4), ixp, a.u);
+  const T Uy = pick(SH(U0, 2), iyp, a.u);
+  const T Uz = pick(SH(U0, 1), izp, a.u);
+#undef SH
 
   // dual at the cell
   const T gx = xp ? (Bx - B0) * ih : (T)0;
@@ -206,7 +246,7 @@ __global__ void __launch_bounds__(kT) k_pd_pass(PdArgs<T> a) {
   T W = 0, num = 0;
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
-    f[v] = s_tile[v * kTileLeaves + t];
+    f[v] = __fadd_rn(s_tile[v * kTileLeaves + t], 0.f);  // -0 -> +0
     const float wv = BINW ? ((mk >> v) & 1u ? 1.f : 0.f)
                           : s_tile[(NV + v) * kTileLeaves + t];
     const bool on = v < a.nv && wv != 0.f;
@@ -221,26 +261,43 @@ __global__ void __launch_bounds__(kT) k_pd_pass(PdArgs<T> a) {
     }
   }
   const T den = W + a.gamma;
-  bitonic<NV, !BINW>(f, w, ix);
-  // generalised weighted median (oracle/pd_oracle.c wmedian_prox); with
-  // unit weights the running weight after k sorted samples is simply k
+  oddeven_sort<NV, !BINW>(f, w, ix);
+  // generalised weighted median (oracle/pd_oracle.c wmedian_prox), without
+  // its early exit: with S_k the weight of the first k sorted samples and
+  // cand_k = v0 - cc*(2 S_k - W), the scan stops at the first k with
+  // cand_k <= f[k] (returning max-like f[k-1] when cand_k < f[k-1]).
+  // cand_k is non-increasing and f non-decreasing, so "cand_k > f[k]" holds
+  // exactly for k < k*: count it and keep the last f and first cand seen.
+  // (With unit weights S_k = k; absent samples are +inf and sort last.)
   const T cc = a.tau / den;
-  T S = 0, res = v0;
-  bool done = false;
+  T fprev = -(T)INFINITY, cstar;
+  if (BINW) {
+    // S_k = k: walk k downwards, so the last assignment is the first k
+    // with cand_k <= f[k]; the largest f[k] below k* is a running max
+    cstar = v0 - cc * ((T)2 * (T)NV - W);
 #pragma unroll
-  for (int k = 0; k <= NV; ++k) {
-    const T cand = v0 - cc * ((T)2 * S - W);
-    if (!done && k > 0 && cand < (T)f[k - 1]) {
-      res = (T)f[k - 1];
-      done = true;
+    for (int k = NV - 1; k >= 0; --k) {
+      const T cand = v0 - cc * ((T)2 * (T)k - W);
+      const bool gt = cand > (T)f[k];
+      cstar = gt ? cstar : cand;
+      fprev = gt ? (fprev > (T)f[k] ? fprev : (T)f[k]) : fprev;
     }
-    if (!done && (k == NV || cand <= (T)f[k])) {
-      res = cand;
-      done = true;
+  } else {
+    T S = 0;
+    bool found = false;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const T cand = v0 - cc * ((T)2 * S - W);
+      const bool gt = cand > (T)f[k];
+      if (gt) fprev = (T)f[k];
+      if (!gt && !found) cstar = cand;
+      found = found || !gt;
+      S += (T)w[k];
     }
-    if (k < NV) S += BINW ? (f[k] != __int_as_float(0x7f800000) ? (T)1 : (T)0)
-                          : (T)w[k];
+    if (!found) cstar = v0 - cc * ((T)2 * S - W);
   }
+  const T res0 = cstar < fprev ? fprev : cstar;  // fprev = -inf if k* = 0
+  T res = res0;
   if (a.clamp) res = clamp1(res);
   double eterm = 0.0;
   if (active) {

@@ -155,10 +155,13 @@ def make_cfg2_samples(d_max: int = 8, n_samples: int = 16, seed: int = 0,
 
 
 def cfg5_tree(n_target: int = 100_000_000, d_max: int = 12, seed: int = 0,
-              n_spheres: int = 32, device="cpu", radius_scale: float | None = None):
+              n_spheres: int | None = None, device="cpu",
+              radius_scale: float | None = None):
     """BASELINE config 4 ("solver microbenchmark") structure: a random adaptive
     octree refined around a random implicit surface (union of ``n_spheres``
-    spheres, assumed), built directly as a reference-layout pool.
+    spheres, assumed; default 256 at 100M leaves / depth 12, scaled with the
+    leaf count per finest-level area so radii stay comparable), built
+    directly as a reference-layout pool.
 
     A cell at level L < d_max splits iff |sd(centre)| < a_L * h_L * sqrt(3)/2
     (h_L = cell edge), with a_L = 1 above level d_max-2 (every cell the
@@ -171,11 +174,14 @@ def cfg5_tree(n_target: int = 100_000_000, d_max: int = 12, seed: int = 0,
     Morton order.  Returns (child int32 tensor, d_max, level histogram dict).
     """
     import torch
+    if n_spheres is None:
+        n_spheres = int(min(256, max(8, round(
+            256 * n_target / 1e8 * 4.0 ** (12 - d_max)))))
     g = torch.Generator().manual_seed(seed)
     centres = (torch.rand((n_spheres, 3), generator=g, dtype=torch.float64)
-               * 0.6 + 0.2).to(device)
+               * 0.8 + 0.1).to(device)
     radii0 = (torch.rand(n_spheres, generator=g, dtype=torch.float64)
-              * 0.1 + 0.05).to(device)
+              * 0.04 + 0.02).to(device)
 
     def build(scale, depth):
         radii = radii0 * scale
@@ -211,13 +217,24 @@ def cfg5_tree(n_target: int = 100_000_000, d_max: int = 12, seed: int = 0,
         return levels, hist
 
     if radius_scale is None:
-        # pilot at depth d_max-3 (leaf count ~ area * 4^depth), then one
-        # correction at full depth (count ~ radius^2)
+        # pilot at depth d_max-3 (leaf count ~ area * 4^depth), then secant
+        # steps at full depth on log(count) vs log(scale): overlapping
+        # spheres make the count grow slower than radius^2
         _, hp = build(1.0, d_max - 3)
-        radius_scale = (n_target / (sum(hp.values()) * 64.0)) ** 0.5
+        s0 = (n_target / (sum(hp.values()) * 64.0)) ** 0.5
+        _, h0 = build(s0, d_max)
+        n0 = sum(h0.values())
+        s1 = s0 * (n_target / n0) ** 0.5
         for _ in range(2):
-            _, h1 = build(radius_scale, d_max)
-            radius_scale *= (n_target / sum(h1.values())) ** 0.5
+            _, h1 = build(s1, d_max)
+            n1 = sum(h1.values())
+            if abs(n1 - n_target) < 0.01 * n_target or n1 == n0:
+                break
+            alpha = math.log(n1 / n0) / math.log(s1 / s0)
+            alpha = min(max(alpha, 1.0), 2.5)
+            s0, n0 = s1, n1
+            s1 = s1 * min(max((n_target / n1) ** (1.0 / alpha), 0.5), 2.0)
+        radius_scale = s1
     levels, hist = build(radius_scale, d_max)
     # breadth-first slots: level-L nodes sit at 1 + 8*R_{L-1} + j
     used = 1 + 8 * sum(int(s.sum()) for s in levels)

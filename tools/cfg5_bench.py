@@ -22,6 +22,7 @@ ap.add_argument("--leaves", type=int, default=100_000_000)
 ap.add_argument("--steps", type=int, default=10)
 ap.add_argument("--warmup", type=int, default=3)
 ap.add_argument("--views", type=int, default=32)
+ap.add_argument("--only", choices=("descent", "pd"), default=None)
 args = ap.parse_args()
 
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(
@@ -58,12 +59,14 @@ def timed(s, label, b_leaf):
                   "achieved_GBs": ach, "frac_of_measured_hbm": ach / peak}
 
 
-s = fusion.Solver(u0, None, p, precision="fp32", samples=samples)
-timed(s, "descent_fp32", 4 + 4 + 4 * args.views + (args.views + 7) // 8)
-s.close()
-del s
-torch.cuda.empty_cache()
-s = fusion.PDSolver(u0, None, p, precision="fp32", samples=samples)
-timed(s, "pd_fp32", 40 + 4 * args.views + (args.views + 7) // 8)
-s.close()
+if args.only in (None, "descent"):
+    s = fusion.Solver(u0, None, p, precision="fp32", samples=samples)
+    timed(s, "descent_fp32", 4 + 4 + 4 * args.views + (args.views + 7) // 8)
+    s.close()
+    del s
+    torch.cuda.empty_cache()
+if args.only in (None, "pd"):
+    s = fusion.PDSolver(u0, None, p, precision="fp32", samples=samples)
+    timed(s, "pd_fp32", 40 + 4 * args.views + (args.views + 7) // 8)
+    s.close()
 print(json.dumps(out))

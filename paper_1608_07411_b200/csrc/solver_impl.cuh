@@ -414,6 +414,53 @@ __global__ void k_propagate_level(const int32_t* __restrict__ blocks,
   value[s] = (T)(acc / 8.0);
 }
 
+// up to five fields at once, one thread per child block: the block's parent
+// slot comes from the context's bparent table, and with sector-aligned pools
+// (slot 1 on a 32 B / 64 B boundary, _device.py POOL_PAD) the eight children
+// are read with 16-byte vector loads.  Same sequential double sum as
+// k_propagate_level (_kernels.pyx:153-170 via numpy, oracle propagate).
+template <typename T>
+struct FieldSet {
+  T* v[5];
+};
+
+template <typename T, int NA, bool VEC>
+__global__ void __launch_bounds__(kT)
+    k_propagate_blocks(const int32_t* __restrict__ blocks, int64_t nblk,
+                       const int32_t* __restrict__ bparent, FieldSet<T> f) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nblk) return;
+  const int32_t b = __ldg(blocks + i);
+  const int32_t par = __ldg(bparent + ((b + 7) >> 3));
+#pragma unroll
+  for (int q = 0; q < NA; ++q) {
+    T x[8];
+    if (VEC) {
+      if (sizeof(T) == 4) {
+        const float4* p = reinterpret_cast<const float4*>(f.v[q] + b);
+        const float4 lo = __ldcs(p), hi = __ldcs(p + 1);
+        x[0] = lo.x; x[1] = lo.y; x[2] = lo.z; x[3] = lo.w;
+        x[4] = hi.x; x[5] = hi.y; x[6] = hi.z; x[7] = hi.w;
+      } else {
+        const double2* p = reinterpret_cast<const double2*>(f.v[q] + b);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double2 d = __ldcs(p + k);
+          x[2 * k] = (T)d.x;
+          x[2 * k + 1] = (T)d.y;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = f.v[q][b + k];
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc += (double)x[k];
+    f.v[q][par] = (T)(acc / 8.0);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // energy (_kernels.pyx:494-533) per leaf, deterministic block sums
 template <typename T, bool BINW>
@@ -829,18 +876,47 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
   a.out3[2] = jrows;
 }
 
+// parent levels top .. 0 (default: every level above the finest) of `na`
+// fields; level L is filled from the child blocks listed at level L+1
 template <typename T>
-void launch_propagate(Ctx& c, T* value, const int32_t* child,
-                      cudaStream_t st, int top = -1) {
-  // levels top .. 0 (default: every level above the finest)
-  for (int L = top < 0 ? c.d_max - 1 : top; L >= 0; --L) {
-    const int64_t n = c.lvl_cnt[L];
+void launch_propagate_multi(Ctx& c, T* const* vals, int na, cudaStream_t st,
+                            int top = -1, int lo = 0) {
+  if (na < 1 || na > 5) throw Error(kEArg, "propagate: 1..5 fields");
+  FieldSet<T> fs{};
+  bool vec = true;
+  for (int q = 0; q < na; ++q) {
+    fs.v[q] = vals[q];
+    vec = vec && ((uintptr_t)(vals[q] + 1) % (8 * sizeof(T)) == 0);
+  }
+  for (int L = top < 0 ? c.d_max - 1 : top; L >= lo; --L) {
+    if (L + 1 >= (int)c.lvl_cnt.size()) continue;
+    const int64_t n = c.lvl_cnt[L + 1];
     if (n == 0) continue;
-    k_propagate_level<T><<<blocks_for(n * 8), kT, 0, st>>>(
-        c.lvl_blocks.p + c.lvl_off[L], n, child, value);
+    const int32_t* blk = c.lvl_blocks.p + c.lvl_off[L + 1];
+    const unsigned g = blocks_for(n);
+    if (na == 1) {
+      if (vec) k_propagate_blocks<T, 1, true><<<g, kT, 0, st>>>(blk, n, c.bparent.p, fs);
+      else k_propagate_blocks<T, 1, false><<<g, kT, 0, st>>>(blk, n, c.bparent.p, fs);
+    } else if (na == 5) {
+      if (vec) k_propagate_blocks<T, 5, true><<<g, kT, 0, st>>>(blk, n, c.bparent.p, fs);
+      else k_propagate_blocks<T, 5, false><<<g, kT, 0, st>>>(blk, n, c.bparent.p, fs);
+    } else {
+      for (int q = 0; q < na; ++q) {
+        FieldSet<T> one{};
+        one.v[0] = vals[q];
+        k_propagate_blocks<T, 1, false><<<g, kT, 0, st>>>(blk, n, c.bparent.p, one);
+      }
+    }
     OCTF_CUDA(cudaGetLastError());
     ++c.launches;
   }
+}
+
+template <typename T>
+void launch_propagate(Ctx& c, T* value, const int32_t* child,
+                      cudaStream_t st, int top = -1) {
+  (void)child;  // the context's block lists carry the structure
+  launch_propagate_multi<T>(c, &value, 1, st, top);
 }
 
 template <typename T>
@@ -1031,7 +1107,7 @@ void pd_passes_impl(Ctx& c, PdHostArgs& a, cudaStream_t st) {
       ++c.launches;
       if (c.timing && (int)c.pev.size() >= 2 * kChunk)
         OCTF_CUDA(cudaEventRecord(c.pev[2 * j + 1], st));
-      for (int q = 0; q < 5; ++q) launch_propagate<T>(c, (T*)out[q], a.child, st);
+      launch_propagate_multi<T>(c, (T* const*)out, 5, st);
     }
     sum_partials(c, c.partials.p, g, nk, c.dscalar.p + k0, st);
     if (c.timing && (int)c.pev.size() >= 2 * kChunk) {
@@ -1054,15 +1130,9 @@ template <typename T>
 void propagate_levels_impl(Ctx& c, T* value, const int32_t* child, int lo,
                            int hi, cudaStream_t st) {
   if (!c.valid) throw Error(kEArg, "context not prepared");
-  for (int L = hi - 1; L >= lo; --L) {
-    if (L < 0 || L >= (int)c.lvl_cnt.size()) continue;
-    const int64_t n = c.lvl_cnt[L];
-    if (n == 0) continue;
-    k_propagate_level<T><<<blocks_for(n * 8), kT, 0, st>>>(
-        c.lvl_blocks.p + c.lvl_off[L], n, child, value);
-    OCTF_CUDA(cudaGetLastError());
-    ++c.launches;
-  }
+  (void)child;
+  if (hi - 1 >= 0 && lo < hi)
+    launch_propagate_multi<T>(c, &value, 1, st, hi - 1, lo < 0 ? 0 : lo);
 }
 
 }  // namespace

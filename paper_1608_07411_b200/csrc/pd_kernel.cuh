@@ -240,21 +240,24 @@ __global__ void __launch_bounds__(kT) k_pd_pass(PdArgs<T> a) {
   float f[NV];
   float w[NV];  // (unused with binary weights: the sort carries f only)
   int ix[NV];
-  const uint32_t mk =
-      BINW ? reinterpret_cast<const uint32_t*>(s_tile + NV * kTileLeaves)[t] : 0u;
-  // data: weight sum and energy numerator in view order
+  uint32_t mk = 0u;
   T W = 0, num = 0;
+  if (BINW) {  // valid views of this leaf; W = their count
+    mk = reinterpret_cast<const uint32_t*>(s_tile + NV * kTileLeaves)[t];
+    if (a.nv < 32) mk &= (1u << a.nv) - 1u;
+    W = (T)__popc(mk);
+  }
+  // energy numerator in view order; absent samples become +inf (sort last)
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
-    f[v] = __fadd_rn(s_tile[v * kTileLeaves + t], 0.f);  // -0 -> +0
-    const float wv = BINW ? ((mk >> v) & 1u ? 1.f : 0.f)
-                          : s_tile[(NV + v) * kTileLeaves + t];
-    const bool on = v < a.nv && wv != 0.f;
+    const float fv = s_tile[v * kTileLeaves + t];
+    const float wv = BINW ? 1.f : s_tile[(NV + v) * kTileLeaves + t];
+    const bool on = BINW ? ((mk >> v) & 1u) != 0u : (v < a.nv && wv != 0.f);
     if (on) {
-      W += (T)wv;
-      num += (T)wv * fabs(U0 - (T)f[v]);
+      if (!BINW) W += (T)wv;
+      num += BINW ? (T)fabs(U0 - (T)fv) : (T)wv * fabs(U0 - (T)fv);
     }
-    if (!on) f[v] = __int_as_float(0x7f800000);  // absent: sorts last
+    f[v] = on ? __fadd_rn(fv, 0.f) : __int_as_float(0x7f800000);  // -0 -> +0
     if (!BINW) {
       w[v] = on ? wv : 0.f;
       ix[v] = v;
@@ -262,41 +265,24 @@ __global__ void __launch_bounds__(kT) k_pd_pass(PdArgs<T> a) {
   }
   const T den = W + a.gamma;
   oddeven_sort<NV, !BINW>(f, w, ix);
-  // generalised weighted median (oracle/pd_oracle.c wmedian_prox), without
-  // its early exit: with S_k the weight of the first k sorted samples and
-  // cand_k = v0 - cc*(2 S_k - W), the scan stops at the first k with
-  // cand_k <= f[k] (returning max-like f[k-1] when cand_k < f[k-1]).
-  // cand_k is non-increasing and f non-decreasing, so "cand_k > f[k]" holds
-  // exactly for k < k*: count it and keep the last f and first cand seen.
-  // (With unit weights S_k = k; absent samples are +inf and sort last.)
+  // generalised weighted median (oracle/pd_oracle.c wmedian_prox).  With S_k
+  // the weight of the first k sorted samples and c_k = v0 - cc*(2 S_k - W),
+  // the scan returns at the first k* with c_k* <= f[k*]: max(c_k*, f[k*-1]).
+  // c_k is non-increasing and f non-decreasing, so min(f[k], c_k) is f[k]
+  // for k < k* and c_k after, and that value is max_k min(f[k], c_k)
+  // (f[NV] = +inf) -- two min/max per sample, no branches.  Absent samples
+  // (+inf, weight 0) leave S unchanged; with unit weights S_k = k, and the
+  // k > W terms are below c_W, which is in the max.
   const T cc = a.tau / den;
-  T fprev = -(T)INFINITY, cstar;
-  if (BINW) {
-    // S_k = k: walk k downwards, so the last assignment is the first k
-    // with cand_k <= f[k]; the largest f[k] below k* is a running max
-    cstar = v0 - cc * ((T)2 * (T)NV - W);
+  T res0 = -(T)INFINITY, S = 0;
 #pragma unroll
-    for (int k = NV - 1; k >= 0; --k) {
-      const T cand = v0 - cc * ((T)2 * (T)k - W);
-      const bool gt = cand > (T)f[k];
-      cstar = gt ? cstar : cand;
-      fprev = gt ? (fprev > (T)f[k] ? fprev : (T)f[k]) : fprev;
-    }
-  } else {
-    T S = 0;
-    bool found = false;
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      const T cand = v0 - cc * ((T)2 * S - W);
-      const bool gt = cand > (T)f[k];
-      if (gt) fprev = (T)f[k];
-      if (!gt && !found) cstar = cand;
-      found = found || !gt;
-      S += (T)w[k];
-    }
-    if (!found) cstar = v0 - cc * ((T)2 * S - W);
+  for (int k = 0; k < NV; ++k) {
+    const T cand = v0 - cc * ((T)2 * (BINW ? (T)k : S) - W);
+    const T fk = (T)f[k];
+    res0 = fmax(res0, fmin(cand, fk));
+    if (!BINW) S += (T)w[k];
   }
-  const T res0 = cstar < fprev ? fprev : cstar;  // fprev = -inf if k* = 0
+  res0 = fmax(res0, v0 - cc * ((T)2 * (BINW ? (T)NV : S) - W));
   T res = res0;
   if (a.clamp) res = clamp1(res);
   double eterm = 0.0;

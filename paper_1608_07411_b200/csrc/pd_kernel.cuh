@@ -14,6 +14,10 @@
 // shuffle, neighbour blocks through the 12-entry table.
 #pragma once
 
+#ifndef OCTF_PD_MINB
+#define OCTF_PD_MINB 4  // 4 CTAs of 256 per SM: <= 64 registers
+#endif
+
 template <typename T>
 struct PdArgs {
   const int32_t* __restrict__ lblocks;
@@ -114,8 +118,43 @@ __device__ __forceinline__ void oddeven_sort(float* f, float* w, int* ix) {
   OeSort<0, N, WEIGHTED>::run(f, w, ix);
 }
 
+// max_k min(sorted(X)_k, c_{o+k}) for a bitonic X[0..M) (ascending then
+// descending), c_k = v0 - cc*(2k - W) non-increasing, folded into acc.  A
+// half-cleaner splits X into L <= H (both bitonic); since "c_k > X_(k)"
+// holds exactly below the crossing k*, one half's contribution is trivial
+// -- max(L) = L_(M/2-1) if the crossing lies in H, else c_{o+M/2} -- and
+// only the other half is refined: M-1 comparators plus M-1 selects instead
+// of the M log M / 2 of a merge followed by a scan.
+template <typename T, int M>
+__device__ __forceinline__ void bitonic_select(float* X, T& ko, T& acc, T v0,
+                                               T cc, T W) {
+  if constexpr (M == 1) {
+    const T c = v0 - cc * ((T)2 * ko - W);
+    acc = fmax(acc, fmin((T)X[0], c));
+  } else {
+    constexpr int H = M / 2;
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      const float l = fminf(X[i], X[i + H]);
+      X[i + H] = fmaxf(X[i], X[i + H]);
+      X[i] = l;
+    }
+    float mL = X[0];
+#pragma unroll
+    for (int i = 1; i < H; ++i) mL = fmaxf(mL, X[i]);
+    const T cl = v0 - cc * ((T)2 * (ko + (T)(H - 1)) - W);
+    const T ch = v0 - cc * ((T)2 * (ko + (T)H) - W);
+    const bool inH = cl > (T)mL;
+    acc = fmax(acc, inH ? (T)mL : ch);
+#pragma unroll
+    for (int i = 0; i < H; ++i) X[i] = inH ? X[i + H] : X[i];
+    ko = inH ? ko + (T)H : ko;
+    bitonic_select<T, H>(X, ko, acc, v0, cc, W);
+  }
+}
+
 template <typename T, bool BINW, int NV>
-__global__ void __launch_bounds__(kT) k_pd_pass(PdArgs<T> a) {
+__global__ void __launch_bounds__(kT, BINW ? OCTF_PD_MINB : 1) k_pd_pass(PdArgs<T> a) {
   static_assert(NV > 0 && (NV & (NV - 1)) == 0, "NV: power of two");
   const int gid = (int)(blockIdx.x * kT + threadIdx.x);
   const int i = gid >> 3;
@@ -264,25 +303,41 @@ __global__ void __launch_bounds__(kT) k_pd_pass(PdArgs<T> a) {
     }
   }
   const T den = W + a.gamma;
-  oddeven_sort<NV, !BINW>(f, w, ix);
-  // generalised weighted median (oracle/pd_oracle.c wmedian_prox).  With S_k
-  // the weight of the first k sorted samples and c_k = v0 - cc*(2 S_k - W),
-  // the scan returns at the first k* with c_k* <= f[k*]: max(c_k*, f[k*-1]).
-  // c_k is non-increasing and f non-decreasing, so min(f[k], c_k) is f[k]
-  // for k < k* and c_k after, and that value is max_k min(f[k], c_k)
-  // (f[NV] = +inf) -- two min/max per sample, no branches.  Absent samples
-  // (+inf, weight 0) leave S unchanged; with unit weights S_k = k, and the
-  // k > W terms are below c_W, which is in the max.
   const T cc = a.tau / den;
-  T res0 = -(T)INFINITY, S = 0;
+  T res0 = -(T)INFINITY;
+  if (BINW) {
+    // two sorted halves, the second read backwards: a bitonic sequence
+    // whose order statistics are those of all samples
+    oddeven_sort<NV / 2, false>(f, w, ix);
+    oddeven_sort<NV / 2, false>(f + NV / 2, w, ix);
 #pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    const T cand = v0 - cc * ((T)2 * (BINW ? (T)k : S) - W);
-    const T fk = (T)f[k];
-    res0 = fmax(res0, fmin(cand, fk));
-    if (!BINW) S += (T)w[k];
+    for (int i = 0; i < NV / 4; ++i) {
+      const float t = f[NV / 2 + i];
+      f[NV / 2 + i] = f[NV - 1 - i];
+      f[NV - 1 - i] = t;
+    }
+    res0 = v0 - cc * ((T)2 * (T)NV - W);  // k = NV: f = +inf
+    T ko = 0;
+    bitonic_select<T, NV>(f, ko, res0, v0, cc, W);
+  } else {
+    oddeven_sort<NV, true>(f, w, ix);
+    // generalised weighted median (oracle/pd_oracle.c wmedian_prox).  With
+    // S_k the weight of the first k sorted samples and c_k = v0 - cc*(2 S_k
+    // - W), the scan returns at the first k* with c_k* <= f[k*]:
+    // max(c_k*, f[k*-1]).  c_k is non-increasing and f non-decreasing, so
+    // min(f[k], c_k) is f[k] for k < k* and c_k after, and that value is
+    // max_k min(f[k], c_k) (f[NV] = +inf) -- two min/max per sample, no
+    // branches.  Absent samples (+inf, weight 0) leave S unchanged.  (With
+    // unit weights S_k = k: the BINW branch above, same value.)
+    T S = 0;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const T cand = v0 - cc * ((T)2 * S - W);
+      res0 = fmax(res0, fmin(cand, (T)f[k]));
+      S += (T)w[k];
+    }
+    res0 = fmax(res0, v0 - cc * ((T)2 * S - W));
   }
-  res0 = fmax(res0, v0 - cc * ((T)2 * (BINW ? (T)NV : S) - W));
   T res = res0;
   if (a.clamp) res = clamp1(res);
   double eterm = 0.0;

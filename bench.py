@@ -239,7 +239,13 @@ def run_cuda(args, rank, world, local_rank):
     if rank == 0 and not args.no_pd:
         out["pd_mode"] = run_pd_mode(views, u0, p, args, nleaves, peak)
     if rank == 0 and not args.no_e2e:
-        out["e2e"] = run_e2e(views, u0, p, args)
+        # host-side allocation and paging make one end-to-end call noisy
+        # (measured 120-700 ms for the same 20 passes): report the median of
+        # three calls, each timed in full, and list all three
+        runs = [run_e2e(views, u0, p, args) for _ in range(3)]
+        runs.sort(key=lambda r: r["ms_total"])
+        out["e2e"] = dict(runs[1], repeats_ms=[r["ms_total"] for r in runs],
+                          statistic="median of 3 end-to-end calls")
     if rank == 0 and world == 1 and not args.no_cpu:
         out["cpu_baseline"] = cpu_baseline(args, threads=1)
     return out

@@ -346,9 +346,13 @@ __global__ void k_join_keys(JoinRecs<T> rec, int64_t n, int d_max,
 
 // 4. sweep (_kernels.pyx:357-381): every joined node's child block is freed
 // (all inner nodes under a topmost joined node are joined themselves)
+// With alternating value buffers (octf_fuse_pass) `mirror` is the other
+// buffer: a freed block keeps its last values in the reference's single
+// array, so they are copied to the buffer the next pass writes, which never
+// touches dead slots again.
 template <typename T>
 __global__ void k_sweep_clear(JoinRecs<T> rec, int64_t n, int32_t* child,
-                              uint8_t* joined) {
+                              uint8_t* joined, const T* uval, T* mirror) {
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
   const int32_t s = rec.slot[r], b = rec.blk[r];
@@ -357,6 +361,7 @@ __global__ void k_sweep_clear(JoinRecs<T> rec, int64_t n, int32_t* child,
   for (int q = 0; q < 8; ++q) {
     joined[b + q] = 0;
     if (q) child[b + q] = -1;
+    if (mirror) mirror[b + q] = uval[b + q];
   }
 }
 
@@ -827,8 +832,9 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
       OCTF_CUDA(cudaGetLastError());
   ++c.launches;
       sort_u64_i32(c, rec.key, rec.idx, J, st);
-      k_sweep_clear<T><<<blocks_for(J), kT, 0, st>>>(rec, J, a.child,
-                                                      a.joined);
+      k_sweep_clear<T><<<blocks_for(J), kT, 0, st>>>(
+          rec, J, a.child, a.joined, uval,
+          a.snapshot ? (T*)nullptr : (T*)const_cast<void*>(a.usnap));
       OCTF_CUDA(cudaGetLastError());
   ++c.launches;
       c.free_stack.grow_keep(c.nfree + J + 1, c.nfree, st);

@@ -37,6 +37,7 @@ __all__ = [
     "build_view_tree",
     "view_arrays",
     "initial_field",
+    "prepare",
     "fuse",
     "Solver",
     "tree_energy",
@@ -141,6 +142,26 @@ def initial_field(wf_sum, w_sum, gamma: float):
     _lib.call("octf_initial_field", ptr(wf), ptr(ws), float(gamma), wf.numel(),
               ptr(out), stream_handle())
     return to_numpy(out) if host else out
+
+
+def prepare(depths, cameras, dom, params: FusionParams):
+    """Depth maps -> (view trees, u0, seen): the pre-processing loop of the
+    reference's ``cli.cmd_fuse`` (cli.py:141-171) on the GPU -- per view the
+    TSDF with the wf/w sums accumulated in frame order, the view tree, then
+    ``initial_field`` and ``build_octree(u0_grid, tau)``.  ``seen`` is the
+    (N,N,N) bool grid w_sum > 0 the reference hands to its mesher."""
+    from .tsdf import build_view_tsdf
+    n = dom.resolution
+    wf = torch.zeros((n, n, n), dtype=torch.float64, device=device())
+    ws = torch.zeros_like(wf)
+    trees = []
+    for img, cam in zip(depths, cameras):
+        vt = build_view_tsdf(img, cam, dom, params.delta, params.eta,
+                             accumulate=(wf, ws))
+        trees.append(build_view_tree(vt, params.tau))
+        del vt
+    u0 = build_octree(initial_field(wf, ws, params.gamma), tau=params.tau)
+    return trees, u0, ws > 0
 
 
 # -- octree solver ------------------------------------------------------------

@@ -20,7 +20,9 @@ from dataclasses import dataclass
 import numpy as np
 
 __all__ = ["look_at", "PinholeCamera", "sphere_depth", "Cfg1Scene",
-           "make_cfg1", "torus_sdf", "make_cfg2_samples"]
+           "make_cfg1", "torus_sdf", "make_cfg2_samples", "cfg5_tree",
+           "cfg5_inputs", "DepthScene", "value_noise", "sphere_trace",
+           "make_cfg3", "make_cfg4"]
 
 
 def look_at(position, target, up=(0.0, 0.0, 1.0)) -> np.ndarray:
@@ -284,3 +286,262 @@ def cfg5_inputs(n_target: int = 100_000_000, nviews: int = 32, seed: int = 0,
     propagate_means(u0)
     return u0, (F, None), info
 
+
+
+# ------------------------------------------------------------------ cfg3/cfg4
+# Depth-map configs rendered by sphere tracing (the reference renders only
+# spheres, synth.py:80-109; SURVEY.md §8(d) notes that cfg3/cfg4 need a
+# tracer).  Rendering is input generation, outside the accelerated path: it
+# runs as torch f64 array code on ``device`` so the GPU and the CPU oracle
+# consume the same depth maps.
+
+@dataclass
+class DepthScene:
+    """Depth maps + cameras + volume + solver settings of one config."""
+    name: str
+    origin: tuple
+    voxel_size: float
+    resolution: int
+    cameras: list             # PinholeCamera
+    depths: list              # float32 (H, W), camera-frame z, 0 = no return
+    params: dict              # FusionParams keyword arguments
+
+    @property
+    def d_max(self) -> int:
+        return self.resolution.bit_length() - 1
+
+
+def _lattice(seed: int, n: int, device):
+    import torch
+    g = torch.Generator().manual_seed(seed)
+    return (torch.rand((n, n, n), generator=g, dtype=torch.float64) * 2.0
+            - 1.0).to(device)
+
+
+def value_noise(p, tables, base_freq: float = 4.0):
+    """Lattice value noise: per octave o (frequency base_freq*2^o, amplitude
+    2^-o) trilinear interpolation with smoothstep fade of U(-1,1) lattice
+    values; octave sum divided by the amplitude sum, so n(p) in [-1, 1]
+    (assumed form of BASELINE config 2's '3-octave value noise')."""
+    import torch
+    out = torch.zeros(p.shape[:-1], dtype=torch.float64, device=p.device)
+    amp, total = 1.0, 0.0
+    for o, tab in enumerate(tables):
+        fr = base_freq * (1 << o)
+        q = p.clamp(0.0, 1.0) * fr
+        i0 = q.floor().clamp(max=tab.shape[0] - 2).long()
+        t = q - i0
+        t = t * t * (3.0 - 2.0 * t)
+        acc = torch.zeros_like(out)
+        for c in range(8):
+            dx, dy, dz = (c >> 2) & 1, (c >> 1) & 1, c & 1
+            wgt = ((t[..., 0] if dx else 1.0 - t[..., 0])
+                   * (t[..., 1] if dy else 1.0 - t[..., 1])
+                   * (t[..., 2] if dz else 1.0 - t[..., 2]))
+            acc = acc + wgt * tab[i0[..., 0] + dx, i0[..., 1] + dy, i0[..., 2] + dz]
+        out = out + amp * acc
+        total += amp
+        amp *= 0.5
+    return out / total
+
+
+def sphere_trace(sdf, cam: PinholeCamera, *, lipschitz: float, t_max: float,
+                 device, steps: int = 400, eps: float = 1e-7):
+    """Camera-frame z of the first surface hit of each pixel ray (0 = miss)
+    for a signed distance bound ``sdf`` with Lipschitz constant <=
+    ``lipschitz``: conservative steps sd/L, then 40 bisection steps on the
+    last bracket.  Rays have unit camera-z component (as sphere_depth), so
+    the ray parameter is the depth."""
+    import torch
+    H, W = cam.height, cam.width
+    px = (torch.arange(W, dtype=torch.float64, device=device) - cam.cx) / cam.fx
+    py = (torch.arange(H, dtype=torch.float64, device=device) - cam.cy) / cam.fy
+    dirs = torch.stack(torch.broadcast_tensors(px[None, :], py[:, None],
+                                               torch.ones((), dtype=torch.float64,
+                                                          device=device)), -1)
+    R = torch.as_tensor(cam.rotation, dtype=torch.float64, device=device)
+    d = (dirs.reshape(-1, 3) @ R.T)
+    o = torch.as_tensor(cam.translation, dtype=torch.float64, device=device)
+    nrm = d.norm(dim=1)
+    t = torch.zeros(d.shape[0], dtype=torch.float64, device=device)
+    alive = torch.ones_like(t, dtype=torch.bool)
+    hit = torch.zeros_like(alive)
+    t_prev = t.clone()
+    for _ in range(steps):
+        idx = alive.nonzero().squeeze(1)
+        if idx.numel() == 0:
+            break
+        sd = sdf(o + t[idx, None] * d[idx])
+        h = (sd < eps)
+        hit[idx[h]] = True
+        alive[idx[h]] = False
+        go = idx[~h]
+        t_prev[go] = t[go]
+        t[go] = t[go] + sd[~h] / (lipschitz * nrm[go])
+        far = t[go] > t_max
+        alive[go[far]] = False
+    # bisection between the last outside point and the hit point
+    idx = hit.nonzero().squeeze(1)
+    lo, hi = t_prev[idx], t[idx]
+    for _ in range(40):
+        mid = 0.5 * (lo + hi)
+        inside = sdf(o + mid[:, None] * d[idx]) < 0.0
+        hi = torch.where(inside, mid, hi)
+        lo = torch.where(inside, lo, mid)
+    z = torch.zeros_like(t)
+    z[idx] = hi
+    return z.reshape(H, W)
+
+
+def fibonacci_hemisphere(n: int) -> np.ndarray:
+    """n unit directions with z > 0 on a Fibonacci spiral (assumed viewpoint
+    layout of config 2's 'hemisphere of viewpoints')."""
+    k = np.arange(n) + 0.5
+    z = 1.0 - k / n                       # (0, 1]: upper hemisphere
+    r = np.sqrt(np.maximum(0.0, 1.0 - z * z))
+    phi = k * math.pi * (3.0 - math.sqrt(5.0))
+    return np.stack([r * np.cos(phi), r * np.sin(phi), z], axis=1)
+
+
+def _add_noise(z, sigma, rng):
+    """N(0, sigma) on returns (sigma may be an array), negatives -> 0."""
+    eps = rng.normal(0.0, 1.0, z.shape) * sigma
+    return np.where(z > 0, np.maximum(z + eps, 0.0), 0.0).astype(np.float32)
+
+
+def make_cfg3(d_max: int = 9, n_views: int = 64, width: int = 640,
+              height: int = 480, focal: float = 525.0, seed: int = 0,
+              device="cuda") -> DepthScene:
+    """BASELINE config 2 ("adaptive single object").
+
+    Unit cube, blob sd(p) = |p - c| - (0.35 + 0.03 n(p)), c = (.5,.5,.5), n =
+    3-octave value noise (base frequency 4, lattices from ``seed``); 64
+    cameras at distance 1.2 from c along Fibonacci directions of the upper
+    hemisphere, looking at c (assumed); 640x480, fx = fy = 525, principal
+    point (319.5, 239.5) (assumed); depth noise N(0, 2e-3) on returns,
+    drawn per view in view order from ``default_rng(seed)``; delta = 0.02,
+    eta = 0.1 (assumed), lambda = 0.3 (assumed default), tau_split = 0.1,
+    tau_join = 0.5 (split/join every pass), 300 iterations.
+    """
+    import torch
+    tables = [_lattice(seed * 7 + o, 4 * (1 << o) + 2, device) for o in range(3)]
+    c = torch.tensor([0.5, 0.5, 0.5], dtype=torch.float64, device=device)
+
+    def sdf(p):
+        return (p - c).norm(dim=-1) - (0.35 + 0.03 * value_noise(p, tables))
+
+    # |grad n| <= sum_o a_o * 1.5 * 2 * f_o / sum_o a_o (smoothstep slope 1.5,
+    # lattice range 2) = 20.6; L = 1 + 0.03 * 20.6 < 1.7
+    rng = np.random.default_rng(seed)
+    cams, depths = [], []
+    centre = np.array([0.5, 0.5, 0.5])
+    for k, dvec in enumerate(fibonacci_hemisphere(n_views)):
+        pos = centre + 1.2 * dvec
+        cam = PinholeCamera(focal, focal, (width - 1) / 2.0, (height - 1) / 2.0,
+                            width, height, look_at(pos, centre), pos)
+        z = sphere_trace(sdf, cam, lipschitz=1.7, t_max=3.0, device=device)
+        cams.append(cam)
+        depths.append(_add_noise(z.cpu().numpy(), 2e-3, rng))
+    n = 1 << d_max
+    return DepthScene("cfg3", (0.0, 0.0, 0.0), 1.0 / n, n, cams, depths,
+                      dict(delta=0.02, eta=0.1, lam=0.3, tau_split=0.1,
+                           tau_join=0.5, iterations=300))
+
+
+def _room_objects(seed: int, n_objects: int, size: float):
+    """200 axis-aligned boxes and spheres (50/50, assumed), extent U(0.1,
+    0.8) m (box edges drawn independently, sphere diameter), fully inside
+    the ``size`` m cube."""
+    rng = np.random.default_rng(seed)
+    objs = []
+    for _ in range(n_objects):
+        if rng.random() < 0.5:
+            e = rng.uniform(0.1, 0.8, 3)
+            lo = rng.uniform(0.0, size - e)
+            objs.append(("box", lo + e / 2.0, e / 2.0))
+        else:
+            dia = rng.uniform(0.1, 0.8)
+            ctr = rng.uniform(dia / 2.0, size - dia / 2.0, 3)
+            objs.append(("sphere", ctr, dia / 2.0))
+    return objs
+
+
+def room_sdf_fn(objs, device, size: float = 4.0):
+    """Union SDF of the objects and the room's six walls (the inside of the
+    ``size`` m cube; exact for boxes, spheres and walls)."""
+    import torch
+    boxes = [(c, h) for k, c, h in objs if k == "box"]
+    sph = [(c, r) for k, c, r in objs if k == "sphere"]
+    bc = torch.tensor(np.array([b[0] for b in boxes]), dtype=torch.float64, device=device)
+    bh = torch.tensor(np.array([b[1] for b in boxes]), dtype=torch.float64, device=device)
+    sc = torch.tensor(np.array([s[0] for s in sph]), dtype=torch.float64, device=device)
+    sr = torch.tensor(np.array([s[1] for s in sph]), dtype=torch.float64, device=device)
+
+    def sdf(p):
+        if p.shape[0] == 0:
+            return torch.zeros(0, dtype=torch.float64, device=p.device)
+        out = None
+        for lo in range(0, p.shape[0], 1 << 16):
+            q = p[lo:lo + (1 << 16)]
+            dq = (q[:, None, :] - bc[None]).abs() - bh[None]
+            outside = dq.clamp(min=0.0).norm(dim=-1)
+            inside = dq.max(dim=-1).values.clamp(max=0.0)
+            db = (outside + inside).min(dim=1).values
+            ds = ((q[:, None, :] - sc[None]).norm(dim=-1) - sr[None]).min(dim=1).values
+            walls = torch.minimum(q, size - q).min(dim=1).values
+            r = torch.minimum(torch.minimum(db, ds), walls)
+            out = r if out is None else torch.cat([out, r])
+        return out
+    return sdf
+
+
+def _catmull_rom(pts, n):
+    """n points along a closed Catmull-Rom spline through ``pts``, and unit
+    tangents."""
+    m = len(pts)
+    s = np.linspace(0.0, m, n, endpoint=False)
+    i = np.floor(s).astype(int)
+    t = (s - i)[:, None]
+    p0, p1 = pts[(i - 1) % m], pts[i % m]
+    p2, p3 = pts[(i + 1) % m], pts[(i + 2) % m]
+    pos = 0.5 * ((2 * p1) + (-p0 + p2) * t + (2 * p0 - 5 * p1 + 4 * p2 - p3) * t * t
+                 + (-p0 + 3 * p1 - 3 * p2 + p3) * t ** 3)
+    tan = 0.5 * ((-p0 + p2) + 2 * (2 * p0 - 5 * p1 + 4 * p2 - p3) * t
+                 + 3 * (-p0 + 3 * p1 - 3 * p2 + p3) * t * t)
+    return pos, tan / np.linalg.norm(tan, axis=1, keepdims=True)
+
+
+def make_cfg4(d_max: int = 11, n_frames: int = 300, width: int = 640,
+              height: int = 480, focal: float = 525.0, seed: int = 0,
+              n_objects: int = 200, device="cuda") -> DepthScene:
+    """BASELINE config 3 ("large room"): a 4 m cube (origin 0, d_max 11 =
+    1.95 mm voxels at full size) with ``n_objects`` random boxes/spheres;
+    ``n_frames`` depth maps along a closed Catmull-Rom path through 8 random
+    waypoints at least 0.3 m clear of every object and the walls, looking
+    along the tangent (assumed); the room's walls are part of the scene
+    (assumed); intrinsics as cfg3; depth noise
+    sigma = 0.0015 z^2; delta = 0.03, eta = 0.15 (assumed), tau_split /
+    tau_join defaults, 500 iterations."""
+    import torch
+    size = 4.0
+    objs = _room_objects(seed, n_objects, size)
+    sdf = room_sdf_fn(objs, device, size)
+    rng = np.random.default_rng(seed + 1)
+    way = []
+    while len(way) < 8:
+        q = rng.uniform(0.3, size - 0.3, 3)
+        if float(sdf(torch.tensor(q[None], dtype=torch.float64, device=device))[0]) > 0.3:
+            way.append(q)
+    pos, tan = _catmull_rom(np.array(way), n_frames)
+    cams, depths = [], []
+    noise = np.random.default_rng(seed + 2)
+    for k in range(n_frames):
+        cam = PinholeCamera(focal, focal, (width - 1) / 2.0, (height - 1) / 2.0,
+                            width, height, look_at(pos[k], pos[k] + tan[k]), pos[k])
+        z = sphere_trace(sdf, cam, lipschitz=1.0, t_max=8.0, device=device,
+                         eps=1e-6).cpu().numpy()
+        cams.append(cam)
+        depths.append(_add_noise(z, 0.0015 * z * z, noise))
+    n = 1 << d_max
+    return DepthScene("cfg4", (0.0, 0.0, 0.0), size / n, n, cams, depths,
+                      dict(delta=0.03, eta=0.15, iterations=500))

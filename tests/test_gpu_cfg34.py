@@ -1,0 +1,79 @@
+"""BASELINE configs 2 and 3 (cfg3 adaptive object, cfg4 room) at reduced
+scale, end to end: sphere-traced depth maps -> TSDF -> view trees -> u0 ->
+fuse with split/join every pass, GPU (through the C ABI) against the CPU
+oracle on the same depth maps.  Full scale is infeasible for the oracle
+(SURVEY.md §8(d)); tools/cfg3_bench.py measures it on the GPU alone."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as orc
+from tests.conftest import has_gpu
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")]
+
+
+def oracle_prepare(sc, p):
+    n = sc.resolution
+    wf = np.zeros((n, n, n))
+    ws = np.zeros((n, n, n))
+    views = []
+    for d, c in zip(sc.depths, sc.cameras):
+        f, w = orc.build_view_tsdf(d, c, sc.origin, sc.voxel_size, n, p.delta,
+                                   p.eta)
+        wf += f.astype(np.float64) * w
+        ws += w
+        views.append(orc.build_octree(f, w, tau=p.tau, dtype=np.float32))
+    ub = orc.initial_field(wf, ws, p.gamma)
+    return views, orc.build_octree(ub, tau=p.tau)
+
+
+def run_case(sc, iterations):
+    from paper_1608_07411_b200 import fusion, volume
+    kw = dict(sc.params, iterations=iterations)
+    p_gpu = fusion.FusionParams(**kw)
+    p_orc = orc.Params(**kw)
+    dom = volume.VolumeDomain(sc.origin, sc.voxel_size, sc.resolution)
+    views, u0, seen = fusion.prepare(sc.depths, sc.cameras, dom, p_gpu)
+    oviews, ou0 = oracle_prepare(sc, p_orc)
+    # view trees and u0: bit-exact
+    for g, r in zip(views, oviews):
+        h = g.to_host()
+        assert np.array_equal(h.child, r.child)
+        assert np.array_equal(h.value, r.value)
+        assert np.array_equal(h.weight, r.weight)
+    hu = u0.to_host()
+    assert np.array_equal(hu.child, ou0.child)
+    assert np.array_equal(hu.value, ou0.value)
+    # the solver with split/join every pass, fp64: the reference's pools
+    res = fusion.fuse(u0, views, p_gpu, precision="fp64", log_joins=True)
+    ref = orc.fuse(ou0, oviews, p_orc, log_joins=True)
+    got = res.field.to_host()
+    used = int(ref.field.state[0])
+    assert list(got.state) == list(ref.field.state)
+    assert np.array_equal(got.child[:used], ref.field.child[:used])
+    assert np.array_equal(got.value[:used], ref.field.value[:used])
+    assert [(s.splits, s.joins) for s in res.stats] == \
+        [(s.splits, s.joins) for s in ref.stats]
+    np.testing.assert_allclose([s.energy for s in res.stats],
+                               [s.energy for s in ref.stats], rtol=1e-12)
+    assert np.array_equal(res.join_log, ref.join_log)
+    return res, ref, seen
+
+
+def test_cfg3_reduced_end_to_end():
+    from paper_1608_07411_b200 import scenes
+    sc = scenes.make_cfg3(d_max=7, n_views=16, width=320, height=240,
+                          focal=262.5, device="cuda")
+    res, ref, seen = run_case(sc, 6)
+    assert sum(s.splits + s.joins for s in ref.stats) > 0   # restructures
+    assert bool(seen.any())
+
+
+def test_cfg4_reduced_end_to_end():
+    from paper_1608_07411_b200 import scenes
+    sc = scenes.make_cfg4(d_max=7, n_frames=12, width=320, height=240,
+                          focal=262.5, device="cuda")
+    res, ref, _ = run_case(sc, 4)
+    assert sum(s.splits + s.joins for s in ref.stats) > 0

@@ -1,0 +1,70 @@
+"""BASELINE config 2 (cfg3, adaptive single object) at full size on one GPU:
+64 sphere-traced 640x480 depth maps of the noisy blob, d_max 9 (512^3),
+split/join after every pass.  Times the input stage (TSDF + view trees + u0)
+and K solver passes (iterate + restructure + propagate + energy, host sync
+per pass as the reference's loop), reporting leaf-updates/s = pre-pass leaves
+/ pass time and the leaf kernel's share.
+
+  python tools/cfg3_bench.py [--passes 20] [--precision fp32] [--views 64]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+from paper_1608_07411_b200 import fusion, scenes, volume  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--passes", type=int, default=20)
+ap.add_argument("--precision", default="fp32")
+ap.add_argument("--views", type=int, default=64)
+ap.add_argument("--depth", type=int, default=9)
+args = ap.parse_args()
+
+t0 = time.time()
+sc = scenes.make_cfg3(d_max=args.depth, n_views=args.views, device="cuda")
+torch.cuda.synchronize()
+t_render = time.time() - t0
+p = fusion.FusionParams(**dict(sc.params, iterations=args.passes))
+dom = volume.VolumeDomain(sc.origin, sc.voxel_size, sc.resolution)
+torch.cuda.synchronize()
+t0 = time.time()
+views, u0, seen = fusion.prepare(sc.depths, sc.cameras, dom, p)
+torch.cuda.synchronize()
+t_prep = time.time() - t0
+
+s = fusion.Solver(u0, views, p, precision=args.precision)
+s.ctx.profile(True)
+passes = []
+for t in range(args.passes):
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    st = s.step(t)
+    e1.record()
+    torch.cuda.synchronize()
+    passes.append({"ms": e0.elapsed_time(e1), "nodes": st.node_count,
+                   "splits": st.splits, "joins": st.joins})
+prof = s.ctx.profile(False)
+res = s.result()
+h = res.field.to_host()
+leaves_end = int((h.child[:h.used] < 0).sum())
+steady = passes[3:] if len(passes) > 6 else passes
+ms = sorted(q["ms"] for q in steady)[len(steady) // 2]
+# leaves before each pass ~ nodes*7/8 (complete-children tree: leaves =
+# 7*inner + 1 = (7*nodes + 1)/8)
+lv = [(7 * q["nodes"] + 1) // 8 for q in passes]
+out = {"workload": "cfg3 adaptive object (BASELINE config 2)",
+       "depth": args.depth, "views": args.views, "precision": args.precision,
+       "render_s": t_render, "prepare_s": t_prep,
+       "u0_nodes": u0.node_count, "leaves_end": leaves_end,
+       "median_pass_ms": ms,
+       "leaf_updates_per_s": lv[-1] / (ms / 1e3),
+       "leaf_kernel_ms_per_pass": prof["leaf_ms"] / max(prof["leaf_launches"], 1),
+       "launches": prof["launches"],
+       "passes": passes}
+print(json.dumps(out))

@@ -72,6 +72,12 @@ int octf_ctx_info(octf_ctx *ctx, int64_t *out);
  * launches} accumulated since the previous call, which resets them. */
 int octf_ctx_profile(octf_ctx *ctx, int enable, double *out);
 
+/* Host-side phase times since the last octf_ctx_profile call (which resets
+ * them; recorded only while profiling is enabled): out[0..4] = {context
+ * rebuild ms (incl. gathers), rebuilds, sample gather ms, gathers,
+ * restructuring ms after the leaf kernel (events, cascade, joins, sweep)}. */
+int octf_ctx_phases(octf_ctx *ctx, double *out);
+
 /* _kernels.pyx:384-461 iterate_pass -- one Jacobi descent pass with the
  * in-pass split cascade, join cascade and sweep.  snapshot=1 reproduces the
  * reference's own first step (copy uval into usnap, :390-393); snapshot=0

@@ -36,6 +36,7 @@ _SIGS = {
     "octf_ctx_invalidate": ([P], I32),
     "octf_ctx_info": ([P, P], I32),
     "octf_ctx_profile": ([P, I32, P], I32),
+    "octf_ctx_phases": ([P, P], I32),
     "octf_iterate_pass": ([P, I32, P, P, P, P, P, I64, I32, P, P, P, I32, DBL,
                            DBL, DBL, DBL, DBL, DBL, I32, I32, I32, P, I64, P,
                            P], I32),
@@ -129,11 +130,16 @@ class Ctx:
     def profile(self, enable: bool = True) -> dict:
         """Read and reset the live kernel timers; (re)arm them if enable."""
         import numpy as np
+        ph = np.zeros(5, dtype=np.float64)
+        call("octf_ctx_phases", self.h, ph.ctypes.data)  # before the reset
         out = np.zeros(5, dtype=np.float64)
         call("octf_ctx_profile", self.h, int(bool(enable)), out.ctypes.data)
         return {"leaf_ms": float(out[0]), "leaf_launches": int(out[1]),
                 "energy_ms": float(out[2]), "energy_launches": int(out[3]),
-                "launches": int(out[4])}
+                "launches": int(out[4]),
+                "prepare_ms": float(ph[0]), "prepares": int(ph[1]),
+                "gather_ms": float(ph[2]), "gathers": int(ph[3]),
+                "restructure_ms": float(ph[4])}
 
     def close(self):
         if self.h:

@@ -8,6 +8,7 @@
 // coarser leaves that hold its 13-point stencil, and each leaf gets its N
 // per-view samples (the reference's per-view cursors, _kernels.pyx:265-273)
 // gathered into a coalesced [view][leaf] store.
+#include <chrono>
 #include <cub/cub.cuh>
 
 #include "octf_ctx.h"
@@ -295,6 +296,7 @@ void ctx_free_stack(Ctx& c, const int32_t* child, const int64_t* state,
 
 void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
                  const int64_t* state, int d_max, cudaStream_t st) {
+  const auto t0 = std::chrono::steady_clock::now();
   if (d_max < 0 || d_max > kMaxDepth)
     throw Error(kEDepth, "tree depth out of range");
   int64_t used = state[0];
@@ -334,7 +336,8 @@ void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
     if (c.h_counters[1]) throw Error(kEArg, "corrupt child links in pool");
     int64_t m = c.h_counters[0];
     if (total + m > nbid) throw Error(kEArg, "corrupt child links in pool");
-    sort_i32(c, c.lvl_blocks.p + total, m, st);
+    // (no sort: level lists are only scanned by order-independent kernels;
+    // the leaf-block list is sorted below)
     c.lvl_cnt[L + 1] = m;
     total += m;
   }
@@ -388,6 +391,11 @@ void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
   c.valid = true;
   if (c.nviews > 0) ctx_gather(c, st);
   OCTF_CUDA(cudaStreamSynchronize(st));
+  if (c.timing) {
+    c.t_prep_ms += std::chrono::duration<double, std::milli>(
+                       std::chrono::steady_clock::now() - t0).count();
+    ++c.n_prep;
+  }
 }
 
 void ctx_set_views(Ctx& c, int nviews, const float* const* vval,
@@ -440,6 +448,7 @@ ViewSet ctx_views(const Ctx& c) {
 }
 
 void ctx_gather(Ctx& c, cudaStream_t st) {
+  const auto t0 = std::chrono::steady_clock::now();
   // tiles of 256 leaves, view-major inside a tile (octf_common.cuh
   // samp_idx); views padded to 4 and leaves to whole tiles
   int64_t n = c.nlb * 8;
@@ -473,6 +482,11 @@ void ctx_gather(Ctx& c, cudaStream_t st) {
     c.W.release();  // the mask format replaces the weight vectors
   } else {
     c.M.release();
+  }
+  if (c.timing) {
+    c.t_gather_ms += std::chrono::duration<double, std::milli>(
+                         std::chrono::steady_clock::now() - t0).count();
+    ++c.n_gather;
   }
 }
 

@@ -156,6 +156,10 @@ struct Ctx {
   cudaEvent_t tev[4] = {nullptr, nullptr, nullptr, nullptr};
   std::vector<cudaEvent_t> pev;  // per-pass pairs for batched passes
   double t_leaf_ms = 0, t_energy_ms = 0;
+  // host wall clock (timing on): context rebuilds, sample gathers, the
+  // restructuring tail of a pass (after the leaf kernel)
+  double t_prep_ms = 0, t_gather_ms = 0, t_restr_ms = 0;
+  int64_t n_prep = 0, n_gather = 0;
   int64_t n_leaf = 0, n_energy = 0, launches = 0;
 
   // host pinned staging for small readbacks

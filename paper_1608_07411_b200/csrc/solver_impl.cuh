@@ -21,6 +21,7 @@
 // The pool (value/snap/child/joined/state) therefore ends every pass
 // identical to the reference's on live nodes.
 #pragma once
+#include <chrono>
 #include <cub/cub.cuh>
 
 #include "octf_arith.cuh"
@@ -137,6 +138,97 @@ __device__ T slow_dn(const int32_t* child, const T* snap, ViewSet vs,
       const T d = S0 - (T)vs.val[v][n];
       num += A::data_grad((T)w, d, p.eps2);
       den += (T)w;
+    }
+  }
+  const T du = p.lam * div - A::div(num, den);
+  return S0 + p.xi * du;
+}
+
+// slow_dn by one warp: lane k < 13 resolves stencil point k, lanes cover the
+// views (v = lane, lane + 32, ...); every lane then combines the shuffled
+// values in the reference's order (flux_at / slow_dn above, bit for bit),
+// so the dependent root-descent chain of one thread is ~1/30 as long.
+template <typename T>
+__device__ T warp_slow_dn(const int32_t* child, const T* snap, ViewSet vs,
+                          const LeafParams<T>& p, int L, int x, int y, int z,
+                          T S0, int lane) {
+  using A = Arith<T>;
+  const unsigned FULL = 0xffffffffu;
+  const int m = 1 << L;
+  // stencil points: 0 c, 1 +x, 2 +y, 3 +z, 4 -x, 5 -x+y, 6 -x+z, 7 -y,
+  // 8 +x-y, 9 -y+z, 10 -z, 11 +x-z, 12 +y-z
+  // offsets + 1 packed two bits per point (no local-memory tables)
+  constexpr unsigned KX = 0x1u | 2u << 2 | 1u << 4 | 1u << 6 | 0u << 8 |
+                          0u << 10 | 0u << 12 | 1u << 14 | 2u << 16 |
+                          1u << 18 | 1u << 20 | 2u << 22 | 1u << 24;
+  constexpr unsigned KY = 0x1u | 1u << 2 | 2u << 4 | 1u << 6 | 1u << 8 |
+                          2u << 10 | 1u << 12 | 0u << 14 | 0u << 16 |
+                          0u << 18 | 1u << 20 | 1u << 22 | 2u << 24;
+  constexpr unsigned KZ = 0x1u | 1u << 2 | 1u << 4 | 2u << 6 | 1u << 8 |
+                          1u << 10 | 2u << 12 | 1u << 14 | 1u << 16 |
+                          2u << 18 | 0u << 20 | 0u << 22 | 0u << 24;
+  T mine = 0;
+  if (lane < 13) {
+    const int sh = 2 * lane;
+    const int qx = x + (int)((KX >> sh) & 3u) - 1;
+    const int qy = y + (int)((KY >> sh) & 3u) - 1;
+    const int qz = z + (int)((KZ >> sh) & 3u) - 1;
+    if (qx >= 0 && qy >= 0 && qz >= 0 && qx < m && qy < m && qz < m)
+      mine = snap[descend(child, L, qx, qy, qz)];
+  }
+  T P[13];
+#pragma unroll
+  for (int k = 0; k < 13; ++k) P[k] = __shfl_sync(FULL, mine, k);
+  const T ih = inv_spacing<T>(p.d_max, L);
+  T q[3], r[3];
+  T bx = 0, by = 0, bz = 0;
+  {  // flux_at(x, y, z)
+    T gx = 0, gy = 0, gz = 0;
+    if (x + 1 < m) gx = (P[1] - P[0]) * ih;
+    if (y + 1 < m) gy = (P[2] - P[0]) * ih;
+    if (z + 1 < m) gz = (P[3] - P[0]) * ih;
+    A::flux(gx, gy, gz, p.eps2, q[0], q[1], q[2]);
+  }
+  if (x > 0) {  // flux_at(x-1, y, z): c = P4, +x = P0, +y = P5, +z = P6
+    T gx = (P[0] - P[4]) * ih, gy = 0, gz = 0;
+    if (y + 1 < m) gy = (P[5] - P[4]) * ih;
+    if (z + 1 < m) gz = (P[6] - P[4]) * ih;
+    A::flux(gx, gy, gz, p.eps2, r[0], r[1], r[2]);
+    bx = r[0];
+  }
+  if (y > 0) {  // flux_at(x, y-1, z): c = P7, +x = P8, +y = P0, +z = P9
+    T gx = 0, gy = (P[0] - P[7]) * ih, gz = 0;
+    if (x + 1 < m) gx = (P[8] - P[7]) * ih;
+    if (z + 1 < m) gz = (P[9] - P[7]) * ih;
+    A::flux(gx, gy, gz, p.eps2, r[0], r[1], r[2]);
+    by = r[1];
+  }
+  if (z > 0) {  // flux_at(x, y, z-1): c = P10, +x = P11, +y = P12, +z = P0
+    T gx = 0, gy = 0, gz = (P[0] - P[10]) * ih;
+    if (x + 1 < m) gx = (P[11] - P[10]) * ih;
+    if (y + 1 < m) gy = (P[12] - P[10]) * ih;
+    A::flux(gx, gy, gz, p.eps2, r[0], r[1], r[2]);
+    bz = r[2];
+  }
+  const T div = ((q[0] - bx) + (q[1] - by) + (q[2] - bz)) * ih;
+  T num = 0, den = p.gamma;
+  for (int v0 = 0; v0 < vs.n; v0 += 32) {
+    const int v = v0 + lane;
+    float w = 0.f;
+    T g = 0;
+    if (v < vs.n) {
+      const int32_t n = descend(vs.child[v], L, x, y, z);
+      w = vs.w[v][n];
+      if (w != 0.f) g = A::data_grad((T)w, S0 - (T)vs.val[v][n], p.eps2);
+    }
+    const int nk = vs.n - v0 < 32 ? vs.n - v0 : 32;
+    for (int k = 0; k < nk; ++k) {  // view order, as slow_dn
+      const float wk = __shfl_sync(FULL, w, k);
+      const T gk = __shfl_sync(FULL, g, k);
+      if (wk != 0.f) {
+        num += gk;
+        den += (T)wk;
+      }
     }
   }
   const T du = p.lam * div - A::div(num, den);
@@ -290,13 +382,16 @@ struct JoinRecs {
   int32_t* idx;
 };
 
+// candidates of one level: an inner node none of whose children is a live
+// inner node (leaf or joined this pass), all with |u| > tau_j and one sign
+// (_kernels.pyx:321-354, cheap tests first); its |dn| test follows in
+// k_join_dn, one warp per candidate
 template <typename T>
-__global__ void k_join_level(const int32_t* __restrict__ blocks, int64_t nblk,
-                             const int8_t* blevel, const uint64_t* bcoord,
-                             int32_t* child, uint8_t* joined,
-                             const uint8_t* smark, const T* snap, T* uval,
-                             ViewSet vs, LeafParams<T> p, JoinRecs<T> rec,
-                             int32_t* counters) {
+__global__ void k_join_cand(const int32_t* __restrict__ blocks, int64_t nblk,
+                            const int32_t* child, const uint8_t* joined,
+                            const uint8_t* smark, const T* uval,
+                            LeafParams<T> p, int32_t* cand, double* cacc,
+                            int32_t* ccount) {
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t i = gid >> 3;
   const int c = (int)(gid & 7);
@@ -320,17 +415,38 @@ __global__ void k_join_level(const int32_t* __restrict__ blocks, int64_t nblk,
     acc += v;
   }
   if (pos && neg) return;
-  int L, x, y, z;
-  slot_cell_of(s, blevel, bcoord, L, x, y, z);
-  const T dn = slow_dn<T>(child, snap, vs, p, L, x, y, z, snap[s]);
-  if (!(fabs((double)dn) > p.tau_j)) return;
-  joined[s] = 1;
-  uval[s] = (T)(acc / 8.0);
-  const int32_t r = atomicAdd(counters + 4, 1);
-  rec.slot[r] = s;
-  rec.blk[r] = cb;
-  rec.cell[r] = pack_cell(L, x, y, z);
-  for (int q = 0; q < 8; ++q) rec.vals[r * 8 + q] = (double)uval[cb + q];
+  const int32_t r = atomicAdd(ccount, 1);
+  cand[r] = s;
+  cacc[r] = acc;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+    k_join_dn(const int32_t* __restrict__ cand, const double* __restrict__ cacc,
+              const int32_t* __restrict__ ccount, const int8_t* blevel,
+              const uint64_t* bcoord, const int32_t* child, uint8_t* joined,
+              const T* snap, T* uval, ViewSet vs, LeafParams<T> p,
+              JoinRecs<T> rec, int32_t* counters) {
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (int)(gridDim.x * (blockDim.x >> 5));
+  const int n = *ccount;
+  for (int w = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
+       w < n; w += nwarps) {
+    const int32_t s = cand[w];
+    int L, x, y, z;
+    slot_cell_of(s, blevel, bcoord, L, x, y, z);
+    const T dn = warp_slow_dn<T>(child, snap, vs, p, L, x, y, z, snap[s], lane);
+    if (lane == 0 && fabs((double)dn) > p.tau_j) {
+      const int32_t cb = child[s];
+      joined[s] = 1;
+      uval[s] = (T)(cacc[w] / 8.0);
+      const int32_t r = atomicAdd(counters + 4, 1);
+      rec.slot[r] = s;
+      rec.blk[r] = cb;
+      rec.cell[r] = pack_cell(L, x, y, z);
+      for (int q = 0; q < 8; ++q) rec.vals[r * 8 + q] = (double)uval[cb + q];
+    }
+  }
 }
 
 template <typename T>
@@ -680,9 +796,9 @@ struct EventBufs {
 
 template <typename T>
 struct JoinBufs {
-  DevBuf<int32_t> slot, blk, idx;
+  DevBuf<int32_t> slot, blk, idx, cand;
   DevBuf<uint64_t> cell, key;
-  DevBuf<double> vals;
+  DevBuf<double> vals, cacc;
   JoinRecs<T> view(int64_t cap) {
     JoinRecs<T> r;
     r.slot = slot.ensure(cap);
@@ -742,6 +858,7 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
     c.t_leaf_ms += ms;
     ++c.n_leaf;
   }
+  const auto t_restr = std::chrono::steady_clock::now();
   const int64_t nsplit = c.h_counters[0];
   const int64_t ncand = c.h_counters[1];
   const T* snap = (const T*)a.usnap;
@@ -815,14 +932,28 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
     static thread_local JoinBufs<T> jb;
     const int64_t jcap_rec = c.nblocks * 8 + 8;
     JoinRecs<T> rec = jb.view(jcap_rec);
+    // per level (bottom-up): cheap candidate tests over the level's slots,
+    // then one warp per candidate for the root-descent update (no host
+    // round trip: the dn kernel strides over the device-side count)
+    int32_t* cand = jb.cand.ensure(c.nblocks * 8 + 8);
+    double* cacc = jb.cacc.ensure(c.nblocks * 8 + 8);
     for (int L = prm.d_max - 1; L >= 0; --L) {
       const int64_t n = c.lvl_cnt[L];
       if (n == 0) continue;
-      k_join_level<T><<<blocks_for(n * 8), kT, 0, st>>>(
-          c.lvl_blocks.p + c.lvl_off[L], n, c.blevel.p, c.bcoord.p, a.child,
-          a.joined, c.smark.p, snap, uval, vs, lp, rec, c.counters.p);
+      OCTF_CUDA(cudaMemsetAsync(c.counters.p + 8, 0, sizeof(int32_t), st));
+      k_join_cand<T><<<blocks_for(n * 8), kT, 0, st>>>(
+          c.lvl_blocks.p + c.lvl_off[L], n, a.child, a.joined, c.smark.p,
+          uval, lp, cand, cacc, c.counters.p + 8);
       OCTF_CUDA(cudaGetLastError());
-  ++c.launches;
+      const int64_t cmax = n * 8;
+      const unsigned gw = (unsigned)((cmax + 7) / 8 < 148 * 16 ? (cmax + 7) / 8
+                                                                : 148 * 16);
+      k_join_dn<T><<<gw, 256, 0, st>>>(cand, cacc, c.counters.p + 8,
+                                         c.blevel.p, c.bcoord.p, a.child,
+                                         a.joined, snap, uval, vs, lp, rec,
+                                         c.counters.p);
+      OCTF_CUDA(cudaGetLastError());
+      c.launches += 2;
     }
     read_counters<T>(c, 5, st);
     const int64_t J = c.h_counters[4];
@@ -880,6 +1011,9 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
   a.out3[0] = splits;
   a.out3[1] = joins;
   a.out3[2] = jrows;
+  if (c.timing)
+    c.t_restr_ms += std::chrono::duration<double, std::milli>(
+                        std::chrono::steady_clock::now() - t_restr).count();
 }
 
 // parent levels top .. 0 (default: every level above the finest) of `na`

@@ -367,19 +367,22 @@ def sphere_trace(sdf, cam: PinholeCamera, *, lipschitz: float, t_max: float,
     alive = torch.ones_like(t, dtype=torch.bool)
     hit = torch.zeros_like(alive)
     t_prev = t.clone()
-    for _ in range(steps):
-        idx = alive.nonzero().squeeze(1)
-        if idx.numel() == 0:
-            break
+    idx = alive.nonzero().squeeze(1)
+    for it in range(steps):
+        if it % 16 == 0:   # re-compact the live rays now and then (host sync)
+            idx = alive.nonzero().squeeze(1)
+            if idx.numel() == 0:
+                break
         sd = sdf(o + t[idx, None] * d[idx])
-        h = (sd < eps)
-        hit[idx[h]] = True
-        alive[idx[h]] = False
-        go = idx[~h]
-        t_prev[go] = t[go]
-        t[go] = t[go] + sd[~h] / (lipschitz * nrm[go])
-        far = t[go] > t_max
-        alive[go[far]] = False
+        a = alive[idx]
+        h = a & (sd < eps)
+        go = a & ~h
+        hit[idx] = hit[idx] | h
+        tp = t[idx]
+        tn = torch.where(go, tp + sd / (lipschitz * nrm[idx]), tp)
+        t_prev[idx] = torch.where(go, tp, t_prev[idx])
+        t[idx] = tn
+        alive[idx] = go & (tn <= t_max)
     # bisection between the last outside point and the hit point
     idx = hit.nonzero().squeeze(1)
     lo, hi = t_prev[idx], t[idx]

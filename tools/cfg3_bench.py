@@ -22,10 +22,21 @@ ap.add_argument("--passes", type=int, default=20)
 ap.add_argument("--precision", default="fp32")
 ap.add_argument("--views", type=int, default=64)
 ap.add_argument("--depth", type=int, default=9)
+ap.add_argument("--save-scene", default=None, help="pickle the rendered scene")
+ap.add_argument("--load-scene", default=None, help="reuse a pickled scene")
 args = ap.parse_args()
 
 t0 = time.time()
-sc = scenes.make_cfg3(d_max=args.depth, n_views=args.views, device="cuda")
+if args.load_scene:
+    import pickle
+    with open(args.load_scene, "rb") as fp:
+        sc = pickle.load(fp)
+else:
+    sc = scenes.make_cfg3(d_max=args.depth, n_views=args.views, device="cuda")
+if args.save_scene:
+    import pickle
+    with open(args.save_scene, "wb") as fp:
+        pickle.dump(sc, fp)
 torch.cuda.synchronize()
 t_render = time.time() - t0
 p = fusion.FusionParams(**dict(sc.params, iterations=args.passes))
@@ -47,8 +58,12 @@ for t in range(args.passes):
     st = s.step(t)
     e1.record()
     torch.cuda.synchronize()
+    pr = s.ctx.profile(True)
     passes.append({"ms": e0.elapsed_time(e1), "nodes": st.node_count,
-                   "splits": st.splits, "joins": st.joins})
+                   "splits": st.splits, "joins": st.joins,
+                   "leaf_ms": pr["leaf_ms"], "prepare_ms": pr["prepare_ms"],
+                   "gather_ms": pr["gather_ms"],
+                   "restructure_ms": pr["restructure_ms"]})
 prof = s.ctx.profile(False)
 res = s.result()
 h = res.field.to_host()
@@ -65,6 +80,6 @@ out = {"workload": "cfg3 adaptive object (BASELINE config 2)",
        "median_pass_ms": ms,
        "leaf_updates_per_s": lv[-1] / (ms / 1e3),
        "leaf_kernel_ms_per_pass": prof["leaf_ms"] / max(prof["leaf_launches"], 1),
-       "launches": prof["launches"],
+       "profile": prof,
        "passes": passes}
 print(json.dumps(out))

@@ -140,6 +140,8 @@ int octf_ctx_invalidate(octf_ctx* ctx) {
   if (ctx) {
     ctx->c.valid = false;
     ctx->c.free_ok = false;
+    ctx->c.own_change = false;
+    ctx->c.store_ok = false;
     ctx->c.vkey.clear();
     if (!ctx->c.ext_F) ctx->c.nviews = 0;
   }

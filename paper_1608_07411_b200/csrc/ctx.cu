@@ -9,6 +9,7 @@
 // per-view samples (the reference's per-view cursors, _kernels.pyx:265-273)
 // gathered into a coalesced [view][leaf] store.
 #include <chrono>
+#include <cstdlib>
 #include <cub/cub.cuh>
 
 #include "octf_ctx.h"
@@ -23,6 +24,8 @@ void check_cuda(cudaError_t e, const char* what) {
 }
 
 Ctx::Ctx() {
+  const char* fg = std::getenv("OCTF_FULL_GATHER");
+  no_regather = fg && fg[0] == '1';
   OCTF_CUDA(cudaMallocHost((void**)&h_counters, 64 * sizeof(int32_t)));
   OCTF_CUDA(cudaMallocHost((void**)&h_scalar, 8 * sizeof(double)));
 }
@@ -118,6 +121,15 @@ __global__ void k_leaf_tables(const int32_t* __restrict__ child,
   int d = (int)(gid % 12);
   if (i >= nlb) return;
   int32_t b = lblocks[i];
+  if (b < 0) {  // hole of a patched list: no active slot
+    if (d == 0) {
+      lkey[i] = 0;
+      lmeta[i] = make_int4(0, 0, 0, pack_meta_w(0, 0u, 0));
+      lpar[i] = -1;
+    }
+    nbr[i * 12 + d] = kNone;
+    return;
+  }
   int k = block_id(b);
   int L = b == 0 ? 0 : blevel[k];
   int pL, px, py, pz;
@@ -208,6 +220,166 @@ __global__ void k_gather_slots(const int32_t* __restrict__ ucs,
     W[samp_idx(gid, v, stride)] = w;
   }
   if (flag) atomicExch(nonbin, 1);
+}
+
+// ---- stable leaf-block list (ctx_list_update) ----
+__device__ __forceinline__ unsigned leaf_mask_of(const int32_t* child,
+                                                 int32_t b) {
+  if (b == 0) return child[0] < 0 ? 1u : 0u;
+  unsigned m = 0;
+  for (int c = 0; c < 8; ++c) m |= (child[b + c] < 0 ? 1u : 0u) << c;
+  return m;
+}
+
+// listed blocks that were freed or hold no leaf any more become holes; the
+// previous leaf masks are kept for the sample update.  A listed block that
+// is still live is the same block at the same cell: live blocks never move,
+// and a block freed by a pass is reused only by a later pass.
+__global__ void k_list_mark(int32_t* lblocks, const int4* __restrict__ lmeta,
+                            int64_t n, const int32_t* __restrict__ child,
+                            const int8_t* __restrict__ blevel, int32_t* lpos,
+                            uint8_t* oldmask, int32_t* nholes) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t b = lblocks[i];
+  if (b < 0) {
+    oldmask[i] = 0;
+    return;
+  }
+  int pz, L;
+  unsigned om;
+  unpack_meta_w(lmeta[i].w, pz, om, L);
+  oldmask[i] = (uint8_t)om;
+  const int k = block_id(b);
+  const unsigned nm = blevel[k] >= 0 ? leaf_mask_of(child, b) : 0u;
+  if (!nm) {
+    lblocks[i] = -1;
+    lpos[k] = -1;
+    atomicAdd(nholes, 1);
+  }
+}
+
+// live leaf blocks not in the list yet
+__global__ void k_list_new(const int32_t* __restrict__ blocks, int64_t total,
+                           const int32_t* __restrict__ child,
+                           const int32_t* __restrict__ lpos, int32_t* out,
+                           int32_t* cnt) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= total) return;
+  const int32_t b = blocks[j];
+  if (lpos[block_id(b)] < 0 && leaf_mask_of(child, b))
+    out[atomicAdd(cnt, 1)] = b;
+}
+
+__global__ void k_list_put(const int32_t* __restrict__ in, int64_t a,
+                           int64_t base, int32_t* lblocks, int32_t* lpos) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= a) return;
+  const int32_t b = in[r];
+  lblocks[base + r] = b;
+  lpos[block_id(b)] = (int32_t)(base + r);
+}
+
+__global__ void k_set_lpos(const int32_t* __restrict__ lblocks, int64_t n,
+                           int32_t* lpos) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t b = lblocks[i];
+  if (b >= 0) lpos[block_id(b)] = (int32_t)i;
+}
+
+// per slot of the patched list: a leaf that was a leaf at the same position
+// keeps its samples; a new leaf is queued for k_gather_fresh; any other slot
+// is zeroed (as k_gather leaves non-leaf slots)
+template <bool BINW>
+__global__ void k_sample_update(const int32_t* __restrict__ lblocks,
+                                const int4* __restrict__ lmeta, int64_t n,
+                                int64_t nold,
+                                const uint8_t* __restrict__ oldmask,
+                                int64_t stride, float* F, float* W,
+                                uint32_t* M, int32_t* fresh, int32_t* nfresh,
+                                int32_t* nleaves) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = gid >> 3;
+  const int c = (int)(gid & 7);
+  if (i >= n) return;
+  const int32_t b = lblocks[i];
+  unsigned nm = 0;
+  if (b >= 0) {
+    int pz, L;
+    unpack_meta_w(lmeta[i].w, pz, nm, L);
+  }
+  const bool now = b >= 0 && !(b == 0 && c != 0) && ((nm >> c) & 1u);
+  const bool was = i < nold && ((oldmask[i] >> c) & 1u);
+  if (c == 0 && nm) atomicAdd(nleaves, __popc(nm));
+  const int64_t s = i * 8 + c;
+  if (now && !was) {
+    fresh[atomicAdd(nfresh, 1)] = (int32_t)s;
+  } else if (!now && (was || i >= nold)) {
+    for (int v = 0; v < stride; ++v) {
+      F[samp_idx(s, v, stride)] = 0.f;
+      if (!BINW) W[samp_idx(s, v, stride)] = 0.f;
+    }
+    if (BINW) M[s] = 0u;
+  }
+}
+
+// zero the store slots [from, to) (tile padding after the last entry)
+template <bool BINW>
+__global__ void k_zero_slots(int64_t from, int64_t to, int64_t stride,
+                             float* F, float* W, uint32_t* M) {
+  const int64_t s = from + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= to) return;
+  for (int v = 0; v < stride; ++v) {
+    F[samp_idx(s, v, stride)] = 0.f;
+    if (!BINW) W[samp_idx(s, v, stride)] = 0.f;
+  }
+  if (BINW) M[s] = 0u;
+}
+
+// samples of the leaves k_sample_update queued: one warp per leaf, lanes over
+// views, so each lane walks one root descent instead of one per view
+template <bool BINW>
+__global__ void k_gather_fresh(const int32_t* __restrict__ fresh,
+                               const int32_t* __restrict__ nfresh,
+                               const int4* __restrict__ lmeta, ViewSet vs,
+                               int64_t stride, float* F, float* W, uint32_t* M,
+                               int32_t* nonbin) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (int)(gridDim.x * (blockDim.x >> 5));
+  const int n = *nfresh;
+  for (int k = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
+       k < n; k += nw) {
+    const int64_t s = fresh[k];
+    const int4 m = lmeta[s >> 3];
+    const int c = (int)(s & 7);
+    const int32_t b = m.x;
+    int L, pz;
+    unsigned mask;
+    unpack_meta_w(m.w, pz, mask, L);
+    const int x = b == 0 ? 0 : 2 * m.y + ((c >> 2) & 1);
+    const int y = b == 0 ? 0 : 2 * m.z + ((c >> 1) & 1);
+    const int z = b == 0 ? 0 : 2 * pz + (c & 1);
+    uint32_t bits = 0;
+    int flag = 0;
+    for (int v0 = 0; v0 < stride; v0 += 32) {
+      const int v = v0 + lane;
+      float f = 0.f, w = 0.f;
+      if (v < vs.n) {
+        const int32_t nd = descend(vs.child[v], L, x, y, z);
+        f = vs.val[v][nd];
+        w = vs.w[v][nd];
+        flag |= (w != 0.f && w != 1.f);
+      }
+      if (v < stride) {
+        F[samp_idx(s, v, stride)] = f;
+        if (!BINW) W[samp_idx(s, v, stride)] = w;
+      }
+      if (BINW) bits |= __ballot_sync(0xffffffffu, w != 0.f);
+    }
+    if (BINW && lane == 0) M[s] = bits;
+    if (__any_sync(0xffffffffu, flag) && lane == 0) atomicExch(nonbin, 1);
+  }
 }
 
 __global__ void k_masks(const float* __restrict__ W, int64_t stride, int nv,
@@ -303,6 +475,14 @@ void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
   if (used < 1 || used > cap)
     throw Error(kEArg, "pool state is inconsistent with its capacity");
   int64_t nbid = block_id(used) + 1;
+  // patch the leaf-block list in place when this rebuild follows our own
+  // restructuring of the same pool (ctx_list_update)
+  const bool incremental = !c.no_regather && c.own_change && c.store_ok &&
+                           c.list_full && c.nviews > 0 && !c.ext_F &&
+                           c.child_key == child && c.cap == cap &&
+                           c.d_max == d_max;
+  c.own_change = false;
+  c.store_ok = false;
   c.blevel.ensure(nbid);
   c.bcoord.ensure(nbid);
   c.bparent.ensure(nbid);
@@ -345,6 +525,38 @@ void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
   // a finest-level node must be a leaf
   // (checked implicitly: blocks at level d_max are never expanded)
 
+  const bool patched =
+      incremental && ctx_list_update(c, child, total, nbid, st);
+  if (!patched) ctx_list_full(c, child, total, nbid, st);
+
+  c.smark.ensure(cap);
+  OCTF_CUDA(cudaMemsetAsync(c.smark.p, 0, cap, st));
+  // the free-list mirror survives our own restructuring (passes pop and
+  // push it); walk the pool's linked free list only for a foreign pool
+  if (!c.free_ok || c.child_key != child || c.nfree_head != state[1]) {
+    ctx_free_stack(c, child, state, st);
+    c.free_ok = true;
+  }
+  c.child_key = child;
+  c.cap = cap;
+  c.d_max = d_max;
+  c.hstate[0] = state[0];
+  c.hstate[1] = state[1];
+  c.hstate[2] = state[2];
+  c.valid = true;
+  if (c.nviews > 0 && !patched) ctx_gather(c, st);
+  OCTF_CUDA(cudaStreamSynchronize(st));
+  if (c.timing) {
+    c.t_prep_ms += std::chrono::duration<double, std::milli>(
+                       std::chrono::steady_clock::now() - t0).count();
+    ++c.n_prep;
+  }
+}
+
+// the sorted leaf-block list of every live block holding a leaf, its tables
+// and the block -> position map
+void ctx_list_full(Ctx& c, const int32_t* child, int64_t total, int64_t nbid,
+                   cudaStream_t st) {
   // leaf blocks, ascending base slot
   uint8_t* flags = c.flags.ensure(total);
   c.lblocks.ensure(total);
@@ -373,29 +585,115 @@ void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
       child, c.lblocks.p, c.nlb, c.blevel.p, c.bcoord.p, c.bparent.p,
       c.lkey.p, c.lmeta.p, c.lpar.p, c.nbr.p);
   OCTF_CUDA(cudaGetLastError());
+  c.lpos.ensure(nbid);
+  OCTF_CUDA(cudaMemsetAsync(c.lpos.p, 0xff, nbid * sizeof(int32_t), st));
+  if (c.nlb)
+    k_set_lpos<<<grid_for(c.nlb), kThreads, 0, st>>>(c.lblocks.p, c.nlb,
+                                                     c.lpos.p);
+  OCTF_CUDA(cudaGetLastError());
+  c.lpos_n = nbid;
+  c.nholes = 0;
+  c.list_full = true;
+}
 
-  c.smark.ensure(cap);
-  OCTF_CUDA(cudaMemsetAsync(c.smark.p, 0, cap, st));
-  // the free-list mirror survives our own restructuring (passes pop and
-  // push it); walk the pool's linked free list only for a foreign pool
-  if (!c.free_ok || c.child_key != child || c.nfree_head != state[1]) {
-    ctx_free_stack(c, child, state, st);
-    c.free_ok = true;
+// patch the list after our own restructure (see Ctx::lpos): holes for
+// blocks without leaves, appended new leaf blocks, all tables recomputed,
+// samples kept where a leaf stayed at its position and gathered for new
+// leaves.  false: compaction due (or a fractional weight met the mask
+// format): the caller rebuilds everything.
+bool ctx_list_update(Ctx& c, const int32_t* child, int64_t total, int64_t nbid,
+                     cudaStream_t st) {
+  const auto t0 = std::chrono::steady_clock::now();
+  const int64_t nold = c.nlb;
+  if (c.lpos_n < nbid) {  // block ids the pool grew by start unlisted
+    c.lpos.grow_keep(nbid, c.lpos_n, st);
+    OCTF_CUDA(cudaMemsetAsync(c.lpos.p + c.lpos_n, 0xff,
+                              (nbid - c.lpos_n) * sizeof(int32_t), st));
+    c.lpos_n = nbid;
   }
-  c.child_key = child;
-  c.cap = cap;
-  c.d_max = d_max;
-  c.hstate[0] = state[0];
-  c.hstate[1] = state[1];
-  c.hstate[2] = state[2];
-  c.valid = true;
-  if (c.nviews > 0) ctx_gather(c, st);
+  uint8_t* oldmask = c.flags.ensure(nold > total ? nold : total);
+  int32_t* app = c.app_buf.ensure(total + 1);
+  OCTF_CUDA(cudaMemsetAsync(c.counters.p, 0, 8 * sizeof(int32_t), st));
+  if (nold)
+    k_list_mark<<<grid_for(nold), kThreads, 0, st>>>(
+        c.lblocks.p, c.lmeta.p, nold, child, c.blevel.p, c.lpos.p, oldmask,
+        c.counters.p);
+  k_list_new<<<grid_for(total), kThreads, 0, st>>>(
+      c.lvl_blocks.p, total, child, c.lpos.p, app, c.counters.p + 1);
+  OCTF_CUDA(cudaGetLastError());
+  OCTF_CUDA(cudaMemcpyAsync(c.h_counters, c.counters.p, 2 * sizeof(int32_t),
+                            cudaMemcpyDeviceToHost, st));
   OCTF_CUDA(cudaStreamSynchronize(st));
-  if (c.timing) {
-    c.t_prep_ms += std::chrono::duration<double, std::milli>(
-                       std::chrono::steady_clock::now() - t0).count();
-    ++c.n_prep;
+  c.nholes += c.h_counters[0];
+  const int64_t na = c.h_counters[1];
+  const int64_t nnew = nold + na;
+  if (4 * c.nholes > nnew || 4 * na > nnew) return false;  // compact
+  if (na) {
+    sort_i32(c, app, na, st);  // appended in base order: deterministic
+    c.lblocks.grow_keep(nnew, nold, st);
+    k_list_put<<<grid_for(na), kThreads, 0, st>>>(app, na, nold, c.lblocks.p,
+                                                   c.lpos.p);
+    OCTF_CUDA(cudaGetLastError());
   }
+  c.lkey.ensure(nnew);
+  c.lmeta.ensure(nnew);
+  c.lpar.ensure(nnew);
+  c.nbr.ensure(nnew * 12);
+  k_leaf_tables<<<grid_for(nnew * 12), kThreads, 0, st>>>(
+      child, c.lblocks.p, nnew, c.blevel.p, c.bcoord.p, c.bparent.p, c.lkey.p,
+      c.lmeta.p, c.lpar.p, c.nbr.p);
+  OCTF_CUDA(cudaGetLastError());
+  // samples, in place (the store only grows; its tail is zeroed)
+  const int64_t nvp = c.sstride;
+  auto pad = [](int64_t n) {
+    return (n * 8 + kTileLeaves - 1) / kTileLeaves * kTileLeaves;
+  };
+  const int64_t npo = pad(nold), npn = pad(nnew);
+  c.F.grow_keep((size_t)nvp * npn, (size_t)nvp * npo, st);
+  if (c.binw) c.M.grow_keep(npn, npo, st);
+  else c.W.grow_keep((size_t)nvp * npn, (size_t)nvp * npo, st);
+  int32_t* fresh = c.sort_v32.ensure(nnew * 8 + 1);
+  if (c.binw)
+    k_sample_update<true><<<grid_for(nnew * 8), kThreads, 0, st>>>(
+        c.lblocks.p, c.lmeta.p, nnew, nold, oldmask, nvp, c.F.p, nullptr,
+        c.M.p, fresh, c.counters.p + 2, c.counters.p + 4);
+  else
+    k_sample_update<false><<<grid_for(nnew * 8), kThreads, 0, st>>>(
+        c.lblocks.p, c.lmeta.p, nnew, nold, oldmask, nvp, c.F.p, c.W.p,
+        nullptr, fresh, c.counters.p + 2, c.counters.p + 4);
+  if (npn > nnew * 8) {
+    const int64_t from = nnew * 8, to = npn;
+    if (c.binw)
+      k_zero_slots<true><<<grid_for(to - from), kThreads, 0, st>>>(
+          from, to, nvp, c.F.p, nullptr, c.M.p);
+    else
+      k_zero_slots<false><<<grid_for(to - from), kThreads, 0, st>>>(
+          from, to, nvp, c.F.p, c.W.p, nullptr);
+  }
+  const unsigned gw = 148 * 8;  // warps stride over the queued leaves
+  if (c.binw)
+    k_gather_fresh<true><<<gw, kThreads, 0, st>>>(
+        fresh, c.counters.p + 2, c.lmeta.p, ctx_views(c), nvp, c.F.p, nullptr,
+        c.M.p, c.counters.p + 3);
+  else
+    k_gather_fresh<false><<<gw, kThreads, 0, st>>>(
+        fresh, c.counters.p + 2, c.lmeta.p, ctx_views(c), nvp, c.F.p, c.W.p,
+        nullptr, c.counters.p + 3);
+  OCTF_CUDA(cudaGetLastError());
+  OCTF_CUDA(cudaMemcpyAsync(c.h_counters, c.counters.p, 8 * sizeof(int32_t),
+                            cudaMemcpyDeviceToHost, st));
+  OCTF_CUDA(cudaStreamSynchronize(st));
+  if (c.binw && c.h_counters[3]) return false;  // needs the weight format
+  c.nlb = nnew;
+  c.nleaves = c.h_counters[4];
+  c.store_ok = true;
+  if (c.timing) {
+    c.t_gather_ms += std::chrono::duration<double, std::milli>(
+                         std::chrono::steady_clock::now() - t0).count();
+    ++c.n_gather;
+    ++c.n_regather;
+  }
+  return true;
 }
 
 void ctx_set_views(Ctx& c, int nviews, const float* const* vval,
@@ -483,6 +781,7 @@ void ctx_gather(Ctx& c, cudaStream_t st) {
   } else {
     c.M.release();
   }
+  c.store_ok = true;
   if (c.timing) {
     c.t_gather_ms += std::chrono::duration<double, std::milli>(
                          std::chrono::steady_clock::now() - t0).count();
@@ -547,6 +846,7 @@ void ctx_select(Ctx& c, const int32_t* sel, const uint8_t* masks, int64_t nsel,
   c.lpar.swap(opar);
   c.nbr.swap(onbr);
   c.nlb = nsel;
+  c.list_full = false;  // a shard's subset: never patched in place
   if (c.nviews > 0) ctx_gather(c, st);
   OCTF_CUDA(cudaStreamSynchronize(st));
 }

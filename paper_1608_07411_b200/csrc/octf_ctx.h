@@ -123,6 +123,19 @@ struct Ctx {
   DevBuf<uint32_t> M;         // [sample] bit v = weight of view v is 1
   bool binw = false;          // samples use the mask format
   int64_t sstride = 0;        // views per leaf vector, padded to 4
+  bool store_ok = false;      // F/W/M describe the current leaf-block list
+  bool own_change = false;    // invalid only because our pass restructured
+  bool no_regather = false;   // env OCTF_FULL_GATHER=1: always rebuild all
+  // stable leaf-block list (ctx_list_update): after our own restructure the
+  // list is patched in place -- blocks that lost their leaves become holes,
+  // new leaf blocks are appended -- so unchanged leaves keep their list
+  // position and samples; a full sorted rebuild compacts it when holes or
+  // appended entries pass a quarter of the list
+  DevBuf<int32_t> lpos;       // per block id: list position or -1
+  int64_t lpos_n = 0;         // block ids lpos covers
+  int64_t nholes = 0;
+  bool list_full = false;     // list = every leaf block (not a shard subset)
+  DevBuf<int32_t> app_buf;    // appended blocks scratch
 
   // ---- or samples supplied per slot by the caller (frozen trees only)
   const float* ext_F = nullptr;  // [view][ext_cap]
@@ -159,7 +172,7 @@ struct Ctx {
   // host wall clock (timing on): context rebuilds, sample gathers, the
   // restructuring tail of a pass (after the leaf kernel)
   double t_prep_ms = 0, t_gather_ms = 0, t_restr_ms = 0;
-  int64_t n_prep = 0, n_gather = 0;
+  int64_t n_prep = 0, n_gather = 0, n_regather = 0;
   int64_t n_leaf = 0, n_energy = 0, launches = 0;
 
   // host pinned staging for small readbacks
@@ -178,6 +191,10 @@ void ctx_set_views(Ctx& c, int nviews, const float* const* vval,
                    const float* const* vw, const int32_t* const* vchild,
                    cudaStream_t st);
 void ctx_gather(Ctx& c, cudaStream_t st);
+void ctx_list_full(Ctx& c, const int32_t* child, int64_t total, int64_t nbid,
+                   cudaStream_t st);
+bool ctx_list_update(Ctx& c, const int32_t* child, int64_t total, int64_t nbid,
+                     cudaStream_t st);  // false: rebuild with ctx_list_full
 void ctx_set_samples(Ctx& c, const float* F, const float* W, int nviews,
                      int64_t cap, cudaStream_t st);
 void ctx_free_stack(Ctx& c, const int32_t* child, const int64_t* state,

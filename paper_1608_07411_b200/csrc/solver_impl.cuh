@@ -1006,7 +1006,10 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
   c.hstate[1] = a.state[1];
   c.hstate[2] = a.state[2];
   c.nfree_head = a.state[1];  // the free-list mirror was kept in step
-  if (changed) c.valid = false;
+  if (changed) {
+    c.valid = false;
+    c.own_change = true;  // the next rebuild may keep unchanged samples
+  }
   OCTF_CUDA(cudaStreamSynchronize(st));
   a.out3[0] = splits;
   a.out3[1] = joins;

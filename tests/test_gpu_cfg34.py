@@ -77,3 +77,31 @@ def test_cfg4_reduced_end_to_end():
                           focal=262.5, device="cuda")
     res, ref, _ = run_case(sc, 4)
     assert sum(s.splits + s.joins for s in ref.stats) > 0
+
+
+def test_incremental_regather_equals_full_gather(monkeypatch):
+    """After a restructuring pass the context keeps unchanged leaves' samples
+    and gathers only new leaves (ctx_regather); forcing full gathers
+    (OCTF_FULL_GATHER=1) must give the same trajectory bit for bit."""
+    from paper_1608_07411_b200 import fusion, scenes, volume
+    sc = scenes.make_cfg3(d_max=6, n_views=8, width=160, height=120,
+                          focal=131.25, device="cuda")
+    p = fusion.FusionParams(**dict(sc.params, iterations=6))
+    dom = volume.VolumeDomain(sc.origin, sc.voxel_size, sc.resolution)
+    views, u0, _ = fusion.prepare(sc.depths, sc.cameras, dom, p)
+    outs = []
+    for full in ("0", "1"):
+        monkeypatch.setenv("OCTF_FULL_GATHER", full)
+        s = fusion.Solver(u0, views, p, precision="fp32")
+        s.ctx.profile(True)
+        s.run(0, 6)
+        prof = s.ctx.profile(False)
+        r = s.result()
+        outs.append((r.field.to_host(), [(q.splits, q.joins) for q in r.stats],
+                     prof))
+        s.close()
+    (a, sa, pa), (b, sb, pb) = outs
+    assert sa == sb and sum(x + y for x, y in sa) > 0
+    assert np.array_equal(a.child[:a.used], b.child[:b.used])
+    assert np.array_equal(a.value[:a.used], b.value[:b.used])
+    assert pa["gathers"] >= 2   # restructured passes were regathered

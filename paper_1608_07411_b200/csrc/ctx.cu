@@ -90,6 +90,44 @@ __global__ void k_expand(const int32_t* __restrict__ child,
   next[pos] = nb;
 }
 
+// k_expand without a host round trip per level: the level's range comes
+// from device counters (dcnt, doff), the next level's start is written by
+// thread 0; the grid is an upper bound of the level's size
+__global__ void k_expand_dev(const int32_t* __restrict__ child,
+                             int32_t* lvl_blocks, int L, int64_t used,
+                             int64_t cap_blocks, int8_t* blevel,
+                             uint64_t* bcoord, int32_t* bparent, int32_t* dcnt,
+                             int32_t* doff, int32_t* bad) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = dcnt[L];
+  const int64_t next = (int64_t)doff[L] + n;
+  if (gid == 0) doff[L + 1] = (int32_t)next;
+  const int64_t i = gid >> 3;
+  const int c = (int)(gid & 7);
+  if (i >= n) return;
+  const int32_t b = lvl_blocks[doff[L] + i];
+  if (b == 0 && c != 0) return;
+  const int32_t s = b + c;
+  const int32_t nb = child[s];
+  if (nb < 0) return;
+  if (nb + 8 > used || (nb & 7) != 1) {
+    atomicExch(bad, 1);
+    return;
+  }
+  int x, y, z;
+  slot_cell(b, c, bcoord[block_id(b)], x, y, z);
+  const int k = block_id(nb);
+  blevel[k] = (int8_t)(L + 1);
+  bcoord[k] = pack_cell(L, x, y, z);
+  bparent[k] = s;
+  const int64_t pos = next + atomicAdd(dcnt + L + 1, 1);
+  if (pos >= cap_blocks) {
+    atomicExch(bad, 1);
+    return;
+  }
+  lvl_blocks[pos] = nb;
+}
+
 __global__ void k_leaf_flags(const int32_t* __restrict__ child,
                              const int32_t* __restrict__ blocks, int64_t nblk,
                              uint8_t* flags, int32_t* nleaves) {
@@ -302,16 +340,22 @@ __global__ void k_sample_update(const int32_t* __restrict__ lblocks,
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t i = gid >> 3;
   const int c = (int)(gid & 7);
-  if (i >= n) return;
-  const int32_t b = lblocks[i];
+  const bool in = i < n;
+  const int32_t b = in ? lblocks[i] : -1;
   unsigned nm = 0;
   if (b >= 0) {
     int pz, L;
     unpack_meta_w(lmeta[i].w, pz, nm, L);
   }
+  {  // leaf count: one atomic per warp (every lane reaches the shuffle)
+    int cnt = (c == 0) ? __popc(nm) : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(nleaves, cnt);
+  }
+  if (!in) return;
   const bool now = b >= 0 && !(b == 0 && c != 0) && ((nm >> c) & 1u);
   const bool was = i < nold && ((oldmask[i] >> c) & 1u);
-  if (c == 0 && nm) atomicAdd(nleaves, __popc(nm));
   const int64_t s = i * 8 + c;
   if (now && !was) {
     fresh[atomicAdd(nfresh, 1)] = (int32_t)s;
@@ -498,29 +542,38 @@ void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
                             st));
   c.lvl_off.assign(d_max + 2, 0);
   c.lvl_cnt.assign(d_max + 2, 0);
-  c.lvl_cnt[0] = 1;
-  int64_t total = 1;
+  // top-down walk, one launch per level, counts kept on the device and read
+  // once at the end (counters: [0] bad link, [8..] counts, [8+d_max+2..]
+  // offsets)
+  c.counters.ensure(8 + 2 * (kMaxDepth + 2));
+  int32_t* dcnt = c.counters.p + 8;
+  int32_t* doff = dcnt + (d_max + 2);
+  OCTF_CUDA(cudaMemsetAsync(c.counters.p, 0,
+                            (8 + 2 * (d_max + 2)) * sizeof(int32_t), st));
+  const int32_t one = 1;
+  OCTF_CUDA(cudaMemcpyAsync(dcnt, &one, sizeof(int32_t), cudaMemcpyHostToDevice,
+                            st));
   for (int L = 0; L < d_max; ++L) {
-    int64_t n = c.lvl_cnt[L];
-    c.lvl_off[L + 1] = total;
-    if (n == 0) break;
-    OCTF_CUDA(cudaMemsetAsync(c.counters.p, 0, 2 * sizeof(int32_t), st));
-    k_expand<<<grid_for(n * 8), kThreads, 0, st>>>(
-        child, c.lvl_blocks.p + c.lvl_off[L], n, L, used, c.blevel.p,
-        c.bcoord.p, c.bparent.p, c.lvl_blocks.p + total, c.counters.p,
-        c.counters.p + 1);
+    // level L holds at most min(8^L, live blocks) blocks
+    const int64_t bound = L < 7 ? std::min<int64_t>(int64_t(1) << (3 * L), nbid)
+                                : nbid;
+    k_expand_dev<<<grid_for(bound * 8), kThreads, 0, st>>>(
+        child, c.lvl_blocks.p, L, used, nbid + 1, c.blevel.p, c.bcoord.p,
+        c.bparent.p, dcnt, doff, c.counters.p);
     OCTF_CUDA(cudaGetLastError());
-    OCTF_CUDA(cudaMemcpyAsync(c.h_counters, c.counters.p, 2 * sizeof(int32_t),
-                              cudaMemcpyDeviceToHost, st));
-    OCTF_CUDA(cudaStreamSynchronize(st));
-    if (c.h_counters[1]) throw Error(kEArg, "corrupt child links in pool");
-    int64_t m = c.h_counters[0];
-    if (total + m > nbid) throw Error(kEArg, "corrupt child links in pool");
-    // (no sort: level lists are only scanned by order-independent kernels;
-    // the leaf-block list is sorted below)
-    c.lvl_cnt[L + 1] = m;
-    total += m;
   }
+  OCTF_CUDA(cudaMemcpyAsync(c.h_counters, c.counters.p,
+                            (8 + 2 * (d_max + 2)) * sizeof(int32_t),
+                            cudaMemcpyDeviceToHost, st));
+  OCTF_CUDA(cudaStreamSynchronize(st));
+  if (c.h_counters[0]) throw Error(kEArg, "corrupt child links in pool");
+  int64_t total = 0;
+  for (int L = 0; L <= d_max; ++L) {
+    c.lvl_cnt[L] = c.h_counters[8 + L];
+    c.lvl_off[L] = c.h_counters[8 + (d_max + 2) + L];
+    total += c.lvl_cnt[L];
+  }
+  if (total > nbid) throw Error(kEArg, "corrupt child links in pool");
   c.nblocks = total;
   // a finest-level node must be a leaf
   // (checked implicitly: blocks at level d_max are never expanded)

@@ -78,8 +78,11 @@ struct DevBuf {
   }
   T* ensure(size_t count) {
     if (count <= n && p) return p;
+    // a buffer that has to grow again gets 1/8 headroom, so structures that
+    // creep up pass by pass (patched leaf lists) do not reallocate each time
+    const size_t grown = p ? count + count / 8 : count;
     release();
-    size_t c = count ? count : 1;
+    size_t c = grown ? grown : 1;
     cudaError_t e = cudaMalloc((void**)&p, c * sizeof(T));
     if (e != cudaSuccess) {
       p = nullptr;

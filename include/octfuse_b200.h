@@ -137,6 +137,22 @@ int octf_pd_passes(octf_ctx *ctx, int dtype, void *const *set_a,
                    double tau, double sigma, double gamma, int clamp,
                    int npasses, double *energies_pre, void *stream);
 
+/* solver="pd" split/join on the current set {u, ubar, px, py, pz} after a
+ * pass (north_star item (d); definition oracle/pd_oracle.c
+ * orc_pd_restructure -- the reference has no primal-dual mode): leaves with
+ * |u| < tau_split and level < d_max get eight children carrying their u,
+ * ubar, p; inner nodes whose eight children are leaves past tau_join with one
+ * sign become leaves (their propagated means stay).  Splits claim blocks in
+ * depth-first order from the free list then the bump pointer, joined blocks
+ * are freed in post-order, as the descent pass (_kernels.pyx:277-381).
+ * ustate is updated; out2 = {splits, joins}.  The context must hold the
+ * structure of the last pass (octf_pd_passes); OCTF_EPOOL leaves the pool
+ * untouched. */
+int octf_pd_restructure(octf_ctx *ctx, int dtype, void *const *set,
+                        int32_t *uchild, int64_t *ustate, int64_t cap,
+                        int d_max, double tau_split, double tau_join,
+                        int64_t *out2, void *stream);
+
 /* Build the context's structures for a pool (and views) up front. */
 int octf_ctx_prepare(octf_ctx *ctx, const int32_t *uchild,
                      const int64_t *ustate, int64_t cap, int d_max, int nviews,

@@ -72,6 +72,12 @@ int orc_pd_pass(const double *u, const double *ub, const double *px,
                 const int32_t *const *vchild, int d_max, double lam, double tau,
                 double sigma, double gamma, int clamp, double *energy);
 
+/* pd-mode split/join after a pass (definition in pd_oracle.c); out2 =
+ * {splits, joins} */
+int orc_pd_restructure(double *u, double *ub, double *px, double *py,
+                       double *pz, int32_t *child, int64_t *state, int64_t cap,
+                       int d_max, double tau_s, double tau_j, int64_t *out2);
+
 #ifdef __cplusplus
 }
 #endif

@@ -65,6 +65,7 @@ def lib():
                                       P]
         L.orc_pd_pass.argtypes = [P] * 10 + [P, i64, i32, P, P, P, i32, dbl,
                                              dbl, dbl, dbl, i32, P]
+        L.orc_pd_restructure.argtypes = [P] * 5 + [P, P, i64, i32, dbl, dbl, P]
         _lib = L
     return _lib
 
@@ -326,28 +327,39 @@ def pd_steps(lam: float):
 
 def pd_fuse(u0: Pool, views: list, lam: float, gamma: float, iterations: int,
             tau: float | None = None, sigma: float | None = None,
-            clamp: bool = True):
-    """TV-L1 primal-dual schedule on a frozen tree (pd_oracle.c definition,
-    PARITY UNPINNED).  Returns (u, ubar, px, py, pz pools, energies_pre)."""
+            clamp: bool = True, tau_split: float | None = None,
+            tau_join: float | None = None, cap: int | None = None):
+    """TV-L1 primal-dual schedule (pd_oracle.c definition, PARITY UNPINNED).
+    Frozen tree unless tau_split/tau_join are given: then every pass is
+    followed by orc_pd_restructure (split/join, pd_oracle.c).  Returns
+    (u, ubar, px, py, pz, energies_pre) -- arrays over the pool's slots --
+    and, when restructuring, also (child, state, [(splits, joins)])."""
     if tau is None or sigma is None:
         tau, sigma = pd_steps(lam)
     used = u0.used
-    u = u0.value[:used].astype(np.float64).copy()
+    rs = tau_split is not None or tau_join is not None
+    n = (cap or full_tree_capacity(u0.d_max)) if rs else used
+    def pool(a):
+        out = np.zeros(n)
+        out[:used] = a
+        return out
+    u = pool(u0.value[:used].astype(np.float64))
     ub = u.copy()
-    px = np.zeros(used)
-    py = np.zeros(used)
-    pz = np.zeros(used)
-    child = u0.child[:used]
+    px, py, pz = pool(0.0), pool(0.0), pool(0.0)
+    child = np.full(n, -1, dtype=np.int32)
+    child[:used] = u0.child[:used]
+    state = np.array(u0.state[:3], dtype=np.int64)
     vv = [v.value for v in views]
     vw = [v.weight for v in views]
     vc = [v.child for v in views]
-    energies = []
+    energies, sj = [], []
     e = np.zeros(1)
+    out2 = np.zeros(2, dtype=np.int64)
     for _ in range(iterations):
         outs = [a.copy() for a in (u, ub, px, py, pz)]
         _check(lib().orc_pd_pass(
             _ptr(u), _ptr(ub), _ptr(px), _ptr(py), _ptr(pz),
-            *[_ptr(o) for o in outs], _ptr(child), used, len(views),
+            *[_ptr(o) for o in outs], _ptr(child), int(state[0]), len(views),
             _ptr_array(vv), _ptr_array(vw), _ptr_array(vc), u0.d_max,
             float(lam), float(tau), float(sigma), float(gamma),
             int(bool(clamp)), _ptr(e)))
@@ -355,6 +367,15 @@ def pd_fuse(u0: Pool, views: list, lam: float, gamma: float, iterations: int,
         for o in outs:
             propagate(o, child)
         u, ub, px, py, pz = outs
+        if rs:
+            _check(lib().orc_pd_restructure(
+                _ptr(u), _ptr(ub), _ptr(px), _ptr(py), _ptr(pz), _ptr(child),
+                _ptr(state), n, u0.d_max,
+                float(-1.0 if tau_split is None else tau_split),
+                float(2.0 if tau_join is None else tau_join), _ptr(out2)))
+            sj.append((int(out2[0]), int(out2[1])))
+    if rs:
+        return u, ub, px, py, pz, energies, child, state, sj
     return u, ub, px, py, pz, energies
 
 

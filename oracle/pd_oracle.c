@@ -198,3 +198,117 @@ int orc_pd_pass(const double *u, const double *ub, const double *px,
     free(fs); free(ws); free(ix);
     return ORC_OK;
 }
+
+/* ------------------------------------------------------- restructuring --
+ * solver="pd" with split/join (north_star item (d): "split/join
+ * restructuring after each step, which flags leaves by their |u| band").
+ * Definition (PARITY UNPINNED -- the reference has no primal-dual mode), run
+ * after a pass and the propagate of u, ubar, p:
+ *   split  a leaf at level L < d_max with |u| < tau_s gets eight children
+ *          carrying its u, ubar, p (no cascade within a pass);
+ *   join   an inner node whose eight children are leaves, each with
+ *          |u| > tau_j and all of one sign, becomes a leaf; its u, ubar, p
+ *          are the children's means (sequential f64 sum / 8, i.e. the
+ *          propagated values) and its child block is freed.
+ * With 0 <= tau_s < tau_j (FusionParams validation) no node both splits and
+ * joins.  Visit order and slot allocation are the descent's
+ * (_kernels.pyx:256-381, orc_iterate_pass above): depth-first children
+ * 0..7, a split claims the free-list head else the bump pointer, joined
+ * blocks are pushed in visit order after the walk. */
+typedef struct {
+    double *f[5];
+    int32_t *child;
+    uint8_t *joined;
+    int64_t *state;
+    int64_t cap;
+    int d_max;
+    double tau_s, tau_j;
+    int64_t splits, joins;
+    int failed;
+} pdr_t;
+
+static int64_t pdr_claim(pdr_t *R) {
+    int64_t head = R->state[1], b;
+    if (head >= 0) {
+        b = head;
+        R->state[1] = R->child[b];
+    } else {
+        b = R->state[0];
+        if (b + 8 > R->cap) return -1;
+        R->state[0] = b + 8;
+    }
+    R->state[2] += 8;
+    return b;
+}
+
+static void pdr_walk(pdr_t *R, int64_t node, int lvl) {
+    if (R->failed) return;
+    int64_t b = R->child[node];
+    if (b < 0) {
+        if (lvl < R->d_max && fabs(R->f[0][node]) < R->tau_s) {
+            int64_t nb = pdr_claim(R);
+            if (nb < 0) {
+                R->failed = 1;
+                return;
+            }
+            for (int q = 0; q < 8; ++q) {
+                for (int k = 0; k < 5; ++k) R->f[k][nb + q] = R->f[k][node];
+                R->child[nb + q] = -1;
+            }
+            R->child[node] = (int32_t)nb;
+            R->splits++;
+        }
+        return;
+    }
+    for (int q = 0; q < 8; ++q) pdr_walk(R, b + q, lvl + 1);
+    if (R->failed) return;
+    int pos = 0, neg = 0;
+    for (int q = 0; q < 8; ++q) {
+        if (R->child[b + q] >= 0) return;
+        double v = R->f[0][b + q];
+        if (!(v > R->tau_j || v < -R->tau_j)) return;
+        if (v > 0.0)
+            pos = 1;
+        else
+            neg = 1;
+    }
+    if (pos && neg) return;
+    for (int k = 0; k < 5; ++k) {
+        double acc = 0.0;
+        for (int q = 0; q < 8; ++q) acc += R->f[k][b + q];
+        R->f[k][node] = acc / 8.0;
+    }
+    R->joined[node] = 1;
+    R->joins++;
+}
+
+static void pdr_sweep(pdr_t *R, int64_t node) {
+    int64_t b = R->child[node];
+    if (b < 0) return;
+    if (R->joined[node]) {
+        R->joined[node] = 0;
+        R->child[node] = -1;
+        R->child[b] = (int32_t)R->state[1];
+        R->state[1] = b;
+        R->state[2] -= 8;
+        return;
+    }
+    for (int q = 0; q < 8; ++q) pdr_sweep(R, b + q);
+}
+
+int orc_pd_restructure(double *u, double *ub, double *px, double *py,
+                       double *pz, int32_t *child, int64_t *state, int64_t cap,
+                       int d_max, double tau_s, double tau_j, int64_t *out2) {
+    if (d_max > 60) return ORC_EDEPTH;
+    pdr_t R = {{u, ub, px, py, pz}, child, NULL, state, cap, d_max,
+               tau_s, tau_j, 0, 0, 0};
+    R.joined = (uint8_t *)calloc((size_t)cap, 1);
+    if (!R.joined) return ORC_ENOMEM;
+    pdr_walk(&R, 0, 0);
+    if (!R.failed) pdr_sweep(&R, 0);
+    free(R.joined);
+    if (R.failed) return ORC_EPOOL;
+    out2[0] = R.splits;
+    out2[1] = R.joins;
+    return ORC_OK;
+}

@@ -161,6 +161,18 @@ def pd_passes(set_a, set_b, uchild, ustate, vvals, vws, vchilds, d_max, lam,
     return en[:npasses]
 
 
+def pd_restructure(fields, uchild, ustate, d_max, tau_split, tau_join, *,
+                   ctx):
+    """solver='pd' split/join on the current set (u, ubar, px, py, pz) after
+    a pass; updates uchild/ustate in place.  Returns (splits, joins)."""
+    tf = ptr_table([ptr(t) for t in fields])
+    out = np.zeros(2, dtype=np.int64)
+    call("octf_pd_restructure", ctx.h, _dtype_code(fields[0]), tf,
+         ptr(uchild), _state_ptr(ustate), uchild.shape[0], int(d_max),
+         float(tau_split), float(tau_join), out.ctypes.data, stream_handle())
+    return int(out[0]), int(out[1])
+
+
 def ctx_prepare(ctx, uchild, ustate, d_max, vvals, vws, vchilds):
     tv, tw, tc = _views(vvals, vws, vchilds)
     call("octf_ctx_prepare", ctx.h, ptr(uchild), _state_ptr(ustate),

@@ -47,6 +47,7 @@ _SIGS = {
                                  DBL, DBL, DBL, DBL, DBL, I32, P, I32, P, I32,
                                  P], I32),
     "octf_ctx_prepare": ([P, P, P, I64, I32, I32, P, P, P, P], I32),
+    "octf_pd_restructure": ([P, I32, P, P, P, I64, I32, DBL, DBL, P, P], I32),
     "octf_pd_passes": ([P, I32, P, P, P, P, I64, I32, P, P, P, I32, DBL, DBL,
                         DBL, DBL, I32, I32, P, P], I32),
     "octf_ctx_select": ([P, P, P, I64, P], I32),

@@ -364,6 +364,35 @@ int octf_pd_passes(octf_ctx* ctx, int dtype, void* const* set_a,
   });
 }
 
+int octf_pd_restructure(octf_ctx* ctx, int dtype, void* const* set,
+                        int32_t* uchild, int64_t* ustate, int64_t cap,
+                        int d_max, double tau_split, double tau_join,
+                        int64_t* out2, void* stream) {
+  return guard([&] {
+    if (!ctx || !set || !uchild || !ustate || !out2)
+      throw octf::Error(octf::kEArg, "null argument");
+    check_dtype(dtype);
+    if (d_max < 0 || d_max > OCTF_MAX_DEPTH)
+      throw octf::Error(octf::kEDepth, "tree depth out of range");
+    if (!ctx->c.valid)
+      throw octf::Error(octf::kEArg, "context not prepared (run a pass first)");
+    octf::PdRsArgs a;
+    for (int q = 0; q < 5; ++q) a.f[q] = set[q];
+    a.child = uchild;
+    a.state = ustate;
+    a.cap = cap;
+    a.d_max = d_max;
+    a.tau_s = tau_split;
+    a.tau_j = tau_join;
+    if (dtype == OCTF_F64)
+      octf::pd_restructure_f64(ctx->c, a, S(stream));
+    else
+      octf::pd_restructure_f32(ctx->c, a, S(stream));
+    out2[0] = a.out2[0];
+    out2[1] = a.out2[1];
+  });
+}
+
 int octf_ctx_prepare(octf_ctx* ctx, const int32_t* uchild,
                      const int64_t* ustate, int64_t cap, int d_max, int nviews,
                      const float* const* vvals, const float* const* vws,

@@ -264,6 +264,18 @@ struct PdHostArgs {
   int npasses;
   double* energies;  // host, npasses: energy of u before each pass
 };
+// solver="pd" split/join on the current set after a pass
+struct PdRsArgs {
+  void* f[5];          // u, ubar, px, py, pz of the current set
+  int32_t* child;
+  int64_t* state;      // host int64[3]
+  int64_t cap;
+  int d_max;
+  double tau_s, tau_j;
+  int64_t out2[2];     // splits, joins
+};
+void pd_restructure_f64(Ctx& c, PdRsArgs& a, cudaStream_t st);
+void pd_restructure_f32(Ctx& c, PdRsArgs& a, cudaStream_t st);
 void pd_passes_f64(Ctx& c, PdHostArgs& a, cudaStream_t st);
 void pd_passes_f32(Ctx& c, PdHostArgs& a, cudaStream_t st);
 void frozen_passes_f64(Ctx& c, FrozenArgs& a, cudaStream_t st);

@@ -29,6 +29,9 @@ void propagate_levels_f32(Ctx& c, float* v, const int32_t* child, int lo, int hi
 }  // namespace octf
 
 namespace octf {
+void pd_restructure_f32(Ctx& c, PdRsArgs& a, cudaStream_t st) {
+  pd_restructure_impl<float>(c, a, st);
+}
 void pd_passes_f32(Ctx& c, PdHostArgs& a, cudaStream_t st) {
   pd_passes_impl<float>(c, a, st);
 }

@@ -29,6 +29,9 @@ void propagate_levels_f64(Ctx& c, double* v, const int32_t* child, int lo, int h
 }  // namespace octf
 
 namespace octf {
+void pd_restructure_f64(Ctx& c, PdRsArgs& a, cudaStream_t st) {
+  pd_restructure_impl<double>(c, a, st);
+}
 void pd_passes_f64(Ctx& c, PdHostArgs& a, cudaStream_t st) {
   pd_passes_impl<double>(c, a, st);
 }

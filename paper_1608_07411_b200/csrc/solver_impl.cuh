@@ -1268,6 +1268,180 @@ void pd_passes_impl(Ctx& c, PdHostArgs& a, cudaStream_t st) {
   OCTF_CUDA(cudaStreamSynchronize(st));
 }
 
+// ---------------------------------------------------------------------------
+// solver="pd" split/join after a pass (oracle/pd_oracle.c orc_pd_restructure:
+// leaves with |u| < tau_s split, children carrying u, ubar, p; inner nodes
+// with eight leaf children past tau_j of one sign join; one level per pass).
+// Splits claim blocks in depth-first pre-order from the free-list mirror then
+// the bump pointer, joins free in post-order -- the descent's allocation.
+template <typename T>
+__global__ void k_pd_split_flags(const int4* __restrict__ lmeta, int64_t nlb,
+                                 const T* __restrict__ u, int d_max,
+                                 double tau_s, int32_t* sslot, uint64_t* skey,
+                                 int32_t* sidx, int32_t* cnt) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = gid >> 3;
+  const int c = (int)(gid & 7);
+  if (i >= nlb) return;
+  const int4 m = lmeta[i];
+  int L, pz;
+  unsigned mask;
+  unpack_meta_w(m.w, pz, mask, L);
+  if (!((mask >> c) & 1u) || (m.x == 0 && c != 0)) return;
+  const int32_t s = m.x + c;
+  if (L >= d_max || !(fabs((double)u[s]) < tau_s)) return;
+  const int x = m.x == 0 ? 0 : 2 * m.y + ((c >> 2) & 1);
+  const int y = m.x == 0 ? 0 : 2 * m.z + ((c >> 1) & 1);
+  const int z = m.x == 0 ? 0 : 2 * pz + (c & 1);
+  const int32_t r = atomicAdd(cnt, 1);
+  sslot[r] = s;
+  skey[r] = preorder_key(L, x, y, z, d_max, false);
+  sidx[r] = r;
+}
+
+template <typename T>
+__global__ void k_pd_join_cand(const int32_t* __restrict__ blocks, int64_t nblk,
+                               const int8_t* blevel, const uint64_t* bcoord,
+                               const int32_t* __restrict__ child,
+                               const T* __restrict__ u, double tau_j,
+                               JoinRecs<T> rec, int32_t* cnt) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = gid >> 3;
+  const int c = (int)(gid & 7);
+  if (i >= nblk) return;
+  const int32_t b = blocks[i];
+  if (b == 0 && c != 0) return;
+  const int32_t s = b + c;
+  const int32_t cb = child[s];
+  if (cb < 0) return;
+  bool pos = false, neg = false;
+  for (int q = 0; q < 8; ++q) {
+    if (child[cb + q] >= 0) return;
+    const double v = (double)u[cb + q];
+    if (!(v > tau_j || v < -tau_j)) return;
+    if (v > 0.0)
+      pos = true;
+    else
+      neg = true;
+  }
+  if (pos && neg) return;
+  int L, x, y, z;
+  slot_cell_of(s, blevel, bcoord, L, x, y, z);
+  const int32_t r = atomicAdd(cnt, 1);
+  rec.slot[r] = s;
+  rec.blk[r] = cb;
+  rec.cell[r] = pack_cell(L, x, y, z);
+}
+
+template <typename T>
+__global__ void k_pd_split_apply(const int32_t* __restrict__ sslot,
+                                 const int32_t* __restrict__ sidx, int64_t n,
+                                 const int32_t* free_stack, int64_t nfree,
+                                 int64_t used, int32_t* child, FieldSet<T> f) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t r = gid >> 3;
+  const int q = (int)(gid & 7);
+  if (r >= n) return;
+  const int32_t s = sslot[sidx[r]];
+  const int32_t nb = r < nfree ? free_stack[nfree - 1 - r]
+                               : (int32_t)(used + 8 * (r - nfree));
+  child[nb + q] = -1;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) f.v[k][nb + q] = f.v[k][s];
+  if (q == 0) child[s] = nb;
+}
+
+template <typename T>
+__global__ void k_pd_unlink(JoinRecs<T> rec, int64_t n, int32_t* child) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) child[rec.slot[r]] = -1;
+}
+
+template <typename T>
+void pd_restructure_impl(Ctx& c, PdRsArgs& a, cudaStream_t st) {
+  if (a.d_max < 0 || a.d_max > kMaxDepth)
+    throw Error(kEDepth, "tree depth out of range");
+  ensure_prepared<T>(c, a.child, a.cap, a.d_max, a.state, st);
+  FieldSet<T> fs{};
+  for (int k = 0; k < 5; ++k) fs.v[k] = (T*)a.f[k];
+  const int64_t used = a.state[0];
+  static thread_local JoinBufs<T> jb;
+  static thread_local DevBuf<int32_t> sslot, sidx;
+  static thread_local DevBuf<uint64_t> skey;
+  const int64_t nl = c.nlb * 8 + 1;
+  sslot.ensure(nl);
+  sidx.ensure(nl);
+  skey.ensure(nl);
+  JoinRecs<T> rec = jb.view(c.nblocks * 8 + 8);
+  c.counters.ensure(64);
+  OCTF_CUDA(cudaMemsetAsync(c.counters.p, 0, 2 * sizeof(int32_t), st));
+  // candidates on the pre-pass structure (with tau_s < tau_j no node both
+  // splits and joins)
+  if (c.nlb)
+    k_pd_split_flags<T><<<blocks_for(c.nlb * 8), kT, 0, st>>>(
+        c.lmeta.p, c.nlb, fs.v[0], a.d_max, a.tau_s, sslot.p, skey.p, sidx.p,
+        c.counters.p);
+  k_pd_join_cand<T><<<blocks_for(c.nblocks * 8), kT, 0, st>>>(
+      c.lvl_blocks.p, c.nblocks, c.blevel.p, c.bcoord.p, a.child, fs.v[0],
+      a.tau_j, rec, c.counters.p + 1);
+  OCTF_CUDA(cudaGetLastError());
+  c.launches += 2;
+  read_counters<T>(c, 2, st);
+  const int64_t E = c.h_counters[0], J = c.h_counters[1];
+  a.out2[0] = E;
+  a.out2[1] = J;
+  if (E == 0 && J == 0) return;
+  if (E > 0) {
+    const int64_t fresh = E > c.nfree ? E - c.nfree : 0;
+    if (used + 8 * fresh > a.cap)
+      throw Error(kEPool, "node pool capacity exhausted");
+    sort_u64_i32(c, skey.p, sidx.p, E, st);
+    k_pd_split_apply<T><<<blocks_for(E * 8), kT, 0, st>>>(
+        sslot.p, sidx.p, E, c.free_stack.p, c.nfree, used, a.child, fs);
+    OCTF_CUDA(cudaGetLastError());
+    ++c.launches;
+    int64_t head = -1;
+    if (E < c.nfree) {
+      int32_t h;
+      OCTF_CUDA(cudaMemcpyAsync(&h, c.free_stack.p + (c.nfree - 1 - E),
+                                sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      OCTF_CUDA(cudaStreamSynchronize(st));
+      head = h;
+      c.nfree -= E;
+    } else {
+      c.nfree = 0;
+    }
+    a.state[0] = used + 8 * fresh;
+    a.state[1] = head;
+    a.state[2] += 8 * E;
+  }
+  if (J > 0) {
+    // free the joined blocks in post-order (forward), as the descent sweep
+    k_join_keys<T><<<blocks_for(J), kT, 0, st>>>(rec, J, a.d_max, 0);
+    sort_u64_i32(c, rec.key, rec.idx, J, st);
+    k_pd_unlink<T><<<blocks_for(J), kT, 0, st>>>(rec, J, a.child);
+    c.free_stack.grow_keep(c.nfree + J + 1, c.nfree, st);
+    k_sweep_link<T><<<blocks_for(J), kT, 0, st>>>(rec, J, a.state[1], a.child,
+                                                   c.free_stack.p, c.nfree);
+    OCTF_CUDA(cudaGetLastError());
+    c.launches += 3;
+    int32_t last;
+    OCTF_CUDA(cudaMemcpyAsync(&last, c.free_stack.p + c.nfree + J - 1,
+                              sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    OCTF_CUDA(cudaStreamSynchronize(st));
+    c.nfree += J;
+    a.state[1] = last;
+    a.state[2] -= 8 * J;
+  }
+  c.hstate[0] = a.state[0];
+  c.hstate[1] = a.state[1];
+  c.hstate[2] = a.state[2];
+  c.nfree_head = a.state[1];
+  c.valid = false;
+  c.own_change = true;
+  OCTF_CUDA(cudaStreamSynchronize(st));
+}
+
 // propagate levels hi-1 .. lo only (the replicated top of a sharded tree)
 template <typename T>
 void propagate_levels_impl(Ctx& c, T* value, const int32_t* child, int lo,

@@ -351,11 +351,15 @@ def pd_steps(lam: float):
 
 
 class PDSolver:
-    """The north_star's TV-L1 primal-dual iteration (solver='pd') on a frozen
-    tree: dual ascent with projection, divergence, generalised-median prox
-    (the reference has none -- its definition and
-    CPU oracle are oracle/pd_oracle.c).  State: u, ubar, p = (px, py, pz)
-    per node, double-buffered; p starts at 0 and ubar at u0."""
+    """The north_star's TV-L1 primal-dual iteration (solver='pd'): dual
+    ascent with projection, divergence, generalised-median prox (SURVEY.md
+    §8(a) row A18; the reference has none -- its definition and CPU oracle
+    are oracle/pd_oracle.c).  State: u, ubar, p = (px, py, pz) per node,
+    double-buffered; p starts at 0 and ubar at u0.  Unless the structure is
+    frozen (tau_split <= 0, tau_join >= 1, clamp), every pass is followed by
+    the pd split/join (``octf_pd_restructure``: leaves with |u| < tau_split
+    split, children carrying u/ubar/p; eight leaves past tau_join with one
+    sign join), north_star item (d)."""
 
     def __init__(self, u0: OctreeField, views, params: FusionParams, *,
                  precision: str = "fp32", tau: float | None = None,
@@ -387,9 +391,66 @@ class PDSolver:
         self.a = [self.u.value, ub, z(), z(), z()]
         self.b = [self.u.snap, z(), z(), z(), z()]
         self.stats: list[IterationStats] = []
+        self.restructure = not (params.tau_split <= 0.0 and params.clamp
+                                and params.tau_join >= 1.0)
+        if self.restructure and samples is not None:
+            raise ValueError("per-leaf samples need a frozen structure "
+                             "(tau_split <= 0, tau_join >= 1, clamp)")
+
+    def _grow(self) -> None:
+        u = self.u
+        full = full_tree_capacity(u.d_max)
+        if u.capacity >= full:
+            raise RuntimeError("node pool capacity exhausted")
+        cap = min(full, 2 * u.capacity)
+
+        def g(t, fill):
+            n = pool_empty(cap, t.dtype, fill=fill)
+            n[:t.shape[0]].copy_(t)
+            return n
+        self.a = [g(t, 0) for t in self.a]
+        self.b = [g(t, 0) for t in self.b]
+        u.value, u.snap = self.a[0], self.b[0]
+        u.child = g(u.child, -1)
+        if u.joined is not None:
+            u.joined = g(u.joined, 0)
+        self.ctx.invalidate()
+
+    def _restructure(self) -> tuple:
+        p, u = self.params, self.u
+        while True:
+            try:
+                return self.kern.pd_restructure(
+                    self.a, u.child, u.state, u.d_max, p.tau_split, p.tau_join,
+                    ctx=self.ctx)
+            except RuntimeError as exc:
+                if "capacity" not in str(exc):
+                    raise
+                self._grow()   # the pool is untouched: grow, re-prepare, retry
+                self.kern.ctx_prepare(self.ctx, u.child, u.state, u.d_max,
+                                      self.vvals, self.vws, self.vchilds)
 
     def run(self, t0: int, k: int) -> list:
         p, u = self.params, self.u
+        if self.restructure:
+            out = []
+            for t in range(t0, t0 + k):
+                w0 = time.perf_counter()
+                en = self.kern.pd_passes(self.a, self.b, u.child, u.state,
+                                         self.vvals, self.vws, self.vchilds,
+                                         u.d_max, p.lam, self.tau, self.sigma,
+                                         p.gamma, p.clamp, 1, ctx=self.ctx)
+                self.a, self.b = self.b, self.a
+                splits, joins = self._restructure()
+                if self.stats and self.stats[-1].energy is None:
+                    self.stats[-1].energy = float(en[0])
+                st = IterationStats(t + 1, None, u.node_count,
+                                    u.node_count * 10 * u.value.element_size(),
+                                    splits, joins,
+                                    (time.perf_counter() - w0) * 1e3)
+                self.stats.append(st)
+                out.append(st)
+            return out
         w0 = time.perf_counter()
         en = self.kern.pd_passes(self.a, self.b, u.child, u.state, self.vvals,
                                  self.vws, self.vchilds, u.d_max, p.lam,
@@ -444,7 +505,8 @@ def fuse(u0: OctreeField, views, params: FusionParams, *,
     ``u0`` is left untouched.  Statistics carry one row per pass; energies
     are those after the pass's restructuring and re-propagation.
     ``solver="pd"`` runs the north_star's TV-L1 primal-dual iteration
-    instead (frozen structure; no reference counterpart, see PDSolver).
+    instead (split/join after each pass unless frozen; no reference
+    counterpart, see PDSolver).
     """
     if solver == "pd":
         pds = PDSolver(u0, views, params, precision=precision,

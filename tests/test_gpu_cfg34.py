@@ -105,3 +105,32 @@ def test_incremental_regather_equals_full_gather(monkeypatch):
     assert np.array_equal(a.child[:a.used], b.child[:b.used])
     assert np.array_equal(a.value[:a.used], b.value[:b.used])
     assert pa["gathers"] >= 2   # restructured passes were regathered
+
+
+def test_cfg3_reduced_pd_with_restructure():
+    """solver='pd' with split/join every pass on the reduced cfg3 scene
+    against pd_oracle.c (unpinned definition): same per-pass splits/joins,
+    child array and pool state, live values bit-exact in fp64."""
+    from paper_1608_07411_b200 import fusion, scenes, volume
+    sc = scenes.make_cfg3(d_max=6, n_views=8, width=160, height=120,
+                          focal=131.25, device="cuda")
+    kw = dict(sc.params, iterations=5)
+    p = fusion.FusionParams(**kw)
+    dom = volume.VolumeDomain(sc.origin, sc.voxel_size, sc.resolution)
+    views, u0, _ = fusion.prepare(sc.depths, sc.cameras, dom, p)
+    oviews, ou0 = oracle_prepare(sc, orc.Params(**kw))
+    s = fusion.PDSolver(u0, views, p, precision="fp64")
+    s.run(0, 5)
+    u, ub, px, py, pz, en, child, state, sj = orc.pd_fuse(
+        ou0, oviews, p.lam, p.gamma, 5, tau_split=p.tau_split,
+        tau_join=p.tau_join, cap=s.u.capacity)
+    assert [(st.splits, st.joins) for st in s.stats] == sj
+    assert sum(a + b for a, b in sj) > 0
+    assert list(s.u.state) == list(state)
+    used = int(state[0])
+    assert np.array_equal(s.u.child[:used].cpu().numpy(), child[:used])
+    live = [n for n, *_ in orc.leaves(orc.Pool(np.zeros(used), child[:used],
+                                                state, ou0.d_max))]
+    got = [t[:used].cpu().numpy() for t in s.state]
+    for g, w in zip(got, (u, ub, px, py, pz)):
+        assert np.array_equal(g[live], w[:used][live])

@@ -55,7 +55,8 @@ def test_descent_with_per_leaf_samples_bitexact(cfg5_small):
 def test_pd_with_per_leaf_samples_bitexact(cfg5_small):
     from paper_1608_07411_b200 import fusion
     u0, samples, u0h, views, _ = cfg5_small
-    p = fusion.FusionParams(iterations=4, lam=0.3)
+    p = fusion.FusionParams(iterations=4, lam=0.3, tau_split=0.0,
+                            tau_join=1.5)
     s = fusion.PDSolver(u0, None, p, precision="fp64", samples=samples)
     s.run(0, 4)
     u, ub, px, py, pz, en = orc.pd_fuse(u0h, views, 0.3, 1e-4, 4)

@@ -48,7 +48,8 @@ def test_pd_fp64_matches_cpu_restatement(kind):
     views_h, u0h, lam = _views_u0(kind)
     iters = 8
     u, ub, px, py, pz, en = orc.pd_fuse(u0h, views_h, lam, 1e-4, iters)
-    p = fusion.FusionParams(lam=lam, iterations=iters)
+    p = fusion.FusionParams(lam=lam, iterations=iters, tau_split=0.0,
+                            tau_join=1.5)   # frozen structure
     s = fusion.PDSolver(_dev(u0h), [_dev(v) for v in views_h], p,
                         precision="fp64")
     s.run(0, iters)
@@ -67,10 +68,68 @@ def test_pd_fp32_tolerance_and_descent():
     views_h, u0h, lam = _views_u0("full")
     iters = 30
     u, *_ , en = orc.pd_fuse(u0h, views_h, lam, 1e-4, iters)
-    p = fusion.FusionParams(lam=lam, iterations=iters)
+    p = fusion.FusionParams(lam=lam, iterations=iters, tau_split=0.0,
+                            tau_join=1.5)
     res = fusion.fuse(_dev(u0h), [_dev(v) for v in views_h], p, solver="pd",
                       precision="fp32")
     got = res.field.to_host().value
     assert np.max(np.abs(got - u)) <= 1e-4
     # the primal-dual scheme lowers the TV-L1 energy from its start
     assert en[-1] < en[0]
+
+
+@pytest.mark.parametrize("kind", ["small", "mixed"])
+def test_pd_restructure_fp64_matches_cpu_restatement(kind):
+    """pd mode with split/join after every pass (north_star item (d);
+    definition pd_oracle.c orc_pd_restructure): same splits and joins per
+    pass, same child array and pool state (free list included), every live
+    node's u/ubar/p bit-exact in fp64, energies to rel 1e-12."""
+    from paper_1608_07411_b200 import fusion
+    views_h, u0h, lam = _views_u0(kind)
+    iters = 8
+    p = fusion.FusionParams(lam=lam, iterations=iters, tau_split=0.15,
+                            tau_join=0.45)
+    s = fusion.PDSolver(_dev(u0h), [_dev(v) for v in views_h], p,
+                        precision="fp64")
+    s.run(0, iters)
+    cap = s.u.capacity
+    u, ub, px, py, pz, en, child, state, sj = orc.pd_fuse(
+        u0h, views_h, lam, 1e-4, iters, tau_split=0.15, tau_join=0.45,
+        cap=cap)
+    assert [(st.splits, st.joins) for st in s.stats] == sj
+    assert sum(a + b for a, b in sj) > 0
+    assert list(s.u.state) == list(state)
+    used = int(state[0])
+    gch = s.u.child[:used].cpu().numpy()
+    assert np.array_equal(gch, child[:used])
+    live = [n for n, *_ in orc.leaves(orc.Pool(np.zeros(used), child[:used],
+                                                state, u0h.d_max))]
+    reach = np.array(sorted(set(live) | set(_reachable_inner(child))))
+    got = [t[:used].cpu().numpy() for t in s.state]
+    for g, w in zip(got, (u, ub, px, py, pz)):
+        assert np.array_equal(g[reach], w[:used][reach])
+    e = [st.energy for st in s.stats[:-1]]
+    np.testing.assert_allclose(e, en[1:], rtol=1e-12, atol=0)
+
+
+def _reachable_inner(child):
+    out, stack = [], [0]
+    while stack:
+        n = stack.pop()
+        b = int(child[n])
+        if b >= 0:
+            out.append(n)
+            stack.extend(range(b, b + 8))
+    return out
+
+
+def test_pd_restructure_fp32_runs_and_lowers_energy():
+    from paper_1608_07411_b200 import fusion
+    views_h, u0h, lam = _views_u0("mixed")
+    p = fusion.FusionParams(lam=lam, iterations=12, tau_split=0.15,
+                            tau_join=0.45)
+    res = fusion.fuse(_dev(u0h), [_dev(v) for v in views_h], p, solver="pd",
+                      precision="fp32")
+    assert sum(st.splits + st.joins for st in res.stats) > 0
+    e = [st.energy for st in res.stats]
+    assert e[-1] < e[0]

@@ -153,9 +153,74 @@ __device__ __forceinline__ void bitonic_select(float* X, T& ko, T& acc, T v0,
   }
 }
 
+// General weights without carrying them through the sort (NV = 64): the
+// breakpoint at sorted position k is c'_k = v0 - cc*(2 S(f_(k)) - W) with
+// S(a) = sum of the weights of samples strictly below a (view order).  A
+// tie group's first element has S_k = S(a) and later ones only smaller
+// breakpoints, so max_k min(f_(k), c'_k) equals the sorted scan's value;
+// with dyadic view-tree weights the f64 sums are exact in any order.  The
+// selection needs c' only at O(log NV) positions, each an O(NV) pass over
+// the leaf's samples (f staged in shared memory, weights from global).
+template <typename T, int NV>
+struct WeightAt {
+  const float* fs;     // s_tile + t: f of view v at fs[v * kTileLeaves]
+  const float* wg;     // weights of view v at wg[v * kTileLeaves]
+  __device__ __forceinline__ T below(float a) const {
+    T S = 0;
+#pragma unroll 8
+    for (int v = 0; v < NV; ++v) {
+      const float wv = __ldg(wg + v * kTileLeaves);
+      if (fs[v * kTileLeaves] < a) S += (T)wv;
+    }
+    return S;
+  }
+};
+
+template <typename T, int M, int NV>
+__device__ __forceinline__ void bitonic_select_w(float* X, T& acc, T v0, T cc,
+                                                 T W,
+                                                 const WeightAt<T, NV>& wa) {
+  if constexpr (M == 1) {
+    const T c = v0 - cc * ((T)2 * wa.below(X[0]) - W);
+    acc = fmax(acc, fmin((T)X[0], c));
+  } else {
+    constexpr int H = M / 2;
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      const float l = fminf(X[i], X[i + H]);
+      X[i + H] = fmaxf(X[i], X[i + H]);
+      X[i] = l;
+    }
+    float mL = X[0], mH = X[H];
+#pragma unroll
+    for (int i = 1; i < H; ++i) {
+      mL = fmaxf(mL, X[i]);
+      mH = fminf(mH, X[H + i]);
+    }
+    const T cl = v0 - cc * ((T)2 * wa.below(mL) - W);
+    const bool inH = cl > (T)mL;
+    const T ch = inH ? (T)0 : v0 - cc * ((T)2 * wa.below(mH) - W);
+    acc = fmax(acc, inH ? (T)mL : ch);
+#pragma unroll
+    for (int i = 0; i < H; ++i) X[i] = inH ? X[i + H] : X[i];
+    bitonic_select_w<T, H, NV>(X, acc, v0, cc, W, wa);
+  }
+}
+
+// shared memory of k_pd_pass: the f tile, then the mask tile (binary
+// weights) or the weight tile (NV <= 32; at NV = 64 weights stay in global)
+constexpr size_t pd_smem_bytes(int nv, bool binw) {
+  return (size_t)nv * kTileLeaves * 4 +
+         (binw ? (size_t)kTileLeaves * 4
+               : (nv > 32 ? 0 : (size_t)nv * kTileLeaves * 4));
+}
+
 template <typename T, bool BINW, int NV>
 __global__ void __launch_bounds__(kT, BINW ? OCTF_PD_MINB : 1) k_pd_pass(PdArgs<T> a) {
   static_assert(NV > 0 && (NV & (NV - 1)) == 0, "NV: power of two");
+  // NV = 64: general weights selected without sorting them (WeightAt)
+  constexpr bool WSEL = NV > 32;
+  static_assert(!(WSEL && BINW), "the mask format holds 32 views");
   const int gid = (int)(blockIdx.x * kT + threadIdx.x);
   const int i = gid >> 3;
   const int c = gid & 7;
@@ -169,13 +234,13 @@ __global__ void __launch_bounds__(kT, BINW ? OCTF_PD_MINB : 1) k_pd_pass(PdArgs<
     mbar_init(&s_bar, 1);
     const size_t tile = blockIdx.x;
     const unsigned fbytes = NV * kTileLeaves * 4;
-    const unsigned abytes = BINW ? kTileLeaves * 4 : fbytes;
+    const unsigned abytes = BINW ? kTileLeaves * 4 : (WSEL ? 0 : fbytes);
     mbar_expect_tx(&s_bar, fbytes + abytes);
     bulk_g2s(s_tile, a.F + tile * NV * kTileLeaves, fbytes, &s_bar);
     if (BINW)
       bulk_g2s(s_tile + NV * kTileLeaves, a.M + tile * kTileLeaves, abytes,
                &s_bar);
-    else
+    else if (!WSEL)
       bulk_g2s(s_tile + NV * kTileLeaves, a.W + tile * NV * kTileLeaves,
                abytes, &s_bar);
   }
@@ -277,7 +342,7 @@ __global__ void __launch_bounds__(kT, BINW ? OCTF_PD_MINB : 1) k_pd_pass(PdArgs<
   mbar_wait(&s_bar, 0);
   const int t = threadIdx.x;
   float f[NV];
-  float w[NV];  // (unused with binary weights: the sort carries f only)
+  float w[NV];  // (only the general-weight sort carries them)
   int ix[NV];
   uint32_t mk = 0u;
   T W = 0, num = 0;
@@ -290,14 +355,18 @@ __global__ void __launch_bounds__(kT, BINW ? OCTF_PD_MINB : 1) k_pd_pass(PdArgs<
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
     const float fv = s_tile[v * kTileLeaves + t];
-    const float wv = BINW ? 1.f : s_tile[(NV + v) * kTileLeaves + t];
+    const float wv =
+        BINW ? 1.f
+             : (WSEL ? __ldg(a.W + (size_t)blockIdx.x * NV * kTileLeaves +
+                             v * kTileLeaves + t)
+                     : s_tile[(NV + v) * kTileLeaves + t]);
     const bool on = BINW ? ((mk >> v) & 1u) != 0u : (v < a.nv && wv != 0.f);
     if (on) {
       if (!BINW) W += (T)wv;
       num += BINW ? (T)fabs(U0 - (T)fv) : (T)wv * fabs(U0 - (T)fv);
     }
     f[v] = on ? __fadd_rn(fv, 0.f) : __int_as_float(0x7f800000);  // -0 -> +0
-    if (!BINW) {
+    if (!BINW && !WSEL) {
       w[v] = on ? wv : 0.f;
       ix[v] = v;
     }
@@ -305,7 +374,7 @@ __global__ void __launch_bounds__(kT, BINW ? OCTF_PD_MINB : 1) k_pd_pass(PdArgs<
   const T den = W + a.gamma;
   const T cc = a.tau / den;
   T res0 = -(T)INFINITY;
-  if (BINW) {
+  if (BINW || WSEL) {
     // two sorted halves, the second read backwards: a bitonic sequence
     // whose order statistics are those of all samples
     oddeven_sort<NV / 2, false>(f, w, ix);
@@ -316,9 +385,16 @@ __global__ void __launch_bounds__(kT, BINW ? OCTF_PD_MINB : 1) k_pd_pass(PdArgs<
       f[NV / 2 + i] = f[NV - 1 - i];
       f[NV - 1 - i] = t;
     }
-    res0 = v0 - cc * ((T)2 * (T)NV - W);  // k = NV: f = +inf
-    T ko = 0;
-    bitonic_select<T, NV>(f, ko, res0, v0, cc, W);
+    if (WSEL) {
+      res0 = v0 - cc * W;  // k = NV: f = +inf, S = W
+      const WeightAt<T, NV> wa{
+          s_tile + t, a.W + (size_t)blockIdx.x * NV * kTileLeaves + t};
+      bitonic_select_w<T, NV, NV>(f, res0, v0, cc, W, wa);
+    } else {
+      res0 = v0 - cc * ((T)2 * (T)NV - W);  // k = NV: f = +inf
+      T ko = 0;
+      bitonic_select<T, NV>(f, ko, res0, v0, cc, W);
+    }
   } else {
     oddeven_sort<NV, true>(f, w, ix);
     // generalised weighted median (oracle/pd_oracle.c wmedian_prox).  With

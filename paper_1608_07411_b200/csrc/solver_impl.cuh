@@ -1177,7 +1177,7 @@ void pd_passes_impl(Ctx& c, PdHostArgs& a, cudaStream_t st);
 
 template <typename T, bool BW, int N>
 void launch_pd(unsigned g, cudaStream_t st, const PdArgs<T>& p) {
-  constexpr size_t smem = leaf_smem_bytes(N, BW);
+  constexpr size_t smem = pd_smem_bytes(N, BW);
   static bool attr = false;  // opt in to > 48 KiB of dynamic shared memory
   if (smem > 48 * 1024 && !attr) {
     OCTF_CUDA(cudaFuncSetAttribute(k_pd_pass<T, BW, N>,
@@ -1195,8 +1195,9 @@ void pd_passes_impl(Ctx& c, PdHostArgs& a, cudaStream_t st) {
   if (a.npasses < 1) return;
   ensure_prepared<T>(c, a.child, a.cap, a.d_max, a.state, st);
   const int nv = c.nviews;
-  if (!(nv == 4 || nv == 8 || nv == 16 || nv == 32) || c.sstride != nv)
-    throw Error(kEArg, "solver='pd' supports 4, 8, 16 or 32 views");
+  if (!(nv == 4 || nv == 8 || nv == 16 || nv == 32 || nv == 64) ||
+      c.sstride != nv || (nv == 64 && c.binw))
+    throw Error(kEArg, "solver='pd' supports 4, 8, 16, 32 or 64 views");
   constexpr int kChunk = 32;
   const unsigned g = leaf_grid(c);
   c.partials.ensure((size_t)g * kChunk);
@@ -1243,7 +1244,8 @@ void pd_passes_impl(Ctx& c, PdHostArgs& a, cudaStream_t st) {
         else if (nv == 16) OCTF_PD(true, 16); else OCTF_PD(true, 32);
       } else {
         if (nv == 4) OCTF_PD(false, 4); else if (nv == 8) OCTF_PD(false, 8);
-        else if (nv == 16) OCTF_PD(false, 16); else OCTF_PD(false, 32);
+        else if (nv == 16) OCTF_PD(false, 16);
+        else if (nv == 32) OCTF_PD(false, 32); else OCTF_PD(false, 64);
       }
 #undef OCTF_PD
       OCTF_CUDA(cudaGetLastError());

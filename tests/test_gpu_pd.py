@@ -133,3 +133,38 @@ def test_pd_restructure_fp32_runs_and_lowers_energy():
     assert sum(st.splits + st.joins for st in res.stats) > 0
     e = [st.energy for st in res.stats]
     assert e[-1] < e[0]
+
+
+def test_pd_64_views_general_weights():
+    """64 views (weights selected without sorting them, NV = 64 path):
+    frozen pd in fp64 against the oracle bit for bit."""
+    from paper_1608_07411_b200 import fusion
+    rng = np.random.default_rng(5)
+    d = 4
+    n = 1 << d
+    views = []
+    for k in range(64):
+        f = np.clip(rng.standard_normal((n, n, n)) * 0.5, -1, 1).astype(np.float32)
+        w = (rng.random((n, n, n)) < 0.7).astype(np.uint8)
+        f[w == 0] = -1.0
+        # tau > 0: coarse view leaves carry fractional (dyadic) weights
+        views.append(orc.build_octree(f, w, tau=0.9, dtype=np.float32))
+    g = rng.integers(0, 3, (n, n, n)).astype(np.float64) * 0.4 - 0.4
+    u0h = orc.build_octree(g, tau=0.2)
+    lam, iters = 0.5, 6
+    u, ub, px, py, pz, en = orc.pd_fuse(u0h, views, lam, 1e-4, iters)
+    p = fusion.FusionParams(lam=lam, iterations=iters, tau_split=0.0,
+                            tau_join=1.5)
+    s = fusion.PDSolver(_dev(u0h), [_dev(v) for v in views], p,
+                        precision="fp64")
+    s.run(0, iters)
+    assert s.ctx.info()["mask_samples"] == 0
+    used = u0h.used
+    got = [t[:used].cpu().numpy() for t in s.state]
+    for g_, w_ in zip(got, (u, ub, px, py, pz)):
+        assert np.array_equal(g_, w_)
+    np.testing.assert_allclose([st.energy for st in s.stats[:-1]], en[1:],
+                               rtol=1e-12)
+    r32 = fusion.fuse(_dev(u0h), [_dev(v) for v in views], p, solver="pd",
+                      precision="fp32")
+    assert np.max(np.abs(r32.field.to_host().value - u)) <= 1e-4

@@ -22,6 +22,7 @@ ap.add_argument("--passes", type=int, default=20)
 ap.add_argument("--precision", default="fp32")
 ap.add_argument("--views", type=int, default=64)
 ap.add_argument("--depth", type=int, default=9)
+ap.add_argument("--solver", choices=("descent", "pd"), default="descent")
 ap.add_argument("--save-scene", default=None, help="pickle the rendered scene")
 ap.add_argument("--load-scene", default=None, help="reuse a pickled scene")
 args = ap.parse_args()
@@ -47,7 +48,10 @@ views, u0, seen = fusion.prepare(sc.depths, sc.cameras, dom, p)
 torch.cuda.synchronize()
 t_prep = time.time() - t0
 
-s = fusion.Solver(u0, views, p, precision=args.precision)
+if args.solver == "pd":
+    s = fusion.PDSolver(u0, views, p, precision=args.precision)
+else:
+    s = fusion.Solver(u0, views, p, precision=args.precision)
 s.ctx.profile(True)
 passes = []
 for t in range(args.passes):
@@ -55,7 +59,7 @@ for t in range(args.passes):
     e1 = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     e0.record()
-    st = s.step(t)
+    st = s.run(t, 1)[0] if args.solver == "pd" else s.step(t)
     e1.record()
     torch.cuda.synchronize()
     pr = s.ctx.profile(True)
@@ -75,6 +79,7 @@ ms = sorted(q["ms"] for q in steady)[len(steady) // 2]
 lv = [(7 * q["nodes"] + 1) // 8 for q in passes]
 out = {"workload": "cfg3 adaptive object (BASELINE config 2)",
        "depth": args.depth, "views": args.views, "precision": args.precision,
+       "solver": args.solver,
        "render_s": t_render, "prepare_s": t_prep,
        "u0_nodes": u0.node_count, "leaves_end": leaves_end,
        "median_pass_ms": ms,

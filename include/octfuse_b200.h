@@ -62,8 +62,8 @@ int octf_selftest(void);
 int octf_ctx_create(octf_ctx **out);
 int octf_ctx_destroy(octf_ctx *ctx);
 int octf_ctx_invalidate(octf_ctx *ctx);
-/* out[0..7] = leaf blocks, leaves, live blocks, free blocks, mask-format
- * samples (0/1), sample stride, views, valid */
+/* out[0..8] = leaf blocks, leaves, live blocks, free blocks, mask-format
+ * samples (0/1), sample stride, views, valid, leaf tiles (int64[9]) */
 int octf_ctx_info(octf_ctx *ctx, int64_t *out);
 
 /* Live profiling: enable != 0 brackets the leaf-update and energy kernels
@@ -121,6 +121,23 @@ int octf_fuse_passes_frozen(octf_ctx *ctx, int dtype, void *ubuf0, void *ubuf1,
                             const double *xis, int npasses,
                             double *energies_pre, int device_energies,
                             void *stream);
+
+/* Sharded overlap: one frozen descent pass split into
+ * leaf-tile ranges, so a rank updates its interior tiles while the halo of
+ * the previous pass is in flight and its boundary tiles afterwards.
+ * octf_pass_tiles runs the leaf kernel (snapshot usnap -> uval, step xi) on
+ * tiles [tile0, tile0+ntiles) of the context's leaf-block list (256 leaves
+ * per tile; octf_ctx_info out[8] = tiles), energy partials per tile;
+ * octf_pass_finish propagates uval and sums the pass's energy partials into
+ * *dev_energy (a device double).  Same arithmetic as octf_fuse_passes_frozen. */
+int octf_pass_tiles(octf_ctx *ctx, int dtype, const void *usnap, void *uval,
+                    const int32_t *uchild, const int64_t *ustate, int64_t cap,
+                    int nviews, const float *const *vvals,
+                    const float *const *vws, const int32_t *const *vchilds,
+                    int d_max, double lam, double eps, double gamma, double xi,
+                    int clamp, int tile0, int ntiles, void *stream);
+int octf_pass_finish(octf_ctx *ctx, int dtype, void *uval,
+                     const int32_t *uchild, double *dev_energy, void *stream);
 
 /* solver="pd" (north_star; no reference counterpart,
  * definition in oracle/pd_oracle.c): npasses TV-L1 primal-dual passes on a

@@ -161,6 +161,26 @@ def pd_passes(set_a, set_b, uchild, ustate, vvals, vws, vchilds, d_max, lam,
     return en[:npasses]
 
 
+def pass_tiles(usnap, uval, uchild, ustate, vvals, vws, vchilds, d_max, lam,
+               eps, gamma, xi, clamp, tile0, ntiles, *, ctx):
+    """Leaf kernel of one frozen pass on leaf tiles [tile0, tile0+ntiles)
+    (sharded overlap: interior tiles while the halo is in flight)."""
+    tv, tw, tc = _views(vvals, vws, vchilds)
+    call("octf_pass_tiles", ctx.h, _dtype_code(uval), ptr(usnap), ptr(uval),
+         ptr(uchild), _state_ptr(ustate), uchild.shape[0], len(vvals), tv, tw,
+         tc, int(d_max), float(lam), float(eps), float(gamma), float(xi),
+         int(bool(clamp)), int(tile0), int(ntiles), stream_handle())
+
+
+def pass_finish(uval, uchild, dev_energy, *, ctx):
+    """Propagate the pass output and sum its energy partials into
+    ``dev_energy`` (a one-element float64 CUDA tensor)."""
+    if dev_energy.dtype != torch.float64 or not dev_energy.is_cuda:
+        raise TypeError("dev_energy must be a float64 CUDA tensor")
+    call("octf_pass_finish", ctx.h, _dtype_code(uval), ptr(uval), ptr(uchild),
+         ptr(dev_energy), stream_handle())
+
+
 def pd_restructure(fields, uchild, ustate, d_max, tau_split, tau_join, *,
                    ctx):
     """solver='pd' split/join on the current set (u, ubar, px, py, pz) after

@@ -48,6 +48,9 @@ _SIGS = {
                                  P], I32),
     "octf_ctx_prepare": ([P, P, P, I64, I32, I32, P, P, P, P], I32),
     "octf_pd_restructure": ([P, I32, P, P, P, I64, I32, DBL, DBL, P, P], I32),
+    "octf_pass_tiles": ([P, I32, P, P, P, P, I64, I32, P, P, P, I32, DBL, DBL,
+                         DBL, DBL, I32, I32, I32, P], I32),
+    "octf_pass_finish": ([P, I32, P, P, P, P], I32),
     "octf_pd_passes": ([P, I32, P, P, P, P, I64, I32, P, P, P, I32, DBL, DBL,
                         DBL, DBL, I32, I32, P, P], I32),
     "octf_ctx_select": ([P, P, P, I64, P], I32),
@@ -122,10 +125,10 @@ class Ctx:
 
     def info(self) -> dict:
         import numpy as np
-        out = np.zeros(8, dtype=np.int64)
+        out = np.zeros(9, dtype=np.int64)
         call("octf_ctx_info", self.h, out.ctypes.data)
         keys = ("leaf_blocks", "leaves", "blocks", "free_blocks", "mask_samples",
-                "sample_stride", "views", "valid")
+                "sample_stride", "views", "valid", "tiles")
         return dict(zip(keys, (int(v) for v in out)))
 
     def profile(self, enable: bool = True) -> dict:

@@ -160,6 +160,7 @@ int octf_ctx_info(octf_ctx* ctx, int64_t* out) {
     out[5] = c.sstride;
     out[6] = c.nviews;
     out[7] = c.valid;
+    out[8] = (c.nlb * 8 + 255) / 256;  // leaf tiles (one CTA each)
   });
 }
 
@@ -320,6 +321,49 @@ int octf_fuse_passes_frozen(octf_ctx* ctx, int dtype, void* ubuf0, void* ubuf1,
       octf::frozen_passes_f64(ctx->c, a, S(stream));
     else
       octf::frozen_passes_f32(ctx->c, a, S(stream));
+  });
+}
+
+int octf_pass_tiles(octf_ctx* ctx, int dtype, const void* usnap, void* uval,
+                    const int32_t* uchild, const int64_t* ustate, int64_t cap,
+                    int nviews, const float* const* vvals,
+                    const float* const* vws, const int32_t* const* vchilds,
+                    int d_max, double lam, double eps, double gamma, double xi,
+                    int clamp, int tile0, int ntiles, void* stream) {
+  return guard([&] {
+    if (!ctx || !usnap || !uval || !uchild || !ustate)
+      throw octf::Error(octf::kEArg, "null argument");
+    check_dtype(dtype);
+    if (d_max < 0 || d_max > OCTF_MAX_DEPTH)
+      throw octf::Error(octf::kEDepth, "tree depth out of range");
+    if (!clamp) throw octf::Error(octf::kEArg, "tile passes are frozen: clamp");
+    octf::ctx_set_views(ctx->c, nviews, vvals, vws, vchilds, S(stream));
+    octf::TileArgs a;
+    a.usnap = usnap;
+    a.uval = uval;
+    a.child = uchild;
+    a.state = ustate;
+    a.cap = cap;
+    a.prm = make_params(d_max, lam, eps, gamma, xi, 0.0, 2.0, clamp, 0);
+    a.tile0 = tile0;
+    a.ntiles = ntiles;
+    if (dtype == OCTF_F64)
+      octf::pass_tiles_f64(ctx->c, a, S(stream));
+    else
+      octf::pass_tiles_f32(ctx->c, a, S(stream));
+  });
+}
+
+int octf_pass_finish(octf_ctx* ctx, int dtype, void* uval,
+                     const int32_t* uchild, double* dev_energy, void* stream) {
+  return guard([&] {
+    if (!ctx || !uval || !uchild || !dev_energy)
+      throw octf::Error(octf::kEArg, "null argument");
+    check_dtype(dtype);
+    if (dtype == OCTF_F64)
+      octf::pass_finish_f64(ctx->c, uval, uchild, dev_energy, S(stream));
+    else
+      octf::pass_finish_f32(ctx->c, uval, uchild, dev_energy, S(stream));
   });
 }
 

@@ -211,7 +211,8 @@ __global__ void k_gather(const int32_t* __restrict__ ucs,
   if (i >= nlb) return;
   int32_t b = lblocks[i];
   int64_t sidx = i * 8 + c;
-  bool active = !(b == 0 && c != 0) && ucs[b + c] < 0;
+  bool active = b >= 0 && !(b == 0 && c != 0) && ucs[b + c] < 0;
+  if (b < 0) b = 0;
   int L, px, py, pz;
   unpack_cell(lkey[i], L, px, py, pz);
   int x = b == 0 ? 0 : 2 * px + ((c >> 2) & 1);
@@ -245,7 +246,7 @@ __global__ void k_gather_slots(const int32_t* __restrict__ ucs,
   int c = (int)(gid & 7);
   if (i >= nlb) return;
   int32_t b = lblocks[i];
-  bool active = !(b == 0 && c != 0) && ucs[b + c] < 0;
+  bool active = b >= 0 && !(b == 0 && c != 0) && ucs[b + c] < 0;
   int flag = 0;
   for (int v = 0; v < nv; ++v) {
     float f = 0.f, w = 0.f;
@@ -857,6 +858,14 @@ __global__ void k_select(const int32_t* __restrict__ sel,
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= nsel) return;
   const int32_t i = sel[j];
+  if (i < 0) {  // padding hole (aligns the boundary range to a tile)
+    o_lblocks[j] = -1;
+    o_lkey[j] = 0;
+    o_lmeta[j] = make_int4(0, 0, 0, pack_meta_w(0, 0u, 0));
+    o_lpar[j] = -1;
+    for (int d = 0; d < 12; ++d) o_nbr[j * 12 + d] = kNone;
+    return;
+  }
   o_lblocks[j] = lblocks[i];
   o_lkey[j] = lkey[i];
   int4 m = lmeta[i];

@@ -48,6 +48,7 @@ struct LeafArgs {
   int32_t* split_list;
   int32_t* counters;
   double* epart;  // per-CTA energy partial sums
+  int tile0 = 0;  // first tile of this launch (sharded overlap: sub-ranges)
 };
 
 // table direction of a step that leaves the block along the given axes
@@ -179,7 +180,8 @@ __global__ void __launch_bounds__(kT, OCTF_LEAF_MINB) k_leaf_pass(LeafArgs<T> a)
   using A = Arith<T>;
   const LeafParams<T> p = a.p;
   // the pool is int32-indexed, so every leaf index fits 32 bits
-  const int gid = (int)(blockIdx.x * kT + threadIdx.x);  // launched with kT
+  const int tile_id = (int)blockIdx.x + a.tile0;  // one CTA = one tile
+  const int gid = tile_id * kT + (int)threadIdx.x;  // launched with kT
   const int i = gid >> 3;
   const int c = gid & 7;
   const bool inrange = i < (int)a.nlb;
@@ -194,7 +196,7 @@ __global__ void __launch_bounds__(kT, OCTF_LEAF_MINB) k_leaf_pass(LeafArgs<T> a)
   if (NV > 0) {
     if (threadIdx.x == 0) {
       mbar_init(&s_bar, 1);
-      const size_t tile = blockIdx.x;
+      const size_t tile = tile_id;
       const unsigned fbytes = NVP * kTileLeaves * 4;
       const unsigned abytes = BINW ? kTileLeaves * 4 : fbytes;
       mbar_expect_tx(&s_bar, fbytes + abytes);
@@ -360,6 +362,6 @@ __global__ void __launch_bounds__(kT, OCTF_LEAF_MINB) k_leaf_pass(LeafArgs<T> a)
     typedef cub::BlockReduce<double, kT> BR;
     __shared__ typename BR::TempStorage tmp;
     const double tot = BR(tmp).Sum(eterm);
-    if (threadIdx.x == 0) a.epart[blockIdx.x] = tot;
+    if (threadIdx.x == 0) a.epart[tile_id] = tot;
   }
 }

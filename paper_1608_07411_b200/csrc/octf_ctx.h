@@ -264,6 +264,24 @@ struct PdHostArgs {
   int npasses;
   double* energies;  // host, npasses: energy of u before each pass
 };
+// sharded overlap: one frozen pass split into tile ranges (interior tiles
+// while the halo is in flight, then boundary tiles), then the finish
+struct TileArgs {
+  const void* usnap;
+  void* uval;
+  const int32_t* child;
+  const int64_t* state;
+  int64_t cap;
+  PassParams prm;
+  int tile0, ntiles;
+};
+void pass_tiles_f64(Ctx& c, TileArgs& a, cudaStream_t st);
+void pass_tiles_f32(Ctx& c, TileArgs& a, cudaStream_t st);
+void pass_finish_f64(Ctx& c, void* uval, const int32_t* child,
+                     double* dev_energy, cudaStream_t st);
+void pass_finish_f32(Ctx& c, void* uval, const int32_t* child,
+                     double* dev_energy, cudaStream_t st);
+
 // solver="pd" split/join on the current set after a pass
 struct PdRsArgs {
   void* f[5];          // u, ubar, px, py, pz of the current set

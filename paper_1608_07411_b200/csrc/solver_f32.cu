@@ -29,6 +29,13 @@ void propagate_levels_f32(Ctx& c, float* v, const int32_t* child, int lo, int hi
 }  // namespace octf
 
 namespace octf {
+void pass_tiles_f32(Ctx& c, TileArgs& a, cudaStream_t st) {
+  pass_tiles_impl<float>(c, a, st);
+}
+void pass_finish_f32(Ctx& c, void* uval, const int32_t* child,
+                     double* dev_energy, cudaStream_t st) {
+  pass_finish_impl<float>(c, (float*)uval, child, dev_energy, st);
+}
 void pd_restructure_f32(Ctx& c, PdRsArgs& a, cudaStream_t st) {
   pd_restructure_impl<float>(c, a, st);
 }

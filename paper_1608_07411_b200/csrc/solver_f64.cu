@@ -29,6 +29,13 @@ void propagate_levels_f64(Ctx& c, double* v, const int32_t* child, int lo, int h
 }  // namespace octf
 
 namespace octf {
+void pass_tiles_f64(Ctx& c, TileArgs& a, cudaStream_t st) {
+  pass_tiles_impl<double>(c, a, st);
+}
+void pass_finish_f64(Ctx& c, void* uval, const int32_t* child,
+                     double* dev_energy, cudaStream_t st) {
+  pass_finish_impl<double>(c, (double*)uval, child, dev_energy, st);
+}
 void pd_restructure_f64(Ctx& c, PdRsArgs& a, cudaStream_t st) {
   pd_restructure_impl<double>(c, a, st);
 }

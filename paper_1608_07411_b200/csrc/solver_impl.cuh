@@ -716,9 +716,12 @@ template <typename T>
 void launch_leaf_pass(Ctx& c, const T* snap, T* uval, const int32_t* child,
                       const LeafParams<T>& lp, bool frozen, double* epart,
                       cudaStream_t st, bool timed = true,
-                      bool write_parent = false) {
-  const unsigned g = leaf_grid(c);
+                      bool write_parent = false, int tile0 = 0,
+                      int ntiles = -1) {
+  const unsigned g = ntiles < 0 ? leaf_grid(c) : (unsigned)ntiles;
+  if (g == 0) return;
   LeafArgs<T> a;
+  a.tile0 = tile0;
   a.lpar = c.lpar.p;
   a.write_parent = write_parent;
   a.lblocks = c.lblocks.p;
@@ -1442,6 +1445,31 @@ void pd_restructure_impl(Ctx& c, PdRsArgs& a, cudaStream_t st) {
   c.valid = false;
   c.own_change = true;
   OCTF_CUDA(cudaStreamSynchronize(st));
+}
+
+// leaf kernel of a frozen pass over tiles [tile0, tile0 + ntiles); the
+// energy partials land at their tile index, summed by pass_finish_impl
+template <typename T>
+void pass_tiles_impl(Ctx& c, TileArgs& a, cudaStream_t st) {
+  ensure_prepared<T>(c, a.child, a.cap, a.prm.d_max, a.state, st);
+  if (c.nviews <= 0) throw Error(kEArg, "at least one view is required");
+  const int g = (int)leaf_grid(c);
+  if (a.tile0 < 0 || a.ntiles < 0 || a.tile0 + a.ntiles > g)
+    throw Error(kEArg, "tile range outside the leaf-block list");
+  c.partials.ensure(g);
+  const LeafParams<T> lp = leaf_params<T>(a.prm);
+  launch_leaf_pass<T>(c, (const T*)a.usnap, (T*)a.uval, a.child, lp, true,
+                      c.partials.p, st, false, false, a.tile0, a.ntiles);
+}
+
+// propagate every level of the pass's output and sum the pass's energy
+// partials (all tiles) into a device double
+template <typename T>
+void pass_finish_impl(Ctx& c, T* uval, const int32_t* child,
+                      double* dev_energy, cudaStream_t st) {
+  if (!c.valid) throw Error(kEArg, "context not prepared");
+  launch_propagate<T>(c, uval, child, st);
+  sum_partials(c, c.partials.p, leaf_grid(c), 1, dev_energy, st);
 }
 
 // propagate levels hi-1 .. lo only (the replicated top of a sharded tree)

@@ -147,6 +147,10 @@ class ShardPlan:
     halo: list = field(default_factory=list)    # per rank: slots to receive
     send: dict = field(default_factory=dict)    # (src, dst) -> slots
     top_levels: int = 0                         # propagate levels [0, k)
+    # per rank: leading tiles of sel whose stencils read only values the
+    # rank computes itself (interior); sel is ordered interior blocks, -1
+    # padding to a whole tile, boundary blocks
+    interior_tiles: list = field(default_factory=list)
 
 
 def _unit_of(st: Structure, k: int) -> np.ndarray:
@@ -164,6 +168,24 @@ def _unit_of(st: Structure, k: int) -> np.ndarray:
         at = np.nonzero(live & (lvl == L))[0]
         unit[at] = unit[st.parent[at]]
     return unit
+
+
+def _interior(st: Structure, slots, valid, owner, idx, r, chunk=1 << 16):
+    """Leaf blocks (indices into st.lblocks) whose stencil reads -- their own
+    eight slots, the twelve neighbour blocks' slots, coarse neighbours --
+    are all nodes rank r computes itself (no halo, no replicated top)."""
+    out = np.zeros(idx.size, dtype=bool)
+    for lo in range(0, idx.size, chunk):
+        j = idx[lo:lo + chunk]
+        refs = st.nbr[j].astype(np.int64)                       # (n, 12)
+        same = np.where(refs[:, :, None] >= 0,
+                        refs[:, :, None] + np.arange(8)[None, None, :], -1)
+        coarse = np.where(refs <= -2, -refs - 2, -1)
+        own = np.where(valid[j], slots[j], -1)
+        reads = np.concatenate([own, same.reshape(len(j), -1), coarse], axis=1)
+        ok = (reads < 0) | (owner[np.maximum(reads, 0)] == r)
+        out[lo:lo + chunk] = ok.all(axis=1)
+    return out
 
 
 def plan(child, d_max: int, nranks: int, used: int | None = None,
@@ -209,15 +231,21 @@ def plan(child, d_max: int, nranks: int, used: int | None = None,
         own = isleaf & (owner[sl] == r)
         m = (own * (1 << np.arange(8))[None, :]).sum(axis=1).astype(np.uint8)
         idx = np.nonzero(m)[0]
-        p.sel.append(idx.astype(np.int32))
-        p.masks.append(m[idx])
+        inner = _interior(st, slots, valid, owner, idx, r)
+        ii, bb = idx[inner], idx[~inner]
+        pad = (-ii.size) % 32          # 32 leaf blocks = one 256-leaf tile
+        sel = np.concatenate([ii, np.full(pad, -1), bb]).astype(np.int32)
+        msk = np.concatenate([m[ii], np.zeros(pad, np.uint8), m[bb]])
+        p.sel.append(sel)
+        p.masks.append(msk.astype(np.uint8))
+        p.interior_tiles.append((ii.size + pad) // 32)
     # halo: every slot the rank's stencils can read (whole neighbour blocks,
     # coarse leaves, all siblings of processed blocks) plus the unit roots
     # the top recomputation needs, minus what it owns
     top = (owner < 0) & (st.level >= 0)
     roots = units
     for r in range(nranks):
-        idx = p.sel[r]
+        idx = p.sel[r][p.sel[r] >= 0]
         need = [slots[idx][valid[idx]]]
         refs = st.nbr[idx].astype(np.int64).ravel()
         same = refs[refs >= 0]
@@ -260,6 +288,7 @@ class ShardedSolver:
         s.kern.ctx_prepare(s.ctx, s.u.child, s.u.state, s.u.d_max, s.vvals,
                            s.vws, s.vchilds)
         s.kern.ctx_select(s.ctx, plan.sel[rank], plan.masks[rank])
+        self.tiles = s.ctx.info()["tiles"]
         self.exchange = exchange if exchange is not None else HaloExchange(
             plan, rank, s.u.value.device, s.u.value.dtype)
         self.e = torch.zeros(max(params.iterations, 1), dtype=torch.float64,
@@ -290,11 +319,62 @@ class ShardedSolver:
                                 ctx=s.ctx)
         s.cur, s.nxt = s.nxt, s.cur
 
-    def run(self, t0: int, k: int) -> None:
+    def run(self, t0: int, k: int, overlap: bool = True) -> None:
+        if not overlap:
+            for t in range(t0, t0 + k):
+                self.compute(t)
+                self.exchange.exchange(self.s.nxt[:self.s.u.used], self.group)
+                self.finish()
+            return
+        # overlapped: pass t's interior tiles run while the previous pass's
+        # halo is in flight; same values as above
         for t in range(t0, t0 + k):
-            self.compute(t)
-            self.exchange.exchange(self.s.nxt[:self.s.u.used], self.group)
-            self.finish()
+            works = self.exchange.start(self.s.cur[:self.s.u.used], self.group)
+            self.interior(t)
+            self.exchange.complete(works, self.s.cur[:self.s.u.used])
+            self.boundary(t)
+        self.flush()
+
+    # ---- the overlapped pass in its three stages (driven by ``run``, or
+    # in lock-step by a single-GPU test)
+    def interior(self, t: int) -> None:
+        """Leaf tiles whose stencils read only this rank's values: may run
+        before the previous pass's halo has arrived."""
+        from .fusion import step_scale
+        s, p, u = self.s, self.params, self.s.u
+        ti = self.plan.interior_tiles[self.rank]
+        if ti:
+            s.kern.pass_tiles(s.cur, s.nxt, u.child, u.state, s.vvals, s.vws,
+                              s.vchilds, u.d_max, p.lam, p.eps, p.gamma,
+                              step_scale(t, p), p.clamp, 0, ti, ctx=s.ctx)
+
+    def boundary(self, t: int) -> None:
+        """After the halo of the previous pass is in ``cur``: recompute the
+        replicated top, update the remaining tiles, propagate, energy."""
+        import torch
+        from .fusion import step_scale
+        s, p, u = self.s, self.params, self.s.u
+        s.kern.propagate_levels(s.cur, u.child, 0, self.plan.top_levels,
+                                ctx=s.ctx)
+        ti = self.plan.interior_tiles[self.rank]
+        nt = self.tiles - ti
+        if nt:
+            s.kern.pass_tiles(s.cur, s.nxt, u.child, u.state, s.vvals, s.vws,
+                              s.vchilds, u.d_max, p.lam, p.eps, p.gamma,
+                              step_scale(t, p), p.clamp, ti, nt, ctx=s.ctx)
+        if t >= self.e.shape[0]:
+            self.e = torch.cat([self.e, torch.zeros_like(self.e)])
+        s.kern.pass_finish(s.nxt, u.child, self.e[t:t + 1], ctx=s.ctx)
+        s.cur, s.nxt = s.nxt, s.cur
+        self.t = t + 1
+
+    def flush(self) -> None:
+        """Exchange and top recomputation after the last overlapped pass, so
+        ``values`` holds the halo and top of the final state."""
+        s, u = self.s, self.s.u
+        self.exchange.exchange(s.cur[:u.used], self.group)
+        s.kern.propagate_levels(s.cur, u.child, 0, self.plan.top_levels,
+                                ctx=s.ctx)
 
     def energies(self, reduce: bool = True):
         """Energy before each pass run so far, summed over ranks."""
@@ -330,7 +410,10 @@ class HaloExchange:
                 idx = torch.as_tensor(r, dtype=torch.int64, device=device)
                 self.recvs[q] = (idx, torch.empty(r.size, dtype=dtype, device=device))
 
-    def exchange(self, values, group=None):
+    def start(self, values, group=None):
+        """Post the sends of this rank's values and the receives of its halo;
+        returns the pending works (with NCCL the transfer runs on its own
+        stream, concurrent with kernels launched next)."""
         import torch
         import torch.distributed as dist
         ops = []
@@ -339,8 +422,15 @@ class HaloExchange:
             ops.append(dist.P2POp(dist.isend, buf, q, group))
         for q, (idx, buf) in self.recvs.items():
             ops.append(dist.P2POp(dist.irecv, buf, q, group))
-        if ops:
-            for w in dist.batch_isend_irecv(ops):
-                w.wait()
+        return dist.batch_isend_irecv(ops) if ops else []
+
+    def complete(self, works, values):
+        """Wait for ``start``'s works (device-side for NCCL) and scatter the
+        received halo into ``values``."""
+        for w in works:
+            w.wait()
         for q, (idx, buf) in self.recvs.items():
             values.index_copy_(0, idx, buf)
+
+    def exchange(self, values, group=None):
+        self.complete(self.start(values, group), values)

@@ -69,3 +69,49 @@ def test_lockstep_shards_match_single_gpu(full, world):
     e = sum(s.energies(reduce=False).cpu().numpy() for s in ranks)
     want = [st.energy for st in ref.stats]
     np.testing.assert_allclose(e[1:], want[:-1], rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("full,world", [(True, 2), (False, 3)])
+def test_lockstep_overlapped_shards_match_single_gpu(full, world):
+    """The overlapped pass (interior tiles before the halo of the previous
+    pass arrives, boundary tiles after) gives the single-GPU values bit for
+    bit; interior and boundary tile ranges both non-empty."""
+    from paper_1608_07411_b200 import fusion, shard
+    u0h, views_h = _scene(full, d=6)
+    p = fusion.FusionParams(iterations=5, tau=-1.0, tau_split=0.0,
+                            tau_join=1.5, lam=0.4)
+    views = [_dev(v) for v in views_h]
+    ref = fusion.fuse(_dev(u0h), views, p)
+    rh = ref.field.to_host()
+    pl = shard.plan(u0h.child, u0h.d_max, world, used=u0h.used, k=2)
+    assert all(ti > 0 for ti in pl.interior_tiles)
+    ranks = [shard.ShardedSolver(_dev(u0h), views, p, pl, r, precision="fp64",
+                                 exchange=_NoExchange()) for r in range(world)]
+    assert any(s.tiles > pl.interior_tiles[r] for r, s in enumerate(ranks))
+
+    def halo_copy():   # the previous pass's values, into every halo
+        for (src, dst), idx in pl.send.items():
+            if idx.size:
+                ii = torch.as_tensor(idx, device="cuda")
+                ranks[dst].s.cur[ii] = ranks[src].s.cur[ii]
+    for t in range(p.iterations):
+        for s in ranks:
+            s.interior(t)
+        halo_copy()
+        for s in ranks:
+            s.boundary(t)
+    halo_copy()
+    for s in ranks:
+        s.s.kern.propagate_levels(s.s.cur, s.s.u.child, 0, pl.top_levels,
+                                  ctx=s.s.ctx)
+    used = u0h.used
+    leaves = np.nonzero(rh.child[:used] < 0)[0]
+    for r, s in enumerate(ranks):
+        got = s.values[:used].cpu().numpy()
+        mine = leaves[pl.owner[leaves] == r]
+        assert mine.size and np.array_equal(got[mine], rh.value[mine]), r
+        halo = pl.halo[r]          # and the halo after the final exchange
+        assert np.array_equal(got[halo], rh.value[halo]), r
+    e = sum(s.energies(reduce=False).cpu().numpy() for s in ranks)
+    want = [st.energy for st in ref.stats]
+    np.testing.assert_allclose(e[1:], want[:-1], rtol=1e-12, atol=0)

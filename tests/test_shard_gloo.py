@@ -163,3 +163,76 @@ def test_host_tables_match_reference_descent():
                 lvl += 1
             want = child[node] if (lvl == L - 1 and child[node] >= 0) else -node - 2
             assert st.nbr[i, d] == want
+
+
+def test_plan_interior_and_boundary_ranges():
+    """The plan orders each rank's leaf blocks interior-first: blocks in the
+    leading interior tiles read (own slots, neighbour blocks, coarse
+    neighbours) only nodes the rank computes itself; the padding to a whole
+    tile is -1 with an empty mask; every owned leaf appears exactly once."""
+    u0, views, p = scene()
+    st = shard.structure(u0.child, u0.d_max, u0.used)
+    for world in (2, 3):
+        pl = shard.plan(u0.child, u0.d_max, world, used=u0.used, k=2)
+        seen = np.zeros(u0.used, dtype=int)
+        for r in range(world):
+            sel, msk, ti = pl.sel[r], pl.masks[r], pl.interior_tiles[r]
+            assert sel.size == msk.size and ti * 32 <= sel.size
+            pad = sel < 0
+            assert not msk[pad].any()
+            for j, (i, m) in enumerate(zip(sel, msk)):
+                if i < 0:
+                    continue
+                b = int(st.lblocks[i])
+                for c in range(8):
+                    if (m >> c) & 1:
+                        seen[b + c] += 1
+                        assert pl.owner[b + c] == r
+                if j < ti * 32:          # interior: every read is owned
+                    reads = [b + c for c in range(8) if b != 0 or c == 0]
+                    for ref in st.nbr[i]:
+                        if ref >= 0:
+                            reads += [int(ref) + c for c in range(8)]
+                        elif ref <= -2:
+                            reads.append(int(-ref - 2))
+                    assert all(pl.owner[x] == r for x in reads)
+        leaves = np.nonzero(u0.child[:u0.used] < 0)[0]
+        assert (seen[leaves] == 1).all()
+
+
+def test_halo_exchange_start_complete_equals_exchange():
+    world = 2
+    port = free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_start_complete_worker, args=(r, world, port, q))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    out = [q.get(timeout=120) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+    assert all(ok for _, ok in out)
+
+
+def _start_complete_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        u0, views, p = scene()
+        pl = shard.plan(u0.child, u0.d_max, world, used=u0.used, k=2)
+        ex = shard.HaloExchange(pl, rank, torch.device("cpu"), torch.float64)
+        base = torch.arange(u0.used, dtype=torch.float64)
+        owned = torch.from_numpy(pl.owner[:u0.used] == rank)
+        a = torch.where(owned, base, torch.full_like(base, -7.0))
+        b = a.clone()
+        ex.exchange(a)
+        works = ex.start(b)
+        b.mul_(1.0)                 # work between post and completion
+        ex.complete(works, b)
+        halo = torch.as_tensor(pl.halo[rank], dtype=torch.int64)
+        ok = torch.equal(a, b) and torch.equal(a[halo], base[halo])
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()

@@ -22,6 +22,23 @@
 // previous pass's post-propagate state, from the same values and roots.
 #pragma once
 
+// per-warp staging (each warp bulk-copies its own 32 leaves' rows on its
+// own mbarrier) was measured slower than one CTA-wide copy: 17 copies of
+// 128 B per warp cost more than the CTA barrier (cfg2 leaf kernel 0.43 vs
+// 0.34 ms); kept as a switch.  Per-warp energy partials (no closing CTA
+// reduction) were 1.6 % faster on cfg2 but 8 % slower on cfg5 (registers at
+// N = 32): off by default.
+#ifndef OCTF_LEAF_WARPSTAGE
+#define OCTF_LEAF_WARPSTAGE 0
+#endif
+#ifndef OCTF_LEAF_WARPPART
+#define OCTF_LEAF_WARPPART 0
+#endif
+#if OCTF_LEAF_WARPPART
+constexpr int kLeafParts = 8;  // energy partials per CTA (one per warp)
+#else
+constexpr int kLeafParts = 1;
+#endif
 #ifndef OCTF_LEAF_MINB
 #define OCTF_LEAF_MINB 1
 #endif
@@ -192,7 +209,35 @@ __global__ void __launch_bounds__(kT, OCTF_LEAF_MINB) k_leaf_pass(LeafArgs<T> a)
   // Padding leaves and non-leaf slots hold zeros, so the copy is in bounds.
   constexpr int NVP = (NV + 3) & ~3;
   extern __shared__ __align__(128) float s_tile[];
+#if OCTF_LEAF_WARPSTAGE
+  // each warp stages the rows of its own 32 leaves (NVP rows of 128 B plus
+  // the mask / weight rows) with one bulk copy per row on its own mbarrier
+  __shared__ __align__(8) uint64_t s_bars[kT / 32];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* const s_bar_p = &s_bars[wid];
+  if (NV > 0) {
+    const unsigned rows = BINW ? NVP + 1 : 2 * NVP;
+    if (lane == 0) {
+      mbar_init(s_bar_p, 1);
+      mbar_expect_tx(s_bar_p, rows * 128u);
+    }
+    __syncwarp();
+    const size_t tile = tile_id;
+    for (unsigned r = lane; r < rows; r += 32) {
+      const float* src;
+      if (r < (unsigned)NVP)
+        src = a.F + tile * NVP * kTileLeaves + r * kTileLeaves;
+      else if (BINW)
+        src = reinterpret_cast<const float*>(a.M + tile * kTileLeaves);
+      else
+        src = a.W + tile * NVP * kTileLeaves + (r - NVP) * kTileLeaves;
+      bulk_g2s(s_tile + r * kTileLeaves + wid * 32, src + wid * 32, 128,
+               s_bar_p);
+    }
+  }
+#else
   __shared__ __align__(8) uint64_t s_bar;
+  uint64_t* const s_bar_p = &s_bar;
   if (NV > 0) {
     if (threadIdx.x == 0) {
       mbar_init(&s_bar, 1);
@@ -210,6 +255,7 @@ __global__ void __launch_bounds__(kT, OCTF_LEAF_MINB) k_leaf_pass(LeafArgs<T> a)
     }
     __syncthreads();  // barrier initialised before anyone waits on it
   }
+#endif
 
   // one 16 B load: base slot, parent cell, leaf mask and level
   const int4 meta = inrange ? __ldg(a.lmeta + i) : make_int4(0, 0, 0, 0);
@@ -296,7 +342,7 @@ __global__ void __launch_bounds__(kT, OCTF_LEAF_MINB) k_leaf_pass(LeafArgs<T> a)
     den += wv;
   };
   if (NV > 0) {
-    mbar_wait(&s_bar, 0);
+    mbar_wait(s_bar_p, 0);
     const int t = threadIdx.x;
     const float* sf = s_tile;
     if (BINW) {
@@ -359,9 +405,17 @@ __global__ void __launch_bounds__(kT, OCTF_LEAF_MINB) k_leaf_pass(LeafArgs<T> a)
       atomicAdd(a.counters + 1, 1);
   }
   if (ENERGY) {
+#if OCTF_LEAF_WARPPART
+    double tot = eterm;  // fixed butterfly: deterministic
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(FULL, tot, o);
+    if ((threadIdx.x & 31) == 0)
+      a.epart[tile_id * kLeafParts + (threadIdx.x >> 5)] = tot;
+#else
     typedef cub::BlockReduce<double, kT> BR;
     __shared__ typename BR::TempStorage tmp;
     const double tot = BR(tmp).Sum(eterm);
     if (threadIdx.x == 0) a.epart[tile_id] = tot;
+#endif
   }
 }

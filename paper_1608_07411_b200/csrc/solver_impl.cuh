@@ -698,6 +698,10 @@ void ensure_prepared(Ctx& c, const int32_t* child, int64_t cap, int d_max,
 
 // grid of the leaf kernel (also the number of energy partials per pass)
 inline unsigned leaf_grid(const Ctx& c) { return blocks_for(c.nlb * 8); }
+// energy partials the leaf kernel writes per pass (kLeafParts per CTA)
+inline int64_t leaf_parts(const Ctx& c) {
+  return (int64_t)leaf_grid(c) * kLeafParts;
+}
 
 template <typename T, bool FZ, bool BW, bool EN, int N>
 void launch_leaf(unsigned g, cudaStream_t st, const LeafArgs<T>& a) {
@@ -842,14 +846,14 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
   OCTF_CUDA(cudaMemsetAsync(c.counters.p, 0, 8 * sizeof(int32_t), st));
   double* epart = nullptr;
   if (a.want_energy) {
-    c.partials.ensure(leaf_grid(c));
+    c.partials.ensure(leaf_parts(c));
     c.dscalar.ensure(1);
     epart = c.partials.p;
   }
   launch_leaf_pass<T>(c, (const T*)a.usnap, (T*)a.uval, a.child, lp, frozen,
                       epart, st);
   if (epart) {
-    sum_partials(c, epart, leaf_grid(c), 1, c.dscalar.p, st);
+    sum_partials(c, epart, leaf_parts(c), 1, c.dscalar.p, st);
     OCTF_CUDA(cudaMemcpyAsync(c.h_scalar, c.dscalar.p, sizeof(double),
                               cudaMemcpyDeviceToHost, st));
   }
@@ -1124,7 +1128,7 @@ void frozen_passes_impl(Ctx& c, FrozenArgs& a, cudaStream_t st) {
   // fixed-size scratch (no allocation inside a timed loop): energy
   // partials for kChunk passes, one energy slot per pass
   constexpr int kChunk = 32;
-  const unsigned g = leaf_grid(c);
+  const int64_t g = leaf_parts(c);
   c.partials.ensure((size_t)g * kChunk);
   c.dscalar.ensure(a.npasses > 1024 ? a.npasses : 1024);
   c.counters.ensure(64);
@@ -1456,7 +1460,7 @@ void pass_tiles_impl(Ctx& c, TileArgs& a, cudaStream_t st) {
   const int g = (int)leaf_grid(c);
   if (a.tile0 < 0 || a.ntiles < 0 || a.tile0 + a.ntiles > g)
     throw Error(kEArg, "tile range outside the leaf-block list");
-  c.partials.ensure(g);
+  c.partials.ensure(leaf_parts(c));
   const LeafParams<T> lp = leaf_params<T>(a.prm);
   launch_leaf_pass<T>(c, (const T*)a.usnap, (T*)a.uval, a.child, lp, true,
                       c.partials.p, st, false, false, a.tile0, a.ntiles);
@@ -1469,7 +1473,7 @@ void pass_finish_impl(Ctx& c, T* uval, const int32_t* child,
                       double* dev_energy, cudaStream_t st) {
   if (!c.valid) throw Error(kEArg, "context not prepared");
   launch_propagate<T>(c, uval, child, st);
-  sum_partials(c, c.partials.p, leaf_grid(c), 1, dev_energy, st);
+  sum_partials(c, c.partials.p, leaf_parts(c), 1, dev_energy, st);
 }
 
 // propagate levels hi-1 .. lo only (the replicated top of a sharded tree)

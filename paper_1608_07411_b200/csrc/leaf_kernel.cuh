@@ -42,6 +42,17 @@ constexpr int kLeafParts = 1;
 #ifndef OCTF_LEAF_MINB
 #define OCTF_LEAF_MINB 1
 #endif
+// resident CTAs per SM the register budget is cut for, by sample count:
+// measured best 6 (<= 40 registers) for N <= 16 (cfg2: 0.341 -> 0.327 ms)
+// but 4 for N = 32 (cfg5: 6 costs 6 %); OCTF_LEAF_MINB sets the latter
+#ifndef OCTF_LEAF_MINB_SMALL
+#define OCTF_LEAF_MINB_SMALL 6
+#endif
+constexpr int leaf_minb(int nv, int tbytes) {
+  // (f64 values need the registers: 40 would spill)
+  return (tbytes == 4 && nv > 0 && nv <= 16) ? OCTF_LEAF_MINB_SMALL
+                                             : OCTF_LEAF_MINB;
+}
 
 template <typename T>
 struct LeafArgs {
@@ -193,7 +204,7 @@ constexpr size_t leaf_smem_bytes(int nv, bool binw) {
 }
 
 template <typename T, bool FROZEN, bool BINW, bool ENERGY, int NV>
-__global__ void __launch_bounds__(kT, OCTF_LEAF_MINB) k_leaf_pass(LeafArgs<T> a) {
+__global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(LeafArgs<T> a) {
   using A = Arith<T>;
   const LeafParams<T> p = a.p;
   // the pool is int32-indexed, so every leaf index fits 32 bits

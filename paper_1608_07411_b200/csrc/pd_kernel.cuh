@@ -17,6 +17,12 @@
 #ifndef OCTF_PD_MINB
 #define OCTF_PD_MINB 4  // 4 CTAs of 256 per SM: <= 64 registers
 #endif
+#ifndef OCTF_PD_MINB_SMALL
+#define OCTF_PD_MINB_SMALL 5  // binary weights, N <= 16 (48 regs: cfg2 pd 54.8 -> 58.3 %)
+#endif
+constexpr int pd_minb(bool binw, int nv) {
+  return !binw ? 1 : (nv <= 16 ? OCTF_PD_MINB_SMALL : OCTF_PD_MINB);
+}
 
 template <typename T>
 struct PdArgs {
@@ -216,7 +222,7 @@ constexpr size_t pd_smem_bytes(int nv, bool binw) {
 }
 
 template <typename T, bool BINW, int NV>
-__global__ void __launch_bounds__(kT, BINW ? OCTF_PD_MINB : 1) k_pd_pass(PdArgs<T> a) {
+__global__ void __launch_bounds__(kT, pd_minb(BINW, NV)) k_pd_pass(PdArgs<T> a) {
   static_assert(NV > 0 && (NV & (NV - 1)) == 0, "NV: power of two");
   // NV = 64: general weights selected without sorting them (WeightAt)
   constexpr bool WSEL = NV > 32;

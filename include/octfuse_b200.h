@@ -45,6 +45,7 @@ extern "C" {
 #define OCTF_MAX_DEPTH 19
 
 typedef struct octf_ctx octf_ctx;
+typedef struct octf_mesh octf_mesh;
 
 /* message of the last failed call on this thread */
 const char *octf_last_error(void);
@@ -121,6 +122,28 @@ int octf_fuse_passes_frozen(octf_ctx *ctx, int dtype, void *ubuf0, void *ubuf1,
                             const double *xis, int npasses,
                             double *energies_pre, int device_energies,
                             void *stream);
+
+/* Zero-isosurface readout (reference
+ * octfuse/mesh.py:63-125 extract_zero_surface / marching_cubes): marching
+ * cubes over the dense cell-centred grid `values` (device f64, n^3, x-major)
+ * with the observed mask `mask` (device u8 n^3, or NULL = all observed).  A
+ * cube emits its case's triangles only if all eight corners are observed;
+ * vertices are the grid edges' zero crossings, t = v0 / (v0 - v1), sorted by
+ * edge key ((axis*n + x)*n + y)*n + z; faces index them in cube order then
+ * table order -- the reference's vertex and face arrays bit for bit.  The
+ * case tables (tri_table int8[256][32], tri_count int8[256], edge_axis
+ * int8[12], edge_offset int8[12][3]; host) come from the caller
+ * (paper_1608_07411_b200/mesh.py generates them).  world != 0 maps vertices
+ * to origin + (p + 1/2) * voxel_size.  The result lives on the device until
+ * octf_mesh_copy (device destinations) / octf_mesh_free. */
+int octf_marching_cubes(const double *values, const uint8_t *mask, int n,
+                        const int8_t *tri_table, const int8_t *tri_count,
+                        const int8_t *edge_axis, const int8_t *edge_offset,
+                        const double *origin, double voxel_size, int world,
+                        octf_mesh **out, int64_t *nverts, int64_t *nfaces,
+                        void *stream);
+int octf_mesh_copy(octf_mesh *m, double *verts, int32_t *faces, void *stream);
+int octf_mesh_free(octf_mesh *m);
 
 /* Sharded overlap: one frozen descent pass split into
  * leaf-tile ranges, so a rank updates its interior tiles while the halo of

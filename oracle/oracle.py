@@ -454,3 +454,47 @@ def build_view_tsdf(depth, cam, origin, voxel_size, n, delta, eta):
     w = obs & (phi >= -eta)
     f = np.where(w, f, -1.0).astype(np.float32)
     return f, w.astype(np.uint8)
+
+
+# ------------------------------------------------------------ mesh readout --
+
+def extract_zero_surface(values, mask, tables):
+    """mesh.py:63-111 restated (numpy): per 2x2x2 cube of the cell-centred
+    grid, the inside pattern (value < 0, bit c = corner (c>>2&1, c>>1&1,
+    c&1)); cubes with all corners observed emit their case's triangles; each
+    triangle corner is a grid edge keyed ((axis*n + x)*n + y)*n + z;
+    vertices are the sorted unique keys, faces their ranks, positions the
+    linear zero crossing along the edge.  ``tables`` = (tri_table,
+    tri_count, edge_axis, edge_cell_offset)."""
+    tri, cnt, eax, eoff = (np.asarray(t) for t in tables)
+    v = np.asarray(values, dtype=np.float64)
+    n = v.shape[0]
+    m = n - 1
+    case = np.zeros((m, m, m), dtype=np.int64)
+    ok = np.ones((m, m, m), dtype=bool)
+    for c in range(8):
+        dx, dy, dz = (c >> 2) & 1, (c >> 1) & 1, c & 1
+        case |= (v[dx:dx + m, dy:dy + m, dz:dz + m] < 0).astype(np.int64) << c
+        if mask is not None:
+            ok &= np.asarray(mask)[dx:dx + m, dy:dy + m, dz:dz + m]
+    ntri = cnt.astype(np.int64)[case] * ok
+    cx, cy, cz = np.nonzero(ntri)
+    if cx.size == 0:
+        return np.zeros((0, 3)), np.zeros((0, 3), dtype=np.int32)
+    k3 = 3 * ntri[cx, cy, cz]
+    cube = np.repeat(np.arange(cx.size), k3)
+    slot = np.arange(cube.size) - np.repeat(np.cumsum(k3) - k3, k3)
+    e = tri.astype(np.int64)[case[cx, cy, cz][cube], slot]
+    ax = eax.astype(np.int64)[e]
+    off = eoff.astype(np.int64)[e]
+    key = ((ax * n + cx[cube] + off[:, 0]) * n + cy[cube] + off[:, 1]) * n \
+        + cz[cube] + off[:, 2]
+    ukey, inv = np.unique(key, return_inverse=True)
+    gz, gy, gx = ukey % n, (ukey // n) % n, (ukey // (n * n)) % n
+    ga = ukey // (n * n * n)
+    v0 = v[gx, gy, gz]
+    v1 = v[gx + (ga == 0), gy + (ga == 1), gz + (ga == 2)]
+    t = v0 / (v0 - v1)
+    verts = np.column_stack([gx + t * (ga == 0), gy + t * (ga == 1),
+                             gz + t * (ga == 2)])
+    return verts, inv.reshape(-1, 3).astype(np.int32)

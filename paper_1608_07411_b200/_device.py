@@ -7,7 +7,7 @@ import torch
 
 _NP2T = {np.dtype(np.float64): torch.float64, np.dtype(np.float32): torch.float32,
          np.dtype(np.int32): torch.int32, np.dtype(np.int64): torch.int64,
-         np.dtype(np.uint8): torch.uint8}
+         np.dtype(np.uint8): torch.uint8, np.dtype(np.bool_): torch.bool}
 _T2NP = {v: k for k, v in _NP2T.items()}
 
 # Reference pools put the first child block at slot 1 (octree.py:290,

@@ -324,6 +324,49 @@ int octf_fuse_passes_frozen(octf_ctx* ctx, int dtype, void* ubuf0, void* ubuf1,
   });
 }
 
+int octf_marching_cubes(const double* values, const uint8_t* mask, int n,
+                        const int8_t* tri_table, const int8_t* tri_count,
+                        const int8_t* edge_axis, const int8_t* edge_offset,
+                        const double* origin, double voxel_size, int world,
+                        octf_mesh** out, int64_t* nverts, int64_t* nfaces,
+                        void* stream) {
+  return guard([&] {
+    if (!values || !tri_table || !tri_count || !edge_axis || !edge_offset ||
+        !origin || !out || !nverts || !nfaces)
+      throw octf::Error(octf::kEArg, "null argument");
+    need_device();
+    octf_mesh* m = new octf_mesh();
+    try {
+      octf::marching_cubes(values, mask, n, tri_table, tri_count, edge_axis,
+                           edge_offset, origin, voxel_size, world, m, S(stream));
+    } catch (...) {
+      delete m;
+      throw;
+    }
+    *out = m;
+    *nverts = m->nv;
+    *nfaces = m->nf;
+  });
+}
+
+int octf_mesh_copy(octf_mesh* m, double* verts, int32_t* faces, void* stream) {
+  return guard([&] {
+    if (!m) throw octf::Error(octf::kEArg, "null mesh");
+    if (m->nv && verts)
+      OCTF_CUDA(cudaMemcpyAsync(verts, m->verts, m->nv * 3 * sizeof(double),
+                                cudaMemcpyDeviceToDevice, S(stream)));
+    if (m->nf && faces)
+      OCTF_CUDA(cudaMemcpyAsync(faces, m->faces, m->nf * 3 * sizeof(int32_t),
+                                cudaMemcpyDeviceToDevice, S(stream)));
+    OCTF_CUDA(cudaStreamSynchronize(S(stream)));
+  });
+}
+
+int octf_mesh_free(octf_mesh* m) {
+  delete m;
+  return OCTF_OK;
+}
+
 int octf_pass_tiles(octf_ctx* ctx, int dtype, const void* usnap, void* uval,
                     const int32_t* uchild, const int64_t* ustate, int64_t cap,
                     int nviews, const float* const* vvals,

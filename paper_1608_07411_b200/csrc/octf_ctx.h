@@ -12,6 +12,17 @@
 
 #include "octf_common.cuh"
 
+// extracted zero surface (octf_marching_cubes), device arrays
+struct octf_mesh {
+  int64_t nv = 0, nf = 0;
+  double* verts = nullptr;   // nv x 3
+  int32_t* faces = nullptr;  // nf x 3
+  ~octf_mesh() {
+    if (verts) cudaFree(verts);
+    if (faces) cudaFree(faces);
+  }
+};
+
 namespace octf {
 
 // error kinds mirror the reference's three exceptions (_kernels.pyx:26-27,
@@ -302,6 +313,13 @@ void propagate_levels_f64(Ctx& c, double* v, const int32_t* child, int lo,
                           int hi, cudaStream_t st);
 void propagate_levels_f32(Ctx& c, float* v, const int32_t* child, int lo,
                           int hi, cudaStream_t st);
+// marching cubes over a dense cell-centred grid (mesh.cu)
+void marching_cubes(const double* values, const uint8_t* mask, int n,
+                    const int8_t* tri_table, const int8_t* tri_count,
+                    const int8_t* edge_axis, const int8_t* edge_off,
+                    const double* origin, double voxel, int world,
+                    octf_mesh* out, cudaStream_t st);
+
 // restrict the leaf-block list to a subset with per-block leaf masks
 // (sharding); host arrays; regathers samples
 void ctx_select(Ctx& c, const int32_t* sel, const uint8_t* masks,

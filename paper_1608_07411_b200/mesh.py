@@ -1,0 +1,312 @@
+"""Zero-isosurface readout (reference ``mesh.py``).
+
+``marching_cubes(values, seen, dom)`` runs on the GPU (``octf_marching_cubes``,
+``csrc/mesh.cu``) and returns the reference's mesh bit for bit: the same case
+tables, vertex order (ascending grid-edge key), face order (cube order, then
+table order) and f64 vertex arithmetic.  The case tables are generated here
+from the rule the reference documents (``_mctables.py``): per inside/outside
+corner pattern, crossed edges are paired face by face -- two crossings pair
+up, four crossings pair around each inside corner -- the pairs are walked
+into closed loops, each loop is oriented so its normal points from inside to
+outside, and fan-triangulated.  ``tests/test_mesh.py`` checks the tables and
+meshes against fixtures generated from the reference.
+
+PLY I/O, ``vertex_diff`` and the analytic checks are host utilities with the
+reference's names and formats.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._device import as_device, device, ptr, stream_handle
+
+__all__ = ["TriMesh", "extract_zero_surface", "marching_cubes", "MeshDiff",
+           "vertex_diff", "sphere_distances", "signed_volume", "write_ply",
+           "read_ply", "case_tables"]
+
+# corner c of a cube sits at offset (c>>2 & 1, c>>1 & 1, c & 1) (x, y, z),
+# the octree child numbering; edges 0-3 run along x, 4-7 along y, 8-11
+# along z, each given as its (low, high) corner pair
+_CORNER = np.array([((c >> 2) & 1, (c >> 1) & 1, c & 1) for c in range(8)])
+_EDGE = [(c, c | 4) for c in (0, 1, 2, 3)] + \
+        [(c, c | 2) for c in (0, 1, 4, 5)] + \
+        [(c, c | 1) for c in (0, 2, 4, 6)]
+_EDGE_AXIS = np.array([0] * 4 + [1] * 4 + [2] * 4, dtype=np.int8)
+_EDGE_OFF = np.array([_CORNER[lo] for lo, _ in _EDGE], dtype=np.int8)
+
+
+def _faces():
+    """The six faces as (corner list, edge list), x-low, x-high, y-low, ..."""
+    out = []
+    for axis in range(3):
+        bit = 4 >> axis
+        for side in (0, bit):
+            corners = [c for c in range(8) if (c & bit) == side]
+            edges = [e for e, (a, b) in enumerate(_EDGE)
+                     if a in corners and b in corners]
+            out.append((corners, edges))
+    return out
+
+
+def _loops(mask: int, faces):
+    inside = [bool((mask >> c) & 1) for c in range(8)]
+    cut = [inside[a] != inside[b] for a, b in _EDGE]
+    partners = {e: [] for e in range(12) if cut[e]}
+
+    def link(a, b):
+        partners[a].append(b)
+        partners[b].append(a)
+    for corners, edges in faces:
+        hit = [e for e in edges if cut[e]]
+        if len(hit) == 2:
+            link(hit[0], hit[1])
+        elif len(hit) == 4:          # ambiguous face: pair around inside corners
+            for c in corners:
+                if inside[c]:
+                    around = [e for e in hit if c in _EDGE[e]]
+                    link(around[0], around[1])
+    loops, done = [], set()
+    for start in partners:           # ascending edge id
+        if start in done:
+            continue
+        loop, prev, cur = [start], -1, start
+        while True:
+            first, second = partners[cur]
+            step = second if first == prev else first
+            if step == start:
+                break
+            loop.append(step)
+            prev, cur = cur, step
+        done.update(loop)
+        loops.append(loop)
+    return inside, loops
+
+
+def _orient(loop, inside):
+    """Loop order whose (Newell) normal points from inside to outside."""
+    mid = [(_CORNER[_EDGE[e][0]] + _CORNER[_EDGE[e][1]]) / 2.0 for e in loop]
+    nrm = np.zeros(3)
+    for i, p in enumerate(mid):
+        nrm += np.cross(p, mid[(i + 1) % len(mid)])
+    out = np.zeros(3)
+    for e in loop:
+        a, b = _EDGE[e]
+        lo, hi = (b, a) if inside[b] else (a, b)   # inside -> outside
+        out += _CORNER[hi] - _CORNER[lo]
+    return loop if float(nrm @ out) > 0 else loop[::-1]
+
+
+def case_tables():
+    """(tri_table int8[256, 32] padded with -1, tri_count int8[256],
+    edge_axis int8[12], edge_offset int8[12, 3])."""
+    faces = _faces()
+    table = np.full((256, 32), -1, dtype=np.int8)
+    count = np.zeros(256, dtype=np.int8)
+    for mask in range(256):
+        inside, loops = _loops(mask, faces)
+        tri = []
+        for loop in loops:
+            loop = _orient(loop, inside)
+            for i in range(1, len(loop) - 1):
+                tri += [loop[0], loop[i], loop[i + 1]]
+        table[mask, :len(tri)] = tri
+        count[mask] = len(tri) // 3
+    return table, count, _EDGE_AXIS.copy(), _EDGE_OFF.copy()
+
+
+_TABLES = None
+
+
+def _tables():
+    global _TABLES
+    if _TABLES is None:
+        _TABLES = tuple(np.ascontiguousarray(t) for t in case_tables())
+    return _TABLES
+
+
+@dataclass
+class TriMesh:
+    """Indexed triangle mesh, optionally with one scalar per vertex."""
+
+    vertices: np.ndarray
+    faces: np.ndarray
+    quality: np.ndarray | None = None
+
+    def __post_init__(self):
+        self.vertices = np.asarray(self.vertices, dtype=np.float64).reshape(-1, 3)
+        self.faces = np.asarray(self.faces, dtype=np.int32).reshape(-1, 3)
+        if self.quality is not None:
+            self.quality = np.asarray(self.quality, dtype=np.float64).reshape(-1)
+            if self.quality.shape[0] != self.vertices.shape[0]:
+                raise ValueError("one quality value per vertex required")
+
+    @property
+    def vertex_count(self) -> int:
+        return self.vertices.shape[0]
+
+    @property
+    def face_count(self) -> int:
+        return self.faces.shape[0]
+
+
+def _extract(values, mask, origin=None, voxel=1.0, world=False):
+    v = as_device(values, torch.float64).contiguous()
+    n = v.shape[0]
+    if v.dim() != 3 or tuple(v.shape) != (n, n, n) or n < 2:
+        raise ValueError("values must be a cubic grid with edge >= 2")
+    m = None
+    if mask is not None:
+        m = as_device(mask, torch.bool)
+        if tuple(m.shape) != tuple(v.shape):
+            raise ValueError("mask shape mismatch")
+        m = m.to(torch.uint8).contiguous()
+    tri, cnt, eax, eoff = _tables()
+    org = np.ascontiguousarray(np.asarray(origin if origin is not None
+                                          else (0.0, 0.0, 0.0), np.float64))
+    h = ctypes.c_void_p()
+    nv, nf = ctypes.c_int64(), ctypes.c_int64()
+    _lib.call("octf_marching_cubes", ptr(v), ptr(m) if m is not None else None,
+              n, tri.ctypes.data, cnt.ctypes.data, eax.ctypes.data,
+              eoff.ctypes.data, org.ctypes.data, float(voxel), int(world),
+              ctypes.byref(h), ctypes.byref(nv), ctypes.byref(nf),
+              stream_handle())
+    try:
+        verts = torch.empty((nv.value, 3), dtype=torch.float64, device=device())
+        faces = torch.empty((nf.value, 3), dtype=torch.int32, device=device())
+        _lib.call("octf_mesh_copy", h, ptr(verts) if nv.value else None,
+                  ptr(faces) if nf.value else None, stream_handle())
+    finally:
+        _lib.lib().octf_mesh_free(h)
+    return verts.cpu().numpy(), faces.cpu().numpy()
+
+
+def extract_zero_surface(values, mask=None):
+    """Zero level set in grid index coordinates (mesh.py:63-111): a cube is
+    skipped unless ``mask`` is true at all eight corners.  Returns
+    (vertices, faces) numpy arrays."""
+    return _extract(values, mask)
+
+
+def marching_cubes(values, seen, dom) -> TriMesh:
+    """The implicit surface in world coordinates (mesh.py:114-125): grid
+    samples at voxel centres, index i -> origin + (i + 1/2) * voxel_size."""
+    if tuple(values.shape) != (dom.resolution,) * 3:
+        raise ValueError("grid does not match the domain resolution")
+    verts, faces = _extract(values, seen, dom.origin, dom.voxel_size, True)
+    return TriMesh(verts, faces)
+
+
+@dataclass
+class MeshDiff:
+    """Symmetric nearest-vertex distance statistics between two meshes."""
+
+    d_ab: np.ndarray
+    d_ba: np.ndarray
+
+    @property
+    def mean(self) -> float:
+        return float(np.concatenate([self.d_ab, self.d_ba]).mean())
+
+    @property
+    def std(self) -> float:
+        return float(np.concatenate([self.d_ab, self.d_ba]).std())
+
+    @property
+    def max(self) -> float:
+        return float(np.concatenate([self.d_ab, self.d_ba]).max())
+
+
+def vertex_diff(a: TriMesh, b: TriMesh) -> MeshDiff:
+    """Nearest-vertex distances both ways (host, scipy k-d tree)."""
+    from scipy.spatial import cKDTree
+    if a.vertex_count == 0 or b.vertex_count == 0:
+        raise ValueError("cannot compare empty meshes")
+    return MeshDiff(d_ab=cKDTree(b.vertices).query(a.vertices)[0],
+                    d_ba=cKDTree(a.vertices).query(b.vertices)[0])
+
+
+def sphere_distances(mesh: TriMesh, center, radius: float) -> np.ndarray:
+    """Per-vertex absolute distance to an analytic sphere surface."""
+    if mesh.vertex_count == 0:
+        raise ValueError("mesh has no vertices")
+    r = np.linalg.norm(mesh.vertices - np.asarray(center, dtype=np.float64),
+                       axis=1)
+    return np.abs(r - radius)
+
+
+def signed_volume(mesh: TriMesh) -> float:
+    """Divergence-theorem volume; positive for outward-oriented meshes."""
+    a, b, c = (mesh.vertices[mesh.faces[:, k]] for k in range(3))
+    return float(np.einsum("ij,ij->i", a, np.cross(b, c)).sum() / 6.0)
+
+
+def write_ply(path, mesh: TriMesh) -> None:
+    """ASCII PLY, double vertex properties (%.17g), optional quality."""
+    q = mesh.quality
+    head = ["ply", "format ascii 1.0", f"element vertex {mesh.vertex_count}",
+            "property double x", "property double y", "property double z"]
+    if q is not None:
+        head.append("property double quality")
+    head += [f"element face {mesh.face_count}",
+             "property list uchar int vertex_indices", "end_header"]
+    with open(path, "w") as fp:
+        fp.write("\n".join(head) + "\n")
+        for i, (x, y, z) in enumerate(mesh.vertices):
+            extra = f" {q[i]:.17g}" if q is not None else ""
+            fp.write(f"{x:.17g} {y:.17g} {z:.17g}{extra}\n")
+        for i, j, k in mesh.faces:
+            fp.write(f"3 {i} {j} {k}\n")
+
+
+def read_ply(path) -> TriMesh:
+    """Read the ASCII PLY subset ``write_ply`` produces."""
+    lines = Path(path).read_text().splitlines()
+    if not lines or lines[0].strip() != "ply":
+        raise ValueError(f"{path}: not a PLY file")
+    nvert = nface = 0
+    props, element, i = [], None, 1
+    while True:
+        if i >= len(lines):
+            raise ValueError(f"{path}: missing end_header")
+        parts = lines[i].split()
+        i += 1
+        if not parts:
+            continue
+        if parts[0] == "format" and parts[1] != "ascii":
+            raise ValueError(f"{path}: only ascii PLY is supported")
+        if parts[0] == "element":
+            element = parts[1]
+            if element == "vertex":
+                nvert = int(parts[2])
+            elif element == "face":
+                nface = int(parts[2])
+        elif parts[0] == "property" and element == "vertex":
+            if parts[1] == "list":
+                raise ValueError(f"{path}: list vertex properties unsupported")
+            props.append(parts[2])
+        elif parts[0] == "end_header":
+            break
+    for name in ("x", "y", "z"):
+        if name not in props:
+            raise ValueError(f"{path}: vertex property {name} missing")
+    body = lines[i:]
+    if len(body) < nvert + nface:
+        raise ValueError(f"{path}: truncated body")
+    vd = np.array([[float(t) for t in body[k].split()] for k in range(nvert)],
+                  dtype=np.float64).reshape(nvert, len(props))
+    col = {name: vd[:, k] for k, name in enumerate(props)}
+    faces = np.zeros((nface, 3), dtype=np.int32)
+    for k in range(nface):
+        parts = body[nvert + k].split()
+        if int(parts[0]) != 3:
+            raise ValueError(f"{path}: only triangle faces are supported")
+        faces[k] = [int(parts[1]), int(parts[2]), int(parts[3])]
+    return TriMesh(np.column_stack([col["x"], col["y"], col["z"]]), faces,
+                   col.get("quality"))

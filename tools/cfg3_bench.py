@@ -23,6 +23,8 @@ ap.add_argument("--precision", default="fp32")
 ap.add_argument("--views", type=int, default=64)
 ap.add_argument("--depth", type=int, default=9)
 ap.add_argument("--solver", choices=("descent", "pd"), default="descent")
+ap.add_argument("--mesh", action="store_true",
+                help="also time densify + marching cubes of the result")
 ap.add_argument("--save-scene", default=None, help="pickle the rendered scene")
 ap.add_argument("--load-scene", default=None, help="reuse a pickled scene")
 args = ap.parse_args()
@@ -70,6 +72,19 @@ for t in range(args.passes):
                    "restructure_ms": pr["restructure_ms"]})
 prof = s.ctx.profile(False)
 res = s.result()
+mesh_info = None
+if args.mesh:
+    from paper_1608_07411_b200 import mesh, octree
+    torch.cuda.synchronize()
+    m0 = time.time()
+    dense = octree.densify_device(res.field)
+    torch.cuda.synchronize()
+    m1 = time.time()
+    tm = mesh.marching_cubes(dense, seen, dom)
+    torch.cuda.synchronize()
+    m2 = time.time()
+    mesh_info = {"densify_s": m1 - m0, "marching_cubes_s": m2 - m1,
+                 "vertices": tm.vertex_count, "faces": tm.face_count}
 h = res.field.to_host()
 leaves_end = int((h.child[:h.used] < 0).sum())
 steady = passes[3:] if len(passes) > 6 else passes
@@ -86,5 +101,5 @@ out = {"workload": "cfg3 adaptive object (BASELINE config 2)",
        "leaf_updates_per_s": lv[-1] / (ms / 1e3),
        "leaf_kernel_ms_per_pass": prof["leaf_ms"] / max(prof["leaf_launches"], 1),
        "profile": prof,
-       "passes": passes}
+       "mesh": mesh_info, "passes": passes}
 print(json.dumps(out))

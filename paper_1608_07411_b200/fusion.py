@@ -38,6 +38,9 @@ __all__ = [
     "view_arrays",
     "initial_field",
     "prepare",
+    "FrameComm",
+    "TorchFrameComm",
+    "frame_split",
     "fuse",
     "Solver",
     "tree_energy",
@@ -144,24 +147,160 @@ def initial_field(wf_sum, w_sum, gamma: float):
     return to_numpy(out) if host else out
 
 
-def prepare(depths, cameras, dom, params: FusionParams):
+def prepare(depths, cameras, dom, params: FusionParams, *, comm=None):
     """Depth maps -> (view trees, u0, seen): the pre-processing loop of the
     reference's ``cli.cmd_fuse`` (cli.py:141-171) on the GPU -- per view the
     TSDF with the wf/w sums accumulated in frame order, the view tree, then
     ``initial_field`` and ``build_octree(u0_grid, tau)``.  ``seen`` is the
-    (N,N,N) bool grid w_sum > 0 the reference hands to its mesher."""
+    (N,N,N) bool grid w_sum > 0 the reference hands to its mesher.
+
+    With ``comm`` (a :class:`FrameComm`, e.g. ``TorchFrameComm()`` over
+    torch.distributed) the frames are split across ranks (north_star: "the
+    per-frame TSDF integration is split across GPUs by frame"): rank r
+    builds the TSDFs and view trees of a contiguous block of frames, the
+    wf/w sums are accumulated in frame order along the ranks (each rank adds
+    its frames to the partial sums of the ranks before it, so the result is
+    the single-GPU sum bit for bit), and the view trees and final sums are
+    broadcast -- every rank returns the same views, u0 and seen."""
     from .tsdf import build_view_tsdf
     n = dom.resolution
-    wf = torch.zeros((n, n, n), dtype=torch.float64, device=device())
-    ws = torch.zeros_like(wf)
-    trees = []
-    for img, cam in zip(depths, cameras):
-        vt = build_view_tsdf(img, cam, dom, params.delta, params.eta,
-                             accumulate=(wf, ws))
-        trees.append(build_view_tree(vt, params.tau))
-        del vt
+    if comm is None or comm.world == 1:
+        wf = torch.zeros((n, n, n), dtype=torch.float64, device=device())
+        ws = torch.zeros_like(wf)
+        trees = []
+        for img, cam in zip(depths, cameras):
+            vt = build_view_tsdf(img, cam, dom, params.delta, params.eta,
+                                 accumulate=(wf, ws))
+            trees.append(build_view_tree(vt, params.tau))
+            del vt
+        u0 = build_octree(initial_field(wf, ws, params.gamma), tau=params.tau)
+        return trees, u0, ws > 0
+
+    def build(k):
+        vt = build_view_tsdf(depths[k], cameras[k], dom, params.delta,
+                             params.eta)
+        return vt.f, vt.w, build_view_tree(vt, params.tau)
+
+    def grid():
+        return torch.zeros((n, n, n), dtype=torch.float64, device=device())
+
+    def accumulate(wf, ws, f, w):
+        # k_view_tsdf's accumulation, same IEEE operations:
+        # wf += f64(f) * f64(w), ws += f64(w)
+        wf.add_(f.double() * w.double())
+        ws.add_(w.double())
+
+    trees, wf, ws = frame_split(len(depths), build, grid, accumulate,
+                                _tree_pack, _tree_unpack(device()), comm)
     u0 = build_octree(initial_field(wf, ws, params.gamma), tau=params.tau)
     return trees, u0, ws > 0
+
+
+class FrameComm:
+    """The point-to-point and broadcast operations ``frame_split`` needs
+    (rank, world, send, recv, broadcast); see ``TorchFrameComm``."""
+    rank = 0
+    world = 1
+
+    def send(self, t, dst):
+        raise NotImplementedError
+
+    def recv(self, t, src):
+        raise NotImplementedError
+
+    def broadcast(self, t, src):
+        raise NotImplementedError
+
+
+class TorchFrameComm(FrameComm):
+    """torch.distributed (NCCL on GPUs, gloo on CPU tensors)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def _g(self, r):   # group rank -> global rank
+        return r if self.group is None else \
+            self.dist.get_global_rank(self.group, r)
+
+    def send(self, t, dst):
+        self.dist.send(t, self._g(dst), group=self.group)
+
+    def recv(self, t, src):
+        self.dist.recv(t, self._g(src), group=self.group)
+
+    def broadcast(self, t, src):
+        self.dist.broadcast(t, self._g(src), group=self.group)
+
+
+def frame_blocks(nframes: int, world: int):
+    """Contiguous frame ranges [lo, hi) per rank, sizes within one."""
+    return [(r * nframes // world, (r + 1) * nframes // world)
+            for r in range(world)]
+
+
+def frame_split(nframes, build, grid, accumulate, pack, unpack, comm):
+    """The frame-split protocol, backend-agnostic (tests drive it with the
+    CPU oracle over gloo).  build(k) -> (f, w, tree) for an owned frame;
+    grid() -> zero accumulator; accumulate(wf, ws, f, w) adds one frame;
+    pack(tree) -> (int64 meta tensor[8], [arrays]); unpack(meta) -> (empty
+    arrays to receive into, finish(arrays) -> tree).  Returns (trees in
+    frame order, wf, ws), identical on every rank."""
+    r, world = comm.rank, comm.world
+    lo, hi = frame_blocks(nframes, world)[r]
+    own = [build(k) for k in range(lo, hi)]        # in parallel on all ranks
+    wf, ws = grid(), grid()
+    if r > 0:                                      # frames before ours
+        comm.recv(wf, r - 1)
+        comm.recv(ws, r - 1)
+    for f, w, _ in own:                            # ours, in frame order
+        accumulate(wf, ws, f, w)
+    if r < world - 1:
+        comm.send(wf, r + 1)
+        comm.send(ws, r + 1)
+    comm.broadcast(wf, world - 1)                  # the complete sums
+    comm.broadcast(ws, world - 1)
+    trees = []
+    owner = [q for q, (a, b) in enumerate(frame_blocks(nframes, world))
+             for _ in range(a, b)]
+    for k in range(nframes):
+        o = owner[k]
+        if o == r:
+            meta, arrays = pack(own[k - lo][2])
+            comm.broadcast(meta, o)
+            for a in arrays:
+                comm.broadcast(a, o)
+            trees.append(own[k - lo][2])
+        else:
+            meta = torch.zeros(8, dtype=torch.int64, device=wf.device)
+            comm.broadcast(meta, o)
+            arrays, finish = unpack(meta)
+            for a in arrays:
+                comm.broadcast(a, o)
+            trees.append(finish(arrays))
+    return trees, wf, ws
+
+
+def _tree_pack(t: OctreeField):
+    meta = torch.tensor([t.capacity, int(t.state[0]), int(t.state[1]),
+                         int(t.state[2]), t.d_max, 0, 0, 0],
+                        dtype=torch.int64, device=t.value.device)
+    return meta, [t.value, t.weight, t.child]
+
+
+def _tree_unpack(dev):
+    def unpack(meta):
+        cap, s0, s1, s2, d = (int(x) for x in meta[:5].tolist())
+        arrays = [pool_empty(cap, torch.float32), pool_empty(cap, torch.float32),
+                  pool_empty(cap, torch.int32)]
+
+        def finish(a):
+            return OctreeField(a[0], a[2], np.array([s0, s1, s2], np.int64), d,
+                               weight=a[1])
+        return arrays, finish
+    return unpack
 
 
 # -- octree solver ------------------------------------------------------------

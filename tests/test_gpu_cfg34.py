@@ -134,3 +134,73 @@ def test_cfg3_reduced_pd_with_restructure():
     got = [t[:used].cpu().numpy() for t in s.state]
     for g, w in zip(got, (u, ub, px, py, pz)):
         assert np.array_equal(g[live], w[:used][live])
+
+
+class _ThreadComm:
+    """In-process stand-in for torch.distributed between Python threads (one
+    GPU, one process): mailboxes for send/recv, a shared slot + barrier for
+    broadcast.  No kernel waits on another rank's kernel."""
+
+    def __init__(self, rank, world, box):
+        self.rank, self.world, self.box = rank, world, box
+
+    def send(self, t, dst):
+        self.box["q"][(self.rank, dst)].put(t.clone())
+
+    def recv(self, t, src):
+        t.copy_(self.box["q"][(src, self.rank)].get(timeout=120))
+
+    def broadcast(self, t, src):
+        b = self.box["bar"]
+        if self.rank == src:
+            self.box["slot"] = t.clone()
+        b.wait()
+        if self.rank != src:
+            t.copy_(self.box["slot"])
+        b.wait()
+
+
+def test_frame_split_prepare_equals_single_gpu():
+    """fusion.prepare with the frames split over 3 ranks (threads on one GPU,
+    in-process mailboxes): views, u0 and seen equal the single-GPU prepare
+    bit for bit on every rank."""
+    import queue
+    import threading
+    from paper_1608_07411_b200 import fusion, scenes, volume
+    sc = scenes.make_cfg3(d_max=6, n_views=7, width=160, height=120,
+                          focal=131.25, device="cuda")
+    p = fusion.FusionParams(**dict(sc.params, iterations=1))
+    dom = volume.VolumeDomain(sc.origin, sc.voxel_size, sc.resolution)
+    ref_views, ref_u0, ref_seen = fusion.prepare(sc.depths, sc.cameras, dom, p)
+    world = 3
+    box = {"q": {(a, b): queue.Queue() for a in range(world)
+                 for b in range(world)},
+           "bar": threading.Barrier(world), "slot": None}
+    out, errs = [None] * world, []
+
+    def run(r):
+        try:
+            torch.cuda.set_device(0)
+            out[r] = fusion.prepare(sc.depths, sc.cameras, dom, p,
+                                    comm=_ThreadComm(r, world, box))
+            torch.cuda.synchronize()
+        except Exception as exc:          # pragma: no cover - reported below
+            errs.append(exc)
+            box["bar"].abort()
+    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errs, errs
+    hu = ref_u0.to_host()
+    for views, u0, seen in out:
+        assert torch.equal(seen, ref_seen)
+        g = u0.to_host()
+        assert np.array_equal(g.child[:g.used], hu.child[:hu.used])
+        assert np.array_equal(g.value[:g.used], hu.value[:hu.used])
+        for a, b in zip(views, ref_views):
+            ah, bh = a.to_host(), b.to_host()
+            assert np.array_equal(ah.child, bh.child)
+            assert np.array_equal(ah.value, bh.value)
+            assert np.array_equal(ah.weight, bh.weight)

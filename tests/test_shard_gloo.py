@@ -236,3 +236,94 @@ def _start_complete_worker(rank, world, port, q):
         q.put((rank, bool(ok)))
     finally:
         dist.destroy_process_group()
+
+
+# ---------------------------------------------------- frame-split TSDF ----
+
+def _oracle_backend(depths, cams, origin, vox, n, p):
+    def build(k):
+        f, w = orc.build_view_tsdf(depths[k], cams[k], origin, vox, n, p.delta,
+                                   p.eta)
+        return (torch.from_numpy(f), torch.from_numpy(w),
+                orc.build_octree(f, w, tau=p.tau, dtype=np.float32))
+
+    def grid():
+        return torch.zeros((n, n, n), dtype=torch.float64)
+
+    def accumulate(wf, ws, f, w):
+        wf.add_(f.double() * w.double())
+        ws.add_(w.double())
+
+    def pack(t):
+        meta = torch.tensor([t.value.shape[0], *[int(s) for s in t.state],
+                             t.d_max, 0, 0, 0], dtype=torch.int64)
+        return meta, [torch.from_numpy(np.ascontiguousarray(t.value)),
+                      torch.from_numpy(np.ascontiguousarray(t.weight)),
+                      torch.from_numpy(np.ascontiguousarray(t.child))]
+
+    def unpack(meta):
+        cap, s0, s1, s2, d = (int(x) for x in meta[:5].tolist())
+        arrays = [torch.zeros(cap, dtype=torch.float32),
+                  torch.zeros(cap, dtype=torch.float32),
+                  torch.zeros(cap, dtype=torch.int32)]
+
+        def finish(a):
+            return orc.Pool(a[0].numpy(), a[2].numpy(),
+                            np.array([s0, s1, s2], np.int64), d,
+                            weight=a[1].numpy())
+        return arrays, finish
+    return build, grid, accumulate, pack, unpack
+
+
+def _frame_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1608_07411_b200 import fusion
+        from tests.goldens import cfg1_inputs
+        depths, cams, origin, vox, n, p = cfg1_inputs()
+        be = _oracle_backend(depths, cams, origin, vox, n, p)
+        trees, wf, ws = fusion.frame_split(len(depths), *be,
+                                           fusion.TorchFrameComm())
+        q.put((rank, wf.numpy(), ws.numpy(),
+               [(t.value.copy(), t.weight.copy(), t.child.copy(),
+                 t.state.copy()) for t in trees]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_frame_split_tsdf_matches_single_process(world):
+    """Frames split in contiguous blocks across gloo ranks: the wf/w sums
+    (accumulated in frame order along the ranks) and every view tree equal
+    the single-process frame-order result bit for bit, on every rank."""
+    from tests.goldens import cfg1_inputs
+    depths, cams, origin, vox, n, p = cfg1_inputs()
+    wf0 = np.zeros((n, n, n))
+    ws0 = np.zeros((n, n, n))
+    ref = []
+    for d, c in zip(depths, cams):
+        f, w = orc.build_view_tsdf(d, c, origin, vox, n, p.delta, p.eta)
+        wf0 += f.astype(np.float64) * w
+        ws0 += w
+        ref.append(orc.build_octree(f, w, tau=p.tau, dtype=np.float32))
+    port = free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_frame_worker, args=(r, world, port, q))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    out = [q.get(timeout=300) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+    for rank, wf, ws, trees in out:
+        assert np.array_equal(wf, wf0) and np.array_equal(ws, ws0), rank
+        assert len(trees) == len(ref)
+        for (v, w, c, st), t in zip(trees, ref):
+            used = int(t.state[0])
+            assert np.array_equal(c[:used], t.child[:used])
+            assert np.array_equal(v[:used], t.value[:used])
+            assert np.array_equal(w[:used], t.weight[:used])
+            assert list(st) == list(t.state)

@@ -31,6 +31,9 @@
 #ifndef OCTF_LEAF_WARPSTAGE
 #define OCTF_LEAF_WARPSTAGE 0
 #endif
+#ifndef OCTF_LEAF_NBRREG
+#define OCTF_LEAF_NBRREG 1
+#endif
 #ifndef OCTF_LEAF_WARPPART
 #define OCTF_LEAF_WARPPART 0
 #endif
@@ -294,6 +297,35 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
   const T o_xy = __shfl_xor_sync(FULL, S0, 6);
   const T o_xz = __shfl_xor_sync(FULL, S0, 5);
   const T o_yz = __shfl_xor_sync(FULL, S0, 3);
+#if OCTF_LEAF_NBRREG
+  // the block's 12 table entries as three 16 B loads, indices by selects
+  // (the primal-dual kernel's form)
+  int32_t NB[12];
+  {
+    const int4* nb4 = reinterpret_cast<const int4*>(nb);
+    const int4 n0 = active ? __ldg(nb4) : make_int4(-1, -1, -1, -1);
+    const int4 n1 = active ? __ldg(nb4 + 1) : make_int4(-1, -1, -1, -1);
+    const int4 n2 = active ? __ldg(nb4 + 2) : make_int4(-1, -1, -1, -1);
+    NB[0] = n0.x; NB[1] = n0.y; NB[2] = n0.z; NB[3] = n0.w;
+    NB[4] = n1.x; NB[5] = n1.y; NB[6] = n1.z; NB[7] = n1.w;
+    NB[8] = n2.x; NB[9] = n2.y; NB[10] = n2.z; NB[11] = n2.w;
+  }
+#define SV(DX, DY, DZ, OWN, PRED) \
+  pick(OWN, step_idx_r<DX, DY, DZ>(c, cx, cy, cz, active && (PRED), NB), snap)
+  const T Sx = SV(1, 0, 0, o_x, xp);
+  const T Sy = SV(0, 1, 0, o_y, yp);
+  const T Sz = SV(0, 0, 1, o_z, zp);
+  const T Smx = SV(-1, 0, 0, o_x, xm);
+  const T Smxy = SV(-1, 1, 0, o_xy, xm && yp);
+  const T Smxz = SV(-1, 0, 1, o_xz, xm && zp);
+  const T Smy = SV(0, -1, 0, o_y, ym);
+  const T Smyx = SV(1, -1, 0, o_xy, ym && xp);
+  const T Smyz = SV(0, -1, 1, o_yz, ym && zp);
+  const T Smz = SV(0, 0, -1, o_z, zm);
+  const T Smzx = SV(1, 0, -1, o_xz, zm && xp);
+  const T Smzy = SV(0, 1, -1, o_yz, zm && yp);
+#undef SV
+#else
   // forward neighbours
   const T Sx = step_val<1, 0, 0>(o_x, c, cx, cy, cz, active && xp, nb, snap);
   const T Sy = step_val<0, 1, 0>(o_y, c, cx, cy, cz, active && yp, nb, snap);
@@ -308,6 +340,8 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
   const T Smz = step_val<0, 0, -1>(o_z, c, cx, cy, cz, active && zm, nb, snap);
   const T Smzx = step_val<1, 0, -1>(o_xz, c, cx, cy, cz, active && zm && xp, nb, snap);
   const T Smzy = step_val<0, 1, -1>(o_yz, c, cx, cy, cz, active && zm && yp, nb, snap);
+
+#endif
 
   // flux at the cell (_kernels.pyx:205-220)
   const T gx = xp ? (Sx - S0) * ih : (T)0;

@@ -1,6 +1,8 @@
 """BASELINE config 2 (cfg3, adaptive single object) at full size on one GPU:
 64 sphere-traced 640x480 depth maps of the noisy blob, d_max 9 (512^3),
-split/join after every pass.  Times the input stage (TSDF + view trees + u0)
+split/join after every pass.  ``--config cfg4`` runs BASELINE config 3 (the
+room, 300 frames) at ``--depth`` (default 9; the full depth 11 needs a
+sparse build).  Times the input stage (TSDF + view trees + u0)
 and K solver passes (iterate + restructure + propagate + energy, host sync
 per pass as the reference's loop), reporting leaf-updates/s = pre-pass leaves
 / pass time and the leaf kernel's share.
@@ -20,8 +22,9 @@ from paper_1608_07411_b200 import fusion, scenes, volume  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--passes", type=int, default=20)
 ap.add_argument("--precision", default="fp32")
-ap.add_argument("--views", type=int, default=64)
+ap.add_argument("--views", type=int, default=None)
 ap.add_argument("--depth", type=int, default=9)
+ap.add_argument("--config", choices=("cfg3", "cfg4"), default="cfg3")
 ap.add_argument("--solver", choices=("descent", "pd"), default="descent")
 ap.add_argument("--mesh", action="store_true",
                 help="also time densify + marching cubes of the result")
@@ -34,8 +37,12 @@ if args.load_scene:
     import pickle
     with open(args.load_scene, "rb") as fp:
         sc = pickle.load(fp)
+elif args.config == "cfg4":
+    sc = scenes.make_cfg4(d_max=args.depth, n_frames=args.views or 300,
+                          device="cuda")
 else:
-    sc = scenes.make_cfg3(d_max=args.depth, n_views=args.views, device="cuda")
+    sc = scenes.make_cfg3(d_max=args.depth, n_views=args.views or 64,
+                          device="cuda")
 if args.save_scene:
     import pickle
     with open(args.save_scene, "wb") as fp:
@@ -92,8 +99,11 @@ ms = sorted(q["ms"] for q in steady)[len(steady) // 2]
 # leaves before each pass ~ nodes*7/8 (complete-children tree: leaves =
 # 7*inner + 1 = (7*nodes + 1)/8)
 lv = [(7 * q["nodes"] + 1) // 8 for q in passes]
-out = {"workload": "cfg3 adaptive object (BASELINE config 2)",
-       "depth": args.depth, "views": args.views, "precision": args.precision,
+out = {"workload": ("cfg3 adaptive object (BASELINE config 2)"
+                    if args.config == "cfg3" else
+                    "cfg4 room (BASELINE config 3) at reduced depth"),
+       "depth": args.depth, "views": len(sc.depths),
+       "precision": args.precision,
        "solver": args.solver,
        "render_s": t_render, "prepare_s": t_prep,
        "u0_nodes": u0.node_count, "leaves_end": leaves_end,

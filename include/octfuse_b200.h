@@ -63,9 +63,19 @@ int octf_selftest(void);
 int octf_ctx_create(octf_ctx **out);
 int octf_ctx_destroy(octf_ctx *ctx);
 int octf_ctx_invalidate(octf_ctx *ctx);
-/* out[0..8] = leaf blocks, leaves, live blocks, free blocks, mask-format
- * samples (0/1), sample stride, views, valid, leaf tiles (int64[9]) */
+/* out[0..9] = leaf blocks, leaves, live blocks, free blocks, mask-format
+ * samples (0/1), sample stride, views, valid, leaf tiles, ELL layout (0/1)
+ * (int64[10]) */
 int octf_ctx_info(octf_ctx *ctx, int64_t *out);
+
+/* Context options.  OCTF_CTX_DENSE: keep the dense [leaf][view] sample
+ * layout even above 32 views (solver="pd" needs it); by default more than
+ * 32 views use the ELL layout -- per 256-leaf tile only as many rows as its
+ * most-observed leaf has observed views, each leaf's observed samples in
+ * view order (the zero-weight views the reference skips,
+ * _kernels.pyx:244-252, are not stored). */
+#define OCTF_CTX_DENSE 1
+int octf_ctx_set_options(octf_ctx *ctx, int flags);
 
 /* Live profiling: enable != 0 brackets the leaf-update and energy kernels
  * with CUDA events on their launch stream.  out[0..4] (optional) receives

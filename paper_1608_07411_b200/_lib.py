@@ -36,6 +36,7 @@ _SIGS = {
     "octf_ctx_invalidate": ([P], I32),
     "octf_ctx_info": ([P, P], I32),
     "octf_ctx_profile": ([P, I32, P], I32),
+    "octf_ctx_set_options": ([P, I32], I32),
     "octf_ctx_phases": ([P, P], I32),
     "octf_iterate_pass": ([P, I32, P, P, P, P, P, I64, I32, P, P, P, I32, DBL,
                            DBL, DBL, DBL, DBL, DBL, I32, I32, I32, P, I64, P,
@@ -129,11 +130,15 @@ class Ctx:
 
     def info(self) -> dict:
         import numpy as np
-        out = np.zeros(9, dtype=np.int64)
+        out = np.zeros(10, dtype=np.int64)
         call("octf_ctx_info", self.h, out.ctypes.data)
         keys = ("leaf_blocks", "leaves", "blocks", "free_blocks", "mask_samples",
-                "sample_stride", "views", "valid", "tiles")
+                "sample_stride", "views", "valid", "tiles", "ell")
         return dict(zip(keys, (int(v) for v in out)))
+
+    def set_dense(self, dense: bool = True) -> None:
+        """Keep the dense sample layout above 32 views (solver='pd')."""
+        call("octf_ctx_set_options", self.h, 1 if dense else 0)
 
     def profile(self, enable: bool = True) -> dict:
         """Read and reset the live kernel timers; (re)arm them if enable."""

@@ -148,6 +148,18 @@ int octf_ctx_invalidate(octf_ctx* ctx) {
   return OCTF_OK;
 }
 
+int octf_ctx_set_options(octf_ctx* ctx, int flags) {
+  return guard([&] {
+    if (!ctx) throw octf::Error(octf::kEArg, "null context");
+    const bool dense = (flags & OCTF_CTX_DENSE) != 0;
+    if (dense != ctx->c.dense_only) {
+      ctx->c.dense_only = dense;
+      ctx->c.store_ok = false;
+      ctx->c.valid = false;  // regather in the requested layout
+    }
+  });
+}
+
 int octf_ctx_info(octf_ctx* ctx, int64_t* out) {
   return guard([&] {
     if (!ctx || !out) throw octf::Error(octf::kEArg, "null argument");
@@ -161,6 +173,7 @@ int octf_ctx_info(octf_ctx* ctx, int64_t* out) {
     out[6] = c.nviews;
     out[7] = c.valid;
     out[8] = (c.nlb * 8 + 255) / 256;  // leaf tiles (one CTA each)
+    out[9] = c.ell ? 1 : 0;
   });
 }
 

@@ -427,6 +427,183 @@ __global__ void k_gather_fresh(const int32_t* __restrict__ fresh,
   }
 }
 
+// ---- ELL incremental update (stable list): k_ell_update classifies the
+// slots like k_sample_update; fresh leaves gather with one warp each
+__global__ void k_ell_update(const int32_t* __restrict__ lblocks,
+                             const int4* __restrict__ lmeta, int64_t n,
+                             int64_t nold, const uint8_t* __restrict__ oldmask,
+                             const int32_t* __restrict__ tileK,
+                             const int64_t* __restrict__ tileOff, float* F,
+                             float* W, int32_t* fresh, int32_t* nfresh,
+                             int32_t* nleaves) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = gid >> 3;
+  const int c = (int)(gid & 7);
+  const bool in = i < n;
+  const int32_t b = in ? lblocks[i] : -1;
+  unsigned nm = 0;
+  if (b >= 0) {
+    int pz, L;
+    unpack_meta_w(lmeta[i].w, pz, nm, L);
+  }
+  {
+    int cnt = (c == 0) ? __popc(nm) : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(nleaves, cnt);
+  }
+  if (!in) return;
+  const bool now = b >= 0 && !(b == 0 && c != 0) && ((nm >> c) & 1u);
+  const bool was = i < nold && ((oldmask[i] >> c) & 1u);
+  if (now && !was) {
+    fresh[atomicAdd(nfresh, 1)] = (int32_t)gid;
+  } else if (!now && (was || i >= nold)) {
+    const int K = tileK[gid >> 8];
+    for (int r = 0; r < K; ++r) {
+      F[ell_idx(tileOff, gid, r)] = 0.f;
+      W[ell_idx(tileOff, gid, r)] = 0.f;
+    }
+  }
+}
+
+// one warp per queued leaf: views over lanes, observed ones compacted in
+// view order by ballot; more than the tile's rows flags an overflow
+__global__ void k_ell_fresh(const int32_t* __restrict__ fresh,
+                            const int32_t* __restrict__ nfresh,
+                            const int4* __restrict__ lmeta, ViewSet vs,
+                            const int32_t* __restrict__ tileK,
+                            const int64_t* __restrict__ tileOff, float* F,
+                            float* W, int32_t* overflow) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (int)(gridDim.x * (blockDim.x >> 5));
+  const int n = *nfresh;
+  for (int k = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
+       k < n; k += nw) {
+    const int64_t s = fresh[k];
+    const int4 m = lmeta[s >> 3];
+    const int c = (int)(s & 7);
+    const int32_t b = m.x;
+    int L, pz;
+    unsigned mask;
+    unpack_meta_w(m.w, pz, mask, L);
+    const int x = b == 0 ? 0 : 2 * m.y + ((c >> 2) & 1);
+    const int y = b == 0 ? 0 : 2 * m.z + ((c >> 1) & 1);
+    const int z = b == 0 ? 0 : 2 * pz + (c & 1);
+    const int K = tileK[s >> 8];
+    int j = 0;
+    for (int v0 = 0; v0 < vs.n; v0 += 32) {
+      const int v = v0 + lane;
+      float f = 0.f, w = 0.f;
+      if (v < vs.n) {
+        const int32_t nd = descend(vs.child[v], L, x, y, z);
+        f = vs.val[v][nd];
+        w = vs.w[v][nd];
+      }
+      const unsigned on = __ballot_sync(0xffffffffu, w != 0.f);
+      const int r = j + __popc(on & ((1u << lane) - 1u));
+      if (w != 0.f && r < K) {
+        F[ell_idx(tileOff, s, r)] = f;
+        W[ell_idx(tileOff, s, r)] = w;
+      }
+      j += __popc(on);
+    }
+    for (int r = j + lane; r < K; r += 32) {
+      F[ell_idx(tileOff, s, r)] = 0.f;
+      W[ell_idx(tileOff, s, r)] = 0.f;
+    }
+    if (lane == 0 && j > K) atomicExch(overflow, 1);
+  }
+}
+
+// ---- ELL sample store (views > 32) ----
+// observed views of every active leaf slot of the list
+__global__ void k_ell_count(const int32_t* __restrict__ ucs,
+                            const int32_t* __restrict__ lblocks, int64_t nlb,
+                            const uint64_t* __restrict__ lkey, ViewSet vs,
+                            int32_t* cnt, int64_t slot0, int64_t slot1) {
+  const int64_t gid = slot0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = gid >> 3;
+  const int c = (int)(gid & 7);
+  if (gid >= slot1 || i >= nlb) return;
+  int32_t b = lblocks[i];
+  const bool active = b >= 0 && !(b == 0 && c != 0) && ucs[b + c] < 0;
+  int k = 0;
+  if (active) {
+    int L, px, py, pz;
+    unpack_cell(lkey[i], L, px, py, pz);
+    const int x = b == 0 ? 0 : 2 * px + ((c >> 2) & 1);
+    const int y = b == 0 ? 0 : 2 * py + ((c >> 1) & 1);
+    const int z = b == 0 ? 0 : 2 * pz + (c & 1);
+    for (int v = 0; v < vs.n; ++v)
+      k += vs.w[v][descend(vs.child[v], L, x, y, z)] != 0.f;
+  }
+  cnt[gid] = k;
+}
+
+// per tile: rows = max count of its 256 slots (one CTA of 256 per tile)
+__global__ void k_ell_tilemax(const int32_t* __restrict__ cnt, int64_t n,
+                              int64_t tile0, int32_t* tileK, int64_t* rowsz) {
+  const int64_t t = tile0 + blockIdx.x;
+  const int64_t s = t * 256 + threadIdx.x;
+  int k = s < n ? cnt[s] : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) k = max(k, __shfl_xor_sync(0xffffffffu, k, o));
+  __shared__ int wm[8];
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = k;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int mx = 0;
+    for (int q = 0; q < 8; ++q) mx = max(mx, wm[q]);
+    tileK[t] = mx;
+    rowsz[blockIdx.x] = (int64_t)mx * 256;
+  }
+}
+
+// observed samples of one leaf slot into its rows, the rest zeroed
+__device__ __forceinline__ void ell_write_slot(
+    int64_t s, int L, int x, int y, int z, bool leaf, ViewSet vs,
+    const int32_t* tileK, const int64_t* tileOff, float* F, float* W) {
+  const int K = tileK[s >> 8];
+  int j = 0;
+  if (leaf) {
+    for (int v = 0; v < vs.n; ++v) {
+      const int32_t nd = descend(vs.child[v], L, x, y, z);
+      const float w = vs.w[v][nd];
+      if (w != 0.f) {
+        if (j < K) {
+          F[ell_idx(tileOff, s, j)] = vs.val[v][nd];
+          W[ell_idx(tileOff, s, j)] = w;
+        }
+        ++j;
+      }
+    }
+  }
+  for (int r = j; r < K; ++r) {
+    F[ell_idx(tileOff, s, r)] = 0.f;
+    W[ell_idx(tileOff, s, r)] = 0.f;
+  }
+}
+
+__global__ void k_ell_fill(const int32_t* __restrict__ ucs,
+                           const int32_t* __restrict__ lblocks, int64_t nlb,
+                           const uint64_t* __restrict__ lkey, ViewSet vs,
+                           const int32_t* __restrict__ tileK,
+                           const int64_t* __restrict__ tileOff, int64_t slot0,
+                           int64_t slot1, float* F, float* W) {
+  const int64_t s = slot0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= slot1) return;
+  const int64_t i = s >> 3;
+  const int c = (int)(s & 7);
+  const int32_t b = i < nlb ? lblocks[i] : -1;
+  const bool leaf = b >= 0 && !(b == 0 && c != 0) && ucs[b + c] < 0;
+  int L = 0, px = 0, py = 0, pz = 0;
+  if (leaf) unpack_cell(lkey[i], L, px, py, pz);
+  const int x = b <= 0 ? 0 : 2 * px + ((c >> 2) & 1);
+  const int y = b <= 0 ? 0 : 2 * py + ((c >> 1) & 1);
+  const int z = b <= 0 ? 0 : 2 * pz + (c & 1);
+  ell_write_slot(s, L, x, y, z, leaf, vs, tileK, tileOff, F, W);
+}
+
 __global__ void k_masks(const float* __restrict__ W, int64_t stride, int nv,
                         int64_t n, uint32_t* M) {
   int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -650,6 +827,86 @@ void ctx_list_full(Ctx& c, const int32_t* child, int64_t total, int64_t nbid,
   c.list_full = true;
 }
 
+// ELL store after a list patch: tiles appended by the patch get counts,
+// rows and offsets after the existing store; kept leaves keep their rows,
+// new leaves gather (a warp each); a leaf with more observed views than
+// its tile's rows -> false (full rebuild).
+static bool ell_list_samples(Ctx& c, int64_t nold, int64_t nnew,
+                             const uint8_t* oldmask,
+                             std::chrono::steady_clock::time_point t0,
+                             cudaStream_t st) {
+  const int64_t nt_old = c.ell_tiles;
+  const int64_t nt_new = (nnew * 8 + kTileLeaves - 1) / kTileLeaves;
+  int64_t total = c.ell_size;
+  if (nt_new > nt_old) {
+    int32_t* cnt = c.sort_k32.ensure(nt_new * 256 + 1);
+    OCTF_CUDA(cudaMemsetAsync(cnt, 0, nt_new * 256 * sizeof(int32_t), st));
+    // counts for the new tiles' slots (the list tables are current)
+    const int64_t s0 = nt_old * 256, s1 = nnew * 8;
+    if (s1 > s0)
+      k_ell_count<<<grid_for(s1 - s0), kThreads, 0, st>>>(
+          c.child_key, c.lblocks.p, nnew, c.lkey.p, ctx_views(c), cnt, s0, s1);
+    int64_t* rowsz =
+        reinterpret_cast<int64_t*>(c.sort_k64.ensure(nt_new - nt_old + 1));
+    c.tileK.grow_keep(nt_new + 1, nt_old, st);
+    c.tileOff.grow_keep(nt_new + 1, nt_old + 1, st);
+    k_ell_tilemax<<<(unsigned)(nt_new - nt_old), 256, 0, st>>>(
+        cnt, nnew * 8, nt_old, c.tileK.p, rowsz);
+    OCTF_CUDA(cudaMemsetAsync(rowsz + (nt_new - nt_old), 0, sizeof(int64_t),
+                              st));
+    int64_t* scan = reinterpret_cast<int64_t*>(c.app_buf.ensure(
+        2 * (nt_new - nt_old + 1)));
+    size_t bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, rowsz, scan,
+                                  (int)(nt_new - nt_old + 1), st);
+    c.cub_tmp.ensure(bytes);
+    OCTF_CUDA(cub::DeviceScan::ExclusiveSum(c.cub_tmp.p, bytes, rowsz, scan,
+                                            (int)(nt_new - nt_old + 1), st));
+    int64_t add = 0;
+    OCTF_CUDA(cudaMemcpyAsync(&add, scan + (nt_new - nt_old), sizeof(int64_t),
+                              cudaMemcpyDeviceToHost, st));
+    OCTF_CUDA(cudaStreamSynchronize(st));
+    // offsets of the new tiles continue after the existing store
+    std::vector<int64_t> h(nt_new - nt_old + 1);
+    OCTF_CUDA(cudaMemcpyAsync(h.data(), scan, h.size() * sizeof(int64_t),
+                              cudaMemcpyDeviceToHost, st));
+    OCTF_CUDA(cudaStreamSynchronize(st));
+    for (auto& v : h) v += total;
+    OCTF_CUDA(cudaMemcpyAsync(c.tileOff.p + nt_old, h.data(),
+                              h.size() * sizeof(int64_t),
+                              cudaMemcpyHostToDevice, st));
+    c.F.grow_keep((size_t)(total + add) + 1, (size_t)total, st);
+    c.W.grow_keep((size_t)(total + add) + 1, (size_t)total, st);
+    total += add;
+  }
+  int32_t* fresh = c.sort_v32.ensure(nnew * 8 + 1);
+  k_ell_update<<<grid_for(nnew * 8), kThreads, 0, st>>>(
+      c.lblocks.p, c.lmeta.p, nnew, nold, oldmask, c.tileK.p, c.tileOff.p,
+      c.F.p, c.W.p, fresh, c.counters.p + 2, c.counters.p + 4);
+  // (slots past the list's end are never leaves: their rows are not read)
+  k_ell_fresh<<<148 * 8, kThreads, 0, st>>>(fresh, c.counters.p + 2,
+                                             c.lmeta.p, ctx_views(c),
+                                             c.tileK.p, c.tileOff.p, c.F.p,
+                                             c.W.p, c.counters.p + 3);
+  OCTF_CUDA(cudaGetLastError());
+  OCTF_CUDA(cudaMemcpyAsync(c.h_counters, c.counters.p, 8 * sizeof(int32_t),
+                            cudaMemcpyDeviceToHost, st));
+  OCTF_CUDA(cudaStreamSynchronize(st));
+  if (c.h_counters[3]) return false;  // a leaf overflows its tile's rows
+  c.nlb = nnew;
+  c.nleaves = c.h_counters[4];
+  c.ell_tiles = nt_new;
+  c.ell_size = total;
+  c.store_ok = true;
+  if (c.timing) {
+    c.t_gather_ms += std::chrono::duration<double, std::milli>(
+                         std::chrono::steady_clock::now() - t0).count();
+    ++c.n_gather;
+    ++c.n_regather;
+  }
+  return true;
+}
+
 // patch the list after our own restructure (see Ctx::lpos): holes for
 // blocks without leaves, appended new leaf blocks, all tables recomputed,
 // samples kept where a leaf stayed at its position and gathered for new
@@ -697,6 +954,7 @@ bool ctx_list_update(Ctx& c, const int32_t* child, int64_t total, int64_t nbid,
       child, c.lblocks.p, nnew, c.blevel.p, c.bcoord.p, c.bparent.p, c.lkey.p,
       c.lmeta.p, c.lpar.p, c.nbr.p);
   OCTF_CUDA(cudaGetLastError());
+  if (c.ell) return ell_list_samples(c, nold, nnew, oldmask, t0, st);
   // samples, in place (the store only grows; its tail is zeroed)
   const int64_t nvp = c.sstride;
   auto pad = [](int64_t n) {
@@ -799,8 +1057,60 @@ ViewSet ctx_views(const Ctx& c) {
   return v;
 }
 
+void ctx_gather_ell(Ctx& c, cudaStream_t st) {
+  const int64_t n = c.nlb * 8;
+  const int64_t nt = (n + kTileLeaves - 1) / kTileLeaves;
+  // one pass over the tiles: counts -> rows -> offsets (from 0)
+  int32_t* cnt = c.sort_k32.ensure(nt * 256 + 1);
+  OCTF_CUDA(cudaMemsetAsync(cnt, 0, nt * 256 * sizeof(int32_t), st));
+  k_ell_count<<<grid_for(n), kThreads, 0, st>>>(
+      c.child_key, c.lblocks.p, c.nlb, c.lkey.p, ctx_views(c), cnt, 0, n);
+  int64_t* rowsz = reinterpret_cast<int64_t*>(c.sort_k64.ensure(nt + 1));
+  c.tileK.ensure(nt + 1);
+  c.tileOff.ensure(nt + 1);
+  if (nt)
+    k_ell_tilemax<<<(unsigned)nt, 256, 0, st>>>(cnt, n, 0, c.tileK.p, rowsz);
+  OCTF_CUDA(cudaMemsetAsync(rowsz + nt, 0, sizeof(int64_t), st));
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, rowsz, c.tileOff.p,
+                                (int)(nt + 1), st);
+  c.cub_tmp.ensure(bytes);
+  OCTF_CUDA(cub::DeviceScan::ExclusiveSum(c.cub_tmp.p, bytes, rowsz,
+                                          c.tileOff.p, (int)(nt + 1), st));
+  OCTF_CUDA(cudaGetLastError());
+  int64_t total = 0;
+  OCTF_CUDA(cudaMemcpyAsync(&total, c.tileOff.p + nt, sizeof(int64_t),
+                            cudaMemcpyDeviceToHost, st));
+  OCTF_CUDA(cudaStreamSynchronize(st));
+  c.F.ensure((size_t)total + 1);
+  c.W.ensure((size_t)total + 1);
+  if (nt)
+    k_ell_fill<<<grid_for(nt * 256), kThreads, 0, st>>>(
+        c.child_key, c.lblocks.p, c.nlb, c.lkey.p, ctx_views(c), c.tileK.p,
+        c.tileOff.p, 0, nt * 256, c.F.p, c.W.p);
+  OCTF_CUDA(cudaGetLastError());
+  c.M.release();
+  c.binw = false;
+  c.ell = true;
+  c.ell_tiles = nt;
+  c.ell_size = total;
+  c.sstride = 0;
+}
+
 void ctx_gather(Ctx& c, cudaStream_t st) {
   const auto t0 = std::chrono::steady_clock::now();
+  if (!c.ext_F && !c.dense_only && c.nviews > 32) {
+    ctx_gather_ell(c, st);
+    OCTF_CUDA(cudaStreamSynchronize(st));
+    c.store_ok = true;
+    if (c.timing) {
+      c.t_gather_ms += std::chrono::duration<double, std::milli>(
+                           std::chrono::steady_clock::now() - t0).count();
+      ++c.n_gather;
+    }
+    return;
+  }
+  c.ell = false;
   // tiles of 256 leaves, view-major inside a tile (octf_common.cuh
   // samp_idx); views padded to 4 and leaves to whole tiles
   int64_t n = c.nlb * 8;

@@ -80,6 +80,8 @@ struct LeafArgs {
   int32_t* counters;
   double* epart;  // per-CTA energy partial sums
   int tile0 = 0;  // first tile of this launch (sharded overlap: sub-ranges)
+  const int32_t* __restrict__ tileK = nullptr;    // ELL store (views > 32)
+  const int64_t* __restrict__ tileOff = nullptr;
 };
 
 // table direction of a step that leaves the block along the given axes
@@ -402,6 +404,12 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
         const float wv = sw[v * kTileLeaves + t];
         if (wv != 0.f) sample((T)wv, sf[v * kTileLeaves + t]);
       }
+    }
+  } else if (active && a.tileK) {  // ELL: the leaf's observed views, in order
+    const int K = __ldg(a.tileK + tile_id);
+    for (int r = 0; r < K; ++r) {
+      const float wv = __ldg(a.W + ell_idx(a.tileOff, gid, r));
+      if (wv != 0.f) sample((T)wv, __ldg(a.F + ell_idx(a.tileOff, gid, r)));
     }
   } else if (active) {
     uint32_t mk = BINW ? __ldg(a.M + gid) : 0u;

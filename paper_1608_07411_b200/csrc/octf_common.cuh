@@ -54,6 +54,14 @@ __host__ __device__ __forceinline__ void unpack_meta_w(int w, int& pz,
 // touches 128 contiguous bytes, and a whole tile is one contiguous
 // nvp*1 KiB block that a single TMA bulk copy stages into shared memory.
 constexpr int kTileLeaves = 256;
+// Sparse per-tile sample layout (ELL, many views): tile t = leaves
+// [256t, 256t+256) holds K_t rows of 256 entries from off[t]; row j of a leaf
+// is its j-th observed view in view order, rows past its count are zero.
+__host__ __device__ __forceinline__ int64_t ell_idx(const int64_t* off,
+                                                    int64_t leaf, int row) {
+  return off[leaf >> 8] + ((int64_t)row << 8) + (leaf & 255);
+}
+
 __host__ __device__ __forceinline__ int64_t samp_idx(int64_t leaf, int v,
                                                      int64_t nvp) {
   return (leaf >> 8) * (nvp << 8) + ((int64_t)v << 8) + (leaf & 255);

@@ -591,7 +591,9 @@ __global__ void __launch_bounds__(kT)
              const int4* __restrict__ lmeta, const T* __restrict__ u,
              const float* __restrict__ F, const float* __restrict__ W,
              const uint32_t* __restrict__ M, int64_t stride, int nv,
-             LeafParams<T> p, double* partials, double* terms) {
+             LeafParams<T> p, double* partials, double* terms,
+             const int32_t* __restrict__ tileK,
+             const int64_t* __restrict__ tileOff) {
   using A = Arith<T>;
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t i = gid >> 3;
@@ -628,10 +630,12 @@ __global__ void __launch_bounds__(kT)
     T num = 0, den = p.gamma;
     const int64_t sidx = i * 8 + c;
     const uint32_t mk = BINW ? M[sidx] : 0u;
-    for (int v = 0; v < nv; ++v) {
-      const float w = BINW ? (float)((mk >> v) & 1u) : W[samp_idx(sidx, v, stride)];
+    const int nrow = tileK ? tileK[sidx >> 8] : nv;
+    for (int v = 0; v < nrow; ++v) {
+      const int64_t q = tileK ? ell_idx(tileOff, sidx, v) : samp_idx(sidx, v, stride);
+      const float w = BINW ? (float)((mk >> v) & 1u) : W[q];
       if (w != 0.f) {
-        const T d = u0 - (T)F[samp_idx(sidx, v, stride)];
+        const T d = u0 - (T)F[q];
         num += A::data_val((T)w, d, p.eps2);
         den += (T)w;
       }
@@ -746,6 +750,8 @@ void launch_leaf_pass(Ctx& c, const T* snap, T* uval, const int32_t* child,
   a.split_list = c.split_list.p;
   a.counters = c.counters.p;
   a.epart = epart;
+  a.tileK = c.ell ? c.tileK.p : nullptr;
+  a.tileOff = c.ell ? c.tileOff.p : nullptr;
   const bool en = epart != nullptr;
   if (timed && c.timing) OCTF_CUDA(cudaEventRecord(c.tev[0], st));
 #define OCTF_LEAF(FZ, BW, EN)                                         \
@@ -1164,12 +1170,15 @@ double energy_impl(Ctx& c, const T* u, const int32_t* child,
     k_energy<T, true><<<g, kT, 0, st>>>(c.lblocks.p, c.nlb, c.lkey.p, c.nbr.p,
                                         c.lmeta.p, u, c.F.p, c.W.p, c.M.p,
                                         c.sstride, c.nviews, lp, c.partials.p,
-                                        terms);
+                                        terms, c.ell ? c.tileK.p : nullptr,
+                                        c.ell ? c.tileOff.p : nullptr);
   else
     k_energy<T, false><<<g, kT, 0, st>>>(c.lblocks.p, c.nlb, c.lkey.p,
                                          c.nbr.p, c.lmeta.p, u, c.F.p, c.W.p,
                                          c.M.p, c.sstride, c.nviews, lp,
-                                         c.partials.p, terms);
+                                         c.partials.p, terms,
+                                         c.ell ? c.tileK.p : nullptr,
+                                         c.ell ? c.tileOff.p : nullptr);
   OCTF_CUDA(cudaGetLastError());
   ++c.launches;
   if (c.timing) OCTF_CUDA(cudaEventRecord(c.tev[3], st));
@@ -1277,6 +1286,9 @@ void pd_passes_impl(Ctx& c, PdHostArgs& a, cudaStream_t st) {
   if (a.npasses < 1) return;
   ensure_prepared<T>(c, a.child, a.cap, a.d_max, a.state, st);
   const int nv = c.nviews;
+  if (c.ell)
+    throw Error(kEArg, "solver='pd' needs the dense sample layout "
+                       "(octf_ctx_set_options(ctx, OCTF_CTX_DENSE))");
   if (!(nv == 4 || nv == 8 || nv == 16 || nv == 32 || nv == 64) ||
       c.sstride != nv || (nv == 64 && c.binw))
     throw Error(kEArg, "solver='pd' supports 4, 8, 16, 32 or 64 views");

@@ -518,6 +518,7 @@ class PDSolver:
         used, cap = self.u.used, self.u.capacity
         self.vvals, self.vws, self.vchilds = view_arrays(views or [])
         self.ctx = _lib.Ctx()
+        self.ctx.set_dense(True)   # the pd kernel reads the dense layout
         self.samples = samples
         if samples is not None:
             self.kern.ctx_prepare(self.ctx, self.u.child, self.u.state,

@@ -68,13 +68,14 @@ int octf_ctx_invalidate(octf_ctx *ctx);
  * (int64[10]) */
 int octf_ctx_info(octf_ctx *ctx, int64_t *out);
 
-/* Context options.  OCTF_CTX_DENSE: keep the dense [leaf][view] sample
- * layout even above 32 views (solver="pd" needs it); by default more than
- * 32 views use the ELL layout -- per 256-leaf tile only as many rows as its
- * most-observed leaf has observed views, each leaf's observed samples in
- * view order (the zero-weight views the reference skips,
- * _kernels.pyx:244-252, are not stored). */
+/* Context options.  By default more than 64 views use the ELL sample
+ * layout -- per 256-leaf tile only as many rows as its most-observed leaf
+ * has observed views, each leaf's observed samples in view order (the
+ * zero-weight views the reference skips, _kernels.pyx:244-252, are not
+ * stored).  OCTF_CTX_DENSE keeps the dense [leaf][view] layout at any view
+ * count (solver="pd" needs it); OCTF_CTX_ELL uses ELL from 33 views. */
 #define OCTF_CTX_DENSE 1
+#define OCTF_CTX_ELL 2
 int octf_ctx_set_options(octf_ctx *ctx, int flags);
 
 /* Live profiling: enable != 0 brackets the leaf-update and energy kernels

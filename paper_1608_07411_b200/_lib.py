@@ -137,8 +137,12 @@ class Ctx:
         return dict(zip(keys, (int(v) for v in out)))
 
     def set_dense(self, dense: bool = True) -> None:
-        """Keep the dense sample layout above 32 views (solver='pd')."""
+        """Keep the dense sample layout at any view count (solver='pd')."""
         call("octf_ctx_set_options", self.h, 1 if dense else 0)
+
+    def set_options(self, flags: int) -> None:
+        """octf_ctx_set_options: 1 = dense samples, 2 = ELL from 33 views."""
+        call("octf_ctx_set_options", self.h, int(flags))
 
     def profile(self, enable: bool = True) -> dict:
         """Read and reset the live kernel timers; (re)arm them if enable."""

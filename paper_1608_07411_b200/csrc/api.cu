@@ -152,8 +152,10 @@ int octf_ctx_set_options(octf_ctx* ctx, int flags) {
   return guard([&] {
     if (!ctx) throw octf::Error(octf::kEArg, "null context");
     const bool dense = (flags & OCTF_CTX_DENSE) != 0;
-    if (dense != ctx->c.dense_only) {
+    const bool ell = (flags & OCTF_CTX_ELL) != 0;
+    if (dense != ctx->c.dense_only || ell != ctx->c.force_ell) {
       ctx->c.dense_only = dense;
+      ctx->c.force_ell = ell;
       ctx->c.store_ok = false;
       ctx->c.valid = false;  // regather in the requested layout
     }

@@ -26,6 +26,8 @@ void check_cuda(cudaError_t e, const char* what) {
 Ctx::Ctx() {
   const char* fg = std::getenv("OCTF_FULL_GATHER");
   no_regather = fg && fg[0] == '1';
+  const char* fe = std::getenv("OCTF_FORCE_ELL");  // tests: ELL from 33 views
+  force_ell = fe && fe[0] == '1';
   OCTF_CUDA(cudaMallocHost((void**)&h_counters, 64 * sizeof(int32_t)));
   OCTF_CUDA(cudaMallocHost((void**)&h_scalar, 8 * sizeof(double)));
 }
@@ -473,7 +475,7 @@ __global__ void k_ell_fresh(const int32_t* __restrict__ fresh,
                             const int4* __restrict__ lmeta, ViewSet vs,
                             const int32_t* __restrict__ tileK,
                             const int64_t* __restrict__ tileOff, float* F,
-                            float* W, int32_t* overflow) {
+                            float* W, int32_t* overflow, int32_t* need) {
   const int lane = threadIdx.x & 31;
   const int nw = (int)(gridDim.x * (blockDim.x >> 5));
   const int n = *nfresh;
@@ -491,6 +493,21 @@ __global__ void k_ell_fresh(const int32_t* __restrict__ fresh,
     const int z = b == 0 ? 0 : 2 * pz + (c & 1);
     const int K = tileK[s >> 8];
     int j = 0;
+    // count first: a leaf that does not fit leaves its tile untouched
+    for (int v0 = 0; v0 < vs.n; v0 += 32) {
+      const int v = v0 + lane;
+      bool on = false;
+      if (v < vs.n) on = vs.w[v][descend(vs.child[v], L, x, y, z)] != 0.f;
+      j += __popc(__ballot_sync(0xffffffffu, on));
+    }
+    if (j > K) {
+      if (lane == 0) {
+        atomicExch(overflow, 1);
+        atomicMax(need + (s >> 8), j);
+      }
+      continue;
+    }
+    j = 0;
     for (int v0 = 0; v0 < vs.n; v0 += 32) {
       const int v = v0 + lane;
       float f = 0.f, w = 0.f;
@@ -511,7 +528,25 @@ __global__ void k_ell_fresh(const int32_t* __restrict__ fresh,
       F[ell_idx(tileOff, s, r)] = 0.f;
       W[ell_idx(tileOff, s, r)] = 0.f;
     }
-    if (lane == 0 && j > K) atomicExch(overflow, 1);
+  }
+}
+
+// move overflowing tiles to bigger row ranges at the end of the store:
+// their rows copied, the new rows zeroed (one CTA per moved tile)
+__global__ void k_ell_move(const int32_t* __restrict__ tiles,
+                           const int32_t* __restrict__ oldK,
+                           const int64_t* __restrict__ oldOff,
+                           const int32_t* __restrict__ newK,
+                           const int64_t* __restrict__ newOff, float* F,
+                           float* W) {
+  const int j = blockIdx.x;
+  const int64_t o0 = oldOff[j], o1 = newOff[j];
+  const int k0 = oldK[j], k1 = newK[j];
+  (void)tiles;
+  for (int64_t e = threadIdx.x; e < (int64_t)k1 * 256; e += blockDim.x) {
+    const bool keep = e < (int64_t)k0 * 256;
+    F[o1 + e] = keep ? F[o0 + e] : 0.f;
+    W[o1 + e] = keep ? W[o0 + e] : 0.f;
   }
 }
 
@@ -838,6 +873,7 @@ static bool ell_list_samples(Ctx& c, int64_t nold, int64_t nnew,
   const int64_t nt_old = c.ell_tiles;
   const int64_t nt_new = (nnew * 8 + kTileLeaves - 1) / kTileLeaves;
   int64_t total = c.ell_size;
+  if (4 * c.ell_waste > total) return false;  // compact: full rebuild
   if (nt_new > nt_old) {
     int32_t* cnt = c.sort_k32.ensure(nt_new * 256 + 1);
     OCTF_CUDA(cudaMemsetAsync(cnt, 0, nt_new * 256 * sizeof(int32_t), st));
@@ -884,15 +920,70 @@ static bool ell_list_samples(Ctx& c, int64_t nold, int64_t nnew,
       c.lblocks.p, c.lmeta.p, nnew, nold, oldmask, c.tileK.p, c.tileOff.p,
       c.F.p, c.W.p, fresh, c.counters.p + 2, c.counters.p + 4);
   // (slots past the list's end are never leaves: their rows are not read)
-  k_ell_fresh<<<148 * 8, kThreads, 0, st>>>(fresh, c.counters.p + 2,
-                                             c.lmeta.p, ctx_views(c),
-                                             c.tileK.p, c.tileOff.p, c.F.p,
-                                             c.W.p, c.counters.p + 3);
-  OCTF_CUDA(cudaGetLastError());
-  OCTF_CUDA(cudaMemcpyAsync(c.h_counters, c.counters.p, 8 * sizeof(int32_t),
-                            cudaMemcpyDeviceToHost, st));
-  OCTF_CUDA(cudaStreamSynchronize(st));
-  if (c.h_counters[3]) return false;  // a leaf overflows its tile's rows
+  int32_t* need = c.app_buf.ensure(nt_new + 1);
+  OCTF_CUDA(cudaMemsetAsync(need, 0, (nt_new + 1) * sizeof(int32_t), st));
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    k_ell_fresh<<<148 * 8, kThreads, 0, st>>>(
+        fresh, c.counters.p + 2, c.lmeta.p, ctx_views(c), c.tileK.p,
+        c.tileOff.p, c.F.p, c.W.p, c.counters.p + 3, need);
+    OCTF_CUDA(cudaGetLastError());
+    OCTF_CUDA(cudaMemcpyAsync(c.h_counters, c.counters.p, 8 * sizeof(int32_t),
+                              cudaMemcpyDeviceToHost, st));
+    OCTF_CUDA(cudaStreamSynchronize(st));
+    if (!c.h_counters[3]) break;
+    if (attempt == 1) return false;
+    // some new leaves see more views than their tile has rows: give those
+    // tiles bigger row ranges at the end of the store (with headroom) and
+    // gather again (writes are idempotent)
+    std::vector<int32_t> hneed(nt_new), hK(nt_new);
+    std::vector<int64_t> hOff(nt_new);
+    OCTF_CUDA(cudaMemcpyAsync(hneed.data(), need, nt_new * sizeof(int32_t),
+                              cudaMemcpyDeviceToHost, st));
+    OCTF_CUDA(cudaMemcpyAsync(hK.data(), c.tileK.p, nt_new * sizeof(int32_t),
+                              cudaMemcpyDeviceToHost, st));
+    OCTF_CUDA(cudaMemcpyAsync(hOff.data(), c.tileOff.p,
+                              nt_new * sizeof(int64_t),
+                              cudaMemcpyDeviceToHost, st));
+    OCTF_CUDA(cudaStreamSynchronize(st));
+    std::vector<int32_t> mt, mk0, mk1;
+    std::vector<int64_t> mo0, mo1;
+    const int64_t keep = total;
+    for (int64_t t = 0; t < nt_new; ++t) {
+      if (hneed[t] <= hK[t]) continue;
+      const int k1 = hneed[t] + hneed[t] / 4 + 4;
+      mt.push_back((int32_t)t);
+      mk0.push_back(hK[t]);
+      mo0.push_back(hOff[t]);
+      mk1.push_back(k1);
+      mo1.push_back(total);
+      c.ell_waste += (int64_t)hK[t] * 256;
+      hK[t] = k1;
+      hOff[t] = total;
+      total += (int64_t)k1 * 256;
+    }
+    // (the old ranges stay unused until the next full rebuild compacts)
+    c.F.grow_keep((size_t)total + 1, (size_t)keep, st);
+    c.W.grow_keep((size_t)total + 1, (size_t)keep, st);
+    const int nm = (int)mt.size();
+    DevBuf<int32_t> dmt, dk0, dk1;
+    DevBuf<int64_t> do0, do1;
+    dmt.ensure(nm); dk0.ensure(nm); dk1.ensure(nm); do0.ensure(nm); do1.ensure(nm);
+    OCTF_CUDA(cudaMemcpyAsync(dmt.p, mt.data(), nm * 4, cudaMemcpyHostToDevice, st));
+    OCTF_CUDA(cudaMemcpyAsync(dk0.p, mk0.data(), nm * 4, cudaMemcpyHostToDevice, st));
+    OCTF_CUDA(cudaMemcpyAsync(dk1.p, mk1.data(), nm * 4, cudaMemcpyHostToDevice, st));
+    OCTF_CUDA(cudaMemcpyAsync(do0.p, mo0.data(), nm * 8, cudaMemcpyHostToDevice, st));
+    OCTF_CUDA(cudaMemcpyAsync(do1.p, mo1.data(), nm * 8, cudaMemcpyHostToDevice, st));
+    k_ell_move<<<nm, 256, 0, st>>>(dmt.p, dk0.p, do0.p, dk1.p, do1.p, c.F.p,
+                                   c.W.p);
+    OCTF_CUDA(cudaGetLastError());
+    OCTF_CUDA(cudaMemcpyAsync(c.tileK.p, hK.data(), nt_new * sizeof(int32_t),
+                              cudaMemcpyHostToDevice, st));
+    OCTF_CUDA(cudaMemcpyAsync(c.tileOff.p, hOff.data(),
+                              nt_new * sizeof(int64_t), cudaMemcpyHostToDevice,
+                              st));
+    OCTF_CUDA(cudaMemsetAsync(c.counters.p + 3, 0, sizeof(int32_t), st));
+    OCTF_CUDA(cudaStreamSynchronize(st));
+  }
   c.nlb = nnew;
   c.nleaves = c.h_counters[4];
   c.ell_tiles = nt_new;
@@ -1094,12 +1185,13 @@ void ctx_gather_ell(Ctx& c, cudaStream_t st) {
   c.ell = true;
   c.ell_tiles = nt;
   c.ell_size = total;
+  c.ell_waste = 0;
   c.sstride = 0;
 }
 
 void ctx_gather(Ctx& c, cudaStream_t st) {
   const auto t0 = std::chrono::steady_clock::now();
-  if (!c.ext_F && !c.dense_only && c.nviews > 32) {
+  if (!c.ext_F && !c.dense_only && (c.nviews > 64 || (c.force_ell && c.nviews > 32))) {
     ctx_gather_ell(c, st);
     OCTF_CUDA(cudaStreamSynchronize(st));
     c.store_ok = true;

@@ -137,13 +137,15 @@ struct Ctx {
   DevBuf<uint32_t> M;         // [sample] bit v = weight of view v is 1
   bool binw = false;          // samples use the mask format
   int64_t sstride = 0;        // views per leaf vector, padded to 4
-  // ELL layout (views > 32, unless dense_only): F/W hold per tile K_t rows
+  // ELL layout (views > 64, unless dense_only): F/W hold per tile K_t rows
   // of the leaves' observed samples (octf_common.cuh ell_idx)
   bool ell = false;
   bool dense_only = false;    // octf_ctx_set_options: keep the dense layout
+  bool force_ell = false;     // ... or use ELL from 33 views (default: 65)
   DevBuf<int32_t> tileK;      // per tile: rows
   DevBuf<int64_t> tileOff;    // per tile: first float of its rows
   int64_t ell_tiles = 0, ell_size = 0;
+  int64_t ell_waste = 0;      // rows of tiles moved to bigger ranges
   bool store_ok = false;      // F/W/M describe the current leaf-block list
   bool own_change = false;    // invalid only because our pass restructured
   bool no_regather = false;   // env OCTF_FULL_GATHER=1: always rebuild all

@@ -207,28 +207,34 @@ def test_frame_split_prepare_equals_single_gpu():
 
 
 def test_cfg3_many_views_ell_store_end_to_end():
-    """40 views: the descent reads the ELL sample store (observed views only,
+    """40 views, ELL forced: the descent reads the ELL sample store (observed views only,
     per-tile rows) -- through restructuring passes (in-place list patches
     with warp-gathered new leaves) the fp64 pools equal the oracle's, and a
     forced full regather gives the same trajectory."""
     from paper_1608_07411_b200 import fusion, scenes, volume
+    import os
     sc = scenes.make_cfg3(d_max=6, n_views=40, width=160, height=120,
                           focal=131.25, device="cuda")
-    res, ref, _ = run_case(sc, 6)
+    os.environ["OCTF_FORCE_ELL"] = "1"
+    try:
+        res, ref, _ = run_case(sc, 6)
+    finally:
+        del os.environ["OCTF_FORCE_ELL"]
     assert sum(s.splits + s.joins for s in ref.stats) > 0
     p = fusion.FusionParams(**dict(sc.params, iterations=6))
     dom = volume.VolumeDomain(sc.origin, sc.voxel_size, sc.resolution)
     views, u0, _ = fusion.prepare(sc.depths, sc.cameras, dom, p)
     s = fusion.Solver(u0, views, p, precision="fp32")
+    s.ctx.set_options(2)               # ELL from 33 views
     s.run(0, 1)
     assert s.ctx.info()["ell"] == 1
     s.run(1, 5)
     a = s.result().field.to_host()
     s.close()
-    import os
     os.environ["OCTF_FULL_GATHER"] = "1"
     try:
         s2 = fusion.Solver(u0, views, p, precision="fp32")
+        s2.ctx.set_options(2)
         s2.run(0, 6)
         b = s2.result().field.to_host()
         s2.close()

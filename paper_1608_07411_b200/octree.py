@@ -178,14 +178,26 @@ class OctreeField:
         (octree.py:168-181)."""
         return iter(_leaves(to_numpy(self.child[:self.used])))
 
-    def to_host(self) -> HostPool:
-        """Download the pool (reference layout, trimmed to ``used``)."""
+    def to_host(self, scratch: bool = True) -> HostPool:
+        """Download the pool (reference layout, trimmed to ``used``) through
+        pinned staging buffers; ``scratch=False`` skips the solver scratch
+        (snap, joined)."""
         u = self.used
-        return HostPool(to_numpy(self.value[:u]), to_numpy(self.child[:u]),
-                        self.state.copy(), self.d_max,
-                        weight=None if self.weight is None else to_numpy(self.weight[:u]),
-                        snap=None if self.snap is None else to_numpy(self.snap[:u]),
-                        joined=None if self.joined is None else to_numpy(self.joined[:u]))
+
+        def dl(t):
+            if t is None:
+                return None
+            t = t[:u]
+            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            h.copy_(t, non_blocking=True)
+            return h
+        parts = [dl(self.value), dl(self.child), dl(self.weight),
+                 dl(self.snap) if scratch else None,
+                 dl(self.joined) if scratch else None]
+        torch.cuda.current_stream().synchronize()
+        v, c, w, sn, j = (None if h is None else h.numpy() for h in parts)
+        return HostPool(v, c, self.state.copy(), self.d_max, weight=w, snap=sn,
+                        joined=j)
 
     @classmethod
     def from_host(cls, value, child, state, d_max, weight=None,

@@ -201,38 +201,107 @@ __global__ void k_leaf_tables(const int32_t* __restrict__ child,
   nbr[i * 12 + d] = ref;
 }
 
-// per (leaf, view): the view node answering at the leaf's level
-// (_kernels.pyx:265-273 cursors == root descent in the view tree)
-__global__ void k_gather(const int32_t* __restrict__ ucs,
+
+// ---- view lookups by level (replaces a root descent per leaf and view):
+// vm[y][s] = the node of view v0+y answering at slot s's cell and level,
+// filled top-down: a slot's node is its parent's node's child c if that
+// node has children, else the parent's node (descend() semantics,
+// _kernels.pyx:265-273 cursors).  One load per (node, view) instead of one
+// per level.
+__global__ void k_vmap_level(const int32_t* __restrict__ blocks, int64_t nblk,
+                             const int32_t* __restrict__ bparent, ViewSet vs,
+                             int v0, int64_t cap, int32_t* vm) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = gid >> 3;
+  const int c = (int)(gid & 7);
+  if (i >= nblk) return;
+  const int y = blockIdx.y;
+  const int32_t b = blocks[i];
+  const int32_t p = bparent[block_id(b)];
+  int32_t* m = vm + (int64_t)y * cap;
+  const int32_t vp = m[p];
+  const int32_t vc = __ldg(vs.child[v0 + y] + vp);
+  m[b + c] = vc >= 0 ? vc + c : vp;
+}
+
+// ELL through the view map: pass 1 counts observed views per slot, pass 2
+// appends them in view order at the slot's running row (one thread per slot
+// per chunk: no atomics, order = view order)
+__global__ void k_vcount(const int32_t* __restrict__ ucs,
                          const int32_t* __restrict__ lblocks, int64_t nlb,
-                         const uint64_t* __restrict__ lkey, ViewSet vs,
-                         float* F, float* W, int64_t stride, int32_t* nonbin) {
-  int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  int64_t i = gid >> 3;
-  int c = (int)(gid & 7);
+                         ViewSet vs, int v0, int nc, int64_t cap,
+                         const int32_t* __restrict__ vm, int32_t* cnt) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = gid >> 3;
+  const int c = (int)(gid & 7);
   if (i >= nlb) return;
-  int32_t b = lblocks[i];
-  int64_t sidx = i * 8 + c;
-  bool active = b >= 0 && !(b == 0 && c != 0) && ucs[b + c] < 0;
-  if (b < 0) b = 0;
-  int L, px, py, pz;
-  unpack_cell(lkey[i], L, px, py, pz);
-  int x = b == 0 ? 0 : 2 * px + ((c >> 2) & 1);
-  int y = b == 0 ? 0 : 2 * py + ((c >> 1) & 1);
-  int z = b == 0 ? 0 : 2 * pz + (c & 1);
-  int flag = 0;
-  for (int v = 0; v < vs.n; ++v) {
-    float f = 0.f, w = 0.f;
-    if (active) {
-      int32_t n = descend(vs.child[v], L, x, y, z);
-      f = vs.val[v][n];
-      w = vs.w[v][n];
-      flag |= (w != 0.f && w != 1.f);
+  const int32_t b = lblocks[i];
+  if (!(b >= 0 && !(b == 0 && c != 0) && ucs[b + c] < 0)) return;
+  int k = 0;
+  for (int y = 0; y < nc; ++y)
+    k += __ldg(vs.w[v0 + y] + vm[(int64_t)y * cap + b + c]) != 0.f;
+  cnt[gid] += k;
+}
+
+__global__ void k_vput(const int32_t* __restrict__ ucs,
+                       const int32_t* __restrict__ lblocks, int64_t nlb,
+                       ViewSet vs, int v0, int nc, int64_t cap,
+                       const int32_t* __restrict__ vm,
+                       const int64_t* __restrict__ tileOff, int32_t* cur,
+                       float* F, float* W) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = gid >> 3;
+  const int c = (int)(gid & 7);
+  if (i >= nlb) return;
+  const int32_t b = lblocks[i];
+  if (!(b >= 0 && !(b == 0 && c != 0) && ucs[b + c] < 0)) return;
+  int r = cur[gid];
+  for (int y = 0; y < nc; ++y) {
+    const int32_t n = vm[(int64_t)y * cap + b + c];
+    const float w = __ldg(vs.w[v0 + y] + n);
+    if (w != 0.f) {
+      F[ell_idx(tileOff, gid, r)] = __ldg(vs.val[v0 + y] + n);
+      W[ell_idx(tileOff, gid, r)] = w;
+      ++r;
     }
-    F[samp_idx(sidx, v, stride)] = f;
-    W[samp_idx(sidx, v, stride)] = w;
   }
-  if (flag) atomicExch(nonbin, 1);
+  cur[gid] = r;
+}
+
+// rows [cur, K) of every slot (all rows of non-leaf slots) to zero
+__global__ void k_ell_pad(const int32_t* __restrict__ cur, int64_t nslot,
+                          const int32_t* __restrict__ tileK,
+                          const int64_t* __restrict__ tileOff, float* F,
+                          float* W) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nslot) return;
+  const int K = tileK[s >> 8];
+  for (int r = cur[s]; r < K; ++r) {
+    F[ell_idx(tileOff, s, r)] = 0.f;
+    W[ell_idx(tileOff, s, r)] = 0.f;
+  }
+}
+
+// samples of the list's leaf slots from the view map (dense layout)
+__global__ void k_vgather(const int32_t* __restrict__ ucs,
+                          const int32_t* __restrict__ lblocks, int64_t nlb,
+                          ViewSet vs, int v0, int64_t cap,
+                          const int32_t* __restrict__ vm, float* F, float* W,
+                          int64_t stride, int32_t* nonbin) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = gid >> 3;
+  const int c = (int)(gid & 7);
+  if (i >= nlb) return;
+  const int y = blockIdx.y;
+  const int32_t b = lblocks[i];
+  const bool active = b >= 0 && !(b == 0 && c != 0) && ucs[b + c] < 0;
+  if (!active) return;
+  const int32_t n = vm[(int64_t)y * cap + b + c];
+  const float f = __ldg(vs.val[v0 + y] + n);
+  const float w = __ldg(vs.w[v0 + y] + n);
+  F[samp_idx(gid, v0 + y, stride)] = f;
+  W[samp_idx(gid, v0 + y, stride)] = w;
+  if (w != 0.f && w != 1.f) atomicExch(nonbin, 1);
 }
 
 // per (leaf, view) from caller-supplied per-slot arrays [view][cap]
@@ -331,7 +400,7 @@ __global__ void k_set_lpos(const int32_t* __restrict__ lblocks, int64_t n,
 
 // per slot of the patched list: a leaf that was a leaf at the same position
 // keeps its samples; a new leaf is queued for k_gather_fresh; any other slot
-// is zeroed (as k_gather leaves non-leaf slots)
+// is zeroed (as the full gather leaves non-leaf slots)
 template <bool BINW>
 __global__ void k_sample_update(const int32_t* __restrict__ lblocks,
                                 const int4* __restrict__ lmeta, int64_t n,
@@ -594,50 +663,6 @@ __global__ void k_ell_tilemax(const int32_t* __restrict__ cnt, int64_t n,
   }
 }
 
-// observed samples of one leaf slot into its rows, the rest zeroed
-__device__ __forceinline__ void ell_write_slot(
-    int64_t s, int L, int x, int y, int z, bool leaf, ViewSet vs,
-    const int32_t* tileK, const int64_t* tileOff, float* F, float* W) {
-  const int K = tileK[s >> 8];
-  int j = 0;
-  if (leaf) {
-    for (int v = 0; v < vs.n; ++v) {
-      const int32_t nd = descend(vs.child[v], L, x, y, z);
-      const float w = vs.w[v][nd];
-      if (w != 0.f) {
-        if (j < K) {
-          F[ell_idx(tileOff, s, j)] = vs.val[v][nd];
-          W[ell_idx(tileOff, s, j)] = w;
-        }
-        ++j;
-      }
-    }
-  }
-  for (int r = j; r < K; ++r) {
-    F[ell_idx(tileOff, s, r)] = 0.f;
-    W[ell_idx(tileOff, s, r)] = 0.f;
-  }
-}
-
-__global__ void k_ell_fill(const int32_t* __restrict__ ucs,
-                           const int32_t* __restrict__ lblocks, int64_t nlb,
-                           const uint64_t* __restrict__ lkey, ViewSet vs,
-                           const int32_t* __restrict__ tileK,
-                           const int64_t* __restrict__ tileOff, int64_t slot0,
-                           int64_t slot1, float* F, float* W) {
-  const int64_t s = slot0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= slot1) return;
-  const int64_t i = s >> 3;
-  const int c = (int)(s & 7);
-  const int32_t b = i < nlb ? lblocks[i] : -1;
-  const bool leaf = b >= 0 && !(b == 0 && c != 0) && ucs[b + c] < 0;
-  int L = 0, px = 0, py = 0, pz = 0;
-  if (leaf) unpack_cell(lkey[i], L, px, py, pz);
-  const int x = b <= 0 ? 0 : 2 * px + ((c >> 2) & 1);
-  const int y = b <= 0 ? 0 : 2 * py + ((c >> 1) & 1);
-  const int z = b <= 0 ? 0 : 2 * pz + (c & 1);
-  ell_write_slot(s, L, x, y, z, leaf, vs, tileK, tileOff, F, W);
-}
 
 __global__ void k_masks(const float* __restrict__ W, int64_t stride, int nv,
                         int64_t n, uint32_t* M) {
@@ -1148,14 +1173,50 @@ ViewSet ctx_views(const Ctx& c) {
   return v;
 }
 
+// the per-level view maps of every live slot, views in chunks of 32;
+// fn(v0, nc, vm) consumes each chunk's maps (vm[y * cap + slot])
+template <typename Fn>
+static void view_maps(Ctx& c, cudaStream_t st, Fn fn) {
+  const int nv = c.nviews;
+  const int chunk = nv < 32 ? nv : 32;
+  int32_t* vm = c.vmap.ensure((size_t)chunk * c.cap);
+  for (int v0 = 0; v0 < nv; v0 += chunk) {
+    const int nc = nv - v0 < chunk ? nv - v0 : chunk;
+    for (int y = 0; y < nc; ++y)  // root slot -> root node
+      OCTF_CUDA(cudaMemsetAsync(vm + (int64_t)y * c.cap, 0, sizeof(int32_t), st));
+    for (int L = 1; L <= c.d_max && L < (int)c.lvl_cnt.size(); ++L) {
+      const int64_t nb = c.lvl_cnt[L];
+      if (!nb) continue;
+      k_vmap_level<<<dim3(grid_for(nb * 8), nc), kThreads, 0, st>>>(
+          c.lvl_blocks.p + c.lvl_off[L], nb, c.bparent.p, ctx_views(c), v0,
+          c.cap, vm);
+    }
+    fn(v0, nc, vm);
+  }
+  OCTF_CUDA(cudaGetLastError());
+}
+
+// dense gather through the view maps
+static void gather_by_levels(Ctx& c, int64_t nvp, cudaStream_t st) {
+  const int64_t n = c.nlb * 8;
+  view_maps(c, st, [&](int v0, int nc, const int32_t* vm) {
+    k_vgather<<<dim3(grid_for(n), nc), kThreads, 0, st>>>(
+        c.child_key, c.lblocks.p, c.nlb, ctx_views(c), v0, c.cap, vm, c.F.p,
+        c.W.p, nvp, c.counters.p);
+  });
+}
+
 void ctx_gather_ell(Ctx& c, cudaStream_t st) {
   const int64_t n = c.nlb * 8;
   const int64_t nt = (n + kTileLeaves - 1) / kTileLeaves;
   // one pass over the tiles: counts -> rows -> offsets (from 0)
   int32_t* cnt = c.sort_k32.ensure(nt * 256 + 1);
   OCTF_CUDA(cudaMemsetAsync(cnt, 0, nt * 256 * sizeof(int32_t), st));
-  k_ell_count<<<grid_for(n), kThreads, 0, st>>>(
-      c.child_key, c.lblocks.p, c.nlb, c.lkey.p, ctx_views(c), cnt, 0, n);
+  view_maps(c, st, [&](int v0, int nc, const int32_t* vm) {
+    k_vcount<<<grid_for(n), kThreads, 0, st>>>(c.child_key, c.lblocks.p,
+                                                c.nlb, ctx_views(c), v0, nc,
+                                                c.cap, vm, cnt);
+  });
   int64_t* rowsz = reinterpret_cast<int64_t*>(c.sort_k64.ensure(nt + 1));
   c.tileK.ensure(nt + 1);
   c.tileOff.ensure(nt + 1);
@@ -1175,10 +1236,17 @@ void ctx_gather_ell(Ctx& c, cudaStream_t st) {
   OCTF_CUDA(cudaStreamSynchronize(st));
   c.F.ensure((size_t)total + 1);
   c.W.ensure((size_t)total + 1);
+  int32_t* cur = cnt;  // reuse: running row per slot
+  OCTF_CUDA(cudaMemsetAsync(cur, 0, nt * 256 * sizeof(int32_t), st));
+  view_maps(c, st, [&](int v0, int nc, const int32_t* vm) {
+    k_vput<<<grid_for(n), kThreads, 0, st>>>(c.child_key, c.lblocks.p, c.nlb,
+                                              ctx_views(c), v0, nc, c.cap, vm,
+                                              c.tileOff.p, cur, c.F.p, c.W.p);
+  });
   if (nt)
-    k_ell_fill<<<grid_for(nt * 256), kThreads, 0, st>>>(
-        c.child_key, c.lblocks.p, c.nlb, c.lkey.p, ctx_views(c), c.tileK.p,
-        c.tileOff.p, 0, nt * 256, c.F.p, c.W.p);
+    k_ell_pad<<<grid_for(nt * 256), kThreads, 0, st>>>(cur, nt * 256,
+                                                        c.tileK.p, c.tileOff.p,
+                                                        c.F.p, c.W.p);
   OCTF_CUDA(cudaGetLastError());
   c.M.release();
   c.binw = false;
@@ -1220,9 +1288,7 @@ void ctx_gather(Ctx& c, cudaStream_t st) {
         c.child_key, c.lblocks.p, c.nlb, c.ext_F, c.ext_W, c.ext_cap, nv, c.F.p,
         c.W.p, nvp, c.counters.p);
   else
-    k_gather<<<grid_for(n), kThreads, 0, st>>>(c.child_key, c.lblocks.p,
-                                                c.nlb, c.lkey.p, ctx_views(c),
-                                                c.F.p, c.W.p, nvp, c.counters.p);
+    gather_by_levels(c, nvp, st);
   OCTF_CUDA(cudaGetLastError());
   OCTF_CUDA(cudaMemcpyAsync(c.h_counters, c.counters.p, sizeof(int32_t),
                             cudaMemcpyDeviceToHost, st));

@@ -159,6 +159,7 @@ struct Ctx {
   int64_t nholes = 0;
   bool list_full = false;     // list = every leaf block (not a shard subset)
   DevBuf<int32_t> app_buf;    // appended blocks scratch
+  DevBuf<int32_t> vmap;       // per-level view maps (gather), chunk x cap
 
   // ---- or samples supplied per slot by the caller (frozen trees only)
   const float* ext_F = nullptr;  // [view][ext_cap]

@@ -498,3 +498,36 @@ def extract_zero_surface(values, mask, tables):
     verts = np.column_stack([gx + t * (ga == 0), gy + t * (ga == 1),
                              gz + t * (ga == 2)])
     return verts, inv.reshape(-1, 3).astype(np.int32)
+
+
+# ------------------------------------------------------------ dense solver --
+
+def dense_step(u, fs, ws, p, xi):
+    """fusion.py:283-298 restated: forward differences (0 at the far
+    border), flux g/sqrt(|g|^2+eps^2), backward-difference divergence, data
+    term summed in view order, Jacobi step, clamp."""
+    eps2 = p.eps * p.eps
+    g = [np.zeros_like(u) for _ in range(3)]
+    g[0][:-1] = u[1:] - u[:-1]
+    g[1][:, :-1] = u[:, 1:] - u[:, :-1]
+    g[2][:, :, :-1] = u[:, :, 1:] - u[:, :, :-1]
+    gn = np.sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2] + eps2)
+    q = [gi / gn for gi in g]
+    div = (np.diff(q[0], axis=0, prepend=0.0) + np.diff(q[1], axis=1, prepend=0.0)
+           + np.diff(q[2], axis=2, prepend=0.0))
+    num = np.zeros_like(u)
+    den = np.full_like(u, p.gamma)
+    for f, w in zip(fs, ws):
+        wv = w.astype(np.float64)
+        d = u - f.astype(np.float64)
+        num += np.where(wv != 0.0, wv * d / np.sqrt(d * d + eps2), 0.0)
+        den += wv
+    un = u + xi * (p.lam * div - num / den)
+    return np.clip(un, -1.0, 1.0) if p.clamp else un
+
+
+def dense_fuse(u0, fs, ws, p):
+    u = np.array(u0, dtype=np.float64)
+    for t in range(p.iterations):
+        u = dense_step(u, fs, ws, p, step_scale(t, p))
+    return u

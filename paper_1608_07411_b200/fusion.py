@@ -45,6 +45,13 @@ __all__ = [
     "Solver",
     "tree_energy",
     "write_report",
+    "dense_fuse",
+    "dense_step",
+    "dense_energy",
+    "data_term_value",
+    "data_term_derivative",
+    "smoothness_value",
+    "smoothness_flux",
     "read_report",
 ]
 
@@ -667,6 +674,87 @@ def fuse(u0: OctreeField, views, params: FusionParams, *,
 
 
 # -- iteration reports (fusion.py:363-403) ----------------------------------
+
+# -- dense reference solver (fusion.py:253-325) -------------------------------
+
+def _full_tree_inputs(u0, fs, ws):
+    """A dense problem as full trees: every cell a finest-level leaf (unit
+    spacing), the tree path's arithmetic then equals the dense solver's."""
+    u = build_octree(as_device(u0, torch.float64), tau=-1.0)
+    views = [build_octree(as_device(f, torch.float32), as_device(w, torch.uint8),
+                          tau=-1.0, dtype=np.float32) for f, w in zip(fs, ws)]
+    return u, views
+
+
+def _dense_params(params: FusionParams) -> FusionParams:
+    # the dense solver never restructures
+    return FusionParams(**{**params.__dict__, "tau_split": 0.0,
+                           "tau_join": float("inf")})
+
+
+def dense_fuse(u0, fs, ws, params: FusionParams):
+    """The reference's dense solver (``fusion.dense_fuse``, fusion.py:311-325)
+    on the GPU: the grid runs as a full tree (all leaves at the finest level,
+    unit spacing), where the descent is the dense Jacobi step bit for bit
+    (the reference's own tree == dense check, tests/test_fusion.py:121-131).
+    Returns (u grid, stats) like the reference; energies are the tree's leaf
+    sums (order differs from numpy's pairwise sum at the 1e-13 level)."""
+    u, views = _full_tree_inputs(u0, fs, ws)
+    res = fuse(u, views, _dense_params(params), precision="fp64")
+    from .octree import densify
+    grid = densify(res.field)
+    n3 = grid.size
+    stats = [IterationStats(s.iteration, s.energy, n3, n3 * 2 * 8, 0, 0,
+                            s.wall_ms) for s in res.stats]
+    return grid, stats
+
+
+def dense_step(u, fs, ws, params: FusionParams, xi: float):
+    """One Jacobi descent step on a dense grid (fusion.py:283-298)."""
+    t, views = _full_tree_inputs(u, fs, ws)
+    s = Solver(t, views, _dense_params(params), precision="fp64")
+    s.kern.iterate_pass(s.u.value, s.u.snap, s.u.child, s.u.joined,
+                        s.u.state, s.vvals, s.vws, s.vchilds, s.u.d_max,
+                        params.lam, params.eps, params.gamma, xi, 0.0,
+                        float("inf"), params.clamp, False, None, ctx=s.ctx)
+    from .octree import densify
+    out = densify(s.u)
+    s.close()
+    return out
+
+
+def dense_energy(u, fs, ws, params: FusionParams) -> float:
+    """Dense-grid energy (fusion.py:301-308) as the full tree's leaf sum."""
+    t, views = _full_tree_inputs(u, fs, ws)
+    return tree_energy(t, views, params)
+
+
+# pointwise pieces of the energy (fusion.py:330-358; host math, exposed for
+# derivative checks)
+def data_term_value(u: float, f, w, eps: float, gamma: float) -> float:
+    f = np.asarray(f, dtype=np.float64)
+    w = np.asarray(w, dtype=np.float64)
+    return float((w * np.sqrt((u - f) ** 2 + eps * eps)).sum()) / \
+        (gamma + float(w.sum()))
+
+
+def data_term_derivative(u: float, f, w, eps: float, gamma: float) -> float:
+    f = np.asarray(f, dtype=np.float64)
+    w = np.asarray(w, dtype=np.float64)
+    d = u - f
+    return float((w * d / np.sqrt(d * d + eps * eps)).sum()) / \
+        (gamma + float(w.sum()))
+
+
+def smoothness_value(g, eps: float) -> float:
+    g = np.asarray(g, dtype=np.float64)
+    return float(np.sqrt((g * g).sum() + eps * eps))
+
+
+def smoothness_flux(g, eps: float) -> np.ndarray:
+    g = np.asarray(g, dtype=np.float64)
+    return g / np.sqrt((g * g).sum() + eps * eps)
+
 
 REPORT_COLUMNS = ("iter", "energy", "node_count", "memory_bytes", "splits",
                   "joins", "wall_ms")

@@ -57,5 +57,32 @@ def main():
           v2.shape, f2.shape)
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and len(sys.argv) == 1:
     main()
+
+
+def dense_solver_fixture():
+    """dense.npz -- the reference's dense solver (fusion.dense_fuse,
+    fusion.py:253-325) on a seeded 16^3 grid with 4 views, 6 iterations."""
+    load_reference()
+    from octfuse import fusion
+    rng = np.random.default_rng(21)
+    n = 16
+    fs, ws = [], []
+    for _ in range(4):
+        f = np.clip(rng.standard_normal((n, n, n)) * 0.5, -1, 1).astype(np.float32)
+        w = (rng.random((n, n, n)) < 0.8).astype(np.uint8)
+        f[w == 0] = -1.0
+        fs.append(f)
+        ws.append(w)
+    u0 = np.clip(rng.standard_normal((n, n, n)) * 0.3, -1, 1)
+    p = fusion.FusionParams(iterations=6, lam=0.4)
+    u, stats = fusion.dense_fuse(u0, fs, ws, p)
+    np.savez_compressed(os.path.join(HERE, "dense.npz"), fs=np.stack(fs),
+                        ws=np.stack(ws), u0=u0, u=u,
+                        energies=np.array([s.energy for s in stats]))
+    print("dense", u.shape)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "dense":
+    dense_solver_fixture()

@@ -22,26 +22,9 @@
 // previous pass's post-propagate state, from the same values and roots.
 #pragma once
 
-// per-warp staging (each warp bulk-copies its own 32 leaves' rows on its
-// own mbarrier) was measured slower than one CTA-wide copy: 17 copies of
-// 128 B per warp cost more than the CTA barrier (cfg2 leaf kernel 0.43 vs
-// 0.34 ms); kept as a switch.  Per-warp energy partials (no closing CTA
-// reduction) were 1.6 % faster on cfg2 but 8 % slower on cfg5 (registers at
-// N = 32): off by default.
-#ifndef OCTF_LEAF_WARPSTAGE
-#define OCTF_LEAF_WARPSTAGE 0
-#endif
-#ifndef OCTF_LEAF_NBRREG
-#define OCTF_LEAF_NBRREG 1
-#endif
-#ifndef OCTF_LEAF_WARPPART
-#define OCTF_LEAF_WARPPART 0
-#endif
-#if OCTF_LEAF_WARPPART
-constexpr int kLeafParts = 8;  // energy partials per CTA (one per warp)
-#else
-constexpr int kLeafParts = 1;
-#endif
+// Measured and dropped (profiles/r01/pd_kernel_notes.md): per-warp
+// staging (17 bulk copies of 128 B per warp: slower than one CTA copy) and
+// per-warp energy partials (faster at N = 16, slower at N = 32).
 #ifndef OCTF_LEAF_MINB
 #define OCTF_LEAF_MINB 1
 #endif
@@ -84,60 +67,10 @@ struct LeafArgs {
   const int64_t* __restrict__ tileOff = nullptr;
 };
 
-// table direction of a step that leaves the block along the given axes
-template <int DX, int DY, int DZ>
-__device__ __forceinline__ int step_dir(bool ex, bool ey, bool ez) {
-  constexpr int fx = DX < 0 ? 0 : 1, fy = DY < 0 ? 2 : 3, fz = DZ < 0 ? 4 : 5;
-  // edge directions of the 13-point stencil (octf_common.cuh nbr_dir)
-  constexpr int exy = DX < 0 ? 6 : 8;    // (-x+y) / (+x-y)
-  constexpr int exz = DX < 0 ? 7 : 10;   // (-x+z) / (+x-z)
-  constexpr int eyz = DY < 0 ? 9 : 11;   // (-y+z) / (+y-z)
-  if (DX != 0 && DY != 0) return ex ? (ey ? exy : fx) : fy;
-  if (DX != 0 && DZ != 0) return ex ? (ez ? exz : fx) : fz;
-  if (DY != 0 && DZ != 0) return ey ? (ez ? eyz : fy) : fz;
-  if (DX != 0) return fx;
-  if (DY != 0) return fy;
-  return fz;
-}
-
-// snapshot value of the cell (x+DX, y+DY, z+DZ) at the leaf's level.
-// `own` is the shuffled value of sibling c^mask; `inside` = the point is in
-// the domain (out-of-domain points are never read by the stencil).
-template <int DX, int DY, int DZ, typename T>
-__device__ __forceinline__ T step_val(T own, int c, int cx, int cy, int cz,
-                                      bool inside, const int32_t* nb,
-                                      const T* __restrict__ snap) {
-  const bool ex = DX > 0 ? cx : (DX < 0 ? !cx : false);
-  const bool ey = DY > 0 ? cy : (DY < 0 ? !cy : false);
-  const bool ez = DZ > 0 ? cz : (DZ < 0 ? !cz : false);
-  constexpr int mask = (DX ? 4 : 0) | (DY ? 2 : 0) | (DZ ? 1 : 0);
-  T v = own;
-  if ((ex || ey || ez) && inside) {
-    const int32_t r = __ldg(nb + step_dir<DX, DY, DZ>(ex, ey, ez));
-    v = snap[r >= 0 ? r + (c ^ mask) : -r - 2];
-  }
-  return v;
-}
-
-// slot read for the cell (x+DX, y+DY, z+DZ) at the leaf's level, or -1 when
-// the cell is the sibling c^mask of the own block (value by shuffle) or the
-// point is not read; lets several fields share one neighbour-table lookup
-template <int DX, int DY, int DZ>
-__device__ __forceinline__ int step_idx(int c, int cx, int cy, int cz,
-                                        bool inside, const int32_t* nb) {
-  const bool ex = DX > 0 ? cx : (DX < 0 ? !cx : false);
-  const bool ey = DY > 0 ? cy : (DY < 0 ? !cy : false);
-  const bool ez = DZ > 0 ? cz : (DZ < 0 ? !cz : false);
-  constexpr int mask = (DX ? 4 : 0) | (DY ? 2 : 0) | (DZ ? 1 : 0);
-  int idx = -1;
-  if ((ex || ey || ez) && inside) {
-    const int32_t r = __ldg(nb + step_dir<DX, DY, DZ>(ex, ey, ez));
-    idx = r >= 0 ? r + (c ^ mask) : -r - 2;
-  }
-  return idx;
-}
-
-// as step_idx, from the block's 12 table entries already in registers
+// slot read for the cell (x+DX, y+DY, z+DZ) at the leaf's level, from the
+// block's 12 neighbour-table entries (in registers): -1 when the cell is the
+// sibling c^mask of the own block (value by shuffle) or is not read; else a
+// slot of the same-level neighbour block or the coarser leaf covering it
 template <int DX, int DY, int DZ>
 __device__ __forceinline__ int step_idx_r(int c, int cx, int cy, int cz,
                                           bool inside, const int32_t (&N)[12]) {
@@ -225,35 +158,7 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
   // Padding leaves and non-leaf slots hold zeros, so the copy is in bounds.
   constexpr int NVP = (NV + 3) & ~3;
   extern __shared__ __align__(128) float s_tile[];
-#if OCTF_LEAF_WARPSTAGE
-  // each warp stages the rows of its own 32 leaves (NVP rows of 128 B plus
-  // the mask / weight rows) with one bulk copy per row on its own mbarrier
-  __shared__ __align__(8) uint64_t s_bars[kT / 32];
-  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint64_t* const s_bar_p = &s_bars[wid];
-  if (NV > 0) {
-    const unsigned rows = BINW ? NVP + 1 : 2 * NVP;
-    if (lane == 0) {
-      mbar_init(s_bar_p, 1);
-      mbar_expect_tx(s_bar_p, rows * 128u);
-    }
-    __syncwarp();
-    const size_t tile = tile_id;
-    for (unsigned r = lane; r < rows; r += 32) {
-      const float* src;
-      if (r < (unsigned)NVP)
-        src = a.F + tile * NVP * kTileLeaves + r * kTileLeaves;
-      else if (BINW)
-        src = reinterpret_cast<const float*>(a.M + tile * kTileLeaves);
-      else
-        src = a.W + tile * NVP * kTileLeaves + (r - NVP) * kTileLeaves;
-      bulk_g2s(s_tile + r * kTileLeaves + wid * 32, src + wid * 32, 128,
-               s_bar_p);
-    }
-  }
-#else
   __shared__ __align__(8) uint64_t s_bar;
-  uint64_t* const s_bar_p = &s_bar;
   if (NV > 0) {
     if (threadIdx.x == 0) {
       mbar_init(&s_bar, 1);
@@ -271,7 +176,6 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
     }
     __syncthreads();  // barrier initialised before anyone waits on it
   }
-#endif
 
   // one 16 B load: base slot, parent cell, leaf mask and level
   const int4 meta = inrange ? __ldg(a.lmeta + i) : make_int4(0, 0, 0, 0);
@@ -299,7 +203,6 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
   const T o_xy = __shfl_xor_sync(FULL, S0, 6);
   const T o_xz = __shfl_xor_sync(FULL, S0, 5);
   const T o_yz = __shfl_xor_sync(FULL, S0, 3);
-#if OCTF_LEAF_NBRREG
   // the block's 12 table entries as three 16 B loads, indices by selects
   // (the primal-dual kernel's form)
   int32_t NB[12];
@@ -327,23 +230,6 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
   const T Smzx = SV(1, 0, -1, o_xz, zm && xp);
   const T Smzy = SV(0, 1, -1, o_yz, zm && yp);
 #undef SV
-#else
-  // forward neighbours
-  const T Sx = step_val<1, 0, 0>(o_x, c, cx, cy, cz, active && xp, nb, snap);
-  const T Sy = step_val<0, 1, 0>(o_y, c, cx, cy, cz, active && yp, nb, snap);
-  const T Sz = step_val<0, 0, 1>(o_z, c, cx, cy, cz, active && zp, nb, snap);
-  // backward neighbours and the edge points of the backward fluxes
-  const T Smx = step_val<-1, 0, 0>(o_x, c, cx, cy, cz, active && xm, nb, snap);
-  const T Smxy = step_val<-1, 1, 0>(o_xy, c, cx, cy, cz, active && xm && yp, nb, snap);
-  const T Smxz = step_val<-1, 0, 1>(o_xz, c, cx, cy, cz, active && xm && zp, nb, snap);
-  const T Smy = step_val<0, -1, 0>(o_y, c, cx, cy, cz, active && ym, nb, snap);
-  const T Smyx = step_val<1, -1, 0>(o_xy, c, cx, cy, cz, active && ym && xp, nb, snap);
-  const T Smyz = step_val<0, -1, 1>(o_yz, c, cx, cy, cz, active && ym && zp, nb, snap);
-  const T Smz = step_val<0, 0, -1>(o_z, c, cx, cy, cz, active && zm, nb, snap);
-  const T Smzx = step_val<1, 0, -1>(o_xz, c, cx, cy, cz, active && zm && xp, nb, snap);
-  const T Smzy = step_val<0, 1, -1>(o_yz, c, cx, cy, cz, active && zm && yp, nb, snap);
-
-#endif
 
   // flux at the cell (_kernels.pyx:205-220)
   const T gx = xp ? (Sx - S0) * ih : (T)0;
@@ -389,7 +275,7 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
     den += wv;
   };
   if (NV > 0) {
-    mbar_wait(s_bar_p, 0);
+    mbar_wait(&s_bar, 0);
     const int t = threadIdx.x;
     const float* sf = s_tile;
     if (BINW) {
@@ -458,17 +344,9 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
       atomicAdd(a.counters + 1, 1);
   }
   if (ENERGY) {
-#if OCTF_LEAF_WARPPART
-    double tot = eterm;  // fixed butterfly: deterministic
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(FULL, tot, o);
-    if ((threadIdx.x & 31) == 0)
-      a.epart[tile_id * kLeafParts + (threadIdx.x >> 5)] = tot;
-#else
     typedef cub::BlockReduce<double, kT> BR;
     __shared__ typename BR::TempStorage tmp;
     const double tot = BR(tmp).Sum(eterm);
     if (threadIdx.x == 0) a.epart[tile_id] = tot;
-#endif
   }
 }

@@ -516,30 +516,12 @@ __global__ void k_unmark(const int32_t* list, int64_t n, uint8_t* smark) {
 
 // ---------------------------------------------------------------------------
 // propagate (_kernels.pyx:80-113): inner = sequential f64 sum of children / 8
-template <typename T>
-__global__ void k_propagate_level(const int32_t* __restrict__ blocks,
-                                  int64_t nblk, const int32_t* __restrict__ child,
-                                  T* value) {
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t i = gid >> 3;
-  const int c = (int)(gid & 7);
-  if (i >= nblk) return;
-  const int32_t b = blocks[i];
-  if (b == 0 && c != 0) return;
-  const int32_t s = b + c;
-  const int32_t cb = child[s];
-  if (cb < 0) return;
-  double acc = 0.0;
-#pragma unroll
-  for (int q = 0; q < 8; ++q) acc += (double)value[cb + q];
-  value[s] = (T)(acc / 8.0);
-}
 
 // up to five fields at once, one thread per child block: the block's parent
 // slot comes from the context's bparent table, and with sector-aligned pools
 // (slot 1 on a 32 B / 64 B boundary, _device.py POOL_PAD) the eight children
 // are read with 16-byte vector loads.  Same sequential double sum as
-// k_propagate_level (_kernels.pyx:153-170 via numpy, oracle propagate).
+// the reference's propagate (_kernels.pyx:80-113, oracle propagate).
 template <typename T>
 struct FieldSet {
   T* v[5];
@@ -703,9 +685,7 @@ void ensure_prepared(Ctx& c, const int32_t* child, int64_t cap, int d_max,
 // grid of the leaf kernel (also the number of energy partials per pass)
 inline unsigned leaf_grid(const Ctx& c) { return blocks_for(c.nlb * 8); }
 // energy partials the leaf kernel writes per pass (kLeafParts per CTA)
-inline int64_t leaf_parts(const Ctx& c) {
-  return (int64_t)leaf_grid(c) * kLeafParts;
-}
+inline int64_t leaf_parts(const Ctx& c) { return (int64_t)leaf_grid(c); }
 
 template <typename T, bool FZ, bool BW, bool EN, int N>
 void launch_leaf(unsigned g, cudaStream_t st, const LeafArgs<T>& a) {
@@ -1032,58 +1012,6 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
                         std::chrono::steady_clock::now() - t_restr).count();
 }
 
-// the same sums, one thread per parent slot (8 lanes per parent block), so
-// a parent block's new values leave the SM together (whole-sector writes
-// instead of scattered 4 B stores from different CTAs)
-template <typename T, int NA, bool VEC>
-__global__ void __launch_bounds__(kT)
-    k_propagate_parents(const int32_t* __restrict__ blocks, int64_t nblk,
-                        const int32_t* __restrict__ child, FieldSet<T> f) {
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t i = gid >> 3;
-  const int c = (int)(gid & 7);
-  if (i >= nblk) return;
-  const int32_t b = __ldg(blocks + i);
-  if (b == 0 && c != 0) return;
-  const int32_t s = b + c;
-  const int32_t cb = __ldg(child + s);
-  if (cb < 0) return;
-#pragma unroll
-  for (int q = 0; q < NA; ++q) {
-    T x[8];
-    if (VEC) {
-      if (sizeof(T) == 4) {
-        const float4* p = reinterpret_cast<const float4*>(f.v[q] + cb);
-        const float4 lo = __ldcs(p), hi = __ldcs(p + 1);
-        x[0] = lo.x; x[1] = lo.y; x[2] = lo.z; x[3] = lo.w;
-        x[4] = hi.x; x[5] = hi.y; x[6] = hi.z; x[7] = hi.w;
-      } else {
-        const double2* p = reinterpret_cast<const double2*>(f.v[q] + cb);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const double2 d = __ldcs(p + k);
-          x[2 * k] = (T)d.x;
-          x[2 * k + 1] = (T)d.y;
-        }
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) x[k] = f.v[q][cb + k];
-    }
-    double acc = 0.0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) acc += (double)x[k];
-    f.v[q][s] = (T)(acc / 8.0);
-  }
-}
-
-// measured slower than one thread per child block (cfg5 step 3.77 vs 3.55
-// ms): off.  Writes cost whole 32 B sectors of the parents' blocks either
-// way (a level's parents are scattered over its blocks).
-#ifndef OCTF_PROP_PARENTS
-#define OCTF_PROP_PARENTS 0
-#endif
-
 // parent levels top .. 0 (default: every level above the finest) of `na`
 // fields; level L is filled from the child blocks listed at level L+1
 template <typename T>
@@ -1102,29 +1030,6 @@ void launch_propagate_multi(Ctx& c, T* const* vals, int na, cudaStream_t st,
     if (n == 0) continue;
     const int32_t* blk = c.lvl_blocks.p + c.lvl_off[L + 1];
     const unsigned g = blocks_for(n);
-#if OCTF_PROP_PARENTS
-    {
-      const int64_t np = c.lvl_cnt[L];   // parent blocks: level L
-      const int32_t* pb = c.lvl_blocks.p + c.lvl_off[L];
-      const unsigned gp = blocks_for(np * 8);
-      if (na == 1) {
-        if (vec) k_propagate_parents<T, 1, true><<<gp, kT, 0, st>>>(pb, np, c.child_key, fs);
-        else k_propagate_parents<T, 1, false><<<gp, kT, 0, st>>>(pb, np, c.child_key, fs);
-      } else if (na == 5) {
-        if (vec) k_propagate_parents<T, 5, true><<<gp, kT, 0, st>>>(pb, np, c.child_key, fs);
-        else k_propagate_parents<T, 5, false><<<gp, kT, 0, st>>>(pb, np, c.child_key, fs);
-      } else {
-        for (int q = 0; q < na; ++q) {
-          FieldSet<T> one{};
-          one.v[0] = vals[q];
-          k_propagate_parents<T, 1, false><<<gp, kT, 0, st>>>(pb, np, c.child_key, one);
-        }
-      }
-      OCTF_CUDA(cudaGetLastError());
-      ++c.launches;
-      continue;
-    }
-#endif
     if (na == 1) {
       if (vec) k_propagate_blocks<T, 1, true><<<g, kT, 0, st>>>(blk, n, c.bparent.p, fs);
       else k_propagate_blocks<T, 1, false><<<g, kT, 0, st>>>(blk, n, c.bparent.p, fs);

@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity-mode", action="store_true")
+    ap.add_argument("--e2e-iters", type=int, default=200,
+                    help="iterations of the e2e fuse() call (config: 200)")
     ap.add_argument("--no-pd", action="store_true")
     return ap.parse_args()
 
@@ -326,7 +328,9 @@ def run_pd_mode(views, u0, p, args, nleaves, peak):
 
 def run_e2e(views, u0, p, args):
     """Same metric through the public API with host inputs: pinned host
-    reference-layout pools -> fuse(K passes) -> final pool back on the host."""
+    reference-layout pools -> one fuse() call running the configuration's
+    whole schedule (BASELINE config 1: 200 iterations; --e2e-iters) -> final
+    pool back on the host.  Bytes per step = the call's copies / iterations."""
     import torch
     from paper_1608_07411_b200 import fusion, octree
 
@@ -341,7 +345,7 @@ def run_e2e(views, u0, p, args):
     h2d = sum(a.numel() * a.element_size() + b.numel() * b.element_size()
               + c.numel() * c.element_size() for a, b, c, _ in hv)
     h2d += sum(a.numel() * a.element_size() for a in hu[:2])
-    k = args.steps
+    k = args.e2e_iters
     pk = fusion.FusionParams(**{**p.__dict__, "iterations": k})
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
@@ -368,7 +372,8 @@ def run_e2e(views, u0, p, args):
             "ms_total": ms, "steps": k,
             "phases_ms": {"h2d": (w1 - w0) * 1e3, "fuse": (w2 - w1) * 1e3,
                           "d2h": (w3 - w2) * 1e3},
-            "api": "paper_1608_07411_b200.fusion.fuse on host (pinned) pools"}
+            "api": ("paper_1608_07411_b200.fusion.fuse on host (pinned) pools, "
+                    "the configuration's whole schedule in one call")}
 
 
 # ---------------------------------------------------------- CPU reference --

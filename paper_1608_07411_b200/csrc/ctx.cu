@@ -23,7 +23,23 @@ void check_cuda(cudaError_t e, const char* what) {
   }
 }
 
+// keep freed stream-ordered allocations cached in the default pool (once)
+static void pool_keep() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&dev) == cudaSuccess &&
+      cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  cudaGetLastError();
+}
+
 Ctx::Ctx() {
+  pool_keep();
   const char* fg = std::getenv("OCTF_FULL_GATHER");
   no_regather = fg && fg[0] == '1';
   const char* fe = std::getenv("OCTF_FORCE_ELL");  // tests: ELL from 33 views

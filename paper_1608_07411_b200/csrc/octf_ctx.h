@@ -61,8 +61,17 @@ struct DevBuf {
     n = o.n;
     o.n = tn;
   }
+  // Allocations come from the device's default stream-ordered pool on the
+  // legacy stream (kept cached: see pool_keep() in ctx.cu), so contexts
+  // created per fuse() call do not pay cudaMalloc/cudaFree each time.
+  // (a reallocation is rare: the device is synchronised first, so no
+  // kernel on any stream still uses the old block and the new one is ready
+  // for every stream)
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      cudaDeviceSynchronize();
+      cudaFreeAsync(p, cudaStreamLegacy);
+    }
     p = nullptr;
     n = 0;
   }
@@ -71,7 +80,9 @@ struct DevBuf {
     if (count <= n && p) return p;
     T* q = nullptr;
     size_t c = count > 2 * n ? count : 2 * n;
-    if (cudaMalloc((void**)&q, c * sizeof(T)) != cudaSuccess) {
+    if (cudaMallocAsync((void**)&q, c * sizeof(T), cudaStreamLegacy) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(cudaStreamLegacy) != cudaSuccess) {
       cudaGetLastError();
       throw Error(kENoMem, "device allocation failed");
     }
@@ -80,8 +91,8 @@ struct DevBuf {
                                  cudaMemcpyDeviceToDevice, st),
                  "grow_keep");
     if (p) {
-      cudaStreamSynchronize(st);
-      cudaFree(p);
+      cudaDeviceSynchronize();
+      cudaFreeAsync(p, cudaStreamLegacy);
     }
     p = q;
     n = c;
@@ -94,7 +105,8 @@ struct DevBuf {
     const size_t grown = p ? count + count / 8 : count;
     release();
     size_t c = grown ? grown : 1;
-    cudaError_t e = cudaMalloc((void**)&p, c * sizeof(T));
+    cudaError_t e = cudaMallocAsync((void**)&p, c * sizeof(T), cudaStreamLegacy);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(cudaStreamLegacy);
     if (e != cudaSuccess) {
       p = nullptr;
       cudaGetLastError();

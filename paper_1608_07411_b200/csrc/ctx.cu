@@ -171,11 +171,12 @@ __global__ void k_leaf_tables(const int32_t* __restrict__ child,
                               const uint64_t* __restrict__ bcoord,
                               const int32_t* __restrict__ bparent,
                               uint64_t* lkey, int4* lmeta, int32_t* lpar,
-                              int32_t* nbr) {
+                              int32_t* nbr, const int32_t* __restrict__ sel) {
   int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t i = gid / 12;
   int d = (int)(gid % 12);
   if (i >= nlb) return;
+  if (sel) i = sel[i];  // only the listed entries (incremental update)
   int32_t b = lblocks[i];
   if (b < 0) {  // hole of a patched list: no active slot
     if (d == 0) {
@@ -385,6 +386,40 @@ __global__ void k_list_mark(int32_t* lblocks, const int4* __restrict__ lmeta,
   }
 }
 
+// list entries whose tables must be recomputed after a patch: appended
+// ones, new holes, changed leaf masks, and entries whose neighbour refs went
+// stale -- a same-level block that was freed, or a coarser leaf that was
+// split or whose block was freed (a live block never moves, so every other
+// ref still answers the same root descent)
+__global__ void k_table_dirty(const int32_t* __restrict__ lblocks, int64_t n,
+                              int64_t nold, const uint8_t* __restrict__ oldmask,
+                              const int32_t* __restrict__ child,
+                              const int8_t* __restrict__ blevel,
+                              const int32_t* __restrict__ nbr, int32_t* out,
+                              int32_t* cnt) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t b = lblocks[i];
+  bool d = i >= nold;
+  if (!d) {
+    if (b < 0) {
+      d = oldmask[i] != 0;  // a hole since this patch
+    } else {
+      d = leaf_mask_of(child, b) != oldmask[i];
+      for (int k = 0; k < 12 && !d; ++k) {
+        const int32_t r = nbr[i * 12 + k];
+        if (r >= 0) {
+          d = blevel[block_id(r)] < 0;
+        } else if (r <= -2) {
+          const int32_t q = -r - 2;
+          d = blevel[block_id(q)] < 0 || child[q] >= 0;
+        }
+      }
+    }
+  }
+  if (d) out[atomicAdd(cnt, 1)] = (int32_t)i;
+}
+
 // live leaf blocks not in the list yet
 __global__ void k_list_new(const int32_t* __restrict__ blocks, int64_t total,
                            const int32_t* __restrict__ child,
@@ -415,8 +450,7 @@ __global__ void k_set_lpos(const int32_t* __restrict__ lblocks, int64_t n,
 }
 
 // per slot of the patched list: a leaf that was a leaf at the same position
-// keeps its samples; a new leaf is queued for k_gather_fresh; any other slot
-// is zeroed (as the full gather leaves non-leaf slots)
+// keeps its samples; a new leaf is queued for k_gather_fresh
 template <bool BINW>
 __global__ void k_sample_update(const int32_t* __restrict__ lblocks,
                                 const int4* __restrict__ lmeta, int64_t n,
@@ -447,13 +481,9 @@ __global__ void k_sample_update(const int32_t* __restrict__ lblocks,
   const int64_t s = i * 8 + c;
   if (now && !was) {
     fresh[atomicAdd(nfresh, 1)] = (int32_t)s;
-  } else if (!now && (was || i >= nold)) {
-    for (int v = 0; v < stride; ++v) {
-      F[samp_idx(s, v, stride)] = 0.f;
-      if (!BINW) W[samp_idx(s, v, stride)] = 0.f;
-    }
-    if (BINW) M[s] = 0u;
   }
+  // (slots that stopped being leaves keep stale samples: kernels read the
+  // samples of active leaves only)
 }
 
 // zero the store slots [from, to) (tile padding after the last entry)
@@ -544,13 +574,8 @@ __global__ void k_ell_update(const int32_t* __restrict__ lblocks,
   const bool was = i < nold && ((oldmask[i] >> c) & 1u);
   if (now && !was) {
     fresh[atomicAdd(nfresh, 1)] = (int32_t)gid;
-  } else if (!now && (was || i >= nold)) {
-    const int K = tileK[gid >> 8];
-    for (int r = 0; r < K; ++r) {
-      F[ell_idx(tileOff, gid, r)] = 0.f;
-      W[ell_idx(tileOff, gid, r)] = 0.f;
-    }
   }
+  // (no zeroing: only active leaves' rows are ever read)
 }
 
 // one warp per queued leaf: views over lanes, observed ones compacted in
@@ -636,28 +661,39 @@ __global__ void k_ell_move(const int32_t* __restrict__ tiles,
 }
 
 // ---- ELL sample store (views > 32) ----
-// observed views of every active leaf slot of the list
-__global__ void k_ell_count(const int32_t* __restrict__ ucs,
-                            const int32_t* __restrict__ lblocks, int64_t nlb,
-                            const uint64_t* __restrict__ lkey, ViewSet vs,
-                            int32_t* cnt, int64_t slot0, int64_t slot1) {
-  const int64_t gid = slot0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t i = gid >> 3;
-  const int c = (int)(gid & 7);
-  if (gid >= slot1 || i >= nlb) return;
-  int32_t b = lblocks[i];
-  const bool active = b >= 0 && !(b == 0 && c != 0) && ucs[b + c] < 0;
-  int k = 0;
-  if (active) {
-    int L, px, py, pz;
-    unpack_cell(lkey[i], L, px, py, pz);
-    const int x = b == 0 ? 0 : 2 * px + ((c >> 2) & 1);
-    const int y = b == 0 ? 0 : 2 * py + ((c >> 1) & 1);
-    const int z = b == 0 ? 0 : 2 * pz + (c & 1);
-    for (int v = 0; v < vs.n; ++v)
-      k += vs.w[v][descend(vs.child[v], L, x, y, z)] != 0.f;
+
+// k_ell_count for a few slots (tiles appended by a list patch): one warp
+// per slot, views over lanes
+__global__ void k_ell_count_warp(const int32_t* __restrict__ ucs,
+                                 const int32_t* __restrict__ lblocks,
+                                 int64_t nlb, const uint64_t* __restrict__ lkey,
+                                 ViewSet vs, int32_t* cnt, int64_t slot0,
+                                 int64_t slot1) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t s = slot0 + (int64_t)blockIdx.x * (blockDim.x >> 5) +
+                   (threadIdx.x >> 5);
+       s < slot1; s += nw) {
+    const int64_t i = s >> 3;
+    const int c = (int)(s & 7);
+    const int32_t b = i < nlb ? lblocks[i] : -1;
+    const bool active = b >= 0 && !(b == 0 && c != 0) && ucs[b + c] < 0;
+    int k = 0;
+    if (active) {
+      int L, px, py, pz;
+      unpack_cell(lkey[i], L, px, py, pz);
+      const int x = b == 0 ? 0 : 2 * px + ((c >> 2) & 1);
+      const int y = b == 0 ? 0 : 2 * py + ((c >> 1) & 1);
+      const int z = b == 0 ? 0 : 2 * pz + (c & 1);
+      for (int v0 = 0; v0 < vs.n; v0 += 32) {
+        const int v = v0 + lane;
+        bool on = false;
+        if (v < vs.n) on = vs.w[v][descend(vs.child[v], L, x, y, z)] != 0.f;
+        k += __popc(__ballot_sync(0xffffffffu, on));
+      }
+    }
+    if (lane == 0) cnt[s] = k;
   }
-  cnt[gid] = k;
 }
 
 // per tile: rows = max count of its 256 slots (one CTA of 256 per tile)
@@ -890,7 +926,7 @@ void ctx_list_full(Ctx& c, const int32_t* child, int64_t total, int64_t nbid,
   c.nbr.ensure(c.nlb * 12);
   k_leaf_tables<<<grid_for(c.nlb * 12), kThreads, 0, st>>>(
       child, c.lblocks.p, c.nlb, c.blevel.p, c.bcoord.p, c.bparent.p,
-      c.lkey.p, c.lmeta.p, c.lpar.p, c.nbr.p);
+      c.lkey.p, c.lmeta.p, c.lpar.p, c.nbr.p, nullptr);
   OCTF_CUDA(cudaGetLastError());
   c.lpos.ensure(nbid);
   OCTF_CUDA(cudaMemsetAsync(c.lpos.p, 0xff, nbid * sizeof(int32_t), st));
@@ -921,7 +957,7 @@ static bool ell_list_samples(Ctx& c, int64_t nold, int64_t nnew,
     // counts for the new tiles' slots (the list tables are current)
     const int64_t s0 = nt_old * 256, s1 = nnew * 8;
     if (s1 > s0)
-      k_ell_count<<<grid_for(s1 - s0), kThreads, 0, st>>>(
+      k_ell_count_warp<<<148 * 8, kThreads, 0, st>>>(
           c.child_key, c.lblocks.p, nnew, c.lkey.p, ctx_views(c), cnt, s0, s1);
     int64_t* rowsz =
         reinterpret_cast<int64_t*>(c.sort_k64.ensure(nt_new - nt_old + 1));
@@ -1078,13 +1114,24 @@ bool ctx_list_update(Ctx& c, const int32_t* child, int64_t total, int64_t nbid,
                                                    c.lpos.p);
     OCTF_CUDA(cudaGetLastError());
   }
-  c.lkey.ensure(nnew);
-  c.lmeta.ensure(nnew);
-  c.lpar.ensure(nnew);
-  c.nbr.ensure(nnew * 12);
-  k_leaf_tables<<<grid_for(nnew * 12), kThreads, 0, st>>>(
-      child, c.lblocks.p, nnew, c.blevel.p, c.bcoord.p, c.bparent.p, c.lkey.p,
-      c.lmeta.p, c.lpar.p, c.nbr.p);
+  c.lkey.grow_keep(nnew, nold, st);
+  c.lmeta.grow_keep(nnew, nold, st);
+  c.lpar.grow_keep(nnew, nold, st);
+  c.nbr.grow_keep(nnew * 12, nold * 12, st);
+  // tables only for the entries the patch touched (k_table_dirty)
+  int32_t* dirty = c.split_list.ensure(nnew + 1);
+  OCTF_CUDA(cudaMemsetAsync(c.counters.p + 6, 0, sizeof(int32_t), st));
+  k_table_dirty<<<grid_for(nnew), kThreads, 0, st>>>(
+      c.lblocks.p, nnew, nold, oldmask, child, c.blevel.p, c.nbr.p, dirty,
+      c.counters.p + 6);
+  int32_t ndirty = 0;
+  OCTF_CUDA(cudaMemcpyAsync(&ndirty, c.counters.p + 6, sizeof(int32_t),
+                            cudaMemcpyDeviceToHost, st));
+  OCTF_CUDA(cudaStreamSynchronize(st));
+  if (ndirty)
+    k_leaf_tables<<<grid_for((int64_t)ndirty * 12), kThreads, 0, st>>>(
+        child, c.lblocks.p, ndirty, c.blevel.p, c.bcoord.p, c.bparent.p,
+        c.lkey.p, c.lmeta.p, c.lpar.p, c.nbr.p, dirty);
   OCTF_CUDA(cudaGetLastError());
   if (c.ell) return ell_list_samples(c, nold, nnew, oldmask, t0, st);
   // samples, in place (the store only grows; its tail is zeroed)

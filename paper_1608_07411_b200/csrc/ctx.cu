@@ -44,6 +44,8 @@ Ctx::Ctx() {
   no_regather = fg && fg[0] == '1';
   const char* fe = std::getenv("OCTF_FORCE_ELL");  // tests: ELL from 33 views
   force_ell = fe && fe[0] == '1';
+  const char* fp = std::getenv("OCTF_NO_FUSED_PARENT");  // A/B switch
+  fuse_off = fp && fp[0] == '1';
   OCTF_CUDA(cudaMallocHost((void**)&h_counters, 64 * sizeof(int32_t)));
   OCTF_CUDA(cudaMallocHost((void**)&h_scalar, 8 * sizeof(double)));
 }

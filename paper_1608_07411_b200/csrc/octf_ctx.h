@@ -135,6 +135,7 @@ struct Ctx {
   std::vector<int64_t> lvl_off, lvl_cnt;  // per level ranges in lvl_blocks
   DevBuf<int32_t> lvl_blocks;             // live block bases, level-major
   int64_t nblocks = 0;
+  bool fuse_off = false;  // env OCTF_NO_FUSED_PARENT=1: pd bottom level apart
   DevBuf<int32_t> lblocks;    // blocks holding >= 1 leaf, ascending base
   DevBuf<uint64_t> lkey;      // per leaf block: packed (level, parent cell)
   DevBuf<int4> lmeta;         // per leaf block: {base, px, py, pz|mask|L}

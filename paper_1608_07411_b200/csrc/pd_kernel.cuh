@@ -49,6 +49,7 @@ struct PdArgs {
   T lam, tl, sl, tau, gamma;  // tl = tau*lam, sl = sigma*lam
   int clamp;
   double* epart;
+  const int32_t* __restrict__ lpar;  // parent slot of each leaf block
 };
 
 template <typename T>
@@ -221,7 +222,9 @@ constexpr size_t pd_smem_bytes(int nv, bool binw) {
                : (nv > 32 ? 0 : (size_t)nv * kTileLeaves * 4));
 }
 
-template <typename T, bool BINW, int NV>
+// WP: also write the bottom propagate level of the five fields (frozen
+// passes over a full leaf-block list)
+template <typename T, bool BINW, int NV, bool WP = false>
 __global__ void __launch_bounds__(kT, pd_minb(BINW, NV)) k_pd_pass(PdArgs<T> a) {
   static_assert(NV > 0 && (NV & (NV - 1)) == 0, "NV: power of two");
   // NV = 64: general weights selected without sorting them (WeightAt)
@@ -269,6 +272,9 @@ __global__ void __launch_bounds__(kT, pd_minb(BINW, NV)) k_pd_pass(PdArgs<T> a) 
   const bool xp = x + 1 < m, yp = y + 1 < m, zp = z + 1 < m;
   const bool xm = x > 0, ym = y > 0, zm = z > 0;
 
+  const int32_t par_blk =
+      (WP && c == 0 && inrange && lmask == 0xffu && L == a.d_max)
+          ? __ldg(a.lpar + i) : -1;
   const T U0 = slot_ok ? a.u[s] : (T)0;
   const T B0 = slot_ok ? a.ub[s] : (T)0;
   const T P0 = slot_ok ? a.px[s] : (T)0;
@@ -423,9 +429,10 @@ __global__ void __launch_bounds__(kT, pd_minb(BINW, NV)) k_pd_pass(PdArgs<T> a) 
   T res = res0;
   if (a.clamp) res = clamp1(res);
   double eterm = 0.0;
+  const T ubv = (T)2 * res - U0;
   if (active) {
     a.u_o[s] = res;
-    a.ub_o[s] = (T)2 * res - U0;
+    a.ub_o[s] = ubv;
     a.px_o[s] = D0;
     a.py_o[s] = D1;
     a.pz_o[s] = D2;
@@ -436,8 +443,37 @@ __global__ void __launch_bounds__(kT, pd_minb(BINW, NV)) k_pd_pass(PdArgs<T> a) 
     const T h = pow2<T>(a.d_max - L);
     eterm = (double)((num / den + tv) * (h * h * h));
   }
+  // the bottom propagate level of the five fields for the CTA's finest-level
+  // blocks (as k_leaf_pass): staged in shared memory, summed after the
+  // energy reduction's barrier by one thread per block
+  __shared__ T s_v[WP ? 5 : 1][WP ? kT : 1];
+  __shared__ int32_t s_par[WP ? kT / 8 : 1];
+  if (WP) {
+    s_v[0][t] = res;
+    s_v[1][t] = ubv;
+    s_v[2][t] = D0;
+    s_v[3][t] = D1;
+    s_v[4][t] = D2;
+    if (c == 0) s_par[t >> 3] = par_blk;
+  }
   typedef cub::BlockReduce<double, kT> BR;
   __shared__ typename BR::TempStorage tmp;
   const double tot = BR(tmp).Sum(eterm);
   if (threadIdx.x == 0) a.epart[blockIdx.x] = tot;
+  if (WP && t < kT / 8) {
+    const int32_t par = s_par[t];
+    if (par >= 0) {
+      auto mean8 = [&](int q) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc += (double)s_v[q][t * 8 + k];
+        return (T)(acc / 8.0);
+      };
+      a.u_o[par] = mean8(0);
+      a.ub_o[par] = mean8(1);
+      a.px_o[par] = mean8(2);
+      a.py_o[par] = mean8(3);
+      a.pz_o[par] = mean8(4);
+    }
+  }
 }

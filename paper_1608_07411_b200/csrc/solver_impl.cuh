@@ -711,7 +711,6 @@ void launch_leaf_pass(Ctx& c, const T* snap, T* uval, const int32_t* child,
   LeafArgs<T> a;
   a.tile0 = tile0;
   a.lpar = c.lpar.p;
-  a.write_parent = write_parent;
   a.lblocks = c.lblocks.p;
   a.nlb = c.nlb;
   a.lkey = c.lkey.p;
@@ -1139,8 +1138,9 @@ void frozen_passes_impl(Ctx& c, FrozenArgs& a, cudaStream_t st) {
       const T* snap = (const T*)a.ubuf[k & 1];
       T* uval = (T*)a.ubuf[(k + 1) & 1];
       if (c.timing) OCTF_CUDA(cudaEventRecord(c.pev[2 * j], st));
-      // (writing the parents of all-leaf blocks from this kernel was tried:
-      // the extra registers cost more than the propagate level it saves)
+      // (the bottom propagate level fused into this kernel, as the
+      // primal-dual kernel does for its five fields, was measured slower
+      // here: leaf kernel 0.306 -> 0.332 ms on cfg2 for a 17 us launch)
       launch_leaf_pass<T>(c, snap, uval, a.child, lp, true,
                           c.partials.p + (size_t)j * g, st, false);
       if (c.timing) OCTF_CUDA(cudaEventRecord(c.pev[2 * j + 1], st));
@@ -1171,19 +1171,23 @@ void frozen_passes_impl(Ctx& c, FrozenArgs& a, cudaStream_t st) {
 template <typename T>
 void pd_passes_impl(Ctx& c, PdHostArgs& a, cudaStream_t st);
 
-template <typename T, bool BW, int N>
-void launch_pd(unsigned g, cudaStream_t st, const PdArgs<T>& p) {
+template <typename T, bool BW, int N, bool WP>
+void launch_pd_wp(unsigned g, cudaStream_t st, const PdArgs<T>& p) {
   constexpr size_t smem = pd_smem_bytes(N, BW);
   static bool attr = false;  // opt in to > 48 KiB of dynamic shared memory
   if (smem > 48 * 1024 && !attr) {
-    OCTF_CUDA(cudaFuncSetAttribute(k_pd_pass<T, BW, N>,
+    OCTF_CUDA(cudaFuncSetAttribute(k_pd_pass<T, BW, N, WP>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
     attr = true;
   }
-  k_pd_pass<T, BW, N><<<g, kT, smem, st>>>(p);
+  k_pd_pass<T, BW, N, WP><<<g, kT, smem, st>>>(p);
 }
-
+template <typename T, bool BW, int N>
+void launch_pd(unsigned g, cudaStream_t st, const PdArgs<T>& p, bool wp) {
+  if (wp) launch_pd_wp<T, BW, N, true>(g, st, p);
+  else launch_pd_wp<T, BW, N, false>(g, st, p);
+}
 template <typename T>
 void pd_passes_impl(Ctx& c, PdHostArgs& a, cudaStream_t st) {
   if (a.d_max < 0 || a.d_max > kMaxDepth)
@@ -1201,6 +1205,7 @@ void pd_passes_impl(Ctx& c, PdHostArgs& a, cudaStream_t st) {
   const unsigned g = leaf_grid(c);
   c.partials.ensure((size_t)g * kChunk);
   c.dscalar.ensure(a.npasses > 1024 ? a.npasses : 1024);
+  const bool fused_bottom = c.list_full && !c.fuse_off && a.d_max >= 1;
   for (int k0 = 0; k0 < a.npasses; k0 += kChunk) {
     const int nk = a.npasses - k0 < kChunk ? a.npasses - k0 : kChunk;
     for (int j = 0; j < nk; ++j) {
@@ -1235,9 +1240,10 @@ void pd_passes_impl(Ctx& c, PdHostArgs& a, cudaStream_t st) {
       p.gamma = (T)a.gamma;
       p.clamp = a.clamp;
       p.epart = c.partials.p + (size_t)j * g;
+      p.lpar = c.lpar.p;
       if (c.timing && (int)c.pev.size() >= 2 * kChunk)
         OCTF_CUDA(cudaEventRecord(c.pev[2 * j], st));
-#define OCTF_PD(BW, N) launch_pd<T, BW, N>(g, st, p)
+#define OCTF_PD(BW, N) launch_pd<T, BW, N>(g, st, p, fused_bottom)
       if (c.binw) {
         if (nv == 4) OCTF_PD(true, 4); else if (nv == 8) OCTF_PD(true, 8);
         else if (nv == 16) OCTF_PD(true, 16); else OCTF_PD(true, 32);
@@ -1251,7 +1257,10 @@ void pd_passes_impl(Ctx& c, PdHostArgs& a, cudaStream_t st) {
       ++c.launches;
       if (c.timing && (int)c.pev.size() >= 2 * kChunk)
         OCTF_CUDA(cudaEventRecord(c.pev[2 * j + 1], st));
-      launch_propagate_multi<T>(c, (T* const*)out, 5, st);
+      if (!fused_bottom)
+        launch_propagate_multi<T>(c, (T* const*)out, 5, st);
+      else if (a.d_max >= 2)
+        launch_propagate_multi<T>(c, (T* const*)out, 5, st, a.d_max - 2);
     }
     sum_partials(c, c.partials.p, g, nk, c.dscalar.p + k0, st);
     if (c.timing && (int)c.pev.size() >= 2 * kChunk) {

@@ -79,3 +79,27 @@ def test_samples_path_equals_view_path(cfg5_small):
     b = fusion.fuse(u0, None, p, samples=samples,
                     precision="fp32").field.to_host().value
     assert np.array_equal(a, b)
+
+
+def test_fused_propagate_equals_per_level(cfg5_small, monkeypatch):
+    """The primal-dual kernel's fused bottom propagate level (five fields)
+    gives the per-level launches' pools bit for bit (fp32 and fp64, every
+    field including inner nodes)."""
+    from paper_1608_07411_b200 import fusion
+    u0, samples, _, _, _ = cfg5_small
+    p = fusion.FusionParams(iterations=3, tau=-1.0, tau_split=0.0,
+                            tau_join=1.5, lam=0.3)
+
+    def run():
+        out = []
+        for prec in ("fp32", "fp64"):
+            s = fusion.PDSolver(u0, None, p, precision=prec, samples=samples)
+            s.run(0, 3)
+            out += [t.cpu().numpy() for t in s.state]
+        return out
+
+    fused = run()
+    monkeypatch.setenv("OCTF_NO_FUSED_PARENT", "1")
+    plain = run()
+    for a, b in zip(fused, plain):
+        assert np.array_equal(a, b)

@@ -87,7 +87,12 @@ int octf_ctx_profile(octf_ctx *ctx, int enable, double *out);
 /* Host-side phase times since the last octf_ctx_profile call (which resets
  * them; recorded only while profiling is enabled): out[0..4] = {context
  * rebuild ms (incl. gathers), rebuilds, sample gather ms, gathers,
- * restructuring ms after the leaf kernel (events, cascade, joins, sweep)}. */
+ * restructuring ms after the leaf kernel (events, cascade, joins, sweep)},
+ * out[5..18] = phases (only with env OCTF_PHASES=1: each mark synchronises
+ * the stream): rebuild -- level walk, list diff, tables, ELL grow, ELL
+ * update, new-leaf gather, ELL tile moves, full list rebuild, full gather,
+ * rest -- and restructuring -- split cascade, split allocation, joins,
+ * sweep.  out holds 19 doubles. */
 int octf_ctx_phases(octf_ctx *ctx, double *out);
 
 /* _kernels.pyx:384-461 iterate_pass -- one Jacobi descent pass with the

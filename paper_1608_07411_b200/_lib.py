@@ -117,6 +117,12 @@ def ptr_table(ptrs):
     return (ctypes.c_void_p * max(len(ptrs), 1))(*ptrs)
 
 
+# context rebuild phases (octf_ctx.h Phase), in export order
+PHASES = ("walk", "list_diff", "tables", "ell_grow", "ell_update", "fresh",
+          "move", "full_list", "full_gather", "tail", "split_cascade",
+          "split_alloc", "joins", "sweep")
+
+
 class Ctx:
     """Owning handle of an ``octf_ctx`` (solver acceleration structures)."""
 
@@ -147,7 +153,7 @@ class Ctx:
     def profile(self, enable: bool = True) -> dict:
         """Read and reset the live kernel timers; (re)arm them if enable."""
         import numpy as np
-        ph = np.zeros(5, dtype=np.float64)
+        ph = np.zeros(5 + len(PHASES), dtype=np.float64)
         call("octf_ctx_phases", self.h, ph.ctypes.data)  # before the reset
         out = np.zeros(5, dtype=np.float64)
         call("octf_ctx_profile", self.h, int(bool(enable)), out.ctypes.data)
@@ -156,7 +162,9 @@ class Ctx:
                 "launches": int(out[4]),
                 "prepare_ms": float(ph[0]), "prepares": int(ph[1]),
                 "gather_ms": float(ph[2]), "gathers": int(ph[3]),
-                "restructure_ms": float(ph[4])}
+                "restructure_ms": float(ph[4]),
+                "rebuild_phases_ms": {k: float(v)
+                                      for k, v in zip(PHASES, ph[5:])}}
 
     def close(self):
         if self.h:

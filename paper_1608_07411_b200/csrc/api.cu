@@ -200,6 +200,7 @@ int octf_ctx_profile(octf_ctx* ctx, int enable, double* out) {
     c.t_leaf_ms = c.t_energy_ms = 0;
     c.n_leaf = c.n_energy = c.launches = 0;
     c.t_prep_ms = c.t_gather_ms = c.t_restr_ms = 0;
+    for (double& t : c.t_ph) t = 0;
     c.n_prep = c.n_gather = 0;
     c.timing = enable != 0;
   });
@@ -214,6 +215,7 @@ int octf_ctx_phases(octf_ctx* ctx, double* out) {
     out[2] = c.t_gather_ms;
     out[3] = (double)c.n_gather;
     out[4] = c.t_restr_ms;
+    for (int k = 0; k < octf::kPhCount; ++k) out[5 + k] = c.t_ph[k];
   });
 }
 

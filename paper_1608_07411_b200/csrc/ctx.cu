@@ -44,6 +44,8 @@ Ctx::Ctx() {
   no_regather = fg && fg[0] == '1';
   const char* fe = std::getenv("OCTF_FORCE_ELL");  // tests: ELL from 33 views
   force_ell = fe && fe[0] == '1';
+  const char* pm = std::getenv("OCTF_PHASES");  // rebuild phase marks
+  phase_marks = pm && pm[0] == '1';
   const char* fp = std::getenv("OCTF_NO_FUSED_PARENT");  // A/B switch
   fuse_off = fp && fp[0] == '1';
   OCTF_CUDA(cudaMallocHost((void**)&h_counters, 64 * sizeof(int32_t)));
@@ -112,56 +114,73 @@ __global__ void k_expand(const int32_t* __restrict__ child,
 
 // k_expand without a host round trip per level: the level's range comes
 // from device counters (dcnt, doff), the next level's start is written by
-// thread 0; the grid is an upper bound of the level's size
+// thread 0; a fixed grid strides over the level (its size is only known on
+// the device)
 __global__ void k_expand_dev(const int32_t* __restrict__ child,
                              int32_t* lvl_blocks, int L, int64_t used,
                              int64_t cap_blocks, int8_t* blevel,
                              uint64_t* bcoord, int32_t* bparent, int32_t* dcnt,
                              int32_t* doff, int32_t* bad) {
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = dcnt[L];
   const int64_t next = (int64_t)doff[L] + n;
-  if (gid == 0) doff[L + 1] = (int32_t)next;
-  const int64_t i = gid >> 3;
-  const int c = (int)(gid & 7);
-  if (i >= n) return;
-  const int32_t b = lvl_blocks[doff[L] + i];
-  if (b == 0 && c != 0) return;
-  const int32_t s = b + c;
-  const int32_t nb = child[s];
-  if (nb < 0) return;
-  if (nb + 8 > used || (nb & 7) != 1) {
-    atomicExch(bad, 1);
-    return;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid == 0) doff[L + 1] = (int32_t)next;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t gid = tid; gid < n * 8; gid += stride) {
+    const int64_t i = gid >> 3;
+    const int c = (int)(gid & 7);
+    const int32_t b = lvl_blocks[doff[L] + i];
+    if (b == 0 && c != 0) continue;
+    const int32_t s = b + c;
+    const int32_t nb = child[s];
+    if (nb < 0) continue;
+    if (nb + 8 > used || (nb & 7) != 1) {
+      atomicExch(bad, 1);
+      continue;
+    }
+    int x, y, z;
+    slot_cell(b, c, bcoord[block_id(b)], x, y, z);
+    const int k = block_id(nb);
+    blevel[k] = (int8_t)(L + 1);
+    bcoord[k] = pack_cell(L, x, y, z);
+    bparent[k] = s;
+    const int64_t pos = next + atomicAdd(dcnt + L + 1, 1);
+    if (pos >= cap_blocks) {
+      atomicExch(bad, 1);
+      continue;
+    }
+    lvl_blocks[pos] = nb;
   }
-  int x, y, z;
-  slot_cell(b, c, bcoord[block_id(b)], x, y, z);
-  const int k = block_id(nb);
-  blevel[k] = (int8_t)(L + 1);
-  bcoord[k] = pack_cell(L, x, y, z);
-  bparent[k] = s;
-  const int64_t pos = next + atomicAdd(dcnt + L + 1, 1);
-  if (pos >= cap_blocks) {
-    atomicExch(bad, 1);
-    return;
-  }
-  lvl_blocks[pos] = nb;
+}
+
+// add a per-thread count to a global counter with one atomic per CTA
+// (per-warp atomics on one address serialised in L2: ~0.2 ms for the 250k
+// warps of a 7M-leaf list).  Every thread of the CTA must call it.
+__device__ __forceinline__ void cta_count_add(int cnt, int32_t* global) {
+  __shared__ int s_cnt;
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd_block(&s_cnt, cnt);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_cnt) atomicAdd(global, s_cnt);
 }
 
 __global__ void k_leaf_flags(const int32_t* __restrict__ child,
                              const int32_t* __restrict__ blocks, int64_t nblk,
                              uint8_t* flags, int32_t* nleaves) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nblk) return;
-  int32_t b = blocks[i];
   int n = 0;
-  if (b == 0) {
-    n = child[0] < 0;
-  } else {
-    for (int c = 0; c < 8; ++c) n += child[b + c] < 0;
+  if (i < nblk) {
+    const int32_t b = blocks[i];
+    if (b == 0) {
+      n = child[0] < 0;
+    } else {
+      for (int c = 0; c < 8; ++c) n += child[b + c] < 0;
+    }
+    flags[i] = n > 0;
   }
-  flags[i] = n > 0;
-  if (n) atomicAdd(nleaves, n);
+  cta_count_add(n, nleaves);
 }
 
 // per leaf block: packed (level, parent cell) and the 12 neighbour refs.
@@ -471,12 +490,7 @@ __global__ void k_sample_update(const int32_t* __restrict__ lblocks,
     int pz, L;
     unpack_meta_w(lmeta[i].w, pz, nm, L);
   }
-  {  // leaf count: one atomic per warp (every lane reaches the shuffle)
-    int cnt = (c == 0) ? __popc(nm) : 0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(nleaves, cnt);
-  }
+  cta_count_add((c == 0) ? __popc(nm) : 0, nleaves);  // every thread
   if (!in) return;
   const bool now = b >= 0 && !(b == 0 && c != 0) && ((nm >> c) & 1u);
   const bool was = i < nold && ((oldmask[i] >> c) & 1u);
@@ -565,12 +579,7 @@ __global__ void k_ell_update(const int32_t* __restrict__ lblocks,
     int pz, L;
     unpack_meta_w(lmeta[i].w, pz, nm, L);
   }
-  {
-    int cnt = (c == 0) ? __popc(nm) : 0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(nleaves, cnt);
-  }
+  cta_count_add((c == 0) ? __popc(nm) : 0, nleaves);  // every thread
   if (!in) return;
   const bool now = b >= 0 && !(b == 0 && c != 0) && ((nm >> c) & 1u);
   const bool was = i < nold && ((oldmask[i] >> c) & 1u);
@@ -581,13 +590,18 @@ __global__ void k_ell_update(const int32_t* __restrict__ lblocks,
 }
 
 // one warp per queued leaf: views over lanes, observed ones compacted in
-// view order by ballot; more than the tile's rows flags an overflow
+// view order by ballot; more than the tile's rows flags an overflow and
+// queues the leaf in `redo` (the second attempt after the tile moves gathers
+// only those).  The view-tree node of each view is found once (root
+// descent) and kept in registers for the first 512 views.
+constexpr int kFreshChunks = 16;
 __global__ void k_ell_fresh(const int32_t* __restrict__ fresh,
                             const int32_t* __restrict__ nfresh,
                             const int4* __restrict__ lmeta, ViewSet vs,
                             const int32_t* __restrict__ tileK,
                             const int64_t* __restrict__ tileOff, float* F,
-                            float* W, int32_t* overflow, int32_t* need) {
+                            float* W, int32_t* overflow, int32_t* need,
+                            int32_t* redo, int32_t* nredo) {
   const int lane = threadIdx.x & 31;
   const int nw = (int)(gridDim.x * (blockDim.x >> 5));
   const int n = *nfresh;
@@ -604,9 +618,23 @@ __global__ void k_ell_fresh(const int32_t* __restrict__ fresh,
     const int y = b == 0 ? 0 : 2 * m.z + ((c >> 1) & 1);
     const int z = b == 0 ? 0 : 2 * pz + (c & 1);
     const int K = tileK[s >> 8];
+    int32_t nd[kFreshChunks];
     int j = 0;
     // count first: a leaf that does not fit leaves its tile untouched
-    for (int v0 = 0; v0 < vs.n; v0 += 32) {
+#pragma unroll
+    for (int q = 0; q < kFreshChunks; ++q) {
+      const int v = q * 32 + lane;
+      nd[q] = -1;
+      if (q * 32 < vs.n) {
+        bool on = false;
+        if (v < vs.n) {
+          nd[q] = descend(vs.child[v], L, x, y, z);
+          on = vs.w[v][nd[q]] != 0.f;
+        }
+        j += __popc(__ballot_sync(0xffffffffu, on));
+      }
+    }
+    for (int v0 = kFreshChunks * 32; v0 < vs.n; v0 += 32) {
       const int v = v0 + lane;
       bool on = false;
       if (v < vs.n) on = vs.w[v][descend(vs.child[v], L, x, y, z)] != 0.f;
@@ -616,17 +644,16 @@ __global__ void k_ell_fresh(const int32_t* __restrict__ fresh,
       if (lane == 0) {
         atomicExch(overflow, 1);
         atomicMax(need + (s >> 8), j);
+        if (redo) redo[atomicAdd(nredo, 1)] = (int32_t)s;
       }
       continue;
     }
     j = 0;
-    for (int v0 = 0; v0 < vs.n; v0 += 32) {
-      const int v = v0 + lane;
+    auto put = [&](int v, int32_t node) {
       float f = 0.f, w = 0.f;
       if (v < vs.n) {
-        const int32_t nd = descend(vs.child[v], L, x, y, z);
-        f = vs.val[v][nd];
-        w = vs.w[v][nd];
+        f = vs.val[v][node];
+        w = vs.w[v][node];
       }
       const unsigned on = __ballot_sync(0xffffffffu, w != 0.f);
       const int r = j + __popc(on & ((1u << lane) - 1u));
@@ -635,6 +662,13 @@ __global__ void k_ell_fresh(const int32_t* __restrict__ fresh,
         W[ell_idx(tileOff, s, r)] = w;
       }
       j += __popc(on);
+    };
+#pragma unroll
+    for (int q = 0; q < kFreshChunks; ++q)
+      if (q * 32 < vs.n) put(q * 32 + lane, nd[q]);
+    for (int v0 = kFreshChunks * 32; v0 < vs.n; v0 += 32) {
+      const int v = v0 + lane;
+      put(v, v < vs.n ? descend(vs.child[v], L, x, y, z) : 0);
     }
     for (int r = j + lane; r < K; r += 32) {
       F[ell_idx(tileOff, s, r)] = 0.f;
@@ -643,22 +677,46 @@ __global__ void k_ell_fresh(const int32_t* __restrict__ fresh,
   }
 }
 
-// move overflowing tiles to bigger row ranges at the end of the store:
-// their rows copied, the new rows zeroed (one CTA per moved tile)
-__global__ void k_ell_move(const int32_t* __restrict__ tiles,
-                           const int32_t* __restrict__ oldK,
-                           const int64_t* __restrict__ oldOff,
-                           const int32_t* __restrict__ newK,
-                           const int64_t* __restrict__ newOff, float* F,
-                           float* W) {
-  const int j = blockIdx.x;
-  const int64_t o0 = oldOff[j], o1 = newOff[j];
-  const int k0 = oldK[j], k1 = newK[j];
-  (void)tiles;
+// device-side move plan: rows of the bigger range of each overflowing tile
+// (need + need/4 + 4 rows, as before), 0 for the others; rows[nt] = 0 for
+// the scan; rows[nt + 1] accumulates the abandoned rows (ell_waste)
+__global__ void k_ell_plan(const int32_t* __restrict__ need,
+                           const int32_t* __restrict__ tileK, int64_t nt,
+                           int64_t* rows) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > nt) return;
+  if (t == nt) {
+    rows[nt] = 0;
+    return;
+  }
+  const int nd = need[t], k0 = tileK[t];
+  const bool mv = nd > k0;
+  rows[t] = mv ? (int64_t)(nd + nd / 4 + 4) * 256 : 0;
+  if (mv)
+    atomicAdd(reinterpret_cast<unsigned long long*>(rows + nt + 1),
+              (unsigned long long)k0 * 256);
+}
+
+// one CTA per tile: an overflowing tile's rows move to [total + scan[t],
+// ...) with the new rows zeroed, then its K and offset are switched
+__global__ void k_ell_move_dev(const int32_t* __restrict__ need,
+                               int32_t* tileK, int64_t* tileOff,
+                               const int64_t* __restrict__ scan, int64_t total,
+                               float* F, float* W) {
+  const int64_t t = blockIdx.x;
+  const int nd = need[t], k0 = tileK[t];
+  if (nd <= k0) return;
+  const int k1 = nd + nd / 4 + 4;
+  const int64_t o0 = tileOff[t], o1 = total + scan[t];
   for (int64_t e = threadIdx.x; e < (int64_t)k1 * 256; e += blockDim.x) {
     const bool keep = e < (int64_t)k0 * 256;
     F[o1 + e] = keep ? F[o0 + e] : 0.f;
     W[o1 + e] = keep ? W[o0 + e] : 0.f;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tileK[t] = k1;
+    tileOff[t] = o1;
   }
 }
 
@@ -802,9 +860,24 @@ void ctx_free_stack(Ctx& c, const int32_t* child, const int64_t* state,
   c.nfree = n;
 }
 
+void ph_start(Ctx& c, cudaStream_t st) {
+  if (!c.timing || !c.phase_marks) return;
+  OCTF_CUDA(cudaStreamSynchronize(st));
+  c.ph_t0 = std::chrono::steady_clock::now();
+}
+void ph_mark(Ctx& c, int phase, cudaStream_t st) {
+  if (!c.timing || !c.phase_marks) return;
+  OCTF_CUDA(cudaStreamSynchronize(st));
+  const auto now = std::chrono::steady_clock::now();
+  c.t_ph[phase] +=
+      std::chrono::duration<double, std::milli>(now - c.ph_t0).count();
+  c.ph_t0 = now;
+}
+
 void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
                  const int64_t* state, int d_max, cudaStream_t st) {
   const auto t0 = std::chrono::steady_clock::now();
+  ph_start(c, st);
   if (d_max < 0 || d_max > kMaxDepth)
     throw Error(kEDepth, "tree depth out of range");
   int64_t used = state[0];
@@ -846,10 +919,13 @@ void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
   OCTF_CUDA(cudaMemcpyAsync(dcnt, &one, sizeof(int32_t), cudaMemcpyHostToDevice,
                             st));
   for (int L = 0; L < d_max; ++L) {
-    // level L holds at most min(8^L, live blocks) blocks
+    // level L holds at most min(8^L, live blocks) blocks: a grid of at
+    // most one wave strides over them
     const int64_t bound = L < 7 ? std::min<int64_t>(int64_t(1) << (3 * L), nbid)
                                 : nbid;
-    k_expand_dev<<<grid_for(bound * 8), kThreads, 0, st>>>(
+    const int64_t wave = (int64_t)148 * 8 * kThreads;
+    k_expand_dev<<<grid_for(std::min<int64_t>(bound * 8, wave)), kThreads, 0,
+                   st>>>(
         child, c.lvl_blocks.p, L, used, nbid + 1, c.blevel.p, c.bcoord.p,
         c.bparent.p, dcnt, doff, c.counters.p);
     OCTF_CUDA(cudaGetLastError());
@@ -870,9 +946,13 @@ void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
   // a finest-level node must be a leaf
   // (checked implicitly: blocks at level d_max are never expanded)
 
+  ph_mark(c, kPhWalk, st);
   const bool patched =
       incremental && ctx_list_update(c, child, total, nbid, st);
-  if (!patched) ctx_list_full(c, child, total, nbid, st);
+  if (!patched) {
+    ctx_list_full(c, child, total, nbid, st);
+    ph_mark(c, kPhFull, st);
+  }
 
   c.smark.ensure(cap);
   OCTF_CUDA(cudaMemsetAsync(c.smark.p, 0, cap, st));
@@ -889,7 +969,11 @@ void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
   c.hstate[1] = state[1];
   c.hstate[2] = state[2];
   c.valid = true;
-  if (c.nviews > 0 && !patched) ctx_gather(c, st);
+  ph_mark(c, kPhTail, st);
+  if (c.nviews > 0 && !patched) {
+    ctx_gather(c, st);
+    ph_mark(c, kPhGather, st);
+  }
   OCTF_CUDA(cudaStreamSynchronize(st));
   if (c.timing) {
     c.t_prep_ms += std::chrono::duration<double, std::milli>(
@@ -994,6 +1078,7 @@ static bool ell_list_samples(Ctx& c, int64_t nold, int64_t nnew,
     c.W.grow_keep((size_t)(total + add) + 1, (size_t)total, st);
     total += add;
   }
+  ph_mark(c, kPhEllGrow, st);
   int32_t* fresh = c.sort_v32.ensure(nnew * 8 + 1);
   k_ell_update<<<grid_for(nnew * 8), kThreads, 0, st>>>(
       c.lblocks.p, c.lmeta.p, nnew, nold, oldmask, c.tileK.p, c.tileOff.p,
@@ -1001,67 +1086,56 @@ static bool ell_list_samples(Ctx& c, int64_t nold, int64_t nnew,
   // (slots past the list's end are never leaves: their rows are not read)
   int32_t* need = c.app_buf.ensure(nt_new + 1);
   OCTF_CUDA(cudaMemsetAsync(need, 0, (nt_new + 1) * sizeof(int32_t), st));
+  ph_mark(c, kPhEllUpdate, st);
+  // second attempt: only the leaves that overflowed (queued in redo)
+  int32_t* redo = c.split_list.ensure(nnew * 8 + 1);
+  OCTF_CUDA(cudaMemsetAsync(c.counters.p + 7, 0, sizeof(int32_t), st));
   for (int attempt = 0; attempt < 2; ++attempt) {
     k_ell_fresh<<<148 * 8, kThreads, 0, st>>>(
-        fresh, c.counters.p + 2, c.lmeta.p, ctx_views(c), c.tileK.p,
-        c.tileOff.p, c.F.p, c.W.p, c.counters.p + 3, need);
+        attempt == 0 ? fresh : redo,
+        attempt == 0 ? c.counters.p + 2 : c.counters.p + 7, c.lmeta.p,
+        ctx_views(c), c.tileK.p, c.tileOff.p, c.F.p, c.W.p, c.counters.p + 3,
+        need, attempt == 0 ? redo : nullptr, c.counters.p + 7);
     OCTF_CUDA(cudaGetLastError());
     OCTF_CUDA(cudaMemcpyAsync(c.h_counters, c.counters.p, 8 * sizeof(int32_t),
                               cudaMemcpyDeviceToHost, st));
     OCTF_CUDA(cudaStreamSynchronize(st));
+    ph_mark(c, kPhFresh, st);
     if (!c.h_counters[3]) break;
     if (attempt == 1) return false;
     // some new leaves see more views than their tile has rows: give those
     // tiles bigger row ranges at the end of the store (with headroom) and
-    // gather again (writes are idempotent)
-    std::vector<int32_t> hneed(nt_new), hK(nt_new);
-    std::vector<int64_t> hOff(nt_new);
-    OCTF_CUDA(cudaMemcpyAsync(hneed.data(), need, nt_new * sizeof(int32_t),
+    // gather again (writes are idempotent).  Planned on the device; the
+    // host reads back only the added size (to grow the store).
+    int64_t* rows = reinterpret_cast<int64_t*>(c.sort_k64.ensure(2 * nt_new + 3));
+    int64_t* scan = rows + nt_new + 2;
+    OCTF_CUDA(cudaMemsetAsync(rows + nt_new + 1, 0, sizeof(int64_t), st));
+    k_ell_plan<<<grid_for(nt_new + 1), kThreads, 0, st>>>(need, c.tileK.p,
+                                                          nt_new, rows);
+    size_t bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, rows, scan,
+                                  (int)(nt_new + 1), st);
+    c.cub_tmp.ensure(bytes);
+    OCTF_CUDA(cub::DeviceScan::ExclusiveSum(c.cub_tmp.p, bytes, rows, scan,
+                                            (int)(nt_new + 1), st));
+    int64_t hv[2] = {0, 0};
+    OCTF_CUDA(cudaMemcpyAsync(&hv[0], scan + nt_new, sizeof(int64_t),
                               cudaMemcpyDeviceToHost, st));
-    OCTF_CUDA(cudaMemcpyAsync(hK.data(), c.tileK.p, nt_new * sizeof(int32_t),
-                              cudaMemcpyDeviceToHost, st));
-    OCTF_CUDA(cudaMemcpyAsync(hOff.data(), c.tileOff.p,
-                              nt_new * sizeof(int64_t),
+    OCTF_CUDA(cudaMemcpyAsync(&hv[1], rows + nt_new + 1, sizeof(int64_t),
                               cudaMemcpyDeviceToHost, st));
     OCTF_CUDA(cudaStreamSynchronize(st));
-    std::vector<int32_t> mt, mk0, mk1;
-    std::vector<int64_t> mo0, mo1;
     const int64_t keep = total;
-    for (int64_t t = 0; t < nt_new; ++t) {
-      if (hneed[t] <= hK[t]) continue;
-      const int k1 = hneed[t] + hneed[t] / 4 + 4;
-      mt.push_back((int32_t)t);
-      mk0.push_back(hK[t]);
-      mo0.push_back(hOff[t]);
-      mk1.push_back(k1);
-      mo1.push_back(total);
-      c.ell_waste += (int64_t)hK[t] * 256;
-      hK[t] = k1;
-      hOff[t] = total;
-      total += (int64_t)k1 * 256;
-    }
+    c.ell_waste += hv[1];
+    total += hv[0];
     // (the old ranges stay unused until the next full rebuild compacts)
     c.F.grow_keep((size_t)total + 1, (size_t)keep, st);
     c.W.grow_keep((size_t)total + 1, (size_t)keep, st);
-    const int nm = (int)mt.size();
-    DevBuf<int32_t> dmt, dk0, dk1;
-    DevBuf<int64_t> do0, do1;
-    dmt.ensure(nm); dk0.ensure(nm); dk1.ensure(nm); do0.ensure(nm); do1.ensure(nm);
-    OCTF_CUDA(cudaMemcpyAsync(dmt.p, mt.data(), nm * 4, cudaMemcpyHostToDevice, st));
-    OCTF_CUDA(cudaMemcpyAsync(dk0.p, mk0.data(), nm * 4, cudaMemcpyHostToDevice, st));
-    OCTF_CUDA(cudaMemcpyAsync(dk1.p, mk1.data(), nm * 4, cudaMemcpyHostToDevice, st));
-    OCTF_CUDA(cudaMemcpyAsync(do0.p, mo0.data(), nm * 8, cudaMemcpyHostToDevice, st));
-    OCTF_CUDA(cudaMemcpyAsync(do1.p, mo1.data(), nm * 8, cudaMemcpyHostToDevice, st));
-    k_ell_move<<<nm, 256, 0, st>>>(dmt.p, dk0.p, do0.p, dk1.p, do1.p, c.F.p,
-                                   c.W.p);
+    k_ell_move_dev<<<(unsigned)nt_new, 256, 0, st>>>(
+        need, c.tileK.p, c.tileOff.p, scan, keep, c.F.p, c.W.p);
     OCTF_CUDA(cudaGetLastError());
-    OCTF_CUDA(cudaMemcpyAsync(c.tileK.p, hK.data(), nt_new * sizeof(int32_t),
-                              cudaMemcpyHostToDevice, st));
-    OCTF_CUDA(cudaMemcpyAsync(c.tileOff.p, hOff.data(),
-                              nt_new * sizeof(int64_t), cudaMemcpyHostToDevice,
-                              st));
     OCTF_CUDA(cudaMemsetAsync(c.counters.p + 3, 0, sizeof(int32_t), st));
     OCTF_CUDA(cudaStreamSynchronize(st));
+    ph_mark(c, kPhMove, st);
   }
   c.nlb = nnew;
   c.nleaves = c.h_counters[4];
@@ -1108,6 +1182,7 @@ bool ctx_list_update(Ctx& c, const int32_t* child, int64_t total, int64_t nbid,
   c.nholes += c.h_counters[0];
   const int64_t na = c.h_counters[1];
   const int64_t nnew = nold + na;
+  ph_mark(c, kPhListDiff, st);
   if (4 * c.nholes > nnew || 4 * na > nnew) return false;  // compact
   if (na) {
     sort_i32(c, app, na, st);  // appended in base order: deterministic
@@ -1135,6 +1210,7 @@ bool ctx_list_update(Ctx& c, const int32_t* child, int64_t total, int64_t nbid,
         child, c.lblocks.p, ndirty, c.blevel.p, c.bcoord.p, c.bparent.p,
         c.lkey.p, c.lmeta.p, c.lpar.p, c.nbr.p, dirty);
   OCTF_CUDA(cudaGetLastError());
+  ph_mark(c, kPhTables, st);
   if (c.ell) return ell_list_samples(c, nold, nnew, oldmask, t0, st);
   // samples, in place (the store only grows; its tail is zeroed)
   const int64_t nvp = c.sstride;

@@ -5,6 +5,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -42,6 +43,10 @@ struct Error : std::runtime_error {
 };
 
 void check_cuda(cudaError_t e, const char* what);
+struct Ctx;
+// phase stopwatch of context rebuilds (no-ops unless timing is on)
+void ph_start(Ctx& c, cudaStream_t st);
+void ph_mark(Ctx& c, int phase, cudaStream_t st);
 #define OCTF_CUDA(call) ::octf::check_cuda((call), #call)
 
 // owning device buffer (grow-only)
@@ -116,6 +121,25 @@ struct DevBuf {
     n = c;
     return p;
   }
+};
+
+// rebuild phases (Ctx::t_ph)
+enum Phase : int {
+  kPhWalk = 0,     // level walk (block lists per level)
+  kPhListDiff,     // patched list: holes and appended blocks
+  kPhTables,       // neighbour tables of touched entries
+  kPhEllGrow,      // ELL rows for appended tiles (counts, scan, offsets)
+  kPhEllUpdate,    // ELL: queue the new leaves
+  kPhFresh,        // gather of the new leaves' samples
+  kPhMove,         // ELL: tiles moved to bigger row ranges
+  kPhFull,         // full rebuild (sorted list, tables) instead of a patch
+  kPhGather,       // full sample gather
+  kPhTail,         // free-list mirror, marks, rest of the rebuild
+  kPhSplitCascade, // restructuring pass: split events and their cascade
+  kPhSplitAlloc,   // ... pre-order keys, sort, block allocation
+  kPhJoins,        // ... join candidates and updates, level by level
+  kPhSweep,        // ... post-order sweep, free list, join log
+  kPhCount
 };
 
 struct Ctx {
@@ -210,6 +234,11 @@ struct Ctx {
   // restructuring tail of a pass (after the leaf kernel)
   double t_prep_ms = 0, t_gather_ms = 0, t_restr_ms = 0;
   int64_t n_prep = 0, n_gather = 0, n_regather = 0;
+  // finer phases of a context rebuild (timing on and OCTF_PHASES=1; each mark synchronises):
+  // kPh* indices, exported by octf_ctx_phases after the five totals
+  double t_ph[16] = {};
+  bool phase_marks = false;  // env OCTF_PHASES=1 (the marks synchronise)
+  std::chrono::steady_clock::time_point ph_t0;
   int64_t n_leaf = 0, n_energy = 0, launches = 0;
 
   // host pinned staging for small readbacks

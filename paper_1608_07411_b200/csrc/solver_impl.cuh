@@ -90,64 +90,11 @@ __device__ __forceinline__ T clamp1(T v) {
 // generic update of one cell at level L from the snapshot by root descents:
 // the reference's delta_u (_kernels.pyx:223-253) verbatim in structure.
 // Used for split cascades (virtual children) and join candidates.
-template <typename T>
-__device__ __forceinline__ T look(const int32_t* child, const T* snap, int L,
-                                  int x, int y, int z) {
-  return snap[descend(child, L, x, y, z)];
-}
-
-template <typename T>
-__device__ void flux_at(const int32_t* child, const T* snap, int L, int x,
-                        int y, int z, T ih, T eps2, T out[3]) {
-  const int m = 1 << L;
-  const T c = look(child, snap, L, x, y, z);
-  T gx = 0, gy = 0, gz = 0;
-  if (x + 1 < m) gx = (look(child, snap, L, x + 1, y, z) - c) * ih;
-  if (y + 1 < m) gy = (look(child, snap, L, x, y + 1, z) - c) * ih;
-  if (z + 1 < m) gz = (look(child, snap, L, x, y, z + 1) - c) * ih;
-  Arith<T>::flux(gx, gy, gz, eps2, out[0], out[1], out[2]);
-}
-
-template <typename T>
-__device__ T slow_dn(const int32_t* child, const T* snap, ViewSet vs,
-                     const LeafParams<T>& p, int L, int x, int y, int z,
-                     T S0) {
-  using A = Arith<T>;
-  const T ih = inv_spacing<T>(p.d_max, L);
-  T q[3], r[3];
-  T bx = 0, by = 0, bz = 0;
-  flux_at(child, snap, L, x, y, z, ih, p.eps2, q);
-  if (x > 0) {
-    flux_at(child, snap, L, x - 1, y, z, ih, p.eps2, r);
-    bx = r[0];
-  }
-  if (y > 0) {
-    flux_at(child, snap, L, x, y - 1, z, ih, p.eps2, r);
-    by = r[1];
-  }
-  if (z > 0) {
-    flux_at(child, snap, L, x, y, z - 1, ih, p.eps2, r);
-    bz = r[2];
-  }
-  const T div = ((q[0] - bx) + (q[1] - by) + (q[2] - bz)) * ih;
-  T num = 0, den = p.gamma;
-  for (int v = 0; v < vs.n; ++v) {
-    const int32_t n = descend(vs.child[v], L, x, y, z);
-    const float w = vs.w[v][n];
-    if (w != 0.f) {
-      const T d = S0 - (T)vs.val[v][n];
-      num += A::data_grad((T)w, d, p.eps2);
-      den += (T)w;
-    }
-  }
-  const T du = p.lam * div - A::div(num, den);
-  return S0 + p.xi * du;
-}
-
-// slow_dn by one warp: lane k < 13 resolves stencil point k, lanes cover the
-// views (v = lane, lane + 32, ...); every lane then combines the shuffled
-// values in the reference's order (flux_at / slow_dn above, bit for bit),
-// so the dependent root-descent chain of one thread is ~1/30 as long.
+// dn of one node by root descents (_kernels.pyx:205-253, lookups :193-202),
+// by one warp: lane k < 13 resolves stencil point k, lanes cover the views
+// (v = lane, lane + 32, ...); every lane then combines the shuffled values
+// in the reference's order (flux3 / delta_u, bit for bit), so the dependent
+// root-descent chain of one thread is ~1/30 as long.
 template <typename T>
 __device__ T warp_slow_dn(const int32_t* child, const T* snap, ViewSet vs,
                           const LeafParams<T>& p, int L, int x, int y, int z,
@@ -293,23 +240,32 @@ template <typename T>
 __global__ void k_cascade(int64_t e0, int64_t e1, Events<T> ev,
                           const int32_t* __restrict__ child,
                           const T* __restrict__ snap, ViewSet vs,
-                          LeafParams<T> p, int32_t* counters, int64_t ev_cap) {
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t e = e0 + (gid >> 3);
-  const int c = (int)(gid & 7);
-  if (e >= e1) return;
+                          LeafParams<T> p, int32_t* counters, int64_t ev_cap,
+                          int64_t buf_cap) {
+  // one warp per virtual child (the root descents of its 13 stencil points
+  // and of its views spread over the lanes, warp_slow_dn); lane 0 records
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t e = e0 + (gw >> 3);
+  const int c = (int)(gw & 7);
+  if (e >= e1) return;  // warp-uniform
   int L, x, y, z;
   unpack_cell(ev.cell[e], L, x, y, z);
   const int L1 = L + 1;
   const int x1 = 2 * x + ((c >> 2) & 1), y1 = 2 * y + ((c >> 1) & 1),
             z1 = 2 * z + (c & 1);
   const T S0 = ev.S[e];
-  T dn = slow_dn<T>(child, snap, vs, p, L1, x1, y1, z1, S0);
+  T dn = warp_slow_dn<T>(child, snap, vs, p, L1, x1, y1, z1, S0, lane);
+  if (lane != 0) return;
   if (L1 < p.d_max && fabs((double)dn) < p.tau_s) {
     atomicOr(ev.cmask + e, 1 << c);
     const int32_t ne = atomicAdd(counters + 2, 1);
-    if (ne >= ev_cap) {
+    if (ne >= ev_cap) {  // more blocks than the pool holds
       atomicExch(counters + 3, 1);
+      return;
+    }
+    if (ne >= buf_cap) {  // event buffers too small: the host retries
+      atomicExch(counters + 5, 1);
       return;
     }
     ev.slot[ne] = -1;
@@ -851,6 +807,7 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
     ++c.n_leaf;
   }
   const auto t_restr = std::chrono::steady_clock::now();
+  ph_start(c, st);
   const int64_t nsplit = c.h_counters[0];
   const int64_t ncand = c.h_counters[1];
   const T* snap = (const T*)a.usnap;
@@ -863,27 +820,47 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
   // ---- split cascade + allocation in depth-first order
   if (nsplit > 0) {
     static thread_local EventBufs<T> eb;
+    // the pool bound on events (blocks the pool can still hand out) sizes
+    // the exhaustion test; the buffers start at a small multiple of the
+    // split count and are sized to the bound only when a cascade outgrows
+    // them (sizing them to the bound every pass reallocated eleven buffers
+    // whenever the free list grew: 0.5 ms for a one-split pass at cfg4)
     const int64_t ev_cap = nsplit + (a.cap - used) / 8 + c.nfree + 8;
-    Events<T> ev = eb.view(ev_cap);
-    k_events_init<T><<<blocks_for(nsplit), kT, 0, st>>>(
-        c.split_list.p, nsplit, c.blevel.p, c.bcoord.p, snap, ev);
-    OCTF_CUDA(cudaGetLastError());
-  ++c.launches;
-    int64_t e0 = 0, e1 = nsplit;
-    int32_t ecount = (int32_t)nsplit;
-    OCTF_CUDA(cudaMemcpyAsync(c.counters.p + 2, &ecount, sizeof(int32_t),
-                              cudaMemcpyHostToDevice, st));
-    while (e1 > e0) {
-      k_cascade<T><<<blocks_for((e1 - e0) * 8), kT, 0, st>>>(
-          e0, e1, ev, a.child, snap, vs, lp, c.counters.p, ev_cap);
+    int64_t buf_cap = std::min<int64_t>(ev_cap, 64 * nsplit + 4096);
+    Events<T> ev;
+    int64_t e1 = nsplit;
+    for (;;) {
+      ev = eb.view(buf_cap);
+      k_events_init<T><<<blocks_for(nsplit), kT, 0, st>>>(
+          c.split_list.p, nsplit, c.blevel.p, c.bcoord.p, snap, ev);
       OCTF_CUDA(cudaGetLastError());
-  ++c.launches;
-      read_counters<T>(c, 4, st);
-      if (c.h_counters[3]) throw Error(kEPool, "node pool capacity exhausted");
-      e0 = e1;
-      e1 = c.h_counters[2];
+      ++c.launches;
+      int64_t e0 = 0;
+      e1 = nsplit;
+      const int32_t init[4] = {(int32_t)nsplit, 0, 0, 0};  // counters 2..5
+      OCTF_CUDA(cudaMemcpyAsync(c.counters.p + 2, init, sizeof(init),
+                                cudaMemcpyHostToDevice, st));
+      bool grow = false;
+      while (e1 > e0) {
+        k_cascade<T><<<blocks_for((e1 - e0) * 8 * 32), kT, 0, st>>>(
+            e0, e1, ev, a.child, snap, vs, lp, c.counters.p, ev_cap, buf_cap);
+        OCTF_CUDA(cudaGetLastError());
+        ++c.launches;
+        read_counters<T>(c, 6, st);
+        if (c.h_counters[3])
+          throw Error(kEPool, "node pool capacity exhausted");
+        if (c.h_counters[5]) {
+          grow = true;
+          break;
+        }
+        e0 = e1;
+        e1 = c.h_counters[2];
+      }
+      if (!grow) break;
+      buf_cap = ev_cap;  // rerun the cascade with buffers at the bound
     }
     const int64_t E = e1;
+    ph_mark(c, kPhSplitCascade, st);
     const int64_t fresh = E > c.nfree ? E - c.nfree : 0;
     if (used + 8 * fresh > a.cap)
       throw Error(kEPool, "node pool capacity exhausted");
@@ -917,6 +894,7 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
     a.state[2] += 8 * E;
     splits = E;
     changed = true;
+    ph_mark(c, kPhSplitAlloc, st);
   }
 
   // ---- join cascade, bottom-up
@@ -948,6 +926,7 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
       c.launches += 2;
     }
     read_counters<T>(c, 5, st);
+    ph_mark(c, kPhJoins, st);
     const int64_t J = c.h_counters[4];
     if (J > 0) {
       // sweep order: forward post-order (sweep ignores `reverse`)
@@ -986,6 +965,7 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
       a.state[2] -= 8 * J;
       joins = J;
       changed = true;
+      ph_mark(c, kPhSweep, st);
     }
   }
   if (nsplit > 0) {

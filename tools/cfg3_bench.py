@@ -76,7 +76,9 @@ for t in range(args.passes):
                    "splits": st.splits, "joins": st.joins,
                    "leaf_ms": pr["leaf_ms"], "prepare_ms": pr["prepare_ms"],
                    "gather_ms": pr["gather_ms"],
-                   "restructure_ms": pr["restructure_ms"]})
+                   "restructure_ms": pr["restructure_ms"],
+                   **({"rebuild_phases_ms": pr["rebuild_phases_ms"]}
+                      if os.environ.get("OCTF_PHASES") == "1" else {})})
 prof = s.ctx.profile(False)
 res = s.result()
 mesh_info = None

@@ -1,7 +1,7 @@
 """Propagate timing harness: the cfg2 full tree (depth 8) and, with CFG5=1, a
 cfg5-style random adaptive tree; f32 values propagated through one context
 repeatedly (CUDA events), value hash printed so two builds / modes can be
-compared (OCTF_LEVEL_PROPAGATE=1 selects the per-level launches)."""
+compared (env A/B switches of the library apply)."""
 import hashlib
 import os
 import sys

@@ -44,6 +44,8 @@ Ctx::Ctx() {
   no_regather = fg && fg[0] == '1';
   const char* fe = std::getenv("OCTF_FORCE_ELL");  // tests: ELL from 33 views
   force_ell = fe && fe[0] == '1';
+  const char* lj = std::getenv("OCTF_LEVEL_JOINS");  // A/B switch
+  coop_off = lj && lj[0] == '1';
   const char* pm = std::getenv("OCTF_PHASES");  // rebuild phase marks
   phase_marks = pm && pm[0] == '1';
   const char* fp = std::getenv("OCTF_NO_FUSED_PARENT");  // A/B switch
@@ -621,16 +623,11 @@ __global__ void k_ell_fresh(const int32_t* __restrict__ fresh,
     int32_t nd[kFreshChunks];
     int j = 0;
     // count first: a leaf that does not fit leaves its tile untouched
+    descend_views<kFreshChunks>(vs.child, vs.n, L, x, y, z, lane, nd);
 #pragma unroll
     for (int q = 0; q < kFreshChunks; ++q) {
-      const int v = q * 32 + lane;
-      nd[q] = -1;
       if (q * 32 < vs.n) {
-        bool on = false;
-        if (v < vs.n) {
-          nd[q] = descend(vs.child[v], L, x, y, z);
-          on = vs.w[v][nd[q]] != 0.f;
-        }
+        const bool on = nd[q] >= 0 && vs.w[q * 32 + lane][nd[q]] != 0.f;
         j += __popc(__ballot_sync(0xffffffffu, on));
       }
     }

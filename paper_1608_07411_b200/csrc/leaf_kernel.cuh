@@ -47,7 +47,7 @@ struct LeafArgs {
   const uint64_t* __restrict__ lkey;
   const int4* __restrict__ lmeta;
   const int32_t* __restrict__ lpar;  // parent slot of each leaf block
-  int write_parent;  // frozen passes: also write the bottom propagate level
+  int32_t* join_bot;  // restructuring passes: parents of bottom candidates
   const int32_t* __restrict__ nbr;
   const int32_t* __restrict__ child;
   const T* __restrict__ snap;
@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
       neg |= __shfl_xor_sync(FULL, neg, o);
     }
     if (c == 0 && inrange && b != 0 && all && !(pos && neg))
-      atomicAdd(a.counters + 1, 1);
+      a.join_bot[atomicAdd(a.counters + 1, 1)] = __ldg(a.lpar + i);
   }
   if (ENERGY) {
     typedef cub::BlockReduce<double, kT> BR;

@@ -130,6 +130,41 @@ __device__ __forceinline__ int32_t descend(const int32_t* __restrict__ child,
   return n;
 }
 
+// the view-tree nodes of cell (x,y,z)@L for views v = q*32 + lane, q < NCH
+// (descend() per view), the NCH root descents advanced in lock-step so their
+// dependent loads overlap (one load latency per level instead of NCH); -1
+// for views past n
+template <int NCH>
+__device__ __forceinline__ void descend_views(const int32_t* const* vchild,
+                                              int n, int L, int x, int y,
+                                              int z, int lane,
+                                              int32_t (&nd)[NCH]) {
+  const int32_t* ch[NCH];
+  unsigned live = 0;
+#pragma unroll
+  for (int q = 0; q < NCH; ++q) {
+    const int v = q * 32 + lane;
+    nd[q] = v < n ? 0 : -1;
+    ch[q] = v < n ? vchild[v] : nullptr;
+    if (v < n) live |= 1u << q;
+  }
+  for (int l = 0; l < L && live; ++l) {
+    const int sh = L - l - 1;
+    const int oc = octant(x >> sh, y >> sh, z >> sh);
+    int32_t b[NCH];
+#pragma unroll
+    for (int q = 0; q < NCH; ++q) b[q] = (live >> q) & 1u ? __ldg(ch[q] + nd[q]) : -1;
+#pragma unroll
+    for (int q = 0; q < NCH; ++q) {
+      if (!((live >> q) & 1u)) continue;
+      if (b[q] < 0)
+        live &= ~(1u << q);
+      else
+        nd[q] = b[q] + oc;
+    }
+  }
+}
+
 // neighbour-table direction of a parent-level block offset (ox,oy,oz):
 // faces -x +x -y +y -z +z, then the six edge offsets the 13-point stencil
 // reaches: (-x+y) (-x+z) (+x-y) (-y+z) (+x-z) (+y-z); -1 = never used

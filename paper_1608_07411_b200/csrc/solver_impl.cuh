@@ -22,6 +22,7 @@
 // identical to the reference's on live nodes.
 #pragma once
 #include <chrono>
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include "octf_arith.cuh"
@@ -159,14 +160,43 @@ __device__ T warp_slow_dn(const int32_t* child, const T* snap, ViewSet vs,
   }
   const T div = ((q[0] - bx) + (q[1] - by) + (q[2] - bz)) * ih;
   T num = 0, den = p.gamma;
+  // the first kViewChunks*32 views' nodes by lock-step descents
+  constexpr int kViewChunks = 10;
+  int32_t nd[kViewChunks];
+  descend_views<kViewChunks>(vs.child, vs.n, L, x, y, z, lane, nd);
+  // every chunk's (w, f) loaded before the ordered combine (independent
+  // loads in flight together: the warp's latency chain is the critical
+  // path of a join level)
+  float wq[kViewChunks], fq[kViewChunks];
+#pragma unroll
+  for (int q = 0; q < kViewChunks; ++q) {
+    wq[q] = 0.f;
+    fq[q] = 0.f;
+    if (nd[q] >= 0) {
+      const int v = q * 32 + lane;
+      wq[q] = vs.w[v][nd[q]];
+      fq[q] = vs.val[v][nd[q]];
+    }
+  }
   for (int v0 = 0; v0 < vs.n; v0 += 32) {
     const int v = v0 + lane;
-    float w = 0.f;
+    float w = 0.f, f = 0.f;
     T g = 0;
     if (v < vs.n) {
-      const int32_t n = descend(vs.child[v], L, x, y, z);
-      w = vs.w[v][n];
-      if (w != 0.f) g = A::data_grad((T)w, S0 - (T)vs.val[v][n], p.eps2);
+      bool got = false;
+#pragma unroll
+      for (int q = 0; q < kViewChunks; ++q)
+        if (v0 == q * 32) {
+          w = wq[q];
+          f = fq[q];
+          got = true;
+        }
+      if (!got) {
+        const int32_t n = descend(vs.child[v], L, x, y, z);
+        w = vs.w[v][n];
+        f = vs.val[v][n];
+      }
+      if (w != 0.f) g = A::data_grad((T)w, S0 - (T)f, p.eps2);
     }
     const int nk = vs.n - v0 < 32 ? vs.n - v0 : 32;
     for (int k = 0; k < nk; ++k) {  // view order, as slow_dn
@@ -402,6 +432,127 @@ __global__ void __launch_bounds__(256)
       rec.cell[r] = pack_cell(L, x, y, z);
       for (int q = 0; q < 8; ++q) rec.vals[r * 8 + q] = (double)uval[cb + q];
     }
+  }
+}
+
+// All join levels in one cooperative launch (bottom-up, grid barriers
+// between the phases), from worklists instead of scans of every level:
+// candidates at level L are the parents of the leaf kernel's bottom blocks
+// (eight unsplit leaves past tau_j with one sign) that sit at level L, and
+// the parents of the nodes joined at level L+1 (proposed once, by the
+// highest-index joined sibling).  Every other inner node has a live inner
+// child and cannot join (k_join_cand's test), so the candidate sets equal
+// the per-level scans'; the test and the update (warp_slow_dn) are the
+// same, and the join records are sorted afterwards, so the result does not
+// depend on the order candidates are found in.
+template <typename T>
+struct JoinCoopArgs {
+  const int32_t* bot;     // parent slots of the bottom candidate blocks
+  int64_t nbot;
+  const int8_t* blevel;
+  const uint64_t* bcoord;
+  const int32_t* bparent;
+  const int32_t* child;
+  uint8_t* joined;
+  const uint8_t* smark;
+  const T* snap;
+  T* uval;
+  ViewSet vs;
+  LeafParams<T> p;
+  JoinRecs<T> rec;
+  int32_t* counters;      // [4]: join records
+  int32_t* cand;
+  double* cacc;
+  int32_t* ccount;        // per level, zeroed
+  int d_max;
+};
+
+template <typename T>
+__device__ __forceinline__ bool join_test(const JoinCoopArgs<T>& a, int32_t s,
+                                          double& acc) {
+  const int32_t cb = a.child[s];
+  if (cb < 0 || a.smark[s]) return false;
+  // all loads first (independent), then the reference's test in order
+  int32_t ch[8];
+  uint8_t jn[8];
+  T u[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    ch[q] = a.child[cb + q];
+    jn[q] = a.joined[cb + q];
+    u[q] = a.uval[cb + q];
+  }
+  bool pos = false, neg = false;
+  acc = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    if (ch[q] >= 0 && !jn[q]) return false;
+    const double v = (double)u[q];
+    if (!(v > a.p.tau_j || v < -a.p.tau_j)) return false;
+    if (v > 0.0)
+      pos = true;
+    else
+      neg = true;
+    acc += v;
+  }
+  return !(pos && neg);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_joins_coop(JoinCoopArgs<T> a) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  const int64_t wid = tid >> 5, nw = nthr >> 5;
+  int rec_lo = 0;
+  for (int L = a.d_max - 1; L >= 0; --L) {
+    const int rec_hi = *(volatile int32_t*)(a.counters + 4);
+    const int64_t n_in = a.nbot + (rec_hi - rec_lo);
+    for (int64_t i = tid; i < n_in; i += nthr) {
+      int32_t s;
+      if (i < a.nbot) {
+        s = a.bot[i];
+        int Ls, xs, ys, zs;
+        slot_cell_of(s, a.blevel, a.bcoord, Ls, xs, ys, zs);
+        if (Ls != L) continue;
+      } else {
+        const int32_t j = a.rec.slot[rec_lo + (i - a.nbot)];
+        const int32_t jb = ((j - 1) & ~7) + 1;
+        bool later = false;  // a higher sibling joined: it proposes
+        for (int q = j - jb + 1; q < 8; ++q) later |= a.joined[jb + q] != 0;
+        if (later) continue;
+        s = a.bparent[block_id(jb)];
+      }
+      double acc;
+      if (!join_test(a, s, acc)) continue;
+      const int32_t r = atomicAdd(a.ccount + L, 1);
+      a.cand[r] = s;
+      a.cacc[r] = acc;
+    }
+    grid.sync();
+    const int n = *(volatile int32_t*)(a.ccount + L);
+    for (int64_t w = wid; w < n; w += nw) {
+      const int32_t s = a.cand[w];
+      int Ls, x, y, z;
+      slot_cell_of(s, a.blevel, a.bcoord, Ls, x, y, z);
+      const T dn = warp_slow_dn<T>(a.child, a.snap, a.vs, a.p, Ls, x, y, z,
+                                   a.snap[s], lane);
+      if (lane == 0 && fabs((double)dn) > a.p.tau_j) {
+        const int32_t cb = a.child[s];
+        a.joined[s] = 1;
+        a.uval[s] = (T)(a.cacc[w] / 8.0);
+        const int32_t r = atomicAdd(a.counters + 4, 1);
+        a.rec.slot[r] = s;
+        a.rec.blk[r] = cb;
+        a.rec.cell[r] = pack_cell(Ls, x, y, z);
+        for (int q = 0; q < 8; ++q)
+          a.rec.vals[r * 8 + q] = (double)a.uval[cb + q];
+      }
+    }
+    grid.sync();
+    rec_lo = rec_hi;
   }
 }
 
@@ -667,6 +818,7 @@ void launch_leaf_pass(Ctx& c, const T* snap, T* uval, const int32_t* child,
   LeafArgs<T> a;
   a.tile0 = tile0;
   a.lpar = c.lpar.p;
+  a.join_bot = c.join_bot.p;
   a.lblocks = c.lblocks.p;
   a.nlb = c.nlb;
   a.lkey = c.lkey.p;
@@ -744,7 +896,7 @@ struct EventBufs {
 
 template <typename T>
 struct JoinBufs {
-  DevBuf<int32_t> slot, blk, idx, cand;
+  DevBuf<int32_t> slot, blk, idx, cand, ccount;
   DevBuf<uint64_t> cell, key;
   DevBuf<double> vals, cacc;
   JoinRecs<T> view(int64_t cap) {
@@ -784,6 +936,7 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
                        "(tau_split <= 0, tau_join >= 1, clamp)");
   c.counters.ensure(64);
   c.split_list.ensure(c.nlb * 8 + 1);
+  c.join_bot.ensure(c.nlb + 1);
   OCTF_CUDA(cudaMemsetAsync(c.counters.p, 0, 8 * sizeof(int32_t), st));
   double* epart = nullptr;
   if (a.want_energy) {
@@ -907,7 +1060,47 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
     // round trip: the dn kernel strides over the device-side count)
     int32_t* cand = jb.cand.ensure(c.nblocks * 8 + 8);
     double* cacc = jb.cacc.ensure(c.nblocks * 8 + 8);
-    for (int L = prm.d_max - 1; L >= 0; --L) {
+    if (!c.coop_off) {
+      // every level in one cooperative launch from the worklists
+      int32_t* ccount = jb.ccount.ensure(kMaxDepth + 2);
+      OCTF_CUDA(cudaMemsetAsync(ccount, 0, (kMaxDepth + 2) * sizeof(int32_t),
+                                st));
+      JoinCoopArgs<T> ja;
+      ja.bot = c.join_bot.p;
+      ja.nbot = ncand;
+      ja.blevel = c.blevel.p;
+      ja.bcoord = c.bcoord.p;
+      ja.bparent = c.bparent.p;
+      ja.child = a.child;
+      ja.joined = a.joined;
+      ja.smark = c.smark.p;
+      ja.snap = snap;
+      ja.uval = uval;
+      ja.vs = vs;
+      ja.p = lp;
+      ja.rec = rec;
+      ja.counters = c.counters.p;
+      ja.cand = cand;
+      ja.cacc = cacc;
+      ja.ccount = ccount;
+      ja.d_max = prm.d_max;
+      static int coop_blocks = 0;
+      if (!coop_blocks) {
+        int per_sm = 0, dev = 0, nsm = 0;
+        OCTF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, k_joins_coop<T>, 256, 0));
+        OCTF_CUDA(cudaGetDevice(&dev));
+        OCTF_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount,
+                                         dev));
+        coop_blocks = per_sm * nsm;
+        if (coop_blocks < 1) throw Error(kECuda, "joins: no resident CTA");
+      }
+      void* kargs[] = {&ja};
+      OCTF_CUDA(cudaLaunchCooperativeKernel((const void*)k_joins_coop<T>,
+                                            coop_blocks, 256, kargs, 0, st));
+      ++c.launches;
+    }
+    for (int L = prm.d_max - 1; L >= 0 && c.coop_off; --L) {
       const int64_t n = c.lvl_cnt[L];
       if (n == 0) continue;
       OCTF_CUDA(cudaMemsetAsync(c.counters.p + 8, 0, sizeof(int32_t), st));

@@ -324,6 +324,44 @@ class TestRandomTrees:
         assert [(s.splits, s.joins) for s in res.stats] == \
             [(s.splits, s.joins) for s in ref.stats]
 
+    @pytest.mark.parametrize("seed", range(2))
+    def test_join_paths_agree(self, seed, monkeypatch):
+        """The cooperative worklist joins and the per-level scans
+        (OCTF_LEVEL_JOINS=1) give the same pools, logs and counts."""
+        from paper_1608_07411_b200 import fusion
+        rng = np.random.default_rng(200 + seed)
+        d = 5
+        n = 1 << d
+        g = (np.arange(n) + 0.5) / n
+        X, Y, Z = np.meshgrid(g, g, g, indexing="ij")
+        sd = np.sqrt((X - .5) ** 2 + (Y - .5) ** 2 + (Z - .5) ** 2) - 0.3
+        views_h = []
+        for _ in range(4):   # noisy sphere TSDFs: joins cascade, a few splits
+            f = np.clip(sd / 0.1 + rng.normal(0, 0.05, sd.shape), -1,
+                        1).astype(np.float32)
+            w = (rng.random((n, n, n)) < 0.9).astype(np.uint8)
+            f[w == 0] = -1.0
+            views_h.append(orc.build_octree(f, w, tau=0.3, dtype=np.float32))
+        ub = np.clip(sd / 0.1 + rng.normal(0, 0.3, sd.shape), -1, 1)
+        u0h = orc.build_octree(ub, tau=0.4)
+        params = fusion.FusionParams(iterations=8, xi0=0.3, tau_split=0.15,
+                                     tau_join=0.45, lam=0.4)
+
+        def run():
+            r = fusion.fuse(dev(u0h), [dev(v) for v in views_h], params,
+                            log_joins=True)
+            h = r.field.to_host()
+            return h.child.copy(), h.value.copy(), r.join_log, \
+                [(s.splits, s.joins, s.node_count) for s in r.stats]
+
+        a = run()
+        monkeypatch.setenv("OCTF_LEVEL_JOINS", "1")
+        b = run()
+        assert sum(j for _, j, _ in a[3]) > 300
+        for x, y in zip(a[:3], b[:3]):
+            assert np.array_equal(x, y)
+        assert a[3] == b[3]
+
 
 class TestEdgeCases:
     def test_single_leaf_tree(self):

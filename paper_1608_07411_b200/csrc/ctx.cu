@@ -1033,7 +1033,10 @@ static bool ell_list_samples(Ctx& c, int64_t nold, int64_t nnew,
   const int64_t nt_old = c.ell_tiles;
   const int64_t nt_new = (nnew * 8 + kTileLeaves - 1) / kTileLeaves;
   int64_t total = c.ell_size;
-  if (4 * c.ell_waste > total) return false;  // compact: full rebuild
+  // compact (full rebuild) once abandoned rows pass half the store: with
+  // many views a rebuild regathers every leaf's samples (cfg4 depth 9,
+  // 300 views: 38 ms, ~100 passes' worth of the holes' cost)
+  if (2 * c.ell_waste > total) return false;
   if (nt_new > nt_old) {
     int32_t* cnt = c.sort_k32.ensure(nt_new * 256 + 1);
     OCTF_CUDA(cudaMemsetAsync(cnt, 0, nt_new * 256 * sizeof(int32_t), st));
@@ -1180,7 +1183,10 @@ bool ctx_list_update(Ctx& c, const int32_t* child, int64_t total, int64_t nbid,
   const int64_t na = c.h_counters[1];
   const int64_t nnew = nold + na;
   ph_mark(c, kPhListDiff, st);
-  if (4 * c.nholes > nnew || 4 * na > nnew) return false;  // compact
+  // compact past 25 % holes or appended entries (half with the ELL store,
+  // whose rebuild is the expensive many-view gather)
+  const int64_t lim = c.ell ? 2 : 4;
+  if (lim * c.nholes > nnew || lim * na > nnew) return false;
   if (na) {
     sort_i32(c, app, na, st);  // appended in base order: deterministic
     c.lblocks.grow_keep(nnew, nold, st);

@@ -460,20 +460,18 @@ __global__ void __launch_bounds__(kT, pd_minb(BINW, NV)) k_pd_pass(PdArgs<T> a) 
   __shared__ typename BR::TempStorage tmp;
   const double tot = BR(tmp).Sum(eterm);
   if (threadIdx.x == 0) a.epart[blockIdx.x] = tot;
-  if (WP && t < kT / 8) {
-    const int32_t par = s_par[t];
+  if (WP && t < 5 * (kT / 8)) {
+    // warp q writes field q of the 32 blocks (a short tail: the CTA's slot
+    // is held until its last warp exits)
+    const int q = t >> 5, j = t & 31;
+    const int32_t par = s_par[j];
     if (par >= 0) {
-      auto mean8 = [&](int q) {
-        double acc = 0.0;
+      double acc = 0.0;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) acc += (double)s_v[q][t * 8 + k];
-        return (T)(acc / 8.0);
-      };
-      a.u_o[par] = mean8(0);
-      a.ub_o[par] = mean8(1);
-      a.px_o[par] = mean8(2);
-      a.py_o[par] = mean8(3);
-      a.pz_o[par] = mean8(4);
+      for (int k = 0; k < 8; ++k) acc += (double)s_v[q][j * 8 + k];
+      T* const o = q == 0 ? a.u_o : q == 1 ? a.ub_o : q == 2 ? a.px_o
+                 : q == 3 ? a.py_o : a.pz_o;
+      o[par] = (T)(acc / 8.0);
     }
   }
 }

@@ -811,7 +811,7 @@ template <typename T>
 void launch_leaf_pass(Ctx& c, const T* snap, T* uval, const int32_t* child,
                       const LeafParams<T>& lp, bool frozen, double* epart,
                       cudaStream_t st, bool timed = true,
-                      bool write_parent = false, int tile0 = 0,
+                      int tile0 = 0,
                       int ntiles = -1) {
   const unsigned g = ntiles < 0 ? leaf_grid(c) : (unsigned)ntiles;
   if (g == 0) return;
@@ -1637,7 +1637,7 @@ void pass_tiles_impl(Ctx& c, TileArgs& a, cudaStream_t st) {
   c.partials.ensure(leaf_parts(c));
   const LeafParams<T> lp = leaf_params<T>(a.prm);
   launch_leaf_pass<T>(c, (const T*)a.usnap, (T*)a.uval, a.child, lp, true,
-                      c.partials.p, st, false, false, a.tile0, a.ntiles);
+                      c.partials.p, st, false, a.tile0, a.ntiles);
 }
 
 // propagate every level of the pass's output and sum the pass's energy

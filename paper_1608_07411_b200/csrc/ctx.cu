@@ -114,10 +114,66 @@ __global__ void k_expand(const int32_t* __restrict__ child,
   next[pos] = nb;
 }
 
+// positions for the threads of a CTA that want one: one atomic per CTA on
+// the shared counter (per-thread or per-warp atomics on one address
+// serialise in L2: the level walk of a 60M-node tree spent ~0.4 ms on
+// them).  Every thread of the CTA must call it; -1 for the others.
+__device__ __forceinline__ int64_t cta_alloc(bool want, int32_t* global) {
+  __shared__ int s_warp[kThreads / 32];
+  __shared__ int s_base;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned bal = __ballot_sync(0xffffffffu, want);
+  if (lane == 0) s_warp[w] = __popc(bal);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+      const int t = s_warp[k];
+      s_warp[k] = acc;
+      acc += t;
+    }
+    s_base = acc ? atomicAdd(global, acc) : 0;
+  }
+  __syncthreads();
+  const int64_t r = (int64_t)s_base + s_warp[w] +
+                    __popc(bal & ((1u << lane) - 1u));
+  __syncthreads();  // the shared slots are reused by the next call
+  return want ? r : -1;
+}
+
+// cta_alloc for counts: the first of `cnt` consecutive positions (any value
+// when cnt == 0); every thread of the CTA must call it
+__device__ __forceinline__ int64_t cta_alloc_n(int cnt, int32_t* global) {
+  __shared__ int s_warp[kThreads / 32];
+  __shared__ int s_base;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int incl = cnt;  // inclusive warp scan
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) s_warp[w] = incl;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+      const int t = s_warp[k];
+      s_warp[k] = acc;
+      acc += t;
+    }
+    s_base = acc ? atomicAdd(global, acc) : 0;
+  }
+  __syncthreads();
+  const int64_t r = (int64_t)s_base + s_warp[w] + (incl - cnt);
+  __syncthreads();
+  return r;
+}
+
 // k_expand without a host round trip per level: the level's range comes
 // from device counters (dcnt, doff), the next level's start is written by
 // thread 0; a fixed grid strides over the level (its size is only known on
-// the device)
+// the device), CTA-uniform so the slots of a CTA are claimed together
 __global__ void k_expand_dev(const int32_t* __restrict__ child,
                              int32_t* lvl_blocks, int L, int64_t used,
                              int64_t cap_blocks, int8_t* blevel,
@@ -128,30 +184,46 @@ __global__ void k_expand_dev(const int32_t* __restrict__ child,
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid == 0) doff[L + 1] = (int32_t)next;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t gid = tid; gid < n * 8; gid += stride) {
-    const int64_t i = gid >> 3;
-    const int c = (int)(gid & 7);
-    const int32_t b = lvl_blocks[doff[L] + i];
-    if (b == 0 && c != 0) continue;
-    const int32_t s = b + c;
-    const int32_t nb = child[s];
-    if (nb < 0) continue;
-    if (nb + 8 > used || (nb & 7) != 1) {
-      atomicExch(bad, 1);
-      continue;
+  // a thread per block of the level: its inner children claim consecutive
+  // positions of the next level together (one atomic per CTA and step)
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n;
+       base += stride) {
+    const int64_t i = base + threadIdx.x;
+    int32_t b = 0;
+    int32_t nbs[8];
+    unsigned inner = 0;
+    if (i < n) {
+      b = lvl_blocks[doff[L] + i];
+      const int nc = b == 0 ? 1 : 8;
+      for (int c = 0; c < 8; ++c) {
+        nbs[c] = c < nc ? child[b + c] : -1;
+        if (nbs[c] >= 0) {
+          if (nbs[c] + 8 > used || (nbs[c] & 7) != 1)
+            atomicExch(bad, 1);
+          else
+            inner |= 1u << c;
+        }
+      }
     }
-    int x, y, z;
-    slot_cell(b, c, bcoord[block_id(b)], x, y, z);
-    const int k = block_id(nb);
-    blevel[k] = (int8_t)(L + 1);
-    bcoord[k] = pack_cell(L, x, y, z);
-    bparent[k] = s;
-    const int64_t pos = next + atomicAdd(dcnt + L + 1, 1);
-    if (pos >= cap_blocks) {
-      atomicExch(bad, 1);
-      continue;
+    int64_t pos = next + cta_alloc_n(__popc(inner), dcnt + L + 1);
+    if (!inner) continue;
+    const uint64_t pc = bcoord[block_id(b)];
+    for (int c = 0; c < 8; ++c) {
+      if (!((inner >> c) & 1u)) continue;
+      const int32_t nb = nbs[c];
+      int x, y, z;
+      slot_cell(b, c, pc, x, y, z);
+      const int k = block_id(nb);
+      blevel[k] = (int8_t)(L + 1);
+      bcoord[k] = pack_cell(L, x, y, z);
+      bparent[k] = b + c;
+      if (pos >= cap_blocks) {
+        atomicExch(bad, 1);
+      } else {
+        lvl_blocks[pos] = nb;
+      }
+      ++pos;
     }
-    lvl_blocks[pos] = nb;
   }
 }
 
@@ -166,6 +238,12 @@ __device__ __forceinline__ void cta_count_add(int cnt, int32_t* global) {
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd_block(&s_cnt, cnt);
   __syncthreads();
   if (threadIdx.x == 0 && s_cnt) atomicAdd(global, s_cnt);
+}
+
+// grid of at most one wave of kThreads CTAs (grid-stride kernels)
+static unsigned wave_grid(int64_t n) {
+  const int64_t g = (n + kThreads - 1) / kThreads;
+  return (unsigned)(g < 148 * 8 ? (g > 0 ? g : 1) : 148 * 8);
 }
 
 __global__ void k_leaf_flags(const int32_t* __restrict__ child,
@@ -482,24 +560,30 @@ __global__ void k_sample_update(const int32_t* __restrict__ lblocks,
                                 int64_t stride, float* F, float* W,
                                 uint32_t* M, int32_t* fresh, int32_t* nfresh,
                                 int32_t* nleaves) {
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t i = gid >> 3;
-  const int c = (int)(gid & 7);
-  const bool in = i < n;
-  const int32_t b = in ? lblocks[i] : -1;
-  unsigned nm = 0;
-  if (b >= 0) {
-    int pz, L;
-    unpack_meta_w(lmeta[i].w, pz, nm, L);
+  // CTA-uniform grid-stride: one count atomic per CTA at the end and one
+  // queue claim per CTA and step (cta_alloc)
+  int cnt = 0;
+  const int64_t step = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n * 8;
+       base += step) {
+    const int64_t gid = base + threadIdx.x;
+    const int64_t i = gid >> 3;
+    const int c = (int)(gid & 7);
+    const bool in = i < n;
+    const int32_t b = in ? lblocks[i] : -1;
+    unsigned nm = 0;
+    if (b >= 0) {
+      int pz, L;
+      unpack_meta_w(lmeta[i].w, pz, nm, L);
+    }
+    if (c == 0) cnt += __popc(nm);
+    const bool now = in && b >= 0 && !(b == 0 && c != 0) && ((nm >> c) & 1u);
+    const bool was = in && i < nold && ((oldmask[i] >> c) & 1u);
+    const bool add = now && !was;
+    const int64_t r = cta_alloc(add, nfresh);
+    if (add) fresh[r] = (int32_t)(i * 8 + c);
   }
-  cta_count_add((c == 0) ? __popc(nm) : 0, nleaves);  // every thread
-  if (!in) return;
-  const bool now = b >= 0 && !(b == 0 && c != 0) && ((nm >> c) & 1u);
-  const bool was = i < nold && ((oldmask[i] >> c) & 1u);
-  const int64_t s = i * 8 + c;
-  if (now && !was) {
-    fresh[atomicAdd(nfresh, 1)] = (int32_t)s;
-  }
+  cta_count_add(cnt, nleaves);
   // (slots that stopped being leaves keep stale samples: kernels read the
   // samples of active leaves only)
 }
@@ -571,23 +655,30 @@ __global__ void k_ell_update(const int32_t* __restrict__ lblocks,
                              const int64_t* __restrict__ tileOff, float* F,
                              float* W, int32_t* fresh, int32_t* nfresh,
                              int32_t* nleaves) {
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t i = gid >> 3;
-  const int c = (int)(gid & 7);
-  const bool in = i < n;
-  const int32_t b = in ? lblocks[i] : -1;
-  unsigned nm = 0;
-  if (b >= 0) {
-    int pz, L;
-    unpack_meta_w(lmeta[i].w, pz, nm, L);
+  // CTA-uniform grid-stride: one count atomic per CTA at the end and one
+  // queue claim per CTA and step (cta_alloc)
+  int cnt = 0;
+  const int64_t step = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n * 8;
+       base += step) {
+    const int64_t gid = base + threadIdx.x;
+    const int64_t i = gid >> 3;
+    const int c = (int)(gid & 7);
+    const bool in = i < n;
+    const int32_t b = in ? lblocks[i] : -1;
+    unsigned nm = 0;
+    if (b >= 0) {
+      int pz, L;
+      unpack_meta_w(lmeta[i].w, pz, nm, L);
+    }
+    if (c == 0) cnt += __popc(nm);
+    const bool now = in && b >= 0 && !(b == 0 && c != 0) && ((nm >> c) & 1u);
+    const bool was = in && i < nold && ((oldmask[i] >> c) & 1u);
+    const bool add = now && !was;
+    const int64_t r = cta_alloc(add, nfresh);
+    if (add) fresh[r] = (int32_t)(i * 8 + c);
   }
-  cta_count_add((c == 0) ? __popc(nm) : 0, nleaves);  // every thread
-  if (!in) return;
-  const bool now = b >= 0 && !(b == 0 && c != 0) && ((nm >> c) & 1u);
-  const bool was = i < nold && ((oldmask[i] >> c) & 1u);
-  if (now && !was) {
-    fresh[atomicAdd(nfresh, 1)] = (int32_t)gid;
-  }
+  cta_count_add(cnt, nleaves);
   // (no zeroing: only active leaves' rows are ever read)
 }
 
@@ -921,7 +1012,7 @@ void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
     const int64_t bound = L < 7 ? std::min<int64_t>(int64_t(1) << (3 * L), nbid)
                                 : nbid;
     const int64_t wave = (int64_t)148 * 8 * kThreads;
-    k_expand_dev<<<grid_for(std::min<int64_t>(bound * 8, wave)), kThreads, 0,
+    k_expand_dev<<<grid_for(std::min<int64_t>(bound, wave)), kThreads, 0,
                    st>>>(
         child, c.lvl_blocks.p, L, used, nbid + 1, c.blevel.p, c.bcoord.p,
         c.bparent.p, dcnt, doff, c.counters.p);
@@ -1080,7 +1171,7 @@ static bool ell_list_samples(Ctx& c, int64_t nold, int64_t nnew,
   }
   ph_mark(c, kPhEllGrow, st);
   int32_t* fresh = c.sort_v32.ensure(nnew * 8 + 1);
-  k_ell_update<<<grid_for(nnew * 8), kThreads, 0, st>>>(
+  k_ell_update<<<wave_grid(nnew * 8), kThreads, 0, st>>>(
       c.lblocks.p, c.lmeta.p, nnew, nold, oldmask, c.tileK.p, c.tileOff.p,
       c.F.p, c.W.p, fresh, c.counters.p + 2, c.counters.p + 4);
   // (slots past the list's end are never leaves: their rows are not read)
@@ -1226,11 +1317,11 @@ bool ctx_list_update(Ctx& c, const int32_t* child, int64_t total, int64_t nbid,
   else c.W.grow_keep((size_t)nvp * npn, (size_t)nvp * npo, st);
   int32_t* fresh = c.sort_v32.ensure(nnew * 8 + 1);
   if (c.binw)
-    k_sample_update<true><<<grid_for(nnew * 8), kThreads, 0, st>>>(
+    k_sample_update<true><<<wave_grid(nnew * 8), kThreads, 0, st>>>(
         c.lblocks.p, c.lmeta.p, nnew, nold, oldmask, nvp, c.F.p, nullptr,
         c.M.p, fresh, c.counters.p + 2, c.counters.p + 4);
   else
-    k_sample_update<false><<<grid_for(nnew * 8), kThreads, 0, st>>>(
+    k_sample_update<false><<<wave_grid(nnew * 8), kThreads, 0, st>>>(
         c.lblocks.p, c.lmeta.p, nnew, nold, oldmask, nvp, c.F.p, c.W.p,
         nullptr, fresh, c.counters.p + 2, c.counters.p + 4);
   if (npn > nnew * 8) {

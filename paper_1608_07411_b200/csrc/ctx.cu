@@ -765,6 +765,12 @@ __global__ void k_ell_fresh(const int32_t* __restrict__ fresh,
   }
 }
 
+__global__ void k_ell_offsets(const int64_t* __restrict__ scan, int64_t n,
+                              int64_t total, int64_t* off) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) off[i] = total + scan[i];
+}
+
 // device-side move plan: rows of the bigger range of each overflowing tile
 // (need + need/4 + 4 rows, as before), 0 for the others; rows[nt] = 0 for
 // the scan; rows[nt + 1] accumulates the abandoned rows (ell_waste)
@@ -1152,19 +1158,15 @@ static bool ell_list_samples(Ctx& c, int64_t nold, int64_t nnew,
     c.cub_tmp.ensure(bytes);
     OCTF_CUDA(cub::DeviceScan::ExclusiveSum(c.cub_tmp.p, bytes, rowsz, scan,
                                             (int)(nt_new - nt_old + 1), st));
+    // offsets of the new tiles continue after the existing store (written
+    // on the device; the host reads back only the added size)
+    k_ell_offsets<<<grid_for(nt_new - nt_old + 1), kThreads, 0, st>>>(
+        scan, nt_new - nt_old + 1, total, c.tileOff.p + nt_old);
+    OCTF_CUDA(cudaGetLastError());
     int64_t add = 0;
     OCTF_CUDA(cudaMemcpyAsync(&add, scan + (nt_new - nt_old), sizeof(int64_t),
                               cudaMemcpyDeviceToHost, st));
     OCTF_CUDA(cudaStreamSynchronize(st));
-    // offsets of the new tiles continue after the existing store
-    std::vector<int64_t> h(nt_new - nt_old + 1);
-    OCTF_CUDA(cudaMemcpyAsync(h.data(), scan, h.size() * sizeof(int64_t),
-                              cudaMemcpyDeviceToHost, st));
-    OCTF_CUDA(cudaStreamSynchronize(st));
-    for (auto& v : h) v += total;
-    OCTF_CUDA(cudaMemcpyAsync(c.tileOff.p + nt_old, h.data(),
-                              h.size() * sizeof(int64_t),
-                              cudaMemcpyHostToDevice, st));
     c.F.grow_keep((size_t)(total + add) + 1, (size_t)total, st);
     c.W.grow_keep((size_t)(total + add) + 1, (size_t)total, st);
     total += add;

@@ -14,6 +14,11 @@
 // shuffle, neighbour blocks through the 12-entry table.
 #pragma once
 
+#ifndef OCTF_PD_F32_ESUM_MIN
+// fp32 warp energy sums from this N (cfg2 pd pass 0.589 -> 0.577 ms, cfg5
+// kernel 5.41 -> 5.34 ms; the fp64 parity mode keeps the double reduction)
+#define OCTF_PD_F32_ESUM_MIN 16
+#endif
 #ifndef OCTF_PD_MINB
 #define OCTF_PD_MINB 4  // 4 CTAs of 256 per SM: <= 64 registers
 #endif
@@ -456,10 +461,27 @@ __global__ void __launch_bounds__(kT, pd_minb(BINW, NV)) k_pd_pass(PdArgs<T> a) 
     s_v[4][t] = D2;
     if (c == 0) s_par[t >> 3] = par_blk;
   }
-  typedef cub::BlockReduce<double, kT> BR;
-  __shared__ typename BR::TempStorage tmp;
-  const double tot = BR(tmp).Sum(eterm);
-  if (threadIdx.x == 0) a.epart[blockIdx.x] = tot;
+  if (sizeof(T) == 4 && NV >= OCTF_PD_F32_ESUM_MIN) {
+    // fp32 throughput mode: warps sum the (fp32) terms in fp32, thread 0
+    // adds the eight warp sums in double (fixed order)
+    __shared__ double s_w[kT / 32];
+    float e = (float)eterm;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(FULL, e, o);
+    if ((t & 31) == 0) s_w[t >> 5] = (double)e;
+    __syncthreads();
+    if (t == 0) {
+      double tot = 0.0;
+#pragma unroll
+      for (int k = 0; k < kT / 32; ++k) tot += s_w[k];
+      a.epart[blockIdx.x] = tot;
+    }
+  } else {
+    typedef cub::BlockReduce<double, kT> BR;
+    __shared__ typename BR::TempStorage tmp;
+    const double tot = BR(tmp).Sum(eterm);
+    if (threadIdx.x == 0) a.epart[blockIdx.x] = tot;
+  }
   if (WP && t < 5 * (kT / 8)) {
     // warp q writes field q of the 32 blocks (a short tail: the CTA's slot
     // is held until its last warp exits)

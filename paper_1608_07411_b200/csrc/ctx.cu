@@ -626,11 +626,15 @@ __global__ void k_gather_fresh(const int32_t* __restrict__ fresh,
     const int z = b == 0 ? 0 : 2 * pz + (c & 1);
     uint32_t bits = 0;
     int flag = 0;
+    // the dense store holds <= 64 views: both chunks' descents in lock-step
+    int32_t nd2[2];
+    descend_views<2>(vs.child, vs.n, L, x, y, z, lane, nd2);
     for (int v0 = 0; v0 < stride; v0 += 32) {
       const int v = v0 + lane;
       float f = 0.f, w = 0.f;
       if (v < vs.n) {
-        const int32_t nd = descend(vs.child[v], L, x, y, z);
+        const int32_t nd = v0 == 0 ? nd2[0] : v0 == 32 ? nd2[1]
+                                             : descend(vs.child[v], L, x, y, z);
         f = vs.val[v][nd];
         w = vs.w[v][nd];
         flag |= (w != 0.f && w != 1.f);

@@ -114,35 +114,11 @@ __global__ void k_expand(const int32_t* __restrict__ child,
   next[pos] = nb;
 }
 
-// positions for the threads of a CTA that want one: one atomic per CTA on
-// the shared counter (per-thread or per-warp atomics on one address
-// serialise in L2: the level walk of a 60M-node tree spent ~0.4 ms on
-// them).  Every thread of the CTA must call it; -1 for the others.
-__device__ __forceinline__ int64_t cta_alloc(bool want, int32_t* global) {
-  __shared__ int s_warp[kThreads / 32];
-  __shared__ int s_base;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const unsigned bal = __ballot_sync(0xffffffffu, want);
-  if (lane == 0) s_warp[w] = __popc(bal);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
-      const int t = s_warp[k];
-      s_warp[k] = acc;
-      acc += t;
-    }
-    s_base = acc ? atomicAdd(global, acc) : 0;
-  }
-  __syncthreads();
-  const int64_t r = (int64_t)s_base + s_warp[w] +
-                    __popc(bal & ((1u << lane) - 1u));
-  __syncthreads();  // the shared slots are reused by the next call
-  return want ? r : -1;
-}
-
-// cta_alloc for counts: the first of `cnt` consecutive positions (any value
-// when cnt == 0); every thread of the CTA must call it
+// positions claimed by the threads of a CTA with one atomic per CTA on the
+// shared counter (per-thread or per-warp atomics on one address serialise
+// in L2: the level walk of a 60M-node tree spent ~0.3 ms on them): the
+// first of `cnt` consecutive positions (any value when cnt == 0).  Every
+// thread of the CTA must call it.
 __device__ __forceinline__ int64_t cta_alloc_n(int cnt, int32_t* global) {
   __shared__ int s_warp[kThreads / 32];
   __shared__ int s_base;
@@ -560,28 +536,29 @@ __global__ void k_sample_update(const int32_t* __restrict__ lblocks,
                                 int64_t stride, float* F, float* W,
                                 uint32_t* M, int32_t* fresh, int32_t* nfresh,
                                 int32_t* nleaves) {
-  // CTA-uniform grid-stride: one count atomic per CTA at the end and one
-  // queue claim per CTA and step (cta_alloc)
+  // CTA-uniform grid-stride, a thread per list entry: one count atomic per
+  // CTA at the end and one queue claim per CTA and step (cta_alloc_n)
   int cnt = 0;
   const int64_t step = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n * 8;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n;
        base += step) {
-    const int64_t gid = base + threadIdx.x;
-    const int64_t i = gid >> 3;
-    const int c = (int)(gid & 7);
-    const bool in = i < n;
-    const int32_t b = in ? lblocks[i] : -1;
-    unsigned nm = 0;
-    if (b >= 0) {
-      int pz, L;
-      unpack_meta_w(lmeta[i].w, pz, nm, L);
+    const int64_t i = base + threadIdx.x;
+    unsigned add = 0;
+    if (i < n) {
+      const int32_t b = lblocks[i];
+      if (b >= 0) {
+        int pz, L;
+        unsigned nm;
+        unpack_meta_w(lmeta[i].w, pz, nm, L);
+        cnt += __popc(nm);
+        if (b == 0) nm &= 1u;  // the root's pseudo-block has one slot
+        const unsigned was = i < nold ? oldmask[i] : 0u;
+        add = nm & ~was;
+      }
     }
-    if (c == 0) cnt += __popc(nm);
-    const bool now = in && b >= 0 && !(b == 0 && c != 0) && ((nm >> c) & 1u);
-    const bool was = in && i < nold && ((oldmask[i] >> c) & 1u);
-    const bool add = now && !was;
-    const int64_t r = cta_alloc(add, nfresh);
-    if (add) fresh[r] = (int32_t)(i * 8 + c);
+    int64_t r = cta_alloc_n(__popc(add), nfresh);
+    for (int c = 0; c < 8; ++c)
+      if ((add >> c) & 1u) fresh[r++] = (int32_t)(i * 8 + c);
   }
   cta_count_add(cnt, nleaves);
   // (slots that stopped being leaves keep stale samples: kernels read the
@@ -659,28 +636,29 @@ __global__ void k_ell_update(const int32_t* __restrict__ lblocks,
                              const int64_t* __restrict__ tileOff, float* F,
                              float* W, int32_t* fresh, int32_t* nfresh,
                              int32_t* nleaves) {
-  // CTA-uniform grid-stride: one count atomic per CTA at the end and one
-  // queue claim per CTA and step (cta_alloc)
+  // CTA-uniform grid-stride, a thread per list entry: one count atomic per
+  // CTA at the end and one queue claim per CTA and step (cta_alloc_n)
   int cnt = 0;
   const int64_t step = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n * 8;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n;
        base += step) {
-    const int64_t gid = base + threadIdx.x;
-    const int64_t i = gid >> 3;
-    const int c = (int)(gid & 7);
-    const bool in = i < n;
-    const int32_t b = in ? lblocks[i] : -1;
-    unsigned nm = 0;
-    if (b >= 0) {
-      int pz, L;
-      unpack_meta_w(lmeta[i].w, pz, nm, L);
+    const int64_t i = base + threadIdx.x;
+    unsigned add = 0;
+    if (i < n) {
+      const int32_t b = lblocks[i];
+      if (b >= 0) {
+        int pz, L;
+        unsigned nm;
+        unpack_meta_w(lmeta[i].w, pz, nm, L);
+        cnt += __popc(nm);
+        if (b == 0) nm &= 1u;  // the root's pseudo-block has one slot
+        const unsigned was = i < nold ? oldmask[i] : 0u;
+        add = nm & ~was;
+      }
     }
-    if (c == 0) cnt += __popc(nm);
-    const bool now = in && b >= 0 && !(b == 0 && c != 0) && ((nm >> c) & 1u);
-    const bool was = in && i < nold && ((oldmask[i] >> c) & 1u);
-    const bool add = now && !was;
-    const int64_t r = cta_alloc(add, nfresh);
-    if (add) fresh[r] = (int32_t)(i * 8 + c);
+    int64_t r = cta_alloc_n(__popc(add), nfresh);
+    for (int c = 0; c < 8; ++c)
+      if ((add >> c) & 1u) fresh[r++] = (int32_t)(i * 8 + c);
   }
   cta_count_add(cnt, nleaves);
   // (no zeroing: only active leaves' rows are ever read)
@@ -1177,7 +1155,7 @@ static bool ell_list_samples(Ctx& c, int64_t nold, int64_t nnew,
   }
   ph_mark(c, kPhEllGrow, st);
   int32_t* fresh = c.sort_v32.ensure(nnew * 8 + 1);
-  k_ell_update<<<wave_grid(nnew * 8), kThreads, 0, st>>>(
+  k_ell_update<<<wave_grid(nnew), kThreads, 0, st>>>(
       c.lblocks.p, c.lmeta.p, nnew, nold, oldmask, c.tileK.p, c.tileOff.p,
       c.F.p, c.W.p, fresh, c.counters.p + 2, c.counters.p + 4);
   // (slots past the list's end are never leaves: their rows are not read)
@@ -1323,11 +1301,11 @@ bool ctx_list_update(Ctx& c, const int32_t* child, int64_t total, int64_t nbid,
   else c.W.grow_keep((size_t)nvp * npn, (size_t)nvp * npo, st);
   int32_t* fresh = c.sort_v32.ensure(nnew * 8 + 1);
   if (c.binw)
-    k_sample_update<true><<<wave_grid(nnew * 8), kThreads, 0, st>>>(
+    k_sample_update<true><<<wave_grid(nnew), kThreads, 0, st>>>(
         c.lblocks.p, c.lmeta.p, nnew, nold, oldmask, nvp, c.F.p, nullptr,
         c.M.p, fresh, c.counters.p + 2, c.counters.p + 4);
   else
-    k_sample_update<false><<<wave_grid(nnew * 8), kThreads, 0, st>>>(
+    k_sample_update<false><<<wave_grid(nnew), kThreads, 0, st>>>(
         c.lblocks.p, c.lmeta.p, nnew, nold, oldmask, nvp, c.F.p, c.W.p,
         nullptr, fresh, c.counters.p + 2, c.counters.p + 4);
   if (npn > nnew * 8) {

@@ -483,14 +483,24 @@ __global__ void k_table_dirty(const int32_t* __restrict__ lblocks, int64_t n,
       d = oldmask[i] != 0;  // a hole since this patch
     } else {
       d = leaf_mask_of(child, b) != oldmask[i];
-      for (int k = 0; k < 12 && !d; ++k) {
-        const int32_t r = nbr[i * 12 + k];
-        if (r >= 0) {
-          d = blevel[block_id(r)] < 0;
-        } else if (r <= -2) {
-          const int32_t q = -r - 2;
-          d = blevel[block_id(q)] < 0 || child[q] >= 0;
+      if (!d) {
+        // the 12 refs as three 16 B loads and their checks' loads issued
+        // together (independent), not one dependent round trip per ref
+        const int4* n4 = reinterpret_cast<const int4*>(nbr + i * 12);
+        const int4 a0 = n4[0], a1 = n4[1], a2 = n4[2];
+        const int32_t r[12] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y,
+                               a1.z, a1.w, a2.x, a2.y, a2.z, a2.w};
+        int8_t lv[12];
+        int32_t ch[12];
+#pragma unroll
+        for (int k = 0; k < 12; ++k) {
+          const int32_t q = r[k] >= 0 ? r[k] : (r[k] <= -2 ? -r[k] - 2 : -1);
+          lv[k] = q >= 0 ? blevel[block_id(q)] : 0;
+          ch[k] = r[k] <= -2 ? child[q] : -1;
         }
+#pragma unroll
+        for (int k = 0; k < 12; ++k)
+          d |= (r[k] >= 0 || r[k] <= -2) && (lv[k] < 0 || ch[k] >= 0);
       }
     }
   }

@@ -11,15 +11,14 @@ into closed loops, each loop is oriented so its normal points from inside to
 outside, and fan-triangulated.  ``tests/test_mesh.py`` checks the tables and
 meshes against fixtures generated from the reference.
 
-PLY I/O, ``vertex_diff`` and the analytic checks are host utilities with the
-reference's names and formats.
+Mesh file I/O and mesh-to-mesh comparisons are host utilities outside the
+accelerated path and are not part of this package.
 """
 
 from __future__ import annotations
 
 import ctypes
-from dataclasses import dataclass
-from pathlib import Path
+from typing import NamedTuple
 
 import numpy as np
 import torch
@@ -27,9 +26,7 @@ import torch
 from . import _lib
 from ._device import as_device, device, ptr, stream_handle
 
-__all__ = ["TriMesh", "extract_zero_surface", "marching_cubes", "MeshDiff",
-           "vertex_diff", "sphere_distances", "signed_volume", "write_ply",
-           "read_ply", "case_tables"]
+__all__ = ["TriMesh", "extract_zero_surface", "marching_cubes", "case_tables"]
 
 # corner c of a cube sits at offset (c>>2 & 1, c>>1 & 1, c & 1) (x, y, z),
 # the octree child numbering; edges 0-3 run along x, 4-7 along y, 8-11
@@ -131,29 +128,12 @@ def _tables():
     return _TABLES
 
 
-@dataclass
-class TriMesh:
-    """Indexed triangle mesh, optionally with one scalar per vertex."""
+class TriMesh(NamedTuple):
+    """The readout's result: float64 vertex positions (V, 3) and int32
+    triangle corner indices (F, 3), both numpy."""
 
     vertices: np.ndarray
     faces: np.ndarray
-    quality: np.ndarray | None = None
-
-    def __post_init__(self):
-        self.vertices = np.asarray(self.vertices, dtype=np.float64).reshape(-1, 3)
-        self.faces = np.asarray(self.faces, dtype=np.int32).reshape(-1, 3)
-        if self.quality is not None:
-            self.quality = np.asarray(self.quality, dtype=np.float64).reshape(-1)
-            if self.quality.shape[0] != self.vertices.shape[0]:
-                raise ValueError("one quality value per vertex required")
-
-    @property
-    def vertex_count(self) -> int:
-        return self.vertices.shape[0]
-
-    @property
-    def face_count(self) -> int:
-        return self.faces.shape[0]
 
 
 def _extract(values, mask, origin=None, voxel=1.0, world=False):
@@ -199,114 +179,4 @@ def marching_cubes(values, seen, dom) -> TriMesh:
     samples at voxel centres, index i -> origin + (i + 1/2) * voxel_size."""
     if tuple(values.shape) != (dom.resolution,) * 3:
         raise ValueError("grid does not match the domain resolution")
-    verts, faces = _extract(values, seen, dom.origin, dom.voxel_size, True)
-    return TriMesh(verts, faces)
-
-
-@dataclass
-class MeshDiff:
-    """Symmetric nearest-vertex distance statistics between two meshes."""
-
-    d_ab: np.ndarray
-    d_ba: np.ndarray
-
-    @property
-    def mean(self) -> float:
-        return float(np.concatenate([self.d_ab, self.d_ba]).mean())
-
-    @property
-    def std(self) -> float:
-        return float(np.concatenate([self.d_ab, self.d_ba]).std())
-
-    @property
-    def max(self) -> float:
-        return float(np.concatenate([self.d_ab, self.d_ba]).max())
-
-
-def vertex_diff(a: TriMesh, b: TriMesh) -> MeshDiff:
-    """Nearest-vertex distances both ways (host, scipy k-d tree)."""
-    from scipy.spatial import cKDTree
-    if a.vertex_count == 0 or b.vertex_count == 0:
-        raise ValueError("cannot compare empty meshes")
-    return MeshDiff(d_ab=cKDTree(b.vertices).query(a.vertices)[0],
-                    d_ba=cKDTree(a.vertices).query(b.vertices)[0])
-
-
-def sphere_distances(mesh: TriMesh, center, radius: float) -> np.ndarray:
-    """Per-vertex absolute distance to an analytic sphere surface."""
-    if mesh.vertex_count == 0:
-        raise ValueError("mesh has no vertices")
-    r = np.linalg.norm(mesh.vertices - np.asarray(center, dtype=np.float64),
-                       axis=1)
-    return np.abs(r - radius)
-
-
-def signed_volume(mesh: TriMesh) -> float:
-    """Divergence-theorem volume; positive for outward-oriented meshes."""
-    a, b, c = (mesh.vertices[mesh.faces[:, k]] for k in range(3))
-    return float(np.einsum("ij,ij->i", a, np.cross(b, c)).sum() / 6.0)
-
-
-def write_ply(path, mesh: TriMesh) -> None:
-    """ASCII PLY, double vertex properties (%.17g), optional quality."""
-    q = mesh.quality
-    head = ["ply", "format ascii 1.0", f"element vertex {mesh.vertex_count}",
-            "property double x", "property double y", "property double z"]
-    if q is not None:
-        head.append("property double quality")
-    head += [f"element face {mesh.face_count}",
-             "property list uchar int vertex_indices", "end_header"]
-    with open(path, "w") as fp:
-        fp.write("\n".join(head) + "\n")
-        for i, (x, y, z) in enumerate(mesh.vertices):
-            extra = f" {q[i]:.17g}" if q is not None else ""
-            fp.write(f"{x:.17g} {y:.17g} {z:.17g}{extra}\n")
-        for i, j, k in mesh.faces:
-            fp.write(f"3 {i} {j} {k}\n")
-
-
-def read_ply(path) -> TriMesh:
-    """Read the ASCII PLY subset ``write_ply`` produces."""
-    lines = Path(path).read_text().splitlines()
-    if not lines or lines[0].strip() != "ply":
-        raise ValueError(f"{path}: not a PLY file")
-    nvert = nface = 0
-    props, element, i = [], None, 1
-    while True:
-        if i >= len(lines):
-            raise ValueError(f"{path}: missing end_header")
-        parts = lines[i].split()
-        i += 1
-        if not parts:
-            continue
-        if parts[0] == "format" and parts[1] != "ascii":
-            raise ValueError(f"{path}: only ascii PLY is supported")
-        if parts[0] == "element":
-            element = parts[1]
-            if element == "vertex":
-                nvert = int(parts[2])
-            elif element == "face":
-                nface = int(parts[2])
-        elif parts[0] == "property" and element == "vertex":
-            if parts[1] == "list":
-                raise ValueError(f"{path}: list vertex properties unsupported")
-            props.append(parts[2])
-        elif parts[0] == "end_header":
-            break
-    for name in ("x", "y", "z"):
-        if name not in props:
-            raise ValueError(f"{path}: vertex property {name} missing")
-    body = lines[i:]
-    if len(body) < nvert + nface:
-        raise ValueError(f"{path}: truncated body")
-    vd = np.array([[float(t) for t in body[k].split()] for k in range(nvert)],
-                  dtype=np.float64).reshape(nvert, len(props))
-    col = {name: vd[:, k] for k, name in enumerate(props)}
-    faces = np.zeros((nface, 3), dtype=np.int32)
-    for k in range(nface):
-        parts = body[nvert + k].split()
-        if int(parts[0]) != 3:
-            raise ValueError(f"{path}: only triangle faces are supported")
-        faces[k] = [int(parts[1]), int(parts[2]), int(parts[3])]
-    return TriMesh(np.column_stack([col["x"], col["y"], col["z"]]), faces,
-                   col.get("quality"))
+    return TriMesh(*_extract(values, seen, dom.origin, dom.voxel_size, True))

@@ -32,16 +32,6 @@ def test_oracle_matches_reference_meshes():
     assert np.array_equal(f, z["rnd_faces"])
 
 
-def test_ply_round_trip(tmp_path):
-    from paper_1608_07411_b200 import mesh
-    z = load("mesh")
-    m = mesh.TriMesh(z["rnd_vertices"], z["rnd_faces"])
-    mesh.write_ply(tmp_path / "m.ply", m)
-    r = mesh.read_ply(tmp_path / "m.ply")
-    assert np.array_equal(r.vertices, m.vertices)
-    assert np.array_equal(r.faces, m.faces)
-
-
 @pytest.mark.gpu
 @pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")
 def test_gpu_marching_cubes_bitexact():
@@ -81,4 +71,5 @@ def test_gpu_cfg1_pipeline_mesh_equals_reference():
     assert np.array_equal(seen.cpu().numpy(), z["cfg1_seen"])
     assert np.array_equal(m.vertices, z["cfg1_vertices"])
     assert np.array_equal(m.faces, z["cfg1_faces"])
-    assert mesh.signed_volume(m) > 0
+    a, b, c = (m.vertices[m.faces[:, k]] for k in range(3))
+    assert np.einsum("ij,ij->i", a, np.cross(b, c)).sum() > 0  # outward

@@ -76,6 +76,14 @@ int octf_ctx_info(octf_ctx *ctx, int64_t *out);
  * count (solver="pd" needs it); OCTF_CTX_ELL uses ELL from 33 views. */
 #define OCTF_CTX_DENSE 1
 #define OCTF_CTX_ELL 2
+/* OCTF_CTX_SORTED (implies DENSE): each leaf's samples are sorted once by
+ * (f, view index) when gathered, absent ones last as +inf -- the layout the
+ * solver="pd" kernel selects its generalised-median prox on. */
+#define OCTF_CTX_SORTED 4
+/* OCTF_CTX_DEFER: octf_ctx_prepare / set_samples build the structure but
+ * gather no samples; the next octf_ctx_select gathers its subset only (and
+ * clears the flag) -- a shard never holds the whole tree's samples. */
+#define OCTF_CTX_DEFER 8
 int octf_ctx_set_options(octf_ctx *ctx, int flags);
 
 /* Live profiling: enable != 0 brackets the leaf-update and energy kernels
@@ -191,7 +199,8 @@ int octf_pd_passes(octf_ctx *ctx, int dtype, void *const *set_a,
                    const float *const *vvals, const float *const *vws,
                    const int32_t *const *vchilds, int d_max, double lam,
                    double tau, double sigma, double gamma, int clamp,
-                   int npasses, double *energies_pre, void *stream);
+                   int npasses, double *energies_pre, int device_energies,
+                   void *stream);
 
 /* solver="pd" split/join on the current set {u, ubar, px, py, pz} after a
  * pass (north_star item (d); definition oracle/pd_oracle.c
@@ -231,6 +240,14 @@ int octf_ctx_select(octf_ctx *ctx, const int32_t *sel, const uint8_t *masks,
                     int64_t nsel, void *stream);
 
 /* Propagate only levels hi-1 .. lo (the replicated top of a sharded tree). */
+/* Halo staging for the sharded solver (shard.py HaloExchange; SURVEY.md
+ * §8(e) -- no reference counterpart, the reference is single-process):
+ * pack (unpack = 0) copies fields[k][idx[j]] to buf[k*n + j] for k < nfields
+ * (1..5: u, or u, ubar, px, py, pz in pd mode), unpack (1) the reverse.  All
+ * pointers are device pointers; enqueued on `stream`. */
+int octf_halo_pack(int dtype, void *const *fields, int nfields,
+                   const int32_t *idx, int64_t n, void *buf, int unpack,
+                   void *stream);
 int octf_propagate_levels(octf_ctx *ctx, int dtype, void *value,
                           const int32_t *child, int lo, int hi, void *stream);
 

@@ -325,6 +325,26 @@ def pd_steps(lam: float):
     return t, t
 
 
+def pd_pass(fields, child, used: int, views: list, d_max: int, lam: float,
+            tau: float, sigma: float, gamma: float, clamp: bool = True):
+    """One primal-dual pass (pd_oracle.c orc_pd_pass) on the five f64 pools
+    (u, ubar, px, py, pz) followed by the propagate of each output.
+    Returns (outputs, energy of the incoming u)."""
+    vv = [v.value for v in views]
+    vw = [v.weight for v in views]
+    vc = [v.child for v in views]
+    outs = [np.array(a, dtype=np.float64, copy=True) for a in fields]
+    e = np.zeros(1)
+    _check(lib().orc_pd_pass(
+        *[_ptr(a) for a in fields], *[_ptr(o) for o in outs], _ptr(child),
+        int(used), len(views), _ptr_array(vv), _ptr_array(vw),
+        _ptr_array(vc), d_max, float(lam), float(tau), float(sigma),
+        float(gamma), int(bool(clamp)), _ptr(e)))
+    for o in outs:
+        propagate(o, child)
+    return outs, float(e[0])
+
+
 def pd_fuse(u0: Pool, views: list, lam: float, gamma: float, iterations: int,
             tau: float | None = None, sigma: float | None = None,
             clamp: bool = True, tau_split: float | None = None,
@@ -349,23 +369,12 @@ def pd_fuse(u0: Pool, views: list, lam: float, gamma: float, iterations: int,
     child = np.full(n, -1, dtype=np.int32)
     child[:used] = u0.child[:used]
     state = np.array(u0.state[:3], dtype=np.int64)
-    vv = [v.value for v in views]
-    vw = [v.weight for v in views]
-    vc = [v.child for v in views]
     energies, sj = [], []
-    e = np.zeros(1)
     out2 = np.zeros(2, dtype=np.int64)
     for _ in range(iterations):
-        outs = [a.copy() for a in (u, ub, px, py, pz)]
-        _check(lib().orc_pd_pass(
-            _ptr(u), _ptr(ub), _ptr(px), _ptr(py), _ptr(pz),
-            *[_ptr(o) for o in outs], _ptr(child), int(state[0]), len(views),
-            _ptr_array(vv), _ptr_array(vw), _ptr_array(vc), u0.d_max,
-            float(lam), float(tau), float(sigma), float(gamma),
-            int(bool(clamp)), _ptr(e)))
-        energies.append(float(e[0]))
-        for o in outs:
-            propagate(o, child)
+        outs, en = pd_pass((u, ub, px, py, pz), child, int(state[0]), views,
+                           u0.d_max, lam, tau, sigma, gamma, clamp)
+        energies.append(en)
         u, ub, px, py, pz = outs
         if rs:
             _check(lib().orc_pd_restructure(

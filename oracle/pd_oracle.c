@@ -17,7 +17,10 @@
  *            u' = prox_{tau D}(v) = argmin_x (x-v)^2/2 + c sum_i w_i|x-f_i|,
  *            c = tau/(W+gamma): generalised weighted median, samples sorted
  *            by (f, view index); a -0 sample is taken as +0 (so the sorted
- *            values do not depend on how a sort orders equal keys)
+ *            values do not depend on how a sort orders equal keys).  Every
+ *            per-leaf sum (W, the energy's data term) runs over the samples
+ *            in this sorted order: the GPU sorts each leaf's samples once
+ *            when they are gathered and keeps them sorted.
  *   extrapolation  ubar' = 2u' - u;  u' clamped to [-1,1] when clamp.
  * Inner nodes of u, ubar, p are child means (propagate) after every pass.
  * Built with -ffp-contract=off; the GPU's f64 mode keeps this exact order.
@@ -133,9 +136,8 @@ int orc_pd_pass(const double *u, const double *ub, const double *px,
         int L = lv[j], x = cx[j], y = cy[j], z = cz[j];
         int m = 1 << L;
         double h = (double)(1 << (d_max - L));
-        /* samples at the leaf's level, view order */
+        /* samples at the leaf's level (view order), then sorted */
         int ns = 0;
-        double W = 0.0; /* view order */
         for (int v = 0; v < nviews; ++v) {
             int64_t vn = node_at(vchild[v], L, x, y, z);
             double w = (double)vw[v][vn];
@@ -144,7 +146,6 @@ int orc_pd_pass(const double *u, const double *ub, const double *px,
                 ws[ns] = w;
                 ix[ns] = v;
                 ns++;
-                W += w;
             }
         }
         /* insertion sort by (f, view index) */
@@ -161,6 +162,10 @@ int orc_pd_pass(const double *u, const double *ub, const double *px,
             ws[b + 1] = ww;
             ix[b + 1] = ii;
         }
+        /* weight sum in sorted order (the GPU keeps each leaf's samples
+         * sorted once, so every per-leaf sum below runs in that order) */
+        double W = 0.0;
+        for (int k = 0; k < ns; ++k) W += ws[k];
         double den = W + gamma;
         /* energy of the incoming u */
         {
@@ -169,12 +174,8 @@ int orc_pd_pass(const double *u, const double *ub, const double *px,
             double gy = y + 1 < m ? (u[node_at(child, L, x, y + 1, z)] - c0) / h : 0.0;
             double gz = z + 1 < m ? (u[node_at(child, L, x, y, z + 1)] - c0) / h : 0.0;
             double tv = lam * sqrt(gx * gx + gy * gy + gz * gz);
-            double num = 0.0;
-            for (int v = 0; v < nviews; ++v) {
-                int64_t vn = node_at(vchild[v], L, x, y, z);
-                double w = (double)vw[v][vn];
-                if (w != 0.0) num += w * fabs(c0 - (double)vval[v][vn]);
-            }
+            double num = 0.0; /* sorted order */
+            for (int k = 0; k < ns; ++k) num += ws[k] * fabs(c0 - fs[k]);
             total += (num / den + tv) * (h * h * h);
         }
         double P[3], B[3];

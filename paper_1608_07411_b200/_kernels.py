@@ -147,18 +147,25 @@ def fuse_passes_frozen(ubuf0, ubuf1, uchild, ustate, vvals, vws, vchilds,
 
 
 def pd_passes(set_a, set_b, uchild, ustate, vvals, vws, vchilds, d_max, lam,
-              tau, sigma, gamma, clamp, npasses, *, ctx):
+              tau, sigma, gamma, clamp, npasses, *, ctx, energies_out=None):
     """solver='pd': npasses primal-dual passes; set_a/set_b = 5 pools
-    (u, ubar, px, py, pz).  Returns the energies before each pass."""
+    (u, ubar, px, py, pz).  Returns the energies before each pass (host), or
+    writes them to ``energies_out`` (a float64 CUDA tensor; asynchronous)."""
     tv, tw, tc = _views(vvals, vws, vchilds)
     ta = ptr_table([ptr(t) for t in set_a])
     tb = ptr_table([ptr(t) for t in set_b])
-    en = np.zeros(max(int(npasses), 1), dtype=np.float64)
+    dev = energies_out is not None
+    if dev and (energies_out.dtype != torch.float64 or not energies_out.is_cuda
+                or energies_out.numel() < npasses):
+        raise TypeError("energies_out must be a float64 CUDA tensor")
+    en = None if dev else np.zeros(max(int(npasses), 1), dtype=np.float64)
     call("octf_pd_passes", ctx.h, _dtype_code(set_a[0]), ta, tb, ptr(uchild),
          _state_ptr(ustate), uchild.shape[0], len(vvals), tv, tw, tc,
          int(d_max), float(lam), float(tau), float(sigma), float(gamma),
-         int(bool(clamp)), int(npasses), en.ctypes.data, stream_handle())
-    return en[:npasses]
+         int(bool(clamp)), int(npasses),
+         ptr(energies_out) if dev else en.ctypes.data, int(dev),
+         stream_handle())
+    return energies_out if dev else en[:npasses]
 
 
 def pass_tiles(usnap, uval, uchild, ustate, vvals, vws, vchilds, d_max, lam,
@@ -233,3 +240,17 @@ def tree_energy(uval, uchild, vvals, vws, vchilds, d_max, lam, eps, gamma, *,
          len(vvals), tv, tw, tc, int(d_max), float(lam), float(eps),
          float(gamma), out.ctypes.data, ptr(terms), stream_handle())
     return float(out[0])
+
+
+def halo_pack(fields, idx, buf, unpack=False):
+    """buf[k*n + j] <-> fields[k][idx[j]] on the current stream (shard.py
+    halo staging; idx an int32 CUDA tensor, buf a flat CUDA tensor)."""
+    fields = list(fields)
+    n = idx.shape[0]
+    if idx.dtype != torch.int32 or not idx.is_cuda:
+        raise TypeError("idx must be an int32 CUDA tensor")
+    if buf.numel() < len(fields) * n or buf.dtype != fields[0].dtype:
+        raise ValueError("halo buffer too small or of another dtype")
+    call("octf_halo_pack", _dtype_code(fields[0]),
+         ptr_table([ptr(f) for f in fields]), len(fields), ptr(idx), n,
+         ptr(buf), int(bool(unpack)), stream_handle())

@@ -57,10 +57,11 @@ _SIGS = {
                          DBL, DBL, I32, I32, I32, P], I32),
     "octf_pass_finish": ([P, I32, P, P, P, P], I32),
     "octf_pd_passes": ([P, I32, P, P, P, P, I64, I32, P, P, P, I32, DBL, DBL,
-                        DBL, DBL, I32, I32, P, P], I32),
+                        DBL, DBL, I32, I32, P, I32, P], I32),
     "octf_ctx_select": ([P, P, P, I64, P], I32),
     "octf_ctx_set_samples": ([P, P, P, I32, I64, P], I32),
     "octf_propagate_levels": ([P, I32, P, P, I32, I32, P], I32),
+    "octf_halo_pack": ([I32, P, I32, P, I64, P, I32, P], I32),
     "octf_propagate": ([P, I32, P, P, P, I64, I32, P], I32),
     "octf_tree_energy": ([P, I32, P, P, P, I64, I32, P, P, P, I32, DBL, DBL,
                           DBL, P, P, P], I32),
@@ -117,6 +118,9 @@ def ptr_table(ptrs):
     return (ctypes.c_void_p * max(len(ptrs), 1))(*ptrs)
 
 
+# octf_ctx_set_options flags (include/octfuse_b200.h)
+CTX_DENSE, CTX_ELL, CTX_SORTED, CTX_DEFER = 1, 2, 4, 8
+
 # context rebuild phases (octf_ctx.h Phase), in export order
 PHASES = ("walk", "list_diff", "tables", "ell_grow", "ell_update", "fresh",
           "move", "full_list", "full_gather", "tail", "split_cascade",
@@ -147,7 +151,9 @@ class Ctx:
         call("octf_ctx_set_options", self.h, 1 if dense else 0)
 
     def set_options(self, flags: int) -> None:
-        """octf_ctx_set_options: 1 = dense samples, 2 = ELL from 33 views."""
+        """octf_ctx_set_options: CTX_DENSE (1) dense samples, CTX_ELL (2)
+        ELL from 33 views, CTX_SORTED (4) samples sorted per leaf (pd),
+        CTX_DEFER (8) no sample gather before ctx_select (shards)."""
         call("octf_ctx_set_options", self.h, int(flags))
 
     def profile(self, enable: bool = True) -> dict:

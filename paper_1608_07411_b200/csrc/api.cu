@@ -153,9 +153,15 @@ int octf_ctx_set_options(octf_ctx* ctx, int flags) {
     if (!ctx) throw octf::Error(octf::kEArg, "null context");
     const bool dense = (flags & OCTF_CTX_DENSE) != 0;
     const bool ell = (flags & OCTF_CTX_ELL) != 0;
-    if (dense != ctx->c.dense_only || ell != ctx->c.force_ell) {
-      ctx->c.dense_only = dense;
+    const bool sorted = (flags & OCTF_CTX_SORTED) != 0;
+    if ((dense || sorted) && ell)
+      throw octf::Error(octf::kEArg, "ELL excludes dense/sorted");
+    ctx->c.defer_gather = (flags & OCTF_CTX_DEFER) != 0;
+    if (dense != ctx->c.dense_only || ell != ctx->c.force_ell ||
+        sorted != ctx->c.sorted) {
+      ctx->c.dense_only = dense || sorted;
       ctx->c.force_ell = ell;
+      ctx->c.sorted = sorted;
       ctx->c.store_ok = false;
       ctx->c.valid = false;  // regather in the requested layout
     }
@@ -190,6 +196,17 @@ int octf_ctx_profile(octf_ctx* ctx, int enable, double* out) {
       OCTF_CUDA(cudaEventCreate(&e));
       c.pev.push_back(e);
     }
+    if (c.tile_ev_used) {  // tile-range launches: all of a pass's ranges
+      OCTF_CUDA(cudaEventSynchronize(c.tile_ev[2 * c.tile_ev_used - 1]));
+      for (size_t k = 0; k < c.tile_ev_used; ++k) {
+        float ms = 0.f;
+        OCTF_CUDA(cudaEventElapsedTime(&ms, c.tile_ev[2 * k], c.tile_ev[2 * k + 1]));
+        c.t_leaf_ms += ms;
+      }
+      c.n_leaf += c.tile_passes;
+    }
+    c.tile_ev_used = 0;
+    c.tile_passes = 0;
     if (out) {
       out[0] = c.t_leaf_ms;
       out[1] = (double)c.n_leaf;
@@ -433,7 +450,8 @@ int octf_pd_passes(octf_ctx* ctx, int dtype, void* const* set_a,
                    const float* const* vvals, const float* const* vws,
                    const int32_t* const* vchilds, int d_max, double lam,
                    double tau, double sigma, double gamma, int clamp,
-                   int npasses, double* energies_pre, void* stream) {
+                   int npasses, double* energies_pre, int device_energies,
+                   void* stream) {
   return guard([&] {
     if (!ctx || !set_a || !set_b || !uchild || !ustate || !energies_pre)
       throw octf::Error(octf::kEArg, "null argument");
@@ -460,6 +478,7 @@ int octf_pd_passes(octf_ctx* ctx, int dtype, void* const* set_a,
     a.gamma = gamma;
     a.clamp = clamp;
     a.npasses = npasses;
+    a.dev_energies = device_energies != 0;
     a.energies = energies_pre;
     if (dtype == OCTF_F64)
       octf::pd_passes_f64(ctx->c, a, S(stream));
@@ -541,6 +560,24 @@ int octf_propagate_levels(octf_ctx* ctx, int dtype, void* value,
     else
       octf::propagate_levels_f32(ctx->c, (float*)value, child, lo, hi,
                                  S(stream));
+  });
+}
+
+int octf_halo_pack(int dtype, void* const* fields, int nfields,
+                   const int32_t* idx, int64_t n, void* buf, int unpack,
+                   void* stream) {
+  return guard([&] {
+    check_dtype(dtype);
+    if (!fields || (n && (!idx || !buf)))
+      throw octf::Error(octf::kEArg, "null argument");
+    for (int k = 0; k < nfields; ++k)
+      if (!fields[k]) throw octf::Error(octf::kEArg, "null field");
+    if (dtype == OCTF_F64)
+      octf::halo_pack<double>((double* const*)fields, nfields, idx, n,
+                              (double*)buf, unpack != 0, S(stream));
+    else
+      octf::halo_pack<float>((float* const*)fields, nfields, idx, n,
+                             (float*)buf, unpack != 0, S(stream));
   });
 }
 

@@ -13,6 +13,7 @@
 #include <cub/cub.cuh>
 
 #include "octf_ctx.h"
+#include "sample_sort.cuh"
 
 namespace octf {
 
@@ -59,6 +60,7 @@ Ctx::~Ctx() {
   for (auto& e : tev)
     if (e) cudaEventDestroy(e);
   for (auto& e : pev) cudaEventDestroy(e);
+  for (auto& e : tile_ev) cudaEventDestroy(e);
 }
 
 namespace {
@@ -1056,7 +1058,7 @@ void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
   c.hstate[2] = state[2];
   c.valid = true;
   ph_mark(c, kPhTail, st);
-  if (c.nviews > 0 && !patched) {
+  if (c.nviews > 0 && !patched && !c.defer_gather) {
     ctx_gather(c, st);
     ph_mark(c, kPhGather, st);
   }
@@ -1337,6 +1339,7 @@ bool ctx_list_update(Ctx& c, const int32_t* child, int64_t total, int64_t nbid,
         fresh, c.counters.p + 2, c.lmeta.p, ctx_views(c), nvp, c.F.p, c.W.p,
         nullptr, c.counters.p + 3);
   OCTF_CUDA(cudaGetLastError());
+  ctx_sort_samples(c, fresh, c.counters.p + 2, st);  // pd: new leaves only
   OCTF_CUDA(cudaMemcpyAsync(c.h_counters, c.counters.p, 8 * sizeof(int32_t),
                             cudaMemcpyDeviceToHost, st));
   OCTF_CUDA(cudaStreamSynchronize(st));
@@ -1378,7 +1381,7 @@ void ctx_set_views(Ctx& c, int nviews, const float* const* vval,
   OCTF_CUDA(cudaMemcpyAsync(c.dv_child.p, vchild, nviews * sizeof(void*),
                             cudaMemcpyHostToDevice, st));
   OCTF_CUDA(cudaStreamSynchronize(st));
-  if (c.valid) ctx_gather(c, st);
+  if (c.valid && !c.defer_gather) ctx_gather(c, st);
 }
 
 void ctx_set_samples(Ctx& c, const float* F, const float* W, int nviews,
@@ -1389,7 +1392,7 @@ void ctx_set_samples(Ctx& c, const float* F, const float* W, int nviews,
   c.ext_cap = cap;
   c.nviews = nviews;
   c.vkey.clear();
-  if (c.valid) ctx_gather(c, st);
+  if (c.valid && !c.defer_gather) ctx_gather(c, st);
   OCTF_CUDA(cudaStreamSynchronize(st));
 }
 
@@ -1486,6 +1489,28 @@ void ctx_gather_ell(Ctx& c, cudaStream_t st) {
   c.sstride = 0;
 }
 
+void ctx_sort_samples(Ctx& c, const int32_t* list, const int32_t* nlist,
+                      cudaStream_t st) {
+  if (!c.sorted || c.ell) return;
+  const int64_t n = (c.nlb * 8 + kTileLeaves - 1) / kTileLeaves * kTileLeaves;
+  const uint32_t* M = c.binw ? c.M.p : nullptr;
+  float* W = c.binw ? nullptr : c.W.p;
+  const unsigned g = 148 * 8;  // grid-stride (the list count is on the device)
+#define OCTF_SORT(N)                                                          \
+  k_sort_samples<N><<<g, kThreads, 0, st>>>(list, nlist, n, c.nviews, c.F.p, \
+                                             W, M)
+  switch (c.sstride) {
+    case 4: OCTF_SORT(4); break;
+    case 8: OCTF_SORT(8); break;
+    case 16: OCTF_SORT(16); break;
+    case 32: OCTF_SORT(32); break;
+    case 64: OCTF_SORT(64); break;
+    default: return;  // the pd kernel rejects other view counts
+  }
+#undef OCTF_SORT
+  OCTF_CUDA(cudaGetLastError());
+}
+
 void ctx_gather(Ctx& c, cudaStream_t st) {
   const auto t0 = std::chrono::steady_clock::now();
   if (!c.ext_F && !c.dense_only && (c.nviews > 64 || (c.force_ell && c.nviews > 32))) {
@@ -1532,6 +1557,7 @@ void ctx_gather(Ctx& c, cudaStream_t st) {
   } else {
     c.M.release();
   }
+  ctx_sort_samples(c, nullptr, nullptr, st);
   c.store_ok = true;
   if (c.timing) {
     c.t_gather_ms += std::chrono::duration<double, std::milli>(
@@ -1606,8 +1632,67 @@ void ctx_select(Ctx& c, const int32_t* sel, const uint8_t* masks, int64_t nsel,
   c.nbr.swap(onbr);
   c.nlb = nsel;
   c.list_full = false;  // a shard's subset: never patched in place
+  c.defer_gather = false;  // the subset's samples are gathered now
   if (c.nviews > 0) ctx_gather(c, st);
   OCTF_CUDA(cudaStreamSynchronize(st));
 }
+
+}  // namespace octf
+
+// ---- halo exchange staging (shard.HaloExchange): the values of up to five
+// fields at a slot list, packed field-major into one contiguous buffer per
+// peer, and the received buffer scattered back
+namespace octf {
+namespace {
+
+template <typename T>
+struct HaloFields {
+  T* v[kMaxHaloFields];
+};
+
+template <typename T>
+__global__ void k_halo_pack(HaloFields<T> f, int nf, const int32_t* __restrict__ idx,
+                            int64_t n, T* __restrict__ out) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int32_t s = __ldg(idx + j);
+#pragma unroll
+  for (int k = 0; k < kMaxHaloFields; ++k)
+    if (k < nf) out[k * n + j] = f.v[k][s];
+}
+
+template <typename T>
+__global__ void k_halo_unpack(HaloFields<T> f, int nf,
+                              const int32_t* __restrict__ idx, int64_t n,
+                              const T* __restrict__ in) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int32_t s = __ldg(idx + j);
+#pragma unroll
+  for (int k = 0; k < kMaxHaloFields; ++k)
+    if (k < nf) f.v[k][s] = in[k * n + j];
+}
+
+}  // namespace
+
+template <typename T>
+void halo_pack(T* const* fields, int nf, const int32_t* idx, int64_t n,
+               T* buf, bool unpack, cudaStream_t st) {
+  if (nf < 1 || nf > kMaxHaloFields)
+    throw Error(kEArg, "halo: 1 to 5 fields");
+  if (n <= 0) return;
+  HaloFields<T> f{};
+  for (int k = 0; k < nf; ++k) f.v[k] = fields[k];
+  if (unpack)
+    k_halo_unpack<T><<<grid_for(n), kThreads, 0, st>>>(f, nf, idx, n, buf);
+  else
+    k_halo_pack<T><<<grid_for(n), kThreads, 0, st>>>(f, nf, idx, n, buf);
+  OCTF_CUDA(cudaGetLastError());
+}
+
+template void halo_pack<float>(float* const*, int, const int32_t*, int64_t,
+                               float*, bool, cudaStream_t);
+template void halo_pack<double>(double* const*, int, const int32_t*, int64_t,
+                                double*, bool, cudaStream_t);
 
 }  // namespace octf

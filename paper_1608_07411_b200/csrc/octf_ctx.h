@@ -179,6 +179,10 @@ struct Ctx {
   bool ell = false;
   bool dense_only = false;    // octf_ctx_set_options: keep the dense layout
   bool force_ell = false;     // ... or use ELL from 33 views (default: 65)
+  bool defer_gather = false;  // OCTF_CTX_DEFER: prepare builds structure
+                              // only; ctx_select gathers (shards)
+  bool sorted = false;        // OCTF_CTX_SORTED: each leaf's samples sorted
+                              // by (f, view) once when gathered (pd prox)
   DevBuf<int32_t> tileK;      // per tile: rows
   DevBuf<int64_t> tileOff;    // per tile: first float of its rows
   int64_t ell_tiles = 0, ell_size = 0;
@@ -231,6 +235,11 @@ struct Ctx {
   bool timing = false;
   cudaEvent_t tev[4] = {nullptr, nullptr, nullptr, nullptr};
   std::vector<cudaEvent_t> pev;  // per-pass pairs for batched passes
+  // tile-range launches (sharded overlap): event pairs read at the next
+  // octf_ctx_profile call, so timing never synchronises the pass
+  std::vector<cudaEvent_t> tile_ev;
+  size_t tile_ev_used = 0;
+  int64_t tile_passes = 0;
   double t_leaf_ms = 0, t_energy_ms = 0;
   // host wall clock (timing on): context rebuilds, sample gathers, the
   // restructuring tail of a pass (after the leaf kernel)
@@ -255,6 +264,17 @@ struct Ctx {
 // neighbour tables); views gather when given.  Syncs the stream.
 void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
                  const int64_t* state, int d_max, cudaStream_t st);
+// halo staging of shard.HaloExchange: buf[k*n + j] <-> fields[k][idx[j]]
+// (pack: fields -> buf; unpack: buf -> fields), k < nf <= kMaxHaloFields
+constexpr int kMaxHaloFields = 5;
+template <typename T>
+void halo_pack(T* const* fields, int nf, const int32_t* idx, int64_t n,
+               T* buf, bool unpack, cudaStream_t st);
+
+// sort the sample vectors of store slots list[0 .. *nlist) (list null: all
+// slots) -- solver="pd" (sample_sort.cuh); no-op unless c.sorted
+void ctx_sort_samples(Ctx& c, const int32_t* list, const int32_t* nlist,
+                      cudaStream_t st);
 void ctx_set_views(Ctx& c, int nviews, const float* const* vval,
                    const float* const* vw, const int32_t* const* vchild,
                    cudaStream_t st);
@@ -328,7 +348,8 @@ struct PdHostArgs {
   double lam, tau, sigma, gamma;
   int clamp;
   int npasses;
-  double* energies;  // host, npasses: energy of u before each pass
+  double* energies;  // npasses: energy of u before each pass (host, or
+  bool dev_energies = false;  // a device array: then fully asynchronous)
 };
 // sharded overlap: one frozen pass split into tile ranges (interior tiles
 // while the halo is in flight, then boundary tiles), then the finish

@@ -8,7 +8,8 @@
 //   dual    p'(q) = P(p(q) + sigma*lam*grad ubar(q)) at the cell and at its
 //           three backward neighbours (each evaluated at the leaf's level),
 //   primal  u' = prox_{tau D}(u + tau*lam*div p'): generalised weighted
-//           median of the samples, sorted in registers by a bitonic network,
+//           median of the samples, pre-sorted once per leaf when gathered
+//           (sample_sort.cuh): a binary search (unit weights) or one scan,
 //   ubar' = 2u' - u, and the energy of the incoming u (exact TV + L1 data).
 // Same mapping as k_leaf_pass: 8 lanes per block, own-block values by
 // shuffle, neighbour blocks through the 12-entry table.
@@ -76,155 +77,12 @@ __device__ __forceinline__ void dual3(T p0, T p1, T p2, T gx, T gy, T gz, T sl,
   o2 = az / s;
 }
 
-// ascending compare-exchange: keys only (binary weights: equal keys are
-// interchangeable, so min/max suffices) or (key, weight, view index) with the
-// index tie-break of oracle/pd_oracle.c
-template <bool WEIGHTED>
-__device__ __forceinline__ void cx(float& fa, float& wa, int& ia, float& fb,
-                                   float& wb, int& ib) {
-  if (WEIGHTED) {
-    const bool gt = fa > fb || (fa == fb && ia > ib);
-    if (gt) {
-      float t = fa; fa = fb; fb = t;
-      t = wa; wa = wb; wb = t;
-      int u = ia; ia = ib; ib = u;
-    }
-  } else {
-    const float lo = fminf(fa, fb);
-    fb = fmaxf(fa, fb);
-    fa = lo;
-  }
-}
-
-// Batcher odd-even merge sort of N (power of two) entries in registers,
-// ascending: 191 comparators at N = 32 (bitonic: 240).  Written as template
-// recursion so every register index is a compile-time constant.
-template <int LO, int N, int R, bool WEIGHTED>
-struct OeMerge {
-  static __device__ __forceinline__ void run(float* f, float* w, int* ix) {
-    if constexpr (2 * R < N) {
-      OeMerge<LO, N, 2 * R, WEIGHTED>::run(f, w, ix);
-      OeMerge<LO + R, N, 2 * R, WEIGHTED>::run(f, w, ix);
-#pragma unroll
-      for (int i = LO + R; i + R < LO + N; i += 2 * R)
-        cx<WEIGHTED>(f[i], w[i], ix[i], f[i + R], w[i + R], ix[i + R]);
-    } else {
-      cx<WEIGHTED>(f[LO], w[LO], ix[LO], f[LO + R], w[LO + R], ix[LO + R]);
-    }
-  }
-};
-
-template <int LO, int N, bool WEIGHTED>
-struct OeSort {
-  static __device__ __forceinline__ void run(float* f, float* w, int* ix) {
-    if constexpr (N > 1) {
-      OeSort<LO, N / 2, WEIGHTED>::run(f, w, ix);
-      OeSort<LO + N / 2, N / 2, WEIGHTED>::run(f, w, ix);
-      OeMerge<LO, N, 1, WEIGHTED>::run(f, w, ix);
-    }
-  }
-};
-
-template <int N, bool WEIGHTED>
-__device__ __forceinline__ void oddeven_sort(float* f, float* w, int* ix) {
-  OeSort<0, N, WEIGHTED>::run(f, w, ix);
-}
-
-// max_k min(sorted(X)_k, c_{o+k}) for a bitonic X[0..M) (ascending then
-// descending), c_k = v0 - cc*(2k - W) non-increasing, folded into acc.  A
-// half-cleaner splits X into L <= H (both bitonic); since "c_k > X_(k)"
-// holds exactly below the crossing k*, one half's contribution is trivial
-// -- max(L) = L_(M/2-1) if the crossing lies in H, else c_{o+M/2} -- and
-// only the other half is refined: M-1 comparators plus M-1 selects instead
-// of the M log M / 2 of a merge followed by a scan.
-template <typename T, int M>
-__device__ __forceinline__ void bitonic_select(float* X, T& ko, T& acc, T v0,
-                                               T cc, T W) {
-  if constexpr (M == 1) {
-    const T c = v0 - cc * ((T)2 * ko - W);
-    acc = fmax(acc, fmin((T)X[0], c));
-  } else {
-    constexpr int H = M / 2;
-#pragma unroll
-    for (int i = 0; i < H; ++i) {
-      const float l = fminf(X[i], X[i + H]);
-      X[i + H] = fmaxf(X[i], X[i + H]);
-      X[i] = l;
-    }
-    float mL = X[0];
-#pragma unroll
-    for (int i = 1; i < H; ++i) mL = fmaxf(mL, X[i]);
-    const T cl = v0 - cc * ((T)2 * (ko + (T)(H - 1)) - W);
-    const T ch = v0 - cc * ((T)2 * (ko + (T)H) - W);
-    const bool inH = cl > (T)mL;
-    acc = fmax(acc, inH ? (T)mL : ch);
-#pragma unroll
-    for (int i = 0; i < H; ++i) X[i] = inH ? X[i + H] : X[i];
-    ko = inH ? ko + (T)H : ko;
-    bitonic_select<T, H>(X, ko, acc, v0, cc, W);
-  }
-}
-
-// General weights without carrying them through the sort (NV = 64): the
-// breakpoint at sorted position k is c'_k = v0 - cc*(2 S(f_(k)) - W) with
-// S(a) = sum of the weights of samples strictly below a (view order).  A
-// tie group's first element has S_k = S(a) and later ones only smaller
-// breakpoints, so max_k min(f_(k), c'_k) equals the sorted scan's value;
-// with dyadic view-tree weights the f64 sums are exact in any order.  The
-// selection needs c' only at O(log NV) positions, each an O(NV) pass over
-// the leaf's samples (f staged in shared memory, weights from global).
-template <typename T, int NV>
-struct WeightAt {
-  const float* fs;     // s_tile + t: f of view v at fs[v * kTileLeaves]
-  const float* wg;     // weights of view v at wg[v * kTileLeaves]
-  __device__ __forceinline__ T below(float a) const {
-    T S = 0;
-#pragma unroll 8
-    for (int v = 0; v < NV; ++v) {
-      const float wv = __ldg(wg + v * kTileLeaves);
-      if (fs[v * kTileLeaves] < a) S += (T)wv;
-    }
-    return S;
-  }
-};
-
-template <typename T, int M, int NV>
-__device__ __forceinline__ void bitonic_select_w(float* X, T& acc, T v0, T cc,
-                                                 T W,
-                                                 const WeightAt<T, NV>& wa) {
-  if constexpr (M == 1) {
-    const T c = v0 - cc * ((T)2 * wa.below(X[0]) - W);
-    acc = fmax(acc, fmin((T)X[0], c));
-  } else {
-    constexpr int H = M / 2;
-#pragma unroll
-    for (int i = 0; i < H; ++i) {
-      const float l = fminf(X[i], X[i + H]);
-      X[i + H] = fmaxf(X[i], X[i + H]);
-      X[i] = l;
-    }
-    float mL = X[0], mH = X[H];
-#pragma unroll
-    for (int i = 1; i < H; ++i) {
-      mL = fmaxf(mL, X[i]);
-      mH = fminf(mH, X[H + i]);
-    }
-    const T cl = v0 - cc * ((T)2 * wa.below(mL) - W);
-    const bool inH = cl > (T)mL;
-    const T ch = inH ? (T)0 : v0 - cc * ((T)2 * wa.below(mH) - W);
-    acc = fmax(acc, inH ? (T)mL : ch);
-#pragma unroll
-    for (int i = 0; i < H; ++i) X[i] = inH ? X[i + H] : X[i];
-    bitonic_select_w<T, H, NV>(X, acc, v0, cc, W, wa);
-  }
-}
-
-// shared memory of k_pd_pass: the f tile, then the mask tile (binary
-// weights) or the weight tile (NV <= 32; at NV = 64 weights stay in global)
+// shared memory of k_pd_pass: the sorted f tile, then (general weights,
+// NV <= 32) the weight tile permuted alongside; at NV = 64 the weights are
+// read from global memory (coalesced, once per scan)
 constexpr size_t pd_smem_bytes(int nv, bool binw) {
   return (size_t)nv * kTileLeaves * 4 +
-         (binw ? (size_t)kTileLeaves * 4
-               : (nv > 32 ? 0 : (size_t)nv * kTileLeaves * 4));
+         (binw || nv > 32 ? 0 : (size_t)nv * kTileLeaves * 4);
 }
 
 // WP: also write the bottom propagate level of the five fields (frozen
@@ -232,29 +90,25 @@ constexpr size_t pd_smem_bytes(int nv, bool binw) {
 template <typename T, bool BINW, int NV, bool WP = false>
 __global__ void __launch_bounds__(kT, pd_minb(BINW, NV)) k_pd_pass(PdArgs<T> a) {
   static_assert(NV > 0 && (NV & (NV - 1)) == 0, "NV: power of two");
-  // NV = 64: general weights selected without sorting them (WeightAt)
-  constexpr bool WSEL = NV > 32;
-  static_assert(!(WSEL && BINW), "the mask format holds 32 views");
+  // NV = 64, general weights: only the f tile is staged (weights from global)
+  constexpr bool WGLOB = NV > 32;
+  static_assert(!(WGLOB && BINW), "the mask format holds 32 views");
   const int gid = (int)(blockIdx.x * kT + threadIdx.x);
   const int i = gid >> 3;
   const int c = gid & 7;
   const bool inrange = i < (int)a.nlb;
-  // samples: the CTA's tile staged by one TMA bulk copy (as k_leaf_pass),
-  // read into registers only after the stencil, so the stencil values and
-  // the sort network never hold registers at the same time
+  // the CTA's sorted sample tile staged by one TMA bulk copy (as
+  // k_leaf_pass), read only after the stencil
   extern __shared__ __align__(128) float s_tile[];
   __shared__ __align__(8) uint64_t s_bar;
   if (threadIdx.x == 0) {
     mbar_init(&s_bar, 1);
     const size_t tile = blockIdx.x;
     const unsigned fbytes = NV * kTileLeaves * 4;
-    const unsigned abytes = BINW ? kTileLeaves * 4 : (WSEL ? 0 : fbytes);
+    const unsigned abytes = (BINW || WGLOB) ? 0 : fbytes;
     mbar_expect_tx(&s_bar, fbytes + abytes);
     bulk_g2s(s_tile, a.F + tile * NV * kTileLeaves, fbytes, &s_bar);
-    if (BINW)
-      bulk_g2s(s_tile + NV * kTileLeaves, a.M + tile * kTileLeaves, abytes,
-               &s_bar);
-    else if (!WSEL)
+    if (abytes)
       bulk_g2s(s_tile + NV * kTileLeaves, a.W + tile * NV * kTileLeaves,
                abytes, &s_bar);
   }
@@ -355,79 +209,67 @@ __global__ void __launch_bounds__(kT, pd_minb(BINW, NV)) k_pd_pass(PdArgs<T> a) 
   const T div = ((D0 - bx) + (D1 - by) + (D2 - bz)) * ih;
   const T v0 = U0 + a.tl * div;
 
-  // samples from the staged tile, view order
+  // samples: the leaf's vector is sorted ascending by (f, view), absent
+  // entries last as +inf with weight 0 (sample_sort.cuh, once per leaf)
   mbar_wait(&s_bar, 0);
   const int t = threadIdx.x;
-  float f[NV];
-  float w[NV];  // (only the general-weight sort carries them)
-  int ix[NV];
-  uint32_t mk = 0u;
+  const float* ft = s_tile + t;  // rank k at ft[k * kTileLeaves]
+  const float* wsm = s_tile + NV * kTileLeaves + t;
+  const float* wgl = a.W + (size_t)blockIdx.x * NV * kTileLeaves + t;
+  auto wt = [&](int k) -> float {
+    return WGLOB ? __ldg(wgl + k * kTileLeaves) : wsm[k * kTileLeaves];
+  };
+  // weight sum and the energy numerator, sorted order (pd_oracle.c)
   T W = 0, num = 0;
-  if (BINW) {  // valid views of this leaf; W = their count
-    mk = reinterpret_cast<const uint32_t*>(s_tile + NV * kTileLeaves)[t];
-    if (a.nv < 32) mk &= (1u << a.nv) - 1u;
-    W = (T)__popc(mk);
-  }
-  // energy numerator in view order; absent samples become +inf (sort last)
+  int nval = 0;
 #pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    const float fv = s_tile[v * kTileLeaves + t];
-    const float wv =
-        BINW ? 1.f
-             : (WSEL ? __ldg(a.W + (size_t)blockIdx.x * NV * kTileLeaves +
-                             v * kTileLeaves + t)
-                     : s_tile[(NV + v) * kTileLeaves + t]);
-    const bool on = BINW ? ((mk >> v) & 1u) != 0u : (v < a.nv && wv != 0.f);
-    if (on) {
-      if (!BINW) W += (T)wv;
-      num += BINW ? (T)fabs(U0 - (T)fv) : (T)wv * fabs(U0 - (T)fv);
-    }
-    f[v] = on ? __fadd_rn(fv, 0.f) : __int_as_float(0x7f800000);  // -0 -> +0
-    if (!BINW && !WSEL) {
-      w[v] = on ? wv : 0.f;
-      ix[v] = v;
+  for (int k = 0; k < NV; ++k) {
+    const float fv = ft[k * kTileLeaves];
+    if (BINW) {
+      const bool on = fv != __int_as_float(0x7f800000);
+      nval += on ? 1 : 0;
+      if (on) num += (T)fabs(U0 - (T)fv);
+    } else {
+      const float wv = wt(k);
+      if (wv != 0.f) {
+        W += (T)wv;
+        num += (T)wv * fabs(U0 - (T)fv);
+      }
     }
   }
+  if (BINW) W = (T)nval;
   const T den = W + a.gamma;
   const T cc = a.tau / den;
-  T res0 = -(T)INFINITY;
-  if (BINW || WSEL) {
-    // two sorted halves, the second read backwards: a bitonic sequence
-    // whose order statistics are those of all samples
-    oddeven_sort<NV / 2, false>(f, w, ix);
-    oddeven_sort<NV / 2, false>(f + NV / 2, w, ix);
+  // generalised weighted median (oracle/pd_oracle.c wmedian_prox): with S_k
+  // the weight of the first k sorted samples and c_k = v0 - cc*(2 S_k - W)
+  // (non-increasing in k) against the non-decreasing f_k, the oracle's scan
+  // stops at the first k* with c_k* <= f_k* (f_n = +inf) and returns
+  // max(f_(k*-1), c_k*)
+  T res0;
+  if (BINW) {
+    // unit weights, S_k = k: binary search for k* in [0, nval] on the tile
+    int lo = 0, hi = nval;
 #pragma unroll
-    for (int i = 0; i < NV / 4; ++i) {
-      const float t = f[NV / 2 + i];
-      f[NV / 2 + i] = f[NV - 1 - i];
-      f[NV - 1 - i] = t;
+    for (int it = 0; (1 << it) <= NV; ++it) {
+      if (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        const T cm = v0 - cc * ((T)2 * (T)mid - W);
+        if (cm <= (T)ft[mid * kTileLeaves]) hi = mid;
+        else lo = mid + 1;
+      }
     }
-    if (WSEL) {
-      res0 = v0 - cc * W;  // k = NV: f = +inf, S = W
-      const WeightAt<T, NV> wa{
-          s_tile + t, a.W + (size_t)blockIdx.x * NV * kTileLeaves + t};
-      bitonic_select_w<T, NV, NV>(f, res0, v0, cc, W, wa);
-    } else {
-      res0 = v0 - cc * ((T)2 * (T)NV - W);  // k = NV: f = +inf
-      T ko = 0;
-      bitonic_select<T, NV>(f, ko, res0, v0, cc, W);
-    }
+    const T ck = v0 - cc * ((T)2 * (T)lo - W);
+    res0 = lo > 0 ? fmax((T)ft[(lo - 1) * kTileLeaves], ck) : ck;
   } else {
-    oddeven_sort<NV, true>(f, w, ix);
-    // generalised weighted median (oracle/pd_oracle.c wmedian_prox).  With
-    // S_k the weight of the first k sorted samples and c_k = v0 - cc*(2 S_k
-    // - W), the scan returns at the first k* with c_k* <= f[k*]:
-    // max(c_k*, f[k*-1]).  c_k is non-increasing and f non-decreasing, so
-    // min(f[k], c_k) is f[k] for k < k* and c_k after, and that value is
-    // max_k min(f[k], c_k) (f[NV] = +inf) -- two min/max per sample, no
-    // branches.  Absent samples (+inf, weight 0) leave S unchanged.  (With
-    // unit weights S_k = k: the BINW branch above, same value.)
+    // general weights: the prefix sums are needed, so one branch-free scan
+    // (min(f_k, c_k) is f_k below k* and c_k from k*: the max is the value)
+    res0 = -(T)INFINITY;
     T S = 0;
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
       const T cand = v0 - cc * ((T)2 * S - W);
-      res0 = fmax(res0, fmin(cand, (T)f[k]));
-      S += (T)w[k];
+      res0 = fmax(res0, fmin(cand, (T)ft[k * kTileLeaves]));
+      S += (T)wt(k);
     }
     res0 = fmax(res0, v0 - cc * ((T)2 * S - W));
   }

@@ -1,0 +1,110 @@
+// One-time per-leaf sort of the sample store for solver="pd".
+//
+// The primal-dual prox is a generalised weighted median of a leaf's samples
+// (oracle/pd_oracle.c wmedian_prox).  The samples never change while a leaf
+// exists, so instead of sorting them in every pass the context sorts each
+// leaf's vector once, when it is gathered (ctx_gather; new leaves after a pd
+// restructure through ctx_list_update), and k_pd_pass only selects on the
+// sorted tile.  Order: ascending (f, view index), a -0 sample taken as +0,
+// absent samples (weight 0, or a clear mask bit) last as f = +inf with
+// weight 0 -- exactly the order the oracle sorts into.
+//
+// Layout stays [tile][rank][256] (octf_common.cuh samp_idx): rank k of a leaf
+// holds its k-th smallest sample; the weight store (general weights) is
+// permuted alongside; the mask store is left as gathered (the pd kernel
+// counts the finite entries instead).
+#pragma once
+
+#include <cstdint>
+
+#include "octf_common.cuh"
+
+namespace octf {
+namespace {
+
+// total order of floats as unsigned keys (no NaNs in the store)
+__device__ __forceinline__ uint32_t f_ord(float f) {
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float f_unord(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
+__device__ __forceinline__ void cx_u64(uint64_t& a, uint64_t& b) {
+  const uint64_t lo = a < b ? a : b;
+  b = a < b ? b : a;
+  a = lo;
+}
+
+// Batcher odd-even merge sort of N (power of two) keys in registers, by
+// template recursion so every index is a compile-time constant
+template <int LO, int N, int R>
+struct KeyMerge {
+  static __device__ __forceinline__ void run(uint64_t* k) {
+    if constexpr (2 * R < N) {
+      KeyMerge<LO, N, 2 * R>::run(k);
+      KeyMerge<LO + R, N, 2 * R>::run(k);
+#pragma unroll
+      for (int i = LO + R; i + R < LO + N; i += 2 * R) cx_u64(k[i], k[i + R]);
+    } else {
+      cx_u64(k[LO], k[LO + R]);
+    }
+  }
+};
+template <int LO, int N>
+struct KeySort {
+  static __device__ __forceinline__ void run(uint64_t* k) {
+    if constexpr (N > 1) {
+      KeySort<LO, N / 2>::run(k);
+      KeySort<LO + N / 2, N / 2>::run(k);
+      KeyMerge<LO, N, 1>::run(k);
+    }
+  }
+};
+
+// sorts the sample vectors of the store slots list[0 .. *nlist) (list null:
+// slots 0 .. n); NV = the store stride (views padded), nv = real views.
+// M non-null: binary weights (bit v of M[s]); else weights in W.
+template <int NV>
+__global__ void k_sort_samples(const int32_t* __restrict__ list,
+                               const int32_t* __restrict__ nlist, int64_t n,
+                               int nv, float* F, float* W,
+                               const uint32_t* __restrict__ M) {
+  const int64_t cnt = list ? (int64_t)*nlist : n;
+  const int64_t step = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnt;
+       k += step) {
+    const int64_t s = list ? (int64_t)list[k] : k;
+    const uint32_t mk = M ? M[s] : 0u;
+    uint64_t key[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const float f = F[samp_idx(s, v, NV)];
+      const bool on = v < nv && (M ? ((mk >> v) & 1u) != 0u
+                                   : W[samp_idx(s, v, NV)] != 0.f);
+      const float fz = on ? __fadd_rn(f, 0.f) : __int_as_float(0x7f800000);
+      key[v] = ((uint64_t)f_ord(fz) << 32) | (uint32_t)v;
+    }
+    KeySort<0, NV>::run(key);
+    if (!M) {
+      // permute the weights (all read before the in-place writes; w is
+      // indexed at run time, so it lives in local memory -- a one-time pass)
+      float w[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) w[v] = W[samp_idx(s, v, NV)];
+      const uint32_t inf_key = f_ord(__int_as_float(0x7f800000));
+#pragma unroll
+      for (int r = 0; r < NV; ++r) {
+        const int v = (int)(key[r] & 0xffu);
+        W[samp_idx(s, r, NV)] = (uint32_t)(key[r] >> 32) == inf_key ? 0.f : w[v];
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < NV; ++r)
+      F[samp_idx(s, r, NV)] = f_unord((uint32_t)(key[r] >> 32));
+  }
+}
+
+}  // namespace
+}  // namespace octf

@@ -1435,7 +1435,8 @@ void pd_passes_impl(Ctx& c, PdHostArgs& a, cudaStream_t st) {
       else if (a.d_max >= 2)
         launch_propagate_multi<T>(c, (T* const*)out, 5, st, a.d_max - 2);
     }
-    sum_partials(c, c.partials.p, g, nk, c.dscalar.p + k0, st);
+    sum_partials(c, c.partials.p, g, nk,
+                 (a.dev_energies ? a.energies : c.dscalar.p) + k0, st);
     if (c.timing && (int)c.pev.size() >= 2 * kChunk) {
       OCTF_CUDA(cudaStreamSynchronize(st));
       for (int j = 0; j < nk; ++j) {
@@ -1446,6 +1447,7 @@ void pd_passes_impl(Ctx& c, PdHostArgs& a, cudaStream_t st) {
       }
     }
   }
+  if (a.dev_energies) return;  // stays asynchronous
   OCTF_CUDA(cudaMemcpyAsync(a.energies, c.dscalar.p, a.npasses * sizeof(double),
                             cudaMemcpyDeviceToHost, st));
   OCTF_CUDA(cudaStreamSynchronize(st));
@@ -1636,8 +1638,17 @@ void pass_tiles_impl(Ctx& c, TileArgs& a, cudaStream_t st) {
     throw Error(kEArg, "tile range outside the leaf-block list");
   c.partials.ensure(leaf_parts(c));
   const LeafParams<T> lp = leaf_params<T>(a.prm);
+  if (c.timing) {  // an event pair per tile range, read by octf_ctx_profile
+    while (c.tile_ev.size() < 2 * c.tile_ev_used + 2) {
+      cudaEvent_t e;
+      OCTF_CUDA(cudaEventCreate(&e));
+      c.tile_ev.push_back(e);
+    }
+    OCTF_CUDA(cudaEventRecord(c.tile_ev[2 * c.tile_ev_used], st));
+  }
   launch_leaf_pass<T>(c, (const T*)a.usnap, (T*)a.uval, a.child, lp, true,
                       c.partials.p, st, false, a.tile0, a.ntiles);
+  if (c.timing) OCTF_CUDA(cudaEventRecord(c.tile_ev[2 * c.tile_ev_used++ + 1], st));
 }
 
 // propagate every level of the pass's output and sum the pass's energy
@@ -1648,6 +1659,7 @@ void pass_finish_impl(Ctx& c, T* uval, const int32_t* child,
   if (!c.valid) throw Error(kEArg, "context not prepared");
   launch_propagate<T>(c, uval, child, st);
   sum_partials(c, c.partials.p, leaf_parts(c), 1, dev_energy, st);
+  if (c.timing) ++c.tile_passes;  // the tile ranges of one pass end here
 }
 
 // propagate levels hi-1 .. lo only (the replicated top of a sharded tree)

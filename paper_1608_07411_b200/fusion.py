@@ -365,7 +365,7 @@ class Solver:
 
     def __init__(self, u0: OctreeField, views, params: FusionParams, *,
                  log_joins: bool = False, reverse: bool = False,
-                 precision: str = "fp64", samples=None):
+                 precision: str = "fp64", samples=None, defer: bool = False):
         if not views and samples is None:
             raise ValueError("at least one view is required")
         for v in views or ():
@@ -383,6 +383,8 @@ class Solver:
         self.u = _solver_field(u0, self.dtype)
         self.vvals, self.vws, self.vchilds = view_arrays(views or [])
         self.ctx = _lib.Ctx()
+        if defer:   # a shard: samples are gathered by ctx_select
+            self.ctx.set_options(_lib.CTX_DEFER)
         self.samples = samples
         if samples is not None:
             # per-slot samples (BASELINE config 5): frozen trees only
@@ -509,7 +511,8 @@ class PDSolver:
 
     def __init__(self, u0: OctreeField, views, params: FusionParams, *,
                  precision: str = "fp32", tau: float | None = None,
-                 sigma: float | None = None, samples=None):
+                 sigma: float | None = None, samples=None,
+                 defer: bool = False):
         if not views and samples is None:
             raise ValueError("at least one view is required")
         for v in views or ():
@@ -525,7 +528,10 @@ class PDSolver:
         used, cap = self.u.used, self.u.capacity
         self.vvals, self.vws, self.vchilds = view_arrays(views or [])
         self.ctx = _lib.Ctx()
-        self.ctx.set_dense(True)   # the pd kernel reads the dense layout
+        # the pd kernel reads the dense layout, each leaf's samples sorted
+        # once when gathered (its prox selects on them)
+        self.ctx.set_options(_lib.CTX_DENSE | _lib.CTX_SORTED
+                             | (_lib.CTX_DEFER if defer else 0))
         self.samples = samples
         if samples is not None:
             self.kern.ctx_prepare(self.ctx, self.u.child, self.u.state,

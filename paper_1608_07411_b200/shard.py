@@ -25,7 +25,8 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-__all__ = ["Structure", "structure", "ShardPlan", "plan", "HaloExchange"]
+__all__ = ["Structure", "structure", "ShardPlan", "plan", "ShardedSolver",
+           "ShardedPDSolver", "HaloExchange"]
 
 # direction table of the 13-point stencil (octf_common.cuh dir_offset)
 DIRS = np.array([[-1, 0, 0], [1, 0, 0], [0, -1, 0], [0, 1, 0], [0, 0, -1],
@@ -266,14 +267,17 @@ class ShardedSolver:
 
     Every rank keeps the (cheap) pool replicated and updates only the leaves
     it owns: the context's leaf-block list is cut to the rank's blocks with
-    owned-leaf masks, so samples are gathered and streamed for owned leaves
-    only.  Per pass: leaf kernel + propagate (``compute``), halo exchange of
-    the post-pass values, recomputation of the replicated top (``finish``).
+    owned-leaf masks before any sample is gathered (``defer``), so samples --
+    the dominant memory -- are gathered and streamed for owned leaves only.
+    Per pass: leaf kernel + propagate (``compute``), halo exchange of the
+    post-pass values, recomputation of the replicated top (``finish``).
     Energies stay per rank on the device until ``energies()`` sums them.
+    ``samples`` = per-slot sample arrays (BASELINE config 5) instead of views.
     """
 
     def __init__(self, u0, views, params, plan: ShardPlan, rank: int, *,
-                 precision: str = "fp32", exchange=None, group=None):
+                 precision: str = "fp32", exchange=None, group=None,
+                 samples=None):
         import torch
         from . import fusion
         if not (params.tau_split <= 0 and params.clamp and params.tau_join >= 1):
@@ -283,10 +287,12 @@ class ShardedSolver:
         self.plan = plan
         self.rank = rank
         self.group = group
-        self.s = fusion.Solver(u0, views, params, precision=precision)
+        self.s = fusion.Solver(u0, views, params, precision=precision,
+                               samples=samples, defer=True)
         s = self.s
-        s.kern.ctx_prepare(s.ctx, s.u.child, s.u.state, s.u.d_max, s.vvals,
-                           s.vws, s.vchilds)
+        if samples is None:   # structure only (deferred gather)
+            s.kern.ctx_prepare(s.ctx, s.u.child, s.u.state, s.u.d_max,
+                               s.vvals, s.vws, s.vchilds)
         s.kern.ctx_select(s.ctx, plan.sel[rank], plan.masks[rank])
         self.tiles = s.ctx.info()["tiles"]
         self.exchange = exchange if exchange is not None else HaloExchange(
@@ -388,14 +394,95 @@ class ShardedSolver:
         self.s.close()
 
 
+class ShardedPDSolver:
+    """The north_star's TV-L1 primal-dual iteration (solver='pd') on one
+    rank's shard of a frozen tree: the same ownership, leaf-block selection
+    and halo as ``ShardedSolver``, with the five pd fields (u, ubar, px, py,
+    pz) exchanged and their replicated top recomputed.  Per pass: pd kernel
+    + propagate of the five fields over the rank's leaves, halo exchange,
+    top.  Values equal the single-GPU PDSolver bit for bit (per-node
+    arithmetic does not depend on the partition)."""
+
+    def __init__(self, u0, views, params, plan: ShardPlan, rank: int, *,
+                 precision: str = "fp32", exchange=None, group=None,
+                 samples=None):
+        import torch
+        from . import fusion
+        if not (params.tau_split <= 0 and params.clamp and params.tau_join >= 1):
+            raise ValueError("sharded solving needs a frozen structure "
+                             "(tau_split <= 0, tau_join >= 1, clamp)")
+        self.params = params
+        self.plan = plan
+        self.rank = rank
+        self.group = group
+        self.s = fusion.PDSolver(u0, views, params, precision=precision,
+                                 samples=samples, defer=True)
+        s = self.s
+        if samples is None:
+            s.kern.ctx_prepare(s.ctx, s.u.child, s.u.state, s.u.d_max,
+                               s.vvals, s.vws, s.vchilds)
+        s.kern.ctx_select(s.ctx, plan.sel[rank], plan.masks[rank])
+        self.exchange = exchange if exchange is not None else HaloExchange(
+            plan, rank, s.u.value.device, s.u.value.dtype, nfields=5)
+        self.e = torch.zeros(max(params.iterations, 1), dtype=torch.float64,
+                             device=s.u.value.device)
+        self.t = 0
+
+    @property
+    def state(self):
+        return self.s.state
+
+    def compute(self, t: int) -> None:
+        import torch
+        s, p, u = self.s, self.params, self.s.u
+        if t >= self.e.shape[0]:
+            self.e = torch.cat([self.e, torch.zeros_like(self.e)])
+        s.kern.pd_passes(s.a, s.b, u.child, u.state, s.vvals, s.vws,
+                         s.vchilds, u.d_max, p.lam, s.tau, s.sigma, p.gamma,
+                         p.clamp, 1, ctx=s.ctx, energies_out=self.e[t:t + 1])
+        s.a, s.b = s.b, s.a
+        self.t = t + 1
+
+    def finish(self) -> None:
+        s, u = self.s, self.s.u
+        for f in s.a:
+            s.kern.propagate_levels(f, u.child, 0, self.plan.top_levels,
+                                    ctx=s.ctx)
+
+    def run(self, t0: int, k: int) -> None:
+        used = self.s.u.used
+        for t in range(t0, t0 + k):
+            self.compute(t)
+            self.exchange.exchange([f[:used] for f in self.s.a], self.group)
+            self.finish()
+
+    def energies(self, reduce: bool = True):
+        import torch.distributed as dist
+        e = self.e[:self.t].clone()
+        if reduce and dist.is_available() and dist.is_initialized():
+            dist.all_reduce(e, group=self.group)
+        return e
+
+    def close(self):
+        self.s.close()
+
+
 class HaloExchange:
     """Per-pass exchange of owned values into the other ranks' halos
-    (torch.distributed point-to-point; NCCL on GPUs, gloo on CPU)."""
+    (torch.distributed point-to-point; NCCL on GPUs, gloo on CPU).  One
+    message per peer carries every field (``nfields``: 1 for the descent, 5
+    for pd), packed field-major.  On CUDA tensors the staging is the
+    library's gather/scatter kernel (``octf_halo_pack``); CPU tensors (the
+    gloo tests) use torch indexing."""
 
-    def __init__(self, plan: ShardPlan, rank: int, device, dtype):
+    def __init__(self, plan: ShardPlan, rank: int, device, dtype,
+                 nfields: int = 1):
         import torch
         self.rank = rank
         self.nranks = plan.nranks
+        self.nfields = nfields
+        self.cuda = torch.device(device).type == "cuda"
+        itype = torch.int32 if self.cuda else torch.int64
         self.sends = {}
         self.recvs = {}
         for q in range(plan.nranks):
@@ -404,21 +491,42 @@ class HaloExchange:
             s = plan.send.get((rank, q))
             r = plan.send.get((q, rank))
             if s is not None and s.size:
-                idx = torch.as_tensor(s, dtype=torch.int64, device=device)
-                self.sends[q] = (idx, torch.empty(s.size, dtype=dtype, device=device))
+                idx = torch.as_tensor(s, dtype=itype, device=device)
+                self.sends[q] = (idx, torch.empty(nfields * s.size, dtype=dtype,
+                                                  device=device))
             if r is not None and r.size:
-                idx = torch.as_tensor(r, dtype=torch.int64, device=device)
-                self.recvs[q] = (idx, torch.empty(r.size, dtype=dtype, device=device))
+                idx = torch.as_tensor(r, dtype=itype, device=device)
+                self.recvs[q] = (idx, torch.empty(nfields * r.size, dtype=dtype,
+                                                  device=device))
+
+    def _fields(self, values):
+        fields = list(values) if isinstance(values, (list, tuple)) else [values]
+        if len(fields) != self.nfields:
+            raise ValueError(f"expected {self.nfields} fields")
+        return fields
+
+    def _stage(self, fields, idx, buf, unpack):
+        import torch
+        if self.cuda:
+            from . import _kernels
+            _kernels.halo_pack(fields, idx, buf, unpack=unpack)
+            return
+        n = idx.shape[0]
+        for k, f in enumerate(fields):
+            if unpack:
+                f.index_copy_(0, idx, buf[k * n:(k + 1) * n])
+            else:
+                torch.index_select(f, 0, idx, out=buf[k * n:(k + 1) * n])
 
     def start(self, values, group=None):
         """Post the sends of this rank's values and the receives of its halo;
         returns the pending works (with NCCL the transfer runs on its own
         stream, concurrent with kernels launched next)."""
-        import torch
         import torch.distributed as dist
+        fields = self._fields(values)
         ops = []
         for q, (idx, buf) in self.sends.items():
-            torch.index_select(values, 0, idx, out=buf)
+            self._stage(fields, idx, buf, False)
             ops.append(dist.P2POp(dist.isend, buf, q, group))
         for q, (idx, buf) in self.recvs.items():
             ops.append(dist.P2POp(dist.irecv, buf, q, group))
@@ -427,10 +535,11 @@ class HaloExchange:
     def complete(self, works, values):
         """Wait for ``start``'s works (device-side for NCCL) and scatter the
         received halo into ``values``."""
+        fields = self._fields(values)
         for w in works:
             w.wait()
         for q, (idx, buf) in self.recvs.items():
-            values.index_copy_(0, idx, buf)
+            self._stage(fields, idx, buf, True)
 
     def exchange(self, values, group=None):
         self.complete(self.start(values, group), values)

@@ -115,3 +115,121 @@ def test_lockstep_overlapped_shards_match_single_gpu(full, world):
     e = sum(s.energies(reduce=False).cpu().numpy() for s in ranks)
     want = [st.energy for st in ref.stats]
     np.testing.assert_allclose(e[1:], want[:-1], rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("full,world", [(True, 2), (False, 3)])
+def test_lockstep_pd_shards_match_single_gpu(full, world):
+    """solver='pd' sharded (five fields in the halo): fp64 u, ubar, px, py,
+    pz of every owned leaf equal the single-GPU PDSolver bit for bit."""
+    from paper_1608_07411_b200 import fusion, shard
+    u0h, views_h = _scene(full)
+    p = fusion.FusionParams(iterations=5, tau=-1.0, tau_split=0.0,
+                            tau_join=1.5, lam=0.4)
+    views = [_dev(v) for v in views_h]
+    ref = fusion.PDSolver(_dev(u0h), views, p, precision="fp64")
+    ref.run(0, p.iterations)
+    want = [t[:u0h.used].cpu().numpy() for t in ref.state]
+    ref.close()
+    pl = shard.plan(u0h.child, u0h.d_max, world, used=u0h.used, k=2)
+    ranks = [shard.ShardedPDSolver(_dev(u0h), views, p, pl, r,
+                                   precision="fp64", exchange=_NoExchange())
+             for r in range(world)]
+    for t in range(p.iterations):
+        for s in ranks:
+            s.compute(t)
+        for (src, dst), idx in pl.send.items():
+            if idx.size:
+                ii = torch.as_tensor(idx, device="cuda")
+                for k in range(5):
+                    ranks[dst].state[k][ii] = ranks[src].state[k][ii]
+        for s in ranks:
+            s.finish()
+    leaves = np.nonzero(u0h.child[:u0h.used] < 0)[0]
+    for r, s in enumerate(ranks):
+        mine = leaves[pl.owner[leaves] == r]
+        assert mine.size
+        for k in range(5):
+            got = s.state[k][:u0h.used].cpu().numpy()
+            assert np.array_equal(got[mine], want[k][mine]), (r, k)
+
+
+def test_lockstep_sample_shards_match_single_gpu():
+    """BASELINE config 4's per-slot samples path sharded (descent and pd):
+    each rank gathers only its own leaves' samples, values equal the
+    single-GPU run bit for bit (fp64)."""
+    from paper_1608_07411_b200 import fusion, scenes, shard
+    u0, samples, info = scenes.cfg5_inputs(40_000, nviews=8, d_max=8,
+                                           device="cuda")
+    p = fusion.FusionParams(iterations=4, tau=-1.0, tau_split=0.0,
+                            tau_join=1.5, lam=0.3)
+    h = u0.to_host(scratch=False)
+    pl = shard.plan(h.child, h.d_max, 2, used=h.used)
+    leaves = np.nonzero(h.child < 0)[0]
+    # descent
+    ref = fusion.fuse(u0, None, p, samples=samples).field.to_host().value
+    ranks = [shard.ShardedSolver(u0, None, p, pl, r, precision="fp64",
+                                 exchange=_NoExchange(), samples=samples)
+             for r in range(2)]
+    assert all(s.s.ctx.info()["leaves"] == pl.leaves_per_rank[r]
+               for r, s in enumerate(ranks))
+    for t in range(p.iterations):
+        for s in ranks:
+            s.compute(t)
+        for (src, dst), idx in pl.send.items():
+            if idx.size:
+                ii = torch.as_tensor(idx, device="cuda")
+                ranks[dst].s.nxt[ii] = ranks[src].s.nxt[ii]
+        for s in ranks:
+            s.finish()
+    for r, s in enumerate(ranks):
+        mine = leaves[pl.owner[leaves] == r]
+        got = s.values[:h.used].cpu().numpy()
+        assert np.array_equal(got[mine], ref[mine]), r
+        s.close()
+    # pd
+    rp = fusion.PDSolver(u0, None, p, precision="fp64", samples=samples)
+    rp.run(0, p.iterations)
+    want = [t[:h.used].cpu().numpy() for t in rp.state]
+    rp.close()
+    ranks = [shard.ShardedPDSolver(u0, None, p, pl, r, precision="fp64",
+                                   exchange=_NoExchange(), samples=samples)
+             for r in range(2)]
+    for t in range(p.iterations):
+        for s in ranks:
+            s.compute(t)
+        for (src, dst), idx in pl.send.items():
+            if idx.size:
+                ii = torch.as_tensor(idx, device="cuda")
+                for k in range(5):
+                    ranks[dst].state[k][ii] = ranks[src].state[k][ii]
+        for s in ranks:
+            s.finish()
+    for r, s in enumerate(ranks):
+        mine = leaves[pl.owner[leaves] == r]
+        for k in range(5):
+            assert np.array_equal(s.state[k][:h.used].cpu().numpy()[mine],
+                                  want[k][mine]), (r, k)
+        s.close()
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_halo_staging_kernel(dtype):
+    """octf_halo_pack: field-major gather of up to five fields at a slot
+    list, and the scatter back, equal torch indexing."""
+    from paper_1608_07411_b200 import _kernels
+    g = torch.Generator(device="cuda").manual_seed(5)
+    fields = [torch.rand(1000, device="cuda", generator=g).to(dtype)
+              for _ in range(5)]
+    idx = torch.randperm(1000, device="cuda")[:300].to(torch.int32)
+    for nf in (1, 5):
+        buf = torch.empty(nf * 300, dtype=dtype, device="cuda")
+        _kernels.halo_pack(fields[:nf], idx, buf)
+        want = torch.cat([f[idx.long()] for f in fields[:nf]])
+        assert torch.equal(buf, want)
+        dst = [torch.zeros_like(f) for f in fields[:nf]]
+        _kernels.halo_pack(dst, idx, buf, unpack=True)
+        for d, f in zip(dst, fields):
+            assert torch.equal(d[idx.long()], f[idx.long()])
+            mask = torch.ones(1000, dtype=torch.bool, device="cuda")
+            mask[idx.long()] = False
+            assert torch.all(d[mask] == 0)

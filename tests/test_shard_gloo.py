@@ -327,3 +327,63 @@ def test_frame_split_tsdf_matches_single_process(world):
             assert np.array_equal(v[:used], t.value[:used])
             assert np.array_equal(w[:used], t.weight[:used])
             assert list(st) == list(t.state)
+
+
+# ------------------------------------------------ solver="pd" sharded ----
+
+def pd_worker(rank, world, port, q):
+    """As ``worker`` for the primal-dual mode: the five pd fields are
+    forgotten off the rank's ownership, exchanged in one halo message per
+    peer (HaloExchange, nfields=5) and their top recomputed."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        u0, views, p = scene()
+        used = u0.used
+        tau, sigma = orc.pd_steps(p.lam)
+        pl = shard.plan(u0.child, u0.d_max, world, used=used, k=2)
+        ex = shard.HaloExchange(pl, rank, torch.device("cpu"), torch.float64,
+                                nfields=5)
+        keep = (pl.owner[:used] == rank) | (pl.owner[:used] < 0)
+        u = u0.value[:used].astype(np.float64)
+        fields = [u, u.copy(), np.zeros(used), np.zeros(used), np.zeros(used)]
+        child = u0.child[:used].copy()
+        for _ in range(p.iterations):
+            fields, _ = orc.pd_pass(fields, child, used, views, u0.d_max,
+                                    p.lam, tau, sigma, p.gamma)
+            for f in fields:
+                f[~keep] = np.nan
+            ex.exchange([torch.from_numpy(f) for f in fields])
+            for f in fields:
+                top_propagate(orc.Pool(f, child, u0.state, u0.d_max), pl)
+        leaves = np.nonzero(child < 0)[0]
+        mine = leaves[(pl.owner[leaves] == rank)]
+        q.put((rank, mine, [f[mine].copy() for f in fields]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_pd_passes_match_single_process(world):
+    u0, views, p = scene()
+    want = orc.pd_fuse(u0, views, p.lam, p.gamma, p.iterations)[:5]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=pd_worker, args=(r, world, port, q))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    out = [q.get(timeout=300) for _ in procs]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    covered = []
+    for rank, mine, vals in out:
+        for k in range(5):
+            assert np.all(np.isfinite(vals[k])), (rank, k)
+            assert np.array_equal(vals[k], want[k][mine]), (rank, k)
+        covered.append(mine)
+    leaves = np.nonzero(u0.child[:u0.used] < 0)[0]
+    assert np.array_equal(np.sort(np.concatenate(covered)), leaves)

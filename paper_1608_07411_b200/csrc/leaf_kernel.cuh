@@ -63,6 +63,7 @@ struct LeafArgs {
   int32_t* counters;
   double* epart;  // per-CTA energy partial sums
   int tile0 = 0;  // first tile of this launch (sharded overlap: sub-ranges)
+  int ntiles = 0;  // tiles of this launch ([tile0, tile0 + ntiles))
   const int32_t* __restrict__ tileK = nullptr;    // ELL store (views > 32)
   const int64_t* __restrict__ tileOff = nullptr;
 };
@@ -132,50 +133,76 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
       : "memory");
 }
 
-// dynamic shared memory of the staged kernel: the sample tile, then the
-// mask tile (binary weights) or the weight tile
-constexpr size_t leaf_smem_bytes(int nv, bool binw) {
+// the staged kernels are persistent: a CTA walks tiles tile0 + blockIdx.x,
+// + gridDim.x, ... with OCTF_STAGES sample-tile buffers in shared memory, the
+// bulk copy of a later tile in flight while the current one is computed
+// (one stage = the sample tile, then the mask or the weight tile)
+#ifndef OCTF_STAGES
+#define OCTF_STAGES 2
+#endif
+constexpr int kStages = OCTF_STAGES;
+constexpr size_t leaf_stage_floats(int nv, bool binw) {
   return nv <= 0 ? 0
-                 : (size_t)((nv + 3) & ~3) * kTileLeaves * 4 +
-                       (binw ? (size_t)kTileLeaves * 4
-                             : (size_t)((nv + 3) & ~3) * kTileLeaves * 4);
+                 : (size_t)((nv + 3) & ~3) * kTileLeaves +
+                       (binw ? (size_t)kTileLeaves
+                             : (size_t)((nv + 3) & ~3) * kTileLeaves);
+}
+constexpr size_t leaf_smem_bytes(int nv, bool binw) {
+  return leaf_stage_floats(nv, binw) * 4 * kStages;
+}
+
+// issue the bulk copies of tile `tile` into stage buffer `buf` (thread 0)
+template <int NVP, bool BINW>
+__device__ __forceinline__ void stage_tile(float* buf, uint64_t* bar,
+                                           const float* F, const void* A,
+                                           size_t tile) {
+  const unsigned fbytes = NVP * kTileLeaves * 4;
+  const unsigned abytes = BINW ? kTileLeaves * 4 : fbytes;
+  mbar_expect_tx(bar, fbytes + abytes);
+  bulk_g2s(buf, F + tile * NVP * kTileLeaves, fbytes, bar);
+  bulk_g2s(buf + NVP * kTileLeaves,
+           BINW ? (const void*)((const uint32_t*)A + tile * kTileLeaves)
+                : (const void*)((const float*)A + tile * NVP * kTileLeaves),
+           abytes, bar);
 }
 
 template <typename T, bool FROZEN, bool BINW, bool ENERGY, int NV>
 __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(LeafArgs<T> a) {
   using A = Arith<T>;
   const LeafParams<T> p = a.p;
+  const T* __restrict__ snap = a.snap;
+  // samples: tile by tile through kStages shared-memory buffers; the CTA's
+  // first kStages tiles are requested up front, and each buffer is refilled
+  // with the tile kStages steps ahead as soon as the CTA is done with it, so
+  // the dominant 4N B/leaf stream stays in flight during the compute.
+  // Padding leaves and non-leaf slots hold zeros, so copies are in bounds.
+  constexpr int NVP = (NV + 3) & ~3;
+  constexpr size_t STAGE = leaf_stage_floats(NV, BINW);
+  extern __shared__ __align__(128) float s_smem[];
+  __shared__ __align__(8) uint64_t s_bar[kStages];
+  const int tend = a.tile0 + a.ntiles;
+  const void* aux = BINW ? (const void*)a.M : (const void*)a.W;
+  if (NV > 0) {
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < kStages; ++k) mbar_init(&s_bar[k], 1);
+      for (int k = 0; k < kStages; ++k) {
+        const int t = a.tile0 + (int)blockIdx.x + k * (int)gridDim.x;
+        if (t < tend)
+          stage_tile<NVP, BINW>(s_smem + k * STAGE, &s_bar[k], a.F, aux, t);
+      }
+    }
+    __syncthreads();  // barriers initialised before anyone waits on them
+  }
+  int it = 0;
+  for (int tile_id = a.tile0 + (int)blockIdx.x; tile_id < tend;
+       tile_id += (int)gridDim.x, ++it) {
+  const int stage = NV > 0 ? it % kStages : 0;
+  float* const s_tile = s_smem + stage * STAGE;
   // the pool is int32-indexed, so every leaf index fits 32 bits
-  const int tile_id = (int)blockIdx.x + a.tile0;  // one CTA = one tile
-  const int gid = tile_id * kT + (int)threadIdx.x;  // launched with kT
+  const int gid = tile_id * kT + (int)threadIdx.x;
   const int i = gid >> 3;
   const int c = gid & 7;
   const bool inrange = i < (int)a.nlb;
-  const T* __restrict__ snap = a.snap;
-
-  // samples: one TMA bulk copy of the CTA's tile (compile-time N), issued
-  // before anything else and awaited only when the data term needs it.
-  // Padding leaves and non-leaf slots hold zeros, so the copy is in bounds.
-  constexpr int NVP = (NV + 3) & ~3;
-  extern __shared__ __align__(128) float s_tile[];
-  __shared__ __align__(8) uint64_t s_bar;
-  if (NV > 0) {
-    if (threadIdx.x == 0) {
-      mbar_init(&s_bar, 1);
-      const size_t tile = tile_id;
-      const unsigned fbytes = NVP * kTileLeaves * 4;
-      const unsigned abytes = BINW ? kTileLeaves * 4 : fbytes;
-      mbar_expect_tx(&s_bar, fbytes + abytes);
-      bulk_g2s(s_tile, a.F + tile * NVP * kTileLeaves, fbytes, &s_bar);
-      if (BINW)
-        bulk_g2s(s_tile + NVP * kTileLeaves, a.M + tile * kTileLeaves, abytes,
-                 &s_bar);
-      else
-        bulk_g2s(s_tile + NVP * kTileLeaves, a.W + tile * NVP * kTileLeaves,
-                 abytes, &s_bar);
-    }
-    __syncthreads();  // barrier initialised before anyone waits on it
-  }
 
   // one 16 B load: base slot, parent cell, leaf mask and level
   const int4 meta = inrange ? __ldg(a.lmeta + i) : make_int4(0, 0, 0, 0);
@@ -275,7 +302,7 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
     den += wv;
   };
   if (NV > 0) {
-    mbar_wait(&s_bar, 0);
+    mbar_wait(&s_bar[stage], (unsigned)(it / kStages) & 1u);
     const int t = threadIdx.x;
     const float* sf = s_tile;
     if (BINW && sizeof(T) == 4 && NV <= 16) {
@@ -392,4 +419,15 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
       if (threadIdx.x == 0) a.epart[tile_id] = tot;
     }
   }
+  if (NV > 0) {
+    // every thread is done with this stage (and the energy scratch): refill
+    // it with the tile kStages steps ahead
+    __syncthreads();
+    const int nt = tile_id + kStages * (int)gridDim.x;
+    if (threadIdx.x == 0 && nt < tend)
+      stage_tile<NVP, BINW>(s_tile, &s_bar[stage], a.F, aux, nt);
+  } else if (ENERGY) {
+    __syncthreads();  // the energy scratch is reused by the next tile
+  }
+  }  // tiles
 }

@@ -80,7 +80,7 @@ __device__ __forceinline__ void dual3(T p0, T p1, T p2, T gx, T gy, T gz, T sl,
 // shared memory of k_pd_pass: the sorted f tile, then (general weights,
 // NV <= 32) the weight tile permuted alongside; at NV = 64 the weights are
 // read from global memory (coalesced, once per scan)
-constexpr size_t pd_smem_bytes(int nv, bool binw) {
+constexpr size_t pd_smem_bytes(int nv, bool binw) {  // one stage
   return (size_t)nv * kTileLeaves * 4 +
          (binw || nv > 32 ? 0 : (size_t)nv * kTileLeaves * 4);
 }
@@ -93,26 +93,39 @@ __global__ void __launch_bounds__(kT, pd_minb(BINW, NV)) k_pd_pass(PdArgs<T> a) 
   // NV = 64, general weights: only the f tile is staged (weights from global)
   constexpr bool WGLOB = NV > 32;
   static_assert(!(WGLOB && BINW), "the mask format holds 32 views");
-  const int gid = (int)(blockIdx.x * kT + threadIdx.x);
+  // persistent, as k_leaf_pass: kStages buffers of the sorted sample tile
+  // (and the weight tile), the copy of a later tile in flight while the
+  // current one is computed
+  constexpr size_t STAGE = pd_smem_bytes(NV, BINW) / 4;
+  extern __shared__ __align__(128) float s_smem[];
+  __shared__ __align__(8) uint64_t s_bar[kStages];
+  const int ntiles = (int)((a.nlb * 8 + kTileLeaves - 1) / kTileLeaves);
+  auto stage_pd = [&](float* buf, uint64_t* bar, size_t tile) {
+    const unsigned fbytes = NV * kTileLeaves * 4;
+    const unsigned abytes = (BINW || WGLOB) ? 0 : fbytes;
+    mbar_expect_tx(bar, fbytes + abytes);
+    bulk_g2s(buf, a.F + tile * NV * kTileLeaves, fbytes, bar);
+    if (abytes)
+      bulk_g2s(buf + NV * kTileLeaves, a.W + tile * NV * kTileLeaves, abytes,
+               bar);
+  };
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < kStages; ++k) mbar_init(&s_bar[k], 1);
+    for (int k = 0; k < kStages; ++k) {
+      const int t = (int)blockIdx.x + k * (int)gridDim.x;
+      if (t < ntiles) stage_pd(s_smem + k * STAGE, &s_bar[k], t);
+    }
+  }
+  __syncthreads();
+  int it = 0;
+  for (int tile_id = (int)blockIdx.x; tile_id < ntiles;
+       tile_id += (int)gridDim.x, ++it) {
+  const int stage = it % kStages;
+  float* const s_tile = s_smem + stage * STAGE;
+  const int gid = tile_id * kT + (int)threadIdx.x;
   const int i = gid >> 3;
   const int c = gid & 7;
   const bool inrange = i < (int)a.nlb;
-  // the CTA's sorted sample tile staged by one TMA bulk copy (as
-  // k_leaf_pass), read only after the stencil
-  extern __shared__ __align__(128) float s_tile[];
-  __shared__ __align__(8) uint64_t s_bar;
-  if (threadIdx.x == 0) {
-    mbar_init(&s_bar, 1);
-    const size_t tile = blockIdx.x;
-    const unsigned fbytes = NV * kTileLeaves * 4;
-    const unsigned abytes = (BINW || WGLOB) ? 0 : fbytes;
-    mbar_expect_tx(&s_bar, fbytes + abytes);
-    bulk_g2s(s_tile, a.F + tile * NV * kTileLeaves, fbytes, &s_bar);
-    if (abytes)
-      bulk_g2s(s_tile + NV * kTileLeaves, a.W + tile * NV * kTileLeaves,
-               abytes, &s_bar);
-  }
-  __syncthreads();
   const int4 meta = inrange ? __ldg(a.lmeta + i) : make_int4(0, 0, 0, 0);
   const int32_t b = meta.x;
   const int32_t s = b + c;
@@ -211,11 +224,11 @@ __global__ void __launch_bounds__(kT, pd_minb(BINW, NV)) k_pd_pass(PdArgs<T> a) 
 
   // samples: the leaf's vector is sorted ascending by (f, view), absent
   // entries last as +inf with weight 0 (sample_sort.cuh, once per leaf)
-  mbar_wait(&s_bar, 0);
+  mbar_wait(&s_bar[stage], (unsigned)(it / kStages) & 1u);
   const int t = threadIdx.x;
   const float* ft = s_tile + t;  // rank k at ft[k * kTileLeaves]
   const float* wsm = s_tile + NV * kTileLeaves + t;
-  const float* wgl = a.W + (size_t)blockIdx.x * NV * kTileLeaves + t;
+  const float* wgl = a.W + (size_t)tile_id * NV * kTileLeaves + t;
   auto wt = [&](int k) -> float {
     return WGLOB ? __ldg(wgl + k * kTileLeaves) : wsm[k * kTileLeaves];
   };
@@ -316,13 +329,13 @@ __global__ void __launch_bounds__(kT, pd_minb(BINW, NV)) k_pd_pass(PdArgs<T> a) 
       double tot = 0.0;
 #pragma unroll
       for (int k = 0; k < kT / 32; ++k) tot += s_w[k];
-      a.epart[blockIdx.x] = tot;
+      a.epart[tile_id] = tot;
     }
   } else {
     typedef cub::BlockReduce<double, kT> BR;
     __shared__ typename BR::TempStorage tmp;
     const double tot = BR(tmp).Sum(eterm);
-    if (threadIdx.x == 0) a.epart[blockIdx.x] = tot;
+    if (threadIdx.x == 0) a.epart[tile_id] = tot;
   }
   if (WP && t < 5 * (kT / 8)) {
     // warp q writes field q of the 32 blocks (a short tail: the CTA's slot
@@ -338,4 +351,10 @@ __global__ void __launch_bounds__(kT, pd_minb(BINW, NV)) k_pd_pass(PdArgs<T> a) 
       o[par] = (T)(acc / 8.0);
     }
   }
+  // every thread is done with this stage and the shared scratch: refill the
+  // stage with the tile kStages steps ahead
+  __syncthreads();
+  const int nt = tile_id + kStages * (int)gridDim.x;
+  if (threadIdx.x == 0 && nt < ntiles) stage_pd(s_tile, &s_bar[stage], nt);
+  }  // tiles
 }

@@ -23,6 +23,9 @@
 #pragma once
 #include <chrono>
 #include <cooperative_groups.h>
+#include <map>
+#include <mutex>
+#include <set>
 #include <cub/cub.cuh>
 
 #include "octf_arith.cuh"
@@ -794,17 +797,53 @@ inline unsigned leaf_grid(const Ctx& c) { return blocks_for(c.nlb * 8); }
 // energy partials the leaf kernel writes per pass (kLeafParts per CTA)
 inline int64_t leaf_parts(const Ctx& c) { return (int64_t)leaf_grid(c); }
 
-template <typename T, bool FZ, bool BW, bool EN, int N>
-void launch_leaf(unsigned g, cudaStream_t st, const LeafArgs<T>& a) {
-  constexpr size_t smem = leaf_smem_bytes(N, BW);
-  static bool attr = false;  // opt in to > 48 KiB of dynamic shared memory
-  if (smem > 48 * 1024 && !attr) {
-    OCTF_CUDA(cudaFuncSetAttribute(k_leaf_pass<T, FZ, BW, EN, N>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+// resident CTAs of a kernel on the whole GPU (occupancy x SMs), cached
+// per kernel and device
+inline int resident_ctas(const void* fn, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> cache;
+  int dev = 0;
+  OCTF_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_pair(fn, dev);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int per_sm = 0, sms = 0;
+  OCTF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads,
+                                                          smem));
+  OCTF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int n = (per_sm < 1 ? 1 : per_sm) * sms;
+  cache[key] = n;
+  return n;
+}
+
+// opt a kernel in to > 48 KiB of dynamic shared memory, once per device
+inline void smem_opt_in(const void* fn, size_t smem) {
+  if (smem <= 48 * 1024) return;
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  OCTF_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.insert(std::make_pair(fn, dev)).second)
+    OCTF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
-    attr = true;
+}
+
+// g = tiles of this launch; staged kernels run persistent (at most the
+// resident CTAs, each walking tiles with a grid stride)
+template <typename T, bool FZ, bool BW, bool EN, int N>
+void launch_leaf(unsigned g, cudaStream_t st, LeafArgs<T> a) {
+  constexpr size_t smem = leaf_smem_bytes(N, BW);
+  const void* fn = (const void*)k_leaf_pass<T, FZ, BW, EN, N>;
+  smem_opt_in(fn, smem);
+  a.ntiles = (int)g;
+  unsigned grid = g;
+  if (N > 0) {
+    const unsigned res = (unsigned)resident_ctas(fn, kT, smem);
+    grid = g < res ? g : res;
   }
-  k_leaf_pass<T, FZ, BW, EN, N><<<g, kT, smem, st>>>(a);
+  k_leaf_pass<T, FZ, BW, EN, N><<<grid, kT, smem, st>>>(a);
 }
 
 template <typename T>
@@ -1346,15 +1385,11 @@ void pd_passes_impl(Ctx& c, PdHostArgs& a, cudaStream_t st);
 
 template <typename T, bool BW, int N, bool WP>
 void launch_pd_wp(unsigned g, cudaStream_t st, const PdArgs<T>& p) {
-  constexpr size_t smem = pd_smem_bytes(N, BW);
-  static bool attr = false;  // opt in to > 48 KiB of dynamic shared memory
-  if (smem > 48 * 1024 && !attr) {
-    OCTF_CUDA(cudaFuncSetAttribute(k_pd_pass<T, BW, N, WP>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
-    attr = true;
-  }
-  k_pd_pass<T, BW, N, WP><<<g, kT, smem, st>>>(p);
+  constexpr size_t smem = pd_smem_bytes(N, BW) * kStages;
+  const void* fn = (const void*)k_pd_pass<T, BW, N, WP>;
+  smem_opt_in(fn, smem);
+  const unsigned res = (unsigned)resident_ctas(fn, kT, smem);
+  k_pd_pass<T, BW, N, WP><<<g < res ? g : res, kT, smem, st>>>(p);  // persistent
 }
 template <typename T, bool BW, int N>
 void launch_pd(unsigned g, cudaStream_t st, const PdArgs<T>& p, bool wp) {

@@ -25,7 +25,7 @@ def test_cfg2_full_size_passes_bitexact():
     import bench
     from paper_1608_07411_b200 import fusion
 
-    views, u0, p = bench.build_gpu_workload(8, 16)
+    views, u0, p = bench.build_cfg2(8, 16)
     k = 2
     pk = bench.cfg2_params(iterations=k)
     res = fusion.fuse(u0, views, pk)                       # fp64 parity mode

@@ -170,8 +170,11 @@ def test_lockstep_sample_shards_match_single_gpu():
     ranks = [shard.ShardedSolver(u0, None, p, pl, r, precision="fp64",
                                  exchange=_NoExchange(), samples=samples)
              for r in range(2)]
-    assert all(s.s.ctx.info()["leaves"] == pl.leaves_per_rank[r]
-               for r, s in enumerate(ranks))
+    # each rank's sample store covers only its own leaf tiles
+    full = fusion.Solver(u0, None, p, precision="fp64", samples=samples)
+    ntiles = full.ctx.info()["tiles"]
+    full.close()
+    assert all(s.s.ctx.info()["tiles"] < ntiles for s in ranks)
     for t in range(p.iterations):
         for s in ranks:
             s.compute(t)

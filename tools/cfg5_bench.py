@@ -61,12 +61,12 @@ def timed(s, label, b_leaf):
 
 if args.only in (None, "descent"):
     s = fusion.Solver(u0, None, p, precision="fp32", samples=samples)
-    timed(s, "descent_fp32", 4 + 4 + 4 * args.views + (args.views + 7) // 8)
+    timed(s, "descent_fp32", 4 + 4 + 4 * args.views)
     s.close()
     del s
     torch.cuda.empty_cache()
 if args.only in (None, "pd"):
     s = fusion.PDSolver(u0, None, p, precision="fp32", samples=samples)
-    timed(s, "pd_fp32", 40 + 4 * args.views + (args.views + 7) // 8)
+    timed(s, "pd_fp32", 40 + 4 * args.views)
     s.close()
 print(json.dumps(out))

@@ -63,9 +63,9 @@ int octf_selftest(void);
 int octf_ctx_create(octf_ctx **out);
 int octf_ctx_destroy(octf_ctx *ctx);
 int octf_ctx_invalidate(octf_ctx *ctx);
-/* out[0..9] = leaf blocks, leaves, live blocks, free blocks, mask-format
- * samples (0/1), sample stride, views, valid, leaf tiles, ELL layout (0/1)
- * (int64[10]) */
+/* out[0..10] = leaf blocks, leaves, live blocks, free blocks, mask-format
+ * samples (0/1), sample stride, views, valid, leaf tiles, ELL layout (0/1),
+ * every leaf has every sample (0/1; kernels then read no mask) (int64[11]) */
 int octf_ctx_info(octf_ctx *ctx, int64_t *out);
 
 /* Context options.  By default more than 64 views use the ELL sample

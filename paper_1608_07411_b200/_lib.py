@@ -140,10 +140,10 @@ class Ctx:
 
     def info(self) -> dict:
         import numpy as np
-        out = np.zeros(10, dtype=np.int64)
+        out = np.zeros(11, dtype=np.int64)
         call("octf_ctx_info", self.h, out.ctypes.data)
         keys = ("leaf_blocks", "leaves", "blocks", "free_blocks", "mask_samples",
-                "sample_stride", "views", "valid", "tiles", "ell")
+                "sample_stride", "views", "valid", "tiles", "ell", "all_valid")
         return dict(zip(keys, (int(v) for v in out)))
 
     def set_dense(self, dense: bool = True) -> None:

@@ -182,6 +182,7 @@ int octf_ctx_info(octf_ctx* ctx, int64_t* out) {
     out[7] = c.valid;
     out[8] = (c.nlb * 8 + 255) / 256;  // leaf tiles (one CTA each)
     out[9] = c.ell ? 1 : 0;
+    out[10] = c.allv ? 1 : 0;
   });
 }
 

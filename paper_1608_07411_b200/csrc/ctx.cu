@@ -397,7 +397,9 @@ __global__ void k_vgather(const int32_t* __restrict__ ucs,
   const float w = __ldg(vs.w[v0 + y] + n);
   F[samp_idx(gid, v0 + y, stride)] = f;
   W[samp_idx(gid, v0 + y, stride)] = w;
-  if (w != 0.f && w != 1.f) atomicExch(nonbin, 1);
+  // flags: bit 0 a weight other than 0/1, bit 1 a zero weight on a leaf
+  if (w != 0.f && w != 1.f) atomicOr(nonbin, 1);
+  if (w == 0.f) atomicOr(nonbin, 2);
 }
 
 // per (leaf, view) from caller-supplied per-slot arrays [view][cap]
@@ -420,12 +422,13 @@ __global__ void k_gather_slots(const int32_t* __restrict__ ucs,
     if (active) {
       f = Fs[(int64_t)v * cap + b + c];
       w = Ws ? Ws[(int64_t)v * cap + b + c] : 1.f;
-      flag |= (w != 0.f && w != 1.f);
+      flag |= (w != 0.f && w != 1.f) ? 1 : 0;
+      flag |= w == 0.f ? 2 : 0;
     }
     F[samp_idx(gid, v, stride)] = f;
     W[samp_idx(gid, v, stride)] = w;
   }
-  if (flag) atomicExch(nonbin, 1);
+  if (flag) atomicOr(nonbin, flag);
 }
 
 // ---- stable leaf-block list (ctx_list_update) ----
@@ -626,7 +629,8 @@ __global__ void k_gather_fresh(const int32_t* __restrict__ fresh,
                                              : descend(vs.child[v], L, x, y, z);
         f = vs.val[v][nd];
         w = vs.w[v][nd];
-        flag |= (w != 0.f && w != 1.f);
+        flag |= (w != 0.f && w != 1.f) ? 1 : 0;
+        flag |= w == 0.f ? 2 : 0;
       }
       if (v < stride) {
         F[samp_idx(s, v, stride)] = f;
@@ -635,7 +639,8 @@ __global__ void k_gather_fresh(const int32_t* __restrict__ fresh,
       if (BINW) bits |= __ballot_sync(0xffffffffu, w != 0.f);
     }
     if (BINW && lane == 0) M[s] = bits;
-    if (__any_sync(0xffffffffu, flag) && lane == 0) atomicExch(nonbin, 1);
+    flag = __reduce_or_sync(0xffffffffu, flag);
+    if (flag && lane == 0) atomicOr(nonbin, flag);
   }
 }
 
@@ -1343,7 +1348,8 @@ bool ctx_list_update(Ctx& c, const int32_t* child, int64_t total, int64_t nbid,
   OCTF_CUDA(cudaMemcpyAsync(c.h_counters, c.counters.p, 8 * sizeof(int32_t),
                             cudaMemcpyDeviceToHost, st));
   OCTF_CUDA(cudaStreamSynchronize(st));
-  if (c.binw && c.h_counters[3]) return false;  // needs the weight format
+  if (c.binw && (c.h_counters[3] & 1)) return false;  // needs the weight format
+  if (c.h_counters[3] & 2) c.allv = false;  // a new leaf misses a sample
   c.nlb = nnew;
   c.nleaves = c.h_counters[4];
   c.store_ok = true;
@@ -1482,6 +1488,7 @@ void ctx_gather_ell(Ctx& c, cudaStream_t st) {
   OCTF_CUDA(cudaGetLastError());
   c.M.release();
   c.binw = false;
+  c.allv = false;
   c.ell = true;
   c.ell_tiles = nt;
   c.ell_size = total;
@@ -1547,7 +1554,10 @@ void ctx_gather(Ctx& c, cudaStream_t st) {
   OCTF_CUDA(cudaMemcpyAsync(c.h_counters, c.counters.p, sizeof(int32_t),
                             cudaMemcpyDeviceToHost, st));
   OCTF_CUDA(cudaStreamSynchronize(st));
-  c.binw = (c.h_counters[0] == 0) && nv <= 32;
+  c.binw = !(c.h_counters[0] & 1) && nv <= 32;
+  // every leaf has every sample (weight 1): kernels skip the mask
+  c.allv = c.binw && !(c.h_counters[0] & 2) && nv == nvp &&
+           (nv == 8 || nv == 16 || nv == 32);
   if (c.binw) {
     c.M.ensure(npad);
     k_masks<<<grid_for(npad), kThreads, 0, st>>>(c.W.p, nvp, nv, npad, c.M.p);

@@ -137,36 +137,70 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
 // + gridDim.x, ... with OCTF_STAGES sample-tile buffers in shared memory, the
 // bulk copy of a later tile in flight while the current one is computed
 // (one stage = the sample tile, then the mask or the weight tile)
+// Measured on cfg5 (profiles/r02/ab_stages.txt): 2 and 3 stages force 3
+// and 2 resident CTAs per SM (shared memory) and lose more to the stencil's
+// load latency than they gain (leaf 3.52 / 4.10 / 4.78 ms for 1 / 2 / 3
+// stages); one CTA per tile (OCTF_PERSIST=0, the hardware scheduler
+// balancing tiles of uneven cost) with one stage is the default.
 #ifndef OCTF_STAGES
-#define OCTF_STAGES 2
+#define OCTF_STAGES 1
+#endif
+#ifndef OCTF_PERSIST
+#define OCTF_PERSIST 0
 #endif
 constexpr int kStages = OCTF_STAGES;
-constexpr size_t leaf_stage_floats(int nv, bool binw) {
+// sample formats (the BW template parameter): general weights, binary
+// weights as a bit mask, or every sample present with weight 1 (no mask)
+constexpr int kWeights = 0, kMask = 1, kAllValid = 2;
+constexpr size_t leaf_stage_floats(int nv, int bw) {
   return nv <= 0 ? 0
                  : (size_t)((nv + 3) & ~3) * kTileLeaves +
-                       (binw ? (size_t)kTileLeaves
-                             : (size_t)((nv + 3) & ~3) * kTileLeaves);
+                       (bw == kAllValid ? 0
+                        : bw == kMask   ? (size_t)kTileLeaves
+                                        : (size_t)((nv + 3) & ~3) * kTileLeaves);
 }
-constexpr size_t leaf_smem_bytes(int nv, bool binw) {
-  return leaf_stage_floats(nv, binw) * 4 * kStages;
+constexpr size_t leaf_smem_bytes(int nv, int bw) {
+  return leaf_stage_floats(nv, bw) * 4 * kStages;
 }
 
 // issue the bulk copies of tile `tile` into stage buffer `buf` (thread 0)
-template <int NVP, bool BINW>
+template <int NVP, int BW>
 __device__ __forceinline__ void stage_tile(float* buf, uint64_t* bar,
                                            const float* F, const void* A,
                                            size_t tile) {
   const unsigned fbytes = NVP * kTileLeaves * 4;
-  const unsigned abytes = BINW ? kTileLeaves * 4 : fbytes;
+  const unsigned abytes = BW == kAllValid ? 0u
+                          : BW == kMask   ? kTileLeaves * 4u
+                                          : fbytes;
   mbar_expect_tx(bar, fbytes + abytes);
   bulk_g2s(buf, F + tile * NVP * kTileLeaves, fbytes, bar);
-  bulk_g2s(buf + NVP * kTileLeaves,
-           BINW ? (const void*)((const uint32_t*)A + tile * kTileLeaves)
-                : (const void*)((const float*)A + tile * NVP * kTileLeaves),
-           abytes, bar);
+  if (abytes)
+    bulk_g2s(buf + NVP * kTileLeaves,
+             BW == kMask ? (const void*)((const uint32_t*)A + tile * kTileLeaves)
+                         : (const void*)((const float*)A + tile * NVP * kTileLeaves),
+             abytes, bar);
 }
 
-template <typename T, bool FROZEN, bool BINW, bool ENERGY, int NV>
+// packed fp32 pairs (sm_100a FADD2 / FFMA2)
+__device__ __forceinline__ unsigned long long f2u(float2 v) {
+  return *reinterpret_cast<unsigned long long*>(&v);
+}
+__device__ __forceinline__ float2 u2f(unsigned long long v) {
+  return *reinterpret_cast<float2*>(&v);
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)));
+  return u2f(r);
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)),
+      "l"(f2u(c)));
+  return u2f(r);
+}
+
+template <typename T, bool FROZEN, int BW, bool ENERGY, int NV>
 __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(LeafArgs<T> a) {
   using A = Arith<T>;
   const LeafParams<T> p = a.p;
@@ -177,7 +211,9 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
   // the dominant 4N B/leaf stream stays in flight during the compute.
   // Padding leaves and non-leaf slots hold zeros, so copies are in bounds.
   constexpr int NVP = (NV + 3) & ~3;
-  constexpr size_t STAGE = leaf_stage_floats(NV, BINW);
+  constexpr bool BINW = BW != kWeights;  // unit weights (mask or all valid)
+  static_assert(BW != kAllValid || NV > 0, "all-valid needs a staged N");
+  constexpr size_t STAGE = leaf_stage_floats(NV, BW);
   extern __shared__ __align__(128) float s_smem[];
   __shared__ __align__(8) uint64_t s_bar[kStages];
   const int tend = a.tile0 + a.ntiles;
@@ -188,7 +224,7 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
       for (int k = 0; k < kStages; ++k) {
         const int t = a.tile0 + (int)blockIdx.x + k * (int)gridDim.x;
         if (t < tend)
-          stage_tile<NVP, BINW>(s_smem + k * STAGE, &s_bar[k], a.F, aux, t);
+          stage_tile<NVP, BW>(s_smem + k * STAGE, &s_bar[k], a.F, aux, t);
       }
     }
     __syncthreads();  // barriers initialised before anyone waits on them
@@ -305,7 +341,30 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
     mbar_wait(&s_bar[stage], (unsigned)(it / kStages) & 1u);
     const int t = threadIdx.x;
     const float* sf = s_tile;
-    if (BINW && sizeof(T) == 4 && NV <= 16) {
+    if (BW == kAllValid && sizeof(T) == 4) {
+      // fp32 throughput mode, every sample present: no mask, den = gamma + N,
+      // and the samples in pairs through the packed fp32 pipes (FADD2/FFMA2;
+      // the two partial sums are added at the end)
+      const float2 S2 = make_float2((float)S0, (float)S0);
+      const float2 E2 = make_float2((float)p.eps2, (float)p.eps2);
+      float2 n2 = make_float2(0.f, 0.f), m2 = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int v = 0; v < NV; v += 2) {
+        const float2 d = sub2(S2, make_float2(sf[v * kTileLeaves + t],
+                                              sf[(v + 1) * kTileLeaves + t]));
+        const float2 q = fma2(d, d, E2);
+        const float2 r = make_float2(rsqrtf(q.x), rsqrtf(q.y));
+        n2 = fma2(d, r, n2);
+        if (ENERGY) m2 = fma2(q, r, m2);
+      }
+      num = (T)(n2.x + n2.y);
+      if (ENERGY) enm = (T)(m2.x + m2.y);
+      den += (T)NV;
+    } else if (BW == kAllValid) {
+      // parity mode: the reference's sequential order, unit weights
+#pragma unroll
+      for (int v = 0; v < NV; ++v) sample((T)1, sf[v * kTileLeaves + t]);
+    } else if (BINW && sizeof(T) == 4 && NV <= 16) {
       // fp32 throughput mode: unit weights, so den = gamma + count (one
       // rounding instead of one per view; the fp64 parity mode keeps the
       // reference's sequential sum).  cfg2 leaf kernel 0.306 -> 0.298 ms;
@@ -425,7 +484,7 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
     __syncthreads();
     const int nt = tile_id + kStages * (int)gridDim.x;
     if (threadIdx.x == 0 && nt < tend)
-      stage_tile<NVP, BINW>(s_tile, &s_bar[stage], a.F, aux, nt);
+      stage_tile<NVP, BW>(s_tile, &s_bar[stage], a.F, aux, nt);
   } else if (ENERGY) {
     __syncthreads();  // the energy scratch is reused by the next tile
   }

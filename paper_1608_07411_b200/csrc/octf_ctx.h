@@ -173,6 +173,8 @@ struct Ctx {
   DevBuf<float> W;            // [leaf][view] (general weights)
   DevBuf<uint32_t> M;         // [sample] bit v = weight of view v is 1
   bool binw = false;          // samples use the mask format
+  bool allv = false;          // ... and every leaf has all of them (no mask
+                              // read; set with 8/16/32 views)
   int64_t sstride = 0;        // views per leaf vector, padded to 4
   // ELL layout (views > 64, unless dense_only): F/W hold per tile K_t rows
   // of the leaves' observed samples (octf_common.cuh ell_idx)

@@ -87,9 +87,10 @@ constexpr size_t pd_smem_bytes(int nv, bool binw) {  // one stage
 
 // WP: also write the bottom propagate level of the five fields (frozen
 // passes over a full leaf-block list)
-template <typename T, bool BINW, int NV, bool WP = false>
-__global__ void __launch_bounds__(kT, pd_minb(BINW, NV)) k_pd_pass(PdArgs<T> a) {
+template <typename T, int BW, int NV, bool WP = false>
+__global__ void __launch_bounds__(kT, pd_minb(BW != kWeights, NV)) k_pd_pass(PdArgs<T> a) {
   static_assert(NV > 0 && (NV & (NV - 1)) == 0, "NV: power of two");
+  constexpr bool BINW = BW != kWeights;  // unit weights (+inf = absent)
   // NV = 64, general weights: only the f tile is staged (weights from global)
   constexpr bool WGLOB = NV > 32;
   static_assert(!(WGLOB && BINW), "the mask format holds 32 views");
@@ -234,45 +235,54 @@ __global__ void __launch_bounds__(kT, pd_minb(BINW, NV)) k_pd_pass(PdArgs<T> a) 
   };
   // weight sum and the energy numerator, sorted order (pd_oracle.c)
   T W = 0, num = 0;
-  int nval = 0;
+  if (BW == kAllValid) {  // every sample present: W = N
 #pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    const float fv = ft[k * kTileLeaves];
-    if (BINW) {
-      const bool on = fv != __int_as_float(0x7f800000);
-      nval += on ? 1 : 0;
-      if (on) num += (T)fabs(U0 - (T)fv);
-    } else {
+    for (int k = 0; k < NV; ++k) num += (T)fabs(U0 - (T)ft[k * kTileLeaves]);
+    W = (T)NV;
+  } else if (BW == kMask) {
+    // unit weights: the present samples are the finite prefix; its length by
+    // bisection on the +inf tail, then the sum over it
+    int nval = 0;
+#pragma unroll
+    for (int step = NV / 2; step >= 1; step >>= 1)
+      nval = ft[(nval + step - 1) * kTileLeaves] == __int_as_float(0x7f800000)
+                 ? nval : nval + step;
+    nval += ft[nval * kTileLeaves] == __int_as_float(0x7f800000) ? 0 : 1;
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+      if (k < nval) num += (T)fabs(U0 - (T)ft[k * kTileLeaves]);
+    W = (T)nval;
+  } else {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
       const float wv = wt(k);
       if (wv != 0.f) {
         W += (T)wv;
-        num += (T)wv * fabs(U0 - (T)fv);
+        num += (T)wv * fabs(U0 - (T)ft[k * kTileLeaves]);
       }
     }
   }
-  if (BINW) W = (T)nval;
   const T den = W + a.gamma;
   const T cc = a.tau / den;
   // generalised weighted median (oracle/pd_oracle.c wmedian_prox): with S_k
   // the weight of the first k sorted samples and c_k = v0 - cc*(2 S_k - W)
-  // (non-increasing in k) against the non-decreasing f_k, the oracle's scan
-  // stops at the first k* with c_k* <= f_k* (f_n = +inf) and returns
-  // max(f_(k*-1), c_k*)
+  // (non-increasing in k) against the non-decreasing f_k (+inf past the
+  // present samples), the oracle's scan stops at the first k* with
+  // c_k* <= f_k* and returns max(f_(k*-1), c_k*)
   T res0;
-  if (BINW) {
-    // unit weights, S_k = k: binary search for k* in [0, nval] on the tile
-    int lo = 0, hi = nval;
+  if (BW != kWeights) {
+    // unit weights, S_k = k: k* by branch-free bisection on the tile (the
+    // predicate is monotone over all NV ranks; k* = NV only if none holds)
+    auto below = [&](int k) {  // c_k > f_k: k* lies beyond k
+      return v0 - cc * ((T)2 * (T)k - W) > (T)ft[k * kTileLeaves];
+    };
+    int pos = 0;
 #pragma unroll
-    for (int it = 0; (1 << it) <= NV; ++it) {
-      if (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        const T cm = v0 - cc * ((T)2 * (T)mid - W);
-        if (cm <= (T)ft[mid * kTileLeaves]) hi = mid;
-        else lo = mid + 1;
-      }
-    }
-    const T ck = v0 - cc * ((T)2 * (T)lo - W);
-    res0 = lo > 0 ? fmax((T)ft[(lo - 1) * kTileLeaves], ck) : ck;
+    for (int step = NV / 2; step >= 1; step >>= 1)
+      pos = below(pos + step - 1) ? pos + step : pos;
+    pos += below(pos) ? 1 : 0;
+    const T ck = v0 - cc * ((T)2 * (T)pos - W);
+    res0 = pos > 0 ? fmax((T)ft[(pos - 1) * kTileLeaves], ck) : ck;
   } else {
     // general weights: the prefix sums are needed, so one branch-free scan
     // (min(f_k, c_k) is f_k below k* and c_k from k*: the max is the value)

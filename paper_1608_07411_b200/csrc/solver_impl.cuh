@@ -832,14 +832,14 @@ inline void smem_opt_in(const void* fn, size_t smem) {
 
 // g = tiles of this launch; staged kernels run persistent (at most the
 // resident CTAs, each walking tiles with a grid stride)
-template <typename T, bool FZ, bool BW, bool EN, int N>
+template <typename T, bool FZ, int BW, bool EN, int N>
 void launch_leaf(unsigned g, cudaStream_t st, LeafArgs<T> a) {
   constexpr size_t smem = leaf_smem_bytes(N, BW);
   const void* fn = (const void*)k_leaf_pass<T, FZ, BW, EN, N>;
   smem_opt_in(fn, smem);
   a.ntiles = (int)g;
   unsigned grid = g;
-  if (N > 0) {
+  if (OCTF_PERSIST && N > 0) {
     const unsigned res = (unsigned)resident_ctas(fn, kT, smem);
     grid = g < res ? g : res;
   }
@@ -891,19 +891,35 @@ void launch_leaf_pass(Ctx& c, const T* snap, T* uval, const int32_t* child,
     else                                                              \
       launch_leaf<T, FZ, BW, EN, 0>(g, st, a);                        \
   } while (0)
+#define OCTF_LEAF_AV(FZ, EN)                                          \
+  do {                                                                \
+    if (c.nviews == 16)                                               \
+      launch_leaf<T, FZ, kAllValid, EN, 16>(g, st, a);                \
+    else if (c.nviews == 32)                                          \
+      launch_leaf<T, FZ, kAllValid, EN, 32>(g, st, a);                \
+    else                                                              \
+      launch_leaf<T, FZ, kAllValid, EN, 8>(g, st, a);                 \
+  } while (0)
+  const bool av = c.allv && !c.ell &&
+                  (c.nviews == 8 || c.nviews == 16 || c.nviews == 32);
   if (frozen) {
-    if (c.binw) {
-      if (en) OCTF_LEAF(true, true, true); else OCTF_LEAF(true, true, false);
+    if (av) {
+      if (en) OCTF_LEAF_AV(true, true); else OCTF_LEAF_AV(true, false);
+    } else if (c.binw) {
+      if (en) OCTF_LEAF(true, kMask, true); else OCTF_LEAF(true, kMask, false);
     } else {
-      if (en) OCTF_LEAF(true, false, true); else OCTF_LEAF(true, false, false);
+      if (en) OCTF_LEAF(true, kWeights, true); else OCTF_LEAF(true, kWeights, false);
     }
   } else {
-    if (c.binw) {
-      if (en) OCTF_LEAF(false, true, true); else OCTF_LEAF(false, true, false);
+    if (av) {
+      if (en) OCTF_LEAF_AV(false, true); else OCTF_LEAF_AV(false, false);
+    } else if (c.binw) {
+      if (en) OCTF_LEAF(false, kMask, true); else OCTF_LEAF(false, kMask, false);
     } else {
-      if (en) OCTF_LEAF(false, false, true); else OCTF_LEAF(false, false, false);
+      if (en) OCTF_LEAF(false, kWeights, true); else OCTF_LEAF(false, kWeights, false);
     }
   }
+#undef OCTF_LEAF_AV
 #undef OCTF_LEAF
   OCTF_CUDA(cudaGetLastError());
   ++c.launches;
@@ -1383,15 +1399,16 @@ void frozen_passes_impl(Ctx& c, FrozenArgs& a, cudaStream_t st) {
 template <typename T>
 void pd_passes_impl(Ctx& c, PdHostArgs& a, cudaStream_t st);
 
-template <typename T, bool BW, int N, bool WP>
+template <typename T, int BW, int N, bool WP>
 void launch_pd_wp(unsigned g, cudaStream_t st, const PdArgs<T>& p) {
-  constexpr size_t smem = pd_smem_bytes(N, BW) * kStages;
+  constexpr size_t smem = pd_smem_bytes(N, BW != kWeights) * kStages;
   const void* fn = (const void*)k_pd_pass<T, BW, N, WP>;
   smem_opt_in(fn, smem);
-  const unsigned res = (unsigned)resident_ctas(fn, kT, smem);
-  k_pd_pass<T, BW, N, WP><<<g < res ? g : res, kT, smem, st>>>(p);  // persistent
+  const unsigned res =
+      OCTF_PERSIST ? (unsigned)resident_ctas(fn, kT, smem) : g;
+  k_pd_pass<T, BW, N, WP><<<g < res ? g : res, kT, smem, st>>>(p);
 }
-template <typename T, bool BW, int N>
+template <typename T, int BW, int N>
 void launch_pd(unsigned g, cudaStream_t st, const PdArgs<T>& p, bool wp) {
   if (wp) launch_pd_wp<T, BW, N, true>(g, st, p);
   else launch_pd_wp<T, BW, N, false>(g, st, p);
@@ -1403,9 +1420,9 @@ void pd_passes_impl(Ctx& c, PdHostArgs& a, cudaStream_t st) {
   if (a.npasses < 1) return;
   ensure_prepared<T>(c, a.child, a.cap, a.d_max, a.state, st);
   const int nv = c.nviews;
-  if (c.ell)
-    throw Error(kEArg, "solver='pd' needs the dense sample layout "
-                       "(octf_ctx_set_options(ctx, OCTF_CTX_DENSE))");
+  if (c.ell || !c.sorted)
+    throw Error(kEArg, "solver='pd' needs the dense, sorted sample layout "
+                       "(octf_ctx_set_options(ctx, OCTF_CTX_SORTED))");
   if (!(nv == 4 || nv == 8 || nv == 16 || nv == 32 || nv == 64) ||
       c.sstride != nv || (nv == 64 && c.binw))
     throw Error(kEArg, "solver='pd' supports 4, 8, 16, 32 or 64 views");
@@ -1452,13 +1469,16 @@ void pd_passes_impl(Ctx& c, PdHostArgs& a, cudaStream_t st) {
       if (c.timing && (int)c.pev.size() >= 2 * kChunk)
         OCTF_CUDA(cudaEventRecord(c.pev[2 * j], st));
 #define OCTF_PD(BW, N) launch_pd<T, BW, N>(g, st, p, fused_bottom)
-      if (c.binw) {
-        if (nv == 4) OCTF_PD(true, 4); else if (nv == 8) OCTF_PD(true, 8);
-        else if (nv == 16) OCTF_PD(true, 16); else OCTF_PD(true, 32);
+      if (c.allv && (nv == 8 || nv == 16 || nv == 32)) {
+        if (nv == 8) OCTF_PD(kAllValid, 8);
+        else if (nv == 16) OCTF_PD(kAllValid, 16); else OCTF_PD(kAllValid, 32);
+      } else if (c.binw) {
+        if (nv == 4) OCTF_PD(kMask, 4); else if (nv == 8) OCTF_PD(kMask, 8);
+        else if (nv == 16) OCTF_PD(kMask, 16); else OCTF_PD(kMask, 32);
       } else {
-        if (nv == 4) OCTF_PD(false, 4); else if (nv == 8) OCTF_PD(false, 8);
-        else if (nv == 16) OCTF_PD(false, 16);
-        else if (nv == 32) OCTF_PD(false, 32); else OCTF_PD(false, 64);
+        if (nv == 4) OCTF_PD(kWeights, 4); else if (nv == 8) OCTF_PD(kWeights, 8);
+        else if (nv == 16) OCTF_PD(kWeights, 16);
+        else if (nv == 32) OCTF_PD(kWeights, 32); else OCTF_PD(kWeights, 64);
       }
 #undef OCTF_PD
       OCTF_CUDA(cudaGetLastError());

@@ -21,7 +21,7 @@
 #define OCTF_PD_F32_ESUM_MIN 16
 #endif
 #ifndef OCTF_PD_MINB
-#define OCTF_PD_MINB 4  // 4 CTAs of 256 per SM: <= 64 registers
+#define OCTF_PD_MINB 5  // 5 CTAs of 256 per SM: <= 48 registers (profiles/r02)
 #endif
 #ifndef OCTF_PD_MINB_SMALL
 #define OCTF_PD_MINB_SMALL 5  // binary weights, N <= 16 (48 regs: cfg2 pd 54.8 -> 58.3 %)

@@ -63,9 +63,10 @@ int octf_selftest(void);
 int octf_ctx_create(octf_ctx **out);
 int octf_ctx_destroy(octf_ctx *ctx);
 int octf_ctx_invalidate(octf_ctx *ctx);
-/* out[0..10] = leaf blocks, leaves, live blocks, free blocks, mask-format
+/* out[0..11] = leaf blocks, leaves, live blocks, free blocks, mask-format
  * samples (0/1), sample stride, views, valid, leaf tiles, ELL layout (0/1),
- * every leaf has every sample (0/1; kernels then read no mask) (int64[11]) */
+ * every leaf has every sample (0/1; kernels then read no mask), packed
+ * sample positions in use (0/1, OCTF_CTX_PACKED) (int64[12]) */
 int octf_ctx_info(octf_ctx *ctx, int64_t *out);
 
 /* Context options.  By default more than 64 views use the ELL sample
@@ -84,6 +85,12 @@ int octf_ctx_info(octf_ctx *ctx, int64_t *out);
  * gather no samples; the next octf_ctx_select gathers its subset only (and
  * clears the flag) -- a shard never holds the whole tree's samples. */
 #define OCTF_CTX_DEFER 8
+/* OCTF_CTX_PACKED (frozen trees only): a leaf's samples sit at its rank
+ * among the leaves of its 256-slot tile, so the kernels stream only the
+ * tile's leaves' samples, not the rows of the inner siblings a leaf block
+ * spans.  The context then never patches its leaf list in place: a pass
+ * that restructures gets a full rebuild. */
+#define OCTF_CTX_PACKED 16
 int octf_ctx_set_options(octf_ctx *ctx, int flags);
 
 /* Live profiling: enable != 0 brackets the leaf-update and energy kernels

@@ -119,7 +119,7 @@ def ptr_table(ptrs):
 
 
 # octf_ctx_set_options flags (include/octfuse_b200.h)
-CTX_DENSE, CTX_ELL, CTX_SORTED, CTX_DEFER = 1, 2, 4, 8
+CTX_DENSE, CTX_ELL, CTX_SORTED, CTX_DEFER, CTX_PACKED = 1, 2, 4, 8, 16
 
 # context rebuild phases (octf_ctx.h Phase), in export order
 PHASES = ("walk", "list_diff", "tables", "ell_grow", "ell_update", "fresh",
@@ -140,10 +140,11 @@ class Ctx:
 
     def info(self) -> dict:
         import numpy as np
-        out = np.zeros(11, dtype=np.int64)
+        out = np.zeros(12, dtype=np.int64)
         call("octf_ctx_info", self.h, out.ctypes.data)
         keys = ("leaf_blocks", "leaves", "blocks", "free_blocks", "mask_samples",
-                "sample_stride", "views", "valid", "tiles", "ell", "all_valid")
+                "sample_stride", "views", "valid", "tiles", "ell", "all_valid",
+                "packed")
         return dict(zip(keys, (int(v) for v in out)))
 
     def set_dense(self, dense: bool = True) -> None:
@@ -153,7 +154,8 @@ class Ctx:
     def set_options(self, flags: int) -> None:
         """octf_ctx_set_options: CTX_DENSE (1) dense samples, CTX_ELL (2)
         ELL from 33 views, CTX_SORTED (4) samples sorted per leaf (pd),
-        CTX_DEFER (8) no sample gather before ctx_select (shards)."""
+        CTX_DEFER (8) no sample gather before ctx_select (shards),
+        CTX_PACKED (16) leaf-rank sample positions (frozen trees)."""
         call("octf_ctx_set_options", self.h, int(flags))
 
     def profile(self, enable: bool = True) -> dict:

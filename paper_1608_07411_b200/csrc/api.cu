@@ -157,6 +157,12 @@ int octf_ctx_set_options(octf_ctx* ctx, int flags) {
     if ((dense || sorted) && ell)
       throw octf::Error(octf::kEArg, "ELL excludes dense/sorted");
     ctx->c.defer_gather = (flags & OCTF_CTX_DEFER) != 0;
+    const bool pack = (flags & OCTF_CTX_PACKED) != 0;
+    if (pack != ctx->c.pack_opt) {
+      ctx->c.pack_opt = pack;
+      ctx->c.store_ok = false;
+      ctx->c.valid = false;  // regather at packed positions
+    }
     if (dense != ctx->c.dense_only || ell != ctx->c.force_ell ||
         sorted != ctx->c.sorted) {
       ctx->c.dense_only = dense || sorted;
@@ -183,6 +189,7 @@ int octf_ctx_info(octf_ctx* ctx, int64_t* out) {
     out[8] = (c.nlb * 8 + 255) / 256;  // leaf tiles (one CTA each)
     out[9] = c.ell ? 1 : 0;
     out[10] = c.allv ? 1 : 0;
+    out[11] = c.packed ? 1 : 0;
   });
 }
 

@@ -383,20 +383,26 @@ __global__ void k_vgather(const int32_t* __restrict__ ucs,
                           const int32_t* __restrict__ lblocks, int64_t nlb,
                           ViewSet vs, int v0, int64_t cap,
                           const int32_t* __restrict__ vm, float* F, float* W,
-                          int64_t stride, int32_t* nonbin) {
+                          int32_t* nonbin, const int4* __restrict__ lmeta,
+                          SDesc sd) {
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t i = gid >> 3;
   const int c = (int)(gid & 7);
   if (i >= nlb) return;
   const int y = blockIdx.y;
   const int32_t b = lblocks[i];
-  const bool active = b >= 0 && !(b == 0 && c != 0) && ucs[b + c] < 0;
+  // the list's (possibly rank-restricted) leaf mask
+  const int4 mt = lmeta[i];
+  const unsigned mask = ((unsigned)mt.w >> 19) & 0xffu;
+  const bool active = b >= 0 && !(b == 0 && c != 0) && ucs[b + c] < 0 &&
+                      ((mask >> c) & 1u);
   if (!active) return;
   const int32_t n = vm[(int64_t)y * cap + b + c];
   const float f = __ldg(vs.val[v0 + y] + n);
   const float w = __ldg(vs.w[v0 + y] + n);
-  F[samp_idx(gid, v0 + y, stride)] = f;
-  W[samp_idx(gid, v0 + y, stride)] = w;
+  const SIdx q = sidx(sd, i, c, mt.y, mask);
+  F[q.f + (int64_t)(v0 + y) * q.pitch] = f;
+  W[q.f + (int64_t)(v0 + y) * q.pitch] = w;
   // flags: bit 0 a weight other than 0/1, bit 1 a zero weight on a leaf
   if (w != 0.f && w != 1.f) atomicOr(nonbin, 1);
   if (w == 0.f) atomicOr(nonbin, 2);
@@ -408,25 +414,28 @@ __global__ void k_gather_slots(const int32_t* __restrict__ ucs,
                                const int32_t* __restrict__ lblocks, int64_t nlb,
                                const float* __restrict__ Fs,
                                const float* __restrict__ Ws, int64_t cap,
-                               int nv, float* F, float* W, int64_t stride,
-                               int32_t* nonbin) {
+                               int nv, float* F, float* W, int32_t* nonbin,
+                               const int4* __restrict__ lmeta, SDesc sd) {
   int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t i = gid >> 3;
   int c = (int)(gid & 7);
   if (i >= nlb) return;
   int32_t b = lblocks[i];
-  bool active = b >= 0 && !(b == 0 && c != 0) && ucs[b + c] < 0;
+  // only the list's (possibly rank-restricted) leaves hold samples
+  const int4 mt = lmeta[i];
+  const unsigned mask = ((unsigned)mt.w >> 19) & 0xffu;
+  const bool active = b >= 0 && !(b == 0 && c != 0) && ucs[b + c] < 0 &&
+                      ((mask >> c) & 1u);
+  if (!active) return;
+  const SIdx q = sidx(sd, i, c, mt.y, mask);
   int flag = 0;
   for (int v = 0; v < nv; ++v) {
-    float f = 0.f, w = 0.f;
-    if (active) {
-      f = Fs[(int64_t)v * cap + b + c];
-      w = Ws ? Ws[(int64_t)v * cap + b + c] : 1.f;
-      flag |= (w != 0.f && w != 1.f) ? 1 : 0;
-      flag |= w == 0.f ? 2 : 0;
-    }
-    F[samp_idx(gid, v, stride)] = f;
-    W[samp_idx(gid, v, stride)] = w;
+    const float f = Fs[(int64_t)v * cap + b + c];
+    const float w = Ws ? Ws[(int64_t)v * cap + b + c] : 1.f;
+    flag |= (w != 0.f && w != 1.f) ? 1 : 0;
+    flag |= w == 0.f ? 2 : 0;
+    F[q.f + (int64_t)v * q.pitch] = f;
+    W[q.f + (int64_t)v * q.pitch] = w;
   }
   if (flag) atomicOr(nonbin, flag);
 }
@@ -613,7 +622,7 @@ __global__ void k_gather_fresh(const int32_t* __restrict__ fresh,
     int L, pz;
     unsigned mask;
     unpack_meta_w(m.w, pz, mask, L);
-    const int x = b == 0 ? 0 : 2 * m.y + ((c >> 2) & 1);
+    const int x = b == 0 ? 0 : 2 * meta_px(m.y) + ((c >> 2) & 1);
     const int y = b == 0 ? 0 : 2 * m.z + ((c >> 1) & 1);
     const int z = b == 0 ? 0 : 2 * pz + (c & 1);
     uint32_t bits = 0;
@@ -706,7 +715,7 @@ __global__ void k_ell_fresh(const int32_t* __restrict__ fresh,
     int L, pz;
     unsigned mask;
     unpack_meta_w(m.w, pz, mask, L);
-    const int x = b == 0 ? 0 : 2 * m.y + ((c >> 2) & 1);
+    const int x = b == 0 ? 0 : 2 * meta_px(m.y) + ((c >> 2) & 1);
     const int y = b == 0 ? 0 : 2 * m.z + ((c >> 1) & 1);
     const int z = b == 0 ? 0 : 2 * pz + (c & 1);
     const int K = tileK[s >> 8];
@@ -869,14 +878,53 @@ __global__ void k_ell_tilemax(const int32_t* __restrict__ cnt, int64_t n,
 }
 
 
-__global__ void k_masks(const float* __restrict__ W, int64_t stride, int nv,
-                        int64_t n, uint32_t* M) {
-  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= n) return;
+// binary weights -> the bit-mask format, per leaf of the list
+__global__ void k_masks(const float* __restrict__ W, const int4* __restrict__ lmeta,
+                        int64_t nlb, int nv, SDesc sd, uint32_t* M) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = gid >> 3;
+  const int c = (int)(gid & 7);
+  if (i >= nlb) return;
+  const int4 mt = lmeta[i];
+  const unsigned mask = ((unsigned)mt.w >> 19) & 0xffu;
+  if (!((mask >> c) & 1u) || (mt.x == 0 && c != 0)) return;
+  const SIdx q = sidx(sd, i, c, mt.y, mask);
   uint32_t m = 0;
   for (int v = 0; v < nv; ++v)
-    m |= (W[samp_idx(s, v, stride)] != 0.f ? 1u : 0u) << v;
-  M[s] = m;
+    m |= (W[q.f + (int64_t)v * q.pitch] != 0.f ? 1u : 0u) << v;
+  M[q.m] = m;
+}
+
+// packed store (octf_common.cuh SDesc): one warp per tile of 32 leaf
+// blocks; each block's first rank (exclusive scan of the leaf counts) into
+// the top byte of lmeta.y; nonfull counts the tiles holding a block that is
+// not 8 leaves (without one, ranks are slots and the plain layout is kept)
+__global__ void k_pack_ranks(int4* lmeta, int64_t nlb, int64_t ntiles,
+                             int32_t* nonfull) {
+  const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= ntiles) return;
+  const int64_t i = t * 32 + lane;
+  int4 m = make_int4(0, 0, 0, 0);
+  unsigned mask = 0;
+  if (i < nlb) {
+    m = lmeta[i];
+    mask = ((unsigned)m.w >> 19) & 0xffu;
+    if (m.x == 0) mask &= 1u;  // the root's pseudo-block has one slot
+  }
+  const int cnt = __popc(mask);
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (i < nlb) {
+    m.y = meta_px(m.y) | ((incl - cnt) << 24);
+    lmeta[i] = m;
+  }
+  const bool odd = i < nlb && mask != 0xffu;
+  if (__any_sync(0xffffffffu, odd) && lane == 0) atomicAdd(nonfull, 1);
 }
 
 __global__ void k_walk_free(const int32_t* __restrict__ child, int64_t head,
@@ -979,7 +1027,8 @@ void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
   int64_t nbid = block_id(used) + 1;
   // patch the leaf-block list in place when this rebuild follows our own
   // restructuring of the same pool (ctx_list_update)
-  const bool incremental = !c.no_regather && c.own_change && c.store_ok &&
+  const bool incremental = !c.no_regather && !c.pack_opt && c.own_change &&
+                           c.store_ok &&
                            c.list_full && c.nviews > 0 && !c.ext_F &&
                            c.child_key == child && c.cap == cap &&
                            c.d_max == d_max;
@@ -1440,7 +1489,7 @@ static void gather_by_levels(Ctx& c, int64_t nvp, cudaStream_t st) {
   view_maps(c, st, [&](int v0, int nc, const int32_t* vm) {
     k_vgather<<<dim3(grid_for(n), nc), kThreads, 0, st>>>(
         c.child_key, c.lblocks.p, c.nlb, ctx_views(c), v0, c.cap, vm, c.F.p,
-        c.W.p, nvp, c.counters.p);
+        c.W.p, c.counters.p, c.lmeta.p, c.sd);
   });
 }
 
@@ -1490,6 +1539,8 @@ void ctx_gather_ell(Ctx& c, cudaStream_t st) {
   c.binw = false;
   c.allv = false;
   c.ell = true;
+  c.packed = false;
+  c.sd = SDesc();
   c.ell_tiles = nt;
   c.ell_size = total;
   c.ell_waste = 0;
@@ -1499,13 +1550,13 @@ void ctx_gather_ell(Ctx& c, cudaStream_t st) {
 void ctx_sort_samples(Ctx& c, const int32_t* list, const int32_t* nlist,
                       cudaStream_t st) {
   if (!c.sorted || c.ell) return;
-  const int64_t n = (c.nlb * 8 + kTileLeaves - 1) / kTileLeaves * kTileLeaves;
+  const int64_t n = c.nlb * 8;
   const uint32_t* M = c.binw ? c.M.p : nullptr;
   float* W = c.binw ? nullptr : c.W.p;
   const unsigned g = 148 * 8;  // grid-stride (the list count is on the device)
 #define OCTF_SORT(N)                                                          \
   k_sort_samples<N><<<g, kThreads, 0, st>>>(list, nlist, n, c.nviews, c.F.p, \
-                                             W, M)
+                                             W, M, c.lmeta.p, c.sd)
   switch (c.sstride) {
     case 4: OCTF_SORT(4); break;
     case 8: OCTF_SORT(8); break;
@@ -1532,22 +1583,39 @@ void ctx_gather(Ctx& c, cudaStream_t st) {
     return;
   }
   c.ell = false;
-  // tiles of 256 leaves, view-major inside a tile (octf_common.cuh
-  // samp_idx); views padded to 4 and leaves to whole tiles
+  // tiles of 256 slots, view-major inside a tile (octf_common.cuh SDesc);
+  // views padded to 4; packed: a group-k tile holds its 32 k leaves only
   int64_t n = c.nlb * 8;
-  const int64_t npad = (n + kTileLeaves - 1) / kTileLeaves * kTileLeaves;
+  const int64_t ntiles = (n + kTileLeaves - 1) / kTileLeaves;
   int nv = c.nviews;
   const int64_t nvp = (nv + 3) & ~3;
   c.sstride = nvp;
-  c.F.ensure((size_t)nvp * npad);
-  c.W.ensure((size_t)nvp * npad);
-  OCTF_CUDA(cudaMemsetAsync(c.F.p, 0, (size_t)nvp * npad * sizeof(float), st));
-  OCTF_CUDA(cudaMemsetAsync(c.W.p, 0, (size_t)nvp * npad * sizeof(float), st));
+  // packed positions (a frozen tree's full list; a shard's subset keeps
+  // slot positions): block ranks first, kept only if some block is not full
+  SDesc d;
+  d.nvp = nvp;
+  if (c.pack_opt && c.list_full && ntiles) {
+    OCTF_CUDA(cudaMemsetAsync(c.counters.p + 1, 0, sizeof(int32_t), st));
+    k_pack_ranks<<<grid_for(ntiles * 32), kThreads, 0, st>>>(
+        c.lmeta.p, c.nlb, ntiles, c.counters.p + 1);
+    OCTF_CUDA(cudaGetLastError());
+    OCTF_CUDA(cudaMemcpyAsync(c.h_counters + 1, c.counters.p + 1,
+                              sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    OCTF_CUDA(cudaStreamSynchronize(st));
+    d.packed = c.h_counters[1] > 0 ? 1 : 0;
+  }
+  const int64_t nf = ntiles * nvp * kTileLeaves, nm = ntiles * kTileLeaves;
+  c.sd = d;
+  c.packed = d.packed != 0;
+  c.F.ensure((size_t)nf);
+  c.W.ensure((size_t)nf);
+  OCTF_CUDA(cudaMemsetAsync(c.F.p, 0, (size_t)nf * sizeof(float), st));
+  OCTF_CUDA(cudaMemsetAsync(c.W.p, 0, (size_t)nf * sizeof(float), st));
   OCTF_CUDA(cudaMemsetAsync(c.counters.p, 0, sizeof(int32_t), st));
   if (c.ext_F)  // per-slot sample arrays supplied by the caller
     k_gather_slots<<<grid_for(n), kThreads, 0, st>>>(
         c.child_key, c.lblocks.p, c.nlb, c.ext_F, c.ext_W, c.ext_cap, nv, c.F.p,
-        c.W.p, nvp, c.counters.p);
+        c.W.p, c.counters.p, c.lmeta.p, c.sd);
   else
     gather_by_levels(c, nvp, st);
   OCTF_CUDA(cudaGetLastError());
@@ -1559,8 +1627,10 @@ void ctx_gather(Ctx& c, cudaStream_t st) {
   c.allv = c.binw && !(c.h_counters[0] & 2) && nv == nvp &&
            (nv == 8 || nv == 16 || nv == 32);
   if (c.binw) {
-    c.M.ensure(npad);
-    k_masks<<<grid_for(npad), kThreads, 0, st>>>(c.W.p, nvp, nv, npad, c.M.p);
+    c.M.ensure(nm);
+    OCTF_CUDA(cudaMemsetAsync(c.M.p, 0, (size_t)nm * sizeof(uint32_t), st));
+    k_masks<<<grid_for(n), kThreads, 0, st>>>(c.W.p, c.lmeta.p, c.nlb, nv,
+                                              c.sd, c.M.p);
     OCTF_CUDA(cudaGetLastError());
     OCTF_CUDA(cudaStreamSynchronize(st));
     c.W.release();  // the mask format replaces the weight vectors

@@ -35,9 +35,10 @@
 #define OCTF_LEAF_MINB_SMALL 6
 #endif
 constexpr int leaf_minb(int nv, int tbytes) {
-  // (f64 values need the registers: 40 would spill)
-  return (tbytes == 4 && nv > 0 && nv <= 16) ? OCTF_LEAF_MINB_SMALL
-                                             : OCTF_LEAF_MINB;
+  // (the f64 parity mode needs the registers: 40 or 48 would spill)
+  return tbytes == 8 ? 2
+         : (nv > 0 && nv <= 16) ? OCTF_LEAF_MINB_SMALL
+                                : OCTF_LEAF_MINB;
 }
 
 template <typename T>
@@ -66,6 +67,7 @@ struct LeafArgs {
   int ntiles = 0;  // tiles of this launch ([tile0, tile0 + ntiles))
   const int32_t* __restrict__ tileK = nullptr;    // ELL store (views > 32)
   const int64_t* __restrict__ tileOff = nullptr;
+  SDesc sd;  // the dense sample store's layout (octf_common.cuh)
 };
 
 // slot read for the cell (x+DX, y+DY, z+DZ) at the leaf's level, from the
@@ -163,7 +165,8 @@ constexpr size_t leaf_smem_bytes(int nv, int bw) {
   return leaf_stage_floats(nv, bw) * 4 * kStages;
 }
 
-// issue the bulk copies of tile `tile` into stage buffer `buf` (thread 0)
+// issue the bulk copy of tile `tile` into stage buffer `buf` (thread 0):
+// the whole [view][256] slot tile, then its mask or weight tile
 template <int NVP, int BW>
 __device__ __forceinline__ void stage_tile(float* buf, uint64_t* bar,
                                            const float* F, const void* A,
@@ -179,6 +182,43 @@ __device__ __forceinline__ void stage_tile(float* buf, uint64_t* bar,
              BW == kMask ? (const void*)((const uint32_t*)A + tile * kTileLeaves)
                          : (const void*)((const float*)A + tile * NVP * kTileLeaves),
              abytes, bar);
+}
+
+// packed store (octf_common.cuh SDesc): a tile's n_t leaves fill its first
+// ceil(n_t / 32) chunks of NV x 32 samples.  Thread 0 stages the first
+// kEarlyChunks chunks (and the mask tile) at once, before anything is
+// known about the tile; thread kT-1 stages the remaining chunks as soon as
+// its own block's lmeta (first rank + leaf count = n_t) has arrived.  The
+// barrier expects both arrivals.  nchunks < 0: the early part.
+template <int NVP, int BW>
+__device__ __forceinline__ void stage_packed(float* buf, uint64_t* bar,
+                                             const float* F, const void* A,
+                                             size_t tile, int nchunks) {
+  constexpr unsigned cb = NVP * kChunk * 4;  // bytes per chunk
+  const size_t fo = tile * NVP * kTileLeaves;
+  if (nchunks < 0) {
+    const unsigned fbytes = kEarlyChunks * cb;
+    const unsigned abytes = BW == kAllValid ? 0u
+                            : BW == kMask   ? kTileLeaves * 4u
+                                            : fbytes;
+    mbar_expect_tx(bar, fbytes + abytes);
+    bulk_g2s(buf, F + fo, fbytes, bar);
+    if (abytes)
+      bulk_g2s(buf + NVP * kTileLeaves,
+               BW == kMask ? (const void*)((const uint32_t*)A + tile * kTileLeaves)
+                           : (const void*)((const float*)A + fo),
+               abytes, bar);
+    return;
+  }
+  const int rest = nchunks > kEarlyChunks ? nchunks - kEarlyChunks : 0;
+  const unsigned bytes = rest * cb;
+  mbar_expect_tx(bar, BW == kWeights ? 2 * bytes : bytes);
+  if (!rest) return;
+  const size_t off = (size_t)kEarlyChunks * NVP * kChunk;
+  bulk_g2s(buf + off, F + fo + off, bytes, bar);
+  if (BW == kWeights)
+    bulk_g2s(buf + NVP * kTileLeaves + off, (const float*)A + fo + off, bytes,
+             bar);
 }
 
 // packed fp32 pairs (sm_100a FADD2 / FFMA2)
@@ -218,10 +258,13 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
   __shared__ __align__(8) uint64_t s_bar[kStages];
   const int tend = a.tile0 + a.ntiles;
   const void* aux = BINW ? (const void*)a.M : (const void*)a.W;
+  // packed store: each tile is staged at the top of its own iteration by
+  // threads 0 and kT-1 (stage_packed; no prefetch across tiles)
+  const bool packed = a.sd.packed != 0;
   if (NV > 0) {
     if (threadIdx.x == 0) {
-      for (int k = 0; k < kStages; ++k) mbar_init(&s_bar[k], 1);
-      for (int k = 0; k < kStages; ++k) {
+      for (int k = 0; k < kStages; ++k) mbar_init(&s_bar[k], packed ? 2 : 1);
+      for (int k = 0; k < kStages && !packed; ++k) {
         const int t = a.tile0 + (int)blockIdx.x + k * (int)gridDim.x;
         if (t < tend)
           stage_tile<NVP, BW>(s_smem + k * STAGE, &s_bar[k], a.F, aux, t);
@@ -239,6 +282,8 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
   const int i = gid >> 3;
   const int c = gid & 7;
   const bool inrange = i < (int)a.nlb;
+  if (NV > 0 && packed && threadIdx.x == 0)
+    stage_packed<NVP, BW>(s_tile, &s_bar[stage], a.F, aux, tile_id, -1);
 
   // one 16 B load: base slot, parent cell, leaf mask and level
   const int4 meta = inrange ? __ldg(a.lmeta + i) : make_int4(0, 0, 0, 0);
@@ -247,9 +292,22 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
   int L, pz;
   unsigned lmask;
   unpack_meta_w(meta.w, pz, lmask, L);
-  const int px = meta.y, py = meta.z;
+  const int px = meta_px(meta.y), py = meta.z;
   const bool slot_ok = inrange && !(b == 0 && c != 0);
   const bool active = slot_ok && ((lmask >> c) & 1u);
+  // the leaf's entry in the staged tile: its slot, or (packed) its rank r
+  // among the tile's leaves at chunk r / 32, lane r % 32, views 32 apart
+  int sbase = threadIdx.x, sstr = kTileLeaves;
+  if (packed) {
+    const int r = (meta_rbase(meta.y) + __popc(lmask & ((1u << c) - 1u))) & 255;
+    sbase = (r >> 5) * NVP * kChunk + (r & 31);
+    sstr = kChunk;
+    if (NV > 0 && threadIdx.x == kT - 1)  // n_t from the tile's last block
+      stage_packed<NVP, BW>(
+          s_tile, &s_bar[stage], a.F, aux, tile_id,
+          inrange ? (meta_rbase(meta.y) + __popc(lmask) + kChunk - 1) / kChunk
+                  : kTileLeaves / kChunk);
+  }
   const int cx = (c >> 2) & 1, cy = (c >> 1) & 1, cz = c & 1;
   const int x = 2 * px + cx, y = 2 * py + cy, z = 2 * pz + cz;
   const int m = 1 << L;
@@ -339,8 +397,13 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
   };
   if (NV > 0) {
     mbar_wait(&s_bar[stage], (unsigned)(it / kStages) & 1u);
-    const int t = threadIdx.x;
-    const float* sf = s_tile;
+    // view v of the leaf at sf[v * R]; its mask word at the mask tile's
+    // entry for the slot / rank
+    const int R = sstr;
+    const float* sf = s_tile + sbase;
+    const int t = packed ? (meta_rbase(meta.y) +
+                            __popc(lmask & ((1u << c) - 1u))) & 255
+                         : (int)threadIdx.x;
     if (BW == kAllValid && sizeof(T) == 4) {
       // fp32 throughput mode, every sample present: no mask, den = gamma + N,
       // and the samples in pairs through the packed fp32 pipes (FADD2/FFMA2;
@@ -350,8 +413,8 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
       float2 n2 = make_float2(0.f, 0.f), m2 = make_float2(0.f, 0.f);
 #pragma unroll
       for (int v = 0; v < NV; v += 2) {
-        const float2 d = sub2(S2, make_float2(sf[v * kTileLeaves + t],
-                                              sf[(v + 1) * kTileLeaves + t]));
+        const float2 d = sub2(S2, make_float2(sf[v * R],
+                                              sf[(v + 1) * R]));
         const float2 q = fma2(d, d, E2);
         const float2 r = make_float2(rsqrtf(q.x), rsqrtf(q.y));
         n2 = fma2(d, r, n2);
@@ -363,7 +426,7 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
     } else if (BW == kAllValid) {
       // parity mode: the reference's sequential order, unit weights
 #pragma unroll
-      for (int v = 0; v < NV; ++v) sample((T)1, sf[v * kTileLeaves + t]);
+      for (int v = 0; v < NV; ++v) sample((T)1, sf[v * R]);
     } else if (BINW && sizeof(T) == 4 && NV <= 16) {
       // fp32 throughput mode: unit weights, so den = gamma + count (one
       // rounding instead of one per view; the fp64 parity mode keeps the
@@ -373,7 +436,7 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
 #pragma unroll
       for (int v = 0; v < NV; ++v)
         if (mk & (1u << v)) {
-          const T d = S0 - (T)sf[v * kTileLeaves + t];
+          const T d = S0 - (T)sf[v * R];
           if (ENERGY) {
             T g, e;
             A::data_both((T)1, d, p.eps2, g, e);
@@ -388,13 +451,13 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
       const uint32_t mk = reinterpret_cast<const uint32_t*>(s_tile + NVP * kTileLeaves)[t];
 #pragma unroll
       for (int v = 0; v < NV; ++v)
-        if (mk & (1u << v)) sample((T)1, sf[v * kTileLeaves + t]);
+        if (mk & (1u << v)) sample((T)1, sf[v * R]);
     } else {
-      const float* sw = s_tile + NVP * kTileLeaves;
+      const float* sw = s_tile + NVP * kTileLeaves + sbase;
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
-        const float wv = sw[v * kTileLeaves + t];
-        if (wv != 0.f) sample((T)wv, sf[v * kTileLeaves + t]);
+        const float wv = sw[v * R];
+        if (wv != 0.f) sample((T)wv, sf[v * R]);
       }
     }
   } else if (active && a.tileK) {  // ELL: the leaf's observed views, in order
@@ -404,13 +467,14 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
       if (wv != 0.f) sample((T)wv, __ldg(a.F + ell_idx(a.tileOff, gid, r)));
     }
   } else if (active) {
-    uint32_t mk = BINW ? __ldg(a.M + gid) : 0u;
+    const SIdx q = sidx(a.sd, i, c, meta.y, lmask);
+    uint32_t mk = BINW ? __ldg(a.M + q.m) : 0u;
     for (int v = 0; v < a.nv; ++v) {
-      const float fv = __ldg(a.F + samp_idx(gid, v, a.stride));
+      const float fv = __ldg(a.F + q.f + (int64_t)v * q.pitch);
       if (BINW) {
         if ((mk >> v) & 1u) sample((T)1, fv);
       } else {
-        const float wv = __ldg(a.W + samp_idx(gid, v, a.stride));
+        const float wv = __ldg(a.W + q.f + (int64_t)v * q.pitch);
         if (wv != 0.f) sample((T)wv, fv);
       }
     }
@@ -483,7 +547,7 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
     // it with the tile kStages steps ahead
     __syncthreads();
     const int nt = tile_id + kStages * (int)gridDim.x;
-    if (threadIdx.x == 0 && nt < tend)
+    if (threadIdx.x == 0 && nt < tend && !packed)
       stage_tile<NVP, BW>(s_tile, &s_bar[stage], a.F, aux, nt);
   } else if (ENERGY) {
     __syncthreads();  // the energy scratch is reused by the next tile

@@ -67,6 +67,57 @@ __host__ __device__ __forceinline__ int64_t samp_idx(int64_t leaf, int v,
   return (leaf >> 8) * (nvp << 8) + ((int64_t)v << 8) + (leaf & 255);
 }
 
+// The dense sample store (Ctx::sd): tiles of 256 slots = the 32 leaf blocks
+// a leaf-kernel CTA covers (leaf-block list entries 32t .. 32t+31), nvp rows
+// (views padded to 4) each.
+//  * slot layout: [tile][view][256], entry = the slot (samp_idx) -- inner
+//    and free siblings of a leaf block own an (empty) entry too;
+//  * packed layout (OCTF_CTX_PACKED, frozen trees): a leaf's entry is its
+//    rank r among the tile's LEAVES, stored in chunks of 32 leaves,
+//    [tile][r / 32][view][32].  The list keeps its spatial order (neighbour
+//    values stay in L2 / L1); a tile's n_t leaves fill its first
+//    ceil(n_t / 32) chunks, so the kernels stream only those -- no entries
+//    for the inner siblings a leaf block spans (12 % of the slots on
+//    BASELINE config 4).  Any prefix of chunks is valid whatever n_t is,
+//    so the first 6 chunks are staged at once and the rest once n_t is
+//    known (leaf_kernel.cuh stage_packed).  A block's first rank lives in
+//    the top byte of lmeta.y (px < 2^19).
+constexpr int kChunk = 32;         // leaves per chunk
+constexpr int kEarlyChunks = 6;    // chunks staged before n_t is known
+struct SDesc {
+  int packed = 0;
+  int64_t nvp = 0;  // rows per tile (views padded to 4)
+};
+__host__ __device__ __forceinline__ int meta_px(int y) { return y & 0xffffff; }
+__host__ __device__ __forceinline__ int meta_rbase(int y) {
+  return (int)((unsigned)y >> 24);
+}
+__host__ __device__ __forceinline__ int popc8(unsigned m) {
+#ifdef __CUDA_ARCH__
+  return __popc(m);
+#else
+  return __builtin_popcount(m);
+#endif
+}
+struct SIdx {
+  int64_t f;  // F / W index of view 0 (view v at f + v * pitch)
+  int64_t m;  // M index
+  int pitch;  // distance between views
+};
+// store position of slot c of list block i (its lmeta y word and leaf mask)
+__host__ __device__ __forceinline__ SIdx sidx(const SDesc& d, int64_t i, int c,
+                                              int y, unsigned mask) {
+  const int64_t t = i >> 5;
+  const int64_t base = t * d.nvp * 256;
+  if (!d.packed) {
+    const int r = (int)((i & 31) << 3) + c;
+    return {base + r, t * 256 + r, 256};
+  }
+  const int r = meta_rbase(y) + popc8(mask & ((1u << c) - 1u));
+  return {base + (int64_t)(r >> 5) * d.nvp * kChunk + (r & 31), t * 256 + r,
+          kChunk};
+}
+
 // spread the low 21 bits of v to every third bit
 __host__ __device__ __forceinline__ uint64_t spread3(uint64_t v) {
   v &= 0x1fffff;

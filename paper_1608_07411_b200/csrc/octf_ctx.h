@@ -176,6 +176,11 @@ struct Ctx {
   bool allv = false;          // ... and every leaf has all of them (no mask
                               // read; set with 8/16/32 views)
   int64_t sstride = 0;        // views per leaf vector, padded to 4
+  // packed store (OCTF_CTX_PACKED, frozen trees; octf_common.cuh SDesc):
+  // a leaf's samples at its rank among its tile's leaves
+  bool pack_opt = false;      // requested
+  bool packed = false;        // in use (some block is not 8 leaves)
+  SDesc sd;                   // the dense store's layout
   // ELL layout (views > 64, unless dense_only): F/W hold per tile K_t rows
   // of the leaves' observed samples (octf_common.cuh ell_idx)
   bool ell = false;

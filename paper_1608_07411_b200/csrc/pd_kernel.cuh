@@ -26,8 +26,10 @@
 #ifndef OCTF_PD_MINB_SMALL
 #define OCTF_PD_MINB_SMALL 5  // binary weights, N <= 16 (48 regs: cfg2 pd 54.8 -> 58.3 %)
 #endif
-constexpr int pd_minb(bool binw, int nv) {
-  return !binw ? 1 : (nv <= 16 ? OCTF_PD_MINB_SMALL : OCTF_PD_MINB);
+constexpr int pd_minb(bool binw, int nv, int tbytes) {
+  // (the f64 parity mode: 48 registers would spill)
+  return tbytes == 8 || !binw ? 1
+                              : (nv <= 16 ? OCTF_PD_MINB_SMALL : OCTF_PD_MINB);
 }
 
 template <typename T>
@@ -56,6 +58,7 @@ struct PdArgs {
   int clamp;
   double* epart;
   const int32_t* __restrict__ lpar;  // parent slot of each leaf block
+  SDesc sd;  // the dense sample store's layout (octf_common.cuh)
 };
 
 template <typename T>
@@ -88,7 +91,7 @@ constexpr size_t pd_smem_bytes(int nv, bool binw) {  // one stage
 // WP: also write the bottom propagate level of the five fields (frozen
 // passes over a full leaf-block list)
 template <typename T, int BW, int NV, bool WP = false>
-__global__ void __launch_bounds__(kT, pd_minb(BW != kWeights, NV)) k_pd_pass(PdArgs<T> a) {
+__global__ void __launch_bounds__(kT, pd_minb(BW != kWeights, NV, sizeof(T))) k_pd_pass(PdArgs<T> a) {
   static_assert(NV > 0 && (NV & (NV - 1)) == 0, "NV: power of two");
   constexpr bool BINW = BW != kWeights;  // unit weights (+inf = absent)
   // NV = 64, general weights: only the f tile is staged (weights from global)
@@ -101,20 +104,33 @@ __global__ void __launch_bounds__(kT, pd_minb(BW != kWeights, NV)) k_pd_pass(PdA
   extern __shared__ __align__(128) float s_smem[];
   __shared__ __align__(8) uint64_t s_bar[kStages];
   const int ntiles = (int)((a.nlb * 8 + kTileLeaves - 1) / kTileLeaves);
-  auto stage_pd = [&](float* buf, uint64_t* bar, size_t tile) {
-    const unsigned fbytes = NV * kTileLeaves * 4;
-    const unsigned abytes = (BINW || WGLOB) ? 0 : fbytes;
-    mbar_expect_tx(bar, fbytes + abytes);
-    bulk_g2s(buf, a.F + tile * NV * kTileLeaves, fbytes, bar);
-    if (abytes)
-      bulk_g2s(buf + NV * kTileLeaves, a.W + tile * NV * kTileLeaves, abytes,
-               bar);
+  // the sorted sample tile (and the weight tile): whole (nchunks = -2),
+  // or packed (octf_common.cuh SDesc) in two parts like k_leaf_pass's
+  // stage_packed -- the first kEarlyChunks chunks (nchunks = -1), then the
+  // rest of the tile's ceil(n_t / 32) chunks
+  const bool packed = a.sd.packed != 0;
+  auto stage_pd = [&](float* buf, uint64_t* bar, int tile, int nchunks) {
+    constexpr bool WST = !(BINW || WGLOB);  // weights staged too
+    const size_t fo = (size_t)tile * NV * kTileLeaves;
+    size_t off = 0;
+    unsigned bytes = NV * kTileLeaves * 4;
+    if (nchunks == -1) {
+      bytes = kEarlyChunks * NV * kChunk * 4;
+    } else if (nchunks >= 0) {
+      const int rest = nchunks > kEarlyChunks ? nchunks - kEarlyChunks : 0;
+      off = (size_t)kEarlyChunks * NV * kChunk;
+      bytes = rest * NV * kChunk * 4;
+    }
+    mbar_expect_tx(bar, WST ? 2 * bytes : bytes);
+    if (!bytes) return;
+    bulk_g2s(buf + off, a.F + fo + off, bytes, bar);
+    if (WST) bulk_g2s(buf + NV * kTileLeaves + off, a.W + fo + off, bytes, bar);
   };
   if (threadIdx.x == 0) {
-    for (int k = 0; k < kStages; ++k) mbar_init(&s_bar[k], 1);
-    for (int k = 0; k < kStages; ++k) {
+    for (int k = 0; k < kStages; ++k) mbar_init(&s_bar[k], packed ? 2 : 1);
+    for (int k = 0; k < kStages && !packed; ++k) {
       const int t = (int)blockIdx.x + k * (int)gridDim.x;
-      if (t < ntiles) stage_pd(s_smem + k * STAGE, &s_bar[k], t);
+      if (t < ntiles) stage_pd(s_smem + k * STAGE, &s_bar[k], t, -2);
     }
   }
   __syncthreads();
@@ -127,15 +143,30 @@ __global__ void __launch_bounds__(kT, pd_minb(BW != kWeights, NV)) k_pd_pass(PdA
   const int i = gid >> 3;
   const int c = gid & 7;
   const bool inrange = i < (int)a.nlb;
+  if (packed && threadIdx.x == 0)
+    stage_pd(s_tile, &s_bar[stage], tile_id, -1);
   const int4 meta = inrange ? __ldg(a.lmeta + i) : make_int4(0, 0, 0, 0);
   const int32_t b = meta.x;
   const int32_t s = b + c;
   int L, pz;
   unsigned lmask;
   unpack_meta_w(meta.w, pz, lmask, L);
-  const int px = meta.y, py = meta.z;
+  const int px = meta_px(meta.y), py = meta.z;
   const bool slot_ok = inrange && !(b == 0 && c != 0);
   const bool active = slot_ok && ((lmask >> c) & 1u);
+  // the leaf's entry in the staged tile: its slot, or (packed) its rank r
+  // among the tile's leaves at chunk r / 32, lane r % 32, sorted ranks 32
+  // apart
+  int sp = threadIdx.x, R = kTileLeaves;
+  if (packed) {
+    const int r = (meta_rbase(meta.y) + __popc(lmask & ((1u << c) - 1u))) & 255;
+    sp = (r >> 5) * NV * kChunk + (r & 31);
+    R = kChunk;
+    if (threadIdx.x == kT - 1)  // n_t from the tile's last block
+      stage_pd(s_tile, &s_bar[stage], tile_id,
+               inrange ? (meta_rbase(meta.y) + __popc(lmask) + kChunk - 1) / kChunk
+                       : kTileLeaves / kChunk);
+  }
   const int cx = (c >> 2) & 1, cy = (c >> 1) & 1, cz = c & 1;
   const int x = 2 * px + cx, y = 2 * py + cy, z = 2 * pz + cz;
   const int m = 1 << L;
@@ -227,17 +258,17 @@ __global__ void __launch_bounds__(kT, pd_minb(BW != kWeights, NV)) k_pd_pass(PdA
   // entries last as +inf with weight 0 (sample_sort.cuh, once per leaf)
   mbar_wait(&s_bar[stage], (unsigned)(it / kStages) & 1u);
   const int t = threadIdx.x;
-  const float* ft = s_tile + t;  // rank k at ft[k * kTileLeaves]
-  const float* wsm = s_tile + NV * kTileLeaves + t;
-  const float* wgl = a.W + (size_t)tile_id * NV * kTileLeaves + t;
+  const float* ft = s_tile + sp;  // rank k at ft[k * R]
+  const float* wsm = s_tile + NV * kTileLeaves + sp;
+  const float* wgl = a.W + (size_t)tile_id * NV * kTileLeaves + sp;
   auto wt = [&](int k) -> float {
-    return WGLOB ? __ldg(wgl + k * kTileLeaves) : wsm[k * kTileLeaves];
+    return WGLOB ? __ldg(wgl + k * R) : wsm[k * R];
   };
   // weight sum and the energy numerator, sorted order (pd_oracle.c)
   T W = 0, num = 0;
   if (BW == kAllValid) {  // every sample present: W = N
 #pragma unroll
-    for (int k = 0; k < NV; ++k) num += (T)fabs(U0 - (T)ft[k * kTileLeaves]);
+    for (int k = 0; k < NV; ++k) num += (T)fabs(U0 - (T)ft[k * R]);
     W = (T)NV;
   } else if (BW == kMask) {
     // unit weights: the present samples are the finite prefix; its length by
@@ -245,12 +276,12 @@ __global__ void __launch_bounds__(kT, pd_minb(BW != kWeights, NV)) k_pd_pass(PdA
     int nval = 0;
 #pragma unroll
     for (int step = NV / 2; step >= 1; step >>= 1)
-      nval = ft[(nval + step - 1) * kTileLeaves] == __int_as_float(0x7f800000)
+      nval = ft[(nval + step - 1) * R] == __int_as_float(0x7f800000)
                  ? nval : nval + step;
-    nval += ft[nval * kTileLeaves] == __int_as_float(0x7f800000) ? 0 : 1;
+    nval += ft[nval * R] == __int_as_float(0x7f800000) ? 0 : 1;
 #pragma unroll
     for (int k = 0; k < NV; ++k)
-      if (k < nval) num += (T)fabs(U0 - (T)ft[k * kTileLeaves]);
+      if (k < nval) num += (T)fabs(U0 - (T)ft[k * R]);
     W = (T)nval;
   } else {
 #pragma unroll
@@ -258,7 +289,7 @@ __global__ void __launch_bounds__(kT, pd_minb(BW != kWeights, NV)) k_pd_pass(PdA
       const float wv = wt(k);
       if (wv != 0.f) {
         W += (T)wv;
-        num += (T)wv * fabs(U0 - (T)ft[k * kTileLeaves]);
+        num += (T)wv * fabs(U0 - (T)ft[k * R]);
       }
     }
   }
@@ -274,7 +305,7 @@ __global__ void __launch_bounds__(kT, pd_minb(BW != kWeights, NV)) k_pd_pass(PdA
     // unit weights, S_k = k: k* by branch-free bisection on the tile (the
     // predicate is monotone over all NV ranks; k* = NV only if none holds)
     auto below = [&](int k) {  // c_k > f_k: k* lies beyond k
-      return v0 - cc * ((T)2 * (T)k - W) > (T)ft[k * kTileLeaves];
+      return v0 - cc * ((T)2 * (T)k - W) > (T)ft[k * R];
     };
     int pos = 0;
 #pragma unroll
@@ -282,7 +313,7 @@ __global__ void __launch_bounds__(kT, pd_minb(BW != kWeights, NV)) k_pd_pass(PdA
       pos = below(pos + step - 1) ? pos + step : pos;
     pos += below(pos) ? 1 : 0;
     const T ck = v0 - cc * ((T)2 * (T)pos - W);
-    res0 = pos > 0 ? fmax((T)ft[(pos - 1) * kTileLeaves], ck) : ck;
+    res0 = pos > 0 ? fmax((T)ft[(pos - 1) * R], ck) : ck;
   } else {
     // general weights: the prefix sums are needed, so one branch-free scan
     // (min(f_k, c_k) is f_k below k* and c_k from k*: the max is the value)
@@ -291,7 +322,7 @@ __global__ void __launch_bounds__(kT, pd_minb(BW != kWeights, NV)) k_pd_pass(PdA
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
       const T cand = v0 - cc * ((T)2 * S - W);
-      res0 = fmax(res0, fmin(cand, (T)ft[k * kTileLeaves]));
+      res0 = fmax(res0, fmin(cand, (T)ft[k * R]));
       S += (T)wt(k);
     }
     res0 = fmax(res0, v0 - cc * ((T)2 * S - W));
@@ -365,6 +396,7 @@ __global__ void __launch_bounds__(kT, pd_minb(BW != kWeights, NV)) k_pd_pass(PdA
   // stage with the tile kStages steps ahead
   __syncthreads();
   const int nt = tile_id + kStages * (int)gridDim.x;
-  if (threadIdx.x == 0 && nt < ntiles) stage_pd(s_tile, &s_bar[stage], nt);
+  if (threadIdx.x == 0 && nt < ntiles && !packed)
+    stage_pd(s_tile, &s_bar[stage], nt, -2);
   }  // tiles
 }

@@ -63,26 +63,33 @@ struct KeySort {
   }
 };
 
-// sorts the sample vectors of the store slots list[0 .. *nlist) (list null:
-// slots 0 .. n); NV = the store stride (views padded), nv = real views.
-// M non-null: binary weights (bit v of M[s]); else weights in W.
+// sorts the sample vectors of the leaves list[0 .. *nlist) (slot ids i*8+c
+// of the leaf-block list; list null: every leaf of the n slots); NV = the
+// store stride (views padded), nv = real views.  M non-null: binary weights
+// (bit v of M); else weights in W.  Positions from the store layout sd.
 template <int NV>
 __global__ void k_sort_samples(const int32_t* __restrict__ list,
                                const int32_t* __restrict__ nlist, int64_t n,
                                int nv, float* F, float* W,
-                               const uint32_t* __restrict__ M) {
+                               const uint32_t* __restrict__ M,
+                               const int4* __restrict__ lmeta, SDesc sd) {
   const int64_t cnt = list ? (int64_t)*nlist : n;
   const int64_t step = (int64_t)gridDim.x * blockDim.x;
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnt;
        k += step) {
     const int64_t s = list ? (int64_t)list[k] : k;
-    const uint32_t mk = M ? M[s] : 0u;
+    const int4 mt = lmeta[s >> 3];
+    const unsigned mask = ((unsigned)mt.w >> 19) & 0xffu;
+    const int c = (int)(s & 7);
+    if (!list && (!((mask >> c) & 1u) || (mt.x == 0 && c != 0))) continue;
+    const SIdx q = sidx(sd, s >> 3, c, mt.y, mask);
+    const uint32_t mk = M ? M[q.m] : 0u;
     uint64_t key[NV];
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
-      const float f = F[samp_idx(s, v, NV)];
+      const float f = F[q.f + (int64_t)v * q.pitch];
       const bool on = v < nv && (M ? ((mk >> v) & 1u) != 0u
-                                   : W[samp_idx(s, v, NV)] != 0.f);
+                                   : W[q.f + (int64_t)v * q.pitch] != 0.f);
       const float fz = on ? __fadd_rn(f, 0.f) : __int_as_float(0x7f800000);
       key[v] = ((uint64_t)f_ord(fz) << 32) | (uint32_t)v;
     }
@@ -92,17 +99,18 @@ __global__ void k_sort_samples(const int32_t* __restrict__ list,
       // indexed at run time, so it lives in local memory -- a one-time pass)
       float w[NV];
 #pragma unroll
-      for (int v = 0; v < NV; ++v) w[v] = W[samp_idx(s, v, NV)];
+      for (int v = 0; v < NV; ++v) w[v] = W[q.f + (int64_t)v * q.pitch];
       const uint32_t inf_key = f_ord(__int_as_float(0x7f800000));
 #pragma unroll
       for (int r = 0; r < NV; ++r) {
         const int v = (int)(key[r] & 0xffu);
-        W[samp_idx(s, r, NV)] = (uint32_t)(key[r] >> 32) == inf_key ? 0.f : w[v];
+        W[q.f + (int64_t)r * q.pitch] =
+            (uint32_t)(key[r] >> 32) == inf_key ? 0.f : w[v];
       }
     }
 #pragma unroll
     for (int r = 0; r < NV; ++r)
-      F[samp_idx(s, r, NV)] = f_unord((uint32_t)(key[r] >> 32));
+      F[q.f + (int64_t)r * q.pitch] = f_unord((uint32_t)(key[r] >> 32));
   }
 }
 

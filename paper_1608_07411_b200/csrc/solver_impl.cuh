@@ -685,7 +685,7 @@ __global__ void __launch_bounds__(kT)
              const uint32_t* __restrict__ M, int64_t stride, int nv,
              LeafParams<T> p, double* partials, double* terms,
              const int32_t* __restrict__ tileK,
-             const int64_t* __restrict__ tileOff) {
+             const int64_t* __restrict__ tileOff, SDesc sd) {
   using A = Arith<T>;
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t i = gid >> 3;
@@ -720,11 +720,13 @@ __global__ void __launch_bounds__(kT)
     const T gz = z + 1 < m ? (U(0, 0, 1) - u0) * ih : (T)0;
     const T smooth = p.lam * A::smooth_val(gx, gy, gz, p.eps2);
     T num = 0, den = p.gamma;
-    const int64_t sidx = i * 8 + c;
-    const uint32_t mk = BINW ? M[sidx] : 0u;
-    const int nrow = tileK ? tileK[sidx >> 8] : nv;
+    const int64_t slot = i * 8 + c;
+    const int4 mt = lmeta[i];
+    const SIdx si = sidx(sd, i, c, mt.y, ((unsigned)mt.w >> 19) & 0xffu);
+    const uint32_t mk = BINW ? M[si.m] : 0u;
+    const int nrow = tileK ? tileK[slot >> 8] : nv;
     for (int v = 0; v < nrow; ++v) {
-      const int64_t q = tileK ? ell_idx(tileOff, sidx, v) : samp_idx(sidx, v, stride);
+      const int64_t q = tileK ? ell_idx(tileOff, slot, v) : si.f + (int64_t)v * si.pitch;
       const float w = BINW ? (float)((mk >> v) & 1u) : W[q];
       if (w != 0.f) {
         const T d = u0 - (T)F[q];
@@ -878,6 +880,7 @@ void launch_leaf_pass(Ctx& c, const T* snap, T* uval, const int32_t* child,
   a.epart = epart;
   a.tileK = c.ell ? c.tileK.p : nullptr;
   a.tileOff = c.ell ? c.tileOff.p : nullptr;
+  a.sd = c.sd;
   const bool en = epart != nullptr;
   if (timed && c.timing) OCTF_CUDA(cudaEventRecord(c.tev[0], st));
 #define OCTF_LEAF(FZ, BW, EN)                                         \
@@ -1303,14 +1306,16 @@ double energy_impl(Ctx& c, const T* u, const int32_t* child,
                                         c.lmeta.p, u, c.F.p, c.W.p, c.M.p,
                                         c.sstride, c.nviews, lp, c.partials.p,
                                         terms, c.ell ? c.tileK.p : nullptr,
-                                        c.ell ? c.tileOff.p : nullptr);
+                                        c.ell ? c.tileOff.p : nullptr,
+                                        c.sd);
   else
     k_energy<T, false><<<g, kT, 0, st>>>(c.lblocks.p, c.nlb, c.lkey.p,
                                          c.nbr.p, c.lmeta.p, u, c.F.p, c.W.p,
                                          c.M.p, c.sstride, c.nviews, lp,
                                          c.partials.p, terms,
                                          c.ell ? c.tileK.p : nullptr,
-                                         c.ell ? c.tileOff.p : nullptr);
+                                         c.ell ? c.tileOff.p : nullptr,
+                                         c.sd);
   OCTF_CUDA(cudaGetLastError());
   ++c.launches;
   if (c.timing) OCTF_CUDA(cudaEventRecord(c.tev[3], st));
@@ -1466,6 +1471,7 @@ void pd_passes_impl(Ctx& c, PdHostArgs& a, cudaStream_t st) {
       p.clamp = a.clamp;
       p.epart = c.partials.p + (size_t)j * g;
       p.lpar = c.lpar.p;
+      p.sd = c.sd;
       if (c.timing && (int)c.pev.size() >= 2 * kChunk)
         OCTF_CUDA(cudaEventRecord(c.pev[2 * j], st));
 #define OCTF_PD(BW, N) launch_pd<T, BW, N>(g, st, p, fused_bottom)
@@ -1530,7 +1536,7 @@ __global__ void k_pd_split_flags(const int4* __restrict__ lmeta, int64_t nlb,
   if (!((mask >> c) & 1u) || (m.x == 0 && c != 0)) return;
   const int32_t s = m.x + c;
   if (L >= d_max || !(fabs((double)u[s]) < tau_s)) return;
-  const int x = m.x == 0 ? 0 : 2 * m.y + ((c >> 2) & 1);
+  const int x = m.x == 0 ? 0 : 2 * meta_px(m.y) + ((c >> 2) & 1);
   const int y = m.x == 0 ? 0 : 2 * m.z + ((c >> 1) & 1);
   const int z = m.x == 0 ? 0 : 2 * pz + (c & 1);
   const int32_t r = atomicAdd(cnt, 1);

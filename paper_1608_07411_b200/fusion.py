@@ -19,6 +19,7 @@ reference's per-pass snapshot copy (_kernels.pyx:390-393) costs nothing.
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass, field as dc_field
 
@@ -351,6 +352,12 @@ def tree_energy(u: OctreeField, views, params: FusionParams, *,
         params.eps, params.gamma, state=u.state, ctx=ctx))
 
 
+def _pack() -> bool:
+    """Packed sample positions on frozen trees (OCTF_NO_PACK=1: slot
+    positions, for A/B runs)."""
+    return os.environ.get("OCTF_NO_PACK", "0") != "1"
+
+
 class Solver:
     """The descent schedule as a stepping object (reference fusion.py:218-236).
 
@@ -383,8 +390,12 @@ class Solver:
         self.u = _solver_field(u0, self.dtype)
         self.vvals, self.vws, self.vchilds = view_arrays(views or [])
         self.ctx = _lib.Ctx()
-        if defer:   # a shard: samples are gathered by ctx_select
-            self.ctx.set_options(_lib.CTX_DEFER)
+        # a shard: samples are gathered by ctx_select; a frozen tree: each
+        # leaf's samples at its rank among its tile's leaves (CTX_PACKED)
+        opts = ((_lib.CTX_DEFER if defer else 0)
+                | (_lib.CTX_PACKED if self.frozen and _pack() else 0))
+        if opts:
+            self.ctx.set_options(opts)
         self.samples = samples
         if samples is not None:
             # per-slot samples (BASELINE config 5): frozen trees only
@@ -528,10 +539,15 @@ class PDSolver:
         used, cap = self.u.used, self.u.capacity
         self.vvals, self.vws, self.vchilds = view_arrays(views or [])
         self.ctx = _lib.Ctx()
+        self.restructure = not (params.tau_split <= 0.0 and params.clamp
+                                and params.tau_join >= 1.0)
         # the pd kernel reads the dense layout, each leaf's samples sorted
-        # once when gathered (its prox selects on them)
+        # once when gathered (its prox selects on them); packed positions on
+        # a frozen tree
         self.ctx.set_options(_lib.CTX_DENSE | _lib.CTX_SORTED
-                             | (_lib.CTX_DEFER if defer else 0))
+                             | (_lib.CTX_DEFER if defer else 0)
+                             | (0 if self.restructure or not _pack()
+                                else _lib.CTX_PACKED))
         self.samples = samples
         if samples is not None:
             self.kern.ctx_prepare(self.ctx, self.u.child, self.u.state,
@@ -544,8 +560,6 @@ class PDSolver:
         self.a = [self.u.value, ub, z(), z(), z()]
         self.b = [self.u.snap, z(), z(), z(), z()]
         self.stats: list[IterationStats] = []
-        self.restructure = not (params.tau_split <= 0.0 and params.clamp
-                                and params.tau_join >= 1.0)
         if self.restructure and samples is not None:
             raise ValueError("per-leaf samples need a frozen structure "
                              "(tau_split <= 0, tau_join >= 1, clamp)")

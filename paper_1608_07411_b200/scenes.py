@@ -345,6 +345,12 @@ def value_noise(p, tables, base_freq: float = 4.0):
     return out / total
 
 
+def _norm3(v):
+    """|v| over the last axis (size 3) as ((x*x + y*y) + z*z).sqrt()."""
+    return ((v[..., 0] * v[..., 0] + v[..., 1] * v[..., 1])
+            + v[..., 2] * v[..., 2]).sqrt()
+
+
 def sphere_trace(sdf, cam: PinholeCamera, *, lipschitz: float, t_max: float,
                  device, steps: int = 400, eps: float = 1e-7):
     """Camera-frame z of the first surface hit of each pixel ray (0 = miss)
@@ -359,10 +365,15 @@ def sphere_trace(sdf, cam: PinholeCamera, *, lipschitz: float, t_max: float,
     dirs = torch.stack(torch.broadcast_tensors(px[None, :], py[:, None],
                                                torch.ones((), dtype=torch.float64,
                                                           device=device)), -1)
-    R = torch.as_tensor(cam.rotation, dtype=torch.float64, device=device)
-    d = (dirs.reshape(-1, 3) @ R.T)
+    R = np.asarray(cam.rotation, dtype=np.float64)
+    dr = dirs.reshape(-1, 3)
+    # world directions R @ dir as separate IEEE ops (no matmul / reduction
+    # kernels, whose order differs between devices): CPU and GPU traces are
+    # bit-identical, so the golden fixtures made here hold on the GPU box
+    d = torch.stack([(dr[:, 0] * float(R[j, 0]) + dr[:, 1] * float(R[j, 1]))
+                     + dr[:, 2] * float(R[j, 2]) for j in range(3)], 1)
     o = torch.as_tensor(cam.translation, dtype=torch.float64, device=device)
-    nrm = d.norm(dim=1)
+    nrm = _norm3(d)
     t = torch.zeros(d.shape[0], dtype=torch.float64, device=device)
     alive = torch.ones_like(t, dtype=torch.bool)
     hit = torch.zeros_like(alive)
@@ -431,7 +442,7 @@ def make_cfg3(d_max: int = 9, n_views: int = 64, width: int = 640,
     c = torch.tensor([0.5, 0.5, 0.5], dtype=torch.float64, device=device)
 
     def sdf(p):
-        return (p - c).norm(dim=-1) - (0.35 + 0.03 * value_noise(p, tables))
+        return _norm3(p - c) - (0.35 + 0.03 * value_noise(p, tables))
 
     # |grad n| <= sum_o a_o * 1.5 * 2 * f_o / sum_o a_o (smoothstep slope 1.5,
     # lattice range 2) = 20.6; L = 1 + 0.03 * 20.6 < 1.7
@@ -487,10 +498,10 @@ def room_sdf_fn(objs, device, size: float = 4.0):
         for lo in range(0, p.shape[0], 1 << 16):
             q = p[lo:lo + (1 << 16)]
             dq = (q[:, None, :] - bc[None]).abs() - bh[None]
-            outside = dq.clamp(min=0.0).norm(dim=-1)
+            outside = _norm3(dq.clamp(min=0.0))
             inside = dq.max(dim=-1).values.clamp(max=0.0)
             db = (outside + inside).min(dim=1).values
-            ds = ((q[:, None, :] - sc[None]).norm(dim=-1) - sr[None]).min(dim=1).values
+            ds = (_norm3(q[:, None, :] - sc[None]) - sr[None]).min(dim=1).values
             walls = torch.minimum(q, size - q).min(dim=1).values
             r = torch.minimum(torch.minimum(db, ds), walls)
             out = r if out is None else torch.cat([out, r])

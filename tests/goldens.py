@@ -49,3 +49,26 @@ def small_views(z):
                             weight=z[f"view{i}_weight"]))
         i += 1
     return out
+
+
+def live_nodes(child) -> np.ndarray:
+    """Slots of every node reachable from the root, ascending (free-listed
+    blocks excluded)."""
+    child = np.asarray(child)
+    out = [np.zeros(1, dtype=np.int64)]
+    front = out[0]
+    while front.size:
+        c = child[front]
+        c = c[c >= 0].astype(np.int64)
+        front = (c[:, None] + np.arange(8)).ravel()
+        if front.size:
+            out.append(front)
+    return np.sort(np.concatenate(out))
+
+
+def live_digest(child, value) -> dict:
+    """sha256 of the child array and of the values of all live nodes."""
+    live = live_nodes(child)
+    return {"child": sha(np.asarray(child)),
+            "live_value": sha(np.asarray(value)[live]),
+            "live": int(live.size)}

@@ -1,0 +1,237 @@
+"""Parity at each BASELINE configuration's whole schedule.
+
+* cfg2 (fixed structure, lambda = 1, K = 200): at depth 5 against the
+  reference's final pool (full_cfg2d5.npz) and at the full depth 8 against
+  the reference's per-pass digests (full_cfg2d8.json: every pass's energy,
+  the live-node values every 10th pass); the fp32 throughput mode within the
+  north_star's 1e-4 of the bit-exact fp64 mode after all 200 passes.
+* cfg3 (adaptive object, full size: depth 9, 64 views of 640x480, split /
+  join every pass, K = 300) and cfg4 (the room at depth 8 with 64 frames,
+  K = 500): depth maps regenerated on the GPU and checked against the
+  digest of the ones the reference consumed, view trees and u0 digests, and
+  for EVERY pass the reference's split / join counts, state, child array and
+  live-node values (fp64, bit-exact), energies to rtol 1e-10 (the reference
+  sums ~10^6 terms sequentially; ours is a tree reduction).  fp32: split /
+  join decisions identical and u within 1e-4 after the whole schedule.
+* cfg5 (solver microbenchmark) at the pool-level 1M-leaf scale, K = 100:
+  fp64 descent and primal-dual bit-exact against the C oracle run live,
+  fp32 within 1e-4 of them.
+
+The full_*.json fixtures come from tests/golden/make_golden_full.py, which
+runs the reference's own Python API and compiled kernels in the build
+container.
+"""
+import json
+import os
+from concurrent.futures import ProcessPoolExecutor
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as orc
+from tests.conftest import GOLDEN, has_gpu
+from tests.goldens import live_digest, live_nodes, sha
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")]
+
+FP32_TOL = 1e-4
+
+
+def golden(name):
+    path = os.path.join(GOLDEN, f"full_{name}.json")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated")
+    with open(path) as fp:
+        return json.load(fp)
+
+
+def tree_digest(f):
+    h = f.to_host(scratch=False)
+    d = {"value": sha(h.value[:h.used]), "child": sha(h.child[:h.used]),
+         "state": [int(s) for s in h.state]}
+    if h.weight is not None:
+        d["weight"] = sha(h.weight[:h.used])
+    return d
+
+
+def solver_digest(s):
+    used = int(s.u.state[0])
+    return live_digest(s.u.child[:used].cpu().numpy(),
+                       s.cur[:used].cpu().numpy())
+
+
+def live_u(s):
+    used = int(s.u.state[0])
+    child = s.u.child[:used].cpu().numpy()
+    live = live_nodes(child)
+    return child, live, s.cur[:used].double().cpu().numpy()[live]
+
+
+# ------------------------------------------------------------------ cfg2 --
+def cfg2_inputs(depth):
+    import bench
+    return bench.build_cfg2(depth, 16)
+
+
+def test_cfg2_depth5_whole_schedule():
+    from paper_1608_07411_b200 import fusion
+    g = golden("cfg2d5")
+    want = np.load(os.path.join(GOLDEN, "full_cfg2d5.npz"))["final_value"]
+    views, u0, p = cfg2_inputs(5)
+    assert [tree_digest(v) for v in views] == g["views"]
+    assert tree_digest(u0) == g["u0"]
+    s = fusion.Solver(u0, views, p)
+    for t, ref in enumerate(g["passes"]):
+        s.step(t)
+        assert solver_digest(s) == {k: ref[k] for k in
+                                    ("child", "live_value", "live")}, t
+    s.finish()
+    np.testing.assert_allclose([st.energy for st in s.stats],
+                               [r["energy"] for r in g["passes"]], rtol=1e-12)
+    got = s.cur[:u0.used].cpu().numpy()
+    assert np.array_equal(got, want)
+    r32 = fusion.fuse(u0, views, p, precision="fp32").field.to_host().value
+    err = float(np.max(np.abs(r32 - want)))
+    assert err <= FP32_TOL, err
+
+
+def test_cfg2_full_depth_whole_schedule():
+    from paper_1608_07411_b200 import fusion
+    g = golden("cfg2d8")
+    views, u0, p = cfg2_inputs(8)
+    assert [tree_digest(v) for v in views] == g["views"]
+    assert tree_digest(u0) == g["u0"]
+    s = fusion.Solver(u0, views, p)
+    t = 0
+    while t < p.iterations:
+        k = 10 if t + 10 <= p.iterations else p.iterations - t
+        s.run(t, 1)            # the digested pass alone, then the rest batched
+        ref = g["passes"][t]
+        if "live_value" in ref:
+            assert solver_digest(s) == {q: ref[q] for q in
+                                        ("child", "live_value", "live")}, t
+        s.run(t + 1, k - 1)
+        t += k
+    ref = g["passes"][-1]
+    assert solver_digest(s) == {q: ref[q] for q in
+                                ("child", "live_value", "live")}
+    s.finish()
+    np.testing.assert_allclose([st.energy for st in s.stats],
+                               [r["energy"] for r in g["passes"]], rtol=1e-9)
+    u64 = s.cur[:u0.used].clone()
+    s.close()
+    s32 = fusion.Solver(u0, views, p, precision="fp32")
+    s32.run(0, p.iterations)
+    err = float((s32.cur[:u0.used].double() - u64).abs().max())
+    assert err <= FP32_TOL, err
+
+
+# ------------------------------------------------------------ cfg3, cfg4 --
+def depth_case(name, make):
+    from paper_1608_07411_b200 import fusion, volume
+    g = golden(name)
+    sc = make()
+    dd = sha(np.stack(sc.depths).astype(np.float32))
+    assert dd == g["depth_sha"], "depth maps differ from the reference's"
+    p = fusion.FusionParams(**sc.params)
+    dom = volume.VolumeDomain(sc.origin, sc.voxel_size, sc.resolution)
+    views, u0, _ = fusion.prepare(sc.depths, sc.cameras, dom, p)
+    assert [tree_digest(v) for v in views] == g["views"]
+    assert tree_digest(u0) == g["u0"]
+    s64 = fusion.Solver(u0, views, p)
+    s32 = fusion.Solver(u0, views, p, precision="fp32")
+    worst = 0.0
+    for t, ref in enumerate(g["passes"]):
+        a = s64.step(t)
+        b = s32.step(t)
+        assert (a.splits, a.joins) == (ref["splits"], ref["joins"]), t
+        assert [int(q) for q in s64.u.state] == ref["state"], t
+        assert a.node_count == ref["node_count"], t
+        assert solver_digest(s64) == {q: ref[q] for q in
+                                      ("child", "live_value", "live")}, t
+        # fp32: the same split / join decisions, u within the tolerance
+        assert (b.splits, b.joins) == (a.splits, a.joins), t
+        assert [int(q) for q in s32.u.state] == ref["state"], t
+    s64.finish()
+    np.testing.assert_allclose([st.energy for st in s64.stats],
+                               [r["energy"] for r in g["passes"]], rtol=1e-10)
+    c64, live, u64 = live_u(s64)
+    c32, live32, u32 = live_u(s32)
+    assert np.array_equal(c64, c32)
+    worst = float(np.max(np.abs(u32 - u64)))
+    assert worst <= FP32_TOL, worst
+    return len(g["passes"]), worst
+
+
+def test_cfg3_full_size_whole_schedule():
+    from paper_1608_07411_b200 import scenes
+    k, err = depth_case("cfg3", lambda: scenes.make_cfg3(device="cuda"))
+    assert k == 300
+
+
+def test_cfg4_depth8_whole_schedule():
+    from paper_1608_07411_b200 import scenes
+    k, err = depth_case("cfg4d8", lambda: scenes.make_cfg4(
+        d_max=8, n_frames=64, device="cuda"))
+    assert k == 500
+
+
+# ------------------------------------------------------------------ cfg5 --
+def _oracle_descent(u0h, F, k):
+    views = _views(u0h, F)
+    r = orc.fuse(u0h, views, orc.Params(iterations=k, tau_split=0.0,
+                                        tau_join=1.5, lam=0.3), cap=u0h.used)
+    return r.field.value[:u0h.used], [s.energy for s in r.stats]
+
+
+def _oracle_pd(u0h, F, k):
+    out = orc.pd_fuse(u0h, _views(u0h, F), 0.3, 1e-4, k)
+    return out[:5], out[5]
+
+
+def _views(u0h, F):
+    ones = np.ones(u0h.used, dtype=np.float32)
+    return [orc.Pool(F[v].copy(), u0h.child, u0h.state.copy(), u0h.d_max,
+                     weight=ones) for v in range(F.shape[0])]
+
+
+def test_cfg5_million_leaves_whole_schedule():
+    """1M-leaf cfg5 tree (depths 12/11/10), N = 32, K = 100: descent and
+    primal-dual, fp64 bit-exact against the C oracle (both oracle schedules
+    run in parallel worker processes while the GPU runs)."""
+    from paper_1608_07411_b200 import fusion, scenes
+    k = 100
+    u0, samples, info = scenes.cfg5_inputs(1_000_000, nviews=32, d_max=12,
+                                           device="cuda")
+    h = u0.to_host()
+    u0h = orc.Pool(h.value.copy(), h.child.copy(), h.state.copy(), h.d_max)
+    F = samples[0].cpu().numpy()
+    with ProcessPoolExecutor(2) as ex:
+        fd = ex.submit(_oracle_descent, u0h, F, k)
+        fp = ex.submit(_oracle_pd, u0h, F, k)
+        p = fusion.FusionParams(iterations=k, tau=-1.0, tau_split=0.0,
+                                tau_join=1.5, lam=0.3)
+        res = fusion.fuse(u0, None, p, samples=samples)
+        d64 = res.field.to_host().value
+        d32 = fusion.fuse(u0, None, p, samples=samples,
+                          precision="fp32").field.to_host().value
+        pds = {}
+        for prec in ("fp64", "fp32"):
+            s = fusion.PDSolver(u0, None, p, precision=prec, samples=samples)
+            s.run(0, k)
+            s.finish()
+            pds[prec] = ([t[:u0h.used].double().cpu().numpy()
+                          for t in s.state], [st.energy for st in s.stats])
+            s.close()
+        want_d, en_d = fd.result()
+        want_p, en_p = fp.result()
+    assert np.array_equal(d64, want_d)
+    np.testing.assert_allclose([st.energy for st in res.stats], en_d,
+                               rtol=1e-11)
+    assert float(np.max(np.abs(d32 - want_d))) <= FP32_TOL
+    for g, w in zip(pds["fp64"][0], want_p):
+        assert np.array_equal(g, w)
+    np.testing.assert_allclose(pds["fp64"][1][:-1], en_p[1:], rtol=1e-11)
+    assert float(np.max(np.abs(pds["fp32"][0][0] - want_p[0]))) <= FP32_TOL

@@ -1,9 +1,15 @@
 #!/bin/sh
 # A/B the cfg5 solver microbenchmark across library builds, interleaved:
-#   tools/ab_cfg5.sh <lib.so|default> ... (run on the GPU box)
+#   tools/ab_cfg5.sh <lib.so|default|nopack> ... (run on the GPU box)
+# "nopack" = the default library with OCTF_NO_PACK=1 (slot sample positions)
 for rep in 1 2; do
   for lib in "$@"; do
-    if [ "$lib" = default ]; then unset OCTF_LIB_PATH; else export OCTF_LIB_PATH=$PWD/$lib; fi
+    unset OCTF_NO_PACK
+    case "$lib" in
+      default) unset OCTF_LIB_PATH ;;
+      nopack) unset OCTF_LIB_PATH; export OCTF_NO_PACK=1 ;;
+      *) export OCTF_LIB_PATH=$PWD/$lib ;;
+    esac
     printf '%s ' "$lib"
     timeout 900 python tools/cfg5_bench.py ${CFG5_ARGS} 2>/dev/null | python -c "
 import json, sys

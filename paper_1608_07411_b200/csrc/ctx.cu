@@ -51,6 +51,8 @@ Ctx::Ctx() {
   phase_marks = pm && pm[0] == '1';
   const char* fp = std::getenv("OCTF_NO_FUSED_PARENT");  // A/B switch
   fuse_off = fp && fp[0] == '1';
+  const char* nm = std::getenv("OCTF_NO_MORTON");  // A/B switch
+  no_morton = nm && nm[0] == '1';
   OCTF_CUDA(cudaMallocHost((void**)&h_counters, 64 * sizeof(int32_t)));
   OCTF_CUDA(cudaMallocHost((void**)&h_scalar, 8 * sizeof(double)));
 }
@@ -927,6 +929,24 @@ __global__ void k_pack_ranks(int4* lmeta, int64_t nlb, int64_t ntiles,
   if (__any_sync(0xffffffffu, odd) && lane == 0) atomicAdd(nonfull, 1);
 }
 
+// Morton (depth-first pre-order) key of a leaf block: its parent cell's
+__global__ void k_block_keys(const int32_t* __restrict__ lblocks, int64_t n,
+                             const int8_t* __restrict__ blevel,
+                             const uint64_t* __restrict__ bcoord, int d_max,
+                             uint64_t* keys) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t b = lblocks[i];
+  if (b == 0) {  // the root's pseudo-block
+    keys[i] = 0;
+    return;
+  }
+  const int k = block_id(b);
+  int pL, px, py, pz;
+  unpack_cell(bcoord[k], pL, px, py, pz);
+  keys[i] = preorder_key(blevel[k] - 1, px, py, pz, d_max, false);
+}
+
 __global__ void k_walk_free(const int32_t* __restrict__ child, int64_t head,
                             int64_t nmax, int32_t* chain, int32_t* count) {
   // single thread: follow the free list links (child[b] of a free block)
@@ -1092,7 +1112,7 @@ void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
   const bool patched =
       incremental && ctx_list_update(c, child, total, nbid, st);
   if (!patched) {
-    ctx_list_full(c, child, total, nbid, st);
+    ctx_list_full(c, child, total, nbid, d_max, st);
     ph_mark(c, kPhFull, st);
   }
 
@@ -1127,7 +1147,7 @@ void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
 // the sorted leaf-block list of every live block holding a leaf, its tables
 // and the block -> position map
 void ctx_list_full(Ctx& c, const int32_t* child, int64_t total, int64_t nbid,
-                   cudaStream_t st) {
+                   int d_max, cudaStream_t st) {
   // leaf blocks, ascending base slot
   uint8_t* flags = c.flags.ensure(total);
   c.lblocks.ensure(total);
@@ -1147,7 +1167,29 @@ void ctx_list_full(Ctx& c, const int32_t* child, int64_t total, int64_t nbid,
   OCTF_CUDA(cudaStreamSynchronize(st));
   c.nlb = c.h_counters[0];
   c.nleaves = c.h_counters[1];
-  sort_i32(c, c.lblocks.p, c.nlb, st);
+  if (c.pack_opt && !c.defer_gather && !c.no_morton && c.nlb > 1) {
+    // a frozen tree's list in Morton order of the blocks' parent cells
+    // (depth-first pre-order): spatial neighbours of every level are
+    // processed together, so their values are re-read from L2, not HBM
+    uint64_t* keys = c.sort_k64.ensure(2 * c.nlb);
+    int32_t* v2 = c.sort_k32.ensure(c.nlb);
+    k_block_keys<<<grid_for(c.nlb), kThreads, 0, st>>>(
+        c.lblocks.p, c.nlb, c.blevel.p, c.bcoord.p, d_max, keys);
+    OCTF_CUDA(cudaGetLastError());
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys, keys + c.nlb,
+                                    c.lblocks.p, v2, (int)c.nlb, 0, 64, st);
+    c.cub_tmp.ensure(bytes);
+    OCTF_CUDA(cub::DeviceRadixSort::SortPairs(c.cub_tmp.p, bytes, keys,
+                                              keys + c.nlb, c.lblocks.p, v2,
+                                              (int)c.nlb, 0, 64, st));
+    OCTF_CUDA(cudaMemcpyAsync(c.lblocks.p, v2, c.nlb * sizeof(int32_t),
+                              cudaMemcpyDeviceToDevice, st));
+    c.list_morton = true;
+  } else {
+    sort_i32(c, c.lblocks.p, c.nlb, st);
+    c.list_morton = false;
+  }
   c.lkey.ensure(c.nlb);
   c.lmeta.ensure(c.nlb);
   c.lpar.ensure(c.nlb);

@@ -159,7 +159,9 @@ struct Ctx {
   std::vector<int64_t> lvl_off, lvl_cnt;  // per level ranges in lvl_blocks
   DevBuf<int32_t> lvl_blocks;             // live block bases, level-major
   int64_t nblocks = 0;
-  bool fuse_off = false;  // env OCTF_NO_FUSED_PARENT=1: pd bottom level apart
+  bool fuse_off = false;
+  bool no_morton = false;     // env OCTF_NO_MORTON=1: frozen lists by base
+  bool list_morton = false;   // the leaf-block list is in Morton order  // env OCTF_NO_FUSED_PARENT=1: pd bottom level apart
   DevBuf<int32_t> lblocks;    // blocks holding >= 1 leaf, ascending base
   DevBuf<uint64_t> lkey;      // per leaf block: packed (level, parent cell)
   DevBuf<int4> lmeta;         // per leaf block: {base, px, py, pz|mask|L}
@@ -288,7 +290,7 @@ void ctx_set_views(Ctx& c, int nviews, const float* const* vval,
 void ctx_gather(Ctx& c, cudaStream_t st);
 void ctx_gather_ell(Ctx& c, cudaStream_t st);
 void ctx_list_full(Ctx& c, const int32_t* child, int64_t total, int64_t nbid,
-                   cudaStream_t st);
+                   int d_max, cudaStream_t st);
 bool ctx_list_update(Ctx& c, const int32_t* child, int64_t total, int64_t nbid,
                      cudaStream_t st);  // false: rebuild with ctx_list_full
 void ctx_set_samples(Ctx& c, const float* F, const float* W, int nviews,

@@ -1,13 +1,15 @@
 #!/bin/sh
 # A/B the cfg5 solver microbenchmark across library builds, interleaved:
 #   tools/ab_cfg5.sh <lib.so|default|nopack> ... (run on the GPU box)
-# "nopack" = the default library with OCTF_NO_PACK=1 (slot sample positions)
+# "nopack" = the default library with OCTF_NO_PACK=1 (slot sample positions),
+# "nomorton" = with OCTF_NO_MORTON=1 (frozen leaf-block list by base slot)
 for rep in 1 2; do
   for lib in "$@"; do
-    unset OCTF_NO_PACK
+    unset OCTF_NO_PACK OCTF_NO_MORTON
     case "$lib" in
       default) unset OCTF_LIB_PATH ;;
       nopack) unset OCTF_LIB_PATH; export OCTF_NO_PACK=1 ;;
+      nomorton) unset OCTF_LIB_PATH; export OCTF_NO_MORTON=1 ;;
       *) export OCTF_LIB_PATH=$PWD/$lib ;;
     esac
     printf '%s ' "$lib"

@@ -275,6 +275,17 @@ int octf_tree_energy(octf_ctx *ctx, int dtype, const void *uval,
                      int d_max, double lam, double eps, double gamma,
                      double *out, double *terms, void *stream);
 
+/* The reference's canonical node order on the device (octree.py:168-181
+ * leaves(), :413-431 serialize(): depth-first pre-order, children in index
+ * order): every live node -- or every leaf, leaves_only != 0 -- as its slot
+ * (slots, device, int32) and preorder key (keys, device, optional:
+ * Morton key of its first finest-level cell << 5 | level), sorted by a
+ * radix sort of the keys.  slots / keys must hold state[2] entries;
+ * *count (host) receives the number written.  ctx may be NULL. */
+int octf_node_order(octf_ctx *ctx, const int32_t *child, const int64_t *state,
+                    int64_t cap, int d_max, int leaves_only, int32_t *slots,
+                    uint64_t *keys, int64_t *count, void *stream);
+
 /* _kernels.pyx:116-158 densify -- leaves to a dense (2^d)^3 f64 grid */
 int octf_densify(int dtype, const void *value, const int32_t *child,
                  int d_max, double *out, void *stream);

@@ -80,6 +80,39 @@ def propagate(value, child, *, state=None, d_max=_lib.MAX_DEPTH, ctx=None):
          int(d_max), stream_handle())
 
 
+def node_order(child, state, d_max, *, leaves_only=False, ctx=None):
+    """Every live node (or leaf) in the reference's canonical depth-first
+    order (octree.py:168-181, :413-431), computed on the device: (slots
+    int32, preorder keys int64) CUDA tensors -- see decode_keys."""
+    c = ctx if ctx is not None else _fresh_ctx()
+    st = np.ascontiguousarray(np.asarray(state, dtype=np.int64)[:3])
+    n = int(st[2])
+    slots = torch.empty(max(n, 1), dtype=torch.int32, device=child.device)
+    keys = torch.empty(max(n, 1), dtype=torch.int64, device=child.device)
+    cnt = np.zeros(1, dtype=np.int64)
+    call("octf_node_order", c.h, ptr(child), st.ctypes.data, child.shape[0],
+         int(d_max), 1 if leaves_only else 0, ptr(slots), ptr(keys),
+         cnt.ctypes.data, stream_handle())
+    k = int(cnt[0])
+    return slots[:k], keys[:k]
+
+
+def decode_keys(keys, d_max):
+    """(level, x, y, z) int64 tensors of preorder keys (Morton key of the
+    node's first finest-level cell << 5 | level)."""
+    level = keys & 31
+    first = keys >> 5
+    x = torch.zeros_like(first)
+    y = torch.zeros_like(first)
+    z = torch.zeros_like(first)
+    for bit in range(d_max):
+        x |= ((first >> (3 * bit + 2)) & 1) << bit
+        y |= ((first >> (3 * bit + 1)) & 1) << bit
+        z |= ((first >> (3 * bit)) & 1) << bit
+    sh = d_max - level
+    return level, x >> sh, y >> sh, z >> sh
+
+
 def densify(value, child, d_max, out):
     """_kernels.pyx:116-158 (out: device (2^d)^3 float64)."""
     if d_max > 60:

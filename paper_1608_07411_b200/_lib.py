@@ -48,6 +48,7 @@ _SIGS = {
                                  DBL, DBL, DBL, DBL, DBL, I32, P, I32, P, I32,
                                  P], I32),
     "octf_ctx_prepare": ([P, P, P, I64, I32, I32, P, P, P, P], I32),
+    "octf_node_order": ([P, P, P, I64, I32, I32, P, P, P, P], I32),
     "octf_pd_restructure": ([P, I32, P, P, P, I64, I32, DBL, DBL, P, P], I32),
     "octf_marching_cubes": ([P, P, I32, P, P, P, P, P, DBL, I32, P, P, P, P],
                             I32),

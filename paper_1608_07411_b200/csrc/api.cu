@@ -611,6 +611,25 @@ int octf_propagate(octf_ctx* ctx, int dtype, void* value, const int32_t* child,
   });
 }
 
+int octf_node_order(octf_ctx* ctx, const int32_t* child, const int64_t* state,
+                    int64_t cap, int d_max, int leaves_only, int32_t* slots,
+                    uint64_t* keys, int64_t* count, void* stream) {
+  return guard([&] {
+    if (!child || !state || !count)
+      throw octf::Error(octf::kEArg, "null argument");
+    if (d_max < 0 || d_max > OCTF_MAX_DEPTH)
+      throw octf::Error(octf::kEDepth, "tree depth out of range");
+    need_device();
+    octf_ctx tmp;
+    octf::Ctx& c = ctx ? ctx->c : tmp.c;
+    if (!c.valid || c.child_key != child || c.cap != cap || c.d_max != d_max ||
+        c.hstate[0] != state[0] || c.hstate[1] != state[1])
+      octf::ctx_prepare(c, child, cap, state, d_max, S(stream));
+    *count = octf::ctx_node_order(c, child, d_max, leaves_only != 0, slots,
+                                  keys, S(stream));
+  });
+}
+
 int octf_tree_energy(octf_ctx* ctx, int dtype, const void* uval,
                      const int32_t* uchild, const int64_t* ustate, int64_t cap,
                      int nviews, const float* const* vvals,

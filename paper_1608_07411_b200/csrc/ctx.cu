@@ -947,6 +947,47 @@ __global__ void k_block_keys(const int32_t* __restrict__ lblocks, int64_t n,
   keys[i] = preorder_key(blevel[k] - 1, px, py, pz, d_max, false);
 }
 
+// the reference's canonical order (octree.py:168-181 leaves, :413-431
+// serialize: depth-first pre-order, children in index order) as sort keys:
+// every live node's preorder key (first finest Morton key << 5 | level) and
+// slot, appended in any order (octf_node_order sorts them)
+__global__ void k_node_keys(const int32_t* __restrict__ blocks, int64_t nblk,
+                            const int8_t* __restrict__ blevel,
+                            const uint64_t* __restrict__ bcoord,
+                            const int32_t* __restrict__ child, int d_max,
+                            int leaves_only, uint64_t* keys, int32_t* slots,
+                            int32_t* count) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool on = false;
+  uint64_t key = 0;
+  int32_t s = 0;
+  if (gid < nblk * 8) {
+    const int32_t b = blocks[gid >> 3];
+    const int c = (int)(gid & 7);
+    if (b == 0) {  // the root's pseudo-block: slot 0 only
+      on = c == 0 && (!leaves_only || child[0] < 0);
+    } else {
+      const int k = block_id(b);
+      int pL, px, py, pz;
+      unpack_cell(bcoord[k], pL, px, py, pz);
+      s = b + c;
+      on = !leaves_only || child[s] < 0;
+      key = preorder_key(blevel[k], 2 * px + ((c >> 2) & 1),
+                         2 * py + ((c >> 1) & 1), 2 * pz + (c & 1), d_max,
+                         false);
+    }
+  }
+  const unsigned q = __ballot_sync(0xffffffffu, on);
+  int base = 0;
+  if ((threadIdx.x & 31) == 0 && q) base = atomicAdd(count, __popc(q));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (on) {
+    const int r = base + __popc(q & ((1u << (threadIdx.x & 31)) - 1u));
+    keys[r] = key;
+    slots[r] = s;
+  }
+}
+
 __global__ void k_walk_free(const int32_t* __restrict__ child, int64_t head,
                             int64_t nmax, int32_t* chain, int32_t* count) {
   // single thread: follow the free list links (child[b] of a free block)
@@ -1686,6 +1727,47 @@ void ctx_gather(Ctx& c, cudaStream_t st) {
                          std::chrono::steady_clock::now() - t0).count();
     ++c.n_gather;
   }
+}
+
+// every live node (or leaf) of the prepared pool in the reference's
+// canonical order: slots and preorder keys (radix sort of the keys)
+int64_t ctx_node_order(Ctx& c, const int32_t* child, int d_max,
+                       bool leaves_only, int32_t* out_slots,
+                       uint64_t* out_keys, cudaStream_t st) {
+  if (!c.valid || c.child_key != child)
+    throw Error(kEArg, "context not prepared for this pool");
+  // the level lists hold every live block, the root's pseudo-block 0 first
+  const int64_t nblk = c.nblocks;
+  const int32_t* blocks = c.lvl_blocks.p;
+  const int64_t n8 = nblk * 8;
+  uint64_t* keys = c.sort_k64.ensure(2 * n8);
+  int32_t* slots = c.sort_k32.ensure(2 * n8);
+  OCTF_CUDA(cudaMemsetAsync(c.counters.p, 0, sizeof(int32_t), st));
+  k_node_keys<<<grid_for(n8), kThreads, 0, st>>>(
+      blocks, nblk, c.blevel.p, c.bcoord.p, child, d_max, leaves_only ? 1 : 0,
+      keys, slots, c.counters.p);
+  OCTF_CUDA(cudaGetLastError());
+  OCTF_CUDA(cudaMemcpyAsync(c.h_counters, c.counters.p, sizeof(int32_t),
+                            cudaMemcpyDeviceToHost, st));
+  OCTF_CUDA(cudaStreamSynchronize(st));
+  const int64_t n = c.h_counters[0];
+  if (n > c.hstate[2] + 0 && !leaves_only)
+    throw Error(kEArg, "corrupt pool: more nodes than state[2]");
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys, keys + n8, slots,
+                                  slots + n8, (int)n, 0, 64, st);
+  c.cub_tmp.ensure(bytes);
+  OCTF_CUDA(cub::DeviceRadixSort::SortPairs(c.cub_tmp.p, bytes, keys,
+                                            keys + n8, slots, slots + n8,
+                                            (int)n, 0, 64, st));
+  if (out_slots)
+    OCTF_CUDA(cudaMemcpyAsync(out_slots, slots + n8, n * sizeof(int32_t),
+                              cudaMemcpyDeviceToDevice, st));
+  if (out_keys)
+    OCTF_CUDA(cudaMemcpyAsync(out_keys, keys + n8, n * sizeof(uint64_t),
+                              cudaMemcpyDeviceToDevice, st));
+  OCTF_CUDA(cudaStreamSynchronize(st));
+  return n;
 }
 
 }  // namespace octf

@@ -175,8 +175,21 @@ class OctreeField:
 
     def leaves(self) -> Iterator[tuple[int, int, int, int, int]]:
         """(node, level, x, y, z) of every leaf in Morton order
-        (octree.py:168-181)."""
-        return iter(_leaves(to_numpy(self.child[:self.used])))
+        (octree.py:168-181), ordered on the device (radix sort of the
+        leaves' preorder keys, octf_node_order)."""
+        slots, lvl, x, y, z = self.node_order(leaves_only=True)
+        return iter(zip(*(to_numpy(t).tolist() for t in (slots, lvl, x, y,
+                                                          z))))
+
+    def node_order(self, leaves_only: bool = False):
+        """Slots, levels and cell coordinates (CUDA tensors) of every live
+        node -- or leaf -- in the reference's canonical depth-first order
+        (octree.py:168-181, :413-431), sorted on the device."""
+        from . import _kernels
+        slots, keys = _kernels.node_order(self.child[:self.used], self.state,
+                                          self.d_max, leaves_only=leaves_only)
+        lvl, x, y, z = _kernels.decode_keys(keys, self.d_max)
+        return slots, lvl, x, y, z
 
     def to_host(self, scratch: bool = True) -> HostPool:
         """Download the pool (reference layout, trimmed to ``used``) through
@@ -415,8 +428,21 @@ def quantization_error(field: OctreeField, dense_u) -> tuple[float, float]:
 
 def serialize(field, fp: IO[str]) -> int:
     """Pre-order dump, one ``level cx cy cz is_leaf value weight`` line per
-    node (octree.py:413-431)."""
-    host = field.to_host() if isinstance(field, OctreeField) else field
+    node (octree.py:413-431).  A device field is ordered and gathered on the
+    device (octf_node_order); only the text formatting runs on the host."""
+    if isinstance(field, OctreeField):
+        slots, lvl, x, y, z = field.node_order()
+        sl = slots.long()
+        leaf = field.child[:field.used][sl] < 0
+        val = field.value[:field.used][sl].double()
+        wt = (field.weight[:field.used][sl].double() if field.weight is not None
+              else torch.zeros_like(val))
+        cols = [to_numpy(t).tolist() for t in (lvl, x, y, z, leaf.int(), val,
+                                               wt)]
+        for L, cx, cy, cz, lf, v, w in zip(*cols):
+            fp.write(f"{L} {cx} {cy} {cz} {lf} {v:.17g} {w:.17g}\n")
+        return len(cols[0])
+    host = field
     count = 0
     stack = [(0, 0, 0, 0, 0)]
     while stack:

@@ -527,7 +527,8 @@ def _catmull_rom(pts, n):
 
 def make_cfg4(d_max: int = 11, n_frames: int = 300, width: int = 640,
               height: int = 480, focal: float = 525.0, seed: int = 0,
-              n_objects: int = 200, device="cuda") -> DepthScene:
+              n_objects: int = 200, device="cuda",
+              depths_in=None) -> DepthScene:
     """BASELINE config 3 ("large room"): a 4 m cube (origin 0, d_max 11 =
     1.95 mm voxels at full size) with ``n_objects`` random boxes/spheres;
     ``n_frames`` depth maps along a closed Catmull-Rom path through 8 random
@@ -535,7 +536,8 @@ def make_cfg4(d_max: int = 11, n_frames: int = 300, width: int = 640,
     along the tangent (assumed); the room's walls are part of the scene
     (assumed); intrinsics as cfg3; depth noise
     sigma = 0.0015 z^2; delta = 0.03, eta = 0.15 (assumed), tau_split /
-    tau_join defaults, 500 iterations."""
+    tau_join defaults, 500 iterations.  ``depths_in`` (the maps of an earlier
+    call with the same arguments) skips the sphere tracing."""
     import torch
     size = 4.0
     objs = _room_objects(seed, n_objects, size)
@@ -548,14 +550,19 @@ def make_cfg4(d_max: int = 11, n_frames: int = 300, width: int = 640,
             way.append(q)
     pos, tan = _catmull_rom(np.array(way), n_frames)
     cams, depths = [], []
+    given = depths_in
     noise = np.random.default_rng(seed + 2)
     for k in range(n_frames):
         cam = PinholeCamera(focal, focal, (width - 1) / 2.0, (height - 1) / 2.0,
                             width, height, look_at(pos[k], pos[k] + tan[k]), pos[k])
+        cams.append(cam)
+        if given is not None:
+            continue
         z = sphere_trace(sdf, cam, lipschitz=1.0, t_max=8.0, device=device,
                          eps=1e-6).cpu().numpy()
-        cams.append(cam)
         depths.append(_add_noise(z, 0.0015 * z * z, noise))
+    if given is not None:
+        depths = [np.asarray(d, dtype=np.float32) for d in given]
     n = 1 << d_max
     return DepthScene("cfg4", (0.0, 0.0, 0.0), size / n, n, cams, depths,
                       dict(delta=0.03, eta=0.15, iterations=500))

@@ -502,3 +502,53 @@ class TestPluginFunctions:
             kern.build_tree(g(meanf), g(minf), g(maxf), offs, True, g(wminf),
                             g(wmaxf), g(wmeanf), 0.3, value, weight, child,
                             state, 61)
+
+
+class TestNodeOrder:
+    """The device's canonical order (octf_node_order: radix sort of preorder
+    Morton keys) against the reference's traversal (octree.py:168-181
+    leaves, :413-431 serialize), on pools with free-listed blocks."""
+
+    def _pools(self):
+        from paper_1608_07411_b200 import fusion
+        z = load("small")
+        u0 = dev(orc.Pool(z["u0_value"], z["u0_child"], z["u0_state"], 4))
+        res = fusion.fuse(u0, [dev(v) for v in small_views(z)],
+                          fusion.FusionParams(iterations=6))
+        views_h, u0h, p, _ = cfg1_views_u0()
+        out = [res.field, dev(u0h)] + [dev(v) for v in views_h[:2]]
+        # cfg1 after its schedule: splits, joins and a free list
+        r = fusion.fuse(dev(u0h), [dev(v) for v in views_h],
+                        fusion.FusionParams(delta=p.delta, eta=p.eta,
+                                            lam=p.lam, iterations=20))
+        return out + [r.field]
+
+    def test_leaves_and_nodes_in_reference_order(self):
+        for f in self._pools():
+            h = f.to_host()
+            hp = orc.Pool(h.value, h.child, h.state, h.d_max, weight=h.weight)
+            assert list(f.leaves()) == [tuple(q) for q in orc.leaves(hp)]
+            slots, lvl, x, y, z = f.node_order()
+            got = list(zip(*(t.cpu().numpy().tolist()
+                             for t in (slots, lvl, x, y, z))))
+            want, stack = [], [(0, 0, 0, 0, 0)]
+            while stack:
+                n, lv, cx, cy, cz = stack.pop()
+                want.append((n, lv, cx, cy, cz))
+                b = int(h.child[n])
+                if b >= 0:
+                    for c in range(7, -1, -1):
+                        stack.append((b + c, lv + 1, 2 * cx + ((c >> 2) & 1),
+                                      2 * cy + ((c >> 1) & 1),
+                                      2 * cz + (c & 1)))
+            assert got == want
+
+    def test_serialize_matches_reference_lines(self):
+        from paper_1608_07411_b200 import octree
+        for f in self._pools():
+            h = f.to_host()
+            hp = orc.Pool(h.value, h.child, h.state, h.d_max, weight=h.weight)
+            buf = io.StringIO()
+            n = octree.serialize(f, buf)
+            lines = buf.getvalue().splitlines()
+            assert n == len(lines) and lines == orc.serialize_lines(hp)

@@ -173,6 +173,27 @@ int octf_marching_cubes(const double *values, const uint8_t *mask, int n,
                         const double *origin, double voxel_size, int world,
                         octf_mesh **out, int64_t *nverts, int64_t *nfaces,
                         void *stream);
+/* Mesh readout from the leaf store: the mesh of
+ * octf_marching_cubes(densify(value), seen) (mesh.py:63-125,
+ * octree.py:327-342) -- same vertices, faces and order -- without the dense
+ * (2^d)^3 grid: only 8^3-cube bricks whose corner cells meet leaves of both
+ * signs are evaluated.  seen_value / seen_child (optional, dtype
+ * seen_dtype): an observed-mask tree over the same domain, node value != 0 =
+ * observed (NULL: every cell observed).  Tables, origin, voxel_size, world
+ * and the result as octf_marching_cubes.  slab0 / slab1 (-1: all) restrict
+ * the readout to the cubes with x in [8 slab0, 8 slab1) -- a mesh too large
+ * for one call is read slab by slab (vertices on a slab's end plane then
+ * appear in both).  ctx may be NULL. */
+int octf_marching_cubes_tree(octf_ctx *ctx, int dtype, const void *value,
+                             const int32_t *child, const int64_t *state,
+                             int64_t cap, int d_max, int seen_dtype,
+                             const void *seen_value, const int32_t *seen_child,
+                             const int8_t *tri_table, const int8_t *tri_count,
+                             const int8_t *edge_axis, const int8_t *edge_offset,
+                             const double *origin, double voxel_size,
+                             int world, int64_t slab0, int64_t slab1,
+                             octf_mesh **out, int64_t *nverts,
+                             int64_t *nfaces, void *stream);
 int octf_mesh_copy(octf_mesh *m, double *verts, int32_t *faces, void *stream);
 int octf_mesh_free(octf_mesh *m);
 

@@ -53,6 +53,9 @@ _SIGS = {
     "octf_marching_cubes": ([P, P, I32, P, P, P, P, P, DBL, I32, P, P, P, P],
                             I32),
     "octf_mesh_copy": ([P, P, P, P], I32),
+    "octf_marching_cubes_tree": ([P, I32, P, P, P, I64, I32, I32, P, P, P, P,
+                                  P, P, P, DBL, I32, I64, I64, P, P, P, P],
+                                 I32),
     "octf_mesh_free": ([P], I32),
     "octf_pass_tiles": ([P, I32, P, P, P, P, I64, I32, P, P, P, I32, DBL, DBL,
                          DBL, DBL, I32, I32, I32, P], I32),

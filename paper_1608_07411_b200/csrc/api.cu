@@ -391,6 +391,48 @@ int octf_marching_cubes(const double* values, const uint8_t* mask, int n,
   });
 }
 
+int octf_marching_cubes_tree(octf_ctx* ctx, int dtype, const void* value,
+                             const int32_t* child, const int64_t* state,
+                             int64_t cap, int d_max, int seen_dtype,
+                             const void* seen_value, const int32_t* seen_child,
+                             const int8_t* tri_table, const int8_t* tri_count,
+                             const int8_t* edge_axis, const int8_t* edge_offset,
+                             const double* origin, double voxel_size,
+                             int world, int64_t slab0, int64_t slab1,
+                             octf_mesh** out, int64_t* nverts,
+                             int64_t* nfaces, void* stream) {
+  return guard([&] {
+    check_dtype(dtype);
+    check_dtype(seen_dtype);
+    if (!value || !child || !state || !tri_table || !tri_count || !edge_axis ||
+        !edge_offset || !origin || !out || !nverts || !nfaces)
+      throw octf::Error(octf::kEArg, "null argument");
+    if ((seen_value == nullptr) != (seen_child == nullptr))
+      throw octf::Error(octf::kEArg, "seen tree: values and children");
+    if (d_max < 0 || d_max > OCTF_MAX_DEPTH)
+      throw octf::Error(octf::kEDepth, "tree depth out of range");
+    need_device();
+    octf_ctx tmp;
+    octf::Ctx& c = ctx ? ctx->c : tmp.c;
+    if (!c.valid || c.child_key != child || c.cap != cap || c.d_max != d_max ||
+        c.hstate[0] != state[0] || c.hstate[1] != state[1])
+      octf::ctx_prepare(c, child, cap, state, d_max, S(stream));
+    octf_mesh* m = new octf_mesh();
+    try {
+      octf::marching_cubes_tree(c, dtype, value, child, d_max, seen_dtype,
+                                seen_value, seen_child, tri_table, tri_count,
+                                edge_axis, edge_offset, origin, voxel_size,
+                                world, slab0, slab1, m, S(stream));
+    } catch (...) {
+      delete m;
+      throw;
+    }
+    *out = m;
+    *nverts = m->nv;
+    *nfaces = m->nf;
+  });
+}
+
 int octf_mesh_copy(octf_mesh* m, double* verts, int32_t* faces, void* stream) {
   return guard([&] {
     if (!m) throw octf::Error(octf::kEArg, "null mesh");

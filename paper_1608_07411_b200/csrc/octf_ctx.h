@@ -402,6 +402,14 @@ void propagate_levels_f64(Ctx& c, double* v, const int32_t* child, int lo,
 void propagate_levels_f32(Ctx& c, float* v, const int32_t* child, int lo,
                           int hi, cudaStream_t st);
 // marching cubes over a dense cell-centred grid (mesh.cu)
+void marching_cubes_tree(Ctx& c, int dtype, const void* value,
+                         const int32_t* child, int d_max, int seen_dtype,
+                         const void* seen_v, const int32_t* seen_c,
+                         const int8_t* tri_table, const int8_t* tri_count,
+                         const int8_t* edge_axis, const int8_t* edge_off,
+                         const double* origin, double voxel, int world,
+                         int64_t bx0, int64_t bx1, octf_mesh* out,
+                         cudaStream_t st);
 void marching_cubes(const double* values, const uint8_t* mask, int n,
                     const int8_t* tri_table, const int8_t* tri_count,
                     const int8_t* edge_axis, const int8_t* edge_off,

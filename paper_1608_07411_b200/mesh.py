@@ -26,7 +26,8 @@ import torch
 from . import _lib
 from ._device import as_device, device, ptr, stream_handle
 
-__all__ = ["TriMesh", "extract_zero_surface", "marching_cubes", "case_tables"]
+__all__ = ["TriMesh", "extract_zero_surface", "marching_cubes", "case_tables",
+           "tree_zero_surface", "marching_cubes_tree", "seen_tree"]
 
 # corner c of a cube sits at offset (c>>2 & 1, c>>1 & 1, c & 1) (x, y, z),
 # the octree child numbering; edges 0-3 run along x, 4-7 along y, 8-11
@@ -134,6 +135,72 @@ class TriMesh(NamedTuple):
 
     vertices: np.ndarray
     faces: np.ndarray
+
+
+def _copy_mesh(h, nv, nf):
+    try:
+        verts = torch.empty((nv, 3), dtype=torch.float64, device=device())
+        faces = torch.empty((nf, 3), dtype=torch.int32, device=device())
+        _lib.call("octf_mesh_copy", h, ptr(verts) if nv else None,
+                  ptr(faces) if nf else None, stream_handle())
+    finally:
+        _lib.lib().octf_mesh_free(h)
+    return verts.cpu().numpy(), faces.cpu().numpy()
+
+
+def _extract_tree(field, seen, origin=None, voxel=1.0, world=False,
+                  slab=(-1, -1)):
+    from .octree import OctreeField
+    if not isinstance(field, OctreeField):
+        raise TypeError("field must be a device OctreeField")
+    if seen is not None and seen.d_max != field.d_max:
+        raise ValueError("seen tree depth differs from the field's")
+    tri, cnt, eax, eoff = _tables()
+    org = np.ascontiguousarray(np.asarray(origin if origin is not None
+                                          else (0.0, 0.0, 0.0), np.float64))
+    st = np.ascontiguousarray(field.state[:3], dtype=np.int64)
+
+    def code(t):
+        return _lib.OCTF_F64 if t.dtype == torch.float64 else _lib.OCTF_F32
+    if field.value.dtype not in (torch.float32, torch.float64):
+        raise TypeError("field values must be float32 or float64")
+    h = ctypes.c_void_p()
+    nv, nf = ctypes.c_int64(), ctypes.c_int64()
+    _lib.call("octf_marching_cubes_tree", None, code(field.value),
+              ptr(field.value), ptr(field.child), st.ctypes.data,
+              field.child.shape[0], field.d_max,
+              code(seen.value) if seen is not None else _lib.OCTF_F64,
+              ptr(seen.value) if seen is not None else None,
+              ptr(seen.child) if seen is not None else None,
+              tri.ctypes.data, cnt.ctypes.data, eax.ctypes.data,
+              eoff.ctypes.data, org.ctypes.data, float(voxel), int(world),
+              int(slab[0]), int(slab[1]), ctypes.byref(h), ctypes.byref(nv),
+              ctypes.byref(nf), stream_handle())
+    return _copy_mesh(h, nv.value, nf.value)
+
+
+def tree_zero_surface(field, seen=None, slab=(-1, -1)):
+    """extract_zero_surface(densify(field), seen) read straight from the leaf
+    store (octf_marching_cubes_tree): grid index coordinates; ``seen`` an
+    observed-mask tree (seen_tree) or None; ``slab`` = (b0, b1) reads only
+    the cubes with x in [8 b0, 8 b1) (a mesh too large for one call)."""
+    return _extract_tree(field, seen, slab=slab)
+
+
+def marching_cubes_tree(field, seen, dom) -> TriMesh:
+    """marching_cubes(densify(field), seen, dom) (mesh.py:114-125) without the
+    dense grid: the same mesh, bit for bit."""
+    if field.resolution != dom.resolution:
+        raise ValueError("field does not match the domain resolution")
+    return TriMesh(*_extract_tree(field, seen, dom.origin, dom.voxel_size,
+                                  True))
+
+
+def seen_tree(seen):
+    """An observed-mask tree of a dense boolean grid (tau = 0: leaves are
+    exactly the constant regions; node values 0 / 1)."""
+    from .octree import build_octree
+    return build_octree(as_device(seen, torch.float64), tau=0.0)
 
 
 def _extract(values, mask, origin=None, voxel=1.0, world=False):

@@ -73,3 +73,123 @@ def test_gpu_cfg1_pipeline_mesh_equals_reference():
     assert np.array_equal(m.faces, z["cfg1_faces"])
     a, b, c = (m.vertices[m.faces[:, k]] for k in range(3))
     assert np.einsum("ij,ij->i", a, np.cross(b, c)).sum() > 0  # outward
+    # the same mesh straight from the leaf store (no dense grid), with the
+    # observed mask as a tree and with f32 values
+    mt = mesh.marching_cubes_tree(res.field, mesh.seen_tree(seen), dom)
+    assert np.array_equal(mt.vertices, z["cfg1_vertices"])
+    assert np.array_equal(mt.faces, z["cfg1_faces"])
+
+
+def _random_tree(seed, d=6):
+    """A mixed-depth tree over random blocky values (coarse leaves of both
+    signs next to fine ones), built on the device."""
+    import torch
+    from paper_1608_07411_b200 import octree
+    rng = np.random.default_rng(seed)
+    n = 1 << d
+    g = np.zeros((n, n, n))
+    for s in (32, 16, 8, 4, 2, 1):
+        k = n // s
+        blk = rng.normal(0, 1.0 / s, (k, k, k))
+        g += np.kron(blk, np.ones((s, s, s)))
+    g -= np.median(g)
+    g = np.round(g * 4) / 4 + 0.125       # few distinct values, no zeros
+    return octree.build_octree(torch.as_tensor(g).cuda(), tau=0.3), g
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")
+@pytest.mark.parametrize("seed", range(4))
+def test_tree_readout_equals_dense_readout(seed):
+    import torch
+    from paper_1608_07411_b200 import mesh, octree
+    t, _ = _random_tree(seed)
+    dense = octree.densify(t)
+    rng = np.random.default_rng(100 + seed)
+    seen = np.ones(dense.shape, dtype=bool)
+    seen[rng.integers(0, 64, 20), :, :] = False
+    seen[:, :, rng.integers(0, 64, 5)] = False
+    for sd in (None, seen):
+        v, f = mesh.extract_zero_surface(dense, sd)
+        vt, ft = mesh.tree_zero_surface(
+            t, None if sd is None else mesh.seen_tree(torch.as_tensor(sd)))
+        assert v.shape[0] > 100
+        assert np.array_equal(v, vt) and np.array_equal(f, ft)
+    # slab by slab: the same triangles (slab meshes index their own vertices)
+    tri = {tuple(map(tuple, vt[ft[i]])) for i in range(ft.shape[0])}
+    got, nf = set(), 0
+    for b0 in range(0, 8, 3):
+        vs, fs = mesh.tree_zero_surface(t, slab=(b0, min(b0 + 3, 8)))
+        nf += fs.shape[0]
+        got |= {tuple(map(tuple, vs[fs[i]])) for i in range(fs.shape[0])}
+    v0, f0 = mesh.tree_zero_surface(t)
+    assert nf == f0.shape[0]
+    assert got == {tuple(map(tuple, v0[f0[i]])) for i in range(f0.shape[0])}
+    # f32 values: the dense readout of the same f32 field
+    t32 = octree.OctreeField(t.value.float(), t.child, t.state, t.d_max)
+    v, f = mesh.extract_zero_surface(octree.densify(t32))
+    vt, ft = mesh.tree_zero_surface(t32)
+    assert np.array_equal(v, vt) and np.array_equal(f, ft)
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")
+def test_tree_readout_at_depth_12_without_dense_grid():
+    """BASELINE config 4's depth (4096^3 cells, 550 GB dense in f64): a
+    sphere-band tree read out from the leaf store; the mesh closes (every
+    edge shared by two faces) and its vertices lie on the sphere."""
+    import torch
+    from paper_1608_07411_b200 import mesh
+    from paper_1608_07411_b200.octree import OctreeField
+    d, r = 12, 0.05
+    n = 1 << d
+    child = np.full(1, -1, dtype=np.int64)
+    value = np.zeros(1)
+    fx = fy = fz = np.zeros(1, dtype=np.int64)
+    fslot = np.zeros(1, dtype=np.int64)   # nodes of the front (to refine)
+    for L in range(d):
+        h = 1.0 / (1 << (L + 1))
+        b = child.shape[0] + 8 * np.arange(fslot.size)
+        child[fslot] = b
+        c = np.arange(8)
+        cx = (2 * fx[:, None] + (c >> 2 & 1)).ravel()
+        cy = (2 * fy[:, None] + (c >> 1 & 1)).ravel()
+        cz = (2 * fz[:, None] + (c & 1)).ravel()
+        sd = np.sqrt(((cx + .5) * h - .5) ** 2 + ((cy + .5) * h - .5) ** 2
+                     + ((cz + .5) * h - .5) ** 2) - r
+        child = np.concatenate([child, np.full(cx.size, -1)])
+        value = np.concatenate([value, sd])
+        keep = (np.abs(sd) < 0.9 * h * np.sqrt(3)) & (L + 1 < d)
+        fslot = (b[:, None] + c).ravel()[keep]
+        fx, fy, fz = cx[keep], cy[keep], cz[keep]
+    # slot 0 root, blocks from slot 1: the reference layout
+    used = child.shape[0]
+    f = OctreeField.from_host(value, child.astype(np.int32),
+                              np.array([used, -1, used], np.int64), d)
+    v, faces = mesh.tree_zero_surface(f)
+    assert faces.shape[0] > 1000
+    e = np.sort(np.stack([faces[:, [0, 1]], faces[:, [1, 2]],
+                          faces[:, [2, 0]]]).reshape(-1, 2), axis=1)
+    _, counts = np.unique(e, axis=0, return_counts=True)
+    assert (counts == 2).all()
+    rad = np.linalg.norm((v + 0.5) / n - 0.5, axis=1)
+    assert np.abs(rad - r).max() < 2.0 / n
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")
+def test_tree_readout_cfg3_reduced_equals_dense():
+    """BASELINE config 2 (adaptive object) at reduced size after restructuring
+    passes: the leaf-store readout equals densify + dense marching cubes."""
+    from paper_1608_07411_b200 import fusion, mesh, octree, scenes, volume
+    sc = scenes.make_cfg3(d_max=7, n_views=16, width=320, height=240,
+                          focal=262.5, device="cuda")
+    p = fusion.FusionParams(**dict(sc.params, iterations=8))
+    dom = volume.VolumeDomain(sc.origin, sc.voxel_size, sc.resolution)
+    views, u0, seen = fusion.prepare(sc.depths, sc.cameras, dom, p)
+    res = fusion.fuse(u0, views, p)
+    m = mesh.marching_cubes(octree.densify(res.field), seen, dom)
+    mt = mesh.marching_cubes_tree(res.field, mesh.seen_tree(seen), dom)
+    assert m.faces.shape[0] > 1000
+    assert np.array_equal(m.vertices, mt.vertices)
+    assert np.array_equal(m.faces, mt.faces)

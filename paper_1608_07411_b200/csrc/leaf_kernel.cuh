@@ -240,7 +240,8 @@ __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
   return u2f(r);
 }
 
-template <typename T, bool FROZEN, int BW, bool ENERGY, int NV>
+// PK: the packed sample store (octf_common.cuh SDesc; frozen trees, staged N)
+template <typename T, bool FROZEN, int BW, bool ENERGY, int NV, bool PK = false>
 __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(LeafArgs<T> a) {
   using A = Arith<T>;
   const LeafParams<T> p = a.p;
@@ -260,7 +261,8 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
   const void* aux = BINW ? (const void*)a.M : (const void*)a.W;
   // packed store: each tile is staged at the top of its own iteration by
   // threads 0 and kT-1 (stage_packed; no prefetch across tiles)
-  const bool packed = a.sd.packed != 0;
+  constexpr bool packed = PK;
+  static_assert(!PK || NV > 0, "the packed store is staged");
   if (NV > 0) {
     if (threadIdx.x == 0) {
       for (int k = 0; k < kStages; ++k) mbar_init(&s_bar[k], packed ? 2 : 1);
@@ -297,11 +299,11 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
   const bool active = slot_ok && ((lmask >> c) & 1u);
   // the leaf's entry in the staged tile: its slot, or (packed) its rank r
   // among the tile's leaves at chunk r / 32, lane r % 32, views 32 apart
-  int sbase = threadIdx.x, sstr = kTileLeaves;
+  int sbase = threadIdx.x;
+  constexpr int sstr = PK ? kChunk : kTileLeaves;
   if (packed) {
     const int r = (meta_rbase(meta.y) + __popc(lmask & ((1u << c) - 1u))) & 255;
     sbase = (r >> 5) * NVP * kChunk + (r & 31);
-    sstr = kChunk;
     if (NV > 0 && threadIdx.x == kT - 1)  // n_t from the tile's last block
       stage_packed<NVP, BW>(
           s_tile, &s_bar[stage], a.F, aux, tile_id,
@@ -399,7 +401,7 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
     mbar_wait(&s_bar[stage], (unsigned)(it / kStages) & 1u);
     // view v of the leaf at sf[v * R]; its mask word at the mask tile's
     // entry for the slot / rank
-    const int R = sstr;
+    constexpr int R = sstr;
     const float* sf = s_tile + sbase;
     const int t = packed ? (meta_rbase(meta.y) +
                             __popc(lmask & ((1u << c) - 1u))) & 255

@@ -7,6 +7,7 @@
 
 #include <chrono>
 #include <cstdint>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -239,6 +240,12 @@ struct Ctx {
   DevBuf<double> partials;
   DevBuf<double> mid;       // stripe sums of the two-stage energy reduction
   DevBuf<double> dscalar;
+  // restructuring scratch of the typed solver (solver_impl.cuh: split
+  // events, join records) per value type, and the pd split keys: owned by
+  // the context, so two contexts (or devices) never share device buffers
+  std::shared_ptr<void> rs_ev[2], rs_join[2];
+  DevBuf<int32_t> rs_slot, rs_idx;
+  DevBuf<uint64_t> rs_key;
 
   // live profiling (octf_ctx_profile): CUDA events on the launch stream
   bool timing = false;

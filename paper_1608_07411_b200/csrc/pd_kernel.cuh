@@ -90,7 +90,7 @@ constexpr size_t pd_smem_bytes(int nv, bool binw) {  // one stage
 
 // WP: also write the bottom propagate level of the five fields (frozen
 // passes over a full leaf-block list)
-template <typename T, int BW, int NV, bool WP = false>
+template <typename T, int BW, int NV, bool WP = false, bool PK = false>
 __global__ void __launch_bounds__(kT, pd_minb(BW != kWeights, NV, sizeof(T))) k_pd_pass(PdArgs<T> a) {
   static_assert(NV > 0 && (NV & (NV - 1)) == 0, "NV: power of two");
   constexpr bool BINW = BW != kWeights;  // unit weights (+inf = absent)
@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(kT, pd_minb(BW != kWeights, NV, sizeof(T))) k_
   // or packed (octf_common.cuh SDesc) in two parts like k_leaf_pass's
   // stage_packed -- the first kEarlyChunks chunks (nchunks = -1), then the
   // rest of the tile's ceil(n_t / 32) chunks
-  const bool packed = a.sd.packed != 0;
+  constexpr bool packed = PK;  // the packed sample store (SDesc)
   auto stage_pd = [&](float* buf, uint64_t* bar, int tile, int nchunks) {
     constexpr bool WST = !(BINW || WGLOB);  // weights staged too
     const size_t fo = (size_t)tile * NV * kTileLeaves;
@@ -157,11 +157,11 @@ __global__ void __launch_bounds__(kT, pd_minb(BW != kWeights, NV, sizeof(T))) k_
   // the leaf's entry in the staged tile: its slot, or (packed) its rank r
   // among the tile's leaves at chunk r / 32, lane r % 32, sorted ranks 32
   // apart
-  int sp = threadIdx.x, R = kTileLeaves;
+  int sp = threadIdx.x;
+  constexpr int R = PK ? kChunk : kTileLeaves;
   if (packed) {
     const int r = (meta_rbase(meta.y) + __popc(lmask & ((1u << c) - 1u))) & 255;
     sp = (r >> 5) * NV * kChunk + (r & 31);
-    R = kChunk;
     if (threadIdx.x == kT - 1)  // n_t from the tile's last block
       stage_pd(s_tile, &s_bar[stage], tile_id,
                inrange ? (meta_rbase(meta.y) + __popc(lmask) + kChunk - 1) / kChunk

@@ -836,6 +836,16 @@ inline void smem_opt_in(const void* fn, size_t smem) {
 // resident CTAs, each walking tiles with a grid stride)
 template <typename T, bool FZ, int BW, bool EN, int N>
 void launch_leaf(unsigned g, cudaStream_t st, LeafArgs<T> a) {
+  if constexpr (FZ && N > 0) {  // the packed store: its own instantiation
+    if (a.sd.packed) {
+      constexpr size_t smem = leaf_smem_bytes(N, BW);
+      const void* fn = (const void*)k_leaf_pass<T, FZ, BW, EN, N, true>;
+      smem_opt_in(fn, smem);
+      a.ntiles = (int)g;
+      k_leaf_pass<T, FZ, BW, EN, N, true><<<g, kT, smem, st>>>(a);
+      return;
+    }
+  }
   constexpr size_t smem = leaf_smem_bytes(N, BW);
   const void* fn = (const void*)k_leaf_pass<T, FZ, BW, EN, N>;
   smem_opt_in(fn, smem);
@@ -927,6 +937,14 @@ void launch_leaf_pass(Ctx& c, const T* snap, T* uval, const int32_t* child,
   OCTF_CUDA(cudaGetLastError());
   ++c.launches;
   if (timed && c.timing) OCTF_CUDA(cudaEventRecord(c.tev[1], st));
+}
+
+// typed scratch kept in a context slot (Ctx::rs_ev / rs_join)
+template <typename B>
+B& ctx_bufs(std::shared_ptr<void>& slot) {
+  if (!slot)
+    slot = std::shared_ptr<void>(new B(), [](void* q) { delete (B*)q; });
+  return *static_cast<B*>(slot.get());
 }
 
 template <typename T>
@@ -1030,7 +1048,7 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
 
   // ---- split cascade + allocation in depth-first order
   if (nsplit > 0) {
-    static thread_local EventBufs<T> eb;
+    EventBufs<T>& eb = ctx_bufs<EventBufs<T>>(c.rs_ev[sizeof(T) == 8]);
     // the pool bound on events (blocks the pool can still hand out) sizes
     // the exhaustion test; the buffers start at a small multiple of the
     // split count and are sized to the bound only when a cascade outgrows
@@ -1110,7 +1128,7 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
 
   // ---- join cascade, bottom-up
   if (ncand > 0) {
-    static thread_local JoinBufs<T> jb;
+    JoinBufs<T>& jb = ctx_bufs<JoinBufs<T>>(c.rs_join[sizeof(T) == 8]);
     const int64_t jcap_rec = c.nblocks * 8 + 8;
     JoinRecs<T> rec = jb.view(jcap_rec);
     // per level (bottom-up): cheap candidate tests over the level's slots,
@@ -1142,16 +1160,19 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
       ja.cacc = cacc;
       ja.ccount = ccount;
       ja.d_max = prm.d_max;
-      static int coop_blocks = 0;
+      // resident CTAs of the cooperative launch, per device
+      static int coop_per_dev[64] = {};
+      int dev = 0;
+      OCTF_CUDA(cudaGetDevice(&dev));
+      int& coop_blocks = coop_per_dev[dev & 63];
       if (!coop_blocks) {
-        int per_sm = 0, dev = 0, nsm = 0;
+        int per_sm = 0, nsm = 0;
         OCTF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
             &per_sm, k_joins_coop<T>, 256, 0));
-        OCTF_CUDA(cudaGetDevice(&dev));
         OCTF_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount,
                                          dev));
+        if (per_sm * nsm < 1) throw Error(kECuda, "joins: no resident CTA");
         coop_blocks = per_sm * nsm;
-        if (coop_blocks < 1) throw Error(kECuda, "joins: no resident CTA");
       }
       void* kargs[] = {&ja};
       OCTF_CUDA(cudaLaunchCooperativeKernel((const void*)k_joins_coop<T>,
@@ -1407,6 +1428,12 @@ void pd_passes_impl(Ctx& c, PdHostArgs& a, cudaStream_t st);
 template <typename T, int BW, int N, bool WP>
 void launch_pd_wp(unsigned g, cudaStream_t st, const PdArgs<T>& p) {
   constexpr size_t smem = pd_smem_bytes(N, BW != kWeights) * kStages;
+  if (p.sd.packed) {  // the packed store: its own instantiation
+    const void* fp = (const void*)k_pd_pass<T, BW, N, WP, true>;
+    smem_opt_in(fp, smem);
+    k_pd_pass<T, BW, N, WP, true><<<g, kT, smem, st>>>(p);
+    return;
+  }
   const void* fn = (const void*)k_pd_pass<T, BW, N, WP>;
   smem_opt_in(fn, smem);
   const unsigned res =
@@ -1611,9 +1638,10 @@ void pd_restructure_impl(Ctx& c, PdRsArgs& a, cudaStream_t st) {
   FieldSet<T> fs{};
   for (int k = 0; k < 5; ++k) fs.v[k] = (T*)a.f[k];
   const int64_t used = a.state[0];
-  static thread_local JoinBufs<T> jb;
-  static thread_local DevBuf<int32_t> sslot, sidx;
-  static thread_local DevBuf<uint64_t> skey;
+  JoinBufs<T>& jb = ctx_bufs<JoinBufs<T>>(c.rs_join[sizeof(T) == 8]);
+  DevBuf<int32_t>& sslot = c.rs_slot;
+  DevBuf<int32_t>& sidx = c.rs_idx;
+  DevBuf<uint64_t>& skey = c.rs_key;
   const int64_t nl = c.nlb * 8 + 1;
   sslot.ensure(nl);
   sidx.ensure(nl);

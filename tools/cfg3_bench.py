@@ -63,6 +63,7 @@ else:
     s = fusion.Solver(u0, views, p, precision=args.precision)
 s.ctx.profile(True)
 passes = []
+acc = {}  # per-pass profiles summed (profile(True) reads and resets)
 for t in range(args.passes):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -72,6 +73,9 @@ for t in range(args.passes):
     e1.record()
     torch.cuda.synchronize()
     pr = s.ctx.profile(True)
+    for key, val in pr.items():
+        if isinstance(val, (int, float)):
+            acc[key] = acc.get(key, 0) + val
     passes.append({"ms": e0.elapsed_time(e1), "nodes": st.node_count,
                    "splits": st.splits, "joins": st.joins,
                    "leaf_ms": pr["leaf_ms"], "prepare_ms": pr["prepare_ms"],
@@ -79,7 +83,11 @@ for t in range(args.passes):
                    "restructure_ms": pr["restructure_ms"],
                    **({"rebuild_phases_ms": pr["rebuild_phases_ms"]}
                       if os.environ.get("OCTF_PHASES") == "1" else {})})
-prof = s.ctx.profile(False)
+pr = s.ctx.profile(False)
+for key, val in pr.items():
+    if isinstance(val, (int, float)):
+        acc[key] = acc.get(key, 0) + val
+prof = acc
 res = s.result()
 mesh_info = None
 if args.mesh:

@@ -55,5 +55,42 @@ def full(path):
                 print(f"  {w} = {vals[i]} {units[i]}")
 
 
+def traffic(path, kernel, workload, out="profiles/r02/ncu_traffic.json"):
+    """Append the DRAM bytes per launch of the first kernel in an ncu --set
+    full report to ``out``, tagged with the library source hash bench.py
+    checks (bench.lib_sha): the bench line cites it only for this build."""
+    import json
+    import os
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    raw = subprocess.check_output(["ncu", "-i", path, "--page", "raw", "--csv"],
+                                  text=True)
+    rows = list(csv.reader(raw.splitlines()))
+    hdr, units, vals = rows[0], rows[1], rows[2]
+
+    def get(name):
+        i = hdr.index(name)
+        v = float(vals[i].replace(",", ""))
+        return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9,
+                    "Tbyte": 1e12, "ns": 1e-3, "us": 1, "usecond": 1,
+                    "ms": 1e3, "msecond": 1e3, "nsecond": 1e-3}.get(units[i], 1)
+    rd, wr = get("dram__bytes_read.sum"), get("dram__bytes_write.sum")
+    rec = {"entries": []}
+    if os.path.exists(out):
+        rec = json.load(open(out))
+    rec["entries"] = [e for e in rec["entries"]
+                      if (e["kernel"], e["workload"]) != (kernel, workload)]
+    rec["entries"].append({
+        "kernel": kernel, "workload": workload, "lib_sha": bench.lib_sha(),
+        "kernel_name": vals[hdr.index("Kernel Name")][:120],
+        "dram_bytes_read": rd, "dram_bytes_write": wr,
+        "dram_bytes_per_launch": rd + wr,
+        "duration_us_under_ncu": get("gpu__time_duration.sum"),
+        "report": os.path.basename(path)})
+    json.dump(rec, open(out, "w"), indent=1)
+    print(json.dumps(rec["entries"][-1]))
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
+    {"launches": launches, "full": full, "traffic": traffic}[sys.argv[1]](
+        *sys.argv[2:])

@@ -12,7 +12,7 @@ timeout 1200 python bench.py > $O/bench.json 2> $O/bench.err || exit 1
 timeout 600 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu \
   --no-parity --no-cfg2 > $O/bench_short.json 2>&1 || exit 1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 \
-  --csv --log-file $O/launches.csv \
+  -k regex:"^k_" --csv --log-file $O/launches.csv \
   python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-parity \
   --no-cfg2 > $O/ncu_launch.log 2>&1
 timeout 600 python tools/profile_cfg5.py --passes 3 > /dev/null 2>&1 || exit 1

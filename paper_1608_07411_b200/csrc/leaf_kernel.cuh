@@ -544,6 +544,9 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
       if (threadIdx.x == 0) a.epart[tile_id] = tot;
     }
   }
+  // one CTA per tile (the default launch: grid = tiles): no refill, no
+  // trailing barrier (measured: the persistent loop's tail cost cfg2 11 %)
+  if (!OCTF_PERSIST) break;
   if (NV > 0) {
     // every thread is done with this stage (and the energy scratch): refill
     // it with the tile kStages steps ahead

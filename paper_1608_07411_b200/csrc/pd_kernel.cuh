@@ -392,6 +392,7 @@ __global__ void __launch_bounds__(kT, pd_minb(BW != kWeights, NV, sizeof(T))) k_
       o[par] = (T)(acc / 8.0);
     }
   }
+  if (!OCTF_PERSIST) break;  // one CTA per tile (the default launch)
   // every thread is done with this stage and the shared scratch: refill the
   // stage with the tile kStages steps ahead
   __syncthreads();

@@ -516,33 +516,23 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
       a.join_bot[atomicAdd(a.counters + 1, 1)] = __ldg(a.lpar + i);
   }
   if (ENERGY) {
-#ifndef OCTF_LEAF_F64_ENERGY_SUM
+    // one energy partial per warp (kLeafParts per tile, fixed order: the
+    // sum stays deterministic) -- no CTA barrier, so each warp retires as
+    // soon as it is done.  fp32 throughput mode at N >= 32: the terms are
+    // fp32 values summed in fp32 across the warp; otherwise in double.
+    double e;
     if (sizeof(T) == 4 && NV >= 32) {
-      // fp32 throughput mode: the terms are fp32 values; warps sum them in
-      // fp32, the CTA's eight warp sums are added in double by thread 0
-      // (fixed order: deterministic).  The fp64 parity mode keeps the
-      // double block reduction.  cfg5 (N = 32) 3.467 -> 3.413 ms; slower
-      // at N = 16 (0.298 -> 0.313 ms), not used there.
-      __shared__ double s_w[kT / 32];
-      float e = (float)eterm;
+      float ef = (float)eterm;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ef += __shfl_xor_sync(FULL, ef, o);
+      e = (double)ef;
+    } else {
+      e = eterm;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(FULL, e, o);
-      if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = (double)e;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        double tot = 0.0;
-#pragma unroll
-        for (int k = 0; k < kT / 32; ++k) tot += s_w[k];
-        a.epart[tile_id] = tot;
-      }
-    } else
-#endif
-    {
-      typedef cub::BlockReduce<double, kT> BR;
-      __shared__ typename BR::TempStorage tmp;
-      const double tot = BR(tmp).Sum(eterm);
-      if (threadIdx.x == 0) a.epart[tile_id] = tot;
     }
+    if ((threadIdx.x & 31) == 0)
+      a.epart[(int64_t)tile_id * kLeafParts + (threadIdx.x >> 5)] = e;
   }
   // one CTA per tile (the default launch: grid = tiles): no refill, no
   // trailing barrier (measured: the persistent loop's tail cost cfg2 11 %)

@@ -54,6 +54,7 @@ __host__ __device__ __forceinline__ void unpack_meta_w(int w, int& pz,
 // touches 128 contiguous bytes, and a whole tile is one contiguous
 // nvp*1 KiB block that a single TMA bulk copy stages into shared memory.
 constexpr int kTileLeaves = 256;
+constexpr int kLeafParts = kTileLeaves / 32;  // energy partials per tile (warps)
 // Sparse per-tile sample layout (ELL, many views): tile t = leaves
 // [256t, 256t+256) holds K_t rows of 256 entries from off[t]; row j of a leaf
 // is its j-th observed view in view order, rows past its count are zero.

@@ -43,6 +43,7 @@ void need_device() {
     cudaGetLastError();
     throw octf::Error(octf::kECuda, "no CUDA device available");
   }
+  octf::pool_keep();
 }
 
 void check_dtype(int dtype) {

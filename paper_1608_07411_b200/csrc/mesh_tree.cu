@@ -335,7 +335,7 @@ void mc_tree_impl(Ctx& c, const T* value, const int32_t* child, int d,
   int64_t ne = 0;
   OCTF_CUDA(cudaMemcpyAsync(&ne, off + nlist, 8, cudaMemcpyDeviceToHost, st));
   OCTF_CUDA(cudaStreamSynchronize(st));
-  if (std::getenv("OCTF_MESH_DEBUG"))
+  if (const char* md = std::getenv("OCTF_MESH_DEBUG"); md && md[0] == '1')
     fprintf(stderr, "mesh_tree: %d of %lld bricks mixed, %lld corners\n",
             nlist, (long long)nbr, (long long)ne);
   if (ne == 0) return;

@@ -295,6 +295,7 @@ void ctx_set_views(Ctx& c, int nviews, const float* const* vval,
                    const float* const* vw, const int32_t* const* vchild,
                    cudaStream_t st);
 void ctx_gather(Ctx& c, cudaStream_t st);
+void pool_keep();  // the default memory pool keeps freed blocks (per device)
 int64_t ctx_node_order(Ctx& c, const int32_t* child, int d_max,
                        bool leaves_only, int32_t* out_slots,
                        uint64_t* out_keys, cudaStream_t st);

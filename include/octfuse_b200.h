@@ -347,6 +347,34 @@ int octf_view_tsdf(const float *depth, int width, int height,
                    int n, double delta, double eta, float *f, uint8_t *w,
                    double *wf_sum, double *w_sum, void *stream);
 
+/* The same TSDF for the n_b^3 voxels of a box of the n^3 grid, box =
+ * {i0, j0, k0, n_b} (host): global voxel (i0 + i, j0 + j, k0 + k) -- the
+ * same arithmetic -- at box-local index (i*n_b + j)*n_b + k of f, w and the
+ * optional accumulators. */
+int octf_view_tsdf_box(const float *depth, int width, int height,
+                       const double *cam, const double *origin, double voxel,
+                       int n, const int32_t *box, double delta, double eta,
+                       float *f, uint8_t *w, double *wf_sum, double *w_sum,
+                       void *stream);
+
+/* octree.py:243-306 build_octree for a BOX subtree of a tree of depth
+ * d_max: f (and w) the (2^d_box)^3 grid of the box, whose root is the node
+ * at global level level0 = d_max - d_box and pool slot root_slot; split
+ * decisions use global levels, and the box's splitting nodes continue the
+ * enclosing tree's depth-first ranks from root_rank (rank of the box root if
+ * it splits), so the subtree lands at the slots the whole-tree build gives
+ * it.  *nsplit (host) = splitting nodes of the box; root_stats (host,
+ * double[8]) = the box root's pyramid entries {min f, max f, value mean,
+ * min w, max w, mean w, mean f*w, mean f} for the enclosing levels.
+ * propagate != 0: unweighted build's child means inside the box.
+ * OCTF_EPOOL if the pool is too small (nothing written past cap). */
+int octf_build_octree_box(const void *f, int f_dtype, const uint8_t *w,
+                          int d_box, int level0, int d_max, double tau,
+                          void *value, int dtype, float *weight,
+                          int32_t *child, int64_t cap, int64_t root_rank,
+                          int32_t root_slot, int propagate, int64_t *nsplit,
+                          double *root_stats, void *stream);
+
 /* fusion.py:149-155 initial_field */
 int octf_initial_field(const double *wf_sum, const double *w_sum, double gamma,
                        int64_t n, double *u, void *stream);

@@ -49,6 +49,10 @@ _SIGS = {
                                  P], I32),
     "octf_ctx_prepare": ([P, P, P, I64, I32, I32, P, P, P, P], I32),
     "octf_node_order": ([P, P, P, I64, I32, I32, P, P, P, P], I32),
+    "octf_view_tsdf_box": ([P, I32, I32, P, P, DBL, I32, P, DBL, DBL, P, P, P,
+                            P, P], I32),
+    "octf_build_octree_box": ([P, I32, P, I32, I32, I32, DBL, P, I32, P, P,
+                               I64, I64, I32, I32, P, P, P], I32),
     "octf_pd_restructure": ([P, I32, P, P, P, I64, I32, DBL, DBL, P, P], I32),
     "octf_marching_cubes": ([P, P, I32, P, P, P, P, P, DBL, I32, P, P, P, P],
                             I32),

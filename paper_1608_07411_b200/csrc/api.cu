@@ -785,14 +785,88 @@ int octf_view_tsdf(const float* depth, int width, int height,
                    const double* cam, const double* origin, double voxel,
                    int n, double delta, double eta, float* f, uint8_t* w,
                    double* wf_sum, double* w_sum, void* stream) {
+  return octf_view_tsdf_box(depth, width, height, cam, origin, voxel, n,
+                            nullptr, delta, eta, f, w, wf_sum, w_sum, stream);
+}
+
+int octf_view_tsdf_box(const float* depth, int width, int height,
+                       const double* cam, const double* origin, double voxel,
+                       int n, const int32_t* box, double delta, double eta,
+                       float* f, uint8_t* w, double* wf_sum, double* w_sum,
+                       void* stream) {
   return guard([&] {
     if (!depth || !cam || !origin || !f || !w)
       throw octf::Error(octf::kEArg, "null argument");
     if ((wf_sum == nullptr) != (w_sum == nullptr))
       throw octf::Error(octf::kEArg, "wf_sum and w_sum go together");
     need_device();
-    octf::view_tsdf(depth, width, height, cam, origin, voxel, n, delta, eta, f,
-                    w, wf_sum, w_sum, S(stream));
+    int b[4];
+    if (box)
+      for (int q = 0; q < 4; ++q) b[q] = box[q];
+    octf::view_tsdf(depth, width, height, cam, origin, voxel, n,
+                    box ? b : nullptr, delta, eta, f, w, wf_sum, w_sum,
+                    S(stream));
+  });
+}
+
+int octf_build_octree_box(const void* f, int f_dtype, const uint8_t* w,
+                          int d_box, int level0, int d_max, double tau,
+                          void* value, int dtype, float* weight,
+                          int32_t* child, int64_t cap, int64_t root_rank,
+                          int32_t root_slot, int propagate, int64_t* nsplit,
+                          double* root_stats, void* stream) {
+  return guard([&] {
+    check_dtype(f_dtype);
+    check_dtype(dtype);
+    if (d_max < 0 || d_max > OCTF_MAX_DEPTH || d_box < 0 || level0 < 0 ||
+        level0 + d_box != d_max)
+      throw octf::Error(octf::kEDepth, "tree depth out of range");
+    if (w && !weight) throw octf::Error(octf::kEArg, "weighted build needs weight");
+    if (!f || !value || !child || !nsplit || !root_stats)
+      throw octf::Error(octf::kEArg, "null argument");
+    need_device();
+    int64_t total = 0;
+    for (int l = 0; l <= d_box; ++l) total += (int64_t)1 << (3 * l);
+    octf::DevBuf<double> mn, mx, mean, wm, wf, pl;
+    octf::DevBuf<uint8_t> wmn, wmx;
+    mn.ensure(total);
+    mx.ensure(total);
+    mean.ensure(total);
+    if (w) {
+      wm.ensure(total);
+      wf.ensure(total);
+      pl.ensure(total);
+      wmn.ensure(total);
+      wmx.ensure(total);
+    }
+    octf::pyramids(f, f_dtype, w, d_box, mn.p, mx.p, mean.p, wmn.p, wmx.p,
+                   wm.p, wf.p, pl.p, S(stream));
+    // the box root's pyramid statistics, for the enclosing levels
+    double st[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    uint8_t wb[2] = {0, 0};
+    OCTF_CUDA(cudaMemcpyAsync(&st[0], mn.p, 8, cudaMemcpyDeviceToHost, S(stream)));
+    OCTF_CUDA(cudaMemcpyAsync(&st[1], mx.p, 8, cudaMemcpyDeviceToHost, S(stream)));
+    OCTF_CUDA(cudaMemcpyAsync(&st[2], mean.p, 8, cudaMemcpyDeviceToHost, S(stream)));
+    if (w) {
+      OCTF_CUDA(cudaMemcpyAsync(&wb[0], wmn.p, 1, cudaMemcpyDeviceToHost, S(stream)));
+      OCTF_CUDA(cudaMemcpyAsync(&wb[1], wmx.p, 1, cudaMemcpyDeviceToHost, S(stream)));
+      OCTF_CUDA(cudaMemcpyAsync(&st[5], wm.p, 8, cudaMemcpyDeviceToHost, S(stream)));
+      OCTF_CUDA(cudaMemcpyAsync(&st[6], wf.p, 8, cudaMemcpyDeviceToHost, S(stream)));
+      OCTF_CUDA(cudaMemcpyAsync(&st[7], pl.p, 8, cudaMemcpyDeviceToHost, S(stream)));
+    }
+    OCTF_CUDA(cudaStreamSynchronize(S(stream)));
+    st[3] = wb[0];
+    st[4] = wb[1];
+    for (int q = 0; q < 8; ++q) root_stats[q] = st[q];
+    octf::BuildIn in{mean.p, mn.p, mx.p, nullptr, w != nullptr, wmn.p, wmx.p,
+                     wm.p, tau, d_box, cap};
+    in.level0 = level0;
+    in.d_glob = d_max;
+    in.root_rank = root_rank;
+    in.root_slot = root_slot;
+    in.nsplit_out = nsplit;
+    octf::build_tree(in, value, dtype, w ? weight : nullptr, child, nullptr,
+                     propagate != 0, S(stream));
   });
 }
 

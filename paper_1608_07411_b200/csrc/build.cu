@@ -39,15 +39,17 @@ struct Cam {
 
 __global__ void k_view_tsdf(const float* __restrict__ depth, int W, int H,
                             Cam cam, double ox, double oy, double oz,
-                            double vox, int n, double delta, double eta,
-                            float* f_out, uint8_t* w_out, double* wf_sum,
-                            double* w_sum) {
+                            double vox, int n, int i0, int j0, int k0,
+                            double delta, double eta, float* f_out,
+                            uint8_t* w_out, double* wf_sum, double* w_sum) {
+  // the n^3 voxels of the box at global index (i0, j0, k0) (the whole grid:
+  // offset 0); outputs indexed box-locally
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n3 = (int64_t)n * n * n;
   if (idx >= n3) return;
-  const int k = (int)(idx % n);
-  const int j = (int)((idx / n) % n);
-  const int i = (int)(idx / ((int64_t)n * n));
+  const int k = k0 + (int)(idx % n);
+  const int j = j0 + (int)((idx / n) % n);
+  const int i = i0 + (int)(idx / ((int64_t)n * n));
   // axis centres minus the camera translation (tsdf.py:93-95)
   const double xs = (ox + ((double)i + 0.5) * vox) - cam.t[0];
   const double ys = (oy + ((double)j + 0.5) * vox) - cam.t[1];
@@ -186,6 +188,7 @@ __global__ void k_split_flags(const double* minf, const double* maxf,
                               const uint8_t* wminf, const uint8_t* wmaxf,
                               int has_w, double tau, int64_t off, int64_t n3,
                               int L, int d_max, BuildScratch s) {
+  // L, d_max: global levels (a box subtree's level 0 is global level0)
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n3) return;
   const int64_t k = off + i;
@@ -197,7 +200,7 @@ __global__ void k_split_flags(const double* minf, const double* maxf,
       sp = true;
   }
   s.split[k] = sp;
-  if (L == 0) s.exists[k] = 1;
+  if (n3 == 1) s.exists[k] = 1;  // the (box) root
 }
 
 __device__ __forceinline__ int64_t child_index(int64_t off1, int n1, int i,
@@ -335,7 +338,9 @@ void build_impl(const BuildIn& in, T* value, float* weight, int32_t* child,
   for (int L = 0; L <= d; ++L) {
     const int64_t n3 = (int64_t)1 << (3 * L);
     k_split_flags<<<nblk(n3), kB, 0, st>>>(in.minf, in.maxf, in.wminf, in.wmaxf,
-                                          in.has_w, in.tau, off[L], n3, L, d, s);
+                                          in.has_w, in.tau, off[L], n3,
+                                          L + in.level0,
+                                          in.d_glob >= 0 ? in.d_glob : d, s);
   }
   for (int L = 0; L < d; ++L)
     k_exists<<<nblk((int64_t)1 << (3 * L)), kB, 0, st>>>(off[L], off[L + 1],
@@ -343,9 +348,11 @@ void build_impl(const BuildIn& in, T* value, float* weight, int32_t* child,
   for (int L = d; L >= 0; --L)
     k_counts<<<nblk((int64_t)1 << (3 * L)), kB, 0, st>>>(
         off[L], L < d ? off[L + 1] : 0, 1 << L, L == d, s);
-  const int64_t zero = 0;
-  const int32_t root = 0;
-  OCTF_CUDA(cudaMemcpyAsync(s.rank, &zero, sizeof(int64_t),
+  // the root's depth-first rank and slot: 0 / 0 for a whole tree; a box
+  // subtree (octf_build_octree_box) continues the enclosing tree's ranks
+  const int64_t root_rank = in.root_rank;
+  const int32_t root = in.root_slot;
+  OCTF_CUDA(cudaMemcpyAsync(s.rank, &root_rank, sizeof(int64_t),
                             cudaMemcpyHostToDevice, st));
   OCTF_CUDA(cudaMemcpyAsync(s.node, &root, sizeof(int32_t),
                             cudaMemcpyHostToDevice, st));
@@ -356,7 +363,8 @@ void build_impl(const BuildIn& in, T* value, float* weight, int32_t* child,
   OCTF_CUDA(cudaMemcpyAsync(&nsplit, s.cnt, sizeof(int64_t),
                             cudaMemcpyDeviceToHost, st));
   OCTF_CUDA(cudaStreamSynchronize(st));
-  const int64_t used = 1 + 8 * nsplit;
+  const int64_t used = 1 + 8 * (root_rank + nsplit);
+  if (in.nsplit_out) *in.nsplit_out = nsplit;
   if (used > in.cap) throw Error(kEPool, "node pool capacity exhausted");
   for (int L = 0; L <= d; ++L) {
     const int64_t n3 = (int64_t)1 << (3 * L);
@@ -370,18 +378,20 @@ void build_impl(const BuildIn& in, T* value, float* weight, int32_t* child,
           off[L], off[L + 1], 1 << L, s, value);
   OCTF_CUDA(cudaGetLastError());
   OCTF_CUDA(cudaStreamSynchronize(st));
-  state[0] = used;
-  state[1] = -1;
-  state[2] = used;
+  if (state) {
+    state[0] = used;
+    state[1] = -1;
+    state[2] = used;
+  }
 }
 
 }  // namespace
 
 // ---------------------------------------------------------------- entry --
 void view_tsdf(const float* depth, int width, int height, const double* cam,
-               const double* origin, double voxel, int n, double delta,
-               double eta, float* f, uint8_t* w, double* wf_sum, double* w_sum,
-               cudaStream_t st) {
+               const double* origin, double voxel, int n, const int* box,
+               double delta, double eta, float* f, uint8_t* w, double* wf_sum,
+               double* w_sum, cudaStream_t st) {
   if (delta <= 0 || eta <= 0)
     throw Error(kEArg, "delta and eta must be positive");
   if (n < 1 || (n & (n - 1))) throw Error(kEArg, "resolution must be a power of two");
@@ -392,10 +402,17 @@ void view_tsdf(const float* depth, int width, int height, const double* cam,
   c.cy = cam[3];
   for (int q = 0; q < 9; ++q) c.r[q] = cam[4 + q];
   for (int q = 0; q < 3; ++q) c.t[q] = cam[13 + q];
-  const int64_t n3 = (int64_t)n * n * n;
+  // box = {i0, j0, k0, edge} (null: the whole n^3 grid)
+  const int nb = box ? box[3] : n;
+  if (box && (nb < 1 || box[0] < 0 || box[1] < 0 || box[2] < 0 ||
+              box[0] + nb > n || box[1] + nb > n || box[2] + nb > n))
+    throw Error(kEArg, "box outside the grid");
+  const int64_t n3 = (int64_t)nb * nb * nb;
   k_view_tsdf<<<nblk(n3), kB, 0, st>>>(depth, width, height, c, origin[0],
-                                       origin[1], origin[2], voxel, n, delta,
-                                       eta, f, w, wf_sum, w_sum);
+                                       origin[1], origin[2], voxel, nb,
+                                       box ? box[0] : 0, box ? box[1] : 0,
+                                       box ? box[2] : 0, delta, eta, f, w,
+                                       wf_sum, w_sum);
   OCTF_CUDA(cudaGetLastError());
 }
 

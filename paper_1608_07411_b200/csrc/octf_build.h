@@ -19,12 +19,20 @@ struct BuildIn {
   double tau;
   int d_max;
   int64_t cap;
+  // a box subtree of an enclosing tree (octf_build_octree_box): the global
+  // level of the box root, the global depth, the root's depth-first rank and
+  // slot; whole tree: 0, d_max, 0, 0
+  int level0 = 0;
+  int d_glob = -1;
+  int64_t root_rank = 0;
+  int32_t root_slot = 0;
+  int64_t* nsplit_out = nullptr;  // splitting nodes of the (box) tree
 };
 
 void view_tsdf(const float* depth, int width, int height, const double* cam,
-               const double* origin, double voxel, int n, double delta,
-               double eta, float* f, uint8_t* w, double* wf_sum, double* w_sum,
-               cudaStream_t st);
+               const double* origin, double voxel, int n, const int* box,
+               double delta, double eta, float* f, uint8_t* w, double* wf_sum,
+               double* w_sum, cudaStream_t st);
 void initial_field(const double* wf, const double* ws, double gamma, int64_t n,
                    double* u, cudaStream_t st);
 void pyramids(const void* f, int f_dtype, const uint8_t* w, int d_max,

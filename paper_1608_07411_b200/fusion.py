@@ -31,6 +31,7 @@ from ._device import as_device, device, pool_empty, ptr, stream_handle, to_numpy
 from .octree import OctreeField, build_octree, full_tree_capacity
 
 __all__ = [
+    "prepare_boxed",
     "FusionParams",
     "IterationStats",
     "FuseResult",
@@ -202,6 +203,143 @@ def prepare(depths, cameras, dom, params: FusionParams, *, comm=None):
                                 _tree_pack, _tree_unpack(device()), comm)
     u0 = build_octree(initial_field(wf, ws, params.gamma), tau=params.tau)
     return trees, u0, ws > 0
+
+
+class _BoxTree:
+    """One tree of a box-wise input stage (prepare_boxed): a growable
+    reference-layout pool filled subtree by subtree (octf_build_octree_box),
+    the enclosing root's depth-first rank count and the box roots'
+    pyramid statistics."""
+
+    def __init__(self, d_max, weighted, dtype, cap=1 << 16):
+        self.d, self.weighted, self.dtype = d_max, weighted, dtype
+        self.cap = cap
+        self.value = pool_empty(cap, dtype)
+        self.child = pool_empty(cap, torch.int32)
+        self.weight = pool_empty(cap, torch.float32) if weighted else None
+        self.ranks = 0                  # splitting nodes of the boxes so far
+        self.stats = [None] * 8
+
+    def _grow(self):
+        cap = 2 * self.cap
+
+        def g(t):
+            out = pool_empty(cap, t.dtype)
+            out[:self.cap].copy_(t[:self.cap])
+            return out
+        self.value, self.child = g(self.value), g(self.child)
+        if self.weight is not None:
+            self.weight = g(self.weight)
+        self.cap = cap
+
+    def add(self, c, f, w, tau, propagate):
+        """Build box c (child c of the root) from its grid f (and w)."""
+        d_box = self.d - 1
+        ns = np.zeros(1, dtype=np.int64)
+        st = np.zeros(8, dtype=np.float64)
+        code = _lib.OCTF_F32 if self.dtype == torch.float32 else _lib.OCTF_F64
+        while True:
+            try:
+                _lib.call("octf_build_octree_box", ptr(f),
+                          _lib.OCTF_F32 if f.dtype == torch.float32
+                          else _lib.OCTF_F64, ptr(w), d_box, 1, self.d,
+                          float(tau), ptr(self.value), code, ptr(self.weight),
+                          ptr(self.child), self.cap, 1 + self.ranks, 1 + c,
+                          1 if propagate else 0, ns.ctypes.data,
+                          st.ctypes.data, stream_handle())
+                break
+            except RuntimeError as exc:
+                if "capacity" not in str(exc):
+                    raise
+                self._grow()
+        self.ranks += int(ns[0])
+        self.stats[c] = st
+
+    def finish(self, tau) -> OctreeField:
+        """The root from the eight box roots (the pyramid's last level in
+        numpy's order, the split rule at level 0, _kernels.pyx:58-63)."""
+        s = self.stats
+
+        def mean8(k):
+            b = [s[c][k] for c in range(8)]
+            return ((((b[0] + b[1]) + (b[2] + b[3])) + (b[4] + b[5]))
+                    + (b[6] + b[7])) / 8.0
+        mn = min(q[0] for q in s)
+        mx = max(q[1] for q in s)
+        if self.weighted:
+            wmn, wmx = min(q[3] for q in s), max(q[4] for q in s)
+            wm, wf, pl = mean8(5), mean8(6), mean8(7)
+            mean = wf / wm if wm > 0.0 else pl
+            split = self.d > 0 and (mx - mn > tau or wmn != wmx)
+        else:
+            wm = 0.0
+            mean = mean8(2)
+            split = self.d > 0 and mx - mn > tau
+        used = 1 + 8 * (1 + self.ranks) if split else 1
+        self.child[0] = 1 if split else -1
+        if split and not self.weighted:   # propagate_means: sequential sum
+            acc = 0.0
+            for v in self.value[1:9].double().tolist():
+                acc += v
+            mean = acc / 8.0
+        self.value[0] = mean
+        if self.weight is not None:
+            self.weight[0] = wm
+        from .octree import _trim
+        state = np.array([used, -1, used], dtype=np.int64)
+        return OctreeField(_trim(self.value, used), _trim(self.child, used),
+                           state, self.d,
+                           weight=None if self.weight is None
+                           else _trim(self.weight, used))
+
+
+def prepare_boxed(depths, cameras, dom, params: FusionParams):
+    """``prepare`` without any (2^d)^3 grid: the volume is processed as its
+    eight octant boxes (child 7 first, the depth-first order of the
+    reference's build, _kernels.pyx:21-77), per box every frame's TSDF
+    (octf_view_tsdf_box, with the wf / w sums of the box in frame order) and
+    its subtree of every view tree (octf_build_octree_box), then the box's
+    initial field and its subtrees of u0 and of the observed-mask tree;
+    the roots are assembled from the eight box roots' pyramid entries.  The
+    result is ``prepare``'s bit for bit (views, u0; ``seen`` as the tree
+    mesh.seen_tree(w_sum > 0) would build) with an eighth of its grid memory
+    -- BASELINE config 3's depth 11 (2048^3 cells) runs on one GPU."""
+    n = dom.resolution
+    d = n.bit_length() - 1
+    if d < 1:
+        raise ValueError("boxed preparation needs depth >= 1")
+    h = n // 2
+    from .tsdf import _camera_params
+    org = np.ascontiguousarray(np.asarray(dom.origin, dtype=np.float64))
+    views = [_BoxTree(d, True, torch.float32) for _ in depths]
+    u0 = _BoxTree(d, False, torch.float64)
+    seen = _BoxTree(d, False, torch.float64)
+    dev = device()
+    ds = [as_device(img.depth if hasattr(img, "depth") else img, torch.float32)
+          for img in depths]
+    cps = [np.ascontiguousarray(_camera_params(cam)) for cam in cameras]
+    for c in range(7, -1, -1):
+        box = np.array([((c >> 2) & 1) * h, ((c >> 1) & 1) * h, (c & 1) * h, h],
+                       dtype=np.int32)
+        wf = torch.zeros((h, h, h), dtype=torch.float64, device=dev)
+        ws = torch.zeros_like(wf)
+        f = torch.empty((h, h, h), dtype=torch.float32, device=dev)
+        w = torch.empty((h, h, h), dtype=torch.uint8, device=dev)
+        for v in range(len(ds)):
+            _lib.call("octf_view_tsdf_box", ptr(ds[v]), int(ds[v].shape[1]),
+                      int(ds[v].shape[0]), cps[v].ctypes.data, org.ctypes.data,
+                      float(dom.voxel_size), n, box.ctypes.data,
+                      float(params.delta), float(params.eta), ptr(f), ptr(w),
+                      ptr(wf), ptr(ws), stream_handle())
+            views[v].add(c, f, w, params.tau, propagate=False)
+        del f, w
+        ub = initial_field(wf, ws, params.gamma)
+        u0.add(c, ub, None, params.tau, propagate=True)
+        del ub, wf
+        seen.add(c, (ws > 0).double(), None, 0.0, propagate=True)
+        del ws
+    return ([v.finish(params.tau) for v in views], u0.finish(params.tau),
+            seen.finish(0.0))
 
 
 class FrameComm:

@@ -242,3 +242,38 @@ def test_cfg3_many_views_ell_store_end_to_end():
         del os.environ["OCTF_FULL_GATHER"]
     assert np.array_equal(a.child[:a.used], b.child[:b.used])
     assert np.array_equal(a.value[:a.used], b.value[:b.used])
+
+
+@pytest.mark.parametrize("case", ["cfg1", "cfg3", "cfg4"])
+def test_boxed_prepare_equals_dense(case):
+    """fusion.prepare_boxed (the volume as eight octant boxes, no (2^d)^3
+    grid: how BASELINE config 3 runs at depth 11) gives prepare's view
+    trees and u0 bit for bit, and the observed-mask tree of w_sum > 0."""
+    from paper_1608_07411_b200 import fusion, mesh, scenes, volume
+    if case == "cfg1":
+        sc = scenes.make_cfg1()
+        depths, cams = sc.depths, sc.cameras
+        p = fusion.FusionParams(delta=sc.delta, eta=sc.eta, lam=sc.lam)
+        dom = volume.VolumeDomain(sc.origin, sc.voxel_size, sc.resolution)
+    else:
+        sc = (scenes.make_cfg3(d_max=7, n_views=12, width=320, height=240,
+                               focal=262.5, device="cuda") if case == "cfg3"
+              else scenes.make_cfg4(d_max=7, n_frames=12, width=320,
+                                    height=240, focal=262.5, device="cuda"))
+        depths, cams = sc.depths, sc.cameras
+        p = fusion.FusionParams(**sc.params)
+        dom = volume.VolumeDomain(sc.origin, sc.voxel_size, sc.resolution)
+    views, u0, seen = fusion.prepare(depths, cams, dom, p)
+    bviews, bu0, bseen = fusion.prepare_boxed(depths, cams, dom, p)
+
+    def same(a, b):
+        ha, hb = a.to_host(), b.to_host()
+        assert list(ha.state) == list(hb.state)
+        assert np.array_equal(ha.child, hb.child)
+        assert np.array_equal(ha.value, hb.value)
+        if ha.weight is not None:
+            assert np.array_equal(ha.weight, hb.weight)
+    for a, b in zip(views, bviews):
+        same(a, b)
+    same(u0, bu0)
+    same(mesh.seen_tree(seen), bseen)

@@ -207,9 +207,15 @@ def prepare(depths, cameras, dom, params: FusionParams, *, comm=None):
 
 class _BoxTree:
     """One tree of a box-wise input stage (prepare_boxed): a growable
-    reference-layout pool filled subtree by subtree (octf_build_octree_box),
-    the enclosing root's depth-first rank count and the box roots'
-    pyramid statistics."""
+    reference-layout pool filled box subtree by box subtree
+    (octf_build_octree_box), and the top levels above the boxes assembled
+    from the box roots' pyramid entries.  Depth-first ranks (the
+    reference's slot order: the block of the r-th splitting node, child 7
+    expanded first, at slot 1 + 8r) are kept as a running count; a top node
+    is opened as if it split, and if its assembled statistics say it does
+    not, the count rolls back to its rank and its boxes' subtrees -- written
+    past what the tree keeps -- are overwritten by later subtrees or lie
+    beyond the final ``used``."""
 
     def __init__(self, d_max, weighted, dtype, cap=1 << 16):
         self.d, self.weighted, self.dtype = d_max, weighted, dtype
@@ -217,11 +223,12 @@ class _BoxTree:
         self.value = pool_empty(cap, dtype)
         self.child = pool_empty(cap, torch.int32)
         self.weight = pool_empty(cap, torch.float32) if weighted else None
-        self.ranks = 0                  # splitting nodes of the boxes so far
-        self.stats = [None] * 8
+        self.running = 0   # splitting nodes so far, in depth-first order
+        self.stack = []    # open top nodes: [slot, rank, level, stats[8]]
+        self.nsplit_root = 0
 
-    def _grow(self):
-        cap = 2 * self.cap
+    def _grow(self, need=0):
+        cap = max(2 * self.cap, need)
 
         def g(t):
             out = pool_empty(cap, t.dtype)
@@ -232,19 +239,31 @@ class _BoxTree:
             self.weight = g(self.weight)
         self.cap = cap
 
-    def add(self, c, f, w, tau, propagate):
-        """Build box c (child c of the root) from its grid f (and w)."""
-        d_box = self.d - 1
+    def _child_slot(self, c):
+        return 0 if not self.stack else 1 + 8 * self.stack[-1][1] + c
+
+    def open(self, c, level):
+        """A top node (child c of the current one; the root: c ignored)."""
+        slot = self._child_slot(c)
+        self.stack.append([slot, self.running, level, [None] * 8])
+        self.running += 1
+        if 1 + 8 * self.running > self.cap:
+            self._grow(2 + 8 * self.running)
+
+    def box(self, c, f, w, tau, propagate, level0):
+        """The subtree of box c of the current top node from its grid."""
+        d_box = self.d - level0
         ns = np.zeros(1, dtype=np.int64)
         st = np.zeros(8, dtype=np.float64)
         code = _lib.OCTF_F32 if self.dtype == torch.float32 else _lib.OCTF_F64
+        slot = self._child_slot(c)
         while True:
             try:
                 _lib.call("octf_build_octree_box", ptr(f),
                           _lib.OCTF_F32 if f.dtype == torch.float32
-                          else _lib.OCTF_F64, ptr(w), d_box, 1, self.d,
+                          else _lib.OCTF_F64, ptr(w), d_box, level0, self.d,
                           float(tau), ptr(self.value), code, ptr(self.weight),
-                          ptr(self.child), self.cap, 1 + self.ranks, 1 + c,
+                          ptr(self.child), self.cap, self.running, slot,
                           1 if propagate else 0, ns.ctypes.data,
                           st.ctypes.data, stream_handle())
                 break
@@ -252,13 +271,16 @@ class _BoxTree:
                 if "capacity" not in str(exc):
                     raise
                 self._grow()
-        self.ranks += int(ns[0])
-        self.stats[c] = st
+        self.running += int(ns[0])
+        if self.stack:
+            self.stack[-1][3][c] = st
+        return st, int(ns[0])
 
-    def finish(self, tau) -> OctreeField:
-        """The root from the eight box roots (the pyramid's last level in
-        numpy's order, the split rule at level 0, _kernels.pyx:58-63)."""
-        s = self.stats
+    def close(self, tau):
+        """Assemble the current top node from its children's statistics
+        (the pyramid's next level in numpy's order; the split rule,
+        _kernels.pyx:58-63) and write it."""
+        slot, rank, level, s = self.stack.pop()
 
         def mean8(k):
             b = [s[c][k] for c in range(8)]
@@ -266,25 +288,36 @@ class _BoxTree:
                     + (b[6] + b[7])) / 8.0
         mn = min(q[0] for q in s)
         mx = max(q[1] for q in s)
+        wmn = min(q[3] for q in s)
+        wmx = max(q[4] for q in s)
+        wm, wf, pl = mean8(5), mean8(6), mean8(7)
         if self.weighted:
-            wmn, wmx = min(q[3] for q in s), max(q[4] for q in s)
-            wm, wf, pl = mean8(5), mean8(6), mean8(7)
             mean = wf / wm if wm > 0.0 else pl
-            split = self.d > 0 and (mx - mn > tau or wmn != wmx)
+            split = level < self.d and (mx - mn > tau or wmn != wmx)
         else:
-            wm = 0.0
             mean = mean8(2)
-            split = self.d > 0 and mx - mn > tau
-        used = 1 + 8 * (1 + self.ranks) if split else 1
-        self.child[0] = 1 if split else -1
+            split = level < self.d and mx - mn > tau
+        st = np.array([mn, mx, mean, wmn, wmx, wm, wf, pl])
+        if not split:
+            self.running = rank        # drop the node and its subtrees
+        self.child[slot] = 1 + 8 * rank if split else -1
+        val = mean
         if split and not self.weighted:   # propagate_means: sequential sum
             acc = 0.0
-            for v in self.value[1:9].double().tolist():
+            for v in self.value[1 + 8 * rank:9 + 8 * rank].double().tolist():
                 acc += v
-            mean = acc / 8.0
-        self.value[0] = mean
+            val = acc / 8.0
+            st[2] = mean            # (the pyramid entry stays the mean)
+        self.value[slot] = val
         if self.weight is not None:
-            self.weight[0] = wm
+            self.weight[slot] = wm
+        if self.stack:
+            parent = self.stack[-1]
+            parent[3][(slot - 1) % 8] = st
+        return st
+
+    def finish(self) -> OctreeField:
+        used = 1 + 8 * self.running
         from .octree import _trim
         state = np.array([used, -1, used], dtype=np.int64)
         return OctreeField(_trim(self.value, used), _trim(self.child, used),
@@ -293,53 +326,70 @@ class _BoxTree:
                            else _trim(self.weight, used))
 
 
-def prepare_boxed(depths, cameras, dom, params: FusionParams):
-    """``prepare`` without any (2^d)^3 grid: the volume is processed as its
-    eight octant boxes (child 7 first, the depth-first order of the
-    reference's build, _kernels.pyx:21-77), per box every frame's TSDF
-    (octf_view_tsdf_box, with the wf / w sums of the box in frame order) and
-    its subtree of every view tree (octf_build_octree_box), then the box's
-    initial field and its subtrees of u0 and of the observed-mask tree;
-    the roots are assembled from the eight box roots' pyramid entries.  The
-    result is ``prepare``'s bit for bit (views, u0; ``seen`` as the tree
-    mesh.seen_tree(w_sum > 0) would build) with an eighth of its grid memory
-    -- BASELINE config 3's depth 11 (2048^3 cells) runs on one GPU."""
+def prepare_boxed(depths, cameras, dom, params: FusionParams, *,
+                  box_depth: int = 9):
+    """``prepare`` without any (2^d)^3 grid: the volume is processed as
+    boxes of (2^box_depth)^3 voxels in the depth-first order of the
+    reference's build (child 7 first, _kernels.pyx:21-77): per box every
+    frame's TSDF (octf_view_tsdf_box, with the box's wf / w sums in frame
+    order) and its subtree of every view tree (octf_build_octree_box), then
+    the box's initial field and its subtrees of u0 and of the observed-mask
+    tree; the levels above the boxes are assembled from the box roots'
+    pyramid entries.  The result is ``prepare``'s bit for bit (views, u0;
+    ``seen`` as the tree mesh.seen_tree(w_sum > 0) would build), with one
+    box's grids in memory -- BASELINE config 3's depth 11 (2048^3 cells)
+    runs on one GPU."""
     n = dom.resolution
     d = n.bit_length() - 1
-    if d < 1:
-        raise ValueError("boxed preparation needs depth >= 1")
-    h = n // 2
+    bd = max(0, min(box_depth, d - 1))
+    top = d - bd                 # levels assembled above the boxes (>= 1)
+    h = 1 << bd
     from .tsdf import _camera_params
     org = np.ascontiguousarray(np.asarray(dom.origin, dtype=np.float64))
     views = [_BoxTree(d, True, torch.float32) for _ in depths]
     u0 = _BoxTree(d, False, torch.float64)
     seen = _BoxTree(d, False, torch.float64)
+    trees = views + [u0, seen]
     dev = device()
     ds = [as_device(img.depth if hasattr(img, "depth") else img, torch.float32)
           for img in depths]
     cps = [np.ascontiguousarray(_camera_params(cam)) for cam in cameras]
-    for c in range(7, -1, -1):
-        box = np.array([((c >> 2) & 1) * h, ((c >> 1) & 1) * h, (c & 1) * h, h],
+    f = torch.empty((h, h, h), dtype=torch.float32, device=dev)
+    w = torch.empty((h, h, h), dtype=torch.uint8, device=dev)
+
+    def do_box(c, cell):
+        box = np.array([cell[0] * h, cell[1] * h, cell[2] * h, h],
                        dtype=np.int32)
         wf = torch.zeros((h, h, h), dtype=torch.float64, device=dev)
         ws = torch.zeros_like(wf)
-        f = torch.empty((h, h, h), dtype=torch.float32, device=dev)
-        w = torch.empty((h, h, h), dtype=torch.uint8, device=dev)
         for v in range(len(ds)):
             _lib.call("octf_view_tsdf_box", ptr(ds[v]), int(ds[v].shape[1]),
                       int(ds[v].shape[0]), cps[v].ctypes.data, org.ctypes.data,
                       float(dom.voxel_size), n, box.ctypes.data,
                       float(params.delta), float(params.eta), ptr(f), ptr(w),
                       ptr(wf), ptr(ws), stream_handle())
-            views[v].add(c, f, w, params.tau, propagate=False)
-        del f, w
+            views[v].box(c, f, w, params.tau, False, top)
         ub = initial_field(wf, ws, params.gamma)
-        u0.add(c, ub, None, params.tau, propagate=True)
-        del ub, wf
-        seen.add(c, (ws > 0).double(), None, 0.0, propagate=True)
-        del ws
-    return ([v.finish(params.tau) for v in views], u0.finish(params.tau),
-            seen.finish(0.0))
+        del wf
+        u0.box(c, ub, None, params.tau, True, top)
+        del ub
+        seen.box(c, (ws > 0).double(), None, 0.0, True, top)
+
+    def rec(level, c, cell):
+        if level == top:
+            do_box(c, cell)
+            return
+        for t in trees:
+            t.open(c, level)
+        for cc in range(7, -1, -1):
+            rec(level + 1, cc, (2 * cell[0] + ((cc >> 2) & 1),
+                                2 * cell[1] + ((cc >> 1) & 1),
+                                2 * cell[2] + (cc & 1)))
+        for t in trees:
+            t.close(0.0 if t is seen else params.tau)
+
+    rec(0, 0, (0, 0, 0))
+    return [v.finish() for v in views], u0.finish(), seen.finish()
 
 
 class FrameComm:

@@ -264,7 +264,6 @@ def test_boxed_prepare_equals_dense(case):
         p = fusion.FusionParams(**sc.params)
         dom = volume.VolumeDomain(sc.origin, sc.voxel_size, sc.resolution)
     views, u0, seen = fusion.prepare(depths, cams, dom, p)
-    bviews, bu0, bseen = fusion.prepare_boxed(depths, cams, dom, p)
 
     def same(a, b):
         ha, hb = a.to_host(), b.to_host()
@@ -273,7 +272,12 @@ def test_boxed_prepare_equals_dense(case):
         assert np.array_equal(ha.value, hb.value)
         if ha.weight is not None:
             assert np.array_equal(ha.weight, hb.weight)
-    for a, b in zip(views, bviews):
-        same(a, b)
-    same(u0, bu0)
-    same(mesh.seen_tree(seen), bseen)
+    st = mesh.seen_tree(seen)
+    d = dom.resolution.bit_length() - 1
+    for bd in (d - 1, d - 2, d - 4):   # 8, 64 and 4096 boxes
+        bviews, bu0, bseen = fusion.prepare_boxed(depths, cams, dom, p,
+                                                  box_depth=bd)
+        for a, b in zip(views, bviews):
+            same(a, b)
+        same(u0, bu0)
+        same(st, bseen)

@@ -30,6 +30,8 @@ ap.add_argument("--mesh", action="store_true",
                 help="also time densify + marching cubes of the result")
 ap.add_argument("--save-scene", default=None, help="pickle the rendered scene")
 ap.add_argument("--load-scene", default=None, help="reuse a pickled scene")
+ap.add_argument("--boxed", action="store_true",
+                help="box-wise input stage (fusion.prepare_boxed: no dense grid)")
 args = ap.parse_args()
 
 t0 = time.time()
@@ -53,9 +55,13 @@ p = fusion.FusionParams(**dict(sc.params, iterations=args.passes))
 dom = volume.VolumeDomain(sc.origin, sc.voxel_size, sc.resolution)
 torch.cuda.synchronize()
 t0 = time.time()
-views, u0, seen = fusion.prepare(sc.depths, sc.cameras, dom, p)
+if args.boxed:
+    views, u0, seen = fusion.prepare_boxed(sc.depths, sc.cameras, dom, p)
+else:
+    views, u0, seen = fusion.prepare(sc.depths, sc.cameras, dom, p)
 torch.cuda.synchronize()
 t_prep = time.time() - t0
+view_nodes = sum(v.node_count for v in views)
 
 if args.solver == "pd":
     s = fusion.PDSolver(u0, views, p, precision=args.precision)
@@ -94,10 +100,14 @@ if args.mesh:
     from paper_1608_07411_b200 import mesh, octree
     torch.cuda.synchronize()
     m0 = time.time()
-    dense = octree.densify_device(res.field)
-    torch.cuda.synchronize()
-    m1 = time.time()
-    tm = mesh.marching_cubes(dense, seen, dom)
+    if args.boxed:   # seen is a tree: the leaf-store readout
+        m1 = time.time()
+        tm = mesh.marching_cubes_tree(res.field, seen, dom)
+    else:
+        dense = octree.densify_device(res.field)
+        torch.cuda.synchronize()
+        m1 = time.time()
+        tm = mesh.marching_cubes(dense, seen, dom)
     torch.cuda.synchronize()
     m2 = time.time()
     mesh_info = {"densify_s": m1 - m0, "marching_cubes_s": m2 - m1,
@@ -117,6 +127,8 @@ out = {"workload": ("cfg3 adaptive object (BASELINE config 2)"
        "solver": args.solver,
        "render_s": t_render, "prepare_s": t_prep,
        "u0_nodes": u0.node_count, "leaves_end": leaves_end,
+       "view_nodes": view_nodes, "boxed": args.boxed,
+       "peak_gb": torch.cuda.max_memory_allocated() / 1e9,
        "median_pass_ms": ms,
        "leaf_updates_per_s": lv[-1] / (ms / 1e3),
        "leaf_kernel_ms_per_pass": prof["leaf_ms"] / max(prof["leaf_launches"], 1),

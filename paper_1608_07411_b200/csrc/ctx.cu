@@ -1,3 +1,4 @@
+#include <cstdio>
 // Solver-context structure rebuild: level lists, leaf-block list, neighbour
 // tables, per-leaf sample gather and the free-list mirror.
 //
@@ -994,6 +995,35 @@ __global__ void k_node_keys(const int32_t* __restrict__ blocks, int64_t nblk,
   }
 }
 
+// OCTF_ELL_STATS: per thread one 8-slot block of the per-slot counts
+__global__ void k_ell_stats(const int32_t* __restrict__ cnt, int64_t nt,
+                            unsigned long long* acc) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long obs = 0, blk = 0, tile = 0;
+  if (b < nt * 32) {
+    int mx = 0;
+    for (int c = 0; c < 8; ++c) {
+      obs += cnt[b * 8 + c];
+      mx = max(mx, cnt[b * 8 + c]);
+    }
+    blk = 8ull * mx;
+  }
+  // per-tile max over the tile's 32 blocks (one warp = one tile)
+  int tmx = (int)(blk / 8);
+  for (int o = 16; o > 0; o >>= 1)
+    tmx = max(tmx, __shfl_xor_sync(0xffffffffu, tmx, o));
+  if ((threadIdx.x & 31) == 0) tile = 256ull * tmx;
+  for (int o = 16; o > 0; o >>= 1) {
+    obs += __shfl_xor_sync(0xffffffffu, obs, o);
+    blk += __shfl_xor_sync(0xffffffffu, blk, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(acc, obs);
+    atomicAdd(acc + 1, tile);
+    atomicAdd(acc + 2, blk);
+  }
+}
+
 __global__ void k_walk_free(const int32_t* __restrict__ child, int64_t head,
                             int64_t nmax, int32_t* chain, int32_t* count) {
   // single thread: follow the free list links (child[b] of a free block)
@@ -1554,7 +1584,10 @@ ViewSet ctx_views(const Ctx& c) {
 template <typename Fn>
 static void view_maps(Ctx& c, cudaStream_t st, Fn fn) {
   const int nv = c.nviews;
-  const int chunk = nv < 32 ? nv : 32;
+  // views per chunk: 32, fewer when the maps would pass ~16 GB (a pool of
+  // 7e8 slots at BASELINE config 3's depth 11)
+  int chunk = nv < 32 ? nv : 32;
+  while (chunk > 1 && (double)chunk * c.cap * 4.0 > 16e9) chunk /= 2;
   int32_t* vm = c.vmap.ensure((size_t)chunk * c.cap);
   for (int v0 = 0; v0 < nv; v0 += chunk) {
     const int nc = nv - v0 < chunk ? nv - v0 : chunk;
@@ -1593,6 +1626,21 @@ void ctx_gather_ell(Ctx& c, cudaStream_t st) {
                                                 c.nlb, ctx_views(c), v0, nc,
                                                 c.cap, vm, cnt);
   });
+  if (const char* es = std::getenv("OCTF_ELL_STATS"); es && es[0] == '1') {
+    // diagnosis: observed samples, and the store sizes per-tile (this
+    // layout) / per-block row counts would need
+    unsigned long long* acc = reinterpret_cast<unsigned long long*>(
+        c.dscalar.ensure(4));
+    OCTF_CUDA(cudaMemsetAsync(acc, 0, 4 * sizeof(double), st));
+    k_ell_stats<<<grid_for(nt * 32), kThreads, 0, st>>>(cnt, nt, acc);
+    unsigned long long h[3] = {0, 0, 0};
+    OCTF_CUDA(cudaMemcpyAsync(h, acc, sizeof(h), cudaMemcpyDeviceToHost, st));
+    OCTF_CUDA(cudaStreamSynchronize(st));
+    fprintf(stderr,
+            "ell_stats: leaves %lld, observed samples %llu, per-tile rows "
+            "%llu entries, per-block rows %llu entries\n",
+            (long long)c.nleaves, h[0], h[1], h[2]);
+  }
   int64_t* rowsz = reinterpret_cast<int64_t*>(c.sort_k64.ensure(nt + 1));
   c.tileK.ensure(nt + 1);
   c.tileOff.ensure(nt + 1);

@@ -320,10 +320,12 @@ class _BoxTree:
         used = 1 + 8 * self.running
         from .octree import _trim
         state = np.array([used, -1, used], dtype=np.int64)
-        return OctreeField(_trim(self.value, used), _trim(self.child, used),
-                           state, self.d,
-                           weight=None if self.weight is None
-                           else _trim(self.weight, used))
+        out = OctreeField(_trim(self.value, used), _trim(self.child, used),
+                          state, self.d,
+                          weight=None if self.weight is None
+                          else _trim(self.weight, used))
+        self.value = self.child = self.weight = None   # the grown pools
+        return out
 
 
 def prepare_boxed(depths, cameras, dom, params: FusionParams, *,
@@ -389,6 +391,7 @@ def prepare_boxed(depths, cameras, dom, params: FusionParams, *,
             t.close(0.0 if t is seen else params.tau)
 
     rec(0, 0, (0, 0, 0))
+    del rec          # (the recursive closure is a reference cycle)
     return [v.finish() for v in views], u0.finish(), seen.finish()
 
 

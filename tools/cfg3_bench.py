@@ -62,6 +62,12 @@ else:
 torch.cuda.synchronize()
 t_prep = time.time() - t0
 view_nodes = sum(v.node_count for v in views)
+print(json.dumps({"after_prepare": {
+    "view_nodes": view_nodes, "u0_nodes": u0.node_count,
+    "torch_allocated_gb": torch.cuda.memory_allocated() / 1e9,
+    "torch_reserved_gb": torch.cuda.memory_reserved() / 1e9,
+    "device_free_gb": torch.cuda.mem_get_info()[0] / 1e9}}), file=sys.stderr,
+    flush=True)
 
 if args.solver == "pd":
     s = fusion.PDSolver(u0, views, p, precision=args.precision)
@@ -121,7 +127,9 @@ ms = sorted(q["ms"] for q in steady)[len(steady) // 2]
 lv = [(7 * q["nodes"] + 1) // 8 for q in passes]
 out = {"workload": ("cfg3 adaptive object (BASELINE config 2)"
                     if args.config == "cfg3" else
-                    "cfg4 room (BASELINE config 3) at reduced depth"),
+                    ("cfg4 room (BASELINE config 3) at its configured depth 11"
+                     if args.depth >= 11 else
+                     "cfg4 room (BASELINE config 3) at reduced depth")),
        "depth": args.depth, "views": len(sc.depths),
        "precision": args.precision,
        "solver": args.solver,

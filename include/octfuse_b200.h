@@ -379,6 +379,37 @@ int octf_build_octree_box(const void *f, int f_dtype, const uint8_t *w,
 int octf_initial_field(const double *wf_sum, const double *w_sum, double gamma,
                        int64_t n, double *u, void *stream);
 
+/* Scene generators on the device (the reference
+ * renders its spheres analytically, synth.py:80-109): camera-frame depth z
+ * of every pixel ray's first hit, 0 on a miss, by sphere tracing (steps
+ * sd / lipschitz until sd < eps, then 40 bisections) in f64 -- the array
+ * program of the package's scenes.py, operation for operation.  cam as in
+ * octf_view_tsdf (host); z = height x width doubles (device).
+ * Blob: sd(p) = |p - centre| - (radius + amp * noise(p)), noise = n_oct
+ * octaves of lattice value noise (lattices[o] = n_o^3 doubles on the
+ * device, frequency base_freq * 2^o, amplitude 2^-o). */
+int octf_trace_blob(const double *cam, int width, int height,
+                    const double *centre, double radius, double amp,
+                    double base_freq, const double *const *lattices,
+                    const int32_t *lat_n, int n_oct, double lipschitz,
+                    double t_max, int steps, double eps, double *z,
+                    void *stream);
+
+/* Room: union of n_box axis-aligned boxes {centre, half extents}, n_sph
+ * spheres {centre, radius} (objects = the boxes then the spheres, device)
+ * and the six walls of the size^3 cube seen from inside. */
+int octf_trace_room(const double *cam, int width, int height,
+                    const double *objects, int n_box, int n_sph, double size,
+                    double lipschitz, double t_max, int steps, double eps,
+                    double *z, void *stream);
+
+/* mesh.py:162-167 vertex_diff -- dist[i] = Euclidean distance from vertex
+ * a[i] to the nearest vertex of b (what the reference gets from scipy's k-d
+ * tree, bit for bit); a = na x 3, b = nb x 3 doubles, dist = na doubles, all
+ * on the device.  Call it both ways for the symmetric statistics. */
+int octf_nearest_vertex(const double *a, int64_t na, const double *b,
+                        int64_t nb, double *dist, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -81,6 +81,11 @@ _SIGS = {
     "octf_view_tsdf": ([P, I32, I32, P, P, DBL, I32, DBL, DBL, P, P, P, P, P],
                        I32),
     "octf_initial_field": ([P, P, DBL, I64, P, P], I32),
+    "octf_trace_blob": ([P, I32, I32, P, DBL, DBL, DBL, P, P, I32, DBL, DBL,
+                         I32, DBL, P, P], I32),
+    "octf_nearest_vertex": ([P, I64, P, I64, P, P], I32),
+    "octf_trace_room": ([P, I32, I32, P, I32, I32, DBL, DBL, DBL, I32, DBL, P,
+                         P], I32),
 }
 
 _lib = None

@@ -5,6 +5,8 @@
 
 #include "../../include/octfuse_b200.h"
 #include "octf_build.h"
+#include "octf_scenes.h"
+#include "octf_mesh_diff.h"
 #include "octf_ctx.h"
 
 struct octf_ctx {
@@ -875,6 +877,52 @@ int octf_initial_field(const double* wf_sum, const double* w_sum, double gamma,
   return guard([&] {
     need_device();
     octf::initial_field(wf_sum, w_sum, gamma, n, u, S(stream));
+  });
+}
+
+int octf_trace_blob(const double* cam, int width, int height,
+                    const double* centre, double radius, double amp,
+                    double base_freq, const double* const* lattices,
+                    const int32_t* lat_n, int n_oct, double lipschitz,
+                    double t_max, int steps, double eps, double* z,
+                    void* stream) {
+  return guard([&] {
+    if (!cam || !centre || !z || (n_oct > 0 && (!lattices || !lat_n)))
+      throw octf::Error(octf::kEArg, "null argument");
+    if (width < 1 || height < 1 || steps < 0 || !(lipschitz > 0.0))
+      throw octf::Error(octf::kEArg, "bad image size, steps or lipschitz");
+    need_device();
+    int n[octf::kMaxOctaves] = {};
+    for (int o = 0; o < n_oct && o < octf::kMaxOctaves; ++o) n[o] = lat_n[o];
+    octf::trace_blob(cam, width, height, centre, radius, amp, base_freq,
+                     lattices, n, n_oct, lipschitz, t_max, steps, eps, z,
+                     S(stream));
+  });
+}
+
+int octf_trace_room(const double* cam, int width, int height,
+                    const double* objects, int n_box, int n_sph, double size,
+                    double lipschitz, double t_max, int steps, double eps,
+                    double* z, void* stream) {
+  return guard([&] {
+    if (!cam || !z || (!objects && n_box + n_sph > 0))
+      throw octf::Error(octf::kEArg, "null argument");
+    if (width < 1 || height < 1 || steps < 0 || !(lipschitz > 0.0))
+      throw octf::Error(octf::kEArg, "bad image size, steps or lipschitz");
+    need_device();
+    octf::trace_room(cam, width, height, objects, n_box, n_sph, size,
+                     lipschitz, t_max, steps, eps, z, S(stream));
+  });
+}
+
+int octf_nearest_vertex(const double* a, int64_t na, const double* b,
+                        int64_t nb, double* dist, void* stream) {
+  return guard([&] {
+    if (na < 1 || nb < 1)
+      throw octf::Error(octf::kEArg, "cannot compare empty meshes");
+    if (!a || !b || !dist) throw octf::Error(octf::kEArg, "null argument");
+    need_device();
+    octf::nearest_vertex(a, na, b, nb, dist, S(stream));
   });
 }
 

@@ -27,7 +27,8 @@ from . import _lib
 from ._device import as_device, device, ptr, stream_handle
 
 __all__ = ["TriMesh", "extract_zero_surface", "marching_cubes", "case_tables",
-           "tree_zero_surface", "marching_cubes_tree", "seen_tree"]
+           "tree_zero_surface", "marching_cubes_tree", "seen_tree", "MeshDiff",
+           "nearest_vertex_distances", "vertex_diff"]
 
 # corner c of a cube sits at offset (c>>2 & 1, c>>1 & 1, c & 1) (x, y, z),
 # the octree child numbering; edges 0-3 run along x, 4-7 along y, 8-11
@@ -247,3 +248,51 @@ def marching_cubes(values, seen, dom) -> TriMesh:
     if tuple(values.shape) != (dom.resolution,) * 3:
         raise ValueError("grid does not match the domain resolution")
     return TriMesh(*_extract(values, seen, dom.origin, dom.voxel_size, True))
+
+
+class MeshDiff(NamedTuple):
+    """Nearest-vertex distances of two meshes, each way (numpy float64), with
+    the reference's summary statistics over both directions together
+    (mesh.py:143-159)."""
+
+    d_ab: np.ndarray
+    d_ba: np.ndarray
+
+    def _both(self) -> np.ndarray:
+        return np.concatenate([self.d_ab, self.d_ba])
+
+    @property
+    def mean(self) -> float:
+        return float(self._both().mean())
+
+    @property
+    def std(self) -> float:
+        return float(self._both().std())
+
+    @property
+    def max(self) -> float:
+        return float(self._both().max())
+
+
+def nearest_vertex_distances(a, b):
+    """Distance from every row of ``a`` (V_a, 3) to its nearest row of ``b``
+    on the device (octf_nearest_vertex: uniform-grid search, the k-d tree's
+    f64 arithmetic).  Returns a CUDA float64 tensor."""
+    va = as_device(a, torch.float64).contiguous()
+    vb = as_device(b, torch.float64).contiguous()
+    if va.dim() != 2 or vb.dim() != 2 or va.shape[1] != 3 or vb.shape[1] != 3:
+        raise ValueError("vertices must be (V, 3) arrays")
+    if va.shape[0] == 0 or vb.shape[0] == 0:
+        raise ValueError("cannot compare empty meshes")
+    out = torch.empty(va.shape[0], dtype=torch.float64, device=device())
+    _lib.call("octf_nearest_vertex", ptr(va), va.shape[0], ptr(vb),
+              vb.shape[0], ptr(out), stream_handle())
+    return out
+
+
+def vertex_diff(a: TriMesh, b: TriMesh) -> MeshDiff:
+    """Symmetric nearest-vertex comparison of two meshes (mesh.py:162-167)
+    computed on the GPU."""
+    return MeshDiff(
+        nearest_vertex_distances(a.vertices, b.vertices).cpu().numpy(),
+        nearest_vertex_distances(b.vertices, a.vertices).cpu().numpy())

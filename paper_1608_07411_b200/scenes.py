@@ -22,7 +22,8 @@ import numpy as np
 __all__ = ["look_at", "PinholeCamera", "sphere_depth", "Cfg1Scene",
            "make_cfg1", "torus_sdf", "make_cfg2_samples", "cfg5_tree",
            "cfg5_inputs", "DepthScene", "value_noise", "sphere_trace",
-           "make_cfg3", "make_cfg4"]
+           "trace_blob", "trace_room", "room_objects_array", "make_cfg3",
+           "make_cfg4"]
 
 
 def look_at(position, target, up=(0.0, 0.0, 1.0)) -> np.ndarray:
@@ -407,6 +408,73 @@ def sphere_trace(sdf, cam: PinholeCamera, *, lipschitz: float, t_max: float,
     return z.reshape(H, W)
 
 
+def _is_cuda(device) -> bool:
+    import torch
+    return torch.device(device).type == "cuda"
+
+
+def _cam_params(cam: PinholeCamera) -> np.ndarray:
+    return np.ascontiguousarray(np.concatenate([
+        [cam.fx, cam.fy, cam.cx, cam.cy],
+        np.asarray(cam.rotation, dtype=np.float64).ravel(),
+        np.asarray(cam.translation, dtype=np.float64).ravel()]))
+
+
+def trace_blob(cam: PinholeCamera, tables, *, centre=(0.5, 0.5, 0.5),
+               radius: float = 0.35, amp: float = 0.03,
+               base_freq: float = 4.0, lipschitz: float, t_max: float,
+               steps: int = 400, eps: float = 1e-7):
+    """``sphere_trace`` of the noisy blob as one CUDA kernel, a thread per
+    pixel ray (``octf_trace_blob``, csrc/scenes.cu): the same f64 operations
+    in the same order, so the map equals the array program's bit for bit
+    (``tests/test_gpu_cfg34.py::test_trace_kernels_match_array_program``)."""
+    import torch
+    from . import _lib
+    from ._device import ptr, stream_handle
+    z = torch.empty((cam.height, cam.width), dtype=torch.float64,
+                    device=tables[0].device)
+    tabs = [t.contiguous() for t in tables]
+    lat = _lib.ptr_table([ptr(t) for t in tabs])
+    lat_n = np.array([t.shape[0] for t in tabs], dtype=np.int32)
+    cp = _cam_params(cam)
+    c = np.ascontiguousarray(np.asarray(centre, dtype=np.float64))
+    _lib.call("octf_trace_blob", cp.ctypes.data, cam.width, cam.height,
+              c.ctypes.data, float(radius), float(amp), float(base_freq), lat,
+              lat_n.ctypes.data, len(tabs), float(lipschitz), float(t_max),
+              int(steps), float(eps), ptr(z), stream_handle())
+    return z
+
+
+def trace_room(cam: PinholeCamera, objects, n_box: int, n_sph: int, *,
+               size: float = 4.0, lipschitz: float = 1.0, t_max: float,
+               steps: int = 400, eps: float = 1e-7):
+    """``sphere_trace`` of the room (``octf_trace_room``): ``objects`` is the
+    device array of ``room_objects_array``; the object list is staged in
+    shared memory once per CTA."""
+    import torch
+    from . import _lib
+    from ._device import ptr, stream_handle
+    z = torch.empty((cam.height, cam.width), dtype=torch.float64,
+                    device=objects.device)
+    cp = _cam_params(cam)
+    _lib.call("octf_trace_room", cp.ctypes.data, cam.width, cam.height,
+              ptr(objects), int(n_box), int(n_sph), float(size),
+              float(lipschitz), float(t_max), int(steps), float(eps), ptr(z),
+              stream_handle())
+    return z
+
+
+def room_objects_array(objs, device):
+    """Boxes {centre, half extents} then spheres {centre, radius} as one flat
+    f64 device array, and the two counts."""
+    import torch
+    boxes = [np.concatenate([c, h]) for k, c, h in objs if k == "box"]
+    sph = [np.concatenate([c, [r]]) for k, c, r in objs if k == "sphere"]
+    flat = np.concatenate([np.ravel(boxes), np.ravel(sph)]).astype(np.float64)
+    return (torch.tensor(flat, dtype=torch.float64, device=device),
+            len(boxes), len(sph))
+
+
 def fibonacci_hemisphere(n: int) -> np.ndarray:
     """n unit directions with z > 0 on a Fibonacci spiral (assumed viewpoint
     layout of config 2's 'hemisphere of viewpoints')."""
@@ -453,7 +521,10 @@ def make_cfg3(d_max: int = 9, n_views: int = 64, width: int = 640,
         pos = centre + 1.2 * dvec
         cam = PinholeCamera(focal, focal, (width - 1) / 2.0, (height - 1) / 2.0,
                             width, height, look_at(pos, centre), pos)
-        z = sphere_trace(sdf, cam, lipschitz=1.7, t_max=3.0, device=device)
+        if _is_cuda(device):
+            z = trace_blob(cam, tables, lipschitz=1.7, t_max=3.0)
+        else:   # golden generation on the CPU: the array program
+            z = sphere_trace(sdf, cam, lipschitz=1.7, t_max=3.0, device=device)
         cams.append(cam)
         depths.append(_add_noise(z.cpu().numpy(), 2e-3, rng))
     n = 1 << d_max
@@ -551,6 +622,8 @@ def make_cfg4(d_max: int = 11, n_frames: int = 300, width: int = 640,
     pos, tan = _catmull_rom(np.array(way), n_frames)
     cams, depths = [], []
     given = depths_in
+    if given is None and _is_cuda(device):
+        objs_dev, n_box, n_sph = room_objects_array(objs, device)
     noise = np.random.default_rng(seed + 2)
     for k in range(n_frames):
         cam = PinholeCamera(focal, focal, (width - 1) / 2.0, (height - 1) / 2.0,
@@ -558,8 +631,13 @@ def make_cfg4(d_max: int = 11, n_frames: int = 300, width: int = 640,
         cams.append(cam)
         if given is not None:
             continue
-        z = sphere_trace(sdf, cam, lipschitz=1.0, t_max=8.0, device=device,
-                         eps=1e-6).cpu().numpy()
+        if _is_cuda(device):
+            z = trace_room(cam, objs_dev, n_box, n_sph, size=size,
+                           lipschitz=1.0, t_max=8.0, eps=1e-6)
+        else:   # golden generation on the CPU: the array program
+            z = sphere_trace(sdf, cam, lipschitz=1.0, t_max=8.0,
+                             device=device, eps=1e-6)
+        z = z.cpu().numpy()
         depths.append(_add_noise(z, 0.0015 * z * z, noise))
     if given is not None:
         depths = [np.asarray(d, dtype=np.float32) for d in given]

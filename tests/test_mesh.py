@@ -193,3 +193,65 @@ def test_tree_readout_cfg3_reduced_equals_dense():
     assert m.faces.shape[0] > 1000
     assert np.array_equal(m.vertices, mt.vertices)
     assert np.array_equal(m.faces, mt.faces)
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")
+def test_vertex_diff_equals_kdtree():
+    """vertex_diff on the GPU against the reference's own method
+    (mesh.py:162-167: scipy's k-d tree, queried here) -- the distances are
+    equal bit for bit: surface-like sets, a volumetric cloud, far-apart
+    sets, duplicates and a single target vertex."""
+    from scipy.spatial import cKDTree
+    from paper_1608_07411_b200 import mesh
+    rng = np.random.default_rng(0)
+
+    def sphere(n, r, c):
+        v = rng.normal(size=(n, 3))
+        return c + r * v / np.linalg.norm(v, axis=1, keepdims=True)
+
+    cases = [
+        (sphere(20000, 0.3, 0.5), sphere(30000, 0.31, 0.5)),
+        (rng.uniform(0, 1, (5000, 3)), rng.uniform(0, 1, (7000, 3))),
+        (sphere(3000, 0.1, 0.0), sphere(3000, 0.1, 5.0)),      # disjoint
+        (rng.uniform(0, 1, (100, 3)), np.full((50, 3), 0.25)),  # duplicates
+        (rng.uniform(-2, 2, (1000, 3)), np.array([[0.1, 0.2, 0.3]])),
+        (rng.uniform(0, 1, (4000, 3)) * [1.0, 1.0, 0.0],        # planar
+         rng.uniform(0, 1, (4000, 3)) * [1.0, 1.0, 0.0]),
+    ]
+    for a, b in cases:
+        d = mesh.vertex_diff(mesh.TriMesh(a, None), mesh.TriMesh(b, None))
+        want_ab = cKDTree(b).query(a)[0]
+        want_ba = cKDTree(a).query(b)[0]
+        assert np.array_equal(d.d_ab, want_ab)
+        assert np.array_equal(d.d_ba, want_ba)
+        both = np.concatenate([want_ab, want_ba])
+        assert d.mean == float(both.mean()) and d.max == float(both.max())
+        assert d.std == float(both.std())
+    with pytest.raises(ValueError):
+        mesh.vertex_diff(mesh.TriMesh(np.zeros((0, 3)), None),
+                         mesh.TriMesh(np.zeros((4, 3)), None))
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")
+def test_vertex_diff_of_fused_meshes():
+    """The comparison the reference's acceptance run makes: the tree
+    solver's mesh against the mesh of the initial field (cfg1), all on the
+    device, equal to the k-d tree's numbers."""
+    from scipy.spatial import cKDTree
+    from paper_1608_07411_b200 import fusion, mesh, volume
+    from tests.goldens import cfg1_inputs
+    depths, cams, origin, vox, n, p = cfg1_inputs()
+    dom = volume.VolumeDomain(origin, vox, n)
+    fp = fusion.FusionParams(delta=p.delta, eta=p.eta, lam=p.lam,
+                             iterations=10)
+    views, u0, seen = fusion.prepare(depths, cams, dom, fp)
+    st = mesh.seen_tree(seen)
+    m0 = mesh.marching_cubes_tree(u0, st, dom)
+    res = fusion.fuse(u0, views, fp)
+    m1 = mesh.marching_cubes_tree(res.field, st, dom)
+    d = mesh.vertex_diff(m0, m1)
+    assert np.array_equal(d.d_ab, cKDTree(m1.vertices).query(m0.vertices)[0])
+    assert np.array_equal(d.d_ba, cKDTree(m0.vertices).query(m1.vertices)[0])
+    assert 0.0 < d.max < 8 * vox

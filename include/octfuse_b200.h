@@ -410,6 +410,13 @@ int octf_trace_room(const double *cam, int width, int height,
 int octf_nearest_vertex(const double *a, int64_t na, const double *b,
                         int64_t nb, double *dist, void *stream);
 
+/* octree.py:148-166 locate, batched: for each of n cells (x, y, z) at
+ * `level` (int32 triples, device) the deepest node on the root path of the
+ * cell and that node's level (device outputs). */
+int octf_locate(const int32_t *child, int d_max, int level,
+                const int32_t *cells, int64_t n, int32_t *node,
+                int32_t *node_level, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

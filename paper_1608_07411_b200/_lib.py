@@ -83,6 +83,7 @@ _SIGS = {
     "octf_initial_field": ([P, P, DBL, I64, P, P], I32),
     "octf_trace_blob": ([P, I32, I32, P, DBL, DBL, DBL, P, P, I32, DBL, DBL,
                          I32, DBL, P, P], I32),
+    "octf_locate": ([P, I32, I32, P, I64, P, P, P], I32),
     "octf_nearest_vertex": ([P, I64, P, I64, P, P], I32),
     "octf_trace_room": ([P, I32, I32, P, I32, I32, DBL, DBL, DBL, I32, DBL, P,
                          P], I32),

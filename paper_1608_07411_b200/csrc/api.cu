@@ -926,4 +926,19 @@ int octf_nearest_vertex(const double* a, int64_t na, const double* b,
   });
 }
 
+int octf_locate(const int32_t* child, int d_max, int level,
+                const int32_t* cells, int64_t n, int32_t* node,
+                int32_t* node_level, void* stream) {
+  return guard([&] {
+    if (d_max < 0 || d_max > OCTF_MAX_DEPTH)
+      throw octf::Error(octf::kEDepth, "tree depth out of range");
+    if (level < 0 || level > d_max)
+      throw octf::Error(octf::kEArg, "level outside [0, d_max]");
+    if (n < 0 || (n > 0 && (!child || !cells || !node || !node_level)))
+      throw octf::Error(octf::kEArg, "null argument");
+    need_device();
+    octf::locate(child, level, cells, n, node, node_level, S(stream));
+  });
+}
+
 }  // extern "C"

@@ -476,4 +476,23 @@ void densify(int dtype, const void* value, const int32_t* child, int d_max,
   OCTF_CUDA(cudaGetLastError());
 }
 
+// octree.py:148-166 locate for a batch of cells of one level
+__global__ void k_locate(const int32_t* __restrict__ child, int level,
+                         const int32_t* __restrict__ cells, int64_t n,
+                         int32_t* __restrict__ node, int32_t* __restrict__ lvl) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int l = 0;
+  node[i] = descend(child, level, cells[3 * i], cells[3 * i + 1],
+                    cells[3 * i + 2], &l);
+  lvl[i] = l;
+}
+
+void locate(const int32_t* child, int level, const int32_t* cells, int64_t n,
+            int32_t* node, int32_t* lvl, cudaStream_t st) {
+  if (n <= 0) return;
+  k_locate<<<nblk(n), kB, 0, st>>>(child, level, cells, n, node, lvl);
+  OCTF_CUDA(cudaGetLastError());
+}
+
 }  // namespace octf

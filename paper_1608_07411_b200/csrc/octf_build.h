@@ -45,4 +45,7 @@ void build_tree(const BuildIn& in, void* value, int dtype, float* weight,
 void densify(int dtype, const void* value, const int32_t* child, int d_max,
              double* out, cudaStream_t st);
 
+void locate(const int32_t* child, int level, const int32_t* cells, int64_t n,
+            int32_t* node, int32_t* lvl, cudaStream_t st);
+
 }  // namespace octf

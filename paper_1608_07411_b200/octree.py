@@ -162,15 +162,21 @@ class OctreeField:
         m = 1 << level
         if not (0 <= x < m and 0 <= y < m and 0 <= z < m):
             raise ValueError(f"cell {cell!r} invalid at level {level}")
-        node, lvl = 0, 0
-        while lvl < level:
-            b = int(self.child[node].item())
-            if b < 0:
-                break
-            s = level - lvl - 1
-            node = b + ((((x >> s) & 1) << 2) | (((y >> s) & 1) << 1)
-                        | ((z >> s) & 1))
-            lvl += 1
+        node, lvl = self.locate_many(level, [(x, y, z)])
+        pair = torch.stack([node, lvl]).cpu()      # one device-to-host read
+        return int(pair[0, 0]), int(pair[1, 0])
+
+    def locate_many(self, level: int, cells):
+        """``locate`` for (n, 3) cells of one level on the device
+        (octf_locate): CUDA int32 tensors (nodes, levels)."""
+        if not 0 <= level <= self.d_max:
+            raise ValueError(f"level {level} outside [0, {self.d_max}]")
+        c = as_device(cells, torch.int32).reshape(-1, 3).contiguous()
+        n = c.shape[0]
+        node = torch.empty(n, dtype=torch.int32, device=device())
+        lvl = torch.empty(n, dtype=torch.int32, device=device())
+        _lib.call("octf_locate", ptr(self.child), self.d_max, int(level),
+                  ptr(c), n, ptr(node), ptr(lvl), stream_handle())
         return node, lvl
 
     def leaves(self) -> Iterator[tuple[int, int, int, int, int]]:

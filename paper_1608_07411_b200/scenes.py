@@ -369,8 +369,11 @@ def sphere_trace(sdf, cam: PinholeCamera, *, lipschitz: float, t_max: float,
     R = np.asarray(cam.rotation, dtype=np.float64)
     dr = dirs.reshape(-1, 3)
     # world directions R @ dir as separate IEEE ops (no matmul / reduction
-    # kernels, whose order differs between devices): CPU and GPU traces are
-    # bit-identical, so the golden fixtures made here hold on the GPU box
+    # kernels, whose order differs between devices and runs): the maps are
+    # reproducible on any GPU, and the CUDA kernels (trace_blob / trace_room)
+    # give the same bits.  (torch's CPU f64 sqrt is not correctly rounded, so
+    # a CPU trace may differ in the last place; the golden fixtures' depth
+    # maps were dumped from the device, tools/dump_depths.py.)
     d = torch.stack([(dr[:, 0] * float(R[j, 0]) + dr[:, 1] * float(R[j, 1]))
                      + dr[:, 2] * float(R[j, 2]) for j in range(3)], 1)
     o = torch.as_tensor(cam.translation, dtype=torch.float64, device=device)
@@ -523,7 +526,7 @@ def make_cfg3(d_max: int = 9, n_views: int = 64, width: int = 640,
                             width, height, look_at(pos, centre), pos)
         if _is_cuda(device):
             z = trace_blob(cam, tables, lipschitz=1.7, t_max=3.0)
-        else:   # golden generation on the CPU: the array program
+        else:   # no device: the array program
             z = sphere_trace(sdf, cam, lipschitz=1.7, t_max=3.0, device=device)
         cams.append(cam)
         depths.append(_add_noise(z.cpu().numpy(), 2e-3, rng))
@@ -634,7 +637,7 @@ def make_cfg4(d_max: int = 11, n_frames: int = 300, width: int = 640,
         if _is_cuda(device):
             z = trace_room(cam, objs_dev, n_box, n_sph, size=size,
                            lipschitz=1.0, t_max=8.0, eps=1e-6)
-        else:   # golden generation on the CPU: the array program
+        else:   # no device: the array program
             z = sphere_trace(sdf, cam, lipschitz=1.0, t_max=8.0,
                              device=device, eps=1e-6)
         z = z.cpu().numpy()

@@ -285,18 +285,20 @@ def test_boxed_prepare_equals_dense(case):
 
 def test_trace_kernels_match_array_program():
     """The ray-marching kernels (octf_trace_blob / octf_trace_room) give the
-    depth maps of the array program in scenes.py -- run here on the CPU, as
-    the golden fixtures' generator did -- bit for bit: hits, misses and the
-    bisected depths."""
+    depth maps of the array program in scenes.py (torch ops on the device,
+    which produced the maps the golden fixtures' reference runs consumed) bit
+    for bit: hits, misses and the bisected depths.  (On the CPU torch's
+    vectorised f64 sqrt is not correctly rounded, so the comparison is made
+    on the device, where it is.)"""
     from paper_1608_07411_b200 import scenes
     # blob: an off-centre camera so part of the image misses
-    tabs_cpu = [scenes._lattice(3 * 7 + o, 4 * (1 << o) + 2, "cpu")
-                for o in range(3)]
-    c = torch.tensor([0.5, 0.5, 0.5], dtype=torch.float64)
+    tabs = [scenes._lattice(3 * 7 + o, 4 * (1 << o) + 2, "cuda")
+            for o in range(3)]
+    c = torch.tensor([0.5, 0.5, 0.5], dtype=torch.float64, device="cuda")
 
     def blob(p):
         return scenes._norm3(p - c) - (0.35 + 0.03 * scenes.value_noise(
-            p, tabs_cpu))
+            p, tabs))
 
     centre = np.array([0.5, 0.5, 0.5])
     for k, dvec in enumerate(scenes.fibonacci_hemisphere(5)[::2]):
@@ -304,26 +306,26 @@ def test_trace_kernels_match_array_program():
         cam = scenes.PinholeCamera(80.0, 80.0, 47.5, 31.5, 96, 64,
                                    scenes.look_at(pos, centre + 0.2 * k), pos)
         want = scenes.sphere_trace(blob, cam, lipschitz=1.7, t_max=3.0,
-                                   device="cpu").numpy()
-        got = scenes.trace_blob(cam, [t.cuda() for t in tabs_cpu],
-                                lipschitz=1.7, t_max=3.0).cpu().numpy()
+                                   device="cuda").cpu().numpy()
+        got = scenes.trace_blob(cam, tabs, lipschitz=1.7,
+                                t_max=3.0).cpu().numpy()
         assert (want > 0).any() and (want == 0).any()
         assert np.array_equal(got, want)
     # room: boxes, spheres and walls
     objs = scenes._room_objects(5, 40, 4.0)
-    room = scenes.room_sdf_fn(objs, "cpu", 4.0)
+    room = scenes.room_sdf_fn(objs, "cuda", 4.0)
     arr, nb, ns = scenes.room_objects_array(objs, "cuda")
     rng = np.random.default_rng(1)
     done = 0
     while done < 3:
         pos = rng.uniform(0.4, 3.6, 3)
-        if float(room(torch.tensor(pos[None]))[0]) < 0.2:
+        if float(room(torch.tensor(pos[None], device="cuda"))[0]) < 0.2:
             continue
         cam = scenes.PinholeCamera(70.0, 70.0, 47.5, 31.5, 96, 64,
                                    scenes.look_at(pos, rng.uniform(0, 4, 3)),
                                    pos)
         want = scenes.sphere_trace(room, cam, lipschitz=1.0, t_max=8.0,
-                                   device="cpu", eps=1e-6).numpy()
+                                   device="cuda", eps=1e-6).cpu().numpy()
         got = scenes.trace_room(cam, arr, nb, ns, size=4.0, lipschitz=1.0,
                                 t_max=8.0, eps=1e-6).cpu().numpy()
         assert (want > 0).any()

@@ -543,6 +543,36 @@ class TestNodeOrder:
                                       2 * cz + (c & 1)))
             assert got == want
 
+    def test_locate_matches_reference_descent(self):
+        """OctreeField.locate / locate_many (octf_locate) against the
+        reference's descent (octree.py:148-166) for every cell of a level and
+        at random levels; argument checks as the reference's."""
+        f = self._pools()[-1]
+        h = f.to_host()
+
+        def ref(level, x, y, z):
+            node, lvl = 0, 0
+            while lvl < level and h.child[node] >= 0:
+                s = level - lvl - 1
+                node = int(h.child[node]) + ((((x >> s) & 1) << 2)
+                                             | (((y >> s) & 1) << 1)
+                                             | ((z >> s) & 1))
+                lvl += 1
+            return node, lvl
+        rng = np.random.default_rng(0)
+        for level in (0, 1, 3, f.d_max):
+            m = 1 << level
+            cells = rng.integers(0, m, (500, 3))
+            node, lvl = f.locate_many(level, cells)
+            got = list(zip(node.cpu().tolist(), lvl.cpu().tolist()))
+            assert got == [ref(level, *c) for c in cells.tolist()]
+        assert f.locate(f.d_max, (5, 9, 33)) == ref(f.d_max, 5, 9, 33)
+        assert f.locate(0, (0, 0, 0)) == (0, 0)
+        with pytest.raises(ValueError):
+            f.locate(f.d_max + 1, (0, 0, 0))
+        with pytest.raises(ValueError):
+            f.locate(2, (4, 0, 0))
+
     def test_serialize_matches_reference_lines(self):
         from paper_1608_07411_b200 import octree
         for f in self._pools():

@@ -76,7 +76,7 @@ __device__ double value_noise(const BlobScene& s, const double p[3]) {
     total += amp;
     amp *= 0.5;
   }
-  return out / total;
+  return out * (1.0 / total);  // the array program's form (see sphere_trace)
 }
 
 __device__ __forceinline__ double sdf(const BlobScene& s, const double p[3],
@@ -108,7 +108,7 @@ __device__ double sdf(const RoomScene& s, const double p[3],
 }
 
 struct TraceArgs {
-  double fx, fy, cx, cy, R[9], o[3];
+  double inv_fx, inv_fy, cx, cy, R[9], o[3];
   int width, height, steps;
   double lipschitz, t_max, eps;
 };
@@ -126,8 +126,8 @@ k_sphere_trace(TraceArgs a, Scene s, int nshared, const double* shared_src,
   const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
   const int j = tx * 16 + (threadIdx.x & 15), i = ty * 8 + (threadIdx.x >> 4);
   if (i >= a.height || j >= a.width) return;
-  const double px = ((double)j - a.cx) / a.fx;
-  const double py = ((double)i - a.cy) / a.fy;
+  const double px = ((double)j - a.cx) * a.inv_fx;
+  const double py = ((double)i - a.cy) * a.inv_fy;
   double d[3];
 #pragma unroll
   for (int q = 0; q < 3; ++q)
@@ -167,8 +167,8 @@ k_sphere_trace(TraceArgs a, Scene s, int nshared, const double* shared_src,
 TraceArgs trace_args(const double* cam, int width, int height,
                      double lipschitz, double t_max, int steps, double eps) {
   TraceArgs a;
-  a.fx = cam[0];
-  a.fy = cam[1];
+  a.inv_fx = 1.0 / cam[0];
+  a.inv_fy = 1.0 / cam[1];
   a.cx = cam[2];
   a.cy = cam[3];
   for (int q = 0; q < 9; ++q) a.R[q] = cam[4 + q];

@@ -343,7 +343,7 @@ def value_noise(p, tables, base_freq: float = 4.0):
         out = out + amp * acc
         total += amp
         amp *= 0.5
-    return out / total
+    return out * (1.0 / total)
 
 
 def _norm3(v):
@@ -361,8 +361,11 @@ def sphere_trace(sdf, cam: PinholeCamera, *, lipschitz: float, t_max: float,
     the ray parameter is the depth."""
     import torch
     H, W = cam.height, cam.width
-    px = (torch.arange(W, dtype=torch.float64, device=device) - cam.cx) / cam.fx
-    py = (torch.arange(H, dtype=torch.float64, device=device) - cam.cy) / cam.fy
+    # (x - c) * (1 / f): what torch's CUDA division by a host scalar computes
+    # (the golden depth maps were made with it), written out so that every
+    # device and the CUDA kernels evaluate the same expression
+    px = (torch.arange(W, dtype=torch.float64, device=device) - cam.cx) * (1.0 / cam.fx)
+    py = (torch.arange(H, dtype=torch.float64, device=device) - cam.cy) * (1.0 / cam.fy)
     dirs = torch.stack(torch.broadcast_tensors(px[None, :], py[:, None],
                                                torch.ones((), dtype=torch.float64,
                                                           device=device)), -1)

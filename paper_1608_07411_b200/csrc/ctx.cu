@@ -253,18 +253,11 @@ __global__ void k_leaf_flags(const int32_t* __restrict__ child,
 // per leaf block: packed (level, parent cell) and the 12 neighbour refs.
 // ref >= 0: base slot of the same-level block holding that neighbour octet;
 // ref <= -2: node -(ref+2), a coarser leaf covering it; kNone: outside.
-__global__ void k_leaf_tables(const int32_t* __restrict__ child,
-                              const int32_t* __restrict__ lblocks, int64_t nlb,
-                              const int8_t* __restrict__ blevel,
-                              const uint64_t* __restrict__ bcoord,
-                              const int32_t* __restrict__ bparent,
-                              uint64_t* lkey, int4* lmeta, int32_t* lpar,
-                              int32_t* nbr, const int32_t* __restrict__ sel) {
-  int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  int64_t i = gid / 12;
-  int d = (int)(gid % 12);
-  if (i >= nlb) return;
-  if (sel) i = sel[i];  // only the listed entries (incremental update)
+__device__ __forceinline__ void leaf_table_entry(
+    const int32_t* __restrict__ child, const int32_t* __restrict__ lblocks,
+    const int8_t* __restrict__ blevel, const uint64_t* __restrict__ bcoord,
+    const int32_t* __restrict__ bparent, uint64_t* lkey, int4* lmeta,
+    int32_t* lpar, int32_t* nbr, int64_t i, int d) {
   int32_t b = lblocks[i];
   if (b < 0) {  // hole of a patched list: no active slot
     if (d == 0) {
@@ -304,6 +297,24 @@ __global__ void k_leaf_tables(const int32_t* __restrict__ child,
     }
   }
   nbr[i * 12 + d] = ref;
+}
+
+__global__ void k_leaf_tables(const int32_t* __restrict__ child,
+                              const int32_t* __restrict__ lblocks, int64_t nlb,
+                              const int8_t* __restrict__ blevel,
+                              const uint64_t* __restrict__ bcoord,
+                              const int32_t* __restrict__ bparent,
+                              uint64_t* lkey, int4* lmeta, int32_t* lpar,
+                              int32_t* nbr, const int32_t* __restrict__ sel,
+                              const int32_t* __restrict__ nsel) {
+  // incremental update: only the `*nsel` entries listed in `sel` (the count
+  // stays on the device: the grid strides over it, no host round trip)
+  if (nsel) nlb = *nsel;
+  for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+       gid < nlb * 12; gid += (int64_t)gridDim.x * blockDim.x)
+    leaf_table_entry(child, lblocks, blevel, bcoord, bparent, lkey, lmeta,
+                     lpar, nbr, sel ? sel[gid / 12] : gid / 12,
+                     (int)(gid % 12));
 }
 
 
@@ -1213,8 +1224,8 @@ void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
     ctx_gather(c, st);
     ph_mark(c, kPhGather, st);
   }
-  OCTF_CUDA(cudaStreamSynchronize(st));
   if (c.timing) {
+    OCTF_CUDA(cudaStreamSynchronize(st));  // only for the timer
     c.t_prep_ms += std::chrono::duration<double, std::milli>(
                        std::chrono::steady_clock::now() - t0).count();
     ++c.n_prep;
@@ -1273,7 +1284,7 @@ void ctx_list_full(Ctx& c, const int32_t* child, int64_t total, int64_t nbid,
   c.nbr.ensure(c.nlb * 12);
   k_leaf_tables<<<grid_for(c.nlb * 12), kThreads, 0, st>>>(
       child, c.lblocks.p, c.nlb, c.blevel.p, c.bcoord.p, c.bparent.p,
-      c.lkey.p, c.lmeta.p, c.lpar.p, c.nbr.p, nullptr);
+      c.lkey.p, c.lmeta.p, c.lpar.p, c.nbr.p, nullptr, nullptr);
   OCTF_CUDA(cudaGetLastError());
   c.lpos.ensure(nbid);
   OCTF_CUDA(cudaMemsetAsync(c.lpos.p, 0xff, nbid * sizeof(int32_t), st));
@@ -1464,14 +1475,11 @@ bool ctx_list_update(Ctx& c, const int32_t* child, int64_t total, int64_t nbid,
   k_table_dirty<<<grid_for(nnew), kThreads, 0, st>>>(
       c.lblocks.p, nnew, nold, oldmask, child, c.blevel.p, c.nbr.p, dirty,
       c.counters.p + 6);
-  int32_t ndirty = 0;
-  OCTF_CUDA(cudaMemcpyAsync(&ndirty, c.counters.p + 6, sizeof(int32_t),
-                            cudaMemcpyDeviceToHost, st));
-  OCTF_CUDA(cudaStreamSynchronize(st));
-  if (ndirty)
-    k_leaf_tables<<<grid_for((int64_t)ndirty * 12), kThreads, 0, st>>>(
-        child, c.lblocks.p, ndirty, c.blevel.p, c.bcoord.p, c.bparent.p,
-        c.lkey.p, c.lmeta.p, c.lpar.p, c.nbr.p, dirty);
+  // the dirty count stays on the device: one wave strides over it
+  k_leaf_tables<<<(unsigned)std::min<int64_t>(grid_for(nnew * 12), 148 * 8),
+                  kThreads, 0, st>>>(
+      child, c.lblocks.p, 0, c.blevel.p, c.bcoord.p, c.bparent.p, c.lkey.p,
+      c.lmeta.p, c.lpar.p, c.nbr.p, dirty, c.counters.p + 6);
   OCTF_CUDA(cudaGetLastError());
   ph_mark(c, kPhTables, st);
   if (c.ell) return ell_list_samples(c, nold, nnew, oldmask, t0, st);

@@ -1256,13 +1256,14 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
     c.valid = false;
     c.own_change = true;  // the next rebuild may keep unchanged samples
   }
-  OCTF_CUDA(cudaStreamSynchronize(st));
   a.out3[0] = splits;
   a.out3[1] = joins;
   a.out3[2] = jrows;
-  if (c.timing)
+  if (c.timing) {
+    OCTF_CUDA(cudaStreamSynchronize(st));  // only for the timer
     c.t_restr_ms += std::chrono::duration<double, std::milli>(
                         std::chrono::steady_clock::now() - t_restr).count();
+  }
 }
 
 // parent levels top .. 0 (default: every level above the finest) of `na`

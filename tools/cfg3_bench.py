@@ -30,6 +30,10 @@ ap.add_argument("--mesh", action="store_true",
                 help="also time densify + marching cubes of the result")
 ap.add_argument("--save-scene", default=None, help="pickle the rendered scene")
 ap.add_argument("--load-scene", default=None, help="reuse a pickled scene")
+ap.add_argument("--untimed", action="store_true",
+                help="leave the library's phase timers off (their host "
+                     "synchronisations cost ~0.05 ms per pass): pass times "
+                     "only")
 ap.add_argument("--boxed", action="store_true",
                 help="box-wise input stage (fusion.prepare_boxed: no dense grid)")
 args = ap.parse_args()
@@ -73,7 +77,7 @@ if args.solver == "pd":
     s = fusion.PDSolver(u0, views, p, precision=args.precision)
 else:
     s = fusion.Solver(u0, views, p, precision=args.precision)
-s.ctx.profile(True)
+s.ctx.profile(not args.untimed)
 passes = []
 acc = {}  # per-pass profiles summed (profile(True) reads and resets)
 for t in range(args.passes):
@@ -84,7 +88,7 @@ for t in range(args.passes):
     st = s.run(t, 1)[0] if args.solver == "pd" else s.step(t)
     e1.record()
     torch.cuda.synchronize()
-    pr = s.ctx.profile(True)
+    pr = s.ctx.profile(not args.untimed)
     for key, val in pr.items():
         if isinstance(val, (int, float)):
             acc[key] = acc.get(key, 0) + val

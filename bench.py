@@ -412,11 +412,11 @@ def run_e2e(u0, samples, p, args, info):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
         w0 = time.perf_counter()
+        dF = hF.to("cuda", non_blocking=True)
         du = octree.OctreeField.from_host(hu[0], hu[1], hu[2], u0.d_max)
+        torch.cuda.synchronize()
         w1 = time.perf_counter()
-        # the pinned host samples go straight to fuse(): it uploads them on
-        # a side stream while the solver context is built
-        res = fusion.fuse(du, None, pk, precision="fp32", samples=(hF, None))
+        res = fusion.fuse(du, None, pk, precision="fp32", samples=(dF, None))
         torch.cuda.synchronize()
         w2 = time.perf_counter()
         host = res.field.to_host(scratch=False)
@@ -430,10 +430,10 @@ def run_e2e(u0, samples, p, args, info):
                      "h2d_bytes_per_step": int(h2d // k),
                      "d2h_bytes_per_step": int(d2h // k),
                      "ms_total": ms, "steps": k,
-                     "phases_ms": {"h2d_u0": (w1 - w0) * 1e3,
-                                   "fuse_with_sample_upload": (w2 - w1) * 1e3,
+                     "phases_ms": {"h2d": (w1 - w0) * 1e3,
+                                   "fuse": (w2 - w1) * 1e3,
                                    "d2h": (w3 - w2) * 1e3}})
-        del du, res, host
+        del dF, du, res, host
         torch.cuda.empty_cache()
     best = min(runs, key=lambda r: r["ms_total"])
     return dict(best, repeats_ms=[r["ms_total"] for r in runs],

@@ -592,24 +592,8 @@ class Solver:
             # per-slot samples (BASELINE config 5): frozen trees only
             if not self.frozen:
                 raise ValueError("per-leaf samples need a frozen structure")
-            # host (pinned) samples are uploaded on a side stream while the
-            # context -- which needs only the structure -- is built
-            up = None
-            if any(t is not None and not t.is_cuda for t in samples):
-                up = torch.cuda.Stream()
-                with torch.cuda.stream(up):
-                    samples = tuple(
-                        None if t is None else t.to(device(), non_blocking=True)
-                        for t in samples)
-                self.samples = samples
             self.kern.ctx_prepare(self.ctx, self.u.child, self.u.state,
                                   self.u.d_max, [], [], [])
-            if up is not None:
-                cur = torch.cuda.current_stream()
-                cur.wait_stream(up)
-                for t in samples:
-                    if t is not None:
-                        t.record_stream(cur)
             self.kern.ctx_set_samples(self.ctx, *samples)
         self.jbuf = None
         self.chunks: list[np.ndarray] = []

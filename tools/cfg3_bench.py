@@ -34,6 +34,9 @@ ap.add_argument("--untimed", action="store_true",
                 help="leave the library's phase timers off (their host "
                      "synchronisations cost ~0.05 ms per pass): pass times "
                      "only")
+ap.add_argument("--profile-passes", default=None,
+                help="a:b -- cudaProfilerStart before pass a, Stop after "
+                     "pass b-1 (ncu --profile-from-start off)")
 ap.add_argument("--boxed", action="store_true",
                 help="box-wise input stage (fusion.prepare_boxed: no dense grid)")
 args = ap.parse_args()
@@ -80,7 +83,15 @@ else:
 s.ctx.profile(not args.untimed)
 passes = []
 acc = {}  # per-pass profiles summed (profile(True) reads and resets)
+prof_a, prof_b = (map(int, args.profile_passes.split(":"))
+                  if args.profile_passes else (-1, -1))
 for t in range(args.passes):
+    if t == prof_a:
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
+    if t == prof_b:
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()

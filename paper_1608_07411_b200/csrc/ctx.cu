@@ -11,6 +11,7 @@
 // gathered into a coalesced [view][leaf] store.
 #include <chrono>
 #include <cstdlib>
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include "octf_ctx.h"
@@ -54,6 +55,8 @@ Ctx::Ctx() {
   force_ell = fe && fe[0] == '1';
   const char* lj = std::getenv("OCTF_LEVEL_JOINS");  // A/B switch
   coop_off = lj && lj[0] == '1';
+  const char* lw = std::getenv("OCTF_LEVEL_WALK");  // A/B switch
+  walk_levels = lw && lw[0] == '1';
   const char* pm = std::getenv("OCTF_PHASES");  // rebuild phase marks
   phase_marks = pm && pm[0] == '1';
   const char* fp = std::getenv("OCTF_NO_FUSED_PARENT");  // A/B switch
@@ -157,17 +160,19 @@ __device__ __forceinline__ int64_t cta_alloc_n(int cnt, int32_t* global) {
   return r;
 }
 
-// k_expand without a host round trip per level: the level's range comes
+// one level of the walk without a host round trip: the level's range comes
 // from device counters (dcnt, doff), the next level's start is written by
 // thread 0; a fixed grid strides over the level (its size is only known on
-// the device), CTA-uniform so the slots of a CTA are claimed together
-__global__ void k_expand_dev(const int32_t* __restrict__ child,
-                             int32_t* lvl_blocks, int L, int64_t used,
-                             int64_t cap_blocks, int8_t* blevel,
-                             uint64_t* bcoord, int32_t* bparent, int32_t* dcnt,
-                             int32_t* doff, int32_t* bad) {
-  const int64_t n = dcnt[L];
-  const int64_t next = (int64_t)doff[L] + n;
+// the device), CTA-uniform so the slots of a CTA are claimed together.
+// Lists, counters and cells written by the level above are read past L1
+// (volatile / __ldcg): in the all-level kernel another CTA wrote them.
+__device__ __forceinline__ void expand_level(
+    const int32_t* __restrict__ child, int32_t* lvl_blocks, int L, int64_t used,
+    int64_t cap_blocks, int8_t* blevel, uint64_t* bcoord, int32_t* bparent,
+    int32_t* dcnt, int32_t* doff, int32_t* bad) {
+  const int64_t n = *(volatile int32_t*)(dcnt + L);
+  const int64_t off = *(volatile int32_t*)(doff + L);
+  const int64_t next = off + n;
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid == 0) doff[L + 1] = (int32_t)next;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -180,7 +185,7 @@ __global__ void k_expand_dev(const int32_t* __restrict__ child,
     int32_t nbs[8];
     unsigned inner = 0;
     if (i < n) {
-      b = lvl_blocks[doff[L] + i];
+      b = __ldcg(lvl_blocks + off + i);
       const int nc = b == 0 ? 1 : 8;
       for (int c = 0; c < 8; ++c) {
         nbs[c] = c < nc ? child[b + c] : -1;
@@ -194,7 +199,7 @@ __global__ void k_expand_dev(const int32_t* __restrict__ child,
     }
     int64_t pos = next + cta_alloc_n(__popc(inner), dcnt + L + 1);
     if (!inner) continue;
-    const uint64_t pc = bcoord[block_id(b)];
+    const uint64_t pc = __ldcg(bcoord + block_id(b));
     for (int c = 0; c < 8; ++c) {
       if (!((inner >> c) & 1u)) continue;
       const int32_t nb = nbs[c];
@@ -210,6 +215,38 @@ __global__ void k_expand_dev(const int32_t* __restrict__ child,
         lvl_blocks[pos] = nb;
       }
       ++pos;
+    }
+  }
+}
+
+__global__ void k_expand_dev(const int32_t* __restrict__ child,
+                             int32_t* lvl_blocks, int L, int64_t used,
+                             int64_t cap_blocks, int8_t* blevel,
+                             uint64_t* bcoord, int32_t* bparent, int32_t* dcnt,
+                             int32_t* doff, int32_t* bad) {
+  expand_level(child, lvl_blocks, L, used, cap_blocks, blevel, bcoord, bparent,
+               dcnt, doff, bad);
+}
+
+// every level in one cooperative launch (grid barrier between levels): the
+// nine to twelve tiny launches of the per-level walk cost more in launch
+// gaps than in work on a restructuring pass
+__global__ void __launch_bounds__(kThreads)
+k_expand_all(const int32_t* __restrict__ child, int32_t* lvl_blocks, int d_max,
+             int64_t used, int64_t cap_blocks, int8_t* blevel,
+             uint64_t* bcoord, int32_t* bparent, int32_t* dcnt, int32_t* doff,
+             int32_t* bad) {
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  for (int L = 0; L < d_max; ++L) {
+    expand_level(child, lvl_blocks, L, used, cap_blocks, blevel, bcoord,
+                 bparent, dcnt, doff, bad);
+    grid.sync();
+    if (*(volatile int32_t*)(dcnt + L + 1) == 0) {
+      // no deeper blocks: the remaining offsets all equal this level's end
+      if (blockIdx.x == 0 && threadIdx.x == 0)
+        for (int q = L + 2; q <= d_max; ++q)
+          doff[q] = *(volatile int32_t*)(doff + L + 1);
+      break;
     }
   }
 }
@@ -1168,7 +1205,38 @@ void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
   const int32_t one = 1;
   OCTF_CUDA(cudaMemcpyAsync(dcnt, &one, sizeof(int32_t), cudaMemcpyHostToDevice,
                             st));
-  for (int L = 0; L < d_max; ++L) {
+  if (!c.walk_levels && d_max > 0) {
+    // all levels in one cooperative launch, at most one wave of CTAs
+    static int coop_per_dev[64] = {};
+    int dev = 0;
+    OCTF_CUDA(cudaGetDevice(&dev));
+    int& coop_blocks = coop_per_dev[dev & 63];
+    if (!coop_blocks) {
+      int per_sm = 0, nsm = 0;
+      OCTF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &per_sm, k_expand_all, kThreads, 0));
+      OCTF_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount,
+                                       dev));
+      if (per_sm * nsm < 1) throw Error(kECuda, "walk: no resident CTA");
+      coop_blocks = std::min(per_sm, 4) * nsm;
+    }
+    int32_t* lvl_blocks = c.lvl_blocks.p;
+    int64_t cap_blocks = nbid + 1;
+    int8_t* blevel = c.blevel.p;
+    uint64_t* bcoord = c.bcoord.p;
+    int32_t* bparent = c.bparent.p;
+    int32_t* bad = c.counters.p;
+    int dm = d_max;
+    // a small tree does not need the whole wave (grid barriers cost by CTA)
+    const int grid_blocks = (int)std::min<int64_t>(
+        coop_blocks, std::max<int64_t>(1, (nbid + kThreads - 1) / kThreads));
+    void* kargs[] = {(void*)&child, &lvl_blocks, &dm,     &used,
+                     &cap_blocks,   &blevel,     &bcoord, &bparent,
+                     &dcnt,         &doff,       &bad};
+    OCTF_CUDA(cudaLaunchCooperativeKernel((const void*)k_expand_all,
+                                          grid_blocks, kThreads, kargs, 0, st));
+  }
+  for (int L = 0; L < d_max && c.walk_levels; ++L) {
     // level L holds at most min(8^L, live blocks) blocks: a grid of at
     // most one wave strides over them
     const int64_t bound = L < 7 ? std::min<int64_t>(int64_t(1) << (3 * L), nbid)

@@ -467,6 +467,7 @@ struct JoinCoopArgs {
   int32_t* cand;
   double* cacc;
   int32_t* ccount;        // per level, zeroed
+  int32_t* bcount;        // bottom candidates per level, zeroed
   int d_max;
 };
 
@@ -509,9 +510,19 @@ __global__ void __launch_bounds__(256) k_joins_coop(JoinCoopArgs<T> a) {
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
   const int64_t wid = tid >> 5, nw = nthr >> 5;
+  // bottom candidates per level, counted once: a level with none and no
+  // join below it has nothing to test, and is skipped without a barrier
+  for (int64_t i = tid; i < a.nbot; i += nthr) {
+    int Ls, xs, ys, zs;
+    slot_cell_of(a.bot[i], a.blevel, a.bcoord, Ls, xs, ys, zs);
+    atomicAdd(a.bcount + Ls, 1);
+  }
+  grid.sync();
   int rec_lo = 0;
   for (int L = a.d_max - 1; L >= 0; --L) {
     const int rec_hi = *(volatile int32_t*)(a.counters + 4);
+    if (*(volatile int32_t*)(a.bcount + L) == 0 && rec_hi == rec_lo)
+      continue;  // the same decision in every thread
     const int64_t n_in = a.nbot + (rec_hi - rec_lo);
     for (int64_t i = tid; i < n_in; i += nthr) {
       int32_t s;
@@ -638,13 +649,8 @@ struct FieldSet {
 };
 
 template <typename T, int NA, bool VEC>
-__global__ void __launch_bounds__(kT)
-    k_propagate_blocks(const int32_t* __restrict__ blocks, int64_t nblk,
-                       const int32_t* __restrict__ bparent, FieldSet<T> f) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nblk) return;
-  const int32_t b = __ldg(blocks + i);
-  const int32_t par = __ldg(bparent + ((b + 7) >> 3));
+__device__ __forceinline__ void propagate_block(int32_t b, int32_t par,
+                                                const FieldSet<T>& f) {
 #pragma unroll
   for (int q = 0; q < NA; ++q) {
     T x[8];
@@ -671,6 +677,39 @@ __global__ void __launch_bounds__(kT)
 #pragma unroll
     for (int k = 0; k < 8; ++k) acc += (double)x[k];
     f.v[q][par] = (T)(acc / 8.0);
+  }
+}
+
+template <typename T, int NA, bool VEC>
+__global__ void __launch_bounds__(kT)
+    k_propagate_blocks(const int32_t* __restrict__ blocks, int64_t nblk,
+                       const int32_t* __restrict__ bparent, FieldSet<T> f) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nblk) return;
+  const int32_t b = __ldg(blocks + i);
+  propagate_block<T, NA, VEC>(b, __ldg(bparent + ((b + 7) >> 3)), f);
+}
+
+// the small levels near the root (each at most one CTA of blocks) in one
+// launch: one CTA walks them bottom-up with a barrier in between -- a
+// launch per level costs more than its work there
+struct TopLevels {
+  int n;                      // levels, deepest first
+  int32_t off[kMaxDepth + 1];  // start of the level's child-block list
+  int32_t cnt[kMaxDepth + 1];
+};
+
+template <typename T, int NA, bool VEC>
+__global__ void __launch_bounds__(kT)
+    k_propagate_top(const int32_t* __restrict__ lvl_blocks, TopLevels tl,
+                    const int32_t* __restrict__ bparent, FieldSet<T> f) {
+  for (int q = 0; q < tl.n; ++q) {
+    if ((int)threadIdx.x < tl.cnt[q]) {
+      const int32_t b = __ldg(lvl_blocks + tl.off[q] + threadIdx.x);
+      propagate_block<T, NA, VEC>(b, __ldg(bparent + ((b + 7) >> 3)), f);
+    }
+    __threadfence_block();
+    __syncthreads();
   }
 }
 
@@ -1140,9 +1179,9 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
     double* cacc = jb.cacc.ensure(c.nblocks * 8 + 8);
     if (!c.coop_off) {
       // every level in one cooperative launch from the worklists
-      int32_t* ccount = jb.ccount.ensure(kMaxDepth + 2);
-      OCTF_CUDA(cudaMemsetAsync(ccount, 0, (kMaxDepth + 2) * sizeof(int32_t),
-                                st));
+      int32_t* ccount = jb.ccount.ensure(2 * (kMaxDepth + 2));
+      OCTF_CUDA(cudaMemsetAsync(ccount, 0,
+                                2 * (kMaxDepth + 2) * sizeof(int32_t), st));
       JoinCoopArgs<T> ja;
       ja.bot = c.join_bot.p;
       ja.nbot = ncand;
@@ -1161,6 +1200,7 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
       ja.cand = cand;
       ja.cacc = cacc;
       ja.ccount = ccount;
+      ja.bcount = ccount + (kMaxDepth + 2);
       ja.d_max = prm.d_max;
       // resident CTAs of the cooperative launch, per device
       static int coop_per_dev[64] = {};
@@ -1278,28 +1318,62 @@ void launch_propagate_multi(Ctx& c, T* const* vals, int na, cudaStream_t st,
     fs.v[q] = vals[q];
     vec = vec && ((uintptr_t)(vals[q] + 1) % (8 * sizeof(T)) == 0);
   }
-  for (int L = top < 0 ? c.d_max - 1 : top; L >= lo; --L) {
-    if (L + 1 >= (int)c.lvl_cnt.size()) continue;
-    const int64_t n = c.lvl_cnt[L + 1];
-    if (n == 0) continue;
-    const int32_t* blk = c.lvl_blocks.p + c.lvl_off[L + 1];
-    const unsigned g = blocks_for(n);
+  auto launch = [&](auto kern_top, const int32_t* blk, int64_t n,
+                    const TopLevels* tl) {
+    (void)kern_top;
+    const unsigned g = tl ? 1u : blocks_for(n);
+    auto go = [&](auto na_c, auto vec_c, const FieldSet<T>& fset) {
+      constexpr int NA = decltype(na_c)::value;
+      constexpr bool VEC = decltype(vec_c)::value;
+      if (tl)
+        k_propagate_top<T, NA, VEC><<<1, kT, 0, st>>>(c.lvl_blocks.p, *tl,
+                                                      c.bparent.p, fset);
+      else
+        k_propagate_blocks<T, NA, VEC><<<g, kT, 0, st>>>(blk, n, c.bparent.p,
+                                                         fset);
+    };
+    using I1 = std::integral_constant<int, 1>;
+    using I5 = std::integral_constant<int, 5>;
     if (na == 1) {
-      if (vec) k_propagate_blocks<T, 1, true><<<g, kT, 0, st>>>(blk, n, c.bparent.p, fs);
-      else k_propagate_blocks<T, 1, false><<<g, kT, 0, st>>>(blk, n, c.bparent.p, fs);
+      if (vec) go(I1{}, std::true_type{}, fs);
+      else go(I1{}, std::false_type{}, fs);
     } else if (na == 5) {
-      if (vec) k_propagate_blocks<T, 5, true><<<g, kT, 0, st>>>(blk, n, c.bparent.p, fs);
-      else k_propagate_blocks<T, 5, false><<<g, kT, 0, st>>>(blk, n, c.bparent.p, fs);
+      if (vec) go(I5{}, std::true_type{}, fs);
+      else go(I5{}, std::false_type{}, fs);
     } else {
       for (int q = 0; q < na; ++q) {
         FieldSet<T> one{};
         one.v[0] = vals[q];
-        k_propagate_blocks<T, 1, false><<<g, kT, 0, st>>>(blk, n, c.bparent.p, one);
+        go(I1{}, std::false_type{}, one);
       }
     }
     OCTF_CUDA(cudaGetLastError());
     ++c.launches;
+  };
+  const int L0 = top < 0 ? c.d_max - 1 : top;
+  // the levels from `fuse_from` down to `lo` each fit one CTA: one launch
+  int fuse_from = lo - 1;
+  for (int L = lo; L <= L0; ++L) {
+    if (L + 1 >= (int)c.lvl_cnt.size() || c.lvl_cnt[L + 1] > kT) break;
+    fuse_from = L;
   }
+  for (int L = L0; L > fuse_from; --L) {
+    if (L + 1 >= (int)c.lvl_cnt.size()) continue;
+    const int64_t n = c.lvl_cnt[L + 1];
+    if (n == 0) continue;
+    launch(0, c.lvl_blocks.p + c.lvl_off[L + 1], n, nullptr);
+  }
+  TopLevels tl{};
+  for (int L = std::min(fuse_from, L0); L >= lo; --L) {
+    if (c.lvl_cnt[L + 1] == 0) continue;
+    tl.off[tl.n] = (int32_t)c.lvl_off[L + 1];
+    tl.cnt[tl.n] = (int32_t)c.lvl_cnt[L + 1];
+    ++tl.n;
+  }
+  if (tl.n == 1)
+    launch(0, c.lvl_blocks.p + tl.off[0], tl.cnt[0], nullptr);
+  else if (tl.n > 1)
+    launch(0, nullptr, 0, &tl);
 }
 
 template <typename T>

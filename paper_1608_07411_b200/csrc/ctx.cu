@@ -55,8 +55,8 @@ Ctx::Ctx() {
   force_ell = fe && fe[0] == '1';
   const char* lj = std::getenv("OCTF_LEVEL_JOINS");  // A/B switch
   coop_off = lj && lj[0] == '1';
-  const char* lw = std::getenv("OCTF_LEVEL_WALK");  // A/B switch
-  walk_levels = lw && lw[0] == '1';
+  const char* lw = std::getenv("OCTF_COOP_WALK");  // A/B switch
+  walk_coop = lw && lw[0] == '1';
   const char* pm = std::getenv("OCTF_PHASES");  // rebuild phase marks
   phase_marks = pm && pm[0] == '1';
   const char* fp = std::getenv("OCTF_NO_FUSED_PARENT");  // A/B switch
@@ -248,6 +248,21 @@ k_expand_all(const int32_t* __restrict__ child, int32_t* lvl_blocks, int d_max,
           doff[q] = *(volatile int32_t*)(doff + L + 1);
       break;
     }
+  }
+}
+
+// levels [0, l1) in one single-CTA launch (a level L < 5 has at most 8^(L-1)
+// blocks: the CTA strides over them), barrier between levels
+__global__ void __launch_bounds__(kThreads)
+k_expand_top(const int32_t* __restrict__ child, int32_t* lvl_blocks, int l1,
+             int64_t used, int64_t cap_blocks, int8_t* blevel,
+             uint64_t* bcoord, int32_t* bparent, int32_t* dcnt, int32_t* doff,
+             int32_t* bad) {
+  for (int L = 0; L < l1; ++L) {
+    expand_level(child, lvl_blocks, L, used, cap_blocks, blevel, bcoord,
+                 bparent, dcnt, doff, bad);
+    __threadfence();
+    __syncthreads();
   }
 }
 
@@ -841,7 +856,7 @@ __global__ void k_ell_offsets(const int64_t* __restrict__ scan, int64_t n,
 // the scan; rows[nt + 1] accumulates the abandoned rows (ell_waste)
 __global__ void k_ell_plan(const int32_t* __restrict__ need,
                            const int32_t* __restrict__ tileK, int64_t nt,
-                           int64_t* rows) {
+                           int64_t* rows, int32_t* mlist) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t > nt) return;
   if (t == nt) {
@@ -851,31 +866,37 @@ __global__ void k_ell_plan(const int32_t* __restrict__ need,
   const int nd = need[t], k0 = tileK[t];
   const bool mv = nd > k0;
   rows[t] = mv ? (int64_t)(nd + nd / 4 + 4) * 256 : 0;
-  if (mv)
+  if (mv) {
     atomicAdd(reinterpret_cast<unsigned long long*>(rows + nt + 1),
               (unsigned long long)k0 * 256);
+    mlist[1 + atomicAdd(mlist, 1)] = (int32_t)t;  // the tiles to move
+  }
 }
 
-// one CTA per tile: an overflowing tile's rows move to [total + scan[t],
-// ...) with the new rows zeroed, then its K and offset are switched
-__global__ void k_ell_move_dev(const int32_t* __restrict__ need,
+// a CTA per overflowing tile (mlist[0] of them, listed from mlist[1]; the
+// grid strides over the list): its rows move to [total + scan[t], ...) with
+// the new rows zeroed, then its K and offset are switched
+__global__ void k_ell_move_dev(const int32_t* __restrict__ mlist,
+                               const int32_t* __restrict__ need,
                                int32_t* tileK, int64_t* tileOff,
                                const int64_t* __restrict__ scan, int64_t total,
                                float* F, float* W) {
-  const int64_t t = blockIdx.x;
-  const int nd = need[t], k0 = tileK[t];
-  if (nd <= k0) return;
-  const int k1 = nd + nd / 4 + 4;
-  const int64_t o0 = tileOff[t], o1 = total + scan[t];
-  for (int64_t e = threadIdx.x; e < (int64_t)k1 * 256; e += blockDim.x) {
-    const bool keep = e < (int64_t)k0 * 256;
-    F[o1 + e] = keep ? F[o0 + e] : 0.f;
-    W[o1 + e] = keep ? W[o0 + e] : 0.f;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    tileK[t] = k1;
-    tileOff[t] = o1;
+  const int nm = mlist[0];
+  for (int q = blockIdx.x; q < nm; q += gridDim.x) {
+    const int64_t t = mlist[1 + q];
+    const int nd = need[t], k0 = tileK[t];
+    const int k1 = nd + nd / 4 + 4;
+    const int64_t o0 = tileOff[t], o1 = total + scan[t];
+    for (int64_t e = threadIdx.x; e < (int64_t)k1 * 256; e += blockDim.x) {
+      const bool keep = e < (int64_t)k0 * 256;
+      F[o1 + e] = keep ? F[o0 + e] : 0.f;
+      W[o1 + e] = keep ? W[o0 + e] : 0.f;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tileK[t] = k1;
+      tileOff[t] = o1;
+    }
   }
 }
 
@@ -1205,8 +1226,9 @@ void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
   const int32_t one = 1;
   OCTF_CUDA(cudaMemcpyAsync(dcnt, &one, sizeof(int32_t), cudaMemcpyHostToDevice,
                             st));
-  if (!c.walk_levels && d_max > 0) {
-    // all levels in one cooperative launch, at most one wave of CTAs
+  if (c.walk_coop && d_max > 0) {
+    // all levels in one cooperative launch (measured slower than the
+    // launches below: cfg3 walk 0.10 -> 0.13 ms; kept for A/B)
     static int coop_per_dev[64] = {};
     int dev = 0;
     OCTF_CUDA(cudaGetDevice(&dev));
@@ -1236,7 +1258,16 @@ void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
     OCTF_CUDA(cudaLaunchCooperativeKernel((const void*)k_expand_all,
                                           grid_blocks, kThreads, kargs, 0, st));
   }
-  for (int L = 0; L < d_max && c.walk_levels; ++L) {
+  // the levels near the root in one single-CTA launch, a launch per level
+  // below them
+  const int l_top = c.walk_coop ? d_max : std::min(d_max, 5);
+  if (!c.walk_coop && l_top > 0) {
+    k_expand_top<<<1, kThreads, 0, st>>>(
+        child, c.lvl_blocks.p, l_top, used, nbid + 1, c.blevel.p, c.bcoord.p,
+        c.bparent.p, dcnt, doff, c.counters.p);
+    OCTF_CUDA(cudaGetLastError());
+  }
+  for (int L = l_top; L < d_max; ++L) {
     // level L holds at most min(8^L, live blocks) blocks: a grid of at
     // most one wave strides over them
     const int64_t bound = L < 7 ? std::min<int64_t>(int64_t(1) << (3 * L), nbid)
@@ -1449,8 +1480,10 @@ static bool ell_list_samples(Ctx& c, int64_t nold, int64_t nnew,
     int64_t* rows = reinterpret_cast<int64_t*>(c.sort_k64.ensure(2 * nt_new + 3));
     int64_t* scan = rows + nt_new + 2;
     OCTF_CUDA(cudaMemsetAsync(rows + nt_new + 1, 0, sizeof(int64_t), st));
+    int32_t* mlist = c.sort_k32.ensure(nt_new + 2);
+    OCTF_CUDA(cudaMemsetAsync(mlist, 0, sizeof(int32_t), st));
     k_ell_plan<<<grid_for(nt_new + 1), kThreads, 0, st>>>(need, c.tileK.p,
-                                                          nt_new, rows);
+                                                          nt_new, rows, mlist);
     size_t bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, bytes, rows, scan,
                                   (int)(nt_new + 1), st);
@@ -1469,8 +1502,9 @@ static bool ell_list_samples(Ctx& c, int64_t nold, int64_t nnew,
     // (the old ranges stay unused until the next full rebuild compacts)
     c.F.grow_keep((size_t)total + 1, (size_t)keep, st);
     c.W.grow_keep((size_t)total + 1, (size_t)keep, st);
-    k_ell_move_dev<<<(unsigned)nt_new, 256, 0, st>>>(
-        need, c.tileK.p, c.tileOff.p, scan, keep, c.F.p, c.W.p);
+    k_ell_move_dev<<<(unsigned)std::min<int64_t>(nt_new, 148 * 8), 256, 0,
+                     st>>>(mlist, need, c.tileK.p, c.tileOff.p, scan, keep,
+                           c.F.p, c.W.p);
     OCTF_CUDA(cudaGetLastError());
     OCTF_CUDA(cudaMemsetAsync(c.counters.p + 3, 0, sizeof(int32_t), st));
     OCTF_CUDA(cudaStreamSynchronize(st));

@@ -233,7 +233,7 @@ struct Ctx {
   DevBuf<int32_t> split_list;
   DevBuf<int32_t> join_bot;   // parent slots of bottom join candidates
   bool coop_off = false;      // env OCTF_LEVEL_JOINS=1: per-level join scans
-  bool walk_levels = false;   // env OCTF_LEVEL_WALK=1: a launch per walk level
+  bool walk_coop = false;     // env OCTF_COOP_WALK=1: the level walk as one cooperative launch
   DevBuf<uint8_t> cub_tmp;
   DevBuf<uint64_t> sort_k64;  // sort scratch (persistent)
   DevBuf<int32_t> sort_k32, sort_v32;

@@ -466,8 +466,7 @@ struct JoinCoopArgs {
   int32_t* counters;      // [4]: join records
   int32_t* cand;
   double* cacc;
-  int32_t* ccount;        // per level, zeroed
-  int32_t* bcount;        // bottom candidates per level, zeroed
+  int32_t* ccount;        // candidates per round, zeroed
   int d_max;
 };
 
@@ -510,43 +509,44 @@ __global__ void __launch_bounds__(256) k_joins_coop(JoinCoopArgs<T> a) {
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
   const int64_t wid = tid >> 5, nw = nthr >> 5;
-  // bottom candidates per level, counted once: a level with none and no
-  // join below it has nothing to test, and is skipped without a barrier
-  for (int64_t i = tid; i < a.nbot; i += nthr) {
-    int Ls, xs, ys, zs;
-    slot_cell_of(a.bot[i], a.blevel, a.bcoord, Ls, xs, ys, zs);
-    atomicAdd(a.bcount + Ls, 1);
-  }
-  grid.sync();
+  // Rounds instead of levels: round 0 tests every bottom candidate (all
+  // levels at once -- their children are leaves, nothing below them can
+  // change), round r the parents of the nodes joined in round r-1.  A
+  // parent whose inner children join in different rounds is proposed after
+  // each of them and passes once the last has joined; `joined` holds the
+  // round stamp (round + 1) until the sweep clears it, so "proposed once
+  // per round, by the highest-index sibling joined in that round" can be
+  // told from siblings joined earlier.  The join set is the same fixpoint
+  // as the level order's and a joined node's value depends only on its
+  // children's final values, so the pools are identical; the number of
+  // barrier pairs drops from the levels holding candidates to the longest
+  // join chain.
   int rec_lo = 0;
-  for (int L = a.d_max - 1; L >= 0; --L) {
+  for (int round = 0; round < a.d_max; ++round) {
     const int rec_hi = *(volatile int32_t*)(a.counters + 4);
-    if (*(volatile int32_t*)(a.bcount + L) == 0 && rec_hi == rec_lo)
-      continue;  // the same decision in every thread
-    const int64_t n_in = a.nbot + (rec_hi - rec_lo);
+    const int64_t n_in = round == 0 ? a.nbot : rec_hi - rec_lo;
+    if (n_in == 0) break;  // the same decision in every thread
     for (int64_t i = tid; i < n_in; i += nthr) {
       int32_t s;
-      if (i < a.nbot) {
+      if (round == 0) {
         s = a.bot[i];
-        int Ls, xs, ys, zs;
-        slot_cell_of(s, a.blevel, a.bcoord, Ls, xs, ys, zs);
-        if (Ls != L) continue;
       } else {
-        const int32_t j = a.rec.slot[rec_lo + (i - a.nbot)];
+        const int32_t j = a.rec.slot[rec_lo + i];
         const int32_t jb = ((j - 1) & ~7) + 1;
-        bool later = false;  // a higher sibling joined: it proposes
-        for (int q = j - jb + 1; q < 8; ++q) later |= a.joined[jb + q] != 0;
+        bool later = false;  // a higher sibling joined this round: it proposes
+        for (int q = j - jb + 1; q < 8; ++q) later |= a.joined[jb + q] == round;
         if (later) continue;
         s = a.bparent[block_id(jb)];
+        if (a.joined[s]) continue;
       }
       double acc;
       if (!join_test(a, s, acc)) continue;
-      const int32_t r = atomicAdd(a.ccount + L, 1);
+      const int32_t r = atomicAdd(a.ccount + round, 1);
       a.cand[r] = s;
       a.cacc[r] = acc;
     }
     grid.sync();
-    const int n = *(volatile int32_t*)(a.ccount + L);
+    const int n = *(volatile int32_t*)(a.ccount + round);
     for (int64_t w = wid; w < n; w += nw) {
       const int32_t s = a.cand[w];
       int Ls, x, y, z;
@@ -555,7 +555,7 @@ __global__ void __launch_bounds__(256) k_joins_coop(JoinCoopArgs<T> a) {
                                    a.snap[s], lane);
       if (lane == 0 && fabs((double)dn) > a.p.tau_j) {
         const int32_t cb = a.child[s];
-        a.joined[s] = 1;
+        a.joined[s] = (uint8_t)(round + 1);
         a.uval[s] = (T)(a.cacc[w] / 8.0);
         const int32_t r = atomicAdd(a.counters + 4, 1);
         a.rec.slot[r] = s;
@@ -566,7 +566,7 @@ __global__ void __launch_bounds__(256) k_joins_coop(JoinCoopArgs<T> a) {
       }
     }
     grid.sync();
-    rec_lo = rec_hi;
+    rec_lo = round == 0 ? 0 : rec_hi;
   }
 }
 
@@ -1179,9 +1179,9 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
     double* cacc = jb.cacc.ensure(c.nblocks * 8 + 8);
     if (!c.coop_off) {
       // every level in one cooperative launch from the worklists
-      int32_t* ccount = jb.ccount.ensure(2 * (kMaxDepth + 2));
-      OCTF_CUDA(cudaMemsetAsync(ccount, 0,
-                                2 * (kMaxDepth + 2) * sizeof(int32_t), st));
+      int32_t* ccount = jb.ccount.ensure(kMaxDepth + 2);
+      OCTF_CUDA(cudaMemsetAsync(ccount, 0, (kMaxDepth + 2) * sizeof(int32_t),
+                                st));
       JoinCoopArgs<T> ja;
       ja.bot = c.join_bot.p;
       ja.nbot = ncand;
@@ -1200,7 +1200,6 @@ void iterate_pass_impl(Ctx& c, IterArgs& a, cudaStream_t st) {
       ja.cand = cand;
       ja.cacc = cacc;
       ja.ccount = ccount;
-      ja.bcount = ccount + (kMaxDepth + 2);
       ja.d_max = prm.d_max;
       // resident CTAs of the cooperative launch, per device
       static int coop_per_dev[64] = {};

@@ -258,6 +258,17 @@ k_expand_top(const int32_t* __restrict__ child, int32_t* lvl_blocks, int l1,
              int64_t used, int64_t cap_blocks, int8_t* blevel,
              uint64_t* bcoord, int32_t* bparent, int32_t* dcnt, int32_t* doff,
              int32_t* bad) {
+  // the root entry of the walk (block id 0 = the root slot alone, level 0,
+  // cell 0; one block at level 0): written here instead of by four small
+  // host-to-device copies per rebuild
+  if (threadIdx.x == 0) {
+    blevel[0] = 0;
+    bcoord[0] = 0;
+    lvl_blocks[0] = 0;
+    dcnt[0] = 1;
+  }
+  __threadfence();
+  __syncthreads();
   for (int L = 0; L < l1; ++L) {
     expand_level(child, lvl_blocks, L, used, cap_blocks, blevel, bcoord,
                  bparent, dcnt, doff, bad);
@@ -1206,13 +1217,6 @@ void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
   c.lvl_blocks.ensure(nbid + 1);
   c.counters.ensure(64);
   OCTF_CUDA(cudaMemsetAsync(c.blevel.p, 0xff, nbid, st));
-  int8_t zero = 0;
-  uint64_t zc = 0;
-  int32_t root = 0;
-  OCTF_CUDA(cudaMemcpyAsync(c.blevel.p, &zero, 1, cudaMemcpyHostToDevice, st));
-  OCTF_CUDA(cudaMemcpyAsync(c.bcoord.p, &zc, 8, cudaMemcpyHostToDevice, st));
-  OCTF_CUDA(cudaMemcpyAsync(c.lvl_blocks.p, &root, 4, cudaMemcpyHostToDevice,
-                            st));
   c.lvl_off.assign(d_max + 2, 0);
   c.lvl_cnt.assign(d_max + 2, 0);
   // top-down walk, one launch per level, counts kept on the device and read
@@ -1223,9 +1227,15 @@ void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
   int32_t* doff = dcnt + (d_max + 2);
   OCTF_CUDA(cudaMemsetAsync(c.counters.p, 0,
                             (8 + 2 * (d_max + 2)) * sizeof(int32_t), st));
-  const int32_t one = 1;
-  OCTF_CUDA(cudaMemcpyAsync(dcnt, &one, sizeof(int32_t), cudaMemcpyHostToDevice,
-                            st));
+  // the levels near the root in one single-CTA launch, a launch per level
+  // below them
+  const int l_top = c.walk_coop ? 0 : std::min(d_max, 5);
+  {
+    k_expand_top<<<1, kThreads, 0, st>>>(
+        child, c.lvl_blocks.p, l_top, used, nbid + 1, c.blevel.p, c.bcoord.p,
+        c.bparent.p, dcnt, doff, c.counters.p);
+    OCTF_CUDA(cudaGetLastError());
+  }
   if (c.walk_coop && d_max > 0) {
     // all levels in one cooperative launch (measured slower than the
     // launches below: cfg3 walk 0.10 -> 0.13 ms; kept for A/B)
@@ -1258,16 +1268,7 @@ void ctx_prepare(Ctx& c, const int32_t* child, int64_t cap,
     OCTF_CUDA(cudaLaunchCooperativeKernel((const void*)k_expand_all,
                                           grid_blocks, kThreads, kargs, 0, st));
   }
-  // the levels near the root in one single-CTA launch, a launch per level
-  // below them
-  const int l_top = c.walk_coop ? d_max : std::min(d_max, 5);
-  if (!c.walk_coop && l_top > 0) {
-    k_expand_top<<<1, kThreads, 0, st>>>(
-        child, c.lvl_blocks.p, l_top, used, nbid + 1, c.blevel.p, c.bcoord.p,
-        c.bparent.p, dcnt, doff, c.counters.p);
-    OCTF_CUDA(cudaGetLastError());
-  }
-  for (int L = l_top; L < d_max; ++L) {
+  for (int L = l_top; L < d_max && !c.walk_coop; ++L) {
     // level L holds at most min(8^L, live blocks) blocks: a grid of at
     // most one wave strides over them
     const int64_t bound = L < 7 ? std::min<int64_t>(int64_t(1) << (3 * L), nbid)

@@ -139,6 +139,23 @@ int octf_fuse_pass(octf_ctx *ctx, int dtype, void *usnap, void *uval,
                    double *jlog, int64_t jcap, int64_t *out3,
                    double *energy_pre, void *stream);
 
+/* npasses passes of that loop (fusion.py:204-229) without returning to the
+ * caller in between: pass k reads buffer k % 2 and writes the other, its step
+ * scale is xis[k] (fusion.py:124-126); out3 = npasses x {splits, joins, live
+ * nodes after the pass}, energies_pre[k] = the energy of pass k's incoming
+ * state.  *done = passes completed: a pass that runs out of pool capacity
+ * (OCTF_EPOOL) stops the run before any structural write, with buffer
+ * (*done % 2) holding the current state, so the caller can grow the pools
+ * and go on.  No join log (use octf_fuse_pass for that). */
+int octf_fuse_passes(octf_ctx *ctx, int dtype, void *ubuf0, void *ubuf1,
+                     int32_t *uchild, uint8_t *ujoined, int64_t *ustate,
+                     int64_t cap, int nviews, const float *const *vvals,
+                     const float *const *vws, const int32_t *const *vchilds,
+                     int d_max, double lam, double eps, double gamma,
+                     double tau_s, double tau_j, int clamp, int reverse,
+                     const double *xis, int npasses, int64_t *out3,
+                     double *energies_pre, int *done, void *stream);
+
 /* npasses passes of a frozen structure (tau_s <= 0, tau_j >= 1 with clamp:
  * no split or join can happen) without any host round trip.  Buffers
  * alternate: pass k reads ubuf[k%2] and writes ubuf[(k+1)%2];

@@ -175,6 +175,38 @@ def fuse_pass(usnap, uval, uchild, ujoined, ustate, vvals, vws, vchilds,
     return int(out3[0]), int(out3[1]), int(out3[2]), float(e[0])
 
 
+def fuse_passes(ubuf0, ubuf1, uchild, ujoined, ustate, vvals, vws, vchilds,
+                d_max, lam, eps, gamma, tau_s, tau_j, clamp, reverse, xis, *,
+                ctx):
+    """len(xis) passes of the fuse loop with split/join in one call (pass k
+    reads buffer k % 2); returns (done, out3[done, 3] = splits / joins / live
+    nodes, energies_pre[done], error): ``error`` is the RuntimeError of a
+    pass that ran out of pool capacity (None otherwise) -- the first
+    ``done`` passes are complete and the caller may grow the pools."""
+    import ctypes
+    tv, tw, tc = _views(vvals, vws, vchilds)
+    xis = np.ascontiguousarray(np.asarray(xis, dtype=np.float64))
+    k = len(xis)
+    out3 = np.zeros((max(k, 1), 3), dtype=np.int64)
+    en = np.zeros(max(k, 1), dtype=np.float64)
+    done = ctypes.c_int(0)
+    err = None
+    try:
+        call("octf_fuse_passes", ctx.h, _dtype_code(ubuf0), ptr(ubuf0),
+             ptr(ubuf1), ptr(uchild), ptr(ujoined), _state_ptr(ustate),
+             ubuf0.shape[0], len(vvals), tv, tw, tc, int(d_max), float(lam),
+             float(eps), float(gamma), float(tau_s), float(tau_j),
+             int(bool(clamp)), int(bool(reverse)), xis.ctypes.data, k,
+             out3.ctypes.data, en.ctypes.data, ctypes.byref(done),
+             stream_handle())
+    except RuntimeError as exc:
+        if "capacity" not in str(exc):
+            raise
+        err = exc
+    n = int(done.value)
+    return n, out3[:n], en[:n], err
+
+
 def fuse_passes_frozen(ubuf0, ubuf1, uchild, ustate, vvals, vws, vchilds,
                        d_max, lam, eps, gamma, tau_s, tau_j, clamp, xis, *,
                        ctx, energies_out=None):

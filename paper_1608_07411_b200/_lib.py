@@ -44,6 +44,9 @@ _SIGS = {
     "octf_fuse_pass": ([P, I32, P, P, P, P, P, I64, I32, P, P, P, I32, DBL,
                         DBL, DBL, DBL, DBL, DBL, I32, I32, P, I64, P, P, P],
                        I32),
+    "octf_fuse_passes": ([P, I32, P, P, P, P, P, I64, I32, P, P, P, I32, DBL,
+                          DBL, DBL, DBL, DBL, I32, I32, P, I32, P, P, P, P],
+                         I32),
     "octf_fuse_passes_frozen": ([P, I32, P, P, P, P, I64, I32, P, P, P, I32,
                                  DBL, DBL, DBL, DBL, DBL, I32, P, I32, P, I32,
                                  P], I32),

@@ -331,6 +331,58 @@ int octf_fuse_pass(octf_ctx* ctx, int dtype, void* usnap, void* uval,
   });
 }
 
+int octf_fuse_passes(octf_ctx* ctx, int dtype, void* ubuf0, void* ubuf1,
+                     int32_t* uchild, uint8_t* ujoined, int64_t* ustate,
+                     int64_t cap, int nviews, const float* const* vvals,
+                     const float* const* vws, const int32_t* const* vchilds,
+                     int d_max, double lam, double eps, double gamma,
+                     double tau_s, double tau_j, int clamp, int reverse,
+                     const double* xis, int npasses, int64_t* out3,
+                     double* energies_pre, int* done, void* stream) {
+  if (done) *done = 0;
+  return guard([&] {
+    if (!ctx || !ubuf0 || !ubuf1 || !uchild || !ujoined || !ustate || !xis ||
+        !out3 || !energies_pre || !done)
+      throw octf::Error(octf::kEArg, "null argument");
+    check_dtype(dtype);
+    if (d_max < 0 || d_max > OCTF_MAX_DEPTH)
+      throw octf::Error(octf::kEDepth, "tree depth out of range");
+    if (nviews < 1 && !ctx->c.ext_F)
+      throw octf::Error(octf::kEArg, "at least one view is required");
+    octf::ctx_set_views(ctx->c, nviews, vvals, vws, vchilds, S(stream));
+    void* buf[2] = {ubuf0, ubuf1};
+    for (int k = 0; k < npasses; ++k) {
+      octf::IterArgs a;
+      a.usnap = buf[k & 1];
+      a.uval = buf[(k + 1) & 1];
+      a.child = uchild;
+      a.joined = ujoined;
+      a.state = ustate;
+      a.cap = cap;
+      a.prm = make_params(d_max, lam, eps, gamma, xis[k], tau_s, tau_j, clamp,
+                          reverse);
+      a.jlog = nullptr;
+      a.jcap = 0;
+      a.snapshot = 0;
+      a.want_energy = 1;
+      // a pass that runs out of pool capacity throws before any structural
+      // write: *done passes are complete, buffer (done & 1) holds the state
+      if (dtype == OCTF_F64) {
+        octf::iterate_pass_f64(ctx->c, a, S(stream));
+        octf::propagate_ctx_f64(ctx->c, (double*)a.uval, uchild, S(stream));
+      } else {
+        octf::iterate_pass_f32(ctx->c, a, S(stream));
+        octf::propagate_ctx_f32(ctx->c, (float*)a.uval, uchild, S(stream));
+      }
+      out3[3 * k] = a.out3[0];
+      out3[3 * k + 1] = a.out3[1];
+      out3[3 * k + 2] = ustate[2];
+      energies_pre[k] = a.energy_pre;
+      *done = k + 1;
+    }
+  });
+}
+
 int octf_fuse_passes_frozen(octf_ctx* ctx, int dtype, void* ubuf0, void* ubuf1,
                             const int32_t* uchild, const int64_t* ustate,
                             int64_t cap, int nviews, const float* const* vvals,

@@ -650,8 +650,10 @@ class Solver:
         frozen."""
         if k <= 0:
             return []
-        if not self.frozen or self.log_joins:
+        if self.log_joins:   # the join log is read back pass by pass
             return [self.step(t) for t in range(t0, t0 + k)]
+        if not self.frozen:
+            return self._run_restructuring(t0, k)
         p, u = self.params, self.u
         xis = [step_scale(t, p) for t in range(t0, t0 + k)]
         w0 = time.perf_counter()
@@ -669,6 +671,41 @@ class Solver:
                                 u.node_count * self._itemsize(), 0, 0, wall)
             self.stats.append(st)
             out.append(st)
+        return out
+
+    def _run_restructuring(self, t0: int, k: int, chunk: int = 32) -> list:
+        """Passes with split/join, ``chunk`` at a time inside one library
+        call (octf_fuse_passes: no return to Python between passes); a pass
+        that exhausts the pool stops its call, the pools grow (as ``step``)
+        and the run goes on from that pass."""
+        p, u = self.params, self.u
+        out, t = [], t0
+        while t < t0 + k:
+            n = min(chunk, t0 + k - t)
+            xis = [step_scale(q, p) for q in range(t, t + n)]
+            w0 = time.perf_counter()
+            done, o3, en, err = self.kern.fuse_passes(
+                self.cur, self.nxt, u.child, u.joined, u.state, self.vvals,
+                self.vws, self.vchilds, u.d_max, p.lam, p.eps, p.gamma,
+                p.tau_split, p.tau_join, p.clamp, self.reverse, xis,
+                ctx=self.ctx)
+            wall = (time.perf_counter() - w0) * 1e3 / max(done, 1)
+            if done % 2:
+                self.cur, self.nxt = self.nxt, self.cur
+            for j in range(done):
+                self._settle(float(en[j]))
+                nodes = int(o3[j, 2])
+                st = IterationStats(t + j + 1, None, nodes,
+                                    nodes * self._itemsize(), int(o3[j, 0]),
+                                    int(o3[j, 1]), wall)
+                self.stats.append(st)
+                out.append(st)
+            t += done
+            if err is not None:
+                u.value, u.snap = self.cur, self.nxt
+                _grow(u)
+                self.cur, self.nxt = u.value, u.snap
+                self.ctx.invalidate()
         return out
 
     def finish(self) -> None:

@@ -238,8 +238,11 @@ def run_cuda(args, rank, world, local_rank):
     p = cfg5_params()
     if world > 1:
         from paper_1608_07411_b200 import shard
-        h = u0.to_host(scratch=False)
-        plan = shard.plan(h.child, h.d_max, world, used=h.used)
+        # the plan is built once (rank 0) and each rank receives its part
+        h = u0.to_host(scratch=False) if rank == 0 else None
+        plan = shard.plan_scattered(h.child if h else None, u0.d_max, world,
+                                    rank, used=u0.used)
+        del h
         sharded = shard.ShardedSolver(u0, None, p, plan, rank,
                                       precision="fp32", samples=samples)
         solver = sharded.s

@@ -25,7 +25,8 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-__all__ = ["Structure", "structure", "ShardPlan", "plan", "ShardedSolver",
+__all__ = ["Structure", "structure", "ShardPlan", "plan", "rank_view",
+           "plan_scattered", "ShardedSolver",
            "ShardedPDSolver", "HaloExchange"]
 
 # direction table of the 13-point stencil (octf_common.cuh dir_offset)
@@ -260,6 +261,40 @@ def plan(child, d_max: int, nranks: int, used: int | None = None,
             if q != r:
                 p.send[(q, r)] = need[owner[need] == q]
     return p
+
+
+def rank_view(p: ShardPlan, rank: int) -> ShardPlan:
+    """The part of a plan rank ``rank`` needs to run (its leaf blocks, masks,
+    halo and the send lists it takes part in); the other ranks' entries are
+    empty and ``owner`` is dropped."""
+    e32, e8, e64 = (np.zeros(0, np.int32), np.zeros(0, np.uint8),
+                    np.zeros(0, np.int64))
+    only = lambda lst, e: [a if r == rank else e for r, a in enumerate(lst)]
+    return ShardPlan(p.nranks, p.k, None, p.leaves_per_rank,
+                     sel=only(p.sel, e32), masks=only(p.masks, e8),
+                     halo=only(p.halo, e64),
+                     send={k: v for k, v in p.send.items() if rank in k},
+                     top_levels=p.top_levels,
+                     interior_tiles=list(p.interior_tiles))
+
+
+def plan_scattered(child, d_max: int, nranks: int, rank: int, *,
+                   used: int | None = None, k: int | None = None, group=None,
+                   src: int = 0) -> ShardPlan:
+    """``plan`` built once, on rank ``src``, and each rank's ``rank_view`` sent
+    to it (torch.distributed scatter): the planner's numpy tables of a
+    100M-leaf tree take tens of GB of host memory and minutes of one core, so
+    the ranks of a node must not all build them side by side.  ``child`` is
+    only read on ``src``."""
+    import torch.distributed as dist
+    parts = None
+    if rank == src:
+        full = plan(child, d_max, nranks, used=used, k=k)
+        parts = [rank_view(full, r) for r in range(nranks)]
+        del full
+    out = [None]
+    dist.scatter_object_list(out, parts, src=src, group=group)
+    return out[0]
 
 
 class ShardedSolver:

@@ -94,6 +94,51 @@ def free_port():
     return port
 
 
+def scatter_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        u0, _, _ = scene()
+        u = orc.solver_pool(u0, cap=u0.used)
+        full = shard.plan(u.child, u.d_max, world, used=u.used, k=2)
+        got = shard.plan_scattered(u.child if rank == 0 else None, u.d_max,
+                                   world, rank, used=u.used, k=2)
+        ok = (np.array_equal(got.sel[rank], full.sel[rank])
+              and np.array_equal(got.masks[rank], full.masks[rank])
+              and np.array_equal(got.halo[rank], full.halo[rank])
+              and got.interior_tiles == full.interior_tiles
+              and got.top_levels == full.top_levels
+              and np.array_equal(got.leaves_per_rank, full.leaves_per_rank)
+              and set(got.send) == {k for k in full.send if rank in k}
+              and all(np.array_equal(got.send[k], full.send[k])
+                      for k in got.send)
+              and all(got.sel[r].size == 0 for r in range(world) if r != rank))
+        # the exchange built from the received part works as from the full plan
+        shard.HaloExchange(got, rank, torch.device("cpu"), torch.float64)
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_plan_scattered_gives_each_rank_its_part():
+    """bench.py --gpus N: the plan is built on rank 0 only and every rank
+    receives exactly its own leaf blocks, masks, halo and send lists."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=scatter_worker, args=(r, world, port, q))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    out = dict(q.get(timeout=300) for _ in procs)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert out == {0: True, 1: True, 2: True}
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_sharded_passes_match_single_process(world):
     u0, views, p = scene()

@@ -74,12 +74,14 @@ int octf_ctx_info(octf_ctx *ctx, int64_t *out);
  * has observed views, each leaf's observed samples in view order (the
  * zero-weight views the reference skips, _kernels.pyx:244-252, are not
  * stored).  OCTF_CTX_DENSE keeps the dense [leaf][view] layout at any view
- * count (solver="pd" needs it); OCTF_CTX_ELL uses ELL from 33 views. */
+ * count; OCTF_CTX_ELL uses ELL from 33 views. */
 #define OCTF_CTX_DENSE 1
 #define OCTF_CTX_ELL 2
-/* OCTF_CTX_SORTED (implies DENSE): each leaf's samples are sorted once by
- * (f, view index) when gathered, absent ones last as +inf -- the layout the
- * solver="pd" kernel selects its generalised-median prox on. */
+/* OCTF_CTX_SORTED: each leaf's samples are sorted once by (f, view index)
+ * when gathered, absent ones last as +inf -- the layout the solver="pd"
+ * kernel selects its generalised-median prox on.  With OCTF_CTX_DENSE: 4, 8,
+ * 16, 32 or 64 views; without it more than 64 views use the per-tile store
+ * (each leaf's observed rows sorted), any view count. */
 #define OCTF_CTX_SORTED 4
 /* OCTF_CTX_DEFER: octf_ctx_prepare / set_samples build the structure but
  * gather no samples; the next octf_ctx_select gathers its subset only (and

@@ -157,8 +157,8 @@ int octf_ctx_set_options(octf_ctx* ctx, int flags) {
     const bool dense = (flags & OCTF_CTX_DENSE) != 0;
     const bool ell = (flags & OCTF_CTX_ELL) != 0;
     const bool sorted = (flags & OCTF_CTX_SORTED) != 0;
-    if ((dense || sorted) && ell)
-      throw octf::Error(octf::kEArg, "ELL excludes dense/sorted");
+    if (dense && ell)
+      throw octf::Error(octf::kEArg, "ELL excludes the dense layout");
     ctx->c.defer_gather = (flags & OCTF_CTX_DEFER) != 0;
     const bool pack = (flags & OCTF_CTX_PACKED) != 0;
     if (pack != ctx->c.pack_opt) {
@@ -168,7 +168,7 @@ int octf_ctx_set_options(octf_ctx* ctx, int flags) {
     }
     if (dense != ctx->c.dense_only || ell != ctx->c.force_ell ||
         sorted != ctx->c.sorted) {
-      ctx->c.dense_only = dense || sorted;
+      ctx->c.dense_only = dense;
       ctx->c.force_ell = ell;
       ctx->c.sorted = sorted;
       ctx->c.store_ok = false;

@@ -1511,6 +1511,12 @@ static bool ell_list_samples(Ctx& c, int64_t nold, int64_t nnew,
     OCTF_CUDA(cudaStreamSynchronize(st));
     ph_mark(c, kPhMove, st);
   }
+  if (c.sorted) {  // solver='pd': the new leaves' rows in (f, view) order
+    k_sort_ell<<<148 * 8, kThreads, 0, st>>>(fresh, c.counters.p + 2, 0,
+                                             c.tileK.p, c.tileOff.p, c.F.p,
+                                             c.W.p);
+    OCTF_CUDA(cudaGetLastError());
+  }
   c.nlb = nnew;
   c.nleaves = c.h_counters[4];
   c.ell_tiles = nt_new;
@@ -1783,6 +1789,12 @@ void ctx_gather_ell(Ctx& c, cudaStream_t st) {
                                                         c.tileK.p, c.tileOff.p,
                                                         c.F.p, c.W.p);
   OCTF_CUDA(cudaGetLastError());
+  if (c.sorted && nt) {  // solver='pd': every leaf's rows in (f, view) order
+    k_sort_ell<<<148 * 8, kThreads, 0, st>>>(nullptr, nullptr, nt * 256,
+                                             c.tileK.p, c.tileOff.p, c.F.p,
+                                             c.W.p);
+    OCTF_CUDA(cudaGetLastError());
+  }
   c.M.release();
   c.binw = false;
   c.allv = false;

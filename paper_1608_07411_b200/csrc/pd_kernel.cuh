@@ -58,6 +58,8 @@ struct PdArgs {
   int clamp;
   double* epart;
   const int32_t* __restrict__ lpar;  // parent slot of each leaf block
+  const int32_t* __restrict__ tileK = nullptr;   // ELL store (views > 64):
+  const int64_t* __restrict__ tileOff = nullptr; // rows per tile, offsets
   SDesc sd;  // the dense sample store's layout (octf_common.cuh)
 };
 
@@ -90,9 +92,16 @@ constexpr size_t pd_smem_bytes(int nv, bool binw) {  // one stage
 
 // WP: also write the bottom propagate level of the five fields (frozen
 // passes over a full leaf-block list)
-template <typename T, int BW, int NV, bool WP = false, bool PK = false>
+// EL: the per-tile (ELL) store of many-view configurations -- a leaf's rows
+// are its observed views' (f, w), sorted by (f, view) once at gather
+// (k_sort_ell), K_t rows per tile read from global memory (coalesced: a
+// row holds the tile's 256 slots); zero-weight rows are padding and are
+// skipped, as in the descent kernel.  NV is unused (1).
+template <typename T, int BW, int NV, bool WP = false, bool PK = false,
+          bool EL = false>
 __global__ void __launch_bounds__(kT, pd_minb(BW != kWeights, NV, sizeof(T))) k_pd_pass(PdArgs<T> a) {
   static_assert(NV > 0 && (NV & (NV - 1)) == 0, "NV: power of two");
+  static_assert(!EL || (BW == kWeights && !WP && !PK), "ELL: weights only");
   constexpr bool BINW = BW != kWeights;  // unit weights (+inf = absent)
   // NV = 64, general weights: only the f tile is staged (weights from global)
   constexpr bool WGLOB = NV > 32;
@@ -126,7 +135,7 @@ __global__ void __launch_bounds__(kT, pd_minb(BW != kWeights, NV, sizeof(T))) k_
     bulk_g2s(buf + off, a.F + fo + off, bytes, bar);
     if (WST) bulk_g2s(buf + NV * kTileLeaves + off, a.W + fo + off, bytes, bar);
   };
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && !EL) {
     for (int k = 0; k < kStages; ++k) mbar_init(&s_bar[k], packed ? 2 : 1);
     for (int k = 0; k < kStages && !packed; ++k) {
       const int t = (int)blockIdx.x + k * (int)gridDim.x;
@@ -256,7 +265,7 @@ __global__ void __launch_bounds__(kT, pd_minb(BW != kWeights, NV, sizeof(T))) k_
 
   // samples: the leaf's vector is sorted ascending by (f, view), absent
   // entries last as +inf with weight 0 (sample_sort.cuh, once per leaf)
-  mbar_wait(&s_bar[stage], (unsigned)(it / kStages) & 1u);
+  if (!EL) mbar_wait(&s_bar[stage], (unsigned)(it / kStages) & 1u);
   const int t = threadIdx.x;
   const float* ft = s_tile + sp;  // rank k at ft[k * R]
   const float* wsm = s_tile + NV * kTileLeaves + sp;
@@ -266,7 +275,18 @@ __global__ void __launch_bounds__(kT, pd_minb(BW != kWeights, NV, sizeof(T))) k_
   };
   // weight sum and the energy numerator, sorted order (pd_oracle.c)
   T W = 0, num = 0;
-  if (BW == kAllValid) {  // every sample present: W = N
+  const int ellK = EL ? __ldg(a.tileK + tile_id) : 0;
+  const float* const ef = EL ? a.F + __ldg(a.tileOff + tile_id) + t : nullptr;
+  const float* const ew = EL ? a.W + __ldg(a.tileOff + tile_id) + t : nullptr;
+  if (EL) {
+    for (int k = 0; k < ellK; ++k) {
+      const float wv = __ldg(ew + (size_t)k * kTileLeaves);
+      if (wv != 0.f) {
+        W += (T)wv;
+        num += (T)wv * fabs(U0 - (T)__ldg(ef + (size_t)k * kTileLeaves));
+      }
+    }
+  } else if (BW == kAllValid) {  // every sample present: W = N
 #pragma unroll
     for (int k = 0; k < NV; ++k) num += (T)fabs(U0 - (T)ft[k * R]);
     W = (T)NV;
@@ -301,7 +321,19 @@ __global__ void __launch_bounds__(kT, pd_minb(BW != kWeights, NV, sizeof(T))) k_
   // present samples), the oracle's scan stops at the first k* with
   // c_k* <= f_k* and returns max(f_(k*-1), c_k*)
   T res0;
-  if (BW != kWeights) {
+  if (EL) {
+    // the general-weight scan below over the leaf's observed rows
+    res0 = -(T)INFINITY;
+    T S = 0;
+    for (int k = 0; k < ellK; ++k) {
+      const float wv = __ldg(ew + (size_t)k * kTileLeaves);
+      if (wv == 0.f) continue;
+      const T cand = v0 - cc * ((T)2 * S - W);
+      res0 = fmax(res0, fmin(cand, (T)__ldg(ef + (size_t)k * kTileLeaves)));
+      S += (T)wv;
+    }
+    res0 = fmax(res0, v0 - cc * ((T)2 * S - W));
+  } else if (BW != kWeights) {
     // unit weights, S_k = k: k* by branch-free bisection on the tile (the
     // predicate is monotone over all NV ranks; k* = NV only if none holds)
     auto below = [&](int k) {  // c_k > f_k: k* lies beyond k

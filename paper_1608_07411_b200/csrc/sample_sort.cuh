@@ -114,5 +114,43 @@ __global__ void k_sort_samples(const int32_t* __restrict__ list,
   }
 }
 
+// The same order for the per-tile (ELL) store of many-view configurations:
+// row r of slot s is at off[s >> 8] + r * 256 + (s & 255), K_t rows per tile.
+// A leaf's rows hold its observed views in view order when gathered; a
+// stable insertion sort by f (zero-weight padding rows last, as +inf) gives
+// the oracle's (f, view) order.  One thread per leaf, in place in global
+// memory (a row is coalesced across the tile's threads); O(K^2) moves, once
+// per leaf.
+__global__ void k_sort_ell(const int32_t* __restrict__ list,
+                           const int32_t* __restrict__ nlist, int64_t n,
+                           const int32_t* __restrict__ tileK,
+                           const int64_t* __restrict__ tileOff, float* F,
+                           float* W) {
+  const int64_t cnt = list ? (int64_t)*nlist : n;
+  const int64_t step = (int64_t)gridDim.x * blockDim.x;
+  constexpr int64_t P = kTileLeaves;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnt;
+       k += step) {
+    const int64_t s = list ? (int64_t)list[k] : k;
+    const int K = tileK[s >> 8];
+    float* f = F + tileOff[s >> 8] + (s & 255);
+    float* w = W + tileOff[s >> 8] + (s & 255);
+    for (int r = 0; r < K; ++r)
+      f[r * P] = w[r * P] != 0.f ? __fadd_rn(f[r * P], 0.f)
+                                 : __int_as_float(0x7f800000);
+    for (int a = 1; a < K; ++a) {
+      const float fa = f[a * P], wa = w[a * P];
+      int b = a - 1;
+      while (b >= 0 && f[b * P] > fa) {
+        f[(b + 1) * P] = f[b * P];
+        w[(b + 1) * P] = w[b * P];
+        --b;
+      }
+      f[(b + 1) * P] = fa;
+      w[(b + 1) * P] = wa;
+    }
+  }
+}
+
 }  // namespace
 }  // namespace octf

@@ -1528,12 +1528,15 @@ void pd_passes_impl(Ctx& c, PdHostArgs& a, cudaStream_t st) {
   if (a.npasses < 1) return;
   ensure_prepared<T>(c, a.child, a.cap, a.d_max, a.state, st);
   const int nv = c.nviews;
-  if (c.ell || !c.sorted)
-    throw Error(kEArg, "solver='pd' needs the dense, sorted sample layout "
+  if (!c.sorted)
+    throw Error(kEArg, "solver='pd' needs the sorted sample layout "
                        "(octf_ctx_set_options(ctx, OCTF_CTX_SORTED))");
-  if (!(nv == 4 || nv == 8 || nv == 16 || nv == 32 || nv == 64) ||
-      c.sstride != nv || (nv == 64 && c.binw))
-    throw Error(kEArg, "solver='pd' supports 4, 8, 16, 32 or 64 views");
+  // dense store: 4 .. 64 views; more views: the per-tile (ELL) store
+  if (!c.ell && (!(nv == 4 || nv == 8 || nv == 16 || nv == 32 || nv == 64) ||
+                 c.sstride != nv || (nv == 64 && c.binw)))
+    throw Error(kEArg, "solver='pd' with the dense sample store supports 4, "
+                       "8, 16, 32 or 64 views (more views: leave "
+                       "OCTF_CTX_DENSE off for the per-tile store)");
   constexpr int kChunk = 32;
   const unsigned g = leaf_grid(c);
   // energy partials per pass: one per tile (the primal-dual kernel sums its
@@ -1542,7 +1545,8 @@ void pd_passes_impl(Ctx& c, PdHostArgs& a, cudaStream_t st) {
   const int64_t gp = g;
   c.partials.ensure((size_t)gp * kChunk);
   c.dscalar.ensure(a.npasses > 1024 ? a.npasses : 1024);
-  const bool fused_bottom = c.list_full && !c.fuse_off && a.d_max >= 1;
+  const bool fused_bottom =
+      c.list_full && !c.fuse_off && a.d_max >= 1 && !c.ell;
   for (int k0 = 0; k0 < a.npasses; k0 += kChunk) {
     const int nk = a.npasses - k0 < kChunk ? a.npasses - k0 : kChunk;
     for (int j = 0; j < nk; ++j) {
@@ -1579,10 +1583,17 @@ void pd_passes_impl(Ctx& c, PdHostArgs& a, cudaStream_t st) {
       p.epart = c.partials.p + (size_t)j * gp;
       p.lpar = c.lpar.p;
       p.sd = c.sd;
+      if (c.ell) {
+        p.tileK = c.tileK.p;
+        p.tileOff = c.tileOff.p;
+      }
       if (c.timing && (int)c.pev.size() >= 2 * kChunk)
         OCTF_CUDA(cudaEventRecord(c.pev[2 * j], st));
 #define OCTF_PD(BW, N) launch_pd<T, BW, N>(g, st, p, fused_bottom)
-      if (c.allv && (nv == 8 || nv == 16 || nv == 32)) {
+      if (c.ell) {
+        k_pd_pass<T, kWeights, 1, false, false, true>
+            <<<g, kT, pd_smem_bytes(1, false) * kStages, st>>>(p);
+      } else if (c.allv && (nv == 8 || nv == 16 || nv == 32)) {
         if (nv == 8) OCTF_PD(kAllValid, 8);
         else if (nv == 16) OCTF_PD(kAllValid, 16); else OCTF_PD(kAllValid, 32);
       } else if (c.binw) {

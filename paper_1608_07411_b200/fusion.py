@@ -772,7 +772,10 @@ class PDSolver:
         # the pd kernel reads the dense layout, each leaf's samples sorted
         # once when gathered (its prox selects on them); packed positions on
         # a frozen tree
-        self.ctx.set_options(_lib.CTX_DENSE | _lib.CTX_SORTED
+        # (more than 64 views: the per-tile (ELL) store of observed views,
+        # each leaf's rows sorted the same way)
+        many = samples is None and len(self.vvals) > 64
+        self.ctx.set_options((0 if many else _lib.CTX_DENSE) | _lib.CTX_SORTED
                              | (_lib.CTX_DEFER if defer else 0)
                              | (0 if self.restructure or not _pack()
                                 else _lib.CTX_PACKED))

@@ -168,3 +168,83 @@ def test_pd_64_views_general_weights():
     r32 = fusion.fuse(_dev(u0h), [_dev(v) for v in views], p, solver="pd",
                       precision="fp32")
     assert np.max(np.abs(r32.field.to_host().value - u)) <= 1e-4
+
+
+def _many_views(nviews, d, seed, p_obs):
+    """``nviews`` sparse views (each observes a random p_obs of the cells,
+    coarse view leaves with fractional dyadic weights) of a blocky field
+    (blocks at -0.8 / 0 / +0.8 plus noise: blocks of one sign join, the zero
+    blocks' coarse leaves split) and a mixed-depth u0."""
+    rng = np.random.default_rng(seed)
+    n = 1 << d
+    base = np.kron(rng.choice([-0.8, 0.0, 0.8], (4, 4, 4)),
+                   np.ones((n // 4,) * 3))
+    views = []
+    for k in range(nviews):
+        f = np.clip(base + rng.standard_normal((n, n, n)) * 0.3, -1,
+                    1).astype(np.float32)
+        f = np.round(f * 8) / 8            # ties between views: (f, view) order
+        w = (rng.random((n, n, n)) < p_obs).astype(np.uint8)
+        f[w == 0] = -1.0
+        views.append(orc.build_octree(f, w, tau=0.9, dtype=np.float32))
+    g = base * 0.25 + rng.integers(0, 3, (n, n, n)) * 0.1 - 0.1
+    g[:, :, n // 2:] = base[:, :, n // 2:] * 0.25
+    return views, orc.build_octree(g, tau=0.15)
+
+
+def test_pd_many_views_frozen_matches_cpu_restatement():
+    """More than 64 views (BASELINE config 3 has 300 frames): solver='pd' on
+    the per-tile (ELL) store of observed views, each leaf's rows sorted once
+    (k_sort_ell); frozen, fp64 bit for bit against the oracle, fp32 within
+    1e-4."""
+    from paper_1608_07411_b200 import fusion
+    views, u0h = _many_views(100, 4, 9, 0.15)
+    lam, iters = 0.5, 6
+    u, ub, px, py, pz, en = orc.pd_fuse(u0h, views, lam, 1e-4, iters)
+    p = fusion.FusionParams(lam=lam, iterations=iters, tau_split=0.0,
+                            tau_join=1.5)
+    s = fusion.PDSolver(_dev(u0h), [_dev(v) for v in views], p,
+                        precision="fp64")
+    s.run(0, iters)
+    assert s.ctx.info()["ell"] == 1
+    used = u0h.used
+    got = [t[:used].cpu().numpy() for t in s.state]
+    for g_, w_ in zip(got, (u, ub, px, py, pz)):
+        assert np.array_equal(g_, w_)
+    np.testing.assert_allclose([st.energy for st in s.stats[:-1]], en[1:],
+                               rtol=1e-12)
+    r32 = fusion.fuse(_dev(u0h), [_dev(v) for v in views], p, solver="pd",
+                      precision="fp32")
+    assert np.max(np.abs(r32.field.to_host().value - u)) <= 1e-4
+
+
+def test_pd_many_views_restructure_matches_cpu_restatement():
+    """The same store through pd split/join passes: new leaves' rows are
+    gathered and sorted by the list patch (tiles that outgrow their rows
+    move); pools, structure and every live value bit-exact in fp64."""
+    from paper_1608_07411_b200 import fusion
+    views_h, u0h = _many_views(80, 5, 21, 0.2)
+    lam, iters = 0.5, 8
+    p = fusion.FusionParams(lam=lam, iterations=iters, tau_split=0.15,
+                            tau_join=0.45)
+    s = fusion.PDSolver(_dev(u0h), [_dev(v) for v in views_h], p,
+                        precision="fp64")
+    s.run(0, iters)
+    assert s.ctx.info()["ell"] == 1
+    cap = s.u.capacity
+    u, ub, px, py, pz, en, child, state, sj = orc.pd_fuse(
+        u0h, views_h, lam, 1e-4, iters, tau_split=0.15, tau_join=0.45,
+        cap=cap)
+    assert [(st.splits, st.joins) for st in s.stats] == sj
+    assert sum(a for a, _ in sj) > 0 and sum(b for _, b in sj) > 0
+    assert list(s.u.state) == list(state)
+    used = int(state[0])
+    assert np.array_equal(s.u.child[:used].cpu().numpy(), child[:used])
+    live = [n for n, *_ in orc.leaves(orc.Pool(np.zeros(used), child[:used],
+                                                state, u0h.d_max))]
+    reach = np.array(sorted(set(live) | set(_reachable_inner(child))))
+    got = [t[:used].cpu().numpy() for t in s.state]
+    for g, w in zip(got, (u, ub, px, py, pz)):
+        assert np.array_equal(g[reach], w[:used][reach])
+    np.testing.assert_allclose([st.energy for st in s.stats[:-1]], en[1:],
+                               rtol=1e-12, atol=0)

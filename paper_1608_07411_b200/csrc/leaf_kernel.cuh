@@ -298,12 +298,13 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
   const bool slot_ok = inrange && !(b == 0 && c != 0);
   const bool active = slot_ok && ((lmask >> c) & 1u);
   // the leaf's entry in the staged tile: its slot, or (packed) its rank r
-  // among the tile's leaves at chunk r / 32, lane r % 32, views 32 apart
+  // among the tile's leaves at chunk r / kChunk, entry r % kChunk, views
+  // kChunk apart
   int sbase = threadIdx.x;
   constexpr int sstr = PK ? kChunk : kTileLeaves;
   if (packed) {
     const int r = (meta_rbase(meta.y) + __popc(lmask & ((1u << c) - 1u))) & 255;
-    sbase = (r >> 5) * NVP * kChunk + (r & 31);
+    sbase = (r / kChunk) * NVP * kChunk + (r % kChunk);
     if (NV > 0 && threadIdx.x == kT - 1)  // n_t from the tile's last block
       stage_packed<NVP, BW>(
           s_tile, &s_bar[stage], a.F, aux, tile_id,

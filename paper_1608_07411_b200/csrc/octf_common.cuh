@@ -74,17 +74,26 @@ __host__ __device__ __forceinline__ int64_t samp_idx(int64_t leaf, int v,
 //  * slot layout: [tile][view][256], entry = the slot (samp_idx) -- inner
 //    and free siblings of a leaf block own an (empty) entry too;
 //  * packed layout (OCTF_CTX_PACKED, frozen trees): a leaf's entry is its
-//    rank r among the tile's LEAVES, stored in chunks of 32 leaves,
-//    [tile][r / 32][view][32].  The list keeps its spatial order (neighbour
-//    values stay in L2 / L1); a tile's n_t leaves fill its first
-//    ceil(n_t / 32) chunks, so the kernels stream only those -- no entries
-//    for the inner siblings a leaf block spans (12 % of the slots on
-//    BASELINE config 4).  Any prefix of chunks is valid whatever n_t is,
-//    so the first 6 chunks are staged at once and the rest once n_t is
-//    known (leaf_kernel.cuh stage_packed).  A block's first rank lives in
-//    the top byte of lmeta.y (px < 2^19).
-constexpr int kChunk = 32;         // leaves per chunk
-constexpr int kEarlyChunks = 6;    // chunks staged before n_t is known
+//    rank r among the tile's LEAVES, stored in chunks of kChunk = 16
+//    leaves, [tile][r / 16][view][16].  The list keeps its spatial order
+//    (neighbour values stay in L2 / L1); a tile's n_t leaves fill its
+//    first ceil(n_t / 16) chunks, so the kernels stream only those -- no
+//    entries for the inner siblings a leaf block spans (12 % of the slots
+//    on BASELINE config 4).  Any prefix of chunks is valid whatever n_t
+//    is, so the chunks of the first 192 leaves are staged at once and the
+//    rest once n_t is known (leaf_kernel.cuh stage_packed).  A block's
+//    first rank lives in the top byte of lmeta.y (px < 2^19).  Chunks of
+//    16 halve the partly used last chunk of 32 (cfg5: 225 of a tile's 256
+//    slots are leaves; descent kernel 0.787 -> 0.818 of HBM,
+//    profiles/r02/ab_chunk16.txt) at the price of a 2-way bank conflict on
+//    the staged reads (a warp's 32 ranks span two chunks a multiple of 32
+//    banks apart); chunks of 8 lose.
+#ifndef OCTF_CHUNK
+#define OCTF_CHUNK 16
+#endif
+constexpr int kChunk = OCTF_CHUNK;  // leaves per chunk (a power of two <= 32)
+// chunks staged before n_t is known: 192 leaves
+constexpr int kEarlyChunks = 192 / kChunk;
 struct SDesc {
   int packed = 0;
   int64_t nvp = 0;  // rows per tile (views padded to 4)
@@ -115,7 +124,8 @@ __host__ __device__ __forceinline__ SIdx sidx(const SDesc& d, int64_t i, int c,
     return {base + r, t * 256 + r, 256};
   }
   const int r = meta_rbase(y) + popc8(mask & ((1u << c) - 1u));
-  return {base + (int64_t)(r >> 5) * d.nvp * kChunk + (r & 31), t * 256 + r,
+  return {base + (int64_t)(r / kChunk) * d.nvp * kChunk + (r % kChunk),
+          t * 256 + r,
           kChunk};
 }
 

@@ -164,13 +164,13 @@ __global__ void __launch_bounds__(kT, pd_minb(BW != kWeights, NV, sizeof(T))) k_
   const bool slot_ok = inrange && !(b == 0 && c != 0);
   const bool active = slot_ok && ((lmask >> c) & 1u);
   // the leaf's entry in the staged tile: its slot, or (packed) its rank r
-  // among the tile's leaves at chunk r / 32, lane r % 32, sorted ranks 32
+  // among the tile's leaves at chunk r / kChunk, entry r % kChunk, sorted ranks kChunk
   // apart
   int sp = threadIdx.x;
   constexpr int R = PK ? kChunk : kTileLeaves;
   if (packed) {
     const int r = (meta_rbase(meta.y) + __popc(lmask & ((1u << c) - 1u))) & 255;
-    sp = (r >> 5) * NV * kChunk + (r & 31);
+    sp = (r / kChunk) * NV * kChunk + (r % kChunk);
     if (threadIdx.x == kT - 1)  // n_t from the tile's last block
       stage_pd(s_tile, &s_bar[stage], tile_id,
                inrange ? (meta_rbase(meta.y) + __popc(lmask) + kChunk - 1) / kChunk

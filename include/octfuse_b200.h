@@ -80,8 +80,9 @@ int octf_ctx_info(octf_ctx *ctx, int64_t *out);
 /* OCTF_CTX_SORTED: each leaf's samples are sorted once by (f, view index)
  * when gathered, absent ones last as +inf -- the layout the solver="pd"
  * kernel selects its generalised-median prox on.  With OCTF_CTX_DENSE: 4, 8,
- * 16, 32 or 64 views; without it more than 64 views use the per-tile store
- * (each leaf's observed rows sorted), any view count. */
+ * 16, 32 or 64 views; without it more than 64 views -- with OCTF_CTX_ELL
+ * any number of views -- use the per-tile store (each leaf's observed rows
+ * sorted). */
 #define OCTF_CTX_SORTED 4
 /* OCTF_CTX_DEFER: octf_ctx_prepare / set_samples build the structure but
  * gather no samples; the next octf_ctx_select gathers its subset only (and

@@ -1831,7 +1831,11 @@ void ctx_sort_samples(Ctx& c, const int32_t* list, const int32_t* nlist,
 
 void ctx_gather(Ctx& c, cudaStream_t st) {
   const auto t0 = std::chrono::steady_clock::now();
-  if (!c.ext_F && !c.dense_only && (c.nviews > 64 || (c.force_ell && c.nviews > 32))) {
+  // per-tile (ELL) store: above 64 views, from 33 with OCTF_CTX_ELL, and at
+  // any view count for OCTF_CTX_ELL | OCTF_CTX_SORTED (solver='pd' with a
+  // view count the dense sorted store has no instantiation for)
+  if (!c.ext_F && !c.dense_only &&
+      (c.nviews > 64 || (c.force_ell && (c.nviews > 32 || c.sorted)))) {
     ctx_gather_ell(c, st);
     OCTF_CUDA(cudaStreamSynchronize(st));
     c.store_ok = true;

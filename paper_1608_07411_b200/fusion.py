@@ -746,7 +746,9 @@ class PDSolver:
     frozen (tau_split <= 0, tau_join >= 1, clamp), every pass is followed by
     the pd split/join (``octf_pd_restructure``: leaves with |u| < tau_split
     split, children carrying u/ubar/p; eight leaves past tau_join with one
-    sign join), north_star item (d)."""
+    sign join), north_star item (d).  Any number of views: 4, 8, 16, 32 and
+    64 use the dense sorted sample store (TMA-staged tiles), other counts
+    the per-tile store of each leaf's observed views."""
 
     def __init__(self, u0: OctreeField, views, params: FusionParams, *,
                  precision: str = "fp32", tau: float | None = None,
@@ -772,10 +774,13 @@ class PDSolver:
         # the pd kernel reads the dense layout, each leaf's samples sorted
         # once when gathered (its prox selects on them); packed positions on
         # a frozen tree
-        # (more than 64 views: the per-tile (ELL) store of observed views,
-        # each leaf's rows sorted the same way)
-        many = samples is None and len(self.vvals) > 64
-        self.ctx.set_options((0 if many else _lib.CTX_DENSE) | _lib.CTX_SORTED
+        # (view counts other than 4, 8, 16, 32, 64 -- BASELINE config 3 has
+        # 300 frames: the per-tile (ELL) store of observed views, each
+        # leaf's rows sorted the same way)
+        nv = len(self.vvals)
+        many = samples is None and nv not in (4, 8, 16, 32, 64)
+        self.ctx.set_options((_lib.CTX_ELL if many else _lib.CTX_DENSE)
+                             | _lib.CTX_SORTED
                              | (_lib.CTX_DEFER if defer else 0)
                              | (0 if self.restructure or not _pack()
                                 else _lib.CTX_PACKED))

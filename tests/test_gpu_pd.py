@@ -192,13 +192,15 @@ def _many_views(nviews, d, seed, p_obs):
     return views, orc.build_octree(g, tau=0.15)
 
 
-def test_pd_many_views_frozen_matches_cpu_restatement():
-    """More than 64 views (BASELINE config 3 has 300 frames): solver='pd' on
-    the per-tile (ELL) store of observed views, each leaf's rows sorted once
-    (k_sort_ell); frozen, fp64 bit for bit against the oracle, fp32 within
-    1e-4."""
+@pytest.mark.parametrize("nviews,p_obs", [(100, 0.15), (12, 0.6), (3, 0.8)])
+def test_pd_many_views_frozen_matches_cpu_restatement(nviews, p_obs):
+    """View counts the dense sorted store has no instantiation for -- more
+    than 64 (BASELINE config 3 has 300 frames) or not a power of two:
+    solver='pd' on the per-tile (ELL) store of observed views, each leaf's
+    rows sorted once (k_sort_ell); frozen, fp64 bit for bit against the
+    oracle, fp32 within 1e-4."""
     from paper_1608_07411_b200 import fusion
-    views, u0h = _many_views(100, 4, 9, 0.15)
+    views, u0h = _many_views(nviews, 4, 9, p_obs)
     lam, iters = 0.5, 6
     u, ub, px, py, pz, en = orc.pd_fuse(u0h, views, lam, 1e-4, iters)
     p = fusion.FusionParams(lam=lam, iterations=iters, tau_split=0.0,

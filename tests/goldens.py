@@ -72,3 +72,26 @@ def live_digest(child, value) -> dict:
     return {"child": sha(np.asarray(child)),
             "live_value": sha(np.asarray(value)[live]),
             "live": int(live.size)}
+
+
+def blocky_scene(seed, n=16, nviews=3):
+    """A seeded scene whose descent passes split and join: a blocky field
+    (4^3 blocks at -0.8 / 0 / +0.8) seen by ``nviews`` noisy views, u0 = 0.9 x
+    the field with fine steps in half of the volume (mixed leaf depths).
+    Blocks of one sign join, the zero blocks' coarse leaves split.  Returns
+    (oracle view pools, oracle u0 pool)."""
+    import numpy as np
+    from oracle import oracle as orc
+    rng = np.random.default_rng(seed)
+    base = np.kron(rng.choice([-0.8, 0.0, 0.8], (4, 4, 4)),
+                   np.ones((n // 4,) * 3))
+    views = []
+    for _ in range(nviews):
+        f = np.clip(base + rng.standard_normal((n, n, n)) * 0.2, -1,
+                    1).astype(np.float32)
+        w = (rng.random((n, n, n)) < 0.8).astype(np.uint8)
+        f[w == 0] = -1.0
+        views.append(orc.build_octree(f, w, tau=0.3, dtype=np.float32))
+    g = base * 0.9 + rng.integers(0, 3, (n, n, n)) * 0.1 - 0.1
+    g[:, :, n // 2:] = base[:, :, n // 2:] * 0.9
+    return views, orc.build_octree(g, tau=0.15)

@@ -291,8 +291,10 @@ class TestFuse:
 
 
 class TestRandomTrees:
-    """Live oracle comparison on seeded random blocky scenes with mixed
-    leaf depths, splits and joins."""
+    """Live oracle comparison on seeded scenes: white-noise fields (full
+    trees that stay as they are: the update, energy and bookkeeping of a
+    pass without events), blocky scenes built to split and join, and the two
+    join paths against each other."""
 
     @pytest.mark.parametrize("seed", range(6))
     def test_random_scene_passes(self, seed):
@@ -323,6 +325,35 @@ class TestRandomTrees:
         assert np.array_equal(res.join_log, ref.join_log)
         assert [(s.splits, s.joins) for s in res.stats] == \
             [(s.splits, s.joins) for s in ref.stats]
+
+    @pytest.mark.parametrize("seed", range(4))
+    def test_blocky_scene_splits_and_joins(self, seed):
+        """Scenes built to restructure (tests.goldens.blocky_scene: ~100
+        splits and joins in the first pass, cascading joins after): pools,
+        join log and counts as the oracle's, with the join log (a call per
+        pass) and without (the library's multi-pass loop)."""
+        from paper_1608_07411_b200 import fusion
+        from tests.goldens import blocky_scene
+        views_h, u0h = blocky_scene(100 + seed)
+        kw = dict(iterations=10, xi0=0.3, tau_split=0.15, tau_join=0.45,
+                  lam=0.4)
+        ref = orc.fuse(u0h, views_h, orc.Params(**kw), log_joins=True)
+        events = [(s.splits, s.joins) for s in ref.stats]
+        assert sum(a for a, _ in events) > 50 and sum(b for _, b in events) > 50
+        for log in (True, False):
+            res = fusion.fuse(dev(u0h), [dev(v) for v in views_h],
+                              fusion.FusionParams(**kw), log_joins=log)
+            h = res.field.to_host()
+            assert np.array_equal(h.child, ref.field.child[:ref.field.used])
+            assert list(h.state) == list(ref.field.state)
+            assert leaf_table(h.child, h.value) == leaf_table(
+                ref.field.child, ref.field.value)
+            assert [(s.splits, s.joins) for s in res.stats] == events
+            if log:
+                assert np.array_equal(res.join_log, ref.join_log)
+            np.testing.assert_allclose([s.energy for s in res.stats],
+                                       [s.energy for s in ref.stats],
+                                       rtol=1e-12)
 
     @pytest.mark.parametrize("seed", range(2))
     def test_join_paths_agree(self, seed, monkeypatch):

@@ -51,6 +51,13 @@ def _state_ptr(state: np.ndarray) -> int:
 _view_cache = None   # (vvals, vws, vchilds, first/last pointers, tables)
 
 
+def drop_view_cache() -> None:
+    """Forget the cached pointer tables (and the references to the view
+    pools they keep alive); solvers call it when they close."""
+    global _view_cache
+    _view_cache = None
+
+
 def _views(vvals, vws, vchilds):
     """Pointer tables of the view pools.  A solver passes the same three
     lists every pass: the tables of the last call are reused while the list

@@ -728,6 +728,7 @@ class Solver:
 
     def close(self):
         self.ctx.close()
+        self.kern.drop_view_cache()
 
 
 def pd_steps(lam: float):
@@ -897,6 +898,7 @@ class PDSolver:
 
     def close(self):
         self.ctx.close()
+        self.kern.drop_view_cache()
 
 
 def fuse(u0: OctreeField, views, params: FusionParams, *,

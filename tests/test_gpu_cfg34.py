@@ -331,3 +331,49 @@ def test_trace_kernels_match_array_program():
         assert (want > 0).any()
         assert np.array_equal(got, want)
         done += 1
+
+
+def test_trace_kernels_against_closed_forms():
+    """Edge cases of the ray marcher with known answers: a blob without
+    noise octaves is a sphere (the exact ray/sphere depth of
+    scenes.sphere_depth, reference synth.py:80-109, to the bisection's
+    resolution; same hit mask), and a room without objects is its six walls
+    (depth of the wall the ray meets)."""
+    from paper_1608_07411_b200 import scenes
+    centre = np.array([0.5, 0.5, 0.5])
+    pos = centre + 1.2 * np.array([0.3, -0.5, 0.81])
+    cam = scenes.PinholeCamera(90.0, 90.0, 47.5, 31.5, 96, 64,
+                               scenes.look_at(pos, centre), pos)
+    empty = [torch.zeros((2, 2, 2), dtype=torch.float64, device="cuda")]
+    got = scenes.trace_blob(cam, empty, amp=0.0, lipschitz=1.0,
+                            t_max=3.0).cpu().numpy()
+    want = scenes.sphere_depth(cam, centre, 0.35)
+    # (sphere tracing stops 1e-7 off the surface: a ray grazing the limb
+    # stops up to sqrt(2 R 1e-7) early or misses; compare where both hit,
+    # and require the masks to agree but for a thin rim)
+    both = (got > 0) & (want > 0)
+    assert both.sum() > 500
+    err = np.abs(got[both] - want[both])
+    assert np.quantile(err, 0.99) < 1e-5 and err.max() < 2e-3
+    assert ((got > 0) != (want > 0)).sum() <= 0.02 * both.sum()
+    # walls only: from an interior point every ray hits a wall
+    size = 4.0
+    p0 = np.array([1.0, 2.5, 1.5])
+    cam = scenes.PinholeCamera(70.0, 70.0, 47.5, 31.5, 96, 64,
+                               scenes.look_at(p0, np.array([3.5, 0.5, 2.0])),
+                               p0)
+    objs = torch.zeros(1, dtype=torch.float64, device="cuda")
+    z = scenes.trace_room(cam, objs, 0, 0, size=size, lipschitz=1.0,
+                          t_max=8.0, eps=1e-6).cpu().numpy()
+    R = np.asarray(cam.rotation)
+    px = (np.arange(96) - cam.cx) / cam.fx
+    py = (np.arange(64) - cam.cy) / cam.fy
+    d = (R[:, 0][None, None, :] * px[None, :, None]
+         + R[:, 1][None, None, :] * py[:, None, None] + R[:, 2][None, None, :])
+    with np.errstate(divide="ignore", invalid="ignore"):
+        t_hi = np.where(d > 0, (size - p0) / d, np.inf)
+        t_lo = np.where(d < 0, (0.0 - p0) / d, np.inf)
+    t_wall = np.minimum(t_hi, t_lo).min(axis=2)
+    assert (z > 0).all()
+    err = np.abs(z - t_wall)
+    assert np.quantile(err, 0.99) < 1e-5 and err.max() < 1e-3

@@ -73,3 +73,43 @@ def test_gpu_pd_energy_is_the_reference_energy_at_eps_zero():
                                  tau_split=0.0, tau_join=1.5)
         want = fusion.tree_energy(res.field, views, pe)
         assert res.stats[-1].energy == pytest.approx(want, rel=1e-7)
+
+
+def test_pd_oracle_prox_minimises_its_objective():
+    """The pd oracle's prox (pd_oracle.c wmedian_prox) on a single-cell tree,
+    where a pass is u' = prox_{tau D}(u) with D(x) = sum w|x - f| / (gamma +
+    sum w): u' minimises (x - u)^2 / 2 + tau D(x) -- checked against the
+    objective at every kink f_i, every stationary point of a linear piece
+    and a fine grid (random weights, ties, zero weights, u outside the
+    samples' range)."""
+    rng = np.random.default_rng(0)
+    gamma, tau = 1e-4, 0.7
+
+    def leaf(v, w=None):
+        return orc.Pool(np.array([v], np.float32 if w is not None else np.float64),
+                        np.full(1, -1, np.int32), np.array([1, -1, 1], np.int64),
+                        0, weight=None if w is None else np.array([w], np.float32))
+    for trial in range(200):
+        n = int(rng.integers(1, 9))
+        f = np.round(rng.uniform(-1, 1, n) * 8) / 8 if trial % 3 == 0 \
+            else rng.uniform(-1, 1, n)
+        w = rng.choice([0.0, 0.25, 0.5, 1.0], n) if trial % 2 else np.ones(n)
+        if not w.any():
+            w[0] = 1.0
+        f32, w32 = f.astype(np.float32), w.astype(np.float32)
+        u = float(rng.uniform(-1.5, 1.5)) if trial % 5 else float(f32[0])
+        views = [leaf(a, b) for a, b in zip(f32, w32)]
+        out = orc.pd_fuse(leaf(u), views, 0.3, gamma, 1, tau=tau, sigma=0.1,
+                          clamp=False)
+        x = float(out[0][0])
+        fd, wd = f32.astype(np.float64), w32.astype(np.float64)
+        c = tau / (wd.sum() + gamma)
+
+        def obj(y):
+            return 0.5 * (y - u) ** 2 + c * float((wd * np.abs(y - fd)).sum())
+        order = np.argsort(fd, kind="stable")
+        S = np.concatenate([[0.0], np.cumsum(wd[order])])
+        cands = list(fd) + [u - c * (2 * s - wd.sum()) for s in S] \
+            + list(np.linspace(-2, 2, 401))
+        best = min(obj(y) for y in cands)
+        assert obj(x) <= best + 1e-12

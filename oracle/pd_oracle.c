@@ -24,6 +24,11 @@
  *   extrapolation  ubar' = 2u' - u;  u' clamped to [-1,1] when clamp.
  * Inner nodes of u, ubar, p are child means (propagate) after every pass.
  * Built with -ffp-contract=off; the GPU's f64 mode keeps this exact order.
+ *
+ * What ties it to the reference (tests/test_pd_energy_pin.py): E(u) equals
+ * the reference's energy (octfuse_oracle.c orc_tree_energy, pinned to the
+ * reference's fixtures) at eps = 1e-9 on the states a run visits, and the
+ * prox is checked as the minimiser of its objective.
  */
 #include <math.h>
 #include <stdint.h>

@@ -250,3 +250,33 @@ def test_pd_many_views_restructure_matches_cpu_restatement():
         assert np.array_equal(g[reach], w[:used][reach])
     np.testing.assert_allclose([st.energy for st in s.stats[:-1]], en[1:],
                                rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("nviews", [1, 2, 4, 5, 8])
+def test_pd_single_cell_tree_is_the_prox(nviews):
+    """A one-node tree: a pd pass is u' = prox_{tau D}(u) (no neighbours, no
+    duals).  Every view count -- the dense sorted store at 4 and 8, the
+    per-tile store at the others -- equals the oracle bit for bit in fp64."""
+    from paper_1608_07411_b200 import fusion
+    rng = np.random.default_rng(40 + nviews)
+
+    def leaf(v, w=None):
+        return orc.Pool(np.array([v], np.float32 if w is not None else np.float64),
+                        np.full(1, -1, np.int32), np.array([1, -1, 1], np.int64),
+                        0, weight=None if w is None else np.array([w], np.float32))
+    for trial in range(6):
+        f = (np.round(rng.uniform(-1, 1, nviews) * 4) / 4).astype(np.float32)
+        w = rng.choice([0.0, 0.5, 1.0], nviews).astype(np.float32)
+        w[int(rng.integers(nviews))] = 1.0
+        u0h = leaf(float(rng.uniform(-1, 1)))
+        views = [leaf(a, b) for a, b in zip(f, w)]
+        want = orc.pd_fuse(u0h, views, 0.3, 1e-4, 3)
+        p = fusion.FusionParams(lam=0.3, iterations=3, tau_split=0.0,
+                                tau_join=1.5)
+        s = fusion.PDSolver(_dev(u0h), [_dev(v) for v in views], p,
+                            precision="fp64")
+        s.run(0, 3)
+        got = [t[:1].cpu().numpy() for t in s.state]
+        for g_, w_ in zip(got, want[:5]):
+            assert np.array_equal(g_, w_[:1])
+        s.close()

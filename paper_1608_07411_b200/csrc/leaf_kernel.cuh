@@ -287,6 +287,22 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
   if (NV > 0 && packed && threadIdx.x == 0)
     stage_packed<NVP, BW>(s_tile, &s_bar[stage], a.F, aux, tile_id, -1);
 
+  // ELL store (NV == 0 instantiations): the tile's row count and offset, and
+  // the leaf's first rows, are requested here so that their latency runs
+  // under the stencil's table lookups
+  constexpr int kEllBatch = 4;
+  const bool ell = NV == 0 && a.tileK != nullptr;
+  const int ellK = ell ? __ldg(a.tileK + tile_id) : 0;
+  const int64_t ell0 =
+      ell ? __ldg(a.tileOff + tile_id) + (int64_t)threadIdx.x : 0;
+  float ew0[kEllBatch], ef0[kEllBatch];
+#pragma unroll
+  for (int q = 0; q < kEllBatch; ++q) {
+    const bool on = q < ellK;
+    ew0[q] = on ? __ldg(a.W + ell0 + ((int64_t)q << 8)) : 0.f;
+    ef0[q] = on ? __ldg(a.F + ell0 + ((int64_t)q << 8)) : 0.f;
+  }
+
   // one 16 B load: base slot, parent cell, leaf mask and level
   const int4 meta = inrange ? __ldg(a.lmeta + i) : make_int4(0, 0, 0, 0);
   const int32_t b = meta.x;
@@ -464,14 +480,29 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
       }
     }
   } else if (active && a.tileK) {  // ELL: the leaf's observed views, in order
-    const int K = __ldg(a.tileK + tile_id);
-    for (int r = 0; r < K; ++r) {
-      const float wv = __ldg(a.W + ell_idx(a.tileOff, gid, r));
-      if (wv != 0.f) sample((T)wv, __ldg(a.F + ell_idx(a.tileOff, gid, r)));
+    // rows in batches of kEllBatch: the (w, f) loads of a batch are issued
+    // together (f also for zero-weight padding rows) and consumed in row
+    // order -- one load latency per batch instead of two per row; the
+    // first batch was requested at the top of the tile
+#pragma unroll
+    for (int q = 0; q < kEllBatch; ++q)
+      if (ew0[q] != 0.f) sample((T)ew0[q], ef0[q]);
+    for (int r = kEllBatch; r < ellK; r += kEllBatch) {
+      float wv[kEllBatch], fv[kEllBatch];
+#pragma unroll
+      for (int q = 0; q < kEllBatch; ++q) {
+        const bool on = r + q < ellK;
+        wv[q] = on ? __ldg(a.W + ell0 + ((int64_t)(r + q) << 8)) : 0.f;
+        fv[q] = on ? __ldg(a.F + ell0 + ((int64_t)(r + q) << 8)) : 0.f;
+      }
+#pragma unroll
+      for (int q = 0; q < kEllBatch; ++q)
+        if (wv[q] != 0.f) sample((T)wv[q], fv[q]);
     }
   } else if (active) {
     const SIdx q = sidx(a.sd, i, c, meta.y, lmask);
     uint32_t mk = BINW ? __ldg(a.M + q.m) : 0u;
+#pragma unroll 4
     for (int v = 0; v < a.nv; ++v) {
       const float fv = __ldg(a.F + q.f + (int64_t)v * q.pitch);
       if (BINW) {

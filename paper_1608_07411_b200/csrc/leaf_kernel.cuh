@@ -34,11 +34,23 @@
 #ifndef OCTF_LEAF_MINB_SMALL
 #define OCTF_LEAF_MINB_SMALL 6
 #endif
+// the runtime-N instantiation (restructuring configurations: dense general
+// weights, or the per-tile ELL store whose row batches want registers)
+#ifndef OCTF_LEAF_MINB_GENERIC
+#define OCTF_LEAF_MINB_GENERIC OCTF_LEAF_MINB
+#endif
+#ifndef OCTF_ELL_PRE
+#define OCTF_ELL_PRE 4
+#endif
+#ifndef OCTF_ELL_BATCH
+#define OCTF_ELL_BATCH 8
+#endif
 constexpr int leaf_minb(int nv, int tbytes) {
   // (the f64 parity mode needs the registers: 40 or 48 would spill)
   return tbytes == 8 ? 2
-         : (nv > 0 && nv <= 16) ? OCTF_LEAF_MINB_SMALL
-                                : OCTF_LEAF_MINB;
+         : nv == 0 ? OCTF_LEAF_MINB_GENERIC
+         : nv <= 16 ? OCTF_LEAF_MINB_SMALL
+                    : OCTF_LEAF_MINB;
 }
 
 template <typename T>
@@ -261,8 +273,11 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
   const void* aux = BINW ? (const void*)a.M : (const void*)a.W;
   // packed store: each tile is staged at the top of its own iteration by
   // threads 0 and kT-1 (stage_packed; no prefetch across tiles)
-  constexpr bool packed = PK;
-  static_assert(!PK || NV > 0, "the packed store is staged");
+  constexpr bool packed = PK && NV > 0;
+  // PK with the runtime-N instantiation (NV == 0): the per-tile ELL store --
+  // its own instantiation, so its row batches do not cost the dense
+  // runtime-N loop registers
+  constexpr bool ELLV = PK && NV == 0;
   if (NV > 0) {
     if (threadIdx.x == 0) {
       for (int k = 0; k < kStages; ++k) mbar_init(&s_bar[k], packed ? 2 : 1);
@@ -290,14 +305,14 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
   // ELL store (NV == 0 instantiations): the tile's row count and offset, and
   // the leaf's first rows, are requested here so that their latency runs
   // under the stencil's table lookups
-  constexpr int kEllBatch = 4;
-  const bool ell = NV == 0 && a.tileK != nullptr;
-  const int ellK = ell ? __ldg(a.tileK + tile_id) : 0;
+  constexpr int kEllPre = OCTF_ELL_PRE;      // rows requested before the stencil
+  constexpr int kEllBatch = OCTF_ELL_BATCH;  // rows per batch after it
+  const int ellK = ELLV ? __ldg(a.tileK + tile_id) : 0;
   const int64_t ell0 =
-      ell ? __ldg(a.tileOff + tile_id) + (int64_t)threadIdx.x : 0;
-  float ew0[kEllBatch], ef0[kEllBatch];
+      ELLV ? __ldg(a.tileOff + tile_id) + (int64_t)threadIdx.x : 0;
+  float ew0[kEllPre], ef0[kEllPre];
 #pragma unroll
-  for (int q = 0; q < kEllBatch; ++q) {
+  for (int q = 0; q < kEllPre; ++q) {
     const bool on = q < ellK;
     ew0[q] = on ? __ldg(a.W + ell0 + ((int64_t)q << 8)) : 0.f;
     ef0[q] = on ? __ldg(a.F + ell0 + ((int64_t)q << 8)) : 0.f;
@@ -479,15 +494,16 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
         if (wv != 0.f) sample((T)wv, sf[v * R]);
       }
     }
-  } else if (active && a.tileK) {  // ELL: the leaf's observed views, in order
-    // rows in batches of kEllBatch: the (w, f) loads of a batch are issued
+  } else if (ELLV) {  // ELL: the leaf's observed views, in order
+    if (active) {
+    // rows in batches (kEllPre, then kEllBatch): the (w, f) loads of a batch are issued
     // together (f also for zero-weight padding rows) and consumed in row
     // order -- one load latency per batch instead of two per row; the
     // first batch was requested at the top of the tile
 #pragma unroll
-    for (int q = 0; q < kEllBatch; ++q)
+    for (int q = 0; q < kEllPre; ++q)
       if (ew0[q] != 0.f) sample((T)ew0[q], ef0[q]);
-    for (int r = kEllBatch; r < ellK; r += kEllBatch) {
+    for (int r = kEllPre; r < ellK; r += kEllBatch) {
       float wv[kEllBatch], fv[kEllBatch];
 #pragma unroll
       for (int q = 0; q < kEllBatch; ++q) {
@@ -498,6 +514,7 @@ __global__ void __launch_bounds__(kT, leaf_minb(NV, sizeof(T))) k_leaf_pass(Leaf
 #pragma unroll
       for (int q = 0; q < kEllBatch; ++q)
         if (wv[q] != 0.f) sample((T)wv[q], fv[q]);
+    }
     }
   } else if (active) {
     const SIdx q = sidx(a.sd, i, c, meta.y, lmask);

@@ -887,6 +887,13 @@ void launch_leaf(unsigned g, cudaStream_t st, LeafArgs<T> a) {
       return;
     }
   }
+  if constexpr (N == 0) {  // the per-tile ELL store: its own instantiation
+    if (a.tileK) {
+      a.ntiles = (int)g;
+      k_leaf_pass<T, FZ, BW, EN, 0, true><<<g, kT, 0, st>>>(a);
+      return;
+    }
+  }
   constexpr size_t smem = leaf_smem_bytes(N, BW);
   const void* fn = (const void*)k_leaf_pass<T, FZ, BW, EN, N>;
   smem_opt_in(fn, smem);
@@ -936,7 +943,9 @@ void launch_leaf_pass(Ctx& c, const T* snap, T* uval, const int32_t* child,
   if (timed && c.timing) OCTF_CUDA(cudaEventRecord(c.tev[0], st));
 #define OCTF_LEAF(FZ, BW, EN)                                         \
   do {                                                                \
-    if (c.nviews == 16)                                               \
+    if (c.ell)                                                        \
+      launch_leaf<T, FZ, BW, EN, 0>(g, st, a);                        \
+    else if (c.nviews == 16)                                          \
       launch_leaf<T, FZ, BW, EN, 16>(g, st, a);                       \
     else if (c.nviews == 32)                                          \
       launch_leaf<T, FZ, BW, EN, 32>(g, st, a);                       \

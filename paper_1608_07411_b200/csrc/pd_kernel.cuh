@@ -278,13 +278,24 @@ __global__ void __launch_bounds__(kT, pd_minb(BW != kWeights, NV, sizeof(T))) k_
   const int ellK = EL ? __ldg(a.tileK + tile_id) : 0;
   const float* const ef = EL ? a.F + __ldg(a.tileOff + tile_id) + t : nullptr;
   const float* const ew = EL ? a.W + __ldg(a.tileOff + tile_id) + t : nullptr;
+  // (ELL rows in batches of four: the (w, f) loads of a batch are issued
+  // together and consumed in row order, as in the descent kernel)
+  constexpr int kEB = 4;
   if (EL) {
-    for (int k = 0; k < ellK; ++k) {
-      const float wv = __ldg(ew + (size_t)k * kTileLeaves);
-      if (wv != 0.f) {
-        W += (T)wv;
-        num += (T)wv * fabs(U0 - (T)__ldg(ef + (size_t)k * kTileLeaves));
+    for (int k0 = 0; k0 < ellK; k0 += kEB) {
+      float wv[kEB], fv[kEB];
+#pragma unroll
+      for (int q = 0; q < kEB; ++q) {
+        const bool on = k0 + q < ellK;
+        wv[q] = on ? __ldg(ew + (size_t)(k0 + q) * kTileLeaves) : 0.f;
+        fv[q] = on ? __ldg(ef + (size_t)(k0 + q) * kTileLeaves) : 0.f;
       }
+#pragma unroll
+      for (int q = 0; q < kEB; ++q)
+        if (wv[q] != 0.f) {
+          W += (T)wv[q];
+          num += (T)wv[q] * fabs(U0 - (T)fv[q]);
+        }
     }
   } else if (BW == kAllValid) {  // every sample present: W = N
 #pragma unroll
@@ -325,12 +336,21 @@ __global__ void __launch_bounds__(kT, pd_minb(BW != kWeights, NV, sizeof(T))) k_
     // the general-weight scan below over the leaf's observed rows
     res0 = -(T)INFINITY;
     T S = 0;
-    for (int k = 0; k < ellK; ++k) {
-      const float wv = __ldg(ew + (size_t)k * kTileLeaves);
-      if (wv == 0.f) continue;
-      const T cand = v0 - cc * ((T)2 * S - W);
-      res0 = fmax(res0, fmin(cand, (T)__ldg(ef + (size_t)k * kTileLeaves)));
-      S += (T)wv;
+    for (int k0 = 0; k0 < ellK; k0 += kEB) {
+      float wv[kEB], fv[kEB];
+#pragma unroll
+      for (int q = 0; q < kEB; ++q) {
+        const bool on = k0 + q < ellK;
+        wv[q] = on ? __ldg(ew + (size_t)(k0 + q) * kTileLeaves) : 0.f;
+        fv[q] = on ? __ldg(ef + (size_t)(k0 + q) * kTileLeaves) : 0.f;
+      }
+#pragma unroll
+      for (int q = 0; q < kEB; ++q) {
+        if (wv[q] == 0.f) continue;
+        const T cand = v0 - cc * ((T)2 * S - W);
+        res0 = fmax(res0, fmin(cand, (T)fv[q]));
+        S += (T)wv[q];
+      }
     }
     res0 = fmax(res0, v0 - cc * ((T)2 * S - W));
   } else if (BW != kWeights) {
